@@ -1,0 +1,98 @@
+"""ctypes binding of libgx.so (the C ABI declared in include/gx.h).
+
+The library is built in-tree (``make``) and loaded from this package directory.  There is
+no fallback: if the shared object is missing, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import (POINTER, Structure, c_char_p, c_double, c_float, c_int, c_int64,
+                    c_size_t, c_uint32, c_uint64, c_void_p)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgx.so")
+
+GX_OK, GX_ERR_CONFIG, GX_ERR_INFEASIBLE, GX_ERR_CUDA, GX_ERR_NCCL = 0, 1, 2, 3, 4
+GX_OUT_BF16, GX_OUT_F32, GX_OUT_F32_ACC = 0, 1, 2
+
+
+class GxError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"gx error {code}: {msg}")
+        self.code = code
+        self.msg = msg
+
+
+class ValidationError(GxError):
+    """Mirrors parplan::ValidationError (proj/include/parplan/common.h:26-29)."""
+
+
+class GuardError(GxError):
+    """Mirrors parplan::GuardError (proj/include/parplan/common.h:33-36)."""
+
+
+class GemmEpilogue(Structure):
+    _fields_ = [
+        ("out_kind", c_int), ("out", c_void_p), ("ldo", c_int64), ("alpha", c_float),
+        ("bias", c_void_p), ("gelu", c_int), ("aux", c_void_p), ("ld_aux", c_int64),
+        ("residual", c_void_p), ("ld_res", c_int64), ("row_offset", c_int64),
+        ("col_offset", c_int64), ("drop_ld", c_int64), ("drop_threshold", c_uint32),
+        ("drop_scale", c_float), ("seed", c_uint64), ("site", c_uint64),
+    ]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `make` (or __graft_entry__.build())")
+        _lib = ctypes.CDLL(LIB_PATH)
+        _declare(_lib)
+    return _lib
+
+
+def _declare(L: ctypes.CDLL) -> None:
+    L.gx_last_error.restype = c_char_p
+    L.gx_version.restype = c_int
+    L.gx_k_gemm_bf16.argtypes = [c_void_p, c_int64, c_int, c_void_p, c_int64, c_int, c_int,
+                                 c_int, c_int, POINTER(GemmEpilogue), c_int, c_void_p]
+    L.gx_k_gemm_bf16.restype = c_int
+    for name, args in _EXTRA_SIGNATURES.items():
+        fn = getattr(L, name, None)
+        if fn is not None:
+            fn.argtypes = args
+            fn.restype = c_int
+
+
+_EXTRA_SIGNATURES: dict = {
+    "gx_plan_optimize": [c_char_p, c_char_p, c_char_p, POINTER(c_int), c_int, c_int, c_char_p,
+                         c_int, c_char_p, c_size_t, POINTER(c_size_t)],
+    "gx_plan_exhaustive": [c_char_p, c_char_p, c_char_p, POINTER(c_int), c_int, c_int,
+                           c_char_p, c_char_p, c_size_t, POINTER(c_size_t)],
+    "gx_plan_dp_search": [c_char_p, c_int, c_int, c_int64, c_int, c_int, c_int, c_double,
+                          c_char_p, c_char_p, c_size_t, POINTER(c_size_t)],
+    "gx_plan_estimate": [c_int64, c_int64, c_double, c_char_p, c_int, c_double, c_char_p,
+                         c_char_p, c_size_t, POINTER(c_size_t)],
+    "gx_plan_transformation_ms": [c_int64, c_int64, c_char_p, c_char_p, c_int, c_double,
+                                  POINTER(c_double)],
+    "gx_plan_enumerate": [c_int, c_int, c_char_p, c_size_t, POINTER(c_size_t)],
+}
+
+
+def last_error() -> str:
+    return lib().gx_last_error().decode()
+
+
+def check(code: int) -> None:
+    if code != GX_OK:
+        raise GxError(code, last_error())
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)

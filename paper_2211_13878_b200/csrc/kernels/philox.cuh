@@ -1,0 +1,42 @@
+// philox.cuh — counter-based Philox4x32-10, shared bit-for-bit by every dropout site on the
+// GPU and by the CPU oracle (oracle/layer_oracle.py::philox4x32).  Dropout element `i` of a
+// site uses counter {i>>2 (lo), i>>34 (hi), site_lo, site_hi}, key {seed_lo, seed_hi}, and
+// word (i & 3) of the output; the element is kept iff word >= threshold (= p * 2^32).
+#pragma once
+#include <cstdint>
+
+namespace gx {
+
+struct Philox4 {
+  uint32_t x, y, z, w;
+};
+
+__host__ __device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2,
+                                                         uint32_t c3, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = static_cast<uint64_t>(0xD2511F53u) * c0;
+    const uint64_t p1 = static_cast<uint64_t>(0xCD9E8D57u) * c2;
+    const uint32_t hi0 = static_cast<uint32_t>(p0 >> 32), lo0 = static_cast<uint32_t>(p0);
+    const uint32_t hi1 = static_cast<uint32_t>(p1 >> 32), lo1 = static_cast<uint32_t>(p1);
+    const uint32_t n0 = hi1 ^ c1 ^ k0;
+    const uint32_t n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return Philox4{c0, c1, c2, c3};
+}
+
+// Four consecutive dropout words for elements [4q, 4q+4) of site `site` under `seed`.
+__host__ __device__ __forceinline__ Philox4 dropout_words(uint64_t seed, uint64_t site,
+                                                         uint64_t q) {
+  return philox4x32_10(static_cast<uint32_t>(q), static_cast<uint32_t>(q >> 32),
+                       static_cast<uint32_t>(site), static_cast<uint32_t>(site >> 32),
+                       static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+}
+
+}  // namespace gx
