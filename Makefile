@@ -19,7 +19,7 @@ NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisib
 # The plan/search code must reproduce the reference's floating-point results bit for bit:
 # no fast-math, no FMA contraction, no -march=native (SURVEY.md §7 hard part 1).
 CXXFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -fvisibility=hidden -Wall -Wextra \
-            -Iinclude -I$(CSRC)/kernels -I$(JSON_INC) -I$(NCCL_DIR)/include -I$(CUDA_HOME)/include
+            -Iinclude -I$(CSRC)/kernels -I$(CSRC)/third_party -I$(JSON_INC) -I$(NCCL_DIR)/include -I$(CUDA_HOME)/include
 
 CU_SRCS  := $(wildcard $(CSRC)/kernels/*.cu)
 CC_SRCS  := $(wildcard $(CSRC)/runtime/*.cc) $(wildcard $(CSRC)/parplan/*.cc)

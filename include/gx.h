@@ -35,6 +35,7 @@ extern "C" {
 #define GX_ERR_INFEASIBLE 2
 #define GX_ERR_CUDA 3
 #define GX_ERR_NCCL 4
+#define GX_ERR_GUARD 5 /* brute-force oracle guard tripped (parplan::GuardError) */
 
 #define GX_OUT_BF16 0
 #define GX_OUT_F32 1
@@ -81,6 +82,33 @@ GX_API int gx_plan_transformation_ms(int64_t param_bytes, int64_t act_bytes_per_
 
 /* parplan::EnumerateStrategies (strategy.h:90) -> StrategySetToJson. */
 GX_API int gx_plan_enumerate(int group_size, int prune, char* out, size_t cap, size_t* needed);
+
+/* parplan::ExhaustiveDp (oracle.h:39-44) with the gx_plan_dp_search signature/output. */
+GX_API int gx_plan_exhaustive_dp(const char* model_json, int begin, int end, int64_t budget_bytes,
+                                 int group_size, int prune, int batch_per_group,
+                                 double bandwidth_gbps, const char* profile_json, char* out,
+                                 size_t cap, size_t* needed);
+
+/* parplan::PartitionPipeline (planner.h:44-48): writes [[begin,end],...] or null. */
+GX_API int gx_plan_partition(const char* model_json, int pp_degree, const char* guideline,
+                             char* out, size_t cap, size_t* needed);
+
+/* parplan::StagePipelineCostMs (planner.h:50-54). */
+GX_API int gx_plan_pipeline_cost(const double* stage_costs_ms, int n, int pp_degree,
+                                 int micro_batches, double* out_ms);
+
+/* parplan::CollectiveVolumeBytes (cost_model.h:70-73); kind 0 AR, 1 AG, 2 RS. */
+GX_API int gx_plan_collective_bytes(int kind, int degree, double payload_bytes, double* out);
+
+/* ModelFromJson / ClusterFromJson / ProfileFromJson validation; kind = "model" |
+ * "cluster" | "profile".  Returns 1 with the field-naming message on failure. */
+GX_API int gx_plan_validate(const char* kind, const char* json_text);
+
+/* parplan::GroupBandwidthGbps (cluster.h:51). */
+GX_API int gx_plan_bandwidth(const char* cluster_json, int group_size, double* out_gbps);
+
+/* Message of the calling thread's last gx_plan_* failure (also mirrored in gx_last_error). */
+GX_API const char* gx_plan_last_error(void);
 
 /* ------------------------------------------------------------------ kernels */
 typedef struct gx_gemm_epilogue {

@@ -61,8 +61,14 @@ def _declare(L: ctypes.CDLL) -> None:
     L.gx_k_gemm_bf16.argtypes = [c_void_p, c_int64, c_int, c_void_p, c_int64, c_int, c_int,
                                  c_int, c_int, POINTER(GemmEpilogue), c_int, c_void_p]
     L.gx_k_gemm_bf16.restype = c_int
+    declare_plan_api(L, "gx_plan_")
+
+
+def declare_plan_api(L: ctypes.CDLL, prefix: str) -> None:
+    """Declares the plan/search C surface under `prefix` (gx_plan_ or the oracle's ref_plan_)."""
+    getattr(L, prefix + "last_error").restype = c_char_p
     for name, args in _EXTRA_SIGNATURES.items():
-        fn = getattr(L, name, None)
+        fn = getattr(L, prefix + name[len("gx_plan_"):], None)
         if fn is not None:
             fn.argtypes = args
             fn.restype = c_int
@@ -80,6 +86,13 @@ _EXTRA_SIGNATURES: dict = {
     "gx_plan_transformation_ms": [c_int64, c_int64, c_char_p, c_char_p, c_int, c_double,
                                   POINTER(c_double)],
     "gx_plan_enumerate": [c_int, c_int, c_char_p, c_size_t, POINTER(c_size_t)],
+    "gx_plan_exhaustive_dp": [c_char_p, c_int, c_int, c_int64, c_int, c_int, c_int, c_double,
+                              c_char_p, c_char_p, c_size_t, POINTER(c_size_t)],
+    "gx_plan_partition": [c_char_p, c_int, c_char_p, c_char_p, c_size_t, POINTER(c_size_t)],
+    "gx_plan_pipeline_cost": [POINTER(c_double), c_int, c_int, c_int, POINTER(c_double)],
+    "gx_plan_collective_bytes": [c_int, c_int, c_double, POINTER(c_double)],
+    "gx_plan_validate": [c_char_p, c_char_p],
+    "gx_plan_bandwidth": [c_char_p, c_int, POINTER(c_double)],
 }
 
 

@@ -1,0 +1,40 @@
+"""The reference planner's OWN test programs, run against this repo's drop-in planner.
+
+oracle/Makefile compiles the unmodified sources /root/reference/proj/tests/{model_ir,
+cluster, strategy, cost_model, planner, oracle}_test.cc and acceptance_main.cc twice:
+against the reference library (``*_ref``, sanity) and against this repo's ``namespace
+parplan`` implementation (``*_gx``).  GTest is absent from the image, so
+oracle/gtest_shim provides the gtest subset they use.  Needs /root/reference (the build
+container); skipped elsewhere.
+"""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = "/root/reference/proj"
+SUITES = ["model_ir_test", "cluster_test", "strategy_test", "cost_model_test", "planner_test",
+          "oracle_test", "acceptance"]
+
+pytestmark = pytest.mark.skipif(not os.path.isdir(REF), reason="reference sources absent")
+
+
+@pytest.fixture(scope="module")
+def built():
+    r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "-j8", "all", "suites"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    return os.path.join(ROOT, "oracle", "_ref")
+
+
+@pytest.mark.parametrize("suite", SUITES)
+@pytest.mark.parametrize("impl", ["gx", "ref"])
+def test_reference_suite_passes(built, suite, impl):
+    exe = os.path.join(built, f"{suite}_{impl}")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:]
+    if suite == "acceptance":
+        assert r.stdout.count("PASS") == 9
+    else:
+        assert " 0 failed" in r.stdout
