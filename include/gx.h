@@ -110,6 +110,40 @@ GX_API int gx_plan_bandwidth(const char* cluster_json, int group_size, double* o
 /* Message of the calling thread's last gx_plan_* failure (also mirrored in gx_last_error). */
 GX_API const char* gx_plan_last_error(void);
 
+/* ------------------------------------------------------------------ executor
+ * One gx_exec per process.  config_json:
+ *   {"plan": <PlanToJson object>, "model": <model json, layers carry "shape">,
+ *    "world_size": N, "local_ranks": [...],            (default: all ranks -> sim mode)
+ *    "comm": "sim" | "nccl", "nccl_id_hex": "<256 hex chars>" (nccl mode),
+ *    "dropout_attn": p, "dropout_hidden": p, "seed": s, "optimizer": true,
+ *    "lr", "beta1", "beta2", "eps", "weight_decay"}
+ * Parameters cross the boundary in the canonical unsharded fp32 order
+ * ln1_g ln1_b ln2_g ln2_b b_qkv b_o b_1 b_2 w_qkv w_o w_1 w_2 (row-major, [out][in]); the
+ * executor slices each rank's TP slice and SDP shard.  Batches are global bf16
+ * [batch*seq][hidden] arrays; each rank copies only its own rows. */
+typedef struct gx_exec gx_exec;
+GX_API int gx_exec_create(const char* config_json, gx_exec** out);
+GX_API int gx_exec_destroy(gx_exec* ex);
+GX_API int gx_exec_set_layer_params(gx_exec* ex, int layer, const float* canonical, int64_t n);
+/* what: 0 = fp32 master params, 1 = synchronised fp32 gradients of the last step. */
+GX_API int gx_exec_export_layer(gx_exec* ex, int layer, int what, float* canonical, int64_t n);
+GX_API int gx_exec_load_batch(gx_exec* ex, const void* x_host, const void* target_host);
+GX_API int gx_exec_load_batch_device(gx_exec* ex, const void* x_dev, const void* target_dev);
+/* One training step (fwd + loss + bwd + grad sync + AdamW) on the loaded batch. */
+GX_API int gx_exec_run(gx_exec* ex, int use_graph);
+GX_API int gx_exec_loss(gx_exec* ex, float* out);
+/* load_batch + run + loss: the end-to-end call (host buffers in, loss out). */
+GX_API int gx_exec_step(gx_exec* ex, const void* x_host, const void* target_host, int use_graph,
+                        float* loss_out);
+/* what: 0 = model output y, 1 = gradient w.r.t. the model input; global bf16 layout. */
+GX_API int gx_exec_export_output(gx_exec* ex, int what, void* host_bf16);
+GX_API int gx_exec_stream(gx_exec* ex, void** stream_out);
+GX_API int gx_exec_info(gx_exec* ex, char* out, size_t cap, size_t* needed);
+GX_API int gx_exec_canonical_size(int hidden, int ffn, int64_t* out);
+/* ncclGetUniqueId -> 256 hex chars + NUL (rank 0 creates, torch.distributed broadcasts). */
+GX_API int gx_nccl_unique_id(char* out_hex, size_t cap);
+GX_API int64_t gx_launch_count(void);
+
 /* ------------------------------------------------------------------ kernels */
 typedef struct gx_gemm_epilogue {
   int out_kind;               /* GX_OUT_BF16 | GX_OUT_F32 | GX_OUT_F32_ACC */
@@ -129,6 +163,8 @@ typedef struct gx_gemm_epilogue {
   float drop_scale;           /* 1 / (1 - p) */
   uint64_t seed;
   uint64_t site;
+  int gelu_bwd;               /* out = acc * gelu'(aux) (aux = bf16 pre-activation, read) */
+  const uint64_t* seed_offset;/* optional device counter added to seed (per-step masks) */
 } gx_gemm_epilogue;
 
 /* C[M,N] = A[M,K] * B[N,K]^T with the epilogue above.  a_mn_major: A stored [K][lda]
@@ -136,6 +172,73 @@ typedef struct gx_gemm_epilogue {
 GX_API int gx_k_gemm_bf16(const void* a, int64_t lda, int a_mn_major, const void* b, int64_t ldb,
                    int b_mn_major, int M, int N, int K, const gx_gemm_epilogue* ep,
                    int tile_n, void* stream);
+
+/* Fused multi-head attention over a token-major qkv buffer ([M=batch*seq][3][heads][d],
+ * row stride ld_qkv).  fwd writes ctx ([M][heads*d], ld_ctx) and lse (fp32 [batch*heads][seq],
+ * log2 domain); bwd reads qkv, ctx, lse, dctx and writes dqkv (qkv layout) using the fp32
+ * workspaces dq_accum ([batch*heads*seq*d]) and dsum ([batch*heads*seq]).  Dropout element
+ * (q,k) of global (sample_offset+b, head_offset+h) uses Philox counter
+ * ((sample*heads_total + head)*seq + q)*seq + k (see csrc/kernels/philox.cuh). */
+typedef struct gx_attention_args {
+  int batch, seq, heads, head_dim;
+  int heads_total, head_offset;
+  int64_t sample_offset;
+  float scale;
+  const void* qkv;
+  int64_t ld_qkv;
+  void* ctx;
+  int64_t ld_ctx;
+  void* lse;
+  const void* dctx;
+  void* dqkv;
+  void* dq_accum;
+  void* dsum;
+  uint32_t drop_threshold;
+  float drop_scale;
+  uint64_t seed;
+  uint64_t site;
+  const uint64_t* seed_offset; /* optional device counter added to seed */
+} gx_attention_args;
+
+GX_API int gx_k_attention_fwd(const gx_attention_args* args, void* stream);
+GX_API int gx_k_attention_bwd(const gx_attention_args* args, void* stream);
+
+/* LayerNorm over rows of h (bf16 in/out, fp32 statistics, eps 1e-5).
+ * fwd: y = (x-mean)*rstd*gamma + beta; writes mean/rstd (fp32 [rows]).
+ * bwd: dx = LN'(dy) (+ dres if non-NULL); dgamma/dbeta (fp32 [h]) are ACCUMULATED. */
+GX_API int gx_k_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y,
+                              void* mean, void* rstd, int rows, int h, void* stream);
+GX_API int gx_k_layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
+                              const void* gamma, const void* dres, void* dx, void* dgamma,
+                              void* dbeta, int rows, int h, void* stream);
+
+/* Dropout sites share one parameter block: element (r, c) of a [rows][cols] local tensor is
+ * global element (row_offset + r) * drop_ld + (col_offset + c) of the site's Philox stream. */
+typedef struct gx_dropout {
+  uint32_t threshold;         /* p * 2^32, 0 = off */
+  float scale;                /* 1/(1-p) */
+  uint64_t seed, site;
+  int64_t row_offset, col_offset, drop_ld;
+  const uint64_t* seed_offset; /* optional device counter added to seed */
+} gx_dropout;
+
+/* out = residual + dropout(x + bias)      (bf16; bias may be NULL) */
+GX_API int gx_k_bias_dropout_add(const void* x, const void* bias, const void* residual, void* out,
+                                 int rows, int cols, const gx_dropout* d, void* stream);
+/* dz = dropout_mask(dy) (may alias dy when dropout is off); dbias[c] += sum_r dz[r][c] (fp32). */
+GX_API int gx_k_dropout_bwd_colsum(const void* dy, void* dz, void* dbias, int rows, int cols,
+                                   const gx_dropout* d, void* stream);
+/* acc[c] += sum_r x[r][c] (x bf16 [rows][ld], acc fp32) */
+GX_API int gx_k_colsum(const void* x, int64_t ld, void* acc, int rows, int cols, void* stream);
+/* MSE: loss += sum (y-t)^2 * inv_count (fp32 scalar); dy = 2 (y-t) * inv_count (bf16). */
+GX_API int gx_k_mse_loss(const void* y, const void* target, void* dy, void* loss, int64_t n,
+                         float inv_count, void* stream);
+/* AdamW over n fp32 elements; writes the bf16 compute copy. bias corrections precomputed. */
+GX_API int gx_k_adamw(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n,
+                      float lr, float beta1, float beta2, float eps, float weight_decay,
+                      float bc1, float bc2, void* stream);
+/* fp32 -> bf16 */
+GX_API int gx_k_cast_bf16(const void* src, void* dst, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,238 @@
+"""TEST INFRASTRUCTURE ONLY — CPU restatement of the executor's Transformer-layer math.
+
+PARITY UNPINNED BY THE REFERENCE: the reference (/root/reference/proj) is a planner only and
+contains no layer implementation (SURVEY.md §8(c) "Layer-numerics oracle: NONE").  This
+module restates the layer the executor runs (a pre-LN encoder layer, PAPER.md:136-157
+semantics for how DP/SDP/TP/PP split it) in float64 numpy, and is itself pinned against
+torch.autograd (float64, CPU) in tests/test_layer_oracle.py, with golden vectors committed
+under tests/golden/.  Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline /
+reference legs may use it.
+
+Layer (h hidden, H heads of d, f ffn; x is [tokens, h], tokens = samples * seq):
+    a   = LN1(x)                       (eps 1e-5)
+    qkv = a Wqkv^T + bqkv              (Wqkv rows ordered [3][H][d])
+    ctx = drop_attn(softmax(q k^T / sqrt(d))) v      per (sample, head)
+    x1  = x + drop_h1(ctx Wo^T + bo)
+    c   = LN2(x1)
+    y   = x1 + drop_h2(gelu(c W1^T + b1) W2^T + b2)  (exact erf GeLU)
+Dropout uses the Philox4x32-10 stream of csrc/kernels/philox.cuh: element i of a site is
+kept iff word (i & 3) of philox({i>>2 lo, i>>2 hi, site lo, site hi}, {seed lo, seed hi})
+is >= floor(p * 2^32); kept values are scaled by 1/(1-p).  Site ids per layer l:
+attn = 3l+0, hidden-1 = 3l+1, hidden-2 = 3l+2 (see paper_2211_13878_b200 executor).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+M0, M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+W0, W1 = np.uint64(0x9E3779B9), np.uint64(0xBB67AE85)
+MASK32 = np.uint64(0xFFFFFFFF)
+
+
+def philox4x32_10(c0, c1, c2, c3, k0, k1):
+    """Vectorised Philox4x32-10 (Salmon et al. 2011); inputs uint32-valued arrays."""
+    c0, c1, c2, c3 = (np.asarray(v, dtype=np.uint64) & MASK32 for v in (c0, c1, c2, c3))
+    k0 = np.asarray(k0, dtype=np.uint64) & MASK32
+    k1 = np.asarray(k1, dtype=np.uint64) & MASK32
+    for _ in range(10):
+        p0 = M0 * c0
+        p1 = M1 * c2
+        hi0, lo0 = p0 >> np.uint64(32), p0 & MASK32
+        hi1, lo1 = p1 >> np.uint64(32), p1 & MASK32
+        c0, c1, c2, c3 = (hi1 ^ c1 ^ k0) & MASK32, lo1, (hi0 ^ c3 ^ k1) & MASK32, lo0
+        k0 = (k0 + W0) & MASK32
+        k1 = (k1 + W1) & MASK32
+    return c0, c1, c2, c3
+
+
+def dropout_threshold(p: float) -> int:
+    return 0 if p <= 0 else min(int(p * 4294967296.0), 0xFFFFFFFF)
+
+
+def keep_mask(seed: int, site: int, index: np.ndarray, p: float) -> np.ndarray:
+    """Keep flags for global element indices `index` of dropout site `site`."""
+    index = np.asarray(index, dtype=np.uint64)
+    if p <= 0:
+        return np.ones(index.shape, dtype=bool)
+    q = index >> np.uint64(2)
+    w = philox4x32_10(q & MASK32, q >> np.uint64(32), np.uint64(site & 0xFFFFFFFF),
+                      np.uint64(site >> 32), np.uint64(seed & 0xFFFFFFFF), np.uint64(seed >> 32))
+    sel = (index & np.uint64(3)).astype(np.int64)
+    words = np.stack(w, axis=-1)
+    word = np.take_along_axis(words, sel[..., None], axis=-1)[..., 0]
+    return word >= np.uint64(dropout_threshold(p))
+
+
+@dataclass
+class LayerShape:
+    hidden: int
+    heads: int
+    seq: int
+    ffn: int
+
+    @property
+    def head_dim(self):
+        return self.hidden // self.heads
+
+
+def init_layer_params(shape: LayerShape, rng: np.random.Generator, std=0.02) -> dict:
+    h, f = shape.hidden, shape.ffn
+    return {
+        "ln1_g": 1.0 + 0.1 * rng.standard_normal(h), "ln1_b": 0.1 * rng.standard_normal(h),
+        "w_qkv": std * rng.standard_normal((3 * h, h)), "b_qkv": 0.02 * rng.standard_normal(3 * h),
+        "w_o": std * rng.standard_normal((h, h)), "b_o": 0.02 * rng.standard_normal(h),
+        "ln2_g": 1.0 + 0.1 * rng.standard_normal(h), "ln2_b": 0.1 * rng.standard_normal(h),
+        "w_1": std * rng.standard_normal((f, h)), "b_1": 0.02 * rng.standard_normal(f),
+        "w_2": std * rng.standard_normal((h, f)), "b_2": 0.02 * rng.standard_normal(h),
+    }
+
+
+def _ln_fwd(x, g, b, eps=1e-5):
+    mu = x.mean(-1, keepdims=True)
+    var = ((x - mu) ** 2).mean(-1, keepdims=True)
+    rstd = 1.0 / np.sqrt(var + eps)
+    xh = (x - mu) * rstd
+    return xh * g + b, (xh, rstd)
+
+
+def _ln_bwd(dy, cache, g):
+    xh, rstd = cache
+    h = xh.shape[-1]
+    dxh = dy * g
+    dx = rstd * (dxh - dxh.mean(-1, keepdims=True) - xh * (dxh * xh).mean(-1, keepdims=True))
+    return dx, (dy * xh).sum(0), dy.sum(0)
+
+
+_erf = np.vectorize(math.erf)
+
+
+def _gelu(x):
+    return 0.5 * x * (1.0 + _erf(x / math.sqrt(2.0)))
+
+
+def _gelu_grad(x):
+    return 0.5 * (1.0 + _erf(x / math.sqrt(2.0))) + x * np.exp(-0.5 * x * x) / math.sqrt(2 * math.pi)
+
+
+@dataclass
+class Dropout:
+    p_attn: float = 0.0
+    p_hidden: float = 0.0
+    seed: int = 1234
+
+
+def _hidden_mask(drop: Dropout, site: int, rows: int, cols: int, row_offset: int):
+    idx = (np.arange(rows, dtype=np.uint64)[:, None] + np.uint64(row_offset)) * np.uint64(cols) + \
+        np.arange(cols, dtype=np.uint64)[None, :]
+    return keep_mask(drop.seed, site, idx, drop.p_hidden)
+
+
+def _attn_mask(drop: Dropout, site: int, samples: int, heads: int, seq: int, sample_offset: int):
+    b = np.arange(samples, dtype=np.uint64)[:, None, None, None] + np.uint64(sample_offset)
+    h = np.arange(heads, dtype=np.uint64)[None, :, None, None]
+    q = np.arange(seq, dtype=np.uint64)[None, None, :, None]
+    k = np.arange(seq, dtype=np.uint64)[None, None, None, :]
+    idx = ((b * np.uint64(heads) + h) * np.uint64(seq) + q) * np.uint64(seq) + k
+    return keep_mask(drop.seed, site, idx, drop.p_attn)
+
+
+def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
+                  drop: Dropout = Dropout(), sample_offset: int = 0):
+    """x: [samples*seq, h] float64.  Returns (y, cache)."""
+    h, H, d, s = shape.hidden, shape.heads, shape.head_dim, shape.seq
+    n = x.shape[0] // s
+    a, ln1 = _ln_fwd(x, P["ln1_g"], P["ln1_b"])
+    qkv = a @ P["w_qkv"].T + P["b_qkv"]
+    q = qkv[:, :h].reshape(n, s, H, d).transpose(0, 2, 1, 3)
+    k = qkv[:, h:2 * h].reshape(n, s, H, d).transpose(0, 2, 1, 3)
+    v = qkv[:, 2 * h:].reshape(n, s, H, d).transpose(0, 2, 1, 3)
+    sc = q @ k.transpose(0, 1, 3, 2) / math.sqrt(d)
+    sc = sc - sc.max(-1, keepdims=True)
+    pr = np.exp(sc)
+    pr = pr / pr.sum(-1, keepdims=True)
+    am = _attn_mask(drop, 3 * layer_id, n, H, s, sample_offset)
+    ka = 1.0 / (1.0 - drop.p_attn) if drop.p_attn > 0 else 1.0
+    pd = pr * am * ka
+    ctx4 = pd @ v
+    ctx = ctx4.transpose(0, 2, 1, 3).reshape(n * s, h)
+    o = ctx @ P["w_o"].T + P["b_o"]
+    m1 = _hidden_mask(drop, 3 * layer_id + 1, n * s, h, sample_offset * s)
+    kh = 1.0 / (1.0 - drop.p_hidden) if drop.p_hidden > 0 else 1.0
+    x1 = x + o * m1 * kh
+    c, ln2 = _ln_fwd(x1, P["ln2_g"], P["ln2_b"])
+    pre = c @ P["w_1"].T + P["b_1"]
+    g = _gelu(pre)
+    z = g @ P["w_2"].T + P["b_2"]
+    m2 = _hidden_mask(drop, 3 * layer_id + 2, n * s, h, sample_offset * s)
+    y = x1 + z * m2 * kh
+    cache = dict(x=x, a=a, ln1=ln1, q=q, k=k, v=v, pr=pr, am=am, ka=ka, pd=pd, ctx=ctx, m1=m1,
+                 kh=kh, x1=x1, c=c, ln2=ln2, pre=pre, g=g, m2=m2, n=n)
+    return y, cache
+
+
+def layer_backward(P: dict, dy: np.ndarray, cache: dict, shape: LayerShape):
+    """Returns (dx, grads dict with the same keys as P)."""
+    h, H, d, s = shape.hidden, shape.heads, shape.head_dim, shape.seq
+    n = cache["n"]
+    G = {}
+    dz = dy * cache["m2"] * cache["kh"]
+    G["b_2"] = dz.sum(0)
+    G["w_2"] = dz.T @ cache["g"]
+    dg = dz @ P["w_2"]
+    dpre = dg * _gelu_grad(cache["pre"])
+    G["b_1"] = dpre.sum(0)
+    G["w_1"] = dpre.T @ cache["c"]
+    dc = dpre @ P["w_1"]
+    dx1_ln, G["ln2_g"], G["ln2_b"] = _ln_bwd(dc, cache["ln2"], P["ln2_g"])
+    dx1 = dy + dx1_ln
+    do = dx1 * cache["m1"] * cache["kh"]
+    G["b_o"] = do.sum(0)
+    G["w_o"] = do.T @ cache["ctx"]
+    dctx = do @ P["w_o"]
+    dctx4 = dctx.reshape(n, s, H, d).transpose(0, 2, 1, 3)
+    dv = cache["pd"].transpose(0, 1, 3, 2) @ dctx4
+    dpd = dctx4 @ cache["v"].transpose(0, 1, 3, 2)
+    dpr = dpd * cache["am"] * cache["ka"]
+    pr = cache["pr"]
+    dsc = pr * (dpr - (dpr * pr).sum(-1, keepdims=True))
+    dsc = dsc / math.sqrt(d)
+    dq = dsc @ cache["k"]
+    dk = dsc.transpose(0, 1, 3, 2) @ cache["q"]
+    to2 = lambda t: t.transpose(0, 2, 1, 3).reshape(n * s, h)  # noqa: E731
+    dqkv = np.concatenate([to2(dq), to2(dk), to2(dv)], axis=1)
+    G["b_qkv"] = dqkv.sum(0)
+    G["w_qkv"] = dqkv.T @ cache["a"]
+    da = dqkv @ P["w_qkv"]
+    dx_ln, G["ln1_g"], G["ln1_b"] = _ln_bwd(da, cache["ln1"], P["ln1_g"])
+    dx = dx1 + dx_ln
+    return dx, G
+
+
+def model_step(params: list, x: np.ndarray, target: np.ndarray, shape: LayerShape,
+               drop: Dropout = Dropout(), sample_offset: int = 0, count=None):
+    """Forward through all layers, MSE loss = sum((y-t)^2)/count, backward.
+    Returns (loss, y, dx, grads per layer)."""
+    caches = []
+    hcur = x
+    for l, P in enumerate(params):
+        hcur, c = layer_forward(P, hcur, shape, l, drop, sample_offset)
+        caches.append(c)
+    count = count if count is not None else hcur.size
+    loss = float(((hcur - target) ** 2).sum() / count)
+    dcur = 2.0 * (hcur - target) / count
+    grads = [None] * len(params)
+    for l in reversed(range(len(params))):
+        dcur, grads[l] = layer_backward(params[l], dcur, caches[l], shape)
+    return loss, hcur, dcur, grads
+
+
+def adamw_reference(p, g, m, v, step, lr=1e-4, b1=0.9, b2=0.999, eps=1e-8, wd=0.0):
+    m = b1 * m + (1 - b1) * g
+    v = b2 * v + (1 - b2) * g * g
+    mh = m / (1 - b1 ** step)
+    vh = v / (1 - b2 ** step)
+    p = p - lr * (mh / (np.sqrt(vh) + eps) + wd * p)
+    return p, m, v

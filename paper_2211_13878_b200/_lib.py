@@ -38,7 +38,8 @@ class GemmEpilogue(Structure):
         ("bias", c_void_p), ("gelu", c_int), ("aux", c_void_p), ("ld_aux", c_int64),
         ("residual", c_void_p), ("ld_res", c_int64), ("row_offset", c_int64),
         ("col_offset", c_int64), ("drop_ld", c_int64), ("drop_threshold", c_uint32),
-        ("drop_scale", c_float), ("seed", c_uint64), ("site", c_uint64),
+        ("drop_scale", c_float), ("seed", c_uint64), ("site", c_uint64), ("gelu_bwd", c_int),
+        ("seed_offset", c_void_p),
     ]
 
 
@@ -61,6 +62,43 @@ def _declare(L: ctypes.CDLL) -> None:
     L.gx_k_gemm_bf16.argtypes = [c_void_p, c_int64, c_int, c_void_p, c_int64, c_int, c_int,
                                  c_int, c_int, POINTER(GemmEpilogue), c_int, c_void_p]
     L.gx_k_gemm_bf16.restype = c_int
+    for name in ("gx_k_attention_fwd", "gx_k_attention_bwd", "gx_k_layernorm_fwd",
+                 "gx_k_layernorm_bwd", "gx_k_bias_dropout_add", "gx_k_dropout_bwd_colsum",
+                 "gx_k_colsum", "gx_k_mse_loss", "gx_k_adamw", "gx_k_cast_bf16"):
+        getattr(L, name).restype = c_int
+    vp = c_void_p
+    L.gx_k_attention_fwd.argtypes = [vp, vp]
+    L.gx_k_attention_bwd.argtypes = [vp, vp]
+    L.gx_k_layernorm_fwd.argtypes = [vp, vp, vp, vp, vp, vp, c_int, c_int, vp]
+    L.gx_k_layernorm_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, c_int, c_int, vp]
+    L.gx_k_bias_dropout_add.argtypes = [vp, vp, vp, vp, c_int, c_int, vp, vp]
+    L.gx_k_dropout_bwd_colsum.argtypes = [vp, vp, vp, c_int, c_int, vp, vp]
+    L.gx_k_colsum.argtypes = [c_void_p, c_int64, c_void_p, c_int, c_int, c_void_p]
+    L.gx_k_mse_loss.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_float, c_void_p]
+    L.gx_k_adamw.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_float,
+                             c_float, c_float, c_float, c_float, c_float, c_float, c_void_p]
+    L.gx_k_cast_bf16.argtypes = [c_void_p, c_void_p, c_int64, c_void_p]
+    L.gx_exec_create.argtypes = [c_char_p, POINTER(c_void_p)]
+    L.gx_exec_destroy.argtypes = [vp]
+    L.gx_exec_set_layer_params.argtypes = [vp, c_int, vp, c_int64]
+    L.gx_exec_export_layer.argtypes = [vp, c_int, c_int, vp, c_int64]
+    L.gx_exec_load_batch.argtypes = [vp, vp, vp]
+    L.gx_exec_load_batch_device.argtypes = [vp, vp, vp]
+    L.gx_exec_run.argtypes = [vp, c_int]
+    L.gx_exec_loss.argtypes = [vp, POINTER(c_float)]
+    L.gx_exec_step.argtypes = [vp, vp, vp, c_int, POINTER(c_float)]
+    L.gx_exec_export_output.argtypes = [vp, c_int, vp]
+    L.gx_exec_stream.argtypes = [vp, POINTER(c_void_p)]
+    L.gx_exec_info.argtypes = [vp, c_char_p, c_size_t, POINTER(c_size_t)]
+    L.gx_exec_canonical_size.argtypes = [c_int, c_int, POINTER(c_int64)]
+    L.gx_nccl_unique_id.argtypes = [c_char_p, c_size_t]
+    for name in ("gx_exec_create", "gx_exec_destroy", "gx_exec_set_layer_params",
+                 "gx_exec_export_layer", "gx_exec_load_batch", "gx_exec_load_batch_device",
+                 "gx_exec_run", "gx_exec_loss", "gx_exec_step", "gx_exec_export_output",
+                 "gx_exec_stream", "gx_exec_info", "gx_exec_canonical_size",
+                 "gx_nccl_unique_id"):
+        getattr(L, name).restype = c_int
+    L.gx_launch_count.restype = c_int64
     declare_plan_api(L, "gx_plan_")
 
 

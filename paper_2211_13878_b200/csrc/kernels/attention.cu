@@ -1,0 +1,567 @@
+// attention.cu — fused multi-head self-attention forward / backward (flash-style, exact).
+//
+//   ctx = dropout(softmax(Q K^T / sqrt(d))) V      per (sample, head), no materialised S
+//
+// Layout: qkv rows are tokens ([M = b*s][3][H][d], row stride ld_qkv), ctx rows [M][H*d].
+// Forward keeps a running (max, sum) per query row and stores lse (log2 domain) for the
+// backward, which recomputes P = exp2(S*c - lse) per key block (FA2 scheme: each CTA owns a
+// block of keys, accumulates dK/dV in registers and adds dQ into an fp32 buffer).
+// Dropout masks come from the shared Philox stream (philox.cuh): element (q, k) of global
+// (sample, head) uses counter index ((sample*H_tot + head)*s + q)*s + k, so any TP/DP split
+// of heads or samples reproduces the unsharded masks exactly.
+//
+// Tensor-core path: mma.sync m16n8k16 bf16 with ldmatrix fragments.  (A tcgen05/TMEM
+// variant is the planned next step; attention is ~7% of the layer FLOPs at s=512.)
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "gx_internal.h"
+#include "philox.cuh"
+
+namespace gx {
+
+namespace {
+
+constexpr int kBlk = 64;      // queries (fwd) / keys (bwd) per CTA, 16 per warp
+constexpr int kThreads = 128;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(a));
+}
+__device__ __forceinline__ void mma_bf16(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+  __nv_bfloat162 t = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&t);
+}
+
+// Dropout keep flags for elements e and e+1 of one (sample, head) stream.
+__device__ __forceinline__ void keep_pair(uint64_t seed, uint64_t site, uint64_t e,
+                                          uint32_t thr, bool& k0, bool& k1) {
+  const Philox4 w = dropout_words(seed, site, e >> 2);
+  const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+  const uint32_t i = static_cast<uint32_t>(e & 3);
+  k0 = words[i] >= thr;
+  if (i < 3) {
+    k1 = words[i + 1] >= thr;
+  } else {
+    const Philox4 v = dropout_words(seed, site, (e + 1) >> 2);
+    k1 = v.x >= thr;
+  }
+}
+__device__ __forceinline__ bool keep_one(uint64_t seed, uint64_t site, uint64_t e, uint32_t thr) {
+  const Philox4 w = dropout_words(seed, site, e >> 2);
+  const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+  return words[e & 3] >= thr;
+}
+
+// Loads a [64][HD] tile of rows [r0, r0+64) (rows >= nrows zero-filled) into padded smem.
+template <int HD>
+__device__ __forceinline__ void load_tile(__nv_bfloat16* dst, const __nv_bfloat16* src,
+                                          int64_t ld, int r0, int nrows) {
+  constexpr int kChunks = HD / 8;  // 16 B per chunk
+  for (int i = threadIdx.x; i < kBlk * kChunks; i += kThreads) {
+    const int r = i / kChunks, c = i % kChunks;
+    const bool ok = r0 + r < nrows;
+    const __nv_bfloat16* g = src + static_cast<int64_t>(ok ? r0 + r : 0) * ld + c * 8;
+    cp_async16(dst + r * (HD + 8) + c * 8, g, ok);
+  }
+}
+
+}  // namespace
+
+// --------------------------------------------------------------------------- forward
+template <int HD>
+__global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_args p) {
+  constexpr int LDS = HD + 8;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  __nv_bfloat16* sK = sQ + kBlk * LDS;        // [2][64][LDS]
+  __nv_bfloat16* sV = sK + 2 * kBlk * LDS;    // [2][64][LDS]
+
+  const int s = p.seq;
+  const int H = p.heads;
+  const int bh = blockIdx.y;
+  const int b = bh / H, h = bh % H;
+  const int q0 = blockIdx.x * kBlk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+
+  const auto* qkv = static_cast<const __nv_bfloat16*>(p.qkv);
+  const int64_t ld = p.ld_qkv;
+  const __nv_bfloat16* Qg = qkv + static_cast<int64_t>(b) * s * ld + h * HD;
+  const __nv_bfloat16* Kg = Qg + static_cast<int64_t>(H) * HD;
+  const __nv_bfloat16* Vg = Kg + static_cast<int64_t>(H) * HD;
+
+  load_tile<HD>(sQ, Qg, ld, q0, s);
+  load_tile<HD>(sK, Kg, ld, 0, s);
+  load_tile<HD>(sV, Vg, ld, 0, s);
+  cp_async_commit();
+
+  const float c2 = p.scale * 1.4426950408889634f;  // softmax scale in log2 units
+  const uint32_t thr = p.drop_threshold;
+  const float inv_keep = p.drop_scale;
+  const uint64_t seed = p.seed + (p.seed_offset != nullptr ? *p.seed_offset : 0ull);
+  const uint64_t stream =
+      (static_cast<uint64_t>(p.sample_offset + b) * p.heads_total + (p.head_offset + h)) * s;
+
+  float o[HD / 8][4];
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
+  uint32_t qf[HD / 16][4];
+
+  const int nkb = (s + kBlk - 1) / kBlk;
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int buf = kb & 1;
+    if (kb + 1 < nkb) {
+      load_tile<HD>(sK + (buf ^ 1) * kBlk * LDS, Kg, ld, (kb + 1) * kBlk, s);
+      load_tile<HD>(sV + (buf ^ 1) * kBlk * LDS, Vg, ld, (kb + 1) * kBlk, s);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    if (kb == 0) {
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk)
+        ldsm_x4(qf[kk], sQ + (warp * 16 + (lane & 15)) * LDS + kk * 16 + (lane >> 4) * 8);
+    }
+    const __nv_bfloat16* cK = sK + buf * kBlk * LDS;
+    const __nv_bfloat16* cV = sV + buf * kBlk * LDS;
+
+    float sacc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sacc[i][0] = sacc[i][1] = sacc[i][2] = sacc[i][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+#pragma unroll
+      for (int np = 0; np < 4; ++np) {
+        uint32_t kf[4];
+        ldsm_x4(kf, cK + (np * 16 + (lane & 7) + ((lane >> 4) << 3)) * LDS + kk * 16 +
+                        ((lane >> 3) & 1) * 8);
+        mma_bf16(sacc[2 * np], qf[kk], kf[0], kf[1]);
+        mma_bf16(sacc[2 * np + 1], qf[kk], kf[2], kf[3]);
+      }
+    }
+    // scale, mask key tail, online softmax
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int nb = 0; nb < 8; ++nb) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int key = kb * kBlk + nb * 8 + 2 * t + (j & 1);
+        float v = sacc[nb][j] * c2;
+        if (key >= s) v = -INFINITY;
+        sacc[nb][j] = v;
+        mx[j >> 1] = fmaxf(mx[j >> 1], v);
+      }
+    }
+    float corr[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffff, mx[r], 1));
+      mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffff, mx[r], 2));
+      const float m_new = fmaxf(m_r[r], mx[r]);
+      corr[r] = exp2f(m_r[r] - m_new);
+      m_r[r] = m_new;
+    }
+    float rs[2] = {0.f, 0.f};
+#pragma unroll
+    for (int nb = 0; nb < 8; ++nb) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float e = exp2f(sacc[nb][j] - m_r[j >> 1]);
+        sacc[nb][j] = e;
+        rs[j >> 1] += e;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) l_r[r] = l_r[r] * corr[r] + rs[r];  // quad-partial sums
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) {
+      o[i][0] *= corr[0];
+      o[i][1] *= corr[0];
+      o[i][2] *= corr[1];
+      o[i][3] *= corr[1];
+    }
+    if (thr != 0u) {
+#pragma unroll
+      for (int nb = 0; nb < 8; ++nb) {
+        const int key = kb * kBlk + nb * 8 + 2 * t;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int q = q0 + warp * 16 + g + 8 * r;
+          bool k0, k1;
+          keep_pair(seed, p.site, (stream + static_cast<uint64_t>(q)) * s + key, thr, k0, k1);
+          sacc[nb][2 * r] = k0 ? sacc[nb][2 * r] * inv_keep : 0.f;
+          sacc[nb][2 * r + 1] = k1 ? sacc[nb][2 * r + 1] * inv_keep : 0.f;
+        }
+      }
+    }
+    // O += P V
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {  // 16 keys per step
+      uint32_t pa[4];
+      pa[0] = pack2(sacc[2 * kk][0], sacc[2 * kk][1]);
+      pa[1] = pack2(sacc[2 * kk][2], sacc[2 * kk][3]);
+      pa[2] = pack2(sacc[2 * kk + 1][0], sacc[2 * kk + 1][1]);
+      pa[3] = pack2(sacc[2 * kk + 1][2], sacc[2 * kk + 1][3]);
+#pragma unroll
+      for (int np = 0; np < HD / 16; ++np) {
+        uint32_t vf[4];
+        ldsm_x4_t(vf, cV + (kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + np * 16 +
+                          (lane >> 4) * 8);
+        mma_bf16(o[2 * np], pa, vf[0], vf[1]);
+        mma_bf16(o[2 * np + 1], pa, vf[2], vf[3]);
+      }
+    }
+    __syncthreads();
+  }
+  // finalize
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    l_r[r] += __shfl_xor_sync(0xffffffff, l_r[r], 1);
+    l_r[r] += __shfl_xor_sync(0xffffffff, l_r[r], 2);
+  }
+  auto* ctx = static_cast<__nv_bfloat16*>(p.ctx);
+  auto* lse = static_cast<float*>(p.lse);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int q = q0 + warp * 16 + g + 8 * r;
+    if (q >= s) continue;
+    const float inv = 1.f / l_r[r];
+    __nv_bfloat16* out = ctx + (static_cast<int64_t>(b) * s + q) * p.ld_ctx + h * HD;
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) {
+      *reinterpret_cast<uint32_t*>(out + i * 8 + 2 * t) =
+          pack2(o[i][2 * r] * inv, o[i][2 * r + 1] * inv);
+    }
+    if (t == 0) lse[static_cast<int64_t>(bh) * s + q] = m_r[r] + log2f(l_r[r]);
+  }
+}
+
+// -------------------------------------------------------------- backward pre-process
+// D[bh][q] = sum_d dctx*ctx ; zero the fp32 dQ accumulator.
+template <int HD>
+__global__ void attn_bwd_prep_kernel(const gx_attention_args p) {
+  const int s = p.seq, H = p.heads;
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int total = p.batch * H * s;
+  if (warp_global >= total) return;
+  const int bh = warp_global / s, q = warp_global % s;
+  const int b = bh / H, h = bh % H;
+  const int64_t row = static_cast<int64_t>(b) * s + q;
+  const auto* o = static_cast<const __nv_bfloat16*>(p.ctx) + row * p.ld_ctx + h * HD;
+  const auto* d = static_cast<const __nv_bfloat16*>(p.dctx) + row * p.ld_ctx + h * HD;
+  float acc = 0.f;
+  for (int i = lane; i < HD; i += 32) acc += __bfloat162float(o[i]) * __bfloat162float(d[i]);
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, m);
+  if (lane == 0) static_cast<float*>(p.dsum)[static_cast<int64_t>(bh) * s + q] = acc;
+  float* dq = static_cast<float*>(p.dq_accum) + (static_cast<int64_t>(bh) * s + q) * HD;
+  for (int i = lane; i < HD; i += 32) dq[i] = 0.f;
+}
+
+// --------------------------------------------------------------------------- backward
+template <int HD>
+__global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_args p) {
+  constexpr int LDS = HD + 8;
+  constexpr int LDP = kBlk + 8;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __nv_bfloat16* sK = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  __nv_bfloat16* sV = sK + kBlk * LDS;
+  __nv_bfloat16* sQ = sV + kBlk * LDS;
+  __nv_bfloat16* sdO = sQ + kBlk * LDS;
+  __nv_bfloat16* sdS = sdO + kBlk * LDS;                              // [64 keys][LDP]
+  float* sL = reinterpret_cast<float*>(sdS + kBlk * LDP);             // lse [64]
+  float* sD = sL + kBlk;                                              // D   [64]
+
+  const int s = p.seq, H = p.heads;
+  const int bh = blockIdx.y;
+  const int b = bh / H, h = bh % H;
+  const int k0 = blockIdx.x * kBlk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+
+  const auto* qkv = static_cast<const __nv_bfloat16*>(p.qkv);
+  const int64_t ld = p.ld_qkv;
+  const __nv_bfloat16* Qg = qkv + static_cast<int64_t>(b) * s * ld + h * HD;
+  const __nv_bfloat16* Kg = Qg + static_cast<int64_t>(H) * HD;
+  const __nv_bfloat16* Vg = Kg + static_cast<int64_t>(H) * HD;
+  const __nv_bfloat16* dOg =
+      static_cast<const __nv_bfloat16*>(p.dctx) + static_cast<int64_t>(b) * s * p.ld_ctx + h * HD;
+  const float* lse = static_cast<const float*>(p.lse) + static_cast<int64_t>(bh) * s;
+  const float* dsum = static_cast<const float*>(p.dsum) + static_cast<int64_t>(bh) * s;
+  float* dqacc = static_cast<float*>(p.dq_accum) + static_cast<int64_t>(bh) * s * HD;
+
+  load_tile<HD>(sK, Kg, ld, k0, s);
+  load_tile<HD>(sV, Vg, ld, k0, s);
+  cp_async_commit();
+
+  const float c2 = p.scale * 1.4426950408889634f;
+  const uint32_t thr = p.drop_threshold;
+  const float inv_keep = p.drop_scale;
+  const uint64_t seed = p.seed + (p.seed_offset != nullptr ? *p.seed_offset : 0ull);
+  const uint64_t stream =
+      (static_cast<uint64_t>(p.sample_offset + b) * p.heads_total + (p.head_offset + h)) * s;
+
+  float dk[HD / 8][4], dv[HD / 8][4];
+#pragma unroll
+  for (int i = 0; i < HD / 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) dk[i][j] = dv[i][j] = 0.f;
+  uint32_t kf[HD / 16][4], vfr[HD / 16][4];
+
+  const int nqb = (s + kBlk - 1) / kBlk;
+  for (int qb = 0; qb < nqb; ++qb) {
+    const int q0 = qb * kBlk;
+    load_tile<HD>(sQ, Qg, ld, q0, s);
+    load_tile<HD>(sdO, dOg, p.ld_ctx, q0, s);
+    for (int i = threadIdx.x; i < kBlk; i += kThreads) {
+      const bool ok = q0 + i < s;
+      sL[i] = ok ? lse[q0 + i] : 0.f;
+      sD[i] = ok ? dsum[q0 + i] : 0.f;
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    if (qb == 0) {
+#pragma unroll
+      for (int kk = 0; kk < HD / 16; ++kk) {
+        ldsm_x4(kf[kk], sK + (warp * 16 + (lane & 15)) * LDS + kk * 16 + (lane >> 4) * 8);
+        ldsm_x4(vfr[kk], sV + (warp * 16 + (lane & 15)) * LDS + kk * 16 + (lane >> 4) * 8);
+      }
+    }
+    // S^T = K Q^T and dP^T = V dO^T : 16 keys x 64 queries per warp
+    float st[8][4], dpt[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) st[i][j] = dpt[i][j] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < HD / 16; ++kk) {
+#pragma unroll
+      for (int np = 0; np < 4; ++np) {
+        uint32_t qf[4], of[4];
+        const int row = np * 16 + (lane & 7) + ((lane >> 4) << 3);
+        const int col = kk * 16 + ((lane >> 3) & 1) * 8;
+        ldsm_x4(qf, sQ + row * LDS + col);
+        ldsm_x4(of, sdO + row * LDS + col);
+        mma_bf16(st[2 * np], kf[kk], qf[0], qf[1]);
+        mma_bf16(st[2 * np + 1], kf[kk], qf[2], qf[3]);
+        mma_bf16(dpt[2 * np], vfr[kk], of[0], of[1]);
+        mma_bf16(dpt[2 * np + 1], vfr[kk], of[2], of[3]);
+      }
+    }
+    // P^T, dropout, dS^T
+    float pd[8][4];
+#pragma unroll
+    for (int nb = 0; nb < 8; ++nb) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int ql = nb * 8 + 2 * t + (j & 1);
+        const int q = q0 + ql;
+        const int key = k0 + warp * 16 + g + 8 * (j >> 1);
+        float P = (q < s && key < s) ? exp2f(st[nb][j] * c2 - sL[ql]) : 0.f;
+        float keep = 1.f;
+        if (thr != 0u && P != 0.f) {
+          keep = keep_one(seed, p.site, (stream + static_cast<uint64_t>(q)) * s + key, thr)
+                     ? inv_keep
+                     : 0.f;
+        }
+        pd[nb][j] = P * keep;
+        st[nb][j] = P * (dpt[nb][j] * keep - sD[ql]);  // dS^T
+      }
+    }
+    // dV += Pd^T dO ; dK += dS^T Q   (k-dim = queries)
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      uint32_t pa[4], sa[4];
+      pa[0] = pack2(pd[2 * kk][0], pd[2 * kk][1]);
+      pa[1] = pack2(pd[2 * kk][2], pd[2 * kk][3]);
+      pa[2] = pack2(pd[2 * kk + 1][0], pd[2 * kk + 1][1]);
+      pa[3] = pack2(pd[2 * kk + 1][2], pd[2 * kk + 1][3]);
+      sa[0] = pack2(st[2 * kk][0], st[2 * kk][1]);
+      sa[1] = pack2(st[2 * kk][2], st[2 * kk][3]);
+      sa[2] = pack2(st[2 * kk + 1][0], st[2 * kk + 1][1]);
+      sa[3] = pack2(st[2 * kk + 1][2], st[2 * kk + 1][3]);
+#pragma unroll
+      for (int np = 0; np < HD / 16; ++np) {
+        uint32_t of[4], qf[4];
+        const int row = kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+        const int col = np * 16 + (lane >> 4) * 8;
+        ldsm_x4_t(of, sdO + row * LDS + col);
+        ldsm_x4_t(qf, sQ + row * LDS + col);
+        mma_bf16(dv[2 * np], pa, of[0], of[1]);
+        mma_bf16(dv[2 * np + 1], pa, of[2], of[3]);
+        mma_bf16(dk[2 * np], sa, qf[0], qf[1]);
+        mma_bf16(dk[2 * np + 1], sa, qf[2], qf[3]);
+      }
+      // stash dS^T (bf16) for the dQ product
+      const int kr = warp * 16 + g;
+      *reinterpret_cast<uint32_t*>(sdS + kr * LDP + kk * 16 + 2 * t) = sa[0];
+      *reinterpret_cast<uint32_t*>(sdS + (kr + 8) * LDP + kk * 16 + 2 * t) = sa[1];
+      *reinterpret_cast<uint32_t*>(sdS + kr * LDP + kk * 16 + 8 + 2 * t) = sa[2];
+      *reinterpret_cast<uint32_t*>(sdS + (kr + 8) * LDP + kk * 16 + 8 + 2 * t) = sa[3];
+    }
+    __syncthreads();
+    // dQ[q][d] += sum_k dS[q][k] K[k][d] : warp w owns queries [16w, 16w+16)
+    {
+      float dq[HD / 8][4];
+#pragma unroll
+      for (int i = 0; i < HD / 8; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {  // 16 keys per step
+        uint32_t a[4];
+        // A[q][k] = dS^T[k][q]: transpose-load from the [k][q] stash
+        ldsm_x4_t(a, sdS + (kk * 16 + (lane & 7) + (lane >> 4) * 8) * LDP + warp * 16 +
+                         ((lane >> 3) & 1) * 8);
+#pragma unroll
+        for (int np = 0; np < HD / 16; ++np) {
+          uint32_t bf[4];
+          ldsm_x4_t(bf, sK + (kk * 16 + (lane & 7) + ((lane >> 3) & 1) * 8) * LDS + np * 16 +
+                            (lane >> 4) * 8);
+          mma_bf16(dq[2 * np], a, bf[0], bf[1]);
+          mma_bf16(dq[2 * np + 1], a, bf[2], bf[3]);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int q = q0 + warp * 16 + g + 8 * r;
+        if (q >= s) continue;
+        float* dst = dqacc + static_cast<int64_t>(q) * HD;
+#pragma unroll
+        for (int i = 0; i < HD / 8; ++i) {
+          atomicAdd(dst + i * 8 + 2 * t, dq[i][2 * r]);
+          atomicAdd(dst + i * 8 + 2 * t + 1, dq[i][2 * r + 1]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // write dK, dV (scaled) into dqkv
+  auto* dqkv = static_cast<__nv_bfloat16*>(p.dqkv);
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int key = k0 + warp * 16 + g + 8 * r;
+    if (key >= s) continue;
+    __nv_bfloat16* row = dqkv + (static_cast<int64_t>(b) * s + key) * ld + h * HD;
+    __nv_bfloat16* dK = row + static_cast<int64_t>(H) * HD;
+    __nv_bfloat16* dV = dK + static_cast<int64_t>(H) * HD;
+#pragma unroll
+    for (int i = 0; i < HD / 8; ++i) {
+      *reinterpret_cast<uint32_t*>(dK + i * 8 + 2 * t) =
+          pack2(dk[i][2 * r] * p.scale, dk[i][2 * r + 1] * p.scale);
+      *reinterpret_cast<uint32_t*>(dV + i * 8 + 2 * t) = pack2(dv[i][2 * r], dv[i][2 * r + 1]);
+    }
+  }
+}
+
+// dq (fp32, [bh][s][HD]) * scale -> bf16 Q slot of dqkv
+template <int HD>
+__global__ void attn_bwd_dq_kernel(const gx_attention_args p) {
+  const int s = p.seq, H = p.heads;
+  const int64_t total = static_cast<int64_t>(p.batch) * H * s * (HD / 2);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int d2 = static_cast<int>(i % (HD / 2));
+    const int64_t row = i / (HD / 2);  // bh * s + q
+    const int q = static_cast<int>(row % s);
+    const int bh = static_cast<int>(row / s);
+    const int b = bh / H, h = bh % H;
+    const float2 v = reinterpret_cast<const float2*>(p.dq_accum)[i];
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(p.dqkv) +
+                         (static_cast<int64_t>(b) * s + q) * p.ld_qkv + h * HD + 2 * d2;
+    *reinterpret_cast<uint32_t*>(dst) = pack2(v.x * p.scale, v.y * p.scale);
+  }
+}
+
+// ------------------------------------------------------------------------------ host
+
+template <int HD>
+static int attention_fwd_impl(const gx_attention_args& a, cudaStream_t st) {
+  constexpr int LDS = HD + 8;
+  const int smem = 5 * kBlk * LDS * 2;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(attn_fwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set = true;
+  }
+  dim3 grid((a.seq + kBlk - 1) / kBlk, a.batch * a.heads);
+  attn_fwd_kernel<HD><<<grid, kThreads, smem, st>>>(a);
+  return check_launch("attn_fwd_kernel");
+}
+
+template <int HD>
+static int attention_bwd_impl(const gx_attention_args& a, cudaStream_t st) {
+  constexpr int LDS = HD + 8;
+  const int smem = 4 * kBlk * LDS * 2 + kBlk * (kBlk + 8) * 2 + 2 * kBlk * 4;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(attn_bwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set = true;
+  }
+  const int rows = a.batch * a.heads * a.seq;
+  attn_bwd_prep_kernel<HD><<<(rows + 7) / 8, 256, 0, st>>>(a);
+  if (int rc = check_launch("attn_bwd_prep_kernel")) return rc;
+  dim3 grid((a.seq + kBlk - 1) / kBlk, a.batch * a.heads);
+  attn_bwd_kernel<HD><<<grid, kThreads, smem, st>>>(a);
+  if (int rc = check_launch("attn_bwd_kernel")) return rc;
+  const int64_t work = static_cast<int64_t>(rows) * (HD / 2);
+  int blocks = static_cast<int>((work + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  attn_bwd_dq_kernel<HD><<<blocks, 256, 0, st>>>(a);
+  return check_launch("attn_bwd_dq_kernel");
+}
+
+int attention_fwd(const gx_attention_args& a, cudaStream_t st) {
+  if (a.seq <= 0 || a.batch <= 0 || a.heads <= 0) return set_error(kErrConfig, "attention: empty");
+  switch (a.head_dim) {
+    case 64: return attention_fwd_impl<64>(a, st);
+    case 80: return attention_fwd_impl<80>(a, st);
+    case 128: return attention_fwd_impl<128>(a, st);
+    default: return set_error(kErrConfig, "attention: head_dim must be 64, 80 or 128");
+  }
+}
+
+int attention_bwd(const gx_attention_args& a, cudaStream_t st) {
+  if (a.seq <= 0 || a.batch <= 0 || a.heads <= 0) return set_error(kErrConfig, "attention: empty");
+  switch (a.head_dim) {
+    case 64: return attention_bwd_impl<64>(a, st);
+    case 80: return attention_bwd_impl<80>(a, st);
+    case 128: return attention_bwd_impl<128>(a, st);
+    default: return set_error(kErrConfig, "attention: head_dim must be 64, 80 or 128");
+  }
+}
+
+}  // namespace gx

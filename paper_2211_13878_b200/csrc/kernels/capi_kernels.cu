@@ -9,3 +9,52 @@ extern "C" int gx_k_gemm_bf16(const void* a, int64_t lda, int a_mn_major, const 
   gx::GemmOperand B{b, ldb, b_mn_major != 0};
   return gx::gemm_bf16(A, B, M, N, K, *ep, static_cast<cudaStream_t>(stream), tile_n);
 }
+
+namespace {
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+}  // namespace
+
+extern "C" int gx_k_attention_fwd(const gx_attention_args* a, void* stream) {
+  if (a == nullptr) return gx::set_error(gx::kErrConfig, "attention: args NULL");
+  return gx::attention_fwd(*a, S(stream));
+}
+extern "C" int gx_k_attention_bwd(const gx_attention_args* a, void* stream) {
+  if (a == nullptr) return gx::set_error(gx::kErrConfig, "attention: args NULL");
+  return gx::attention_bwd(*a, S(stream));
+}
+extern "C" int gx_k_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y,
+                                  void* mean, void* rstd, int rows, int h, void* stream) {
+  return gx::layernorm_fwd(x, gamma, beta, y, mean, rstd, rows, h, S(stream));
+}
+extern "C" int gx_k_layernorm_bwd(const void* dy, const void* x, const void* mean,
+                                  const void* rstd, const void* gamma, const void* dres, void* dx,
+                                  void* dgamma, void* dbeta, int rows, int h, void* stream) {
+  return gx::layernorm_bwd(dy, x, mean, rstd, gamma, dres, dx, dgamma, dbeta, rows, h, S(stream));
+}
+extern "C" int gx_k_bias_dropout_add(const void* x, const void* bias, const void* residual,
+                                     void* out, int rows, int cols, const gx_dropout* d,
+                                     void* stream) {
+  gx_dropout off{};
+  return gx::bias_dropout_add(x, bias, residual, out, rows, cols, d ? *d : off, S(stream));
+}
+extern "C" int gx_k_dropout_bwd_colsum(const void* dy, void* dz, void* dbias, int rows, int cols,
+                                       const gx_dropout* d, void* stream) {
+  gx_dropout off{};
+  return gx::dropout_bwd_colsum(dy, dz, dbias, rows, cols, d ? *d : off, S(stream));
+}
+extern "C" int gx_k_colsum(const void* x, int64_t ld, void* acc, int rows, int cols,
+                           void* stream) {
+  return gx::colsum(x, ld, acc, rows, cols, S(stream));
+}
+extern "C" int gx_k_mse_loss(const void* y, const void* target, void* dy, void* loss, int64_t n,
+                             float inv_count, void* stream) {
+  return gx::mse_loss(y, target, dy, loss, n, inv_count, S(stream));
+}
+extern "C" int gx_k_adamw(void* master, const void* grad, void* m, void* v, void* out, int64_t n,
+                          float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
+                          void* stream) {
+  return gx::adamw(master, grad, m, v, out, n, lr, b1, b2, eps, wd, bc1, bc2, S(stream));
+}
+extern "C" int gx_k_cast_bf16(const void* src, void* dst, int64_t n, void* stream) {
+  return gx::cast_bf16(src, dst, n, S(stream));
+}

@@ -43,6 +43,11 @@ struct GemmCfg {
 __device__ __forceinline__ float gelu_erf(float x) {
   return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
 }
+// d/dx [x * Phi(x)] = Phi(x) + x * phi(x)
+__device__ __forceinline__ float gelu_erf_grad(float x) {
+  return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) +
+         x * 0.3989422804014327f * __expf(-0.5f * x * x);
+}
 
 // Applies the epilogue to 32 consecutive accumulator columns [n0, n0+32) of row `row`.
 __device__ __forceinline__ void epilogue_row32(const GemmEpilogue& ep, int64_t row, int n0,
@@ -69,6 +74,26 @@ __device__ __forceinline__ void epilogue_row32(const GemmEpilogue& ep, int64_t r
     } else {
       for (int j = 0; j < 32; ++j)
         if (n0 + j < N) v[j] += __bfloat162float(bias[n0 + j]);
+    }
+  }
+  if (ep.gelu_bwd) {
+    // dgrad epilogue of the MLP up-projection: v <- v * gelu'(pre)
+    const __nv_bfloat16* auxp = static_cast<const __nv_bfloat16*>(ep.aux) + row * ep.ld_aux + n0;
+    if (full) {
+      const uint4* ap = reinterpret_cast<const uint4*>(auxp);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 b = ap[q];
+        const uint32_t w[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          v[q * 8 + 2 * t] *= gelu_erf_grad(bf16_lo(w[t]));
+          v[q * 8 + 2 * t + 1] *= gelu_erf_grad(bf16_hi(w[t]));
+        }
+      }
+    } else {
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < N) v[j] *= gelu_erf_grad(__bfloat162float(auxp[j]));
     }
   }
   if (ep.gelu) {
@@ -100,12 +125,13 @@ __device__ __forceinline__ void epilogue_row32(const GemmEpilogue& ep, int64_t r
     // out = residual + dropout(v), dropout element index = (row_offset+row)*drop_ld + col
     const uint64_t grow = static_cast<uint64_t>(ep.row_offset + row);
     if (ep.drop_threshold != 0u) {
+      const uint64_t seed = ep.seed + (ep.seed_offset != nullptr ? *ep.seed_offset : 0ull);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const uint64_t e0 = grow * static_cast<uint64_t>(ep.drop_ld) +
                             static_cast<uint64_t>(ep.col_offset + n0 + q * 4);
         // e0 is a multiple of 4 whenever drop_ld and the column offsets are (checked on host)
-        const Philox4 w = dropout_words(ep.seed, ep.site, e0 >> 2);
+        const Philox4 w = dropout_words(seed, ep.site, e0 >> 2);
         v[q * 4 + 0] = w.x >= ep.drop_threshold ? v[q * 4 + 0] * ep.drop_scale : 0.f;
         v[q * 4 + 1] = w.y >= ep.drop_threshold ? v[q * 4 + 1] * ep.drop_scale : 0.f;
         v[q * 4 + 2] = w.z >= ep.drop_threshold ? v[q * 4 + 2] * ep.drop_scale : 0.f;
@@ -355,7 +381,7 @@ static bool make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t
   return r == CUDA_SUCCESS;
 }
 
-static int num_sms() {
+int num_sms() {
   static int n = 0;
   if (n == 0) {
     int dev = 0;
@@ -411,8 +437,9 @@ static int pick_bn(int M, int N) {
 int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
               const GemmEpilogue& ep, cudaStream_t stream, int force_bn) {
   if (M <= 0 || N <= 0 || K <= 0) return set_error(kErrConfig, "gemm: empty problem");
-  if ((N % 8) != 0 || (K % 8) != 0 || (M % 8) != 0)
-    return set_error(kErrConfig, "gemm: M, N and K must be multiples of 8");
+  // TMA: row strides must be 16-byte multiples; the epilogue's vector stores need ldo too.
+  if ((a.ld % 8) != 0 || (b.ld % 8) != 0 || (ep.ldo % 8) != 0)
+    return set_error(kErrConfig, "gemm: lda, ldb and ldo must be multiples of 8 elements");
   const int bn = force_bn > 0 ? force_bn : pick_bn(M, N);
 #define GX_GEMM_DISPATCH(BN_)                                                           \
   if (bn == BN_) {                                                                      \

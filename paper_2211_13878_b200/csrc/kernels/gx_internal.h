@@ -22,6 +22,8 @@ enum ErrorCode : int {
 int set_error(int code, const char* msg);
 // Returns kOk or records the pending launch error.
 int check_launch(const char* what);
+// Number of kernels launched successfully through check_launch (process-wide).
+int64_t launch_count();
 
 enum OutKind : int { kOutBF16 = GX_OUT_BF16, kOutF32 = GX_OUT_F32, kOutF32Accumulate = GX_OUT_F32_ACC };
 
@@ -35,5 +37,33 @@ using GemmEpilogue = gx_gemm_epilogue;
 
 int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
               const GemmEpilogue& ep, cudaStream_t stream, int force_bn = 0);
+
+int attention_fwd(const gx_attention_args& a, cudaStream_t st);
+int attention_bwd(const gx_attention_args& a, cudaStream_t st);
+int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, void* mean,
+                  void* rstd, int rows, int h, cudaStream_t st);
+int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
+                  const void* gamma, const void* dres, void* dx, void* dgamma, void* dbeta,
+                  int rows, int h, cudaStream_t st);
+int bias_dropout_add(const void* x, const void* bias, const void* residual, void* out, int rows,
+                     int cols, const gx_dropout& d, cudaStream_t st);
+int dropout_bwd_colsum(const void* dy, void* dz, void* dbias, int rows, int cols,
+                       const gx_dropout& d, cudaStream_t st);
+int colsum(const void* x, int64_t ld, void* acc, int rows, int cols, cudaStream_t st);
+int mse_loss(const void* y, const void* target, void* dy, void* loss, int64_t n, float inv_count,
+             cudaStream_t st);
+int adamw(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n, float lr,
+          float beta1, float beta2, float eps, float wd, float bc1, float bc2, cudaStream_t st);
+int cast_bf16(const void* src, void* dst, int64_t n, cudaStream_t st);
+int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n,
+              float lr, float beta1, float beta2, float eps, float wd, const int64_t* step,
+              cudaStream_t st);
+int bump_step(int64_t* step, uint64_t* seed_offset, cudaStream_t st);
+struct PtrPack {
+  const void* p[16];
+  int n;
+};
+int sum_ptrs(const PtrPack& srcs, void* out, int64_t n, bool bf16, cudaStream_t st);
+int num_sms();
 
 }  // namespace gx

@@ -1,0 +1,1308 @@
+// executor.cc — the plan executor (see executor.h for the contract and the reference
+// semantics each piece follows).
+//
+// Execution model: a set of *local ranks* is driven in lockstep.  NCCL mode has exactly one
+// local rank per process (one GPU each); sim mode places every rank of the world on this
+// device and routes collectives through SimComm.  Each layer's forward/backward is split
+// into phases that end at a collective, and the driver runs phase k for every local rank of
+// the stage before phase k+1, so the same code path serves both modes.
+#include "executor.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <sstream>
+
+#include <nlohmann/json.hpp>
+
+#include "../kernels/gx_internal.h"
+#include "parplan/strategy.h"
+
+namespace gx {
+
+using nlohmann::json;
+
+namespace {
+
+int64_t pad64(int64_t n) { return (n + 63) / 64 * 64; }
+
+#define GX_TRY(expr)                 \
+  do {                               \
+    const int gx_rc_ = (expr);       \
+    if (gx_rc_ != kOk) return gx_rc_; \
+  } while (0)
+
+int cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return kOk;
+  return set_error(kErrCuda, (std::string(what) + ": " + cudaGetErrorString(e)).c_str());
+}
+
+}  // namespace
+
+Layout make_layout(const Shape& s, int tp, int sdp) {
+  Layout L;
+  int64_t off = 0;
+  auto put = [&](Slot& slot, int64_t n) {
+    slot.off = off;
+    slot.n = n;
+    off += pad64(n);
+  };
+  const int64_t h = s.h, f = s.ffn;
+  put(L.ln1g, h);
+  put(L.ln1b, h);
+  put(L.ln2g, h);
+  put(L.ln2b, h);
+  put(L.bqkv, 3 * h / tp);
+  put(L.bo, h);
+  put(L.b1, f / tp);
+  put(L.b2, h);
+  L.acc_end = off;
+  put(L.wqkv, 3 * h / tp * h);
+  put(L.wo, h * (h / tp));
+  put(L.w1, f / tp * h);
+  put(L.w2, h * (f / tp));
+  const int64_t q = 64 * static_cast<int64_t>(sdp);
+  L.total = (off + q - 1) / q * q;
+  return L;
+}
+
+int64_t canonical_size(const Shape& s) {
+  const int64_t h = s.h, f = s.ffn;
+  return 4 * h + 3 * h + h + f + h + 3 * h * h + h * h + f * h + h * f;
+}
+
+namespace {
+
+// Canonical index of local flat element `j` of rank (tp degree t, tp index tr); -1 = padding.
+int64_t canon_index(const Shape& s, const Layout& L, int t, int tr, int64_t j) {
+  const int64_t h = s.h, f = s.ffn, ht = h / t, ft = f / t;
+  // canonical offsets (tp = 1, unpadded)
+  const int64_t c_ln1g = 0, c_ln1b = h, c_ln2g = 2 * h, c_ln2b = 3 * h, c_bqkv = 4 * h,
+                c_bo = 7 * h, c_b1 = 8 * h, c_b2 = 8 * h + f, c_wqkv = 9 * h + f,
+                c_wo = c_wqkv + 3 * h * h, c_w1 = c_wo + h * h, c_w2 = c_w1 + f * h;
+  auto in = [&](const Slot& sl, int64_t& k) {
+    if (j < sl.off || j >= sl.off + sl.n) return false;
+    k = j - sl.off;
+    return true;
+  };
+  int64_t k = 0;
+  if (in(L.ln1g, k)) return c_ln1g + k;
+  if (in(L.ln1b, k)) return c_ln1b + k;
+  if (in(L.ln2g, k)) return c_ln2g + k;
+  if (in(L.ln2b, k)) return c_ln2b + k;
+  if (in(L.bo, k)) return c_bo + k;
+  if (in(L.b2, k)) return c_b2 + k;
+  if (in(L.bqkv, k)) return c_bqkv + (k / ht) * h + tr * ht + k % ht;
+  if (in(L.b1, k)) return c_b1 + tr * ft + k;
+  if (in(L.wqkv, k)) {
+    const int64_t row = k / h, col = k % h;
+    return c_wqkv + ((row / ht) * h + tr * ht + row % ht) * h + col;
+  }
+  if (in(L.w1, k)) return c_w1 + (tr * ft + k / h) * h + k % h;
+  if (in(L.wo, k)) return c_wo + (k / ht) * h + tr * ht + k % ht;
+  if (in(L.w2, k)) return c_w2 + (k / ft) * f + tr * ft + k % ft;
+  return -1;
+}
+
+// ------------------------------------------------------------------ device allocations
+class Arena {
+ public:
+  ~Arena() {
+    for (void* p : ptrs_) cudaFree(p);
+  }
+  void* alloc(size_t bytes) {
+    if (bytes == 0) return nullptr;
+    void* p = nullptr;
+    if (cudaMalloc(&p, (bytes + 255) / 256 * 256) != cudaSuccess) {
+      failed_ = true;
+      return nullptr;
+    }
+    ptrs_.push_back(p);
+    bytes_ += bytes;
+    return p;
+  }
+  template <typename T>
+  T* a(int64_t n) {
+    return static_cast<T*>(alloc(static_cast<size_t>(n) * sizeof(T)));
+  }
+  bool failed() const { return failed_; }
+  size_t bytes() const { return bytes_; }
+
+ private:
+  std::vector<void*> ptrs_;
+  size_t bytes_ = 0;
+  bool failed_ = false;
+};
+
+using bf16 = __nv_bfloat16;
+
+struct Acts {
+  int64_t sample0 = 0;  // first global sample of this chunk (within the iteration)
+  int samples = 0;
+  int rows = 0;  // samples * seq
+  bf16 *x = nullptr, *ln1 = nullptr, *qkv = nullptr, *ctx = nullptr, *x1 = nullptr,
+       *ln2 = nullptr, *pre = nullptr, *gel = nullptr, *y = nullptr;
+  float *lse = nullptr, *mean1 = nullptr, *rstd1 = nullptr, *mean2 = nullptr, *rstd2 = nullptr;
+};
+
+enum class Xin { kSame, kSlice, kGather, kStageInput };
+
+struct RankLayer {
+  int layer = 0;  // global layer id
+  Shape sh;
+  Deg d;
+  int tr = 0, dr = 0, sr = 0, pr = 0;
+  int g_tp = -1, g_sdp = -1, g_dp = -1, g_xin = -1;  // group ids (-1: none)
+  Xin xin = Xin::kStageInput;
+  Layout lay;
+  int64_t shard_n = 0;
+  float *master = nullptr, *m = nullptr, *v = nullptr, *gfull = nullptr, *gshard = nullptr;
+  bf16 *pshard = nullptr, *pfull = nullptr;
+  std::vector<Acts> acts;  // per micro-batch
+};
+
+struct RankCtx {
+  int rank = 0, stage = 0, idx = 0;
+  std::vector<RankLayer> layers;  // this stage's layers in order
+  Arena arena;
+  // scratch
+  bf16 *partial = nullptr, *dz = nullptr, *dpre = nullptr, *dc = nullptr, *dx1 = nullptr,
+       *dout = nullptr, *dctx = nullptr, *dqkv = nullptr, *da = nullptr;
+  bf16* gbuf[2] = {nullptr, nullptr};
+  float *dq_acc = nullptr, *dsum = nullptr;
+  bf16 *x_in = nullptr, *target = nullptr;  // [m micro-batches of this rank's rows][h]
+  bf16* dx_out = nullptr;                   // first stage: input gradient per micro-batch
+  float *loss = nullptr, *loss_dummy = nullptr;
+  int64_t* step = nullptr;
+  uint64_t* seed_off = nullptr;
+  int64_t in_rows_total = 0;
+  std::vector<int64_t> in_row_off;  // per micro-batch offset (rows) into x_in / target
+  int cur = 0;                      // index of gbuf holding the current dY
+};
+
+// --------------------------------------------------------------------------------------
+class ExecutorImpl final : public Executor {
+ public:
+  int init(const json& cfg, std::string* err);
+  int set_layer_params(int layer, const float* canonical, int64_t n) override;
+  int export_layer(int layer, int what, float* canonical, int64_t n) override;
+  int load_batch(const void* x_host, const void* target_host) override;
+  int load_batch_device(const void* x_dev, const void* target_dev) override;
+  int run(bool use_graph) override;
+  int loss(float* out) override;
+  int export_output(void* host_bf16, int what) override;
+  cudaStream_t stream() const override { return stream_; }
+  std::string info() const override;
+  ~ExecutorImpl() override {
+    if (graph_exec_ != nullptr) cudaGraphExecDestroy(graph_exec_);
+    if (graph_ != nullptr) cudaGraphDestroy(graph_);
+    ranks_.clear();
+    comm_.reset();
+    if (stream_ != nullptr) cudaStreamDestroy(stream_);
+  }
+
+ private:
+  // topology helpers
+  int stage_of_layer(int l) const {
+    for (int s = 0; s < P_; ++s)
+      if (l >= stage_range_[s].first && l < stage_range_[s].second) return s;
+    return -1;
+  }
+  void chunk(const Deg& d, int idx, int mb, int64_t& lo, int64_t& hi) const {
+    const int t = d.tp, D = d.data();
+    const int c = idx / t;
+    const int64_t base = static_cast<int64_t>(mb) * Bm_;
+    lo = base + static_cast<int64_t>(c) * Bm_ / D;
+    hi = base + static_cast<int64_t>(c + 1) * Bm_ / D;
+  }
+  int build_groups();
+  int allocate(RankCtx& r);
+  int step_once();
+
+  // per-phase work
+  int fwd_phase(RankCtx& r, int li, int mb, int phase);
+  int bwd_phase(RankCtx& r, int li, int mb, int phase);
+  int sync_phase(RankCtx& r, int li, int phase);
+  int xin_fwd(RankCtx& r, int li, int mb);
+  int xin_bwd(RankCtx& r, int li, int mb);
+  int gather_params(RankCtx& r, int li);
+  int pp_fwd(RankCtx& r, int mb, bool send);
+  int pp_bwd(RankCtx& r, int mb, bool send);
+
+  int gemm(const void* a, int64_t lda, bool amn, const void* b, int64_t ldb, bool bmn, int M, int N,
+           int K, const gx_gemm_epilogue& ep) {
+    return gemm_bf16(GemmOperand{a, lda, amn}, GemmOperand{b, ldb, bmn}, M, N, K, ep, stream_);
+  }
+  gx_gemm_epilogue epi() const {
+    gx_gemm_epilogue e{};
+    e.alpha = 1.f;
+    e.drop_scale = 1.f;
+    return e;
+  }
+  // config
+  json plan_, model_;
+  int world_ = 1, P_ = 1, g_ = 1, m_ = 1, B_ = 1, Bm_ = 1, L_ = 0;
+  std::vector<std::pair<int, int>> stage_range_;
+  std::vector<Deg> deg_;
+  std::vector<Shape> shape_;
+  bool sim_ = true;
+  float p_attn_ = 0.f, p_hidden_ = 0.f;
+  uint32_t thr_attn_ = 0, thr_hidden_ = 0;
+  uint64_t seed_ = 1234;
+  float lr_ = 1e-4f, b1_ = 0.9f, b2_ = 0.999f, eps_ = 1e-8f, wd_ = 0.f;
+  bool optimizer_ = true;
+  float inv_count_ = 1.f;
+
+  std::unique_ptr<Comm> comm_;
+  std::vector<std::unique_ptr<RankCtx>> ranks_;
+  cudaStream_t stream_ = nullptr;
+  cudaGraph_t graph_ = nullptr;
+  cudaGraphExec_t graph_exec_ = nullptr;
+  int64_t steps_run_ = 0;
+  int64_t launches_per_step_ = 0;
+};
+
+uint32_t threshold_of(float p) {
+  if (p <= 0.f) return 0u;
+  const double t = static_cast<double>(p) * 4294967296.0;
+  return t >= 4294967295.0 ? 0xFFFFFFFFu : static_cast<uint32_t>(t);
+}
+
+int ExecutorImpl::init(const json& cfg, std::string* err) {
+  try {
+    plan_ = cfg.at("plan");
+    model_ = cfg.at("model");
+    world_ = cfg.at("world_size").get<int>();
+    sim_ = cfg.value("comm", std::string("sim")) == "sim";
+    p_attn_ = cfg.value("dropout_attn", 0.0f);
+    p_hidden_ = cfg.value("dropout_hidden", 0.0f);
+    seed_ = cfg.value("seed", static_cast<uint64_t>(1234));
+    lr_ = cfg.value("lr", 1e-4f);
+    b1_ = cfg.value("beta1", 0.9f);
+    b2_ = cfg.value("beta2", 0.999f);
+    eps_ = cfg.value("eps", 1e-8f);
+    wd_ = cfg.value("weight_decay", 0.0f);
+    optimizer_ = cfg.value("optimizer", true);
+    thr_attn_ = threshold_of(p_attn_);
+    thr_hidden_ = threshold_of(p_hidden_);
+
+    P_ = plan_.at("pp_degree").get<int>();
+    m_ = plan_.at("micro_batches").get<int>();
+    B_ = plan_.at("batch_size").get<int>();
+    if (world_ % P_ != 0) {
+      *err = "executor: world_size must be a multiple of pp_degree";
+      return kErrConfig;
+    }
+    g_ = world_ / P_;
+    if (B_ % m_ != 0) {
+      *err = "executor: micro_batches must divide batch_size";
+      return kErrConfig;
+    }
+    Bm_ = B_ / m_;
+    const json& layers = model_.at("layers");
+    L_ = static_cast<int>(layers.size());
+    deg_.assign(L_, Deg{});
+    shape_.assign(L_, Shape{});
+    for (int l = 0; l < L_; ++l) {
+      const json& sh = layers[l].at("shape");
+      Shape s;
+      s.h = sh.at("hidden").get<int>();
+      s.heads = sh.at("heads").get<int>();
+      s.hd = sh.value("head_dim", s.h / s.heads);
+      s.seq = sh.at("seq").get<int>();
+      s.ffn = sh.at("ffn").get<int>();
+      const std::string kind = sh.value("kind", std::string("encoder"));
+      if (kind != "encoder") {
+        *err = "executor: layer kind '" + kind + "' not supported yet (encoder only)";
+        return kErrConfig;
+      }
+      if (s.hd * s.heads != s.h) {
+        *err = "executor: heads * head_dim must equal hidden";
+        return kErrConfig;
+      }
+      shape_[l] = s;
+    }
+    for (const json& st : plan_.at("stages")) {
+      const int b = st.at("layer_range")[0].get<int>(), e = st.at("layer_range")[1].get<int>();
+      stage_range_.push_back({b, e});
+      for (const json& jl : st.at("layers")) {
+        const int id = jl.at("id").get<int>();
+        const auto hs = parplan::StrategyFromString(jl.at("strategy").get<std::string>());
+        const auto dd = hs.DimDegrees();
+        if (hs.group_size != g_) {
+          *err = "executor: strategy group size does not match world_size / pp_degree";
+          return kErrConfig;
+        }
+        deg_[id] = Deg{dd.dp, dd.sdp, dd.tp};
+      }
+    }
+    if (static_cast<int>(stage_range_.size()) != P_) {
+      *err = "executor: plan stage count != pp_degree";
+      return kErrConfig;
+    }
+    for (int l = 0; l < L_; ++l) {
+      const Shape& s = shape_[l];
+      const Deg& d = deg_[l];
+      if (s.heads % d.tp || s.ffn % d.tp || s.h % d.tp) {
+        *err = "executor: tp degree must divide heads, hidden and ffn";
+        return kErrConfig;
+      }
+      if ((s.h / d.tp) % 8 || (s.ffn / d.tp) % 8) {
+        *err = "executor: hidden/tp and ffn/tp must be multiples of 8";
+        return kErrConfig;
+      }
+      if (d.data() > Bm_) {
+        *err = "executor: more data replicas than samples per micro-batch";
+        return kErrConfig;
+      }
+      if (l > 0 && shape_[l].h != shape_[l - 1].h && stage_of_layer(l) == stage_of_layer(l - 1)) {
+        *err = "executor: hidden size changes between layers (patch merging) not supported yet";
+        return kErrConfig;
+      }
+    }
+    inv_count_ = 1.0f / (static_cast<float>(B_) * shape_.back().seq * shape_.back().h);
+
+    std::vector<int> local;
+    if (cfg.contains("local_ranks")) {
+      local = cfg.at("local_ranks").get<std::vector<int>>();
+    } else {
+      for (int r = 0; r < world_; ++r) local.push_back(r);
+    }
+    if (sim_) {
+      comm_ = make_sim_comm(world_);
+    } else {
+      if (local.size() != 1) {
+        *err = "executor: nccl mode drives exactly one local rank";
+        return kErrConfig;
+      }
+      std::string hex = cfg.at("nccl_id_hex").get<std::string>();
+      std::string id(hex.size() / 2, '\0');
+      for (size_t i = 0; i < id.size(); ++i)
+        id[i] = static_cast<char>(std::stoi(hex.substr(2 * i, 2), nullptr, 16));
+      comm_ = make_nccl_comm(world_, local[0], id, err);
+      if (!comm_) return kErrNccl;
+    }
+    if (cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking) != cudaSuccess) {
+      *err = "executor: cudaStreamCreate failed";
+      return kErrCuda;
+    }
+    for (int r : local) {
+      auto rc = std::make_unique<RankCtx>();
+      rc->rank = r;
+      rc->stage = r / g_;
+      rc->idx = r % g_;
+      ranks_.push_back(std::move(rc));
+    }
+  } catch (const std::exception& e) {
+    *err = std::string("executor config: ") + e.what();
+    return kErrConfig;
+  }
+  int rc = build_groups();
+  if (rc != kOk) {
+    *err = gx_last_error();
+    return rc;
+  }
+  for (auto& r : ranks_) {
+    rc = allocate(*r);
+    if (rc != kOk) {
+      *err = gx_last_error();
+      return rc;
+    }
+  }
+  return kOk;
+}
+
+int ExecutorImpl::build_groups() {
+  // Identical registration order on every process (NCCL splits are world collectives).
+  for (int s = 0; s < P_; ++s) {
+    const int base = s * g_;
+    for (int l = stage_range_[s].first; l < stage_range_[s].second; ++l) {
+      const Deg& d = deg_[l];
+      for (int i = 0; i < g_; ++i) {
+        const int tr = i % d.tp, dr = i / d.tp, sr = dr % d.sdp, pr = dr / d.sdp;
+        std::vector<int> tp, sdp, dp;
+        for (int j = 0; j < d.tp; ++j) tp.push_back(base + dr * d.tp + j);
+        for (int j = 0; j < d.sdp; ++j) sdp.push_back(base + (pr * d.sdp + j) * d.tp + tr);
+        for (int j = 0; j < d.dp; ++j) dp.push_back(base + (j * d.sdp + sr) * d.tp + tr);
+        const int gtp = d.tp > 1 ? comm_->add_group(tp) : -1;
+        const int gsdp = d.sdp > 1 ? comm_->add_group(sdp) : -1;
+        const int gdp = d.dp > 1 ? comm_->add_group(dp) : -1;
+        int gx = -1;
+        Xin xin = Xin::kStageInput;
+        if (l > stage_range_[s].first) {
+          const Deg& p = deg_[l - 1];
+          if (p.data() == d.data()) {
+            xin = Xin::kSame;
+          } else if (d.data() > p.data()) {
+            // slice forward; backward all-gathers dY over the k sub-chunks of the prev chunk
+            xin = Xin::kSlice;
+            const int c = i / p.tp, k = p.tp / d.tp;
+            std::vector<int> mem;
+            for (int r = 0; r < k; ++r) mem.push_back(base + c * p.tp + r * d.tp + i % d.tp);
+            gx = comm_->add_group(mem);
+          } else {
+            xin = Xin::kGather;
+            const int j = i / d.tp, k = d.tp / p.tp;
+            std::vector<int> mem;
+            for (int r = 0; r < k; ++r) mem.push_back(base + j * d.tp + r * p.tp + i % p.tp);
+            gx = comm_->add_group(mem);
+          }
+        }
+        for (auto& rc : ranks_) {
+          if (rc->rank != base + i) continue;
+          RankLayer L;
+          L.layer = l;
+          L.sh = shape_[l];
+          L.d = d;
+          L.tr = tr;
+          L.dr = dr;
+          L.sr = sr;
+          L.pr = pr;
+          L.g_tp = gtp;
+          L.g_sdp = gsdp;
+          L.g_dp = gdp;
+          L.g_xin = gx;
+          L.xin = xin;
+          rc->layers.push_back(std::move(L));
+        }
+      }
+    }
+  }
+  return comm_->finalize();
+}
+
+int ExecutorImpl::allocate(RankCtx& r) {
+  Arena& A = r.arena;
+  int64_t max_rows = 0, max_h = 0, max_f = 0, max_q = 0, max_c = 0, max_lse = 0;
+  for (size_t li = 0; li < r.layers.size(); ++li) {
+    RankLayer& L = r.layers[li];
+    const Shape& s = L.sh;
+    const int t = L.d.tp;
+    L.lay = make_layout(s, t, L.d.sdp);
+    L.shard_n = L.lay.total / L.d.sdp;
+    L.master = A.a<float>(L.shard_n);
+    L.m = A.a<float>(L.shard_n);
+    L.v = A.a<float>(L.shard_n);
+    L.gfull = A.a<float>(L.lay.total);
+    L.gshard = L.d.sdp > 1 ? A.a<float>(L.shard_n) : L.gfull;
+    L.pshard = A.a<bf16>(L.shard_n);
+    L.pfull = L.d.sdp > 1 ? A.a<bf16>(L.lay.total) : L.pshard;
+    cudaMemset(L.m, 0, L.shard_n * 4);
+    cudaMemset(L.v, 0, L.shard_n * 4);
+    L.acts.resize(m_);
+    for (int mb = 0; mb < m_; ++mb) {
+      Acts& a = L.acts[mb];
+      int64_t lo, hi;
+      chunk(L.d, r.idx, mb, lo, hi);
+      a.sample0 = lo;
+      a.samples = static_cast<int>(hi - lo);
+      a.rows = a.samples * s.seq;
+      const int64_t rows = a.rows;
+      const int64_t h = s.h, ht = s.h / t, ft = s.ffn / t;
+      // layer input: alias into the previous layer's output where the relayout allows
+      if (L.xin == Xin::kSame) {
+        a.x = r.layers[li - 1].acts[mb].y;
+      } else if (L.xin == Xin::kSlice) {
+        const Acts& p = r.layers[li - 1].acts[mb];
+        a.x = p.y + (a.sample0 - p.sample0) * s.seq * h;
+      } else {
+        a.x = A.a<bf16>(rows * h);
+      }
+      a.ln1 = A.a<bf16>(rows * h);
+      a.qkv = A.a<bf16>(rows * 3 * ht);
+      a.ctx = A.a<bf16>(rows * ht);
+      a.x1 = A.a<bf16>(rows * h);
+      a.ln2 = A.a<bf16>(rows * h);
+      a.pre = A.a<bf16>(rows * ft);
+      a.gel = A.a<bf16>(rows * ft);
+      a.y = A.a<bf16>(rows * h);
+      a.lse = A.a<float>(static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq);
+      a.mean1 = A.a<float>(rows);
+      a.rstd1 = A.a<float>(rows);
+      a.mean2 = A.a<float>(rows);
+      a.rstd2 = A.a<float>(rows);
+      max_rows = std::max(max_rows, rows);
+      max_h = std::max(max_h, rows * h);
+      max_f = std::max(max_f, rows * ft);
+      max_q = std::max(max_q, rows * 3 * ht);
+      max_c = std::max(max_c, rows * ht);
+      max_lse = std::max(max_lse, static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq);
+    }
+  }
+  r.partial = A.a<bf16>(max_h);
+  r.dz = A.a<bf16>(max_h);
+  r.dpre = A.a<bf16>(max_f);
+  r.dc = A.a<bf16>(max_h);
+  r.dx1 = A.a<bf16>(max_h);
+  r.dout = A.a<bf16>(max_h);
+  r.dctx = A.a<bf16>(max_c);
+  r.dqkv = A.a<bf16>(max_q);
+  r.da = A.a<bf16>(max_h);
+  r.gbuf[0] = A.a<bf16>(max_h);
+  r.gbuf[1] = A.a<bf16>(max_h);
+  r.dq_acc = A.a<float>(max_c);
+  r.dsum = A.a<float>(max_lse);
+  r.loss = A.a<float>(1);
+  r.loss_dummy = A.a<float>(1);
+  r.step = A.a<int64_t>(1);
+  r.seed_off = A.a<uint64_t>(1);
+  cudaMemset(r.step, 0, 8);
+  cudaMemset(r.seed_off, 0, 8);
+  // stage input (first stage) / targets (last stage) for all micro-batches of this rank
+  const RankLayer& first = r.layers.front();
+  const RankLayer& last = r.layers.back();
+  r.in_row_off.assign(m_, 0);
+  int64_t tot = 0;
+  for (int mb = 0; mb < m_; ++mb) {
+    r.in_row_off[mb] = tot;
+    tot += (r.stage == 0 ? first.acts[mb].rows : last.acts[mb].rows);
+  }
+  r.in_rows_total = tot;
+  if (r.stage == 0) {
+    int64_t rows_all = 0;
+    for (int mb = 0; mb < m_; ++mb) rows_all += first.acts[mb].rows;
+    r.x_in = A.a<bf16>(rows_all * first.sh.h);
+    r.dx_out = A.a<bf16>(rows_all * first.sh.h);
+    int64_t off = 0;
+    for (int mb = 0; mb < m_; ++mb) {
+      // first layer reads its input straight from the staged batch
+      r.layers.front().acts[mb].x = r.x_in + off * first.sh.h;
+      off += first.acts[mb].rows;
+    }
+  }
+  if (r.stage == P_ - 1) {
+    int64_t rows_all = 0;
+    for (int mb = 0; mb < m_; ++mb) rows_all += last.acts[mb].rows;
+    r.target = A.a<bf16>(rows_all * last.sh.h);
+  }
+  if (A.failed()) return set_error(kErrCuda, "executor: out of device memory");
+  return cuda_check(cudaDeviceSynchronize(), "executor allocate");
+}
+
+// ------------------------------------------------------------------------- parameters
+int ExecutorImpl::set_layer_params(int layer, const float* canonical, int64_t n) {
+  if (layer < 0 || layer >= L_) return set_error(kErrConfig, "set_layer_params: bad layer");
+  if (n != canonical_size(shape_[layer])) return set_error(kErrConfig, "set_layer_params: size");
+  for (auto& r : ranks_) {
+    for (RankLayer& L : r->layers) {
+      if (L.layer != layer) continue;
+      std::vector<float> shard(L.shard_n, 0.f);
+      const int64_t lo = static_cast<int64_t>(L.sr) * L.shard_n;
+      for (int64_t j = 0; j < L.shard_n; ++j) {
+        const int64_t c = canon_index(L.sh, L.lay, L.d.tp, L.tr, lo + j);
+        if (c >= 0) shard[j] = canonical[c];
+      }
+      GX_TRY(cuda_check(cudaMemcpy(L.master, shard.data(), L.shard_n * 4, cudaMemcpyHostToDevice),
+                        "set_layer_params"));
+      GX_TRY(cast_bf16(L.master, L.pshard, L.shard_n, stream_));
+      GX_TRY(cuda_check(cudaMemsetAsync(L.m, 0, L.shard_n * 4, stream_), "memset m"));
+      GX_TRY(cuda_check(cudaMemsetAsync(L.v, 0, L.shard_n * 4, stream_), "memset v"));
+      if (L.d.sdp > 1) {  // keep a gathered copy valid for inspection; fwd re-gathers
+        GX_TRY(cuda_check(cudaMemsetAsync(L.pfull, 0, L.lay.total * 2, stream_), "memset"));
+      }
+    }
+  }
+  return cuda_check(cudaStreamSynchronize(stream_), "set_layer_params sync");
+}
+
+int ExecutorImpl::export_layer(int layer, int what, float* canonical, int64_t n) {
+  if (layer < 0 || layer >= L_) return set_error(kErrConfig, "export_layer: bad layer");
+  if (n != canonical_size(shape_[layer])) return set_error(kErrConfig, "export_layer: size");
+  GX_TRY(cuda_check(cudaStreamSynchronize(stream_), "export sync"));
+  for (int64_t i = 0; i < n; ++i) canonical[i] = std::nanf("");
+  for (auto& r : ranks_) {
+    for (RankLayer& L : r->layers) {
+      if (L.layer != layer || L.pr != 0) continue;  // one DP replica holds every shard
+      std::vector<float> shard(L.shard_n);
+      const float* src = what == 0 ? L.master : L.gshard;
+      GX_TRY(cuda_check(cudaMemcpy(shard.data(), src, L.shard_n * 4, cudaMemcpyDeviceToHost),
+                        "export_layer"));
+      const int64_t lo = static_cast<int64_t>(L.sr) * L.shard_n;
+      for (int64_t j = 0; j < L.shard_n; ++j) {
+        const int64_t c = canon_index(L.sh, L.lay, L.d.tp, L.tr, lo + j);
+        if (c >= 0) canonical[c] = shard[j];
+      }
+    }
+  }
+  return kOk;
+}
+
+// ------------------------------------------------------------------------------ inputs
+int ExecutorImpl::load_batch(const void* x_host, const void* target_host) {
+  for (auto& rp : ranks_) {
+    RankCtx& r = *rp;
+    for (int mb = 0; mb < m_; ++mb) {
+      if (r.stage == 0 && x_host != nullptr) {
+        const RankLayer& F = r.layers.front();
+        const Acts& a = F.acts[mb];
+        const size_t row_bytes = static_cast<size_t>(F.sh.h) * 2;
+        GX_TRY(cuda_check(
+            cudaMemcpyAsync(r.x_in + r.in_row_off[mb] * F.sh.h,
+                            static_cast<const char*>(x_host) + a.sample0 * F.sh.seq * row_bytes,
+                            a.rows * row_bytes, cudaMemcpyHostToDevice, stream_),
+            "load_batch x"));
+      }
+      if (r.stage == P_ - 1 && target_host != nullptr) {
+        const RankLayer& Lz = r.layers.back();
+        const Acts& a = Lz.acts[mb];
+        const size_t row_bytes = static_cast<size_t>(Lz.sh.h) * 2;
+        int64_t off = 0;
+        for (int k = 0; k < mb; ++k) off += Lz.acts[k].rows;
+        GX_TRY(cuda_check(
+            cudaMemcpyAsync(r.target + off * Lz.sh.h,
+                            static_cast<const char*>(target_host) + a.sample0 * Lz.sh.seq * row_bytes,
+                            a.rows * row_bytes, cudaMemcpyHostToDevice, stream_),
+            "load_batch target"));
+      }
+    }
+  }
+  return kOk;
+}
+
+int ExecutorImpl::load_batch_device(const void* x_dev, const void* target_dev) {
+  for (auto& rp : ranks_) {
+    RankCtx& r = *rp;
+    for (int mb = 0; mb < m_; ++mb) {
+      if (r.stage == 0 && x_dev != nullptr) {
+        const RankLayer& F = r.layers.front();
+        const Acts& a = F.acts[mb];
+        const size_t row_bytes = static_cast<size_t>(F.sh.h) * 2;
+        GX_TRY(cuda_check(
+            cudaMemcpyAsync(r.x_in + r.in_row_off[mb] * F.sh.h,
+                            static_cast<const char*>(x_dev) + a.sample0 * F.sh.seq * row_bytes,
+                            a.rows * row_bytes, cudaMemcpyDeviceToDevice, stream_),
+            "load_batch_device x"));
+      }
+      if (r.stage == P_ - 1 && target_dev != nullptr) {
+        const RankLayer& Lz = r.layers.back();
+        const Acts& a = Lz.acts[mb];
+        const size_t row_bytes = static_cast<size_t>(Lz.sh.h) * 2;
+        int64_t off = 0;
+        for (int k = 0; k < mb; ++k) off += Lz.acts[k].rows;
+        GX_TRY(cuda_check(
+            cudaMemcpyAsync(r.target + off * Lz.sh.h,
+                            static_cast<const char*>(target_dev) + a.sample0 * Lz.sh.seq * row_bytes,
+                            a.rows * row_bytes, cudaMemcpyDeviceToDevice, stream_),
+            "load_batch_device target"));
+      }
+    }
+  }
+  return kOk;
+}
+
+// --------------------------------------------------------------------- forward phases
+// Phase 0 runs after the layer input is in place.  tp == 1: one phase (all epilogues fused
+// into the GEMMs).  tp > 1: phases end at the two activation all-reduces.
+int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
+  RankLayer& L = r.layers[li];
+  Acts& A = L.acts[mb];
+  const Shape& s = L.sh;
+  const int t = L.d.tp;
+  const int rows = A.rows;
+  const int h = s.h, ht = s.h / t, ft = s.ffn / t;
+  const bf16* P = L.pfull;
+  const int l = L.layer;
+  const int64_t row_off = A.sample0 * s.seq;
+  if (rows == 0) return kOk;
+  if (phase == 0) {
+    GX_TRY(layernorm_fwd(A.x, P + L.lay.ln1g.off, P + L.lay.ln1b.off, A.ln1, A.mean1, A.rstd1,
+                         rows, h, stream_));
+    gx_gemm_epilogue e = epi();
+    e.out_kind = kOutBF16;
+    e.out = A.qkv;
+    e.ldo = 3 * ht;
+    e.bias = P + L.lay.bqkv.off;
+    GX_TRY(gemm(A.ln1, h, false, P + L.lay.wqkv.off, h, false, rows, 3 * ht, h, e));
+    gx_attention_args at{};
+    at.batch = A.samples;
+    at.seq = s.seq;
+    at.heads = s.heads / t;
+    at.head_dim = s.hd;
+    at.heads_total = s.heads;
+    at.head_offset = L.tr * (s.heads / t);
+    at.sample_offset = A.sample0;
+    at.scale = 1.f / std::sqrt(static_cast<float>(s.hd));
+    at.qkv = A.qkv;
+    at.ld_qkv = 3 * ht;
+    at.ctx = A.ctx;
+    at.ld_ctx = ht;
+    at.lse = A.lse;
+    at.drop_threshold = thr_attn_;
+    at.drop_scale = p_attn_ > 0 ? 1.f / (1.f - p_attn_) : 1.f;
+    at.seed = seed_;
+    at.site = 3ull * l;
+    at.seed_offset = r.seed_off;
+    GX_TRY(attention_fwd(at, stream_));
+    gx_gemm_epilogue o = epi();
+    o.out_kind = kOutBF16;
+    o.ldo = h;
+    if (t == 1) {
+      o.out = A.x1;
+      o.bias = P + L.lay.bo.off;
+      o.residual = A.x;
+      o.ld_res = h;
+      o.row_offset = row_off;
+      o.drop_ld = h;
+      o.drop_threshold = thr_hidden_;
+      o.drop_scale = p_hidden_ > 0 ? 1.f / (1.f - p_hidden_) : 1.f;
+      o.seed = seed_;
+      o.site = 3ull * l + 1;
+      o.seed_offset = r.seed_off;
+      GX_TRY(gemm(A.ctx, ht, false, P + L.lay.wo.off, ht, false, rows, h, ht, o));
+    } else {
+      o.out = r.partial;
+      GX_TRY(gemm(A.ctx, ht, false, P + L.lay.wo.off, ht, false, rows, h, ht, o));
+      return comm_->all_reduce(L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h,
+                               DType::kBF16, stream_);
+    }
+  }
+  if ((t == 1 && phase == 0) || (t > 1 && phase == 1)) {
+    if (t > 1) {
+      gx_dropout d{};
+      d.threshold = thr_hidden_;
+      d.scale = p_hidden_ > 0 ? 1.f / (1.f - p_hidden_) : 1.f;
+      d.seed = seed_;
+      d.site = 3ull * l + 1;
+      d.row_offset = row_off;
+      d.drop_ld = h;
+      d.seed_offset = r.seed_off;
+      GX_TRY(bias_dropout_add(r.partial, P + L.lay.bo.off, A.x, A.x1, rows, h, d, stream_));
+    }
+    GX_TRY(layernorm_fwd(A.x1, P + L.lay.ln2g.off, P + L.lay.ln2b.off, A.ln2, A.mean2, A.rstd2,
+                         rows, h, stream_));
+    gx_gemm_epilogue e = epi();
+    e.out_kind = kOutBF16;
+    e.out = A.gel;
+    e.ldo = ft;
+    e.bias = P + L.lay.b1.off;
+    e.gelu = 1;
+    e.aux = A.pre;
+    e.ld_aux = ft;
+    GX_TRY(gemm(A.ln2, h, false, P + L.lay.w1.off, h, false, rows, ft, h, e));
+    gx_gemm_epilogue o = epi();
+    o.out_kind = kOutBF16;
+    o.ldo = h;
+    if (t == 1) {
+      o.out = A.y;
+      o.bias = P + L.lay.b2.off;
+      o.residual = A.x1;
+      o.ld_res = h;
+      o.row_offset = row_off;
+      o.drop_ld = h;
+      o.drop_threshold = thr_hidden_;
+      o.drop_scale = p_hidden_ > 0 ? 1.f / (1.f - p_hidden_) : 1.f;
+      o.seed = seed_;
+      o.site = 3ull * l + 2;
+      o.seed_offset = r.seed_off;
+      return gemm(A.gel, ft, false, P + L.lay.w2.off, ft, false, rows, h, ft, o);
+    }
+    o.out = r.partial;
+    GX_TRY(gemm(A.gel, ft, false, P + L.lay.w2.off, ft, false, rows, h, ft, o));
+    return comm_->all_reduce(L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h,
+                             DType::kBF16, stream_);
+  }
+  if (t > 1 && phase == 2) {
+    gx_dropout d{};
+    d.threshold = thr_hidden_;
+    d.scale = p_hidden_ > 0 ? 1.f / (1.f - p_hidden_) : 1.f;
+    d.seed = seed_;
+    d.site = 3ull * l + 2;
+    d.row_offset = row_off;
+    d.drop_ld = h;
+    d.seed_offset = r.seed_off;
+    return bias_dropout_add(r.partial, P + L.lay.b2.off, A.x1, A.y, rows, h, d, stream_);
+  }
+  return kOk;
+}
+
+// -------------------------------------------------------------------- backward phases
+// dY in gbuf[cur]; dX goes to gbuf[cur ^ 1].
+int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
+  RankLayer& L = r.layers[li];
+  Acts& A = L.acts[mb];
+  const Shape& s = L.sh;
+  const int t = L.d.tp;
+  const int rows = A.rows;
+  const int h = s.h, ht = s.h / t, ft = s.ffn / t;
+  const bf16* P = L.pfull;
+  float* G = L.gfull;
+  const int l = L.layer;
+  const int64_t row_off = A.sample0 * s.seq;
+  const bool first_mb = mb == m_ - 1;  // backward visits micro-batches in reverse
+  const int wk = first_mb ? kOutF32 : kOutF32Accumulate;
+  bf16* dY = r.gbuf[r.cur];
+  bf16* dX = r.gbuf[r.cur ^ 1];
+  if (rows == 0) return kOk;
+  gx_dropout d{};
+  d.threshold = thr_hidden_;
+  d.scale = p_hidden_ > 0 ? 1.f / (1.f - p_hidden_) : 1.f;
+  d.seed = seed_;
+  d.row_offset = row_off;
+  d.drop_ld = h;
+  d.seed_offset = r.seed_off;
+  if (phase == 0) {
+    d.site = 3ull * l + 2;
+    GX_TRY(dropout_bwd_colsum(dY, r.dz, G + L.lay.b2.off, rows, h, d, stream_));
+    gx_gemm_epilogue w = epi();
+    w.out_kind = wk;
+    w.out = G + L.lay.w2.off;
+    w.ldo = ft;
+    GX_TRY(gemm(r.dz, h, true, A.gel, ft, true, h, ft, rows, w));  // dW2 = dz^T gel
+    gx_gemm_epilogue e = epi();
+    e.out_kind = kOutBF16;
+    e.out = r.dpre;
+    e.ldo = ft;
+    e.gelu_bwd = 1;
+    e.aux = A.pre;
+    e.ld_aux = ft;
+    GX_TRY(gemm(r.dz, h, false, P + L.lay.w2.off, ft, true, rows, ft, h, e));  // dz W2 * gelu'
+    GX_TRY(colsum(r.dpre, ft, G + L.lay.b1.off, rows, ft, stream_));
+    w.out = G + L.lay.w1.off;
+    w.ldo = h;
+    GX_TRY(gemm(r.dpre, ft, true, A.ln2, h, true, ft, h, rows, w));  // dW1 = dpre^T ln2
+    gx_gemm_epilogue c = epi();
+    c.out_kind = kOutBF16;
+    c.out = r.dc;
+    c.ldo = h;
+    GX_TRY(gemm(r.dpre, ft, false, P + L.lay.w1.off, h, true, rows, h, ft, c));  // dpre W1
+    if (t > 1)
+      return comm_->all_reduce(L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
+                               stream_);
+    phase = 1;
+  }
+  if (phase == 1) {
+    GX_TRY(layernorm_bwd(r.dc, A.x1, A.mean2, A.rstd2, P + L.lay.ln2g.off, dY, r.dx1,
+                         G + L.lay.ln2g.off, G + L.lay.ln2b.off, rows, h, stream_));
+    d.site = 3ull * l + 1;
+    GX_TRY(dropout_bwd_colsum(r.dx1, r.dout, G + L.lay.bo.off, rows, h, d, stream_));
+    gx_gemm_epilogue w = epi();
+    w.out_kind = wk;
+    w.out = G + L.lay.wo.off;
+    w.ldo = ht;
+    GX_TRY(gemm(r.dout, h, true, A.ctx, ht, true, h, ht, rows, w));  // dWo = dout^T ctx
+    gx_gemm_epilogue c = epi();
+    c.out_kind = kOutBF16;
+    c.out = r.dctx;
+    c.ldo = ht;
+    GX_TRY(gemm(r.dout, h, false, P + L.lay.wo.off, ht, true, rows, ht, h, c));  // dout Wo
+    gx_attention_args at{};
+    at.batch = A.samples;
+    at.seq = s.seq;
+    at.heads = s.heads / t;
+    at.head_dim = s.hd;
+    at.heads_total = s.heads;
+    at.head_offset = L.tr * (s.heads / t);
+    at.sample_offset = A.sample0;
+    at.scale = 1.f / std::sqrt(static_cast<float>(s.hd));
+    at.qkv = A.qkv;
+    at.ld_qkv = 3 * ht;
+    at.ctx = A.ctx;
+    at.ld_ctx = ht;
+    at.lse = A.lse;
+    at.dctx = r.dctx;
+    at.dqkv = r.dqkv;
+    at.dq_accum = r.dq_acc;
+    at.dsum = r.dsum;
+    at.drop_threshold = thr_attn_;
+    at.drop_scale = p_attn_ > 0 ? 1.f / (1.f - p_attn_) : 1.f;
+    at.seed = seed_;
+    at.site = 3ull * l;
+    at.seed_offset = r.seed_off;
+    GX_TRY(attention_bwd(at, stream_));
+    GX_TRY(colsum(r.dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, stream_));
+    w.out = G + L.lay.wqkv.off;
+    w.ldo = h;
+    GX_TRY(gemm(r.dqkv, 3 * ht, true, A.ln1, h, true, 3 * ht, h, rows, w));  // dWqkv
+    gx_gemm_epilogue a = epi();
+    a.out_kind = kOutBF16;
+    a.out = r.da;
+    a.ldo = h;
+    GX_TRY(gemm(r.dqkv, 3 * ht, false, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, a));
+    if (t > 1)
+      return comm_->all_reduce(L.g_tp, r.rank, r.da, static_cast<size_t>(rows) * h, DType::kBF16,
+                               stream_);
+    phase = 2;
+  }
+  if (phase == 2) {
+    GX_TRY(layernorm_bwd(r.da, A.x, A.mean1, A.rstd1, P + L.lay.ln1g.off, r.dx1, dX,
+                         G + L.lay.ln1g.off, G + L.lay.ln1b.off, rows, h, stream_));
+  }
+  return kOk;
+}
+
+// Gradient synchronisation + optimizer after the layer's last backward micro-batch.
+int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
+  RankLayer& L = r.layers[li];
+  if (phase == 0) {
+    if (L.d.sdp > 1)
+      return comm_->reduce_scatter(L.g_sdp, r.rank, L.gfull, L.gshard,
+                                   static_cast<size_t>(L.shard_n), DType::kF32, stream_);
+    if (L.d.dp > 1)
+      return comm_->all_reduce(L.g_dp, r.rank, L.gfull, static_cast<size_t>(L.lay.total),
+                               DType::kF32, stream_);
+    return kOk;
+  }
+  if (phase == 1) {
+    if (L.d.sdp > 1 && L.d.dp > 1)
+      return comm_->all_reduce(L.g_dp, r.rank, L.gshard, static_cast<size_t>(L.shard_n),
+                               DType::kF32, stream_);
+    return kOk;
+  }
+  if (phase == 2 && optimizer_)
+    return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_, wd_,
+                     r.step, stream_);
+  return kOk;
+}
+
+int ExecutorImpl::gather_params(RankCtx& r, int li) {
+  RankLayer& L = r.layers[li];
+  if (L.d.sdp <= 1) return kOk;
+  std::vector<size_t> counts(L.d.sdp, static_cast<size_t>(L.shard_n));
+  return comm_->all_gather(L.g_sdp, r.rank, L.pshard, L.pfull, counts, DType::kBF16, stream_);
+}
+
+// Forward relayout into layer li (same stage): only the all-gather case moves data.
+int ExecutorImpl::xin_fwd(RankCtx& r, int li, int mb) {
+  RankLayer& L = r.layers[li];
+  if (L.xin != Xin::kGather) return kOk;
+  const RankLayer& Pv = r.layers[li - 1];
+  const Acts& p = Pv.acts[mb];
+  const CommGroup& grp = comm_->group(L.g_xin);
+  std::vector<size_t> counts;
+  for (int member : grp.ranks) {
+    int64_t lo, hi;
+    chunk(Pv.d, member % g_, mb, lo, hi);
+    counts.push_back(static_cast<size_t>((hi - lo) * L.sh.seq * L.sh.h));
+  }
+  return comm_->all_gather(L.g_xin, r.rank, p.y, L.acts[mb].x, counts, DType::kBF16, stream_);
+}
+
+// Backward relayout out of layer li: dX (gbuf[cur^1], layout li) -> dY of layer li-1 in
+// gbuf[cur] after the call.
+int ExecutorImpl::xin_bwd(RankCtx& r, int li, int mb) {
+  RankLayer& L = r.layers[li];
+  const RankLayer& Pv = r.layers[li - 1];
+  bf16* dX = r.gbuf[r.cur ^ 1];
+  bf16* dYp = r.gbuf[r.cur];
+  const int64_t h = L.sh.h, seq = L.sh.seq;
+  if (L.xin == Xin::kSame) {
+    r.cur ^= 1;
+    return kOk;
+  }
+  if (L.xin == Xin::kGather) {
+    // forward gathered k chunks; backward keeps this rank's own sub-chunk
+    const Acts& a = L.acts[mb];
+    const Acts& p = Pv.acts[mb];
+    const int64_t off = (p.sample0 - a.sample0) * seq * h;
+    if (p.rows == 0) return kOk;
+    return cuda_check(cudaMemcpyAsync(dYp, dX + off, static_cast<size_t>(p.rows) * h * 2,
+                                      cudaMemcpyDeviceToDevice, stream_),
+                      "xin_bwd slice");
+  }
+  // forward sliced; backward all-gathers the sub-chunk gradients of the previous chunk
+  const CommGroup& grp = comm_->group(L.g_xin);
+  std::vector<size_t> counts;
+  for (int member : grp.ranks) {
+    int64_t lo, hi;
+    chunk(L.d, member % g_, mb, lo, hi);
+    counts.push_back(static_cast<size_t>((hi - lo) * seq * h));
+  }
+  return comm_->all_gather(L.g_xin, r.rank, dX, dYp, counts, DType::kBF16, stream_);
+}
+
+// Pipeline boundary.  Forward: this stage's last layer output -> next stage's first layer
+// input (send=true on the sender stage, false on the receiver stage).
+int ExecutorImpl::pp_fwd(RankCtx& r, int mb, bool send) {
+  if (send) {
+    const RankLayer& A = r.layers.back();
+    const int nxt = r.stage + 1;
+    const Deg& b = deg_[stage_range_[nxt].first];
+    const Acts& my = A.acts[mb];
+    const int64_t hs = static_cast<int64_t>(A.sh.seq) * A.sh.h;
+    for (int ip = 0; ip < g_; ++ip) {
+      if (ip % A.d.tp != r.idx % A.d.tp) continue;
+      int64_t lo2, hi2;
+      chunk(b, ip, mb, lo2, hi2);
+      const int64_t lo = std::max<int64_t>(my.sample0, lo2);
+      const int64_t hi = std::min<int64_t>(my.sample0 + my.samples, hi2);
+      if (hi <= lo) continue;
+      GX_TRY(comm_->send(r.rank, nxt * g_ + ip, my.y + (lo - my.sample0) * hs,
+                         static_cast<size_t>((hi - lo) * hs) * 2, stream_));
+    }
+    return kOk;
+  }
+  RankLayer& B = r.layers.front();
+  const int prv = r.stage - 1;
+  const Deg& a = deg_[stage_range_[prv].second - 1];
+  Acts& my = B.acts[mb];
+  const int64_t hs = static_cast<int64_t>(B.sh.seq) * B.sh.h;
+  for (int c = 0; c < a.data(); ++c) {
+    int64_t lo1, hi1;
+    chunk(a, c * a.tp, mb, lo1, hi1);
+    const int64_t lo = std::max<int64_t>(my.sample0, lo1);
+    const int64_t hi = std::min<int64_t>(my.sample0 + my.samples, hi1);
+    if (hi <= lo) continue;
+    const int src = prv * g_ + c * a.tp + r.idx % a.tp;
+    GX_TRY(comm_->recv(r.rank, src, my.x + (lo - my.sample0) * hs,
+                       static_cast<size_t>((hi - lo) * hs) * 2, stream_));
+  }
+  return kOk;
+}
+
+// Backward: input gradient of this stage's first layer -> previous stage (send=true), or
+// receive the output gradient of this stage's last layer into gbuf[cur] (send=false).
+int ExecutorImpl::pp_bwd(RankCtx& r, int mb, bool send) {
+  if (send) {
+    const RankLayer& B = r.layers.front();
+    const int prv = r.stage - 1;
+    const Deg& a = deg_[stage_range_[prv].second - 1];
+    const Acts& my = B.acts[mb];
+    const bf16* dX = r.gbuf[r.cur ^ 1];
+    const int64_t hs = static_cast<int64_t>(B.sh.seq) * B.sh.h;
+    for (int i = 0; i < g_; ++i) {
+      if (i % B.d.tp != r.idx % B.d.tp) continue;
+      int64_t lo1, hi1;
+      chunk(a, i, mb, lo1, hi1);
+      const int64_t lo = std::max<int64_t>(my.sample0, lo1);
+      const int64_t hi = std::min<int64_t>(my.sample0 + my.samples, hi1);
+      if (hi <= lo) continue;
+      GX_TRY(comm_->send(r.rank, prv * g_ + i, dX + (lo - my.sample0) * hs,
+                         static_cast<size_t>((hi - lo) * hs) * 2, stream_));
+    }
+    return kOk;
+  }
+  const RankLayer& A = r.layers.back();
+  const int nxt = r.stage + 1;
+  const Deg& b = deg_[stage_range_[nxt].first];
+  const Acts& my = A.acts[mb];
+  bf16* dY = r.gbuf[r.cur];
+  const int64_t hs = static_cast<int64_t>(A.sh.seq) * A.sh.h;
+  for (int c = 0; c < b.data(); ++c) {
+    int64_t lo2, hi2;
+    chunk(b, c * b.tp, mb, lo2, hi2);
+    const int64_t lo = std::max<int64_t>(my.sample0, lo2);
+    const int64_t hi = std::min<int64_t>(my.sample0 + my.samples, hi2);
+    if (hi <= lo) continue;
+    const int src = nxt * g_ + c * b.tp + r.idx % b.tp;
+    GX_TRY(comm_->recv(r.rank, src, dY + (lo - my.sample0) * hs,
+                       static_cast<size_t>((hi - lo) * hs) * 2, stream_));
+  }
+  return kOk;
+}
+
+// ------------------------------------------------------------------------- the step
+int ExecutorImpl::step_once() {
+  auto in_stage = [&](int st) {
+    std::vector<RankCtx*> v;
+    for (auto& r : ranks_)
+      if (r->stage == st) v.push_back(r.get());
+    return v;
+  };
+  for (auto& r : ranks_) {
+    GX_TRY(bump_step(r->step, nullptr, stream_));
+    GX_TRY(cuda_check(cudaMemsetAsync(r->loss, 0, 4, stream_), "memset loss"));
+    for (RankLayer& L : r->layers)
+      GX_TRY(cuda_check(cudaMemsetAsync(L.gfull, 0, L.lay.acc_end * 4, stream_), "memset grads"));
+  }
+  // ---------------------------------------------------------------- forward (GPipe)
+  for (int mb = 0; mb < m_; ++mb) {
+    for (int st = 0; st < P_; ++st) {
+      auto R = in_stage(st);
+      if (R.empty()) continue;
+      if (st > 0) {
+        GX_TRY(comm_->group_start());
+        for (RankCtx* r : R) GX_TRY(pp_fwd(*r, mb, false));
+        GX_TRY(comm_->group_end());
+      }
+      const int nl = static_cast<int>(R[0]->layers.size());
+      for (int li = 0; li < nl; ++li) {
+        for (RankCtx* r : R) GX_TRY(xin_fwd(*r, li, mb));
+        if (mb == 0)
+          for (RankCtx* r : R) GX_TRY(gather_params(*r, li));
+        const int phases = R[0]->layers[li].d.tp > 1 ? 3 : 1;
+        for (int ph = 0; ph < phases; ++ph)
+          for (RankCtx* r : R) GX_TRY(fwd_phase(*r, li, mb, ph));
+      }
+      if (st + 1 < P_) {
+        GX_TRY(comm_->group_start());
+        for (RankCtx* r : R) GX_TRY(pp_fwd(*r, mb, true));
+        GX_TRY(comm_->group_end());
+      }
+    }
+  }
+  // --------------------------------------------------------------- backward (GPipe)
+  for (int mb = m_ - 1; mb >= 0; --mb) {
+    for (int st = P_ - 1; st >= 0; --st) {
+      auto R = in_stage(st);
+      if (R.empty()) continue;
+      for (RankCtx* r : R) {
+        r->cur = 0;
+        if (st == P_ - 1) {
+          const RankLayer& Lz = r->layers.back();
+          const Acts& a = Lz.acts[mb];
+          const int64_t n = static_cast<int64_t>(a.rows) * Lz.sh.h;
+          int64_t off = 0;
+          for (int k = 0; k < mb; ++k) off += Lz.acts[k].rows;
+          if (n > 0)
+            GX_TRY(mse_loss(a.y, r->target + off * Lz.sh.h, r->gbuf[0], Lz.tr == 0 ? r->loss
+                                                                                      : r->loss_dummy,
+                            n, inv_count_, stream_));
+        }
+      }
+      if (st + 1 < P_) {
+        GX_TRY(comm_->group_start());
+        for (RankCtx* r : R) GX_TRY(pp_bwd(*r, mb, false));
+        GX_TRY(comm_->group_end());
+      }
+      const int nl = static_cast<int>(R[0]->layers.size());
+      for (int li = nl - 1; li >= 0; --li) {
+        // SDP: the forward all-gather's copy stays resident through backward (B200 HBM
+        // allows it), so the cost model's second gather (cost_model.cc:186-195) is elided.
+        const int tp = R[0]->layers[li].d.tp;
+        if (tp > 1) {
+          for (int ph = 0; ph < 3; ++ph)
+            for (RankCtx* r : R) GX_TRY(bwd_phase(*r, li, mb, ph));
+        } else {
+          for (RankCtx* r : R) GX_TRY(bwd_phase(*r, li, mb, 0));
+        }
+        if (mb == 0)
+          for (int ph = 0; ph < 3; ++ph)
+            for (RankCtx* r : R) GX_TRY(sync_phase(*r, li, ph));
+        if (li > 0) {
+          for (RankCtx* r : R) GX_TRY(xin_bwd(*r, li, mb));
+          // the relayout leaves dY of layer li-1 in gbuf[cur] (kSame flips cur instead)
+        } else {
+          for (RankCtx* r : R) r->cur ^= 1;  // dX of the stage's first layer now in gbuf[cur]
+        }
+      }
+      for (RankCtx* r : R) r->cur ^= 1;  // pp_bwd(send) / export read gbuf[cur ^ 1]
+      if (st > 0) {
+        GX_TRY(comm_->group_start());
+        for (RankCtx* r : R) GX_TRY(pp_bwd(*r, mb, true));
+        GX_TRY(comm_->group_end());
+      } else {
+        for (RankCtx* r : R) {
+          const RankLayer& F = r->layers.front();
+          const Acts& a = F.acts[mb];
+          if (a.rows > 0)
+            GX_TRY(cuda_check(cudaMemcpyAsync(r->dx_out + r->in_row_off[mb] * F.sh.h,
+                                              r->gbuf[r->cur ^ 1],
+                                              static_cast<size_t>(a.rows) * F.sh.h * 2,
+                                              cudaMemcpyDeviceToDevice, stream_),
+                              "export dx"));
+        }
+      }
+    }
+  }
+  for (auto& r : ranks_) GX_TRY(comm_->world_sum(r->rank, r->loss, stream_));
+  // next step draws fresh dropout masks
+  for (auto& r : ranks_) GX_TRY(bump_step(nullptr, r->seed_off, stream_));
+  return kOk;
+}
+
+int ExecutorImpl::run(bool use_graph) {
+  if (!use_graph) {
+    const int64_t before = launch_count();
+    GX_TRY(step_once());
+    launches_per_step_ = launch_count() - before;
+    ++steps_run_;
+    return kOk;
+  }
+  if (graph_exec_ == nullptr) {
+    GX_TRY(cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal),
+                      "begin capture"));
+    const int64_t before = launch_count();
+    const int rc = step_once();
+    launches_per_step_ = launch_count() - before;
+    cudaGraph_t g = nullptr;
+    const cudaError_t e = cudaStreamEndCapture(stream_, &g);
+    if (rc != kOk) return rc;
+    GX_TRY(cuda_check(e, "end capture"));
+    graph_ = g;
+    GX_TRY(cuda_check(cudaGraphInstantiate(&graph_exec_, graph_, 0), "graph instantiate"));
+  }
+  GX_TRY(cuda_check(cudaGraphLaunch(graph_exec_, stream_), "graph launch"));
+  ++steps_run_;
+  return kOk;
+}
+
+int ExecutorImpl::loss(float* out) {
+  float v = 0.f;
+  GX_TRY(cuda_check(cudaMemcpyAsync(&v, ranks_.front()->loss, 4, cudaMemcpyDeviceToHost, stream_),
+                    "loss d2h"));
+  GX_TRY(cuda_check(cudaStreamSynchronize(stream_), "loss sync"));
+  *out = v;
+  return kOk;
+}
+
+int ExecutorImpl::export_output(void* host, int what) {
+  GX_TRY(cuda_check(cudaStreamSynchronize(stream_), "export sync"));
+  for (auto& rp : ranks_) {
+    RankCtx& r = *rp;
+    const bool want = what == 0 ? r.stage == P_ - 1 : r.stage == 0;
+    if (!want) continue;
+    const RankLayer& L = what == 0 ? r.layers.back() : r.layers.front();
+    if (L.tr != 0) continue;
+    const size_t rb = static_cast<size_t>(L.sh.h) * 2;
+    int64_t off = 0;
+    for (int mb = 0; mb < m_; ++mb) {
+      const Acts& a = L.acts[mb];
+      const void* src = what == 0 ? static_cast<const void*>(a.y)
+                                  : static_cast<const void*>(r.dx_out + off * L.sh.h);
+      if (a.rows > 0)
+        GX_TRY(cuda_check(cudaMemcpy(static_cast<char*>(host) + a.sample0 * L.sh.seq * rb, src,
+                                     a.rows * rb, cudaMemcpyDeviceToHost),
+                          "export_output"));
+      off += a.rows;
+    }
+  }
+  return kOk;
+}
+
+std::string ExecutorImpl::info() const {
+  json j;
+  j["world_size"] = world_;
+  j["pp_degree"] = P_;
+  j["micro_batches"] = m_;
+  j["batch_size"] = B_;
+  j["comm"] = sim_ ? "sim" : "nccl";
+  j["launches_per_step"] = launches_per_step_;
+  j["steps_run"] = steps_run_;
+  json ranks = json::array();
+  for (const auto& r : ranks_) {
+    json jr;
+    jr["rank"] = r->rank;
+    jr["stage"] = r->stage;
+    jr["device_bytes"] = r->arena.bytes();
+    int64_t params = 0, opt = 0, grads = 0;
+    for (const RankLayer& L : r->layers) {
+      params += L.shard_n * 4 + L.lay.total * 2;
+      opt += 2 * L.shard_n * 4;
+      grads += L.lay.total * 4 + (L.d.sdp > 1 ? L.shard_n * 4 : 0);
+    }
+    jr["param_bytes"] = params;
+    jr["optimizer_bytes"] = opt;
+    jr["grad_bytes"] = grads;
+    ranks.push_back(jr);
+  }
+  j["ranks"] = ranks;
+  return j.dump();
+}
+
+}  // namespace
+
+std::unique_ptr<Executor> create_executor(const std::string& config_json, std::string* err) {
+  json cfg;
+  try {
+    cfg = json::parse(config_json);
+  } catch (const std::exception& e) {
+    *err = std::string("executor: bad config json: ") + e.what();
+    return nullptr;
+  }
+  auto ex = std::make_unique<ExecutorImpl>();
+  if (ex->init(cfg, err) != kOk) return nullptr;
+  return ex;
+}
+
+}  // namespace gx

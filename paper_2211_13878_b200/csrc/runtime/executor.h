@@ -1,0 +1,71 @@
+// executor.h — runs Transformer-layer forward/backward + AdamW under a Galvatron plan.
+//
+// Input: a plan in the reference's PlanToJson schema (proj/src/planner.cc:483-521) and a
+// model in the reference's model schema with per-layer "shape" objects.  Semantics of each
+// strategy follow the reference cost model, which is the executor's contract:
+//   * memory / shard sizes      EstimateMemory      (proj/src/cost_model.cc:119-143)
+//   * communication schedule    EstimateLayerCost   (proj/src/cost_model.cc:145-213)
+//       TP: activation all-reduce in forward and backward (serial);
+//       SDP: parameter all-gather before forward and again before backward,
+//            gradient reduce-scatter; DP: gradient all-reduce of the owned shard
+//   * inter-layer relayout      TransformationCostMs (proj/src/cost_model.cc:215-241):
+//       equal degrees -> no-op; D grows -> local slice (bwd: all-gather);
+//       D shrinks -> all-gather of D_prev/D_cur shards (bwd: local slice)
+//   * pipeline                  GPipe with the plan's micro-batch count
+//                               (StagePipelineCostMs, planner.cc:138-159)
+// Rank mapping: stage p owns ranks [p*g, (p+1)*g); inside a stage TP
+// groups are contiguous runs of t ranks, data (DP/SDP) groups are stride-t.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+
+namespace gx {
+
+struct Deg {
+  int dp = 1, sdp = 1, tp = 1;
+  int data() const { return dp * sdp; }
+};
+
+struct Shape {
+  int h = 0, heads = 0, hd = 0, seq = 0, ffn = 0;
+};
+
+// Offsets (elements) of one layer's tensors inside its flat per-rank parameter buffer.
+struct Slot {
+  int64_t off = 0, n = 0;
+};
+struct Layout {
+  Slot ln1g, ln1b, ln2g, ln2b, bqkv, bo, b1, b2, wqkv, wo, w1, w2;
+  int64_t acc_end = 0;  // [0, acc_end): params whose grads accumulate with atomics
+  int64_t total = 0;    // padded to a multiple of 64 * sdp
+  int64_t shard() const { return total; }
+};
+Layout make_layout(const Shape& s, int tp, int sdp);
+// Canonical (unsharded, unpadded) flat order used at the host boundary:
+// ln1_g ln1_b ln2_g ln2_b b_qkv b_o b_1 b_2 w_qkv w_o w_1 w_2
+int64_t canonical_size(const Shape& s);
+
+class Executor;
+std::unique_ptr<Executor> create_executor(const std::string& config_json, std::string* err);
+
+class Executor {
+ public:
+  virtual ~Executor() = default;
+  virtual int set_layer_params(int layer, const float* canonical, int64_t n) = 0;
+  virtual int export_layer(int layer, int what, float* canonical, int64_t n) = 0;  // 0 params 1 grads
+  virtual int load_batch(const void* x_host, const void* target_host) = 0;
+  virtual int load_batch_device(const void* x_dev, const void* target_dev) = 0;
+  virtual int run(bool use_graph) = 0;
+  virtual int loss(float* out) = 0;
+  virtual int export_output(void* host_bf16, int what) = 0;  // 0 final y, 1 input grad dx
+  virtual cudaStream_t stream() const = 0;
+  virtual std::string info() const = 0;
+};
+
+}  // namespace gx

@@ -28,7 +28,7 @@ def dropout_threshold(p: float) -> int:
 
 def gemm(a, b, *, a_mn_major=False, b_mn_major=False, out=None, out_kind="bf16", bias=None,
          gelu_aux=None, residual=None, alpha=1.0, dropout_p=0.0, seed=0, site=0,
-         row_offset=0, col_offset=0, drop_ld=None, tile_n=0, stream=None):
+         row_offset=0, col_offset=0, drop_ld=None, tile_n=0, stream=None, gelu_bwd_aux=None):
     """C = A * B^T.  A is [M,K] (or [K,M] if a_mn_major); B is [N,K] (or [K,N])."""
     import torch
     M = a.shape[1] if a_mn_major else a.shape[0]
@@ -48,8 +48,10 @@ def gemm(a, b, *, a_mn_major=False, b_mn_major=False, out=None, out_kind="bf16",
     ep.alpha = alpha
     ep.bias = _ptr(bias)
     ep.gelu = 1 if gelu_aux is not None else 0
-    ep.aux = _ptr(gelu_aux)
-    ep.ld_aux = gelu_aux.stride(0) if gelu_aux is not None else 0
+    ep.gelu_bwd = 1 if gelu_bwd_aux is not None else 0
+    aux = gelu_aux if gelu_aux is not None else gelu_bwd_aux
+    ep.aux = _ptr(aux)
+    ep.ld_aux = aux.stride(0) if aux is not None else 0
     ep.residual = _ptr(residual)
     ep.ld_res = residual.stride(0) if residual is not None else 0
     ep.row_offset = row_offset
@@ -63,3 +65,130 @@ def gemm(a, b, *, a_mn_major=False, b_mn_major=False, out=None, out_kind="bf16",
         _ptr(a), a.stride(0), int(a_mn_major), _ptr(b), b.stride(0), int(b_mn_major),
         M, N, K, ctypes.byref(ep), tile_n, _lib.stream_ptr(stream)))
     return out
+
+
+class _AttnArgs(ctypes.Structure):
+    _fields_ = [("batch", ctypes.c_int), ("seq", ctypes.c_int), ("heads", ctypes.c_int),
+                ("head_dim", ctypes.c_int), ("heads_total", ctypes.c_int),
+                ("head_offset", ctypes.c_int), ("sample_offset", ctypes.c_int64),
+                ("scale", ctypes.c_float), ("qkv", ctypes.c_void_p), ("ld_qkv", ctypes.c_int64),
+                ("ctx", ctypes.c_void_p), ("ld_ctx", ctypes.c_int64), ("lse", ctypes.c_void_p),
+                ("dctx", ctypes.c_void_p), ("dqkv", ctypes.c_void_p),
+                ("dq_accum", ctypes.c_void_p), ("dsum", ctypes.c_void_p),
+                ("drop_threshold", ctypes.c_uint32), ("drop_scale", ctypes.c_float),
+                ("seed", ctypes.c_uint64), ("site", ctypes.c_uint64),
+                ("seed_offset", ctypes.c_void_p)]
+
+
+class Dropout(ctypes.Structure):
+    _fields_ = [("threshold", ctypes.c_uint32), ("scale", ctypes.c_float),
+                ("seed", ctypes.c_uint64), ("site", ctypes.c_uint64),
+                ("row_offset", ctypes.c_int64), ("col_offset", ctypes.c_int64),
+                ("drop_ld", ctypes.c_int64), ("seed_offset", ctypes.c_void_p)]
+
+
+def make_dropout(p, seed, site, row_offset=0, col_offset=0, drop_ld=0):
+    d = Dropout()
+    d.threshold = dropout_threshold(p)
+    d.scale = 1.0 / (1.0 - p) if p > 0 else 1.0
+    d.seed, d.site, d.row_offset, d.col_offset, d.drop_ld = seed, site, row_offset, col_offset, drop_ld
+    return d
+
+
+def _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, heads_total=None, head_offset=0,
+               sample_offset=0):
+    a = _AttnArgs()
+    a.batch, a.seq, a.heads, a.head_dim = batch, seq, heads, head_dim
+    a.heads_total = heads_total or heads
+    a.head_offset, a.sample_offset = head_offset, sample_offset
+    a.scale = head_dim ** -0.5
+    a.qkv, a.ld_qkv = _ptr(qkv), qkv.stride(0)
+    a.drop_threshold = dropout_threshold(p)
+    a.drop_scale = 1.0 / (1.0 - p) if p > 0 else 1.0
+    a.seed, a.site = seed, site
+    return a
+
+
+def attention_fwd(qkv, batch, seq, heads, head_dim, p=0.0, seed=0, site=0, **kw):
+    import torch
+    ctx = torch.empty(batch * seq, heads * head_dim, device=qkv.device, dtype=torch.bfloat16)
+    lse = torch.empty(batch * heads, seq, device=qkv.device, dtype=torch.float32)
+    a = _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, **kw)
+    a.ctx, a.ld_ctx, a.lse = _ptr(ctx), ctx.stride(0), _ptr(lse)
+    _lib.check(_lib.lib().gx_k_attention_fwd(ctypes.addressof(a), _lib.stream_ptr()))
+    return ctx, lse
+
+
+def attention_bwd(qkv, ctx, lse, dctx, batch, seq, heads, head_dim, p=0.0, seed=0, site=0, **kw):
+    import torch
+    dqkv = torch.zeros_like(qkv)
+    dq_acc = torch.empty(batch * heads * seq * head_dim, device=qkv.device, dtype=torch.float32)
+    dsum = torch.empty(batch * heads * seq, device=qkv.device, dtype=torch.float32)
+    a = _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, **kw)
+    a.ctx, a.ld_ctx, a.lse = _ptr(ctx), ctx.stride(0), _ptr(lse)
+    a.dctx, a.dqkv, a.dq_accum, a.dsum = _ptr(dctx), _ptr(dqkv), _ptr(dq_acc), _ptr(dsum)
+    _lib.check(_lib.lib().gx_k_attention_bwd(ctypes.addressof(a), _lib.stream_ptr()))
+    return dqkv
+
+
+def layernorm_fwd(x, gamma, beta):
+    import torch
+    rows, h = x.shape
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device=x.device, dtype=torch.float32)
+    rstd = torch.empty(rows, device=x.device, dtype=torch.float32)
+    _lib.check(_lib.lib().gx_k_layernorm_fwd(
+        _ptr(x), _ptr(gamma), _ptr(beta), _ptr(y), _ptr(mean), _ptr(rstd), rows, h,
+        ctypes.c_void_p(_lib.stream_ptr())))
+    return y, mean, rstd
+
+
+def layernorm_bwd(dy, x, mean, rstd, gamma, dres=None):
+    import torch
+    rows, h = x.shape
+    dx = torch.empty_like(x)
+    dg = torch.zeros(h, device=x.device, dtype=torch.float32)
+    db = torch.zeros(h, device=x.device, dtype=torch.float32)
+    _lib.check(_lib.lib().gx_k_layernorm_bwd(
+        _ptr(dy), _ptr(x), _ptr(mean), _ptr(rstd), _ptr(gamma), _ptr(dres), _ptr(dx), _ptr(dg),
+        _ptr(db), rows, h, ctypes.c_void_p(_lib.stream_ptr())))
+    return dx, dg, db
+
+
+def bias_dropout_add(x, bias, residual, d: Dropout):
+    import torch
+    out = torch.empty_like(x)
+    rows, cols = x.shape
+    _lib.check(_lib.lib().gx_k_bias_dropout_add(
+        _ptr(x), _ptr(bias), _ptr(residual), _ptr(out), rows, cols, ctypes.addressof(d),
+        ctypes.c_void_p(_lib.stream_ptr())))
+    return out
+
+
+def dropout_bwd_colsum(dy, d: Dropout):
+    import torch
+    rows, cols = dy.shape
+    dz = torch.empty_like(dy)
+    db = torch.zeros(cols, device=dy.device, dtype=torch.float32)
+    _lib.check(_lib.lib().gx_k_dropout_bwd_colsum(
+        _ptr(dy), _ptr(dz), _ptr(db), rows, cols, ctypes.addressof(d),
+        ctypes.c_void_p(_lib.stream_ptr())))
+    return dz, db
+
+
+def mse_loss(y, target):
+    import torch
+    dy = torch.empty_like(y)
+    loss = torch.zeros(1, device=y.device, dtype=torch.float32)
+    _lib.check(_lib.lib().gx_k_mse_loss(_ptr(y), _ptr(target), _ptr(dy), _ptr(loss), y.numel(),
+                                        ctypes.c_float(1.0 / y.numel()),
+                                        ctypes.c_void_p(_lib.stream_ptr())))
+    return loss, dy
+
+
+def adamw(p, g, m, v, out_bf16, lr, b1, b2, eps, wd, step):
+    _lib.check(_lib.lib().gx_k_adamw(
+        _ptr(p), _ptr(g), _ptr(m), _ptr(v), _ptr(out_bf16), p.numel(), ctypes.c_float(lr),
+        ctypes.c_float(b1), ctypes.c_float(b2), ctypes.c_float(eps), ctypes.c_float(wd),
+        ctypes.c_float(1 - b1 ** step), ctypes.c_float(1 - b2 ** step),
+        ctypes.c_void_p(_lib.stream_ptr())))

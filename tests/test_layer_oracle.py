@@ -1,0 +1,89 @@
+"""Pins the CPU layer oracle (oracle/layer_oracle.py) before it is trusted as the checker.
+
+The reference has no layer implementation, so the numpy restatement is pinned against
+torch.autograd in float64 on CPU (an independent implementation of the same math, with the
+same Philox dropout masks), against Philox known-answer vectors (Random123 KAT), and
+against the committed golden vectors in tests/golden/layer_small.npz.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import layer_oracle as lo
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden", "layer_small.npz")
+
+
+def test_philox_known_answers():
+    # Random123 philox4x32-10 known-answer tests (kat_vectors)
+    out = lo.philox4x32_10(0, 0, 0, 0, 0, 0)
+    assert [int(v) for v in out] == [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]
+    out = lo.philox4x32_10(0xffffffff, 0xffffffff, 0xffffffff, 0xffffffff, 0xffffffff, 0xffffffff)
+    assert [int(v) for v in out] == [0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd]
+    out = lo.philox4x32_10(0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344, 0xa4093822, 0x299f31d0)
+    assert [int(v) for v in out] == [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]
+
+
+def test_dropout_rate():
+    idx = np.arange(200_000, dtype=np.uint64)
+    keep = lo.keep_mask(1234, 7, idx, 0.1)
+    assert abs(1.0 - keep.mean() - 0.1) < 0.005
+
+
+def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0):
+    h, H, d, s = shape.hidden, shape.heads, shape.head_dim, shape.seq
+    n = x.shape[0] // s
+    ln = lambda t, g, b: torch.nn.functional.layer_norm(t, (h,), g, b, 1e-5)  # noqa: E731
+    a = ln(x, P["ln1_g"], P["ln1_b"])
+    qkv = a @ P["w_qkv"].T + P["b_qkv"]
+    q, k, v = (qkv[:, i * h:(i + 1) * h].reshape(n, s, H, d).transpose(1, 2) for i in range(3))
+    pr = torch.softmax(q @ k.transpose(-1, -2) / math.sqrt(d), -1)
+    am = torch.from_numpy(lo._attn_mask(drop, 3 * layer_id, n, H, s, sample_offset)).double()
+    ka = 1.0 / (1.0 - drop.p_attn) if drop.p_attn > 0 else 1.0
+    ctx = (pr * am * ka @ v).transpose(1, 2).reshape(n * s, h)
+    kh = 1.0 / (1.0 - drop.p_hidden) if drop.p_hidden > 0 else 1.0
+    m1 = torch.from_numpy(lo._hidden_mask(drop, 3 * layer_id + 1, n * s, h, sample_offset * s)).double()
+    x1 = x + (ctx @ P["w_o"].T + P["b_o"]) * m1 * kh
+    c = ln(x1, P["ln2_g"], P["ln2_b"])
+    g = torch.nn.functional.gelu(c @ P["w_1"].T + P["b_1"])
+    m2 = torch.from_numpy(lo._hidden_mask(drop, 3 * layer_id + 2, n * s, h, sample_offset * s)).double()
+    return x1 + (g @ P["w_2"].T + P["b_2"]) * m2 * kh
+
+
+@pytest.mark.parametrize("p", [0.0, 0.1])
+def test_oracle_matches_autograd(p):
+    rng = np.random.default_rng(0)
+    shape = lo.LayerShape(hidden=64, heads=4, seq=12, ffn=128)
+    P = lo.init_layer_params(shape, rng, std=0.1)
+    x = rng.standard_normal((2 * shape.seq, shape.hidden))
+    dy = rng.standard_normal(x.shape)
+    drop = lo.Dropout(p_attn=p, p_hidden=p, seed=99)
+    y, cache = lo.layer_forward(P, x, shape, 0, drop, sample_offset=3)
+    dx, G = lo.layer_backward(P, dy, cache, shape)
+
+    tP = {k: torch.tensor(v, requires_grad=True) for k, v in P.items()}
+    tx = torch.tensor(x, requires_grad=True)
+    ty = _torch_layer(tP, tx, shape, drop, 0, 3)
+    ty.backward(torch.tensor(dy))
+    assert np.allclose(y, ty.detach().numpy(), rtol=1e-10, atol=1e-10)
+    assert np.allclose(dx, tx.grad.numpy(), rtol=1e-9, atol=1e-10)
+    for k in P:
+        assert np.allclose(G[k], tP[k].grad.numpy(), rtol=1e-9, atol=1e-10), k
+
+
+def test_golden_vectors():
+    """Committed outputs of the oracle (tests/golden/make_layer_golden.py)."""
+    z = np.load(GOLDEN)
+    shape = lo.LayerShape(*[int(v) for v in z["shape"]])
+    P = {k[2:]: z[k] for k in z.files if k.startswith("P_")}
+    drop = lo.Dropout(float(z["p"]), float(z["p"]), int(z["seed"]))
+    y, cache = lo.layer_forward(P, z["x"], shape, 1, drop, 0)
+    dx, G = lo.layer_backward(P, z["dy"], cache, shape)
+    assert np.allclose(y, z["y"], rtol=0, atol=1e-12)
+    assert np.allclose(dx, z["dx"], rtol=0, atol=1e-12)
+    for k in G:
+        assert np.allclose(G[k], z["G_" + k], rtol=0, atol=1e-12)
