@@ -252,6 +252,7 @@ class ExecutorImpl final : public Executor {
   uint64_t seed_ = 1234;
   float lr_ = 1e-4f, b1_ = 0.9f, b2_ = 0.999f, eps_ = 1e-8f, wd_ = 0.f;
   bool optimizer_ = true;
+  bool forward_only_ = false;  // profiler / debugging: skip loss, backward and optimizer
   float inv_count_ = 1.f;
 
   std::unique_ptr<Comm> comm_;
@@ -284,6 +285,7 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     eps_ = cfg.value("eps", 1e-8f);
     wd_ = cfg.value("weight_decay", 0.0f);
     optimizer_ = cfg.value("optimizer", true);
+    forward_only_ = cfg.value("forward_only", false);
     thr_attn_ = threshold_of(p_attn_);
     thr_hidden_ = threshold_of(p_hidden_);
 
@@ -593,8 +595,12 @@ int ExecutorImpl::set_layer_params(int layer, const float* canonical, int64_t n)
         const int64_t c = canon_index(L.sh, L.lay, L.d.tp, L.tr, lo + j);
         if (c >= 0) shard[j] = canonical[c];
       }
-      GX_TRY(cuda_check(cudaMemcpy(L.master, shard.data(), L.shard_n * 4, cudaMemcpyHostToDevice),
+      // Same stream as the cast below: a pageable cudaMemcpy may return before its DMA
+      // lands, and stream_ does not synchronise with the legacy default stream.
+      GX_TRY(cuda_check(cudaMemcpyAsync(L.master, shard.data(), L.shard_n * 4,
+                                        cudaMemcpyHostToDevice, stream_),
                         "set_layer_params"));
+      GX_TRY(cuda_check(cudaStreamSynchronize(stream_), "set_layer_params h2d"));
       GX_TRY(cast_bf16(L.master, L.pshard, L.shard_n, stream_));
       GX_TRY(cuda_check(cudaMemsetAsync(L.m, 0, L.shard_n * 4, stream_), "memset m"));
       GX_TRY(cuda_check(cudaMemsetAsync(L.v, 0, L.shard_n * 4, stream_), "memset v"));
@@ -615,9 +621,19 @@ int ExecutorImpl::export_layer(int layer, int what, float* canonical, int64_t n)
     for (RankLayer& L : r->layers) {
       if (L.layer != layer || L.pr != 0) continue;  // one DP replica holds every shard
       std::vector<float> shard(L.shard_n);
-      const float* src = what == 0 ? L.master : L.gshard;
-      GX_TRY(cuda_check(cudaMemcpy(shard.data(), src, L.shard_n * 4, cudaMemcpyDeviceToHost),
-                        "export_layer"));
+      if (what == 2) {  // bf16 compute copy of this rank's shard
+        std::vector<uint16_t> b(L.shard_n);
+        GX_TRY(cuda_check(cudaMemcpy(b.data(), L.pshard, L.shard_n * 2, cudaMemcpyDeviceToHost),
+                          "export_layer"));
+        for (int64_t j = 0; j < L.shard_n; ++j) {
+          const uint32_t u = static_cast<uint32_t>(b[j]) << 16;
+          std::memcpy(&shard[j], &u, 4);
+        }
+      } else {
+        const float* src = what == 0 ? L.master : L.gshard;
+        GX_TRY(cuda_check(cudaMemcpy(shard.data(), src, L.shard_n * 4, cudaMemcpyDeviceToHost),
+                          "export_layer"));
+      }
       const int64_t lo = static_cast<int64_t>(L.sr) * L.shard_n;
       for (int64_t j = 0; j < L.shard_n; ++j) {
         const int64_t c = canon_index(L.sh, L.lay, L.d.tp, L.tr, lo + j);
@@ -1132,7 +1148,7 @@ int ExecutorImpl::step_once() {
     }
   }
   // --------------------------------------------------------------- backward (GPipe)
-  for (int mb = m_ - 1; mb >= 0; --mb) {
+  for (int mb = m_ - 1; mb >= 0 && !forward_only_; --mb) {
     for (int st = P_ - 1; st >= 0; --st) {
       auto R = in_stage(st);
       if (R.empty()) continue;
@@ -1237,18 +1253,41 @@ int ExecutorImpl::loss(float* out) {
 }
 
 int ExecutorImpl::export_output(void* host, int what) {
+  // what: 0 = model output, 1 = model input gradient, 2 + l = output of layer l,
+  // 1000 + 16*l + k = activation k of layer l (debug: 0 x 1 ln1 2 x1 3 ln2 4 gel 5 y), [rows][h|ffn]
   GX_TRY(cuda_check(cudaStreamSynchronize(stream_), "export sync"));
+  if (what >= 1000) {
+    const int l = (what - 1000) / 16, k = (what - 1000) % 16;
+    for (auto& rp : ranks_) {
+      for (const RankLayer& L : rp->layers) {
+        if (L.layer != l || L.tr != 0) continue;
+        const int64_t w = k == 4 ? L.sh.ffn / L.d.tp : L.sh.h;
+        for (int mb = 0; mb < m_; ++mb) {
+          const Acts& a = L.acts[mb];
+          const bf16* src = k == 0 ? a.x : k == 1 ? a.ln1 : k == 2 ? a.x1 : k == 3 ? a.ln2 : k == 4 ? a.gel : a.y;
+          if (a.rows > 0)
+            GX_TRY(cuda_check(cudaMemcpy(static_cast<char*>(host) + a.sample0 * L.sh.seq * w * 2, src,
+                                         a.rows * w * 2, cudaMemcpyDeviceToHost), "export act"));
+        }
+      }
+    }
+    return kOk;
+  }
   for (auto& rp : ranks_) {
     RankCtx& r = *rp;
-    const bool want = what == 0 ? r.stage == P_ - 1 : r.stage == 0;
-    if (!want) continue;
-    const RankLayer& L = what == 0 ? r.layers.back() : r.layers.front();
-    if (L.tr != 0) continue;
+    const RankLayer* Lp = nullptr;
+    if (what == 0 && r.stage == P_ - 1) Lp = &r.layers.back();
+    if (what == 1 && r.stage == 0) Lp = &r.layers.front();
+    if (what >= 2)
+      for (const RankLayer& L : r.layers)
+        if (L.layer == what - 2) Lp = &L;
+    if (Lp == nullptr || Lp->tr != 0) continue;
+    const RankLayer& L = *Lp;
     const size_t rb = static_cast<size_t>(L.sh.h) * 2;
     int64_t off = 0;
     for (int mb = 0; mb < m_; ++mb) {
       const Acts& a = L.acts[mb];
-      const void* src = what == 0 ? static_cast<const void*>(a.y)
+      const void* src = what != 1 ? static_cast<const void*>(a.y)
                                   : static_cast<const void*>(r.dx_out + off * L.sh.h);
       if (a.rows > 0)
         GX_TRY(cuda_check(cudaMemcpy(static_cast<char*>(host) + a.sample0 * L.sh.seq * rb, src,

@@ -61,11 +61,12 @@ class PlanExecutor:
     def __init__(self, plan: dict, model: dict, world_size: int, local_ranks=None,
                  comm: str = "sim", nccl_id_hex: str = "", dropout_attn=0.0, dropout_hidden=0.0,
                  seed=1234, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0,
-                 optimizer=True):
+                 optimizer=True, forward_only=False):
         cfg = {"plan": plan, "model": model, "world_size": world_size, "comm": comm,
                "dropout_attn": dropout_attn, "dropout_hidden": dropout_hidden, "seed": seed,
                "lr": lr, "beta1": beta1, "beta2": beta2, "eps": eps,
-               "weight_decay": weight_decay, "optimizer": optimizer}
+               "weight_decay": weight_decay, "optimizer": optimizer,
+               "forward_only": forward_only}
         if local_ranks is not None:
             cfg["local_ranks"] = list(local_ranks)
         if comm == "nccl":
@@ -101,7 +102,8 @@ class PlanExecutor:
         n = self._canon_n(layer)
         out = np.empty(n, dtype=np.float32)
         _lib.check(_lib.lib().gx_exec_export_layer(
-            self._h, layer, 0 if what == "params" else 1, out.ctypes.data_as(ctypes.c_void_p), n))
+            self._h, layer, {"params": 0, "grads": 1, "bf16": 2}[what],
+            out.ctypes.data_as(ctypes.c_void_p), n))
         s = self.shapes[layer]
         return unpack_canonical(out, s["hidden"], s["ffn"])
 
@@ -134,11 +136,13 @@ class PlanExecutor:
                                            int(use_graph), ctypes.byref(v)))
         return v.value
 
-    def export_output(self, what: str = "y") -> np.ndarray:
-        s = self.shapes[-1] if what == "y" else self.shapes[0]
+    def export_output(self, what="y") -> np.ndarray:
+        """"y" = model output, "dx" = input gradient, int l = output of layer l."""
+        s = self.shapes[-1] if what == "y" else (self.shapes[0] if what == "dx" else self.shapes[what])
+        code = 0 if what == "y" else (1 if what == "dx" else 2 + int(what))
         rows = self.plan["batch_size"] * s["seq"]
         out = np.zeros((rows, s["hidden"]), dtype=np.uint16)
-        _lib.check(_lib.lib().gx_exec_export_output(self._h, 0 if what == "y" else 1,
+        _lib.check(_lib.lib().gx_exec_export_output(self._h, code,
                                                     out.ctypes.data_as(ctypes.c_void_p)))
         return bf16_bits_to_f32(out)
 

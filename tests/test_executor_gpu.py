@@ -25,7 +25,7 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
 
 
-def _small_model(L=4, h=128, heads=2, seq=64, ffn=512):
+def _small_model(L=4, h=256, heads=4, seq=64, ffn=512):
     shape = {"hidden": h, "heads": heads, "head_dim": h // heads, "seq": seq, "ffn": ffn,
              "kind": "encoder"}
     return {"dtype_bytes": 4, "layers": [
