@@ -129,8 +129,16 @@ GX_API int gx_exec_set_layer_params(gx_exec* ex, int layer, const float* canonic
 GX_API int gx_exec_export_layer(gx_exec* ex, int layer, int what, float* canonical, int64_t n);
 GX_API int gx_exec_load_batch(gx_exec* ex, const void* x_host, const void* target_host);
 GX_API int gx_exec_load_batch_device(gx_exec* ex, const void* x_dev, const void* target_dev);
-/* One training step (fwd + loss + bwd + grad sync + AdamW) on the loaded batch. */
-GX_API int gx_exec_run(gx_exec* ex, int use_graph);
+/* One training step (fwd + loss + bwd + grad sync + AdamW) on the loaded batch.
+ * flags bit 0: replay as a CUDA graph (captured on first use); bit 1: instrumented run that
+ * brackets every launch with CUDA events (read back with gx_exec_profile_report). */
+GX_API int gx_exec_run(gx_exec* ex, int flags);
+/* Per-category device time / launches / algorithmic flops+bytes of the last instrumented
+ * run, plus per-GEMM-launch (ms, flops) pairs: the per-strategy profiler's raw data. */
+GX_API int gx_exec_profile_report(gx_exec* ex, char* out, size_t cap, size_t* needed);
+/* Deterministic synthetic parameters on the device (value depends only on seed, layer and
+ * canonical index, never on the sharding): LN gains 1, biases 0, weights N(0, std^2). */
+GX_API int gx_exec_init_params(gx_exec* ex, uint64_t seed, float std_dev);
 GX_API int gx_exec_loss(gx_exec* ex, float* out);
 /* load_batch + run + loss: the end-to-end call (host buffers in, loss out). */
 GX_API int gx_exec_step(gx_exec* ex, const void* x_host, const void* target_host, int use_graph,

@@ -106,7 +106,10 @@ def _ln_bwd(dy, cache, g):
     return dx, (dy * xh).sum(0), dy.sum(0)
 
 
-_erf = np.vectorize(math.erf)
+try:  # vectorised erf when scipy is present (CPU-baseline speed); identical math otherwise
+    from scipy.special import erf as _erf
+except ImportError:  # pragma: no cover
+    _erf = np.vectorize(math.erf)
 
 
 def _gelu(x):

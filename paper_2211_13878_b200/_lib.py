@@ -99,6 +99,10 @@ def _declare(L: ctypes.CDLL) -> None:
                  "gx_nccl_unique_id"):
         getattr(L, name).restype = c_int
     L.gx_launch_count.restype = c_int64
+    L.gx_exec_profile_report.argtypes = [vp, c_char_p, c_size_t, POINTER(c_size_t)]
+    L.gx_exec_profile_report.restype = c_int
+    L.gx_exec_init_params.argtypes = [vp, c_uint64, c_float]
+    L.gx_exec_init_params.restype = c_int
     declare_plan_api(L, "gx_plan_")
 
 

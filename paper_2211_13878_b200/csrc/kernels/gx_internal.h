@@ -64,6 +64,15 @@ struct PtrPack {
   int n;
 };
 int sum_ptrs(const PtrPack& srcs, void* out, int64_t n, bool bf16, cudaStream_t st);
+// Flat per-rank parameter layout (slot order ln1g ln1b ln2g ln2b bqkv bo b1 b2 wqkv wo w1 w2).
+struct InitLayout {
+  int64_t off[12], n[12];
+  int64_t h, f;
+  int t, tr;
+  int64_t lo;  // first flat element of the shard
+};
+int init_params(float* master, int64_t n, const InitLayout& L, uint64_t seed, uint64_t layer,
+                float std_dev, cudaStream_t st);
 int num_sms();
 
 }  // namespace gx

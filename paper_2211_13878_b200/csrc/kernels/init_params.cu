@@ -1,0 +1,74 @@
+// init_params.cu — deterministic synthetic initialisation of a rank's parameter shard on
+// the device (no host traffic for multi-GB models).  Every value is a function of
+// (seed, layer, canonical index) only, so any TP/SDP sharding of the same model holds
+// bit-identical parameters: LayerNorm gains 1, biases and LayerNorm shifts 0, weights
+// N(0, std^2) by Box-Muller over the Philox stream.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "gx_internal.h"
+#include "philox.cuh"
+
+namespace gx {
+
+__device__ int64_t canon_of(const InitLayout& L, int64_t j) {
+  const int64_t h = L.h, f = L.f, ht = h / L.t, ft = f / L.t, tr = L.tr;
+  const int64_t c_ln1g = 0, c_ln1b = h, c_ln2g = 2 * h, c_ln2b = 3 * h, c_bqkv = 4 * h,
+                c_bo = 7 * h, c_b1 = 8 * h, c_b2 = 8 * h + f, c_wqkv = 9 * h + f,
+                c_wo = c_wqkv + 3 * h * h, c_w1 = c_wo + h * h, c_w2 = c_w1 + f * h;
+  int s = -1;
+  for (int i = 0; i < 12; ++i)
+    if (j >= L.off[i] && j < L.off[i] + L.n[i]) s = i;
+  if (s < 0) return -1;
+  const int64_t k = j - L.off[s];
+  switch (s) {
+    case 0: return c_ln1g + k;
+    case 1: return c_ln1b + k;
+    case 2: return c_ln2g + k;
+    case 3: return c_ln2b + k;
+    case 4: return c_bqkv + (k / ht) * h + tr * ht + k % ht;
+    case 5: return c_bo + k;
+    case 6: return c_b1 + tr * ft + k;
+    case 7: return c_b2 + k;
+    case 8: return c_wqkv + ((k / h) / ht * h + tr * ht + (k / h) % ht) * h + k % h;
+    case 9: return c_wo + (k / ht) * h + tr * ht + k % ht;
+    case 10: return c_w1 + (tr * ft + k / h) * h + k % h;
+    default: return c_w2 + (k / ft) * f + tr * ft + k % ft;
+  }
+}
+
+__global__ void init_params_kernel(float* __restrict__ master, int64_t n, InitLayout L,
+                                   uint64_t seed, uint64_t layer, float std_dev) {
+  const int64_t h = L.h, f = L.f;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t c = canon_of(L, L.lo + i);
+    float v = 0.f;
+    if (c >= 0) {
+      if (c < h || (c >= 2 * h && c < 3 * h)) {
+        v = 1.f;  // LayerNorm gains
+      } else if (c >= 9 * h + f) {
+        const Philox4 w = philox4x32_10(static_cast<uint32_t>(c), static_cast<uint32_t>(c >> 32),
+                                        static_cast<uint32_t>(layer), 0x5eedu,
+                                        static_cast<uint32_t>(seed),
+                                        static_cast<uint32_t>(seed >> 32));
+        const float u1 = (static_cast<float>(w.x) + 1.f) * 2.3283064e-10f;
+        const float u2 = static_cast<float>(w.y) * 2.3283064e-10f;
+        v = std_dev * sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+      }
+    }
+    master[i] = v;
+  }
+}
+
+int init_params(float* master, int64_t n, const InitLayout& L, uint64_t seed, uint64_t layer,
+                float std_dev, cudaStream_t st) {
+  if (n <= 0) return kOk;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > num_sms() * 16) blocks = num_sms() * 16;
+  init_params_kernel<<<static_cast<int>(blocks), 256, 0, st>>>(master, n, L, seed, layer, std_dev);
+  return check_launch("init_params_kernel");
+}
+
+}  // namespace gx

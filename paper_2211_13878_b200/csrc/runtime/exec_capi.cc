@@ -57,9 +57,24 @@ int gx_exec_load_batch_device(gx_exec* ex, const void* x, const void* t) {
   return ex->impl->load_batch_device(x, t);
 }
 
-int gx_exec_run(gx_exec* ex, int use_graph) {
+int gx_exec_run(gx_exec* ex, int flags) {
   if (ex == nullptr) return bad("exec: NULL handle");
-  return ex->impl->run(use_graph != 0);
+  return ex->impl->run2((flags & 1) != 0, (flags & 2) != 0);
+}
+
+int gx_exec_profile_report(gx_exec* ex, char* out, size_t cap, size_t* needed) {
+  if (ex == nullptr) return bad("exec: NULL handle");
+  const std::string s = ex->impl->profile_report();
+  if (needed != nullptr) *needed = s.size() + 1;
+  if (out == nullptr || cap == 0) return gx::kOk;
+  if (cap < s.size() + 1) return bad("profile_report: buffer too small");
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return gx::kOk;
+}
+
+int gx_exec_init_params(gx_exec* ex, uint64_t seed, float std_dev) {
+  if (ex == nullptr) return bad("exec: NULL handle");
+  return ex->impl->init_params(seed, std_dev);
 }
 
 int gx_exec_loss(gx_exec* ex, float* out) {

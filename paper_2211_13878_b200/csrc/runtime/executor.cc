@@ -189,7 +189,8 @@ class ExecutorImpl final : public Executor {
   int export_layer(int layer, int what, float* canonical, int64_t n) override;
   int load_batch(const void* x_host, const void* target_host) override;
   int load_batch_device(const void* x_dev, const void* target_dev) override;
-  int run(bool use_graph) override;
+  int run(bool use_graph) override { return run2(use_graph, false); }
+  int run2(bool use_graph, bool profile) override;
   int loss(float* out) override;
   int export_output(void* host_bf16, int what) override;
   cudaStream_t stream() const override { return stream_; }
@@ -197,6 +198,9 @@ class ExecutorImpl final : public Executor {
   ~ExecutorImpl() override {
     if (graph_exec_ != nullptr) cudaGraphExecDestroy(graph_exec_);
     if (graph_ != nullptr) cudaGraphDestroy(graph_);
+    if (pgraph_exec_ != nullptr) cudaGraphExecDestroy(pgraph_exec_);
+    if (pgraph_ != nullptr) cudaGraphDestroy(pgraph_);
+    for (cudaEvent_t e : events_) cudaEventDestroy(e);
     ranks_.clear();
     comm_.reset();
     if (stream_ != nullptr) cudaStreamDestroy(stream_);
@@ -230,10 +234,69 @@ class ExecutorImpl final : public Executor {
   int pp_fwd(RankCtx& r, int mb, bool send);
   int pp_bwd(RankCtx& r, int mb, bool send);
 
+  // ------------------------------------------------------------ kernel profiler
+  // Categories of launched work; every launch site goes through timed(), which (when
+  // profiling) brackets it with CUDA events on the executor stream.  Inside graph capture
+  // the events become external event-record nodes, so a replay of the instrumented graph
+  // yields per-launch device durations of exactly the kernels the plain graph runs.
+  enum Cat { kGemm, kAttnFwd, kAttnBwd, kNorm, kElementwise, kOptim, kComm, kNumCats };
+  struct Rec {
+    int cat;
+    double flops, bytes;
+    cudaEvent_t a, b;
+  };
+  template <class F>
+  int timed(int cat, double flops, double bytes, F&& f) {
+    if (!profiling_) return f();
+    cudaEvent_t a = next_event(), b = next_event();
+    record_event(a);
+    const int rc = f();
+    record_event(b);
+    recs_.push_back(Rec{cat, flops, bytes, a, b});
+    return rc;
+  }
+  cudaEvent_t next_event() {
+    if (ev_used_ == events_.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      events_.push_back(e);
+    }
+    return events_[ev_used_++];
+  }
+  void record_event(cudaEvent_t e) {
+    if (capturing_)
+      cudaEventRecordWithFlags(e, stream_, cudaEventRecordExternal);
+    else
+      cudaEventRecord(e, stream_);
+  }
+  int c_all_reduce(int g, int rank, void* buf, size_t n, DType t, cudaStream_t st) {
+    return timed(kComm, 0, 2.0 * n * dtype_bytes(t),
+                 [&] { return comm_->all_reduce(g, rank, buf, n, t, st); });
+  }
+  int c_reduce_scatter(int g, int rank, const void* a, void* b, size_t n, DType t, cudaStream_t st) {
+    return timed(kComm, 0, 1.0 * n * dtype_bytes(t) * comm_->group(g).ranks.size(),
+                 [&] { return comm_->reduce_scatter(g, rank, a, b, n, t, st); });
+  }
+  int c_all_gather(int g, int rank, const void* a, void* b, const std::vector<size_t>& c, DType t,
+                   cudaStream_t st) {
+    size_t n = 0;
+    for (size_t x : c) n += x;
+    return timed(kComm, 0, 1.0 * n * dtype_bytes(t),
+                 [&] { return comm_->all_gather(g, rank, a, b, c, t, st); });
+  }
   int gemm(const void* a, int64_t lda, bool amn, const void* b, int64_t ldb, bool bmn, int M, int N,
            int K, const gx_gemm_epilogue& ep) {
-    return gemm_bf16(GemmOperand{a, lda, amn}, GemmOperand{b, ldb, bmn}, M, N, K, ep, stream_);
+    const double flops = 2.0 * M * N * K;
+    const double bytes = 2.0 * (static_cast<double>(M) * K + static_cast<double>(N) * K) +
+                         (ep.out_kind == kOutBF16 ? 2.0 : 4.0) * M * N;
+    return timed(kGemm, flops, bytes, [&] {
+      return gemm_bf16(GemmOperand{a, lda, amn}, GemmOperand{b, ldb, bmn}, M, N, K, ep, stream_);
+    });
   }
+ public:
+  std::string profile_report() const override;
+  int init_params(uint64_t seed, float std_dev) override;
+ private:
   gx_gemm_epilogue epi() const {
     gx_gemm_epilogue e{};
     e.alpha = 1.f;
@@ -260,6 +323,13 @@ class ExecutorImpl final : public Executor {
   cudaStream_t stream_ = nullptr;
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
+  cudaGraph_t pgraph_ = nullptr;  // instrumented (profiling) variant
+  cudaGraphExec_t pgraph_exec_ = nullptr;
+  bool profiling_ = false, capturing_ = false;
+  std::vector<cudaEvent_t> events_;
+  size_t ev_used_ = 0;
+  std::vector<Rec> recs_, prof_recs_;
+  double last_profile_ms_ = 0;
   int64_t steps_run_ = 0;
   int64_t launches_per_step_ = 0;
 };
@@ -644,6 +714,32 @@ int ExecutorImpl::export_layer(int layer, int what, float* canonical, int64_t n)
   return kOk;
 }
 
+int ExecutorImpl::init_params(uint64_t seed, float std_dev) {
+  for (auto& r : ranks_) {
+    for (RankLayer& L : r->layers) {
+      InitLayout il{};
+      const Slot* slots[12] = {&L.lay.ln1g, &L.lay.ln1b, &L.lay.ln2g, &L.lay.ln2b, &L.lay.bqkv,
+                               &L.lay.bo,   &L.lay.b1,   &L.lay.b2,   &L.lay.wqkv, &L.lay.wo,
+                               &L.lay.w1,   &L.lay.w2};
+      for (int i = 0; i < 12; ++i) {
+        il.off[i] = slots[i]->off;
+        il.n[i] = slots[i]->n;
+      }
+      il.h = L.sh.h;
+      il.f = L.sh.ffn;
+      il.t = L.d.tp;
+      il.tr = L.tr;
+      il.lo = static_cast<int64_t>(L.sr) * L.shard_n;
+      GX_TRY(gx::init_params(L.master, L.shard_n, il, seed, static_cast<uint64_t>(L.layer), std_dev,
+                             stream_));
+      GX_TRY(cast_bf16(L.master, L.pshard, L.shard_n, stream_));
+      GX_TRY(cuda_check(cudaMemsetAsync(L.m, 0, L.shard_n * 4, stream_), "memset m"));
+      GX_TRY(cuda_check(cudaMemsetAsync(L.v, 0, L.shard_n * 4, stream_), "memset v"));
+    }
+  }
+  return cuda_check(cudaStreamSynchronize(stream_), "init_params");
+}
+
 // ------------------------------------------------------------------------------ inputs
 int ExecutorImpl::load_batch(const void* x_host, const void* target_host) {
   for (auto& rp : ranks_) {
@@ -722,8 +818,8 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
   const int64_t row_off = A.sample0 * s.seq;
   if (rows == 0) return kOk;
   if (phase == 0) {
-    GX_TRY(layernorm_fwd(A.x, P + L.lay.ln1g.off, P + L.lay.ln1b.off, A.ln1, A.mean1, A.rstd1,
-                         rows, h, stream_));
+    GX_TRY(timed(kNorm, 0, 4.0 * rows * h, [&] { return layernorm_fwd(A.x, P + L.lay.ln1g.off, P + L.lay.ln1b.off, A.ln1, A.mean1, A.rstd1,
+                         rows, h, stream_); }));
     gx_gemm_epilogue e = epi();
     e.out_kind = kOutBF16;
     e.out = A.qkv;
@@ -749,7 +845,10 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     at.seed = seed_;
     at.site = 3ull * l;
     at.seed_offset = r.seed_off;
-    GX_TRY(attention_fwd(at, stream_));
+    {
+      const double af = 4.0 * A.samples * (s.heads / t) * double(s.seq) * s.seq * s.hd;
+      GX_TRY(timed(kAttnFwd, af, 2.0 * rows * 4 * ht, [&] { return attention_fwd(at, stream_); }));
+    }
     gx_gemm_epilogue o = epi();
     o.out_kind = kOutBF16;
     o.ldo = h;
@@ -769,7 +868,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     } else {
       o.out = r.partial;
       GX_TRY(gemm(A.ctx, ht, false, P + L.lay.wo.off, ht, false, rows, h, ht, o));
-      return comm_->all_reduce(L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h,
+      return c_all_reduce(L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h,
                                DType::kBF16, stream_);
     }
   }
@@ -783,10 +882,10 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
       d.row_offset = row_off;
       d.drop_ld = h;
       d.seed_offset = r.seed_off;
-      GX_TRY(bias_dropout_add(r.partial, P + L.lay.bo.off, A.x, A.x1, rows, h, d, stream_));
+      GX_TRY(timed(kElementwise, 0, 6.0 * rows * h, [&] { return bias_dropout_add(r.partial, P + L.lay.bo.off, A.x, A.x1, rows, h, d, stream_); }));
     }
-    GX_TRY(layernorm_fwd(A.x1, P + L.lay.ln2g.off, P + L.lay.ln2b.off, A.ln2, A.mean2, A.rstd2,
-                         rows, h, stream_));
+    GX_TRY(timed(kNorm, 0, 4.0 * rows * h, [&] { return layernorm_fwd(A.x1, P + L.lay.ln2g.off, P + L.lay.ln2b.off, A.ln2, A.mean2, A.rstd2,
+                         rows, h, stream_); }));
     gx_gemm_epilogue e = epi();
     e.out_kind = kOutBF16;
     e.out = A.gel;
@@ -815,7 +914,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     }
     o.out = r.partial;
     GX_TRY(gemm(A.gel, ft, false, P + L.lay.w2.off, ft, false, rows, h, ft, o));
-    return comm_->all_reduce(L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h,
+    return c_all_reduce(L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h,
                              DType::kBF16, stream_);
   }
   if (t > 1 && phase == 2) {
@@ -827,7 +926,9 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     d.row_offset = row_off;
     d.drop_ld = h;
     d.seed_offset = r.seed_off;
-    return bias_dropout_add(r.partial, P + L.lay.b2.off, A.x1, A.y, rows, h, d, stream_);
+    return timed(kElementwise, 0, 6.0 * rows * h, [&] {
+      return bias_dropout_add(r.partial, P + L.lay.b2.off, A.x1, A.y, rows, h, d, stream_);
+    });
   }
   return kOk;
 }
@@ -859,7 +960,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
   d.seed_offset = r.seed_off;
   if (phase == 0) {
     d.site = 3ull * l + 2;
-    GX_TRY(dropout_bwd_colsum(dY, r.dz, G + L.lay.b2.off, rows, h, d, stream_));
+    GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(dY, r.dz, G + L.lay.b2.off, rows, h, d, stream_); }));
     gx_gemm_epilogue w = epi();
     w.out_kind = wk;
     w.out = G + L.lay.w2.off;
@@ -873,7 +974,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     e.aux = A.pre;
     e.ld_aux = ft;
     GX_TRY(gemm(r.dz, h, false, P + L.lay.w2.off, ft, true, rows, ft, h, e));  // dz W2 * gelu'
-    GX_TRY(colsum(r.dpre, ft, G + L.lay.b1.off, rows, ft, stream_));
+    GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(r.dpre, ft, G + L.lay.b1.off, rows, ft, stream_); }));
     w.out = G + L.lay.w1.off;
     w.ldo = h;
     GX_TRY(gemm(r.dpre, ft, true, A.ln2, h, true, ft, h, rows, w));  // dW1 = dpre^T ln2
@@ -883,15 +984,15 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     c.ldo = h;
     GX_TRY(gemm(r.dpre, ft, false, P + L.lay.w1.off, h, true, rows, h, ft, c));  // dpre W1
     if (t > 1)
-      return comm_->all_reduce(L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
+      return c_all_reduce(L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
                                stream_);
     phase = 1;
   }
   if (phase == 1) {
-    GX_TRY(layernorm_bwd(r.dc, A.x1, A.mean2, A.rstd2, P + L.lay.ln2g.off, dY, r.dx1,
-                         G + L.lay.ln2g.off, G + L.lay.ln2b.off, rows, h, stream_));
+    GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd(r.dc, A.x1, A.mean2, A.rstd2, P + L.lay.ln2g.off, dY, r.dx1,
+                         G + L.lay.ln2g.off, G + L.lay.ln2b.off, rows, h, stream_); }));
     d.site = 3ull * l + 1;
-    GX_TRY(dropout_bwd_colsum(r.dx1, r.dout, G + L.lay.bo.off, rows, h, d, stream_));
+    GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(r.dx1, r.dout, G + L.lay.bo.off, rows, h, d, stream_); }));
     gx_gemm_epilogue w = epi();
     w.out_kind = wk;
     w.out = G + L.lay.wo.off;
@@ -925,8 +1026,11 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     at.seed = seed_;
     at.site = 3ull * l;
     at.seed_offset = r.seed_off;
-    GX_TRY(attention_bwd(at, stream_));
-    GX_TRY(colsum(r.dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, stream_));
+    {
+      const double af = 10.0 * A.samples * (s.heads / t) * double(s.seq) * s.seq * s.hd;
+      GX_TRY(timed(kAttnBwd, af, 2.0 * rows * 8 * ht, [&] { return attention_bwd(at, stream_); }));
+    }
+    GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(r.dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, stream_); }));
     w.out = G + L.lay.wqkv.off;
     w.ldo = h;
     GX_TRY(gemm(r.dqkv, 3 * ht, true, A.ln1, h, true, 3 * ht, h, rows, w));  // dWqkv
@@ -936,13 +1040,13 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     a.ldo = h;
     GX_TRY(gemm(r.dqkv, 3 * ht, false, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, a));
     if (t > 1)
-      return comm_->all_reduce(L.g_tp, r.rank, r.da, static_cast<size_t>(rows) * h, DType::kBF16,
+      return c_all_reduce(L.g_tp, r.rank, r.da, static_cast<size_t>(rows) * h, DType::kBF16,
                                stream_);
     phase = 2;
   }
   if (phase == 2) {
-    GX_TRY(layernorm_bwd(r.da, A.x, A.mean1, A.rstd1, P + L.lay.ln1g.off, r.dx1, dX,
-                         G + L.lay.ln1g.off, G + L.lay.ln1b.off, rows, h, stream_));
+    GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd(r.da, A.x, A.mean1, A.rstd1, P + L.lay.ln1g.off, r.dx1, dX,
+                         G + L.lay.ln1g.off, G + L.lay.ln1b.off, rows, h, stream_); }));
   }
   return kOk;
 }
@@ -952,22 +1056,24 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
   RankLayer& L = r.layers[li];
   if (phase == 0) {
     if (L.d.sdp > 1)
-      return comm_->reduce_scatter(L.g_sdp, r.rank, L.gfull, L.gshard,
+      return c_reduce_scatter(L.g_sdp, r.rank, L.gfull, L.gshard,
                                    static_cast<size_t>(L.shard_n), DType::kF32, stream_);
     if (L.d.dp > 1)
-      return comm_->all_reduce(L.g_dp, r.rank, L.gfull, static_cast<size_t>(L.lay.total),
+      return c_all_reduce(L.g_dp, r.rank, L.gfull, static_cast<size_t>(L.lay.total),
                                DType::kF32, stream_);
     return kOk;
   }
   if (phase == 1) {
     if (L.d.sdp > 1 && L.d.dp > 1)
-      return comm_->all_reduce(L.g_dp, r.rank, L.gshard, static_cast<size_t>(L.shard_n),
+      return c_all_reduce(L.g_dp, r.rank, L.gshard, static_cast<size_t>(L.shard_n),
                                DType::kF32, stream_);
     return kOk;
   }
   if (phase == 2 && optimizer_)
-    return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_, wd_,
-                     r.step, stream_);
+    return timed(kOptim, 0, 30.0 * L.shard_n, [&] {
+      return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_, wd_,
+                       r.step, stream_);
+    });
   return kOk;
 }
 
@@ -975,7 +1081,7 @@ int ExecutorImpl::gather_params(RankCtx& r, int li) {
   RankLayer& L = r.layers[li];
   if (L.d.sdp <= 1) return kOk;
   std::vector<size_t> counts(L.d.sdp, static_cast<size_t>(L.shard_n));
-  return comm_->all_gather(L.g_sdp, r.rank, L.pshard, L.pfull, counts, DType::kBF16, stream_);
+  return c_all_gather(L.g_sdp, r.rank, L.pshard, L.pfull, counts, DType::kBF16, stream_);
 }
 
 // Forward relayout into layer li (same stage): only the all-gather case moves data.
@@ -991,7 +1097,7 @@ int ExecutorImpl::xin_fwd(RankCtx& r, int li, int mb) {
     chunk(Pv.d, member % g_, mb, lo, hi);
     counts.push_back(static_cast<size_t>((hi - lo) * L.sh.seq * L.sh.h));
   }
-  return comm_->all_gather(L.g_xin, r.rank, p.y, L.acts[mb].x, counts, DType::kBF16, stream_);
+  return c_all_gather(L.g_xin, r.rank, p.y, L.acts[mb].x, counts, DType::kBF16, stream_);
 }
 
 // Backward relayout out of layer li: dX (gbuf[cur^1], layout li) -> dY of layer li-1 in
@@ -1024,7 +1130,7 @@ int ExecutorImpl::xin_bwd(RankCtx& r, int li, int mb) {
     chunk(L.d, member % g_, mb, lo, hi);
     counts.push_back(static_cast<size_t>((hi - lo) * seq * h));
   }
-  return comm_->all_gather(L.g_xin, r.rank, dX, dYp, counts, DType::kBF16, stream_);
+  return c_all_gather(L.g_xin, r.rank, dX, dYp, counts, DType::kBF16, stream_);
 }
 
 // Pipeline boundary.  Forward: this stage's last layer output -> next stage's first layer
@@ -1217,30 +1323,76 @@ int ExecutorImpl::step_once() {
   return kOk;
 }
 
-int ExecutorImpl::run(bool use_graph) {
+int ExecutorImpl::run2(bool use_graph, bool profile) {
+  profiling_ = profile;
+  ev_used_ = 0;
+  recs_.clear();
   if (!use_graph) {
     const int64_t before = launch_count();
-    GX_TRY(step_once());
+    const int rc = step_once();
+    profiling_ = false;
+    GX_TRY(rc);
     launches_per_step_ = launch_count() - before;
     ++steps_run_;
     return kOk;
   }
-  if (graph_exec_ == nullptr) {
+  cudaGraphExec_t& exec = profile ? pgraph_exec_ : graph_exec_;
+  cudaGraph_t& graph = profile ? pgraph_ : graph_;
+  if (exec == nullptr) {
     GX_TRY(cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal),
                       "begin capture"));
+    capturing_ = true;
     const int64_t before = launch_count();
     const int rc = step_once();
-    launches_per_step_ = launch_count() - before;
+    if (!profile) launches_per_step_ = launch_count() - before;
     cudaGraph_t g = nullptr;
     const cudaError_t e = cudaStreamEndCapture(stream_, &g);
-    if (rc != kOk) return rc;
+    capturing_ = false;
+    if (rc != kOk) {
+      profiling_ = false;
+      return rc;
+    }
     GX_TRY(cuda_check(e, "end capture"));
-    graph_ = g;
-    GX_TRY(cuda_check(cudaGraphInstantiate(&graph_exec_, graph_, 0), "graph instantiate"));
+    graph = g;
+    GX_TRY(cuda_check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate"));
+    if (profile) prof_recs_ = recs_;
   }
-  GX_TRY(cuda_check(cudaGraphLaunch(graph_exec_, stream_), "graph launch"));
+  profiling_ = false;
+  GX_TRY(cuda_check(cudaGraphLaunch(exec, stream_), "graph launch"));
+  if (profile) recs_ = prof_recs_;
   ++steps_run_;
   return kOk;
+}
+
+std::string ExecutorImpl::profile_report() const {
+  static const char* kNames[kNumCats] = {"gemm", "attention_fwd", "attention_bwd", "layernorm",
+                                         "elementwise", "optimizer", "comm"};
+  cudaStreamSynchronize(stream_);
+  double ms[kNumCats] = {}, fl[kNumCats] = {}, by[kNumCats] = {};
+  int64_t n[kNumCats] = {};
+  json launches = json::array();
+  for (const Rec& r : recs_) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) continue;
+    ms[r.cat] += t;
+    fl[r.cat] += r.flops;
+    by[r.cat] += r.bytes;
+    n[r.cat] += 1;
+    if (r.cat == kGemm) launches.push_back({t, r.flops});
+  }
+  json j;
+  double total = 0;
+  for (int c = 0; c < kNumCats; ++c) {
+    j["categories"][kNames[c]] = {{"ms", ms[c]}, {"launches", n[c]}, {"flops", fl[c]},
+                                  {"bytes", by[c]}};
+    total += ms[c];
+  }
+  float span = 0.f;
+  if (!recs_.empty()) cudaEventElapsedTime(&span, recs_.front().a, recs_.back().b);
+  j["sum_ms"] = total;
+  j["span_ms"] = span;
+  j["gemm_launches"] = launches;
+  return j.dump();
 }
 
 int ExecutorImpl::loss(float* out) {

@@ -66,6 +66,10 @@ class Executor {
   virtual int export_output(void* host_bf16, int what) = 0;  // 0 final y, 1 input grad dx
   virtual cudaStream_t stream() const = 0;
   virtual std::string info() const = 0;
+  // bit 0: CUDA graph, bit 1: instrumented (per-launch events) variant
+  virtual int run2(bool use_graph, bool profile) = 0;
+  virtual std::string profile_report() const = 0;
+  virtual int init_params(uint64_t seed, float std_dev) = 0;
 };
 
 }  // namespace gx

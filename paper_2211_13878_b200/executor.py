@@ -122,8 +122,18 @@ class PlanExecutor:
             self._h, x_dev.data_ptr() if x_dev is not None else None,
             target_dev.data_ptr() if target_dev is not None else None))
 
-    def run(self, use_graph=False):
-        _lib.check(_lib.lib().gx_exec_run(self._h, int(use_graph)))
+    def run(self, use_graph=False, profile=False):
+        _lib.check(_lib.lib().gx_exec_run(self._h, int(use_graph) | (2 if profile else 0)))
+
+    def profile_report(self) -> dict:
+        need = ctypes.c_size_t()
+        _lib.check(_lib.lib().gx_exec_profile_report(self._h, None, 0, ctypes.byref(need)))
+        buf = ctypes.create_string_buffer(need.value)
+        _lib.check(_lib.lib().gx_exec_profile_report(self._h, buf, need.value, ctypes.byref(need)))
+        return json.loads(buf.value.decode())
+
+    def init_params(self, seed=1, std=0.02):
+        _lib.check(_lib.lib().gx_exec_init_params(self._h, seed, std))
 
     def loss(self) -> float:
         v = ctypes.c_float()
