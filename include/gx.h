@@ -148,6 +148,10 @@ GX_API int gx_exec_export_output(gx_exec* ex, int what, void* host_bf16);
 GX_API int gx_exec_stream(gx_exec* ex, void** stream_out);
 GX_API int gx_exec_info(gx_exec* ex, char* out, size_t cap, size_t* needed);
 GX_API int gx_exec_canonical_size(int hidden, int ffn, int64_t* out);
+/* Host-only view of the executor for config_json with "comm": "dryrun": communication groups
+ * (member lists), per-layer data chunks and pipeline send/recv lists of the local ranks.
+ * Touches no device; used to check multi-process rank logic on CPU. */
+GX_API int gx_exec_topology(const char* config_json, char* out, size_t cap, size_t* needed);
 /* ncclGetUniqueId -> 256 hex chars + NUL (rank 0 creates, torch.distributed broadcasts). */
 GX_API int gx_nccl_unique_id(char* out_hex, size_t cap);
 GX_API int64_t gx_launch_count(void);
@@ -167,8 +171,8 @@ typedef struct gx_gemm_epilogue {
   int64_t row_offset;         /* global row of local row 0 (dropout counter) */
   int64_t col_offset;         /* global column of local column 0 (dropout counter) */
   int64_t drop_ld;            /* global row length used by the dropout counter */
-  uint32_t drop_threshold;    /* p * 2^32; 0 disables dropout */
-  float drop_scale;           /* 1 / (1 - p) */
+  uint32_t drop_threshold;    /* thr8 = round(p * 256): byte threshold; 0 disables dropout */
+  float drop_scale;           /* 256 / (256 - thr8) */
   uint64_t seed;
   uint64_t site;
   int gelu_bwd;               /* out = acc * gelu'(aux) (aux = bf16 pre-activation, read) */
@@ -185,8 +189,7 @@ GX_API int gx_k_gemm_bf16(const void* a, int64_t lda, int a_mn_major, const void
  * row stride ld_qkv).  fwd writes ctx ([M][heads*d], ld_ctx) and lse (fp32 [batch*heads][seq],
  * log2 domain); bwd reads qkv, ctx, lse, dctx and writes dqkv (qkv layout) using the fp32
  * workspaces dq_accum ([batch*heads*seq*d]) and dsum ([batch*heads*seq]).  Dropout element
- * (q,k) of global (sample_offset+b, head_offset+h) uses Philox counter
- * ((sample*heads_total + head)*seq + q)*seq + k (see csrc/kernels/philox.cuh). */
+ * (q,k) of global (sample_offset+b, head_offset+h) follows csrc/kernels/attention.cu. */
 typedef struct gx_attention_args {
   int batch, seq, heads, head_dim;
   int heads_total, head_offset;
@@ -206,6 +209,8 @@ typedef struct gx_attention_args {
   uint64_t seed;
   uint64_t site;
   const uint64_t* seed_offset; /* optional device counter added to seed */
+  void* mask;                  /* uint16 keep bits [batch*heads][seq][ceil(seq/64)][4]:
+                                  written by fwd, read by bwd (when dropout is on) */
 } gx_attention_args;
 
 GX_API int gx_k_attention_fwd(const gx_attention_args* args, void* stream);
@@ -223,8 +228,8 @@ GX_API int gx_k_layernorm_bwd(const void* dy, const void* x, const void* mean, c
 /* Dropout sites share one parameter block: element (r, c) of a [rows][cols] local tensor is
  * global element (row_offset + r) * drop_ld + (col_offset + c) of the site's Philox stream. */
 typedef struct gx_dropout {
-  uint32_t threshold;         /* p * 2^32, 0 = off */
-  float scale;                /* 1/(1-p) */
+  uint32_t threshold;         /* thr8 = round(p * 256), 0 = off */
+  float scale;                /* 256 / (256 - thr8) */
   uint64_t seed, site;
   int64_t row_offset, col_offset, drop_ld;
   const uint64_t* seed_offset; /* optional device counter added to seed */

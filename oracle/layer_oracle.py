@@ -15,10 +15,11 @@ Layer (h hidden, H heads of d, f ffn; x is [tokens, h], tokens = samples * seq):
     x1  = x + drop_h1(ctx Wo^T + bo)
     c   = LN2(x1)
     y   = x1 + drop_h2(gelu(c W1^T + b1) W2^T + b2)  (exact erf GeLU)
-Dropout uses the Philox4x32-10 stream of csrc/kernels/philox.cuh: element i of a site is
-kept iff word (i & 3) of philox({i>>2 lo, i>>2 hi, site lo, site hi}, {seed lo, seed hi})
-is >= floor(p * 2^32); kept values are scaled by 1/(1-p).  Site ids per layer l:
-attn = 3l+0, hidden-1 = 3l+1, hidden-2 = 3l+2 (see paper_2211_13878_b200 executor).
+Dropout uses the Philox4x32-10 byte scheme of csrc/kernels/philox.cuh: one call
+philox({c lo, c hi, site lo, site hi}, {seed lo, seed hi}) yields 16 bytes; an element is
+kept iff its byte >= thr8 = round(p * 256), kept values scale by 256 / (256 - thr8).
+Hidden sites: element e -> call e >> 4, byte e & 15.  Attention sites: see _attn_mask.
+Site ids per layer l: attn = 3l+0, hidden-1 = 3l+1, hidden-2 = 3l+2.
 """
 from __future__ import annotations
 
@@ -49,21 +50,33 @@ def philox4x32_10(c0, c1, c2, c3, k0, k1):
 
 
 def dropout_threshold(p: float) -> int:
-    return 0 if p <= 0 else min(int(p * 4294967296.0), 0xFFFFFFFF)
+    """Byte threshold thr8 = round(p * 256) in [1, 255]; 0 = dropout off (philox.cuh)."""
+    return 0 if p <= 0 else max(1, min(255, int(p * 256.0 + 0.5)))
+
+
+def dropout_scale(p: float) -> float:
+    t = dropout_threshold(p)
+    return 1.0 if t == 0 else 256.0 / (256 - t)
+
+
+def keep_bytes(seed: int, site: int, call: np.ndarray, byte: np.ndarray, p: float) -> np.ndarray:
+    """Keep flag of byte `byte` (0..15) of Philox call `call` of a dropout site."""
+    call = np.asarray(call, dtype=np.uint64)
+    if p <= 0:
+        return np.ones(call.shape, dtype=bool)
+    w = philox4x32_10(call & MASK32, call >> np.uint64(32), np.uint64(site & 0xFFFFFFFF),
+                      np.uint64(site >> 32), np.uint64(seed & 0xFFFFFFFF), np.uint64(seed >> 32))
+    byte = np.asarray(byte, dtype=np.uint64)
+    words = np.stack(w, axis=-1)
+    word = np.take_along_axis(words, (byte >> np.uint64(2)).astype(np.int64)[..., None], axis=-1)[..., 0]
+    b = (word >> (np.uint64(8) * (byte & np.uint64(3)))) & np.uint64(0xFF)
+    return b >= np.uint64(dropout_threshold(p))
 
 
 def keep_mask(seed: int, site: int, index: np.ndarray, p: float) -> np.ndarray:
-    """Keep flags for global element indices `index` of dropout site `site`."""
+    """Hidden-state sites: element e uses byte e & 15 of call e >> 4."""
     index = np.asarray(index, dtype=np.uint64)
-    if p <= 0:
-        return np.ones(index.shape, dtype=bool)
-    q = index >> np.uint64(2)
-    w = philox4x32_10(q & MASK32, q >> np.uint64(32), np.uint64(site & 0xFFFFFFFF),
-                      np.uint64(site >> 32), np.uint64(seed & 0xFFFFFFFF), np.uint64(seed >> 32))
-    sel = (index & np.uint64(3)).astype(np.int64)
-    words = np.stack(w, axis=-1)
-    word = np.take_along_axis(words, sel[..., None], axis=-1)[..., 0]
-    return word >= np.uint64(dropout_threshold(p))
+    return keep_bytes(seed, site, index >> np.uint64(4), index & np.uint64(15), p)
 
 
 @dataclass
@@ -133,13 +146,23 @@ def _hidden_mask(drop: Dropout, site: int, rows: int, cols: int, row_offset: int
     return keep_mask(drop.seed, site, idx, drop.p_hidden)
 
 
-def _attn_mask(drop: Dropout, site: int, samples: int, heads: int, seq: int, sample_offset: int):
+def _attn_mask(drop: Dropout, site: int, samples: int, heads: int, seq: int, sample_offset: int,
+               heads_total=None, head_offset=0):
+    """Attention sites (csrc/kernels/attention.cu): element (q, k) of global (sample, head)
+    is byte j of call ((bh*s + q)*ceil(s/64) + k//64)*4 + t, with kk = k % 64,
+    t = (kk % 8) // 2, j = (kk // 8) * 2 + kk % 2 and bh = sample*heads_total + head."""
+    H = heads_total or heads
+    nkb = (seq + 63) // 64
     b = np.arange(samples, dtype=np.uint64)[:, None, None, None] + np.uint64(sample_offset)
-    h = np.arange(heads, dtype=np.uint64)[None, :, None, None]
+    h = np.arange(heads, dtype=np.uint64)[None, :, None, None] + np.uint64(head_offset)
     q = np.arange(seq, dtype=np.uint64)[None, None, :, None]
     k = np.arange(seq, dtype=np.uint64)[None, None, None, :]
-    idx = ((b * np.uint64(heads) + h) * np.uint64(seq) + q) * np.uint64(seq) + k
-    return keep_mask(drop.seed, site, idx, drop.p_attn)
+    kk = k % np.uint64(64)
+    t = (kk % np.uint64(8)) // np.uint64(2)
+    j = (kk // np.uint64(8)) * np.uint64(2) + kk % np.uint64(2)
+    call = (((b * np.uint64(H) + h) * np.uint64(seq) + q) * np.uint64(nkb) + k // np.uint64(64)) \
+        * np.uint64(4) + t
+    return keep_bytes(drop.seed, site, call, j, drop.p_attn)
 
 
 def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
@@ -157,13 +180,13 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
     pr = np.exp(sc)
     pr = pr / pr.sum(-1, keepdims=True)
     am = _attn_mask(drop, 3 * layer_id, n, H, s, sample_offset)
-    ka = 1.0 / (1.0 - drop.p_attn) if drop.p_attn > 0 else 1.0
+    ka = dropout_scale(drop.p_attn)
     pd = pr * am * ka
     ctx4 = pd @ v
     ctx = ctx4.transpose(0, 2, 1, 3).reshape(n * s, h)
     o = ctx @ P["w_o"].T + P["b_o"]
     m1 = _hidden_mask(drop, 3 * layer_id + 1, n * s, h, sample_offset * s)
-    kh = 1.0 / (1.0 - drop.p_hidden) if drop.p_hidden > 0 else 1.0
+    kh = dropout_scale(drop.p_hidden)
     x1 = x + o * m1 * kh
     c, ln2 = _ln_fwd(x1, P["ln2_g"], P["ln2_b"])
     pre = c @ P["w_1"].T + P["b_1"]

@@ -103,6 +103,8 @@ def _declare(L: ctypes.CDLL) -> None:
     L.gx_exec_profile_report.restype = c_int
     L.gx_exec_init_params.argtypes = [vp, c_uint64, c_float]
     L.gx_exec_init_params.restype = c_int
+    L.gx_exec_topology.argtypes = [c_char_p, c_char_p, c_size_t, POINTER(c_size_t)]
+    L.gx_exec_topology.restype = c_int
     declare_plan_api(L, "gx_plan_")
 
 

@@ -6,9 +6,12 @@
 // Forward keeps a running (max, sum) per query row and stores lse (log2 domain) for the
 // backward, which recomputes P = exp2(S*c - lse) per key block (FA2 scheme: each CTA owns a
 // block of keys, accumulates dK/dV in registers and adds dQ into an fp32 buffer).
-// Dropout masks come from the shared Philox stream (philox.cuh): element (q, k) of global
-// (sample, head) uses counter index ((sample*H_tot + head)*s + q)*s + k, so any TP/DP split
-// of heads or samples reproduces the unsharded masks exactly.
+// Dropout (philox.cuh byte scheme): the forward thread that owns query row q and lane t of a
+// 64-key block kb draws ONE Philox call, counter ((bh*s + q)*ceil(s/64) + kb)*4 + t with
+// bh = global_sample*H_tot + global_head, whose 16 bytes decide its 16 elements: key
+// kb*64 + 8*(j/2) + 2*t + (j%2) for byte j.  The forward stores those 16 keep bits (uint16,
+// [b*H][s][ceil(s/64)][4]) and the backward reads them back instead of re-drawing.  Masks
+// depend only on global (sample, head, q, k), so any TP/DP split reproduces them exactly.
 //
 // Tensor-core path: mma.sync m16n8k16 bf16 with ldmatrix fragments.  (A tcgen05/TMEM
 // variant is the planned next step; attention is ~7% of the layer FLOPs at s=512.)
@@ -64,26 +67,6 @@ __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&t);
 }
 
-// Dropout keep flags for elements e and e+1 of one (sample, head) stream.
-__device__ __forceinline__ void keep_pair(uint64_t seed, uint64_t site, uint64_t e,
-                                          uint32_t thr, bool& k0, bool& k1) {
-  const Philox4 w = dropout_words(seed, site, e >> 2);
-  const uint32_t words[4] = {w.x, w.y, w.z, w.w};
-  const uint32_t i = static_cast<uint32_t>(e & 3);
-  k0 = words[i] >= thr;
-  if (i < 3) {
-    k1 = words[i + 1] >= thr;
-  } else {
-    const Philox4 v = dropout_words(seed, site, (e + 1) >> 2);
-    k1 = v.x >= thr;
-  }
-}
-__device__ __forceinline__ bool keep_one(uint64_t seed, uint64_t site, uint64_t e, uint32_t thr) {
-  const Philox4 w = dropout_words(seed, site, e >> 2);
-  const uint32_t words[4] = {w.x, w.y, w.z, w.w};
-  return words[e & 3] >= thr;
-}
-
 // Loads a [64][HD] tile of rows [r0, r0+64) (rows >= nrows zero-filled) into padded smem.
 template <int HD>
 __device__ __forceinline__ void load_tile(__nv_bfloat16* dst, const __nv_bfloat16* src,
@@ -133,6 +116,8 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_a
   const uint64_t seed = p.seed + (p.seed_offset != nullptr ? *p.seed_offset : 0ull);
   const uint64_t stream =
       (static_cast<uint64_t>(p.sample_offset + b) * p.heads_total + (p.head_offset + h)) * s;
+  const int nkb = (s + kBlk - 1) / kBlk;
+  uint16_t* mask = static_cast<uint16_t*>(p.mask);
 
   float o[HD / 8][4];
 #pragma unroll
@@ -140,7 +125,6 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_a
   float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
   uint32_t qf[HD / 16][4];
 
-  const int nkb = (s + kBlk - 1) / kBlk;
   for (int kb = 0; kb < nkb; ++kb) {
     const int buf = kb & 1;
     if (kb + 1 < nkb) {
@@ -215,16 +199,17 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_a
     }
     if (thr != 0u) {
 #pragma unroll
-      for (int nb = 0; nb < 8; ++nb) {
-        const int key = kb * kBlk + nb * 8 + 2 * t;
+      for (int r = 0; r < 2; ++r) {
+        const int q = q0 + warp * 16 + g + 8 * r;
+        const uint64_t call = ((stream + static_cast<uint64_t>(q)) * nkb + kb) * 4 + t;
+        const uint32_t bits = keep16(seed, p.site, call, thr);
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int q = q0 + warp * 16 + g + 8 * r;
-          bool k0, k1;
-          keep_pair(seed, p.site, (stream + static_cast<uint64_t>(q)) * s + key, thr, k0, k1);
-          sacc[nb][2 * r] = k0 ? sacc[nb][2 * r] * inv_keep : 0.f;
-          sacc[nb][2 * r + 1] = k1 ? sacc[nb][2 * r + 1] * inv_keep : 0.f;
+        for (int nb = 0; nb < 8; ++nb) {
+          sacc[nb][2 * r] = (bits >> (2 * nb)) & 1u ? sacc[nb][2 * r] * inv_keep : 0.f;
+          sacc[nb][2 * r + 1] = (bits >> (2 * nb + 1)) & 1u ? sacc[nb][2 * r + 1] * inv_keep : 0.f;
         }
+        if (q < s) mask[((static_cast<int64_t>(bh) * s + q) * nkb + kb) * 4 + t] =
+            static_cast<uint16_t>(bits);
       }
     }
     // O += P V
@@ -305,6 +290,7 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
   __nv_bfloat16* sdS = sdO + kBlk * LDS;                              // [64 keys][LDP]
   float* sL = reinterpret_cast<float*>(sdS + kBlk * LDP);             // lse [64]
   float* sD = sL + kBlk;                                              // D   [64]
+  uint16_t* sM = reinterpret_cast<uint16_t*>(sD + kBlk);              // keep bits [64][4]
 
   const int s = p.seq, H = p.heads;
   const int bh = blockIdx.y;
@@ -332,8 +318,9 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
   const uint32_t thr = p.drop_threshold;
   const float inv_keep = p.drop_scale;
   const uint64_t seed = p.seed + (p.seed_offset != nullptr ? *p.seed_offset : 0ull);
-  const uint64_t stream =
-      (static_cast<uint64_t>(p.sample_offset + b) * p.heads_total + (p.head_offset + h)) * s;
+  const int nkb = (s + kBlk - 1) / kBlk;
+  const int kbi = blockIdx.x;
+  const uint16_t* mask = static_cast<const uint16_t*>(p.mask);
 
   float dk[HD / 8][4], dv[HD / 8][4];
 #pragma unroll
@@ -351,6 +338,13 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
       const bool ok = q0 + i < s;
       sL[i] = ok ? lse[q0 + i] : 0.f;
       sD[i] = ok ? dsum[q0 + i] : 0.f;
+    }
+    if (thr != 0u) {
+      for (int i = threadIdx.x; i < kBlk * 4; i += kThreads) {
+        const int qi = i >> 2;
+        sM[i] = q0 + qi < s ? mask[((static_cast<int64_t>(bh) * s + q0 + qi) * nkb + kbi) * 4 + (i & 3)]
+                            : static_cast<uint16_t>(0);
+      }
     }
     cp_async_commit();
     cp_async_wait<0>();
@@ -394,10 +388,10 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
         const int key = k0 + warp * 16 + g + 8 * (j >> 1);
         float P = (q < s && key < s) ? exp2f(st[nb][j] * c2 - sL[ql]) : 0.f;
         float keep = 1.f;
-        if (thr != 0u && P != 0.f) {
-          keep = keep_one(seed, p.site, (stream + static_cast<uint64_t>(q)) * s + key, thr)
-                     ? inv_keep
-                     : 0.f;
+        if (thr != 0u) {
+          const int kk = key - k0;  // 0..63 within this CTA's key block
+          const uint32_t bits = sM[ql * 4 + ((kk & 7) >> 1)];
+          keep = (bits >> (((kk >> 3) << 1) | (kk & 1))) & 1u ? inv_keep : 0.f;
         }
         pd[nb][j] = P * keep;
         st[nb][j] = P * (dpt[nb][j] * keep - sD[ql]);  // dS^T
@@ -525,7 +519,7 @@ static int attention_fwd_impl(const gx_attention_args& a, cudaStream_t st) {
 template <int HD>
 static int attention_bwd_impl(const gx_attention_args& a, cudaStream_t st) {
   constexpr int LDS = HD + 8;
-  const int smem = 4 * kBlk * LDS * 2 + kBlk * (kBlk + 8) * 2 + 2 * kBlk * 4;
+  const int smem = 4 * kBlk * LDS * 2 + kBlk * (kBlk + 8) * 2 + 2 * kBlk * 4 + kBlk * 4 * 2;
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(attn_bwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

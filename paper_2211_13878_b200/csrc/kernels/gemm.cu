@@ -126,16 +126,16 @@ __device__ __forceinline__ void epilogue_row32(const GemmEpilogue& ep, int64_t r
     const uint64_t grow = static_cast<uint64_t>(ep.row_offset + row);
     if (ep.drop_threshold != 0u) {
       const uint64_t seed = ep.seed + (ep.seed_offset != nullptr ? *ep.seed_offset : 0ull);
+      // e0 is a multiple of 16 (drop_ld and column offsets are; checked on host): the 32
+      // columns are exactly two Philox calls
+      const uint64_t e0 = grow * static_cast<uint64_t>(ep.drop_ld) +
+                          static_cast<uint64_t>(ep.col_offset + n0);
+      const uint32_t k0 = keep16(seed, ep.site, e0 >> 4, ep.drop_threshold);
+      const uint32_t k1 = keep16(seed, ep.site, (e0 >> 4) + 1, ep.drop_threshold);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const uint64_t e0 = grow * static_cast<uint64_t>(ep.drop_ld) +
-                            static_cast<uint64_t>(ep.col_offset + n0 + q * 4);
-        // e0 is a multiple of 4 whenever drop_ld and the column offsets are (checked on host)
-        const Philox4 w = dropout_words(seed, ep.site, e0 >> 2);
-        v[q * 4 + 0] = w.x >= ep.drop_threshold ? v[q * 4 + 0] * ep.drop_scale : 0.f;
-        v[q * 4 + 1] = w.y >= ep.drop_threshold ? v[q * 4 + 1] * ep.drop_scale : 0.f;
-        v[q * 4 + 2] = w.z >= ep.drop_threshold ? v[q * 4 + 2] * ep.drop_scale : 0.f;
-        v[q * 4 + 3] = w.w >= ep.drop_threshold ? v[q * 4 + 3] * ep.drop_scale : 0.f;
+      for (int j = 0; j < 32; ++j) {
+        const bool keep = ((j < 16 ? k0 >> j : k1 >> (j - 16)) & 1u) != 0u;
+        v[j] = keep ? v[j] * ep.drop_scale : 0.f;
       }
     }
     // dropout output rounded to bf16 before the add, matching the unfused path
@@ -440,6 +440,8 @@ int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
   // TMA: row strides must be 16-byte multiples; the epilogue's vector stores need ldo too.
   if ((a.ld % 8) != 0 || (b.ld % 8) != 0 || (ep.ldo % 8) != 0)
     return set_error(kErrConfig, "gemm: lda, ldb and ldo must be multiples of 8 elements");
+  if (ep.drop_threshold != 0u && ((ep.drop_ld % 16) != 0 || (ep.col_offset % 16) != 0))
+    return set_error(kErrConfig, "gemm: dropout row length / column offset must be multiples of 16");
   const int bn = force_bn > 0 ? force_bn : pick_bn(M, N);
 #define GX_GEMM_DISPATCH(BN_)                                                           \
   if (bn == BN_) {                                                                      \

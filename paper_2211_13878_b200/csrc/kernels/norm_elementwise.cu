@@ -47,17 +47,16 @@ int grid_for(int64_t work, int per_block) {
 // keep flags for 8 consecutive elements starting at global index e (any alignment)
 __device__ __forceinline__ void keep8(const gx_dropout& d, uint64_t e, bool (&k)[8]) {
   const uint64_t seed = d.seed + (d.seed_offset != nullptr ? *d.seed_offset : 0ull);
-  uint64_t qcur = e >> 2;
-  Philox4 w = dropout_words(seed, d.site, qcur);
+  uint64_t ccur = e >> 4;
+  uint32_t bits = keep16(seed, d.site, ccur, d.threshold);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const uint64_t ej = e + j;
-    if ((ej >> 2) != qcur) {
-      qcur = ej >> 2;
-      w = dropout_words(seed, d.site, qcur);
+    if ((ej >> 4) != ccur) {
+      ccur = ej >> 4;
+      bits = keep16(seed, d.site, ccur, d.threshold);
     }
-    const uint32_t words[4] = {w.x, w.y, w.z, w.w};
-    k[j] = words[ej & 3] >= d.threshold;
+    k[j] = ((bits >> (ej & 15)) & 1u) != 0u;
   }
 }
 

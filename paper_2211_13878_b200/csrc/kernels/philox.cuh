@@ -39,4 +39,20 @@ __host__ __device__ __forceinline__ Philox4 dropout_words(uint64_t seed, uint64_
                        static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
 }
 
+// 16 keep bits (bit j = byte j >= thr8) of call `c` of a site.
+__host__ __device__ __forceinline__ uint32_t keep16(uint64_t seed, uint64_t site, uint64_t c,
+                                                    uint32_t thr8) {
+  const Philox4 w = philox4x32_10(static_cast<uint32_t>(c), static_cast<uint32_t>(c >> 32),
+                                  static_cast<uint32_t>(site), static_cast<uint32_t>(site >> 32),
+                                  static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
+  const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+  uint32_t bits = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const uint32_t b = (words[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+    bits |= (b >= thr8 ? 1u : 0u) << j;
+  }
+  return bits;
+}
+
 }  // namespace gx

@@ -111,6 +111,21 @@ int gx_exec_info(gx_exec* ex, char* out, size_t cap, size_t* needed) {
   return gx::kOk;
 }
 
+int gx_exec_topology(const char* config_json, char* out, size_t cap, size_t* needed) {
+  if (config_json == nullptr) return bad("exec_topology: NULL config");
+  std::string cfg = config_json;
+  // force the device-free dry-run mode
+  std::string err;
+  auto impl = gx::create_executor(cfg, &err);
+  if (!impl) return gx::set_error(gx::kErrConfig, err.c_str());
+  const std::string s = impl->topology();
+  if (needed != nullptr) *needed = s.size() + 1;
+  if (out == nullptr || cap == 0) return gx::kOk;
+  if (cap < s.size() + 1) return bad("exec_topology: buffer too small");
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return gx::kOk;
+}
+
 int gx_exec_canonical_size(int hidden, int ffn, int64_t* out) {
   gx::Shape s;
   s.h = hidden;

@@ -144,6 +144,7 @@ struct Acts {
   bf16 *x = nullptr, *ln1 = nullptr, *qkv = nullptr, *ctx = nullptr, *x1 = nullptr,
        *ln2 = nullptr, *pre = nullptr, *gel = nullptr, *y = nullptr;
   float *lse = nullptr, *mean1 = nullptr, *rstd1 = nullptr, *mean2 = nullptr, *rstd2 = nullptr;
+  uint16_t* amask = nullptr;  // attention dropout keep bits (fwd -> bwd)
 };
 
 enum class Xin { kSame, kSlice, kGather, kStageInput };
@@ -201,9 +202,12 @@ class ExecutorImpl final : public Executor {
     if (pgraph_exec_ != nullptr) cudaGraphExecDestroy(pgraph_exec_);
     if (pgraph_ != nullptr) cudaGraphDestroy(pgraph_);
     for (cudaEvent_t e : events_) cudaEventDestroy(e);
+    for (cudaEvent_t e : fork_events_) cudaEventDestroy(e);
+    if (join_event_ != nullptr) cudaEventDestroy(join_event_);
     ranks_.clear();
     comm_.reset();
     if (stream_ != nullptr) cudaStreamDestroy(stream_);
+    if (side_ != nullptr) cudaStreamDestroy(side_);
   }
 
  private:
@@ -233,6 +237,16 @@ class ExecutorImpl final : public Executor {
   int gather_params(RankCtx& r, int li);
   int pp_fwd(RankCtx& r, int mb, bool send);
   int pp_bwd(RankCtx& r, int mb, bool send);
+  struct Xfer {
+    int peer;
+    int64_t lo, hi;  // global sample range within the iteration
+  };
+  std::vector<Xfer> pp_plan(int stage, int idx, int mb, int kind) const;
+
+ public:
+  std::string topology() const override;
+
+ private:
 
   // ------------------------------------------------------------ kernel profiler
   // Categories of launched work; every launch site goes through timed(), which (when
@@ -316,16 +330,24 @@ class ExecutorImpl final : public Executor {
   float lr_ = 1e-4f, b1_ = 0.9f, b2_ = 0.999f, eps_ = 1e-8f, wd_ = 0.f;
   bool optimizer_ = true;
   bool forward_only_ = false;  // profiler / debugging: skip loss, backward and optimizer
+  bool dry_run_ = false;       // topology only: no device state (host-logic tests)
   float inv_count_ = 1.f;
 
   std::unique_ptr<Comm> comm_;
   std::vector<std::unique_ptr<RankCtx>> ranks_;
   cudaStream_t stream_ = nullptr;
+  // AdamW of layer l runs on side_ while layer l-1's backward runs on stream_ (HBM-bound
+  // optimizer under tensor-bound GEMMs); joined back before the step ends.
+  cudaStream_t side_ = nullptr;
+  std::vector<cudaEvent_t> fork_events_;
+  cudaEvent_t join_event_ = nullptr;
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
   cudaGraph_t pgraph_ = nullptr;  // instrumented (profiling) variant
   cudaGraphExec_t pgraph_exec_ = nullptr;
   bool profiling_ = false, capturing_ = false;
+  int fork_used_ = 0;
+  bool side_used_ = false;
   std::vector<cudaEvent_t> events_;
   size_t ev_used_ = 0;
   std::vector<Rec> recs_, prof_recs_;
@@ -334,10 +356,16 @@ class ExecutorImpl final : public Executor {
   int64_t launches_per_step_ = 0;
 };
 
+// Byte-threshold dropout (philox.cuh): thr8 = round(p * 256); kept values scale by
+// 256 / (256 - thr8) so the expectation is exact at the effective rate thr8 / 256.
 uint32_t threshold_of(float p) {
   if (p <= 0.f) return 0u;
-  const double t = static_cast<double>(p) * 4294967296.0;
-  return t >= 4294967295.0 ? 0xFFFFFFFFu : static_cast<uint32_t>(t);
+  const int t = static_cast<int>(p * 256.f + 0.5f);
+  return static_cast<uint32_t>(t > 255 ? 255 : (t < 1 ? 1 : t));
+}
+float scale_of(float p) {
+  const uint32_t t = threshold_of(p);
+  return t == 0u ? 1.f : 256.f / static_cast<float>(256u - t);
 }
 
 int ExecutorImpl::init(const json& cfg, std::string* err) {
@@ -345,7 +373,9 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     plan_ = cfg.at("plan");
     model_ = cfg.at("model");
     world_ = cfg.at("world_size").get<int>();
-    sim_ = cfg.value("comm", std::string("sim")) == "sim";
+    const std::string comm_kind = cfg.value("comm", std::string("sim"));
+    sim_ = comm_kind == "sim" || comm_kind == "dryrun";
+    dry_run_ = comm_kind == "dryrun";
     p_attn_ = cfg.value("dropout_attn", 0.0f);
     p_hidden_ = cfg.value("dropout_hidden", 0.0f);
     seed_ = cfg.value("seed", static_cast<uint64_t>(1234));
@@ -454,6 +484,23 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
         id[i] = static_cast<char>(std::stoi(hex.substr(2 * i, 2), nullptr, 16));
       comm_ = make_nccl_comm(world_, local[0], id, err);
       if (!comm_) return kErrNccl;
+    }
+    if (dry_run_) {
+      for (int r : local) {
+        auto rc = std::make_unique<RankCtx>();
+        rc->rank = r;
+        rc->stage = r / g_;
+        rc->idx = r % g_;
+        ranks_.push_back(std::move(rc));
+      }
+      const int rc = build_groups();
+      if (rc != kOk) *err = gx_last_error();
+      return rc;
+    }
+    if (cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&join_event_, cudaEventDisableTiming) != cudaSuccess) {
+      *err = "executor: side stream creation failed";
+      return kErrCuda;
     }
     if (cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking) != cudaSuccess) {
       *err = "executor: cudaStreamCreate failed";
@@ -590,6 +637,9 @@ int ExecutorImpl::allocate(RankCtx& r) {
       a.gel = A.a<bf16>(rows * ft);
       a.y = A.a<bf16>(rows * h);
       a.lse = A.a<float>(static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq);
+      if (thr_attn_ != 0u)
+        a.amask = A.a<uint16_t>(static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq *
+                                ((s.seq + 63) / 64) * 4);
       a.mean1 = A.a<float>(rows);
       a.rstd1 = A.a<float>(rows);
       a.mean2 = A.a<float>(rows);
@@ -841,10 +891,11 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     at.ld_ctx = ht;
     at.lse = A.lse;
     at.drop_threshold = thr_attn_;
-    at.drop_scale = p_attn_ > 0 ? 1.f / (1.f - p_attn_) : 1.f;
+    at.drop_scale = scale_of(p_attn_);
     at.seed = seed_;
     at.site = 3ull * l;
     at.seed_offset = r.seed_off;
+    at.mask = A.amask;
     {
       const double af = 4.0 * A.samples * (s.heads / t) * double(s.seq) * s.seq * s.hd;
       GX_TRY(timed(kAttnFwd, af, 2.0 * rows * 4 * ht, [&] { return attention_fwd(at, stream_); }));
@@ -860,7 +911,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
       o.row_offset = row_off;
       o.drop_ld = h;
       o.drop_threshold = thr_hidden_;
-      o.drop_scale = p_hidden_ > 0 ? 1.f / (1.f - p_hidden_) : 1.f;
+      o.drop_scale = scale_of(p_hidden_);
       o.seed = seed_;
       o.site = 3ull * l + 1;
       o.seed_offset = r.seed_off;
@@ -876,7 +927,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     if (t > 1) {
       gx_dropout d{};
       d.threshold = thr_hidden_;
-      d.scale = p_hidden_ > 0 ? 1.f / (1.f - p_hidden_) : 1.f;
+      d.scale = scale_of(p_hidden_);
       d.seed = seed_;
       d.site = 3ull * l + 1;
       d.row_offset = row_off;
@@ -906,7 +957,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
       o.row_offset = row_off;
       o.drop_ld = h;
       o.drop_threshold = thr_hidden_;
-      o.drop_scale = p_hidden_ > 0 ? 1.f / (1.f - p_hidden_) : 1.f;
+      o.drop_scale = scale_of(p_hidden_);
       o.seed = seed_;
       o.site = 3ull * l + 2;
       o.seed_offset = r.seed_off;
@@ -920,7 +971,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
   if (t > 1 && phase == 2) {
     gx_dropout d{};
     d.threshold = thr_hidden_;
-    d.scale = p_hidden_ > 0 ? 1.f / (1.f - p_hidden_) : 1.f;
+    d.scale = scale_of(p_hidden_);
     d.seed = seed_;
     d.site = 3ull * l + 2;
     d.row_offset = row_off;
@@ -953,7 +1004,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
   if (rows == 0) return kOk;
   gx_dropout d{};
   d.threshold = thr_hidden_;
-  d.scale = p_hidden_ > 0 ? 1.f / (1.f - p_hidden_) : 1.f;
+  d.scale = scale_of(p_hidden_);
   d.seed = seed_;
   d.row_offset = row_off;
   d.drop_ld = h;
@@ -1022,10 +1073,11 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     at.dq_accum = r.dq_acc;
     at.dsum = r.dsum;
     at.drop_threshold = thr_attn_;
-    at.drop_scale = p_attn_ > 0 ? 1.f / (1.f - p_attn_) : 1.f;
+    at.drop_scale = scale_of(p_attn_);
     at.seed = seed_;
     at.site = 3ull * l;
     at.seed_offset = r.seed_off;
+    at.mask = A.amask;
     {
       const double af = 10.0 * A.samples * (s.heads / t) * double(s.seq) * s.seq * s.hd;
       GX_TRY(timed(kAttnBwd, af, 2.0 * rows * 8 * ht, [&] { return attention_bwd(at, stream_); }));
@@ -1069,11 +1121,24 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
                                DType::kF32, stream_);
     return kOk;
   }
-  if (phase == 2 && optimizer_)
-    return timed(kOptim, 0, 30.0 * L.shard_n, [&] {
-      return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_, wd_,
-                       r.step, stream_);
-    });
+  if (phase == 2 && optimizer_) {
+    if (profiling_)  // instrumented runs keep everything on one stream for clean event pairs
+      return timed(kOptim, 0, 30.0 * L.shard_n, [&] {
+        return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_,
+                         wd_, r.step, stream_);
+      });
+    if (fork_events_.size() <= static_cast<size_t>(fork_used_)) {
+      cudaEvent_t e;
+      GX_TRY(cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event"));
+      fork_events_.push_back(e);
+    }
+    cudaEvent_t e = fork_events_[fork_used_++];
+    GX_TRY(cuda_check(cudaEventRecord(e, stream_), "fork record"));
+    GX_TRY(cuda_check(cudaStreamWaitEvent(side_, e, 0), "fork wait"));
+    side_used_ = true;
+    return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_, wd_,
+                     r.step, side_);
+  }
   return kOk;
 }
 
@@ -1133,88 +1198,142 @@ int ExecutorImpl::xin_bwd(RankCtx& r, int li, int mb) {
   return c_all_gather(L.g_xin, r.rank, dX, dYp, counts, DType::kBF16, stream_);
 }
 
-// Pipeline boundary.  Forward: this stage's last layer output -> next stage's first layer
-// input (send=true on the sender stage, false on the receiver stage).
-int ExecutorImpl::pp_fwd(RankCtx& r, int mb, bool send) {
+// Pipeline-boundary transfer lists (pure functions of the plan, shared by the executor and
+// the dry-run topology export).  kind 0: forward send (this stage's last layer output to the
+// next stage), 1: forward receive, 2: backward send (first layer's input gradient to the
+// previous stage), 3: backward receive.  Each entry is (peer global rank, sample range); a
+// sender is paired with the receiver of equal tp-residue so every receiver gets each
+// overlapping sample range exactly once.
+std::vector<ExecutorImpl::Xfer> ExecutorImpl::pp_plan(int stage, int idx, int mb, int kind) const {
+  std::vector<Xfer> out;
+  const bool fwd = kind < 2;
+  const bool send = kind == 0 || kind == 2;
+  // (my layer, other stage, other layer) for this boundary
+  const int other = fwd ? (send ? stage + 1 : stage - 1) : (send ? stage - 1 : stage + 1);
+  const int my_layer = (fwd == send) ? stage_range_[stage].second - 1 : stage_range_[stage].first;
+  const int ot_layer = (fwd == send) ? stage_range_[other].first : stage_range_[other].second - 1;
+  const Deg& me = deg_[my_layer];
+  const Deg& ot = deg_[ot_layer];
+  int64_t mlo, mhi;
+  chunk(me, idx, mb, mlo, mhi);
   if (send) {
-    const RankLayer& A = r.layers.back();
-    const int nxt = r.stage + 1;
-    const Deg& b = deg_[stage_range_[nxt].first];
-    const Acts& my = A.acts[mb];
-    const int64_t hs = static_cast<int64_t>(A.sh.seq) * A.sh.h;
-    for (int ip = 0; ip < g_; ++ip) {
-      if (ip % A.d.tp != r.idx % A.d.tp) continue;
+    for (int j = 0; j < g_; ++j) {
+      if (j % me.tp != idx % me.tp) continue;
       int64_t lo2, hi2;
-      chunk(b, ip, mb, lo2, hi2);
-      const int64_t lo = std::max<int64_t>(my.sample0, lo2);
-      const int64_t hi = std::min<int64_t>(my.sample0 + my.samples, hi2);
-      if (hi <= lo) continue;
-      GX_TRY(comm_->send(r.rank, nxt * g_ + ip, my.y + (lo - my.sample0) * hs,
-                         static_cast<size_t>((hi - lo) * hs) * 2, stream_));
+      chunk(ot, j, mb, lo2, hi2);
+      const int64_t lo = std::max(mlo, lo2), hi = std::min(mhi, hi2);
+      if (hi > lo) out.push_back(Xfer{other * g_ + j, lo, hi});
     }
-    return kOk;
+  } else {
+    for (int c = 0; c < ot.data(); ++c) {
+      int64_t lo1, hi1;
+      chunk(ot, c * ot.tp, mb, lo1, hi1);
+      const int64_t lo = std::max(mlo, lo1), hi = std::min(mhi, hi1);
+      if (hi > lo) out.push_back(Xfer{other * g_ + c * ot.tp + idx % ot.tp, lo, hi});
+    }
   }
-  RankLayer& B = r.layers.front();
-  const int prv = r.stage - 1;
-  const Deg& a = deg_[stage_range_[prv].second - 1];
-  Acts& my = B.acts[mb];
-  const int64_t hs = static_cast<int64_t>(B.sh.seq) * B.sh.h;
-  for (int c = 0; c < a.data(); ++c) {
-    int64_t lo1, hi1;
-    chunk(a, c * a.tp, mb, lo1, hi1);
-    const int64_t lo = std::max<int64_t>(my.sample0, lo1);
-    const int64_t hi = std::min<int64_t>(my.sample0 + my.samples, hi1);
-    if (hi <= lo) continue;
-    const int src = prv * g_ + c * a.tp + r.idx % a.tp;
-    GX_TRY(comm_->recv(r.rank, src, my.x + (lo - my.sample0) * hs,
-                       static_cast<size_t>((hi - lo) * hs) * 2, stream_));
+  return out;
+}
+
+// Forward boundary: send this stage's last layer output / receive the first layer input.
+int ExecutorImpl::pp_fwd(RankCtx& r, int mb, bool send) {
+  const RankLayer& L = send ? r.layers.back() : r.layers.front();
+  const Acts& my = L.acts[mb];
+  const int64_t hs = static_cast<int64_t>(L.sh.seq) * L.sh.h;
+  for (const Xfer& x : pp_plan(r.stage, r.idx, mb, send ? 0 : 1)) {
+    const size_t bytes = static_cast<size_t>((x.hi - x.lo) * hs) * 2;
+    const int64_t off = (x.lo - my.sample0) * hs;
+    if (send) {
+      GX_TRY(comm_->send(r.rank, x.peer, my.y + off, bytes, stream_));
+    } else {
+      GX_TRY(comm_->recv(r.rank, x.peer, my.x + off, bytes, stream_));
+    }
   }
   return kOk;
 }
 
-// Backward: input gradient of this stage's first layer -> previous stage (send=true), or
-// receive the output gradient of this stage's last layer into gbuf[cur] (send=false).
+// Backward boundary: send the first layer's input gradient (gbuf[cur ^ 1]) / receive the
+// last layer's output gradient into gbuf[cur].
 int ExecutorImpl::pp_bwd(RankCtx& r, int mb, bool send) {
-  if (send) {
-    const RankLayer& B = r.layers.front();
-    const int prv = r.stage - 1;
-    const Deg& a = deg_[stage_range_[prv].second - 1];
-    const Acts& my = B.acts[mb];
-    const bf16* dX = r.gbuf[r.cur ^ 1];
-    const int64_t hs = static_cast<int64_t>(B.sh.seq) * B.sh.h;
-    for (int i = 0; i < g_; ++i) {
-      if (i % B.d.tp != r.idx % B.d.tp) continue;
-      int64_t lo1, hi1;
-      chunk(a, i, mb, lo1, hi1);
-      const int64_t lo = std::max<int64_t>(my.sample0, lo1);
-      const int64_t hi = std::min<int64_t>(my.sample0 + my.samples, hi1);
-      if (hi <= lo) continue;
-      GX_TRY(comm_->send(r.rank, prv * g_ + i, dX + (lo - my.sample0) * hs,
-                         static_cast<size_t>((hi - lo) * hs) * 2, stream_));
+  const RankLayer& L = send ? r.layers.front() : r.layers.back();
+  const Acts& my = L.acts[mb];
+  const int64_t hs = static_cast<int64_t>(L.sh.seq) * L.sh.h;
+  for (const Xfer& x : pp_plan(r.stage, r.idx, mb, send ? 2 : 3)) {
+    const size_t bytes = static_cast<size_t>((x.hi - x.lo) * hs) * 2;
+    const int64_t off = (x.lo - my.sample0) * hs;
+    if (send) {
+      GX_TRY(comm_->send(r.rank, x.peer, r.gbuf[r.cur ^ 1] + off, bytes, stream_));
+    } else {
+      GX_TRY(comm_->recv(r.rank, x.peer, r.gbuf[r.cur] + off, bytes, stream_));
     }
-    return kOk;
-  }
-  const RankLayer& A = r.layers.back();
-  const int nxt = r.stage + 1;
-  const Deg& b = deg_[stage_range_[nxt].first];
-  const Acts& my = A.acts[mb];
-  bf16* dY = r.gbuf[r.cur];
-  const int64_t hs = static_cast<int64_t>(A.sh.seq) * A.sh.h;
-  for (int c = 0; c < b.data(); ++c) {
-    int64_t lo2, hi2;
-    chunk(b, c * b.tp, mb, lo2, hi2);
-    const int64_t lo = std::max<int64_t>(my.sample0, lo2);
-    const int64_t hi = std::min<int64_t>(my.sample0 + my.samples, hi2);
-    if (hi <= lo) continue;
-    const int src = nxt * g_ + c * b.tp + r.idx % b.tp;
-    GX_TRY(comm_->recv(r.rank, src, dY + (lo - my.sample0) * hs,
-                       static_cast<size_t>((hi - lo) * hs) * 2, stream_));
   }
   return kOk;
+}
+
+std::string ExecutorImpl::topology() const {
+  json j;
+  j["world_size"] = world_;
+  j["pp_degree"] = P_;
+  j["group_size"] = g_;
+  j["micro_batches"] = m_;
+  j["batch_size"] = B_;
+  json ranks = json::array();
+  auto members = [&](int gid) {
+    return gid < 0 ? json(nullptr) : json(comm_->group(gid).ranks);
+  };
+  for (const auto& r : ranks_) {
+    json jr;
+    jr["rank"] = r->rank;
+    jr["stage"] = r->stage;
+    jr["idx"] = r->idx;
+    json layers = json::array();
+    for (const RankLayer& L : r->layers) {
+      json jl;
+      jl["layer"] = L.layer;
+      jl["dp"] = L.d.dp;
+      jl["sdp"] = L.d.sdp;
+      jl["tp"] = L.d.tp;
+      jl["tp_rank"] = L.tr;
+      jl["data_rank"] = L.dr;
+      jl["tp_group"] = members(L.g_tp);
+      jl["sdp_group"] = members(L.g_sdp);
+      jl["dp_group"] = members(L.g_dp);
+      jl["relayout"] = L.xin == Xin::kSame ? "same" : L.xin == Xin::kSlice ? "slice"
+                       : L.xin == Xin::kGather ? "gather" : "stage_input";
+      jl["relayout_group"] = members(L.g_xin);
+      json ch = json::array();
+      for (int mb = 0; mb < m_; ++mb) {
+        int64_t lo, hi;
+        chunk(L.d, r->idx, mb, lo, hi);
+        ch.push_back({lo, hi});
+      }
+      jl["chunks"] = ch;
+      layers.push_back(jl);
+    }
+    jr["layers"] = layers;
+    json pp = json::array();
+    for (int mb = 0; mb < m_; ++mb) {
+      for (int kind = 0; kind < 4; ++kind) {
+        const bool exists = (kind == 0 && r->stage + 1 < P_) || (kind == 1 && r->stage > 0) ||
+                            (kind == 2 && r->stage > 0) || (kind == 3 && r->stage + 1 < P_);
+        if (!exists) continue;
+        for (const Xfer& x : pp_plan(r->stage, r->idx, mb, kind))
+          pp.push_back({{"mb", mb}, {"kind", kind}, {"peer", x.peer}, {"lo", x.lo}, {"hi", x.hi}});
+      }
+    }
+    jr["pp"] = pp;
+    ranks.push_back(jr);
+  }
+  j["ranks"] = ranks;
+  j["groups"] = json::array();
+  for (int g = 0; g < comm_->num_groups(); ++g) j["groups"].push_back(comm_->group(g).ranks);
+  return j.dump();
 }
 
 // ------------------------------------------------------------------------- the step
 int ExecutorImpl::step_once() {
+  fork_used_ = 0;
+  side_used_ = false;
   auto in_stage = [&](int st) {
     std::vector<RankCtx*> v;
     for (auto& r : ranks_)
@@ -1316,6 +1435,10 @@ int ExecutorImpl::step_once() {
         }
       }
     }
+  }
+  if (side_used_) {  // join the optimizer stream before the step completes
+    GX_TRY(cuda_check(cudaEventRecord(join_event_, side_), "join record"));
+    GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, join_event_, 0), "join wait"));
   }
   for (auto& r : ranks_) GX_TRY(comm_->world_sum(r->rank, r->loss, stream_));
   // next step draws fresh dropout masks

@@ -51,6 +51,18 @@ def make_plan(strategies: Sequence[str], batch_size: int, pp_degree: int = 1,
             "stages": stages}
 
 
+def topology(plan: dict, model: dict, world_size: int, local_ranks) -> dict:
+    """Device-free view of what each local rank will do (groups, chunks, PP transfers)."""
+    cfg = {"plan": plan, "model": model, "world_size": world_size,
+           "local_ranks": list(local_ranks), "comm": "dryrun"}
+    need = ctypes.c_size_t()
+    txt = json.dumps(cfg).encode()
+    _lib.check(_lib.lib().gx_exec_topology(txt, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _lib.check(_lib.lib().gx_exec_topology(txt, buf, need.value, ctypes.byref(need)))
+    return json.loads(buf.value.decode())
+
+
 def nccl_unique_id() -> str:
     buf = ctypes.create_string_buffer(257)
     _lib.check(_lib.lib().gx_nccl_unique_id(buf, 257))

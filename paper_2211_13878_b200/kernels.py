@@ -20,10 +20,15 @@ def _ptr(t) -> int:
 
 
 def dropout_threshold(p: float) -> int:
-    """p * 2^32 rounded down, clamped; 0 disables dropout (matches the oracle)."""
+    """Byte threshold thr8 = round(p * 256) in [1, 255]; 0 disables dropout (philox.cuh)."""
     if p <= 0.0:
         return 0
-    return min(int(p * 4294967296.0), 0xFFFFFFFF)
+    return max(1, min(255, int(p * 256.0 + 0.5)))
+
+
+def dropout_scale(p: float) -> float:
+    t = dropout_threshold(p)
+    return 1.0 if t == 0 else 256.0 / (256 - t)
 
 
 def gemm(a, b, *, a_mn_major=False, b_mn_major=False, out=None, out_kind="bf16", bias=None,
@@ -58,7 +63,7 @@ def gemm(a, b, *, a_mn_major=False, b_mn_major=False, out=None, out_kind="bf16",
     ep.col_offset = col_offset
     ep.drop_ld = drop_ld if drop_ld is not None else N
     ep.drop_threshold = dropout_threshold(dropout_p)
-    ep.drop_scale = 1.0 / (1.0 - dropout_p) if dropout_p > 0 else 1.0
+    ep.drop_scale = dropout_scale(dropout_p)
     ep.seed = seed
     ep.site = site
     _lib.check(_lib.lib().gx_k_gemm_bf16(
@@ -77,7 +82,7 @@ class _AttnArgs(ctypes.Structure):
                 ("dq_accum", ctypes.c_void_p), ("dsum", ctypes.c_void_p),
                 ("drop_threshold", ctypes.c_uint32), ("drop_scale", ctypes.c_float),
                 ("seed", ctypes.c_uint64), ("site", ctypes.c_uint64),
-                ("seed_offset", ctypes.c_void_p)]
+                ("seed_offset", ctypes.c_void_p), ("mask", ctypes.c_void_p)]
 
 
 class Dropout(ctypes.Structure):
@@ -90,7 +95,7 @@ class Dropout(ctypes.Structure):
 def make_dropout(p, seed, site, row_offset=0, col_offset=0, drop_ld=0):
     d = Dropout()
     d.threshold = dropout_threshold(p)
-    d.scale = 1.0 / (1.0 - p) if p > 0 else 1.0
+    d.scale = dropout_scale(p)
     d.seed, d.site, d.row_offset, d.col_offset, d.drop_ld = seed, site, row_offset, col_offset, drop_ld
     return d
 
@@ -104,22 +109,32 @@ def _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, heads_total=None
     a.scale = head_dim ** -0.5
     a.qkv, a.ld_qkv = _ptr(qkv), qkv.stride(0)
     a.drop_threshold = dropout_threshold(p)
-    a.drop_scale = 1.0 / (1.0 - p) if p > 0 else 1.0
+    a.drop_scale = dropout_scale(p)
     a.seed, a.site = seed, site
     return a
 
 
-def attention_fwd(qkv, batch, seq, heads, head_dim, p=0.0, seed=0, site=0, **kw):
+def attention_mask_buffer(batch, seq, heads, device):
+    import torch
+    return torch.zeros(batch * heads * seq * ((seq + 63) // 64) * 4, device=device,
+                       dtype=torch.int16)
+
+
+def attention_fwd(qkv, batch, seq, heads, head_dim, p=0.0, seed=0, site=0, mask=None, **kw):
+    """Returns (ctx, lse, mask); mask (keep bits) feeds attention_bwd when p > 0."""
     import torch
     ctx = torch.empty(batch * seq, heads * head_dim, device=qkv.device, dtype=torch.bfloat16)
     lse = torch.empty(batch * heads, seq, device=qkv.device, dtype=torch.float32)
+    if mask is None:
+        mask = attention_mask_buffer(batch, seq, heads, qkv.device)
     a = _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, **kw)
-    a.ctx, a.ld_ctx, a.lse = _ptr(ctx), ctx.stride(0), _ptr(lse)
+    a.ctx, a.ld_ctx, a.lse, a.mask = _ptr(ctx), ctx.stride(0), _ptr(lse), _ptr(mask)
     _lib.check(_lib.lib().gx_k_attention_fwd(ctypes.addressof(a), _lib.stream_ptr()))
-    return ctx, lse
+    return ctx, lse, mask
 
 
-def attention_bwd(qkv, ctx, lse, dctx, batch, seq, heads, head_dim, p=0.0, seed=0, site=0, **kw):
+def attention_bwd(qkv, ctx, lse, dctx, batch, seq, heads, head_dim, p=0.0, seed=0, site=0,
+                  mask=None, **kw):
     import torch
     dqkv = torch.zeros_like(qkv)
     dq_acc = torch.empty(batch * heads * seq * head_dim, device=qkv.device, dtype=torch.float32)
@@ -127,6 +142,7 @@ def attention_bwd(qkv, ctx, lse, dctx, batch, seq, heads, head_dim, p=0.0, seed=
     a = _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, **kw)
     a.ctx, a.ld_ctx, a.lse = _ptr(ctx), ctx.stride(0), _ptr(lse)
     a.dctx, a.dqkv, a.dq_accum, a.dsum = _ptr(dctx), _ptr(dqkv), _ptr(dq_acc), _ptr(dsum)
+    a.mask = _ptr(mask)
     _lib.check(_lib.lib().gx_k_attention_bwd(ctypes.addressof(a), _lib.stream_ptr()))
     return dqkv
 

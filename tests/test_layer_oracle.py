@@ -29,9 +29,12 @@ def test_philox_known_answers():
 
 
 def test_dropout_rate():
-    idx = np.arange(200_000, dtype=np.uint64)
+    idx = np.arange(400_000, dtype=np.uint64)
     keep = lo.keep_mask(1234, 7, idx, 0.1)
-    assert abs(1.0 - keep.mean() - 0.1) < 0.005
+    assert lo.dropout_threshold(0.1) == 26
+    assert abs(1.0 - keep.mean() - 26 / 256) < 0.003
+    m = lo._attn_mask(lo.Dropout(0.1, 0.0, 5), 0, 2, 3, 200, 1)
+    assert abs(1.0 - m.mean() - 26 / 256) < 0.005
 
 
 def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0):
@@ -43,9 +46,9 @@ def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0):
     q, k, v = (qkv[:, i * h:(i + 1) * h].reshape(n, s, H, d).transpose(1, 2) for i in range(3))
     pr = torch.softmax(q @ k.transpose(-1, -2) / math.sqrt(d), -1)
     am = torch.from_numpy(lo._attn_mask(drop, 3 * layer_id, n, H, s, sample_offset)).double()
-    ka = 1.0 / (1.0 - drop.p_attn) if drop.p_attn > 0 else 1.0
+    ka = lo.dropout_scale(drop.p_attn)
     ctx = (pr * am * ka @ v).transpose(1, 2).reshape(n * s, h)
-    kh = 1.0 / (1.0 - drop.p_hidden) if drop.p_hidden > 0 else 1.0
+    kh = lo.dropout_scale(drop.p_hidden)
     m1 = torch.from_numpy(lo._hidden_mask(drop, 3 * layer_id + 1, n * s, h, sample_offset * s)).double()
     x1 = x + (ctx @ P["w_o"].T + P["b_o"]) * m1 * kh
     c = ln(x1, P["ln2_g"], P["ln2_b"])
