@@ -253,6 +253,13 @@ GX_API int gx_k_adamw(void* master, const void* grad, void* m, void* v, void* bf
 /* fp32 -> bf16 */
 GX_API int gx_k_cast_bf16(const void* src, void* dst, int64_t n, void* stream);
 
+/* Split-K GEMM: out_f32[M,N] += A * B^T, each of `splits` K-slices reduce-adding its fp32
+ * partial via TMA (caller zeroes out_f32 for a plain product).  splits <= 0 picks the plan
+ * the executor uses (CTA-pair 256-wide tiles, one wave).  tile_n as in gx_k_gemm_bf16. */
+GX_API int gx_k_gemm_bf16_splitk(const void* a, int64_t lda, int a_mn_major, const void* b,
+                                 int64_t ldb, int b_mn_major, int M, int N, int K, void* out_f32,
+                                 int64_t ldo, int splits, int tile_n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

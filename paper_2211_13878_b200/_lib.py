@@ -62,6 +62,9 @@ def _declare(L: ctypes.CDLL) -> None:
     L.gx_k_gemm_bf16.argtypes = [c_void_p, c_int64, c_int, c_void_p, c_int64, c_int, c_int,
                                  c_int, c_int, POINTER(GemmEpilogue), c_int, c_void_p]
     L.gx_k_gemm_bf16.restype = c_int
+    L.gx_k_gemm_bf16_splitk.argtypes = [c_void_p, c_int64, c_int, c_void_p, c_int64, c_int, c_int,
+                                        c_int, c_int, c_void_p, c_int64, c_int, c_int, c_void_p]
+    L.gx_k_gemm_bf16_splitk.restype = c_int
     for name in ("gx_k_attention_fwd", "gx_k_attention_bwd", "gx_k_layernorm_fwd",
                  "gx_k_layernorm_bwd", "gx_k_bias_dropout_add", "gx_k_dropout_bwd_colsum",
                  "gx_k_colsum", "gx_k_mse_loss", "gx_k_adamw", "gx_k_cast_bf16"):

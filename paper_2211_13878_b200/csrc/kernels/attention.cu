@@ -21,6 +21,7 @@
 #include <cstdint>
 
 #include "gx_internal.h"
+#include "launch.cuh"
 #include "philox.cuh"
 
 namespace gx {
@@ -85,6 +86,7 @@ __device__ __forceinline__ void load_tile(__nv_bfloat16* dst, const __nv_bfloat1
 // --------------------------------------------------------------------------- forward
 template <int HD>
 __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_args p) {
+  pdl_enter();
   constexpr int LDS = HD + 8;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
@@ -258,6 +260,7 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_a
 // D[bh][q] = sum_d dctx*ctx ; zero the fp32 dQ accumulator.
 template <int HD>
 __global__ void attn_bwd_prep_kernel(const gx_attention_args p) {
+  pdl_enter();
   const int s = p.seq, H = p.heads;
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -280,6 +283,7 @@ __global__ void attn_bwd_prep_kernel(const gx_attention_args p) {
 // --------------------------------------------------------------------------- backward
 template <int HD>
 __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_args p) {
+  pdl_enter();
   constexpr int LDS = HD + 8;
   constexpr int LDP = kBlk + 8;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -317,7 +321,6 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
   const float c2 = p.scale * 1.4426950408889634f;
   const uint32_t thr = p.drop_threshold;
   const float inv_keep = p.drop_scale;
-  const uint64_t seed = p.seed + (p.seed_offset != nullptr ? *p.seed_offset : 0ull);
   const int nkb = (s + kBlk - 1) / kBlk;
   const int kbi = blockIdx.x;
   const uint16_t* mask = static_cast<const uint16_t*>(p.mask);
@@ -484,6 +487,7 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
 // dq (fp32, [bh][s][HD]) * scale -> bf16 Q slot of dqkv
 template <int HD>
 __global__ void attn_bwd_dq_kernel(const gx_attention_args p) {
+  pdl_enter();
   const int s = p.seq, H = p.heads;
   const int64_t total = static_cast<int64_t>(p.batch) * H * s * (HD / 2);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
@@ -512,7 +516,7 @@ static int attention_fwd_impl(const gx_attention_args& a, cudaStream_t st) {
     set = true;
   }
   dim3 grid((a.seq + kBlk - 1) / kBlk, a.batch * a.heads);
-  attn_fwd_kernel<HD><<<grid, kThreads, smem, st>>>(a);
+  launch_k(attn_fwd_kernel<HD>, grid, dim3(kThreads), smem, st, a);
   return check_launch("attn_fwd_kernel");
 }
 
@@ -526,15 +530,15 @@ static int attention_bwd_impl(const gx_attention_args& a, cudaStream_t st) {
     set = true;
   }
   const int rows = a.batch * a.heads * a.seq;
-  attn_bwd_prep_kernel<HD><<<(rows + 7) / 8, 256, 0, st>>>(a);
+  launch_k(attn_bwd_prep_kernel<HD>, dim3((rows + 7) / 8), dim3(256), 0, st, a);
   if (int rc = check_launch("attn_bwd_prep_kernel")) return rc;
   dim3 grid((a.seq + kBlk - 1) / kBlk, a.batch * a.heads);
-  attn_bwd_kernel<HD><<<grid, kThreads, smem, st>>>(a);
+  launch_k(attn_bwd_kernel<HD>, grid, dim3(kThreads), smem, st, a);
   if (int rc = check_launch("attn_bwd_kernel")) return rc;
   const int64_t work = static_cast<int64_t>(rows) * (HD / 2);
   int blocks = static_cast<int>((work + 255) / 256);
   if (blocks > 148 * 16) blocks = 148 * 16;
-  attn_bwd_dq_kernel<HD><<<blocks, 256, 0, st>>>(a);
+  launch_k(attn_bwd_dq_kernel<HD>, dim3(blocks), dim3(256), 0, st, a);
   return check_launch("attn_bwd_dq_kernel");
 }
 

@@ -14,6 +14,23 @@ namespace {
 cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 }  // namespace
 
+extern "C" int gx_k_gemm_bf16_splitk(const void* a, int64_t lda, int a_mn_major, const void* b,
+                                     int64_t ldb, int b_mn_major, int M, int N, int K,
+                                     void* out_f32, int64_t ldo, int splits, int tile_n,
+                                     void* stream) {
+  gx_gemm_epilogue ep{};
+  ep.out_kind = GX_OUT_F32_ACC;
+  ep.out = out_f32;
+  ep.ldo = ldo;
+  ep.alpha = 1.f;
+  ep.drop_scale = 1.f;
+  int tile = tile_n;
+  if (splits <= 0) splits = gx::splitk_plan(M, N, K, &tile);
+  gx::GemmOperand A{a, lda, a_mn_major != 0};
+  gx::GemmOperand B{b, ldb, b_mn_major != 0};
+  return gx::gemm_bf16(A, B, M, N, K, ep, S(stream), tile, splits);
+}
+
 extern "C" int gx_k_attention_fwd(const gx_attention_args* a, void* stream) {
   if (a == nullptr) return gx::set_error(gx::kErrConfig, "attention: args NULL");
   return gx::attention_fwd(*a, S(stream));
@@ -29,7 +46,18 @@ extern "C" int gx_k_layernorm_fwd(const void* x, const void* gamma, const void* 
 extern "C" int gx_k_layernorm_bwd(const void* dy, const void* x, const void* mean,
                                   const void* rstd, const void* gamma, const void* dres, void* dx,
                                   void* dgamma, void* dbeta, int rows, int h, void* stream) {
-  return gx::layernorm_bwd(dy, x, mean, rstd, gamma, dres, dx, dgamma, dbeta, rows, h, S(stream));
+  // standalone entry point: grow-only workspace owned here (the executor passes its own)
+  static float* ws = nullptr;
+  static size_t ws_floats = 0;
+  const size_t need = static_cast<size_t>(gx::layernorm_bwd_blocks(rows)) * 2 * h;
+  if (need > ws_floats) {
+    if (ws != nullptr) cudaFree(ws);
+    if (cudaMalloc(&ws, need * sizeof(float)) != cudaSuccess)
+      return gx::set_error(gx::kErrCuda, "layernorm_bwd: workspace allocation failed");
+    ws_floats = need;
+  }
+  return gx::layernorm_bwd(dy, x, mean, rstd, gamma, dres, dx, dgamma, dbeta, rows, h, ws,
+                           S(stream));
 }
 extern "C" int gx_k_bias_dropout_add(const void* x, const void* bias, const void* residual,
                                      void* out, int rows, int cols, const gx_dropout* d,

@@ -18,9 +18,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdio>
 
 #include "gx_internal.h"
+#include "launch.cuh"
 #include "philox.cuh"
 #include "sm100.cuh"
 
@@ -29,15 +31,18 @@ namespace gx {
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 B = one swizzle span
 constexpr int kThreads = 256;
+constexpr int kStagingBytesDecl = 4 * 2 * (4096 + 2048);          // epilogue staging (below)
+constexpr int kSmemBudget = 227 * 1024 - kStagingBytesDecl - 2048;  // left for the A/B ring
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (kSmemBudget / kStageBytes) > 8 ? 8 : (kSmemBudget / kStageBytes);
   static constexpr int kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmemBytes =
+      kStages * kStageBytes + kStagingBytesDecl + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 __device__ __forceinline__ float gelu_erf(float x) {
@@ -49,21 +54,24 @@ __device__ __forceinline__ float gelu_erf_grad(float x) {
          x * 0.3989422804014327f * __expf(-0.5f * x * x);
 }
 
-// Applies the epilogue to 32 consecutive accumulator columns [n0, n0+32) of row `row`.
-__device__ __forceinline__ void epilogue_row32(const GemmEpilogue& ep, int64_t row, int n0,
-                                               int N, const uint32_t (&acc)[32]) {
-  float v[32];
+// Epilogue math for 32 consecutive accumulator columns [n0, n0+32) of row `row`: v <- final
+// values, pre <- bf16-rounded pre-activation (GeLU forward).  Operand reads are guarded for
+// rows >= M / columns >= N; the TMA store clips those elements.
+__device__ __forceinline__ void epilogue_math(const GemmEpilogue& ep, int64_t row, bool row_ok,
+                                              int n0, int N, const uint32_t (&acc)[32],
+                                              float (&v)[32], float (&pre)[32]) {
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(acc[j]) * ep.alpha;
-  const bool full = n0 + 32 <= N;
+  const bool full = row_ok && n0 + 32 <= N;
   const __nv_bfloat16* bias = static_cast<const __nv_bfloat16*>(ep.bias);
   const __nv_bfloat16* residual = static_cast<const __nv_bfloat16*>(ep.residual);
-  if (bias != nullptr) {
-    if (full) {
-      const uint4* bp = reinterpret_cast<const uint4*>(bias + n0);
+  auto add_bf16x32 = [&](const __nv_bfloat16* src, bool ok_full, float scale_dummy) {
+    (void)scale_dummy;
+    if (ok_full) {
+      const uint4* sp = reinterpret_cast<const uint4*>(src);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint4 b = __ldg(bp + q);
+        const uint4 b = sp[q];
         const uint32_t w[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -71,11 +79,12 @@ __device__ __forceinline__ void epilogue_row32(const GemmEpilogue& ep, int64_t r
           v[q * 8 + 2 * t + 1] += bf16_hi(w[t]);
         }
       }
-    } else {
+    } else if (row_ok) {
       for (int j = 0; j < 32; ++j)
-        if (n0 + j < N) v[j] += __bfloat162float(bias[n0 + j]);
+        if (n0 + j < N) v[j] += __bfloat162float(src[j]);
     }
-  }
+  };
+  if (bias != nullptr) add_bf16x32(bias + n0, n0 + 32 <= N, 0.f);
   if (ep.gelu_bwd) {
     // dgrad epilogue of the MLP up-projection: v <- v * gelu'(pre)
     const __nv_bfloat16* auxp = static_cast<const __nv_bfloat16*>(ep.aux) + row * ep.ld_aux + n0;
@@ -91,34 +100,17 @@ __device__ __forceinline__ void epilogue_row32(const GemmEpilogue& ep, int64_t r
           v[q * 8 + 2 * t + 1] *= gelu_erf_grad(bf16_hi(w[t]));
         }
       }
-    } else {
+    } else if (row_ok) {
       for (int j = 0; j < 32; ++j)
         if (n0 + j < N) v[j] *= gelu_erf_grad(__bfloat162float(auxp[j]));
     }
   }
   if (ep.gelu) {
-    // aux <- pre-activation (needed by the GeLU backward), v <- gelu(v)
-    __nv_bfloat16* auxp = static_cast<__nv_bfloat16*>(ep.aux) + row * ep.ld_aux + n0;
-    if (full) {
-      uint4* ap = reinterpret_cast<uint4*>(auxp);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 o;
-        o.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-        o.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-        o.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-        o.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
-        ap[q] = o;
-      }
-    } else {
-      for (int j = 0; j < 32; ++j)
-        if (n0 + j < N) auxp[j] = __float2bfloat16_rn(v[j]);
-    }
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       // GeLU is applied to the bf16-rounded pre-activation so forward and backward agree.
-      const float pre = __bfloat162float(__float2bfloat16_rn(v[j]));
-      v[j] = gelu_erf(pre);
+      pre[j] = __bfloat162float(__float2bfloat16_rn(v[j]));
+      v[j] = gelu_erf(pre[j]);
     }
   }
   if (residual != nullptr) {
@@ -141,70 +133,126 @@ __device__ __forceinline__ void epilogue_row32(const GemmEpilogue& ep, int64_t r
     // dropout output rounded to bf16 before the add, matching the unfused path
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));
-    const __nv_bfloat16* rp = residual + row * ep.ld_res + n0;
-    if (full) {
-      const uint4* rq = reinterpret_cast<const uint4*>(rp);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 b = rq[q];
-        const uint32_t w[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          v[q * 8 + 2 * t] += bf16_lo(w[t]);
-          v[q * 8 + 2 * t + 1] += bf16_hi(w[t]);
-        }
-      }
-    } else {
-      for (int j = 0; j < 32; ++j)
-        if (n0 + j < N) v[j] += __bfloat162float(rp[j]);
-    }
+    add_bf16x32(residual + row * ep.ld_res + n0, full, 0.f);
   }
+}
+
+// ---------------------------------------------------------------- TMA-store epilogue
+// Each epilogue warp owns 32 rows; a 32 x 32 block of results is written to a swizzled
+// staging buffer (64 B rows + SWIZZLE_64B for bf16, 128 B rows + SWIZZLE_128B for fp32:
+// conflict-free st.shared.v4 with one row per lane) and leaves through one TMA bulk
+// store (or bulk reduce-add for fp32 accumulation).  Two buffers per warp alternate, so
+// the store of block i overlaps the math of block i+1.
+constexpr int kStageOutBytes = 4096;  // 32 x 32 fp32
+constexpr int kStageAuxBytes = 2048;  // 32 x 32 bf16
+constexpr int kStagingBytes = 4 * 2 * (kStageOutBytes + kStageAuxBytes);
+
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                             uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ void stage_bf16_row(uint32_t base, uint32_t r, const float (&v)[32]) {
+#pragma unroll
+  for (uint32_t c = 0; c < 4; ++c) {
+    const uint32_t addr = base + r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
+    st_shared_v4(addr, pack_bf16(v[c * 8 + 0], v[c * 8 + 1]), pack_bf16(v[c * 8 + 2], v[c * 8 + 3]),
+                 pack_bf16(v[c * 8 + 4], v[c * 8 + 5]), pack_bf16(v[c * 8 + 6], v[c * 8 + 7]));
+  }
+}
+__device__ __forceinline__ void stage_f32_row(uint32_t base, uint32_t r, const float (&v)[32]) {
+#pragma unroll
+  for (uint32_t c = 0; c < 8; ++c) {
+    const uint32_t addr = base + r * 128 + ((c ^ (r & 7)) << 4);
+    st_shared_v4(addr, __float_as_uint(v[c * 4 + 0]), __float_as_uint(v[c * 4 + 1]),
+                 __float_as_uint(v[c * 4 + 2]), __float_as_uint(v[c * 4 + 3]));
+  }
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int32_t c0,
+                                             int32_t c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32_t src, int32_t c0,
+                                                  int32_t c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// One 32 x 32 output block: math, staging, TMA store.  Executed by a whole epilogue warp.
+__device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUtensorMap* map_out,
+                                               const CUtensorMap* map_aux, uint8_t* staging,
+                                               int q, uint32_t& block_ctr, int64_t m_base,
+                                               int n0, int M, int N, const uint32_t (&acc)[32]) {
+  const uint32_t lane = lane_id();
+  const int64_t row = m_base + lane;
+  float v[32], pre[32];
+  epilogue_math(ep, row, row < M, n0, N, acc, v, pre);
+  const uint32_t b = block_ctr & 1u;
+  ++block_ctr;
+  const uint32_t out_buf = smem_u32(staging) + (q * 2 + b) * (kStageOutBytes + kStageAuxBytes);
+  const uint32_t aux_buf = out_buf + kStageOutBytes;
+  if (lane == 0) bulk_wait_read1();  // the store that last used this buffer has read it
+  __syncwarp();
   if (ep.out_kind == kOutBF16) {
-    __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(ep.out) + row * ep.ldo + n0;
-    if (full) {
-      uint4* oq = reinterpret_cast<uint4*>(op);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 o;
-        o.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-        o.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-        o.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-        o.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
-        oq[q] = o;
-      }
-    } else {
-      for (int j = 0; j < 32; ++j)
-        if (n0 + j < N) op[j] = __float2bfloat16_rn(v[j]);
-    }
+    stage_bf16_row(out_buf, lane, v);
   } else {
-    float* op = reinterpret_cast<float*>(ep.out) + row * ep.ldo + n0;
-    const bool acc_mode = ep.out_kind == kOutF32Accumulate;
-    if (full) {
-      float4* oq = reinterpret_cast<float4*>(op);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float4 o = make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
-        if (acc_mode) {
-          const float4 p = oq[q];
-          o.x += p.x;
-          o.y += p.y;
-          o.z += p.z;
-          o.w += p.w;
-        }
-        oq[q] = o;
-      }
+    stage_f32_row(out_buf, lane, v);
+  }
+  if (ep.gelu) stage_bf16_row(aux_buf, lane, pre);
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    if (ep.out_kind == kOutF32Accumulate) {
+      tma_reduce_add_2d(map_out, out_buf, n0, static_cast<int32_t>(m_base));
     } else {
-      for (int j = 0; j < 32; ++j)
-        if (n0 + j < N) op[j] = acc_mode ? op[j] + v[j] : v[j];
+      tma_store_2d(map_out, out_buf, n0, static_cast<int32_t>(m_base));
     }
+    if (ep.gelu) tma_store_2d(map_aux, aux_buf, n0, static_cast<int32_t>(m_base));
+    bulk_commit();
+  }
+}
+
+
+// All BN/32 chunks of one accumulator tile for one epilogue warp.  (A ping-pong variant
+// that keeps the next chunk's TMEM load in flight measured slower: the extra 32 live
+// registers cost more than the hidden LDTM latency.)
+template <int BN>
+__device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const CUtensorMap* map_out,
+                                              const CUtensorMap* map_aux, uint8_t* staging, int q,
+                                              uint32_t& block_ctr, uint32_t taddr, int64_t m_base,
+                                              int n0, int M, int N) {
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+    tmem_ld_wait();
+    if (m_base < M && n0 + c * 32 < N)
+      epilogue_block(ep, map_out, map_aux, staging, q, block_ctr, m_base, n0 + c * 32, M, N, r);
   }
 }
 
 template <int BN, bool kAMN, bool kBMN>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap map_a,
-                        const __grid_constant__ CUtensorMap map_b, int M, int N, int K,
-                        const GemmEpilogue ep) {
+                        const __grid_constant__ CUtensorMap map_b,
+                        const __grid_constant__ CUtensorMap map_out,
+                        const __grid_constant__ CUtensorMap map_aux, int M, int N, int K,
+                        int splits, const GemmEpilogue ep) {
   using Cfg = GemmCfg<BN>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
@@ -212,7 +260,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint8_t* staging = smem + S * Cfg::kStageBytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(staging + kStagingBytes);
   uint64_t* empty_bar = full_bar + S;
   uint64_t* tfull_bar = empty_bar + S;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -222,7 +271,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int num_m = (M + kBM - 1) / kBM;
   const int num_n = (N + BN - 1) / BN;
   const int num_tiles = num_m * num_n;
-  const int num_kb = (K + kBK - 1) / kBK;
+  const int num_units = num_tiles * splits;  // split-K: unit = (split, tile)
+  const int kb_total = (K + kBK - 1) / kBK;
+  const int kb_per = (kb_total + splits - 1) / splits;
 
   if (warp == 0 && elect_one()) {
     tma_prefetch(&map_a);
@@ -242,13 +293,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_enter();  // everything above overlapped the previous kernel's tail
 
   if (warp == 0) {
     if (elect_one()) {
       // ------------------------------------------------------------ TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x) {
+        const int tile = unit % num_tiles;
+        const int kb0 = (unit / num_tiles) * kb_per;
+        const int num_kb = min(kb_per, kb_total - kb0);
         const int m0 = (tile % num_m) * kBM;
         const int n0 = (tile / num_m) * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -256,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(&full_bar[stage], Cfg::kStageBytes);
           uint8_t* a_dst = sA + stage * Cfg::kABytes;
           uint8_t* b_dst = sB + stage * Cfg::kBBytes;
-          const int k0 = kb * kBK;
+          const int k0 = (kb0 + kb) * kBK;
           if constexpr (!kAMN) {
             tma_load_2d(a_dst, &map_a, &full_bar[stage], k0, m0);
           } else {
@@ -284,7 +339,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+    for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++local) {
+      const int num_kb = min(kb_per, kb_total - (unit / num_tiles) * kb_per);
       const int buf = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       mbar_wait(&tempty_bar[buf], acc_phase ^ 1);
@@ -317,33 +373,215 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
+    uint32_t block_ctr = 0;
     int local = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+    for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++local) {
+      const int tile = unit % num_tiles;
       const int buf = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
       const int m0 = (tile % num_m) * kBM;
       const int n0 = (tile / num_m) * BN;
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
-      const int64_t row = m0 + q * 32 + static_cast<int>(lane_id());
-      const bool row_ok = row < M;
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN + c * 32, r);
-        tmem_ld_wait();
-        const int col = n0 + c * 32;
-        if (row_ok && col < N) epilogue_row32(ep, row, col, N, r);
-      }
+      const int64_t m_base = m0 + q * 32;
+      epilogue_tile<BN>(ep, &map_out, &map_aux, staging, q, block_ctr,
+                        tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base, n0,
+                        M, N);
       tc_fence_before();
       mbar_arrive(&tempty_bar[buf]);
     }
+    if (lane_id() == 0) bulk_wait_all();
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<Cfg::kTmemCols>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ CTA-pair variant
+// cta_group::2: a cluster of 2 CTAs on one TPC computes a 256 x BN tile.  Each CTA stages
+// its own 128 rows of A and HALF of the BN columns of B (so each SM receives 2x fewer B
+// bytes per MAC than the 1-CTA kernel), the leader's elected thread issues
+// tcgen05.mma.cta_group::2 (M = 256) reading both CTAs' smem, and each CTA's TMEM holds the
+// accumulator rows of its own half.  TMA completions of both CTAs land on the leader's
+// full barrier; the leader's MMA commits multicast to both CTAs' empty / tmem-full
+// barriers; epilogue warps of both CTAs release the accumulator on the leader's barrier.
+template <int BN>
+struct PairCfg {
+  static constexpr int kABytes = 128 * kBK * 2;        // this CTA's 128 rows of A
+  static constexpr int kBBytes = (BN / 2) * kBK * 2;   // this CTA's half of B
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = kSmemBudget / kStageBytes > 8 ? 8 : kSmemBudget / kStageBytes;
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kStagingBytesDecl + 1024 + 256;
+};
+
+template <int BN, bool kAMN, bool kBMN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
+                     const __grid_constant__ CUtensorMap map_b,
+                     const __grid_constant__ CUtensorMap map_out,
+                     const __grid_constant__ CUtensorMap map_aux, int M, int N, int K,
+                     int splits, const GemmEpilogue ep) {
+  using Cfg = PairCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  uint8_t* staging = smem + S * Cfg::kStageBytes;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(staging + kStagingBytes);
+  uint64_t* empty_bar = full_bar + S;
+  uint64_t* tfull_bar = empty_bar + S;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = static_cast<int>(warp_id());
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1;
+  const int num_pairs = gridDim.x >> 1;
+  const int num_pm = (M + 255) / 256;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_pm * num_n;
+  const int num_units = num_tiles * splits;
+  const int kb_total = (K + kBK - 1) / kBK;
+  const int kb_per = (kb_total + splits - 1) / splits;
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full_bar[s], 1);   // leader: its arrive.expect_tx (+ both CTAs' tx bytes)
+      mbar_init(&empty_bar[s], 1);  // the leader's multicast MMA commit
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);  // the leader's multicast MMA commit
+      mbar_init(&tempty_bar[b], 8); // 4 epilogue warps x 2 CTAs (leader copy is used)
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_enter();  // everything above overlapped the previous kernel's tail
+
+  if (warp == 0) {
+    if (elect_one()) {
+      // -------------------------------------------------------- TMA producer (both CTAs)
+      const uint32_t leader_full0 = mapa_shared(smem_u32(&full_bar[0]), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int unit = pair; unit < num_units; unit += num_pairs) {
+        const int tile = unit % num_tiles;
+        const int kb0 = (unit / num_tiles) * kb_per;
+        const int num_kb = min(kb_per, kb_total - kb0);
+        const int m0 = (tile % num_pm) * 256 + static_cast<int>(rank) * 128;
+        const int nb0 = (tile / num_pm) * BN + static_cast<int>(rank) * (BN / 2);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&full_bar[stage], 2 * Cfg::kStageBytes);
+          const uint32_t fb = leader_full0 + stage * 8;
+          uint8_t* a_dst = sA + stage * Cfg::kABytes;
+          uint8_t* b_dst = sB + stage * Cfg::kBBytes;
+          const int k0 = (kb0 + kb) * kBK;
+          if constexpr (!kAMN) {
+            tma_load_2d_pair(a_dst, &map_a, fb, k0, m0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+              tma_load_2d_pair(a_dst + c * kBK * 128, &map_a, fb, m0 + c * 64, k0);
+          }
+          if constexpr (!kBMN) {
+            tma_load_2d_pair(b_dst, &map_b, fb, k0, nb0);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN / 128; ++c)
+              tma_load_2d_pair(b_dst + c * kBK * 128, &map_b, fb, nb0 + c * 64, k0);
+          }
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // ------------------------------------------------------------ MMA issuer (leader)
+      constexpr uint32_t idesc = idesc_bf16_f32(256, BN, kAMN, kBMN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int unit = pair; unit < num_units; unit += num_pairs, ++local) {
+        const int num_kb = min(kb_per, kb_total - (unit / num_tiles) * kb_per);
+        const int buf = local & 1;
+        const uint32_t acc_phase = (local >> 1) & 1;
+        mbar_wait_cluster(&tempty_bar[buf], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + buf * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a_base = smem_u32(sA + stage * Cfg::kABytes);
+            const uint32_t b_base = smem_u32(sB + stage * Cfg::kBBytes);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t adesc = kAMN ? sdesc_sw128(a_base + k * 2048, kBK * 128, 1024)
+                                          : sdesc_sw128(a_base + k * 32, 16, 1024);
+              const uint64_t bdesc = kBMN ? sdesc_sw128(b_base + k * 2048, kBK * 128, 1024)
+                                          : sdesc_sw128(b_base + k * 32, 16, 1024);
+              umma_bf16_pair(d_tmem, adesc, bdesc, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
+            umma_commit_pair(&empty_bar[stage], 0x3);
+            if (kb == num_kb - 1) umma_commit_pair(&tfull_bar[buf], 0x3);
+          }
+          __syncwarp();
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int q = warp & 3;
+    const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
+    uint32_t block_ctr = 0;
+    int local = 0;
+    for (int unit = pair; unit < num_units; unit += num_pairs, ++local) {
+      const int tile = unit % num_tiles;
+      const int buf = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      const int m0 = (tile % num_pm) * 256 + static_cast<int>(rank) * 128;
+      const int n0 = (tile / num_pm) * BN;
+      mbar_wait(&tfull_bar[buf], acc_phase);
+      tc_fence_after();
+      const int64_t m_base = m0 + q * 32;
+      epilogue_tile<BN>(ep, &map_out, &map_aux, staging, q, block_ctr,
+                        tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base, n0,
+                        M, N);
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive_remote(leader_tempty0 + buf * 8);
+    }
+    if (lane_id() == 0) bulk_wait_all();
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);
   }
 }
 
@@ -362,6 +600,31 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   }
   return fn;
+}
+
+// Epilogue store map: 32 x 32 boxes over the [M][ld] output; bf16 uses 64 B swizzle,
+// fp32 128 B (matching the staging layout in epilogue_block).
+static bool make_out_map(CUtensorMap* map, const void* ptr, uint64_t cols, uint64_t rows,
+                         uint64_t ld, bool f32) {
+  auto fn = encode_fn();
+  if (fn == nullptr || ptr == nullptr) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * (f32 ? 4 : 2)};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static bool make_epi_maps(const GemmEpilogue& ep, int M, int N, CUtensorMap* mo, CUtensorMap* mx) {
+  const bool f32 = ep.out_kind != kOutBF16;
+  if (!make_out_map(mo, ep.out, N, M, ep.ldo, f32)) return false;
+  if (ep.gelu) return make_out_map(mx, ep.aux, N, M, ep.ld_aux, false);
+  *mx = *mo;
+  return true;
 }
 
 // 2-D bf16 map over a row-major [outer][inner] view with row stride `ld` elements,
@@ -394,12 +657,14 @@ int num_sms() {
 
 template <int BN, bool kAMN, bool kBMN>
 static int launch_gemm(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
-                       const GemmEpilogue& ep, cudaStream_t stream) {
+                       const GemmEpilogue& ep, cudaStream_t stream, int splits) {
   using Cfg = GemmCfg<BN>;
   CUtensorMap ma, mb;
   // A: K-major view [M][K] (inner K); MN-major view [K][M] (inner M)
   bool ok = kAMN ? make_map(&ma, a.ptr, M, K, a.ld, kBK) : make_map(&ma, a.ptr, K, M, a.ld, kBM);
   ok = ok && (kBMN ? make_map(&mb, b.ptr, N, K, b.ld, kBK) : make_map(&mb, b.ptr, K, N, b.ld, BN));
+  CUtensorMap mo, mx;
+  ok = ok && make_epi_maps(ep, M, N, &mo, &mx);
   if (!ok) return set_error(kErrCuda, "gemm: cuTensorMapEncodeTiled failed");
   static bool attr_set = false;
   if (!attr_set) {
@@ -407,14 +672,59 @@ static int launch_gemm(const GemmOperand& a, const GemmOperand& b, int M, int N,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     attr_set = true;
   }
-  const int tiles = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_tcgen05_kernel<BN, kAMN, kBMN>
-      <<<grid, kThreads, Cfg::kSmemBytes, stream>>>(ma, mb, M, N, K, ep);
+  const int units = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * splits;
+  const int grid = units < num_sms() ? units : num_sms();
+  launch_k(gemm_tcgen05_kernel<BN, kAMN, kBMN>, dim3(grid), dim3(kThreads), Cfg::kSmemBytes,
+           stream, ma, mb, mo, mx, M, N, K, splits, ep);
   return check_launch("gemm_tcgen05_kernel");
 }
 
+template <int BN, bool kAMN, bool kBMN>
+static int launch_gemm_pair(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
+                            const GemmEpilogue& ep, cudaStream_t stream, int splits) {
+  using Cfg = PairCfg<BN>;
+  CUtensorMap ma, mb;
+  // each CTA loads 128 rows of A and BN/2 rows (K-major) / columns (MN-major) of B
+  bool ok = kAMN ? make_map(&ma, a.ptr, M, K, a.ld, kBK) : make_map(&ma, a.ptr, K, M, a.ld, 128);
+  ok = ok && (kBMN ? make_map(&mb, b.ptr, N, K, b.ld, kBK)
+                   : make_map(&mb, b.ptr, K, N, b.ld, BN / 2));
+  CUtensorMap mo, mx;
+  ok = ok && make_epi_maps(ep, M, N, &mo, &mx);
+  if (!ok) return set_error(kErrCuda, "gemm: cuTensorMapEncodeTiled failed");
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_pair_kernel<BN, kAMN, kBMN>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
+    attr_set = true;
+  }
+  const int units = ((M + 255) / 256) * ((N + BN - 1) / BN) * splits;
+  const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
+  launch_k(gemm_pair_kernel<BN, kAMN, kBMN>, dim3(2 * pairs), dim3(kThreads), Cfg::kSmemBytes,
+           stream, ma, mb, mo, mx, M, N, K, splits, ep);
+  return check_launch("gemm_pair_kernel");
+}
+
 // Picks the N tile that minimises the number of waves (ties -> larger tile).
+static int pick_bn(int M, int N);
+// Tile choice: CTA-pair (negative) when M >= 256, else the 1-CTA kernel.
+static int pick_tile(int M, int N) {
+  if (M < 256) return pick_bn(M, N);
+  const int pairs = num_sms() / 2;
+  int best = -256;
+  double best_cost = 1e30;
+  for (int bn : {256, 128}) {
+    if (bn == 256 && N <= 128) continue;
+    const int tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
+    const int waves = (tiles + pairs - 1) / pairs;
+    const double cost = waves * (bn + 48.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = -bn;
+    }
+  }
+  return best;
+}
+
 static int pick_bn(int M, int N) {
   const int sms = num_sms();
   const int cands[3] = {256, 128, 64};
@@ -434,25 +744,59 @@ static int pick_bn(int M, int N) {
   return best;
 }
 
+// Split-K plan for a reduce-add GEMM: the CTA-pair 256-wide tile when M allows, and as many
+// K splits as fit one wave of pairs while keeping >= 4 k-blocks per split.  Returns the
+// split count and sets *tile (the force_bn argument of gemm_bf16).
+int splitk_plan(int M, int N, int K, int* tile) {
+  const int kb = (K + kBK - 1) / kBK;
+  if (M >= 256) {
+    const int bn = N > 128 ? 256 : 128;
+    *tile = -bn;
+    const int tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
+    int sp = (num_sms() / 2) / tiles;
+    sp = std::min(sp, kb / 4);
+    return std::max(1, std::min(sp, 16));
+  }
+  *tile = 128;
+  const int tiles = ((M + kBM - 1) / kBM) * ((N + 127) / 128);
+  int sp = num_sms() / tiles;
+  sp = std::min(sp, kb / 4);
+  return std::max(1, std::min(sp, 16));
+}
+
 int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
-              const GemmEpilogue& ep, cudaStream_t stream, int force_bn) {
+              const GemmEpilogue& ep, cudaStream_t stream, int force_bn, int splits) {
+  if (splits < 1) splits = 1;
+  {  // every split must own >= 1 k-block (an empty split would never signal its epilogue)
+    const int kb_total = (K + kBK - 1) / kBK;
+    const int kb_per = (kb_total + splits - 1) / splits;
+    splits = (kb_total + kb_per - 1) / kb_per;
+  }
+  if (splits > 1 && (ep.out_kind != kOutF32Accumulate || ep.bias != nullptr || ep.gelu ||
+                     ep.gelu_bwd || ep.residual != nullptr || ep.alpha != 1.f))
+    return set_error(kErrConfig, "gemm: split-K needs a plain fp32 accumulate epilogue");
   if (M <= 0 || N <= 0 || K <= 0) return set_error(kErrConfig, "gemm: empty problem");
   // TMA: row strides must be 16-byte multiples; the epilogue's vector stores need ldo too.
-  if ((a.ld % 8) != 0 || (b.ld % 8) != 0 || (ep.ldo % 8) != 0)
-    return set_error(kErrConfig, "gemm: lda, ldb and ldo must be multiples of 8 elements");
+  if ((a.ld % 8) != 0 || (b.ld % 8) != 0 || (ep.ldo % 8) != 0 || (ep.gelu && ep.ld_aux % 8 != 0))
+    return set_error(kErrConfig, "gemm: lda, ldb, ldo and ld_aux must be multiples of 8 elements");
   if (ep.drop_threshold != 0u && ((ep.drop_ld % 16) != 0 || (ep.col_offset % 16) != 0))
     return set_error(kErrConfig, "gemm: dropout row length / column offset must be multiples of 16");
-  const int bn = force_bn > 0 ? force_bn : pick_bn(M, N);
-#define GX_GEMM_DISPATCH(BN_)                                                           \
-  if (bn == BN_) {                                                                      \
-    if (!a.mn_major && !b.mn_major) return launch_gemm<BN_, false, false>(a, b, M, N, K, ep, stream); \
-    if (!a.mn_major && b.mn_major) return launch_gemm<BN_, false, true>(a, b, M, N, K, ep, stream);   \
-    if (a.mn_major && b.mn_major) return launch_gemm<BN_, true, true>(a, b, M, N, K, ep, stream);     \
-    return launch_gemm<BN_, true, false>(a, b, M, N, K, ep, stream);                     \
+  // force_bn: >0 selects the 1-CTA kernel with that N tile, <0 the CTA-pair kernel with
+  // N tile -force_bn, 0 = automatic (pair kernel whenever M spans at least one 256-row tile).
+  int bn = force_bn;
+  if (bn == 0) bn = pick_tile(M, N);
+#define GX_GEMM_DISPATCH(BN_, LAUNCH)                                                        \
+  if (bn == BN_) {                                                                           \
+    if (!a.mn_major && !b.mn_major) return LAUNCH<BN_ < 0 ? -BN_ : BN_, false, false>(a, b, M, N, K, ep, stream, splits); \
+    if (!a.mn_major && b.mn_major) return LAUNCH<BN_ < 0 ? -BN_ : BN_, false, true>(a, b, M, N, K, ep, stream, splits);   \
+    if (a.mn_major && b.mn_major) return LAUNCH<BN_ < 0 ? -BN_ : BN_, true, true>(a, b, M, N, K, ep, stream, splits);     \
+    return LAUNCH<BN_ < 0 ? -BN_ : BN_, true, false>(a, b, M, N, K, ep, stream, splits);                 \
   }
-  GX_GEMM_DISPATCH(256)
-  GX_GEMM_DISPATCH(128)
-  GX_GEMM_DISPATCH(64)
+  GX_GEMM_DISPATCH(256, launch_gemm)
+  GX_GEMM_DISPATCH(128, launch_gemm)
+  GX_GEMM_DISPATCH(64, launch_gemm)
+  GX_GEMM_DISPATCH(-256, launch_gemm_pair)
+  GX_GEMM_DISPATCH(-128, launch_gemm_pair)
 #undef GX_GEMM_DISPATCH
   return set_error(kErrConfig, "gemm: unsupported N tile");
 }

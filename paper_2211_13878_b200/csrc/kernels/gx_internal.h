@@ -35,18 +35,23 @@ struct GemmOperand {
 
 using GemmEpilogue = gx_gemm_epilogue;
 
+// splits > 1: split-K, each split TMA-reduce-adds its fp32 partial into ep.out (caller
+// zeroes it); requires a plain kOutF32Accumulate epilogue.
 int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
-              const GemmEpilogue& ep, cudaStream_t stream, int force_bn = 0);
+              const GemmEpilogue& ep, cudaStream_t stream, int force_bn = 0, int splits = 1);
+int splitk_plan(int M, int N, int K, int* tile);
 
 int attention_fwd(const gx_attention_args& a, cudaStream_t st);
 int attention_bwd(const gx_attention_args& a, cudaStream_t st);
 int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, void* mean,
                   void* rstd, int rows, int h, cudaStream_t st);
+// workspace: fp32 [layernorm_bwd_blocks(rows)][2h] (block partials of dgamma / dbeta)
 int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
                   const void* gamma, const void* dres, void* dx, void* dgamma, void* dbeta,
-                  int rows, int h, cudaStream_t st);
+                  int rows, int h, float* workspace, cudaStream_t st, bool dy_f32 = false);
+int layernorm_bwd_blocks(int rows);
 int bias_dropout_add(const void* x, const void* bias, const void* residual, void* out, int rows,
-                     int cols, const gx_dropout& d, cudaStream_t st);
+                     int cols, const gx_dropout& d, cudaStream_t st, bool x_f32 = false);
 int dropout_bwd_colsum(const void* dy, void* dz, void* dbias, int rows, int cols,
                        const gx_dropout& d, cudaStream_t st);
 int colsum(const void* x, int64_t ld, void* acc, int rows, int cols, cudaStream_t st);
@@ -55,9 +60,10 @@ int mse_loss(const void* y, const void* target, void* dy, void* loss, int64_t n,
 int adamw(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n, float lr,
           float beta1, float beta2, float eps, float wd, float bc1, float bc2, cudaStream_t st);
 int cast_bf16(const void* src, void* dst, int64_t n, cudaStream_t st);
+// max_blocks > 0 caps the grid (the overlapped optimizer stream leaves SMs to the backward)
 int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n,
               float lr, float beta1, float beta2, float eps, float wd, const int64_t* step,
-              cudaStream_t st);
+              cudaStream_t st, int max_blocks = 0);
 int bump_step(int64_t* step, uint64_t* seed_offset, cudaStream_t st);
 struct PtrPack {
   const void* p[16];

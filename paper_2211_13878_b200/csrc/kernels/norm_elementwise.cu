@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "gx_internal.h"
+#include "launch.cuh"
 #include "philox.cuh"
 
 namespace gx {
@@ -16,6 +17,12 @@ namespace gx {
 namespace {
 
 constexpr float kLnEps = 1e-5f;
+
+#define GX_RC(expr)                 \
+  do {                              \
+    const int gx_rc_ = (expr);      \
+    if (gx_rc_ != kOk) return gx_rc_; \
+  } while (0)
 
 __device__ __forceinline__ float lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
@@ -27,6 +34,23 @@ __device__ __forceinline__ void unpack8(const uint4& u, float (&f)[8]) {
   f[0] = lo(u.x); f[1] = hi(u.x); f[2] = lo(u.y); f[3] = hi(u.y);
   f[4] = lo(u.z); f[5] = hi(u.z); f[6] = lo(u.w); f[7] = hi(u.w);
 }
+// 8 consecutive elements (chunk `i`) of a bf16 (kF32 = false) or fp32 row-major buffer
+template <bool kF32>
+__device__ __forceinline__ void load8(const void* base, int64_t i, float (&f)[8]) {
+  if constexpr (kF32) {
+    const float4* p = static_cast<const float4*>(base) + 2 * i;
+    const float4 a = p[0], b = p[1];
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  } else {
+    const uint4 u = static_cast<const uint4*>(base)[i];
+    f[0] = __uint_as_float(u.x << 16); f[1] = __uint_as_float(u.x & 0xFFFF0000u);
+    f[2] = __uint_as_float(u.y << 16); f[3] = __uint_as_float(u.y & 0xFFFF0000u);
+    f[4] = __uint_as_float(u.z << 16); f[5] = __uint_as_float(u.z & 0xFFFF0000u);
+    f[6] = __uint_as_float(u.w << 16); f[7] = __uint_as_float(u.w & 0xFFFF0000u);
+  }
+}
+
 __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   return make_uint4(pk(f[0], f[1]), pk(f[2], f[3]), pk(f[4], f[5]), pk(f[6], f[7]));
 }
@@ -71,6 +95,7 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const uint4* __restr
                                                            float* __restrict__ mean,
                                                            float* __restrict__ rstd, int rows,
                                                            int h) {
+  pdl_enter();
   const int chunks = h >> 3;
   const int lane = threadIdx.x & 31;
   const int warps_total = gridDim.x * (blockDim.x >> 5);
@@ -124,13 +149,16 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const uint4* __restr
 }
 
 // ---------------------------------------------------------------------- LayerNorm bwd
-// Block = 8 warps; dgamma/dbeta partials reduced in shared memory, one global atomic per
-// column per block.
-template <int NC>
+// Pass 1: one warp per row computes dx (+ residual gradient) and keeps per-lane dgamma /
+// dbeta partials in registers; each block reduces them in shared memory and writes one
+// [2][h] partial row to a workspace (no global atomics).  Pass 2 sums the block partials
+// column-parallel and accumulates into dgamma / dbeta.
+template <int NC, bool kF32Dy>
 __global__ void __launch_bounds__(256) layernorm_bwd_kernel(
-    const uint4* __restrict__ dy, const uint4* __restrict__ x, const float* __restrict__ mean,
+    const void* __restrict__ dy, const uint4* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, const uint4* __restrict__ gamma, const uint4* __restrict__ dres,
-    uint4* __restrict__ dx, float* __restrict__ dgamma, float* __restrict__ dbeta, int rows, int h) {
+    uint4* __restrict__ dx, float* __restrict__ partial, int rows, int h) {
+  pdl_enter();
   extern __shared__ float sred[];  // [2][h]
   const int chunks = h >> 3;
   const int lane = threadIdx.x & 31;
@@ -163,7 +191,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_kernel(
       if (ci < chunks) {
         float xv[8], dv[8];
         unpack8(x[static_cast<int64_t>(r) * chunks + ci], xv);
-        unpack8(dy[static_cast<int64_t>(r) * chunks + ci], dv);
+        load8<kF32Dy>(dy, static_cast<int64_t>(r) * chunks + ci, dv);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           xh[c][j] = (xv[j] - mu) * rs;
@@ -206,10 +234,28 @@ __global__ void __launch_bounds__(256) layernorm_bwd_kernel(
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < h; i += blockDim.x) {
-    atomicAdd(dgamma + i, sred[i]);
-    atomicAdd(dbeta + i, sred[h + i]);
+  float* out = partial + static_cast<int64_t>(blockIdx.x) * 2 * h;
+  for (int i = threadIdx.x; i < 2 * h; i += blockDim.x) out[i] = sred[i];
+}
+
+__global__ void layernorm_bwd_reduce_kernel(const float* __restrict__ partial, int blocks, int h,
+                                            float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  pdl_enter();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // 0 .. 2h
+  if (i >= 2 * h) return;
+  float acc = 0.f;
+  for (int b = 0; b < blocks; ++b) acc += partial[static_cast<int64_t>(b) * 2 * h + i];
+  if (i < h) {
+    dgamma[i] += acc;
+  } else {
+    dbeta[i - h] += acc;
   }
+}
+
+int layernorm_bwd_blocks(int rows) {
+  int grid = (rows + 7) / 8;  // one row per warp: latency-bound, so favour parallelism
+  if (grid > 2 * num_sms()) grid = 2 * num_sms();
+  return grid < 1 ? 1 : grid;
 }
 
 int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, void* mean,
@@ -221,10 +267,10 @@ int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, v
   const int grid = grid_for(rows, 8);
 #define GX_LN_FWD(N)                                                                         \
   case N:                                                                                    \
-    layernorm_fwd_kernel<N><<<grid, 256, 0, st>>>(                                           \
-        static_cast<const uint4*>(x), static_cast<const uint4*>(gamma),                      \
-        static_cast<const uint4*>(beta), static_cast<uint4*>(y), static_cast<float*>(mean), \
-        static_cast<float*>(rstd), rows, h);                                                 \
+    launch_k(layernorm_fwd_kernel<N>, dim3(grid), dim3(256), 0, st,                          \
+             static_cast<const uint4*>(x), static_cast<const uint4*>(gamma),                 \
+             static_cast<const uint4*>(beta), static_cast<uint4*>(y),                        \
+             static_cast<float*>(mean), static_cast<float*>(rstd), rows, h);                 \
     break;
   switch (nc) {
     GX_LN_FWD(1) GX_LN_FWD(2) GX_LN_FWD(3) GX_LN_FWD(4) GX_LN_FWD(5) GX_LN_FWD(6)
@@ -237,22 +283,20 @@ int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, v
 
 int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
                   const void* gamma, const void* dres, void* dx, void* dgamma, void* dbeta,
-                  int rows, int h, cudaStream_t st) {
+                  int rows, int h, float* workspace, cudaStream_t st, bool dy_f32) {
   if (h % 8 != 0 || h > 4096) return set_error(kErrConfig, "layernorm: h must be a multiple of 8, <= 4096");
   if (rows <= 0) return kOk;
   int nc = (h / 8 + 31) / 32;
   nc = nc <= 6 ? nc : (nc <= 8 ? 8 : (nc <= 10 ? 10 : (nc <= 12 ? 12 : 16)));
-  int grid = (rows + 7) / 8;
-  if (grid > num_sms()) grid = num_sms();
+  const int grid = layernorm_bwd_blocks(rows);
   const int smem = 2 * h * 4;
 #define GX_LN_BWD(N)                                                                          \
   case N:                                                                                     \
-    layernorm_bwd_kernel<N><<<grid, 256, smem, st>>>(                                         \
-        static_cast<const uint4*>(dy), static_cast<const uint4*>(x),                          \
-        static_cast<const float*>(mean), static_cast<const float*>(rstd),                     \
-        static_cast<const uint4*>(gamma), static_cast<const uint4*>(dres),                    \
-        static_cast<uint4*>(dx), static_cast<float*>(dgamma), static_cast<float*>(dbeta), rows, \
-        h);                                                                                   \
+    launch_k(dy_f32 ? layernorm_bwd_kernel<N, true> : layernorm_bwd_kernel<N, false>,         \
+             dim3(grid), dim3(256), smem, st, dy, static_cast<const uint4*>(x),               \
+             static_cast<const float*>(mean), static_cast<const float*>(rstd),                \
+             static_cast<const uint4*>(gamma), static_cast<const uint4*>(dres),               \
+             static_cast<uint4*>(dx), workspace, rows, h);                                   \
     break;
   switch (nc) {
     GX_LN_BWD(1) GX_LN_BWD(2) GX_LN_BWD(3) GX_LN_BWD(4) GX_LN_BWD(5) GX_LN_BWD(6)
@@ -260,20 +304,26 @@ int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* r
     default: break;
   }
 #undef GX_LN_BWD
-  return check_launch("layernorm_bwd_kernel");
+  GX_RC(check_launch("layernorm_bwd_kernel"));
+  launch_k(layernorm_bwd_reduce_kernel, dim3((2 * h + 255) / 256), dim3(256), 0, st,
+           static_cast<const float*>(workspace), grid, h, static_cast<float*>(dgamma),
+           static_cast<float*>(dbeta));
+  return check_launch("layernorm_bwd_reduce_kernel");
 }
 
 // -------------------------------------------------------- bias + dropout + residual
-__global__ void bias_dropout_add_kernel(const uint4* __restrict__ x, const uint4* __restrict__ bias,
+template <bool kF32In>
+__global__ void bias_dropout_add_kernel(const void* __restrict__ x, const uint4* __restrict__ bias,
                                         const uint4* __restrict__ res, uint4* __restrict__ out,
                                         int rows, int cols, gx_dropout d) {
+  pdl_enter();
   const int cchunks = cols >> 3;
   const int64_t n = static_cast<int64_t>(rows) * cchunks;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int r = static_cast<int>(i / cchunks), c = static_cast<int>(i % cchunks);
     float v[8], b[8], rr[8];
-    unpack8(x[i], v);
+    load8<kF32In>(x, i, v);
     if (bias != nullptr) {
       unpack8(__ldg(bias + c), b);
 #pragma unroll
@@ -293,12 +343,12 @@ __global__ void bias_dropout_add_kernel(const uint4* __restrict__ x, const uint4
 }
 
 int bias_dropout_add(const void* x, const void* bias, const void* residual, void* out, int rows,
-                     int cols, const gx_dropout& d, cudaStream_t st) {
+                     int cols, const gx_dropout& d, cudaStream_t st, bool x_f32) {
   if (cols % 8) return set_error(kErrConfig, "bias_dropout_add: cols % 8 != 0");
   const int64_t n = static_cast<int64_t>(rows) * (cols / 8);
-  bias_dropout_add_kernel<<<grid_for(n, 256), 256, 0, st>>>(
-      static_cast<const uint4*>(x), static_cast<const uint4*>(bias),
-      static_cast<const uint4*>(residual), static_cast<uint4*>(out), rows, cols, d);
+  launch_k(x_f32 ? bias_dropout_add_kernel<true> : bias_dropout_add_kernel<false>,
+           dim3(grid_for(n, 256)), dim3(256), 0, st, x, static_cast<const uint4*>(bias),
+           static_cast<const uint4*>(residual), static_cast<uint4*>(out), rows, cols, d);
   return check_launch("bias_dropout_add_kernel");
 }
 
@@ -308,6 +358,7 @@ int bias_dropout_add(const void* x, const void* bias, const void* residual, void
 __global__ void __launch_bounds__(256) dropout_bwd_colsum_kernel(
     const uint4* __restrict__ dy, uint4* __restrict__ dz, float* __restrict__ dbias, int rows,
     int cols, int64_t ld_chunks, gx_dropout d, int rows_per_block) {
+  pdl_enter();
   __shared__ float red[32][65];
   const int cchunks = cols >> 3;
   const int cstrip = blockIdx.x * 8;           // first chunk of this strip
@@ -358,9 +409,9 @@ int dropout_bwd_colsum(const void* dy, void* dz, void* dbias, int rows, int cols
   if (ysplit < 1) ysplit = 1;
   const int rpb = (rows + ysplit - 1) / ysplit;
   dim3 grid(strips, ysplit);
-  dropout_bwd_colsum_kernel<<<grid, 256, 0, st>>>(
-      static_cast<const uint4*>(dy), static_cast<uint4*>(dz), static_cast<float*>(dbias), rows,
-      cols, cols / 8, d, rpb);
+  launch_k(dropout_bwd_colsum_kernel, grid, dim3(256), 0, st, static_cast<const uint4*>(dy),
+           static_cast<uint4*>(dz), static_cast<float*>(dbias), rows, cols,
+           static_cast<int64_t>(cols / 8), d, rpb);
   return check_launch("dropout_bwd_colsum_kernel");
 }
 
@@ -375,9 +426,9 @@ int colsum(const void* x, int64_t ld, void* acc, int rows, int cols, cudaStream_
   if (ysplit < 1) ysplit = 1;
   const int rpb = (rows + ysplit - 1) / ysplit;
   dim3 grid(strips, ysplit);
-  dropout_bwd_colsum_kernel<<<grid, 256, 0, st>>>(
-      static_cast<const uint4*>(x), const_cast<uint4*>(static_cast<const uint4*>(x)),
-      static_cast<float*>(acc), rows, cols, ld / 8, off, rpb);
+  launch_k(dropout_bwd_colsum_kernel, grid, dim3(256), 0, st, static_cast<const uint4*>(x),
+           const_cast<uint4*>(static_cast<const uint4*>(x)), static_cast<float*>(acc), rows,
+           cols, static_cast<int64_t>(ld / 8), off, rpb);
   return check_launch("colsum_kernel");
 }
 
@@ -385,6 +436,7 @@ int colsum(const void* x, int64_t ld, void* acc, int rows, int cols, cudaStream_
 __global__ void mse_loss_kernel(const uint4* __restrict__ y, const uint4* __restrict__ t,
                                 uint4* __restrict__ dy, float* __restrict__ loss, int64_t n8,
                                 float inv) {
+  pdl_enter();
   float acc = 0.f;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -413,9 +465,9 @@ __global__ void mse_loss_kernel(const uint4* __restrict__ y, const uint4* __rest
 int mse_loss(const void* y, const void* target, void* dy, void* loss, int64_t n, float inv_count,
              cudaStream_t st) {
   if (n % 8) return set_error(kErrConfig, "mse_loss: n % 8 != 0");
-  mse_loss_kernel<<<grid_for(n / 8, 256), 256, 0, st>>>(
-      static_cast<const uint4*>(y), static_cast<const uint4*>(target), static_cast<uint4*>(dy),
-      static_cast<float*>(loss), n / 8, inv_count);
+  launch_k(mse_loss_kernel, dim3(grid_for(n / 8, 256)), dim3(256), 0, st,
+           static_cast<const uint4*>(y), static_cast<const uint4*>(target),
+           static_cast<uint4*>(dy), static_cast<float*>(loss), n / 8, inv_count);
   return check_launch("mse_loss_kernel");
 }
 
@@ -424,6 +476,7 @@ __global__ void adamw_kernel(float4* __restrict__ p, const float4* __restrict__ 
                              float4* __restrict__ m, float4* __restrict__ v,
                              uint2* __restrict__ out, int64_t n4, float lr, float b1, float b2,
                              float eps, float wd, float bc1, float bc2) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     float4 pp = p[i];
@@ -463,6 +516,7 @@ __global__ void adamw_dev_kernel(float4* __restrict__ p, const float4* __restric
                                  float4* __restrict__ m, float4* __restrict__ v,
                                  uint2* __restrict__ out, int64_t n4, float lr, float b1, float b2,
                                  float eps, float wd, const int64_t* __restrict__ step) {
+  pdl_enter();
   const float t = static_cast<float>(*step);
   const float bc1 = 1.f - powf(b1, t), bc2 = 1.f - powf(b2, t);
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
@@ -490,17 +544,20 @@ __global__ void adamw_dev_kernel(float4* __restrict__ p, const float4* __restric
 
 int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n,
               float lr, float beta1, float beta2, float eps, float wd, const int64_t* step,
-              cudaStream_t st) {
+              cudaStream_t st, int max_blocks) {
   if (n % 4) return set_error(kErrConfig, "adamw: n % 4 != 0");
   if (n == 0) return kOk;
-  adamw_dev_kernel<<<grid_for(n / 4, 256), 256, 0, st>>>(
-      static_cast<float4*>(master), static_cast<const float4*>(grad), static_cast<float4*>(m),
-      static_cast<float4*>(v), static_cast<uint2*>(bf16_out), n / 4, lr, beta1, beta2, eps, wd,
-      step);
+  int blocks = grid_for(n / 4, 256);
+  if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
+  launch_k(adamw_dev_kernel, dim3(blocks), dim3(256), 0, st,
+           static_cast<float4*>(master), static_cast<const float4*>(grad),
+           static_cast<float4*>(m), static_cast<float4*>(v), static_cast<uint2*>(bf16_out), n / 4,
+           lr, beta1, beta2, eps, wd, step);
   return check_launch("adamw_dev_kernel");
 }
 
 __global__ void step_counters_kernel(int64_t* step, uint64_t* seed_offset) {
+  pdl_enter();
   if (step != nullptr) *step += 1;
   if (seed_offset != nullptr) *seed_offset += 0x9E3779B97F4A7C15ull;
 }
@@ -514,6 +571,7 @@ int bump_step(int64_t* step, uint64_t* seed_offset, cudaStream_t st) {
 // reduction used when several ranks share one device (collectives in "sim" comm mode).
 template <typename T>
 __global__ void sum_ptrs_kernel(PtrPack pk_, T* __restrict__ out, int64_t n) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     float acc = 0.f;
@@ -544,6 +602,7 @@ int sum_ptrs(const PtrPack& srcs, void* out, int64_t n, bool bf16, cudaStream_t 
 }
 
 __global__ void cast_bf16_kernel(const float4* __restrict__ s, uint2* __restrict__ d, int64_t n4) {
+  pdl_enter();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const float4 v = s[i];

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <sstream>
@@ -172,6 +173,8 @@ struct RankCtx {
        *dout = nullptr, *dctx = nullptr, *dqkv = nullptr, *da = nullptr;
   bf16* gbuf[2] = {nullptr, nullptr};
   float *dq_acc = nullptr, *dsum = nullptr;
+  float* ln_ws = nullptr;  // LayerNorm-backward block partials
+  float* acc32 = nullptr;  // split-K fp32 reduction target [rows][h]
   bf16 *x_in = nullptr, *target = nullptr;  // [m micro-batches of this rank's rows][h]
   bf16* dx_out = nullptr;                   // first stage: input gradient per micro-batch
   float *loss = nullptr, *loss_dummy = nullptr;
@@ -180,6 +183,7 @@ struct RankCtx {
   int64_t in_rows_total = 0;
   std::vector<int64_t> in_row_off;  // per micro-batch offset (rows) into x_in / target
   int cur = 0;                      // index of gbuf holding the current dY
+  bool dc_f32 = false, da_f32 = false;  // split-K results pending in acc32
 };
 
 // --------------------------------------------------------------------------------------
@@ -298,6 +302,32 @@ class ExecutorImpl final : public Executor {
     return timed(kComm, 0, 1.0 * n * dtype_bytes(t),
                  [&] { return comm_->all_gather(g, rank, a, b, c, t, st); });
   }
+  // Split-K into r.acc32 (fp32 [M][N]) when it pays (small M*N, long K); returns the split
+  // count used, 1 meaning "not split" (nothing launched).
+  int gemm_splitk(RankCtx& r, const void* a, int64_t lda, const void* b, int64_t ldb, bool bmn,
+                  int M, int N, int K, int* used) {
+    *used = 1;
+    if (!splitk_) return kOk;
+    int tile = 0;
+    const int sp = splitk_plan(M, N, K, &tile);
+    if (sp < 2) return kOk;
+    GX_TRY(cuda_check(cudaMemsetAsync(r.acc32, 0, static_cast<size_t>(M) * N * 4, stream_),
+                      "memset acc32"));
+    gx_gemm_epilogue e{};
+    e.alpha = 1.f;
+    e.drop_scale = 1.f;
+    e.out_kind = kOutF32Accumulate;
+    e.out = r.acc32;
+    e.ldo = N;
+    const double flops = 2.0 * M * N * K;
+    const double bytes = 2.0 * (static_cast<double>(M) * K + static_cast<double>(N) * K) + 4.0 * M * N;
+    GX_TRY(timed(kGemm, flops, bytes, [&] {
+      return gemm_bf16(GemmOperand{a, lda, false}, GemmOperand{b, ldb, bmn}, M, N, K, e, stream_,
+                       tile, sp);
+    }));
+    *used = sp;
+    return kOk;
+  }
   int gemm(const void* a, int64_t lda, bool amn, const void* b, int64_t ldb, bool bmn, int M, int N,
            int K, const gx_gemm_epilogue& ep) {
     const double flops = 2.0 * M * N * K;
@@ -330,6 +360,8 @@ class ExecutorImpl final : public Executor {
   float lr_ = 1e-4f, b1_ = 0.9f, b2_ = 0.999f, eps_ = 1e-8f, wd_ = 0.f;
   bool optimizer_ = true;
   bool forward_only_ = false;  // profiler / debugging: skip loss, backward and optimizer
+  bool splitk_ = true;         // split-K for long-K / small-MN GEMMs (GX_SPLITK=0 disables)
+  int opt_blocks_ = 0;         // grid cap of the overlapped AdamW (GX_OPT_BLOCKS; 0 = full)
   bool dry_run_ = false;       // topology only: no device state (host-logic tests)
   float inv_count_ = 1.f;
 
@@ -386,6 +418,10 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     wd_ = cfg.value("weight_decay", 0.0f);
     optimizer_ = cfg.value("optimizer", true);
     forward_only_ = cfg.value("forward_only", false);
+    splitk_ = cfg.value("splitk", true);
+    if (const char* e = std::getenv("GX_SPLITK")) splitk_ = e[0] != '0';
+    opt_blocks_ = cfg.value("optimizer_blocks", 0);
+    if (const char* e = std::getenv("GX_OPT_BLOCKS")) opt_blocks_ = std::atoi(e);
     thr_attn_ = threshold_of(p_attn_);
     thr_hidden_ = threshold_of(p_hidden_);
 
@@ -664,6 +700,13 @@ int ExecutorImpl::allocate(RankCtx& r) {
   r.gbuf[0] = A.a<bf16>(max_h);
   r.gbuf[1] = A.a<bf16>(max_h);
   r.dq_acc = A.a<float>(max_c);
+  r.acc32 = A.a<float>(max_h);
+  {
+    int64_t max_hdim = 0;
+    for (const RankLayer& L : r.layers) max_hdim = std::max<int64_t>(max_hdim, L.sh.h);
+    r.ln_ws = A.a<float>(static_cast<int64_t>(layernorm_bwd_blocks(static_cast<int>(max_rows))) * 2 *
+                         max_hdim);
+  }
   r.dsum = A.a<float>(max_lse);
   r.loss = A.a<float>(1);
   r.loss_dummy = A.a<float>(1);
@@ -950,6 +993,21 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     o.out_kind = kOutBF16;
     o.ldo = h;
     if (t == 1) {
+      int sp = 1;
+      GX_TRY(gemm_splitk(r, A.gel, ft, P + L.lay.w2.off, ft, false, rows, h, ft, &sp));
+      if (sp > 1) {  // split-K partials summed in fp32, then bias + dropout + residual
+        gx_dropout d{};
+        d.threshold = thr_hidden_;
+        d.scale = scale_of(p_hidden_);
+        d.seed = seed_;
+        d.site = 3ull * l + 2;
+        d.row_offset = row_off;
+        d.drop_ld = h;
+        d.seed_offset = r.seed_off;
+        return timed(kElementwise, 0, 8.0 * rows * h, [&] {
+          return bias_dropout_add(r.acc32, P + L.lay.b2.off, A.x1, A.y, rows, h, d, stream_, true);
+        });
+      }
       o.out = A.y;
       o.bias = P + L.lay.b2.off;
       o.residual = A.x1;
@@ -1029,19 +1087,26 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     w.out = G + L.lay.w1.off;
     w.ldo = h;
     GX_TRY(gemm(r.dpre, ft, true, A.ln2, h, true, ft, h, rows, w));  // dW1 = dpre^T ln2
-    gx_gemm_epilogue c = epi();
-    c.out_kind = kOutBF16;
-    c.out = r.dc;
-    c.ldo = h;
-    GX_TRY(gemm(r.dpre, ft, false, P + L.lay.w1.off, h, true, rows, h, ft, c));  // dpre W1
+    int sp_c = 1;
+    if (t == 1)
+      GX_TRY(gemm_splitk(r, r.dpre, ft, P + L.lay.w1.off, h, true, rows, h, ft, &sp_c));
+    r.dc_f32 = sp_c > 1;
+    if (sp_c == 1) {
+      gx_gemm_epilogue c = epi();
+      c.out_kind = kOutBF16;
+      c.out = r.dc;
+      c.ldo = h;
+      GX_TRY(gemm(r.dpre, ft, false, P + L.lay.w1.off, h, true, rows, h, ft, c));  // dpre W1
+    }
     if (t > 1)
       return c_all_reduce(L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
                                stream_);
     phase = 1;
   }
   if (phase == 1) {
-    GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd(r.dc, A.x1, A.mean2, A.rstd2, P + L.lay.ln2g.off, dY, r.dx1,
-                         G + L.lay.ln2g.off, G + L.lay.ln2b.off, rows, h, stream_); }));
+    const void* dc_in = r.dc_f32 ? static_cast<const void*>(r.acc32) : static_cast<const void*>(r.dc);
+    GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd(dc_in, A.x1, A.mean2, A.rstd2, P + L.lay.ln2g.off, dY, r.dx1,
+                         G + L.lay.ln2g.off, G + L.lay.ln2b.off, rows, h, r.ln_ws, stream_, r.dc_f32); }));
     d.site = 3ull * l + 1;
     GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(r.dx1, r.dout, G + L.lay.bo.off, rows, h, d, stream_); }));
     gx_gemm_epilogue w = epi();
@@ -1086,19 +1151,26 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     w.out = G + L.lay.wqkv.off;
     w.ldo = h;
     GX_TRY(gemm(r.dqkv, 3 * ht, true, A.ln1, h, true, 3 * ht, h, rows, w));  // dWqkv
-    gx_gemm_epilogue a = epi();
-    a.out_kind = kOutBF16;
-    a.out = r.da;
-    a.ldo = h;
-    GX_TRY(gemm(r.dqkv, 3 * ht, false, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, a));
+    int sp_a = 1;
+    if (t == 1)
+      GX_TRY(gemm_splitk(r, r.dqkv, 3 * ht, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, &sp_a));
+    r.da_f32 = sp_a > 1;
+    if (sp_a == 1) {
+      gx_gemm_epilogue a = epi();
+      a.out_kind = kOutBF16;
+      a.out = r.da;
+      a.ldo = h;
+      GX_TRY(gemm(r.dqkv, 3 * ht, false, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, a));
+    }
     if (t > 1)
       return c_all_reduce(L.g_tp, r.rank, r.da, static_cast<size_t>(rows) * h, DType::kBF16,
                                stream_);
     phase = 2;
   }
   if (phase == 2) {
-    GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd(r.da, A.x, A.mean1, A.rstd1, P + L.lay.ln1g.off, r.dx1, dX,
-                         G + L.lay.ln1g.off, G + L.lay.ln1b.off, rows, h, stream_); }));
+    const void* da_in = r.da_f32 ? static_cast<const void*>(r.acc32) : static_cast<const void*>(r.da);
+    GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd(da_in, A.x, A.mean1, A.rstd1, P + L.lay.ln1g.off, r.dx1, dX,
+                         G + L.lay.ln1g.off, G + L.lay.ln1b.off, rows, h, r.ln_ws, stream_, r.da_f32); }));
   }
   return kOk;
 }
@@ -1137,7 +1209,7 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
     GX_TRY(cuda_check(cudaStreamWaitEvent(side_, e, 0), "fork wait"));
     side_used_ = true;
     return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_, wd_,
-                     r.step, side_);
+                     r.step, side_, opt_blocks_);
   }
   return kOk;
 }

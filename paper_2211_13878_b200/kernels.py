@@ -72,6 +72,21 @@ def gemm(a, b, *, a_mn_major=False, b_mn_major=False, out=None, out_kind="bf16",
     return out
 
 
+def gemm_splitk(a, b, *, a_mn_major=False, b_mn_major=False, out=None, splits=0, tile_n=0,
+                stream=None):
+    """out (fp32, zero-initialised here if None) += A * B^T over `splits` K-slices."""
+    import torch
+    M = a.shape[1] if a_mn_major else a.shape[0]
+    K = a.shape[0] if a_mn_major else a.shape[1]
+    N = b.shape[1] if b_mn_major else b.shape[0]
+    if out is None:
+        out = torch.zeros(M, N, device=a.device, dtype=torch.float32)
+    _lib.check(_lib.lib().gx_k_gemm_bf16_splitk(
+        _ptr(a), a.stride(0), int(a_mn_major), _ptr(b), b.stride(0), int(b_mn_major), M, N, K,
+        _ptr(out), out.stride(0), splits, tile_n, _lib.stream_ptr(stream)))
+    return out
+
+
 class _AttnArgs(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int), ("seq", ctypes.c_int), ("heads", ctypes.c_int),
                 ("head_dim", ctypes.c_int), ("heads_total", ctypes.c_int),

@@ -15,8 +15,9 @@ def _rel(x, ref):
 
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True), (True, False)])
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (512, 3840, 1280), (520, 480, 160),
-                                   (1024, 1280, 5120), (256, 200, 72)])
-@pytest.mark.parametrize("tile_n", [0, 64, 128, 256])
+                                   (1024, 1280, 5120), (256, 200, 72), (1280, 5120, 512),
+                                   (776, 640, 1280)])
+@pytest.mark.parametrize("tile_n", [0, 64, 128, 256, -128, -256])
 def test_gemm_layouts(cuda, a_mn, b_mn, M, N, K, tile_n):
     from paper_2211_13878_b200 import kernels
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N * 3 + K)
@@ -77,3 +78,19 @@ def test_gemm_residual_dropout(cuda):
     y1 = kernels.gemm(X, W, bias=b, residual=R, dropout_p=0.1, seed=1234, site=9)
     dropped = ((y1.float() - R.float()).abs() < 1e-6).float().mean().item()
     assert 0.08 < dropped < 0.12
+
+
+@pytest.mark.parametrize("M,N,K,b_mn", [(512, 1280, 5120, False), (512, 1280, 3840, True),
+                                         (128, 256, 512, False), (2048, 1280, 5120, True),
+                                         (520, 640, 1000, False)])
+@pytest.mark.parametrize("splits,tile", [(0, 0), (3, -256), (5, -128), (4, 128), (7, 64)])
+def test_gemm_splitk(cuda, M, N, K, b_mn, splits, tile):
+    from paper_2211_13878_b200 import kernels
+    g = torch.Generator(device="cpu").manual_seed(M + N + K)
+    A = torch.randn(M, K, generator=g).to(cuda, torch.bfloat16)
+    B = torch.randn(N, K, generator=g).to(cuda, torch.bfloat16)
+    ref = A.float() @ B.float().t()
+    b_arg = B.t().contiguous() if b_mn else B
+    out = kernels.gemm_splitk(A, b_arg, b_mn_major=b_mn, splits=splits, tile_n=tile)
+    torch.cuda.synchronize()
+    assert _rel(out, ref) <= 1e-5
