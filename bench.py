@@ -261,11 +261,14 @@ def run_gx(args, rank, world, local_rank):
     gemm_tflops = gemm["flops"] / (gemm["ms"] * 1e-3) / 1e12 if gemm["ms"] > 0 else 0.0
     peaks, peak_src = _peaks()
     peak = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")))
-    traffic = None
+    traffic, traffic_note = None, None
     tp = os.path.join(ROOT, "profiles", "ncu_gemm_traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            tj = json.load(f)
+        traffic = tj.get("dram_bytes_per_launch")
+        traffic_note = (f"ncu dram bytes of one {tj.get('kernel')} launch; algorithmic "
+                        f"{tj.get('algorithmic_bytes_per_launch')} B")
     cats = {k: round(v["ms"], 4) for k, v in prof["categories"].items()}
 
     cpu = None
@@ -297,7 +300,8 @@ def run_gx(args, rank, world, local_rank):
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4},
             "roofline": {"bound": "tensor", "achieved": round(gemm_tflops, 2), "peak": peak,
                          "unit": "TFLOP/s", "frac": round(gemm_tflops / peak, 4),
-                         "traffic": traffic, "kernel": "gemm_tcgen05_kernel (all layer GEMMs)",
+                         "traffic": traffic, "traffic_note": traffic_note,
+                         "kernel": "gemm_pair_kernel / gemm_tcgen05_kernel (all layer GEMMs)",
                          "peak_source": f"{peak_src} bf16_tflops_sustained",
                          "gemm_launches_per_step": gemm["launches"],
                          "gemm_ms_per_step": round(gemm["ms"], 4),

@@ -30,8 +30,9 @@ namespace gx {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 B = one swizzle span
-constexpr int kThreads = 256;
-constexpr int kStagingBytesDecl = 4 * 2 * (4096 + 2048);          // epilogue staging (below)
+constexpr int kEpiWarps = 8;  // warps 4..11: two per TMEM lane quarter, each half the columns
+constexpr int kThreads = 128 + 32 * kEpiWarps;
+constexpr int kStagingBytesDecl = kEpiWarps * (4096 + 2048);      // epilogue staging (below)
 constexpr int kSmemBudget = 227 * 1024 - kStagingBytesDecl - 2048;  // left for the A/B ring
 
 template <int BN>
@@ -145,7 +146,7 @@ __device__ __forceinline__ void epilogue_math(const GemmEpilogue& ep, int64_t ro
 // the store of block i overlaps the math of block i+1.
 constexpr int kStageOutBytes = 4096;  // 32 x 32 fp32
 constexpr int kStageAuxBytes = 2048;  // 32 x 32 bf16
-constexpr int kStagingBytes = 4 * 2 * (kStageOutBytes + kStageAuxBytes);
+constexpr int kStagingBytes = kEpiWarps * (kStageOutBytes + kStageAuxBytes);
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                              uint32_t d) {
@@ -185,8 +186,8 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32
       : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() {
-  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -202,11 +203,10 @@ __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUt
   const int64_t row = m_base + lane;
   float v[32], pre[32];
   epilogue_math(ep, row, row < M, n0, N, acc, v, pre);
-  const uint32_t b = block_ctr & 1u;
   ++block_ctr;
-  const uint32_t out_buf = smem_u32(staging) + (q * 2 + b) * (kStageOutBytes + kStageAuxBytes);
+  const uint32_t out_buf = smem_u32(staging) + q * (kStageOutBytes + kStageAuxBytes);
   const uint32_t aux_buf = out_buf + kStageOutBytes;
-  if (lane == 0) bulk_wait_read1();  // the store that last used this buffer has read it
+  if (lane == 0) bulk_wait_read0();  // the previous store from this buffer has read it
   __syncwarp();
   if (ep.out_kind == kOutBF16) {
     stage_bf16_row(out_buf, lane, v);
@@ -231,13 +231,18 @@ __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUt
 // All BN/32 chunks of one accumulator tile for one epilogue warp.  (A ping-pong variant
 // that keeps the next chunk's TMEM load in flight measured slower: the extra 32 live
 // registers cost more than the hidden LDTM latency.)
+// `ew` (0..kEpiWarps-1) selects the staging buffer and the column half this warp owns.
 template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const CUtensorMap* map_out,
-                                              const CUtensorMap* map_aux, uint8_t* staging, int q,
+                                              const CUtensorMap* map_aux, uint8_t* staging, int ew,
                                               uint32_t& block_ctr, uint32_t taddr, int64_t m_base,
                                               int n0, int M, int N) {
+  constexpr int NC = BN / 32;
+  constexpr int kHalves = kEpiWarps / 4;
+  const int c_lo = (ew / 4) * NC / kHalves, c_hi = (ew / 4 + 1) * NC / kHalves;
+  const int q = ew;
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
+  for (int c = c_lo; c < c_hi; ++c) {
     uint32_t r[32];
     tmem_ld32(taddr + c * 32, r);
     tmem_ld_wait();
@@ -284,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 128);
+      mbar_init(&tempty_bar[b], 32 * kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -384,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
       const int64_t m_base = m0 + q * 32;
-      epilogue_tile<BN>(ep, &map_out, &map_aux, staging, q, block_ctr,
+      epilogue_tile<BN>(ep, &map_out, &map_aux, staging, warp - 4, block_ctr,
                         tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base, n0,
                         M, N);
       tc_fence_before();
@@ -461,7 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);  // the leader's multicast MMA commit
-      mbar_init(&tempty_bar[b], 8); // 4 epilogue warps x 2 CTAs (leader copy is used)
+      mbar_init(&tempty_bar[b], 2 * kEpiWarps);  // epilogue warps x 2 CTAs (leader copy)
     }
     fence_barrier_init();
   }
@@ -566,7 +571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
       const int64_t m_base = m0 + q * 32;
-      epilogue_tile<BN>(ep, &map_out, &map_aux, staging, q, block_ctr,
+      epilogue_tile<BN>(ep, &map_out, &map_aux, staging, warp - 4, block_ctr,
                         tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base, n0,
                         M, N);
       tc_fence_before();
