@@ -40,6 +40,7 @@ extern "C" {
 #define GX_OUT_BF16 0
 #define GX_OUT_F32 1
 #define GX_OUT_F32_ACC 2
+#define GX_OUT_F32_SPLIT 3  /* split-K: out is [splits][M][ldo] fp32, split s stores slice s */
 
 /* ------------------------------------------------------------------ library */
 GX_API const char* gx_last_error(void);
@@ -158,7 +159,7 @@ GX_API int64_t gx_launch_count(void);
 
 /* ------------------------------------------------------------------ kernels */
 typedef struct gx_gemm_epilogue {
-  int out_kind;               /* GX_OUT_BF16 | GX_OUT_F32 | GX_OUT_F32_ACC */
+  int out_kind;               /* GX_OUT_BF16 | GX_OUT_F32 | GX_OUT_F32_ACC | GX_OUT_F32_SPLIT */
   void* out;                  /* [M][ldo] */
   int64_t ldo;
   float alpha;                /* acc scale */

@@ -49,10 +49,11 @@ extern "C" int gx_k_layernorm_bwd(const void* dy, const void* x, const void* mea
   // standalone entry point: grow-only workspace owned here (the executor passes its own)
   static float* ws = nullptr;
   static size_t ws_floats = 0;
-  const size_t need = static_cast<size_t>(gx::layernorm_bwd_blocks(rows)) * 2 * h;
+  const size_t need = static_cast<size_t>(gx::layernorm_bwd_ws_floats(h));
   if (need > ws_floats) {
     if (ws != nullptr) cudaFree(ws);
-    if (cudaMalloc(&ws, need * sizeof(float)) != cudaSuccess)
+    if (cudaMalloc(&ws, need * sizeof(float)) != cudaSuccess ||
+        cudaMemset(ws, 0, need * sizeof(float)) != cudaSuccess)
       return gx::set_error(gx::kErrCuda, "layernorm_bwd: workspace allocation failed");
     ws_floats = need;
   }
@@ -76,7 +77,13 @@ extern "C" int gx_k_colsum(const void* x, int64_t ld, void* acc, int rows, int c
 }
 extern "C" int gx_k_mse_loss(const void* y, const void* target, void* dy, void* loss, int64_t n,
                              float inv_count, void* stream) {
-  return gx::mse_loss(y, target, dy, loss, n, inv_count, S(stream));
+  static float* ws = nullptr;  // standalone entry point: workspace owned here
+  if (ws == nullptr) {
+    if (cudaMalloc(&ws, (gx::kLossBlocks + 1) * sizeof(float)) != cudaSuccess ||
+        cudaMemset(ws, 0, (gx::kLossBlocks + 1) * sizeof(float)) != cudaSuccess)
+      return gx::set_error(gx::kErrCuda, "mse_loss: workspace allocation failed");
+  }
+  return gx::mse_loss(y, target, dy, loss, n, inv_count, S(stream), ws);
 }
 extern "C" int gx_k_adamw(void* master, const void* grad, void* m, void* v, void* out, int64_t n,
                           float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,

@@ -198,7 +198,8 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUtensorMap* map_out,
                                                const CUtensorMap* map_aux, uint8_t* staging,
                                                int q, uint32_t& block_ctr, int64_t m_base,
-                                               int n0, int M, int N, const uint32_t (&acc)[32]) {
+                                               int32_t store_row, int n0, int M, int N,
+                                               const uint32_t (&acc)[32]) {
   const uint32_t lane = lane_id();
   const int64_t row = m_base + lane;
   float v[32], pre[32];
@@ -218,9 +219,9 @@ __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUt
   __syncwarp();
   if (lane == 0) {
     if (ep.out_kind == kOutF32Accumulate) {
-      tma_reduce_add_2d(map_out, out_buf, n0, static_cast<int32_t>(m_base));
+      tma_reduce_add_2d(map_out, out_buf, n0, store_row);
     } else {
-      tma_store_2d(map_out, out_buf, n0, static_cast<int32_t>(m_base));
+      tma_store_2d(map_out, out_buf, n0, store_row);
     }
     if (ep.gelu) tma_store_2d(map_aux, aux_buf, n0, static_cast<int32_t>(m_base));
     bulk_commit();
@@ -236,7 +237,7 @@ template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const CUtensorMap* map_out,
                                               const CUtensorMap* map_aux, uint8_t* staging, int ew,
                                               uint32_t& block_ctr, uint32_t taddr, int64_t m_base,
-                                              int n0, int M, int N) {
+                                              int32_t store_row, int n0, int M, int N) {
   constexpr int NC = BN / 32;
   constexpr int kHalves = kEpiWarps / 4;
   const int c_lo = (ew / 4) * NC / kHalves, c_hi = (ew / 4 + 1) * NC / kHalves;
@@ -247,7 +248,8 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const CUte
     tmem_ld32(taddr + c * 32, r);
     tmem_ld_wait();
     if (m_base < M && n0 + c * 32 < N)
-      epilogue_block(ep, map_out, map_aux, staging, q, block_ctr, m_base, n0 + c * 32, M, N, r);
+      epilogue_block(ep, map_out, map_aux, staging, q, block_ctr, m_base, store_row, n0 + c * 32,
+                     M, N, r);
   }
 }
 
@@ -389,9 +391,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
       const int64_t m_base = m0 + q * 32;
+      // split-K slices: split s stores rows [s*M, (s+1)*M) of the [splits*M][N] output
+      const int32_t store_row = static_cast<int32_t>(
+          m_base + (ep.out_kind == kOutF32Split ? static_cast<int64_t>(unit / num_tiles) * M : 0));
       epilogue_tile<BN>(ep, &map_out, &map_aux, staging, warp - 4, block_ctr,
-                        tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base, n0,
-                        M, N);
+                        tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base,
+                        store_row, n0, M, N);
       tc_fence_before();
       mbar_arrive(&tempty_bar[buf]);
     }
@@ -571,9 +576,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
       const int64_t m_base = m0 + q * 32;
+      const int32_t store_row = static_cast<int32_t>(
+          m_base + (ep.out_kind == kOutF32Split ? static_cast<int64_t>(unit / num_tiles) * M : 0));
       epilogue_tile<BN>(ep, &map_out, &map_aux, staging, warp - 4, block_ctr,
-                        tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base, n0,
-                        M, N);
+                        tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base,
+                        store_row, n0, M, N);
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive_remote(leader_tempty0 + buf * 8);
@@ -624,9 +631,11 @@ static bool make_out_map(CUtensorMap* map, const void* ptr, uint64_t cols, uint6
   return r == CUDA_SUCCESS;
 }
 
-static bool make_epi_maps(const GemmEpilogue& ep, int M, int N, CUtensorMap* mo, CUtensorMap* mx) {
+static bool make_epi_maps(const GemmEpilogue& ep, int M, int N, int splits, CUtensorMap* mo,
+                          CUtensorMap* mx) {
   const bool f32 = ep.out_kind != kOutBF16;
-  if (!make_out_map(mo, ep.out, N, M, ep.ldo, f32)) return false;
+  const uint64_t rows = static_cast<uint64_t>(M) * (ep.out_kind == kOutF32Split ? splits : 1);
+  if (!make_out_map(mo, ep.out, N, rows, ep.ldo, f32)) return false;
   if (ep.gelu) return make_out_map(mx, ep.aux, N, M, ep.ld_aux, false);
   *mx = *mo;
   return true;
@@ -669,7 +678,7 @@ static int launch_gemm(const GemmOperand& a, const GemmOperand& b, int M, int N,
   bool ok = kAMN ? make_map(&ma, a.ptr, M, K, a.ld, kBK) : make_map(&ma, a.ptr, K, M, a.ld, kBM);
   ok = ok && (kBMN ? make_map(&mb, b.ptr, N, K, b.ld, kBK) : make_map(&mb, b.ptr, K, N, b.ld, BN));
   CUtensorMap mo, mx;
-  ok = ok && make_epi_maps(ep, M, N, &mo, &mx);
+  ok = ok && make_epi_maps(ep, M, N, splits, &mo, &mx);
   if (!ok) return set_error(kErrCuda, "gemm: cuTensorMapEncodeTiled failed");
   static bool attr_set = false;
   if (!attr_set) {
@@ -694,7 +703,7 @@ static int launch_gemm_pair(const GemmOperand& a, const GemmOperand& b, int M, i
   ok = ok && (kBMN ? make_map(&mb, b.ptr, N, K, b.ld, kBK)
                    : make_map(&mb, b.ptr, K, N, b.ld, BN / 2));
   CUtensorMap mo, mx;
-  ok = ok && make_epi_maps(ep, M, N, &mo, &mx);
+  ok = ok && make_epi_maps(ep, M, N, splits, &mo, &mx);
   if (!ok) return set_error(kErrCuda, "gemm: cuTensorMapEncodeTiled failed");
   static bool attr_set = false;
   if (!attr_set) {
@@ -760,13 +769,13 @@ int splitk_plan(int M, int N, int K, int* tile) {
     const int tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
     int sp = (num_sms() / 2) / tiles;
     sp = std::min(sp, kb / 4);
-    return std::max(1, std::min(sp, 16));
+    return std::max(1, std::min(sp, kMaxSplits));
   }
   *tile = 128;
   const int tiles = ((M + kBM - 1) / kBM) * ((N + 127) / 128);
   int sp = num_sms() / tiles;
   sp = std::min(sp, kb / 4);
-  return std::max(1, std::min(sp, 16));
+  return std::max(1, std::min(sp, kMaxSplits));
 }
 
 int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
@@ -777,9 +786,10 @@ int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
     const int kb_per = (kb_total + splits - 1) / splits;
     splits = (kb_total + kb_per - 1) / kb_per;
   }
-  if (splits > 1 && (ep.out_kind != kOutF32Accumulate || ep.bias != nullptr || ep.gelu ||
+  if (splits > 1 && ((ep.out_kind != kOutF32Accumulate && ep.out_kind != kOutF32Split) ||
+                     ep.bias != nullptr || ep.gelu ||
                      ep.gelu_bwd || ep.residual != nullptr || ep.alpha != 1.f))
-    return set_error(kErrConfig, "gemm: split-K needs a plain fp32 accumulate epilogue");
+    return set_error(kErrConfig, "gemm: split-K needs a plain fp32 accumulate / split epilogue");
   if (M <= 0 || N <= 0 || K <= 0) return set_error(kErrConfig, "gemm: empty problem");
   // TMA: row strides must be 16-byte multiples; the epilogue's vector stores need ldo too.
   if ((a.ld % 8) != 0 || (b.ld % 8) != 0 || (ep.ldo % 8) != 0 || (ep.gelu && ep.ld_aux % 8 != 0))

@@ -25,7 +25,12 @@ int check_launch(const char* what);
 // Number of kernels launched successfully through check_launch (process-wide).
 int64_t launch_count();
 
-enum OutKind : int { kOutBF16 = GX_OUT_BF16, kOutF32 = GX_OUT_F32, kOutF32Accumulate = GX_OUT_F32_ACC };
+enum OutKind : int {
+  kOutBF16 = GX_OUT_BF16,
+  kOutF32 = GX_OUT_F32,
+  kOutF32Accumulate = GX_OUT_F32_ACC,
+  kOutF32Split = GX_OUT_F32_SPLIT
+};
 
 struct GemmOperand {
   const void* ptr;
@@ -39,24 +44,38 @@ using GemmEpilogue = gx_gemm_epilogue;
 // zeroes it); requires a plain kOutF32Accumulate epilogue.
 int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
               const GemmEpilogue& ep, cudaStream_t stream, int force_bn = 0, int splits = 1);
+// Split-K: at most kMaxSplits K slices; with GX_OUT_F32_SPLIT the slices land in a
+// [splits][M][N] fp32 buffer and the consumer (bias_dropout_add / layernorm_bwd) sums them in
+// slice order, so the result is deterministic (no atomics, no zero-fill).
+constexpr int kMaxSplits = 8;
 int splitk_plan(int M, int N, int K, int* tile);
 
 int attention_fwd(const gx_attention_args& a, cudaStream_t st);
 int attention_bwd(const gx_attention_args& a, cudaStream_t st);
 int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, void* mean,
                   void* rstd, int rows, int h, cudaStream_t st);
-// workspace: fp32 [layernorm_bwd_blocks(rows)][2h] (block partials of dgamma / dbeta)
+// workspace: layernorm_bwd_ws_floats(h) fp32 words, zero-initialised once (column-pass
+// slice partials + per-strip tickets; the kernel leaves the tickets reset).  With `drop`
+// set, also dz = dropout_mask(dx) and dbias[c] += sum_r dz[r][c] (the dropout_bwd_colsum
+// of dx fused in).  Deterministic (no floating-point atomics).
+constexpr int kLnBwdMaxSlices = 64;
 int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
                   const void* gamma, const void* dres, void* dx, void* dgamma, void* dbeta,
-                  int rows, int h, float* workspace, cudaStream_t st, bool dy_f32 = false);
-int layernorm_bwd_blocks(int rows);
+                  int rows, int h, float* workspace, cudaStream_t st, bool dy_f32 = false,
+                  const gx_dropout* drop = nullptr, void* dz = nullptr, void* dbias = nullptr,
+                  int dy_slices = 1, int64_t dy_slice_stride = 0);
+int64_t layernorm_bwd_ws_floats(int h);
+// x_f32: x is fp32, the sum of x_slices slices slice_stride elements apart (split-K output)
 int bias_dropout_add(const void* x, const void* bias, const void* residual, void* out, int rows,
-                     int cols, const gx_dropout& d, cudaStream_t st, bool x_f32 = false);
+                     int cols, const gx_dropout& d, cudaStream_t st, bool x_f32 = false,
+                     int x_slices = 1, int64_t slice_stride = 0);
 int dropout_bwd_colsum(const void* dy, void* dz, void* dbias, int rows, int cols,
                        const gx_dropout& d, cudaStream_t st);
 int colsum(const void* x, int64_t ld, void* acc, int rows, int cols, cudaStream_t st);
+// workspace: kLossBlocks + 1 words, zero-initialised once (the kernel leaves it reset)
+constexpr int kLossBlocks = 512;
 int mse_loss(const void* y, const void* target, void* dy, void* loss, int64_t n, float inv_count,
-             cudaStream_t st);
+             cudaStream_t st, float* workspace);
 int adamw(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n, float lr,
           float beta1, float beta2, float eps, float wd, float bc1, float bc2, cudaStream_t st);
 int cast_bf16(const void* src, void* dst, int64_t n, cudaStream_t st);

@@ -51,6 +51,21 @@ __device__ __forceinline__ void load8(const void* base, int64_t i, float (&f)[8]
   }
 }
 
+// fp32: the fixed-order sum of `slices` split-K slices `stride` elements apart
+template <bool kF32>
+__device__ __forceinline__ void load8s(const void* base, int64_t i, float (&f)[8], int slices,
+                                       int64_t stride) {
+  load8<kF32>(base, i, f);
+  if constexpr (kF32) {
+    for (int s = 1; s < slices; ++s) {
+      float g[8];
+      load8<true>(static_cast<const float*>(base) + s * stride, i, g);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] += g[j];
+    }
+  }
+}
+
 __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   return make_uint4(pk(f[0], f[1]), pk(f[2], f[3]), pk(f[4], f[5]), pk(f[6], f[7]));
 }
@@ -148,116 +163,6 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const uint4* __restr
   }
 }
 
-// ---------------------------------------------------------------------- LayerNorm bwd
-// Pass 1: one warp per row computes dx (+ residual gradient) and keeps per-lane dgamma /
-// dbeta partials in registers; each block reduces them in shared memory and writes one
-// [2][h] partial row to a workspace (no global atomics).  Pass 2 sums the block partials
-// column-parallel and accumulates into dgamma / dbeta.
-template <int NC, bool kF32Dy>
-__global__ void __launch_bounds__(256) layernorm_bwd_kernel(
-    const void* __restrict__ dy, const uint4* __restrict__ x, const float* __restrict__ mean,
-    const float* __restrict__ rstd, const uint4* __restrict__ gamma, const uint4* __restrict__ dres,
-    uint4* __restrict__ dx, float* __restrict__ partial, int rows, int h) {
-  pdl_enter();
-  extern __shared__ float sred[];  // [2][h]
-  const int chunks = h >> 3;
-  const int lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < 2 * h; i += blockDim.x) sred[i] = 0.f;
-  __syncthreads();
-  float accg[NC][8], accb[NC][8];
-#pragma unroll
-  for (int c = 0; c < NC; ++c)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) accg[c][j] = accb[c][j] = 0.f;
-  float gm[NC][8];
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int ci = c * 32 + lane;
-    if (ci < chunks) {
-      unpack8(__ldg(gamma + ci), gm[c]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) gm[c][j] = 0.f;
-    }
-  }
-  const int warps_total = gridDim.x * (blockDim.x >> 5);
-  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps_total) {
-    const float mu = mean[r], rs = rstd[r];
-    float xh[NC][8], g[NC][8];
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ci = c * 32 + lane;
-      if (ci < chunks) {
-        float xv[8], dv[8];
-        unpack8(x[static_cast<int64_t>(r) * chunks + ci], xv);
-        load8<kF32Dy>(dy, static_cast<int64_t>(r) * chunks + ci, dv);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          xh[c][j] = (xv[j] - mu) * rs;
-          g[c][j] = dv[j] * gm[c][j];
-          s1 += g[c][j];
-          s2 += g[c][j] * xh[c][j];
-          accg[c][j] += dv[j] * xh[c][j];
-          accb[c][j] += dv[j];
-        }
-      }
-    }
-    const float m1 = warp_sum(s1) / static_cast<float>(h);
-    const float m2 = warp_sum(s2) / static_cast<float>(h);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ci = c * 32 + lane;
-      if (ci < chunks) {
-        float o[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = rs * (g[c][j] - m1 - xh[c][j] * m2);
-        if (dres != nullptr) {
-          float rv[8];
-          unpack8(dres[static_cast<int64_t>(r) * chunks + ci], rv);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) o[j] += rv[j];
-        }
-        dx[static_cast<int64_t>(r) * chunks + ci] = pack8(o);
-      }
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < NC; ++c) {
-    const int ci = c * 32 + lane;
-    if (ci < chunks) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        atomicAdd(&sred[ci * 8 + j], accg[c][j]);
-        atomicAdd(&sred[h + ci * 8 + j], accb[c][j]);
-      }
-    }
-  }
-  __syncthreads();
-  float* out = partial + static_cast<int64_t>(blockIdx.x) * 2 * h;
-  for (int i = threadIdx.x; i < 2 * h; i += blockDim.x) out[i] = sred[i];
-}
-
-__global__ void layernorm_bwd_reduce_kernel(const float* __restrict__ partial, int blocks, int h,
-                                            float* __restrict__ dgamma, float* __restrict__ dbeta) {
-  pdl_enter();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // 0 .. 2h
-  if (i >= 2 * h) return;
-  float acc = 0.f;
-  for (int b = 0; b < blocks; ++b) acc += partial[static_cast<int64_t>(b) * 2 * h + i];
-  if (i < h) {
-    dgamma[i] += acc;
-  } else {
-    dbeta[i - h] += acc;
-  }
-}
-
-int layernorm_bwd_blocks(int rows) {
-  int grid = (rows + 7) / 8;  // one row per warp: latency-bound, so favour parallelism
-  if (grid > 2 * num_sms()) grid = 2 * num_sms();
-  return grid < 1 ? 1 : grid;
-}
-
 int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, void* mean,
                   void* rstd, int rows, int h, cudaStream_t st) {
   if (h % 8 != 0 || h > 4096) return set_error(kErrConfig, "layernorm: h must be a multiple of 8, <= 4096");
@@ -281,22 +186,204 @@ int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, v
   return check_launch("layernorm_fwd_kernel");
 }
 
+// ---------------------------------------------------------------------- LayerNorm bwd
+// Two passes, both deterministic (no floating-point atomics):
+//  rows:    one warp per row computes dx = rstd * (g - mean(g) - xhat * mean(g * xhat)) + dres
+//           with g = dy * gamma; with `drop` set it also emits dz = dropout_mask(dx), the
+//           gradient entering the preceding bias + dropout (the dropout_bwd_colsum of dx,
+//           fused in).
+//  columns: dgamma += sum_r dy * xhat, dbeta += sum_r dy (and dbias += sum_r dz), computed by
+//           (64-column strip x row slice) blocks; each writes its partial sums and the last
+//           block of a strip (ticket counter) adds the slices in slice order.
+template <int NC, bool kF32Dy, bool kDrop>
+__global__ void __launch_bounds__(256) layernorm_bwd_rows_kernel(
+    const void* __restrict__ dy, const uint4* __restrict__ x, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const uint4* __restrict__ gamma, const uint4* __restrict__ dres,
+    uint4* __restrict__ dx, uint4* __restrict__ dz, gx_dropout d, int rows, int h, int dy_slices,
+    int64_t dy_stride) {
+  pdl_enter();
+  const int chunks = h >> 3;
+  const int lane = threadIdx.x & 31;
+  const int warps_total = gridDim.x * (blockDim.x >> 5);
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps_total) {
+    const float mu = mean[r], rs = rstd[r];
+    float xh[NC][8], dv[NC][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int ci = c * 32 + lane;
+      if (ci < chunks) {
+        float gm[8];
+        unpack8(x[static_cast<int64_t>(r) * chunks + ci], xh[c]);
+        load8s<kF32Dy>(dy, static_cast<int64_t>(r) * chunks + ci, dv[c], dy_slices, dy_stride);
+        unpack8(__ldg(gamma + ci), gm);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          xh[c][j] = (xh[c][j] - mu) * rs;
+          const float g = dv[c][j] * gm[j];
+          s1 += g;
+          s2 += g * xh[c][j];
+        }
+      }
+    }
+    const float m1 = warp_sum(s1) / static_cast<float>(h);
+    const float m2 = warp_sum(s2) / static_cast<float>(h);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int ci = c * 32 + lane;
+      if (ci < chunks) {
+        const int64_t i = static_cast<int64_t>(r) * chunks + ci;
+        float gm[8], rv[8], o[8];
+        unpack8(__ldg(gamma + ci), gm);
+        if (dres != nullptr) {
+          unpack8(dres[i], rv);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) rv[j] = 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = rs * (dv[c][j] * gm[j] - m1 - xh[c][j] * m2) + rv[j];
+        const uint4 ob = pack8(o);
+        dx[i] = ob;
+        if constexpr (kDrop) {
+          // identical arithmetic to dropout_bwd_colsum on the stored bf16 dx
+          float v[8];
+          unpack8(ob, v);
+          if (d.threshold != 0u) {
+            bool k[8];
+            keep8(d, static_cast<uint64_t>(d.row_offset + r) * d.drop_ld + d.col_offset + ci * 8, k);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = k[j] ? v[j] * d.scale : 0.f;
+          }
+          dz[i] = pack8(v);
+        }
+      }
+    }
+  }
+}
+
+template <bool kF32Dy, bool kDrop>
+__global__ void __launch_bounds__(256) layernorm_bwd_cols_kernel(
+    const void* __restrict__ dy, const uint4* __restrict__ x, const float* __restrict__ mean,
+    const float* __restrict__ rstd, const uint4* __restrict__ dz, float* __restrict__ dgamma,
+    float* __restrict__ dbeta, float* __restrict__ dbias, float* __restrict__ ws,
+    unsigned int* __restrict__ tickets, int rows, int h, int rows_per_slice, int dy_slices,
+    int64_t dy_stride) {
+  pdl_enter();
+  constexpr int kParts = kDrop ? 3 : 2;
+  __shared__ float red[32][kParts * 64 + 1];
+  __shared__ bool last;
+  const int chunks = h >> 3;
+  const int strip = blockIdx.x;
+  const int cl = threadIdx.x & 7;       // chunk within the 64-column strip
+  const int ci = strip * 8 + cl;        // global chunk index
+  const int rlane = threadIdx.x >> 3;   // 32 row lanes
+  const int r0 = blockIdx.y * rows_per_slice;
+  const int r1 = min(rows, r0 + rows_per_slice);
+  float ag[8] = {0, 0, 0, 0, 0, 0, 0, 0}, ab[8] = {0, 0, 0, 0, 0, 0, 0, 0},
+        az[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (ci < chunks) {
+    for (int r = r0 + rlane; r < r1; r += 32) {
+      const int64_t i = static_cast<int64_t>(r) * chunks + ci;
+      float xv[8], dv[8];
+      unpack8(x[i], xv);
+      load8s<kF32Dy>(dy, i, dv, dy_slices, dy_stride);
+      const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        ag[j] += dv[j] * ((xv[j] - mu) * rs);
+        ab[j] += dv[j];
+      }
+      if constexpr (kDrop) {
+        float zv[8];
+        unpack8(dz[i], zv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) az[j] += zv[j];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    red[rlane][cl * 8 + j] = ag[j];
+    red[rlane][64 + cl * 8 + j] = ab[j];
+    if constexpr (kDrop) red[rlane][128 + cl * 8 + j] = az[j];
+  }
+  __syncthreads();
+  const int width = kParts * h;
+  const int slices = gridDim.y;
+  // column t of this strip's partial: part t / 64, column strip*64 + t % 64
+  const int t = threadIdx.x;
+  const int col = strip * 64 + (t & 63);
+  const bool owner = t < kParts * 64 && col < h;
+  float s = 0.f;
+  if (owner) {
+    for (int rl = 0; rl < 32; ++rl) s += red[rl][t];
+  }
+  float* outs[3] = {dgamma, dbeta, dbias};
+  if (slices == 1) {
+    if (owner) outs[t >> 6][col] += s;
+    return;
+  }
+  if (owner) ws[static_cast<int64_t>(blockIdx.y) * width + (t >> 6) * h + col] = s;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&tickets[strip], 1u) == static_cast<unsigned>(slices - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (owner) {
+    float acc = 0.f;
+    for (int y = 0; y < slices; ++y)
+      acc += __ldcg(ws + static_cast<int64_t>(y) * width + (t >> 6) * h + col);
+    outs[t >> 6][col] += acc;
+  }
+  if (threadIdx.x == 0) tickets[strip] = 0u;  // ready for the next call / graph replay
+}
+
+static void ln_cols_grid(int rows, int h, int* strips, int* slices, int* rows_per_slice) {
+  *strips = (h / 8 + 7) / 8;
+  int ys = (2 * num_sms() + *strips - 1) / *strips;
+  const int max_y = (rows + 31) / 32;
+  if (ys > max_y) ys = max_y;
+  if (ys > kLnBwdMaxSlices) ys = kLnBwdMaxSlices;
+  if (ys < 1) ys = 1;
+  *rows_per_slice = (rows + ys - 1) / ys;
+  *slices = (rows + *rows_per_slice - 1) / *rows_per_slice;
+}
+
+int64_t layernorm_bwd_ws_floats(int h) {
+  return static_cast<int64_t>(kLnBwdMaxSlices) * 3 * h + (h / 64 + 64);
+}
+
 int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
                   const void* gamma, const void* dres, void* dx, void* dgamma, void* dbeta,
-                  int rows, int h, float* workspace, cudaStream_t st, bool dy_f32) {
+                  int rows, int h, float* workspace, cudaStream_t st, bool dy_f32,
+                  const gx_dropout* drop, void* dz, void* dbias, int dy_slices,
+                  int64_t dy_slice_stride) {
   if (h % 8 != 0 || h > 4096) return set_error(kErrConfig, "layernorm: h must be a multiple of 8, <= 4096");
   if (rows <= 0) return kOk;
+  if (dy_slices < 1 || (dy_slices > 1 && !dy_f32))
+    return set_error(kErrConfig, "layernorm_bwd: dy slices need fp32 dy");
+  const bool fuse = drop != nullptr;
+  if (fuse && (dz == nullptr || dbias == nullptr))
+    return set_error(kErrConfig, "layernorm_bwd: fused dropout needs dz and dbias");
+  const gx_dropout dd = fuse ? *drop : gx_dropout{};
   int nc = (h / 8 + 31) / 32;
   nc = nc <= 6 ? nc : (nc <= 8 ? 8 : (nc <= 10 ? 10 : (nc <= 12 ? 12 : 16)));
-  const int grid = layernorm_bwd_blocks(rows);
-  const int smem = 2 * h * 4;
-#define GX_LN_BWD(N)                                                                          \
-  case N:                                                                                     \
-    launch_k(dy_f32 ? layernorm_bwd_kernel<N, true> : layernorm_bwd_kernel<N, false>,         \
-             dim3(grid), dim3(256), smem, st, dy, static_cast<const uint4*>(x),               \
-             static_cast<const float*>(mean), static_cast<const float*>(rstd),                \
-             static_cast<const uint4*>(gamma), static_cast<const uint4*>(dres),               \
-             static_cast<uint4*>(dx), workspace, rows, h);                                   \
+  const int grid = grid_for(rows, 8);
+#define GX_LN_BWD_K(N, F32, DROP)                                                             \
+  launch_k(layernorm_bwd_rows_kernel<N, F32, DROP>, dim3(grid), dim3(256), 0, st, dy,         \
+           static_cast<const uint4*>(x), static_cast<const float*>(mean),                     \
+           static_cast<const float*>(rstd), static_cast<const uint4*>(gamma),                 \
+           static_cast<const uint4*>(dres), static_cast<uint4*>(dx), static_cast<uint4*>(dz), \
+           dd, rows, h, dy_slices, dy_slice_stride);
+#define GX_LN_BWD(N)                                                              \
+  case N:                                                                         \
+    if (dy_f32) {                                                                 \
+      if (fuse) GX_LN_BWD_K(N, true, true) else GX_LN_BWD_K(N, true, false)      \
+    } else {                                                                      \
+      if (fuse) GX_LN_BWD_K(N, false, true) else GX_LN_BWD_K(N, false, false)    \
+    }                                                                             \
     break;
   switch (nc) {
     GX_LN_BWD(1) GX_LN_BWD(2) GX_LN_BWD(3) GX_LN_BWD(4) GX_LN_BWD(5) GX_LN_BWD(6)
@@ -304,18 +391,27 @@ int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* r
     default: break;
   }
 #undef GX_LN_BWD
-  GX_RC(check_launch("layernorm_bwd_kernel"));
-  launch_k(layernorm_bwd_reduce_kernel, dim3((2 * h + 255) / 256), dim3(256), 0, st,
-           static_cast<const float*>(workspace), grid, h, static_cast<float*>(dgamma),
-           static_cast<float*>(dbeta));
-  return check_launch("layernorm_bwd_reduce_kernel");
+#undef GX_LN_BWD_K
+  GX_RC(check_launch("layernorm_bwd_rows_kernel"));
+  int strips, slices, rps;
+  ln_cols_grid(rows, h, &strips, &slices, &rps);
+  unsigned int* tickets = reinterpret_cast<unsigned int*>(
+      workspace + static_cast<int64_t>(kLnBwdMaxSlices) * 3 * h);
+  auto* kcols = dy_f32 ? (fuse ? layernorm_bwd_cols_kernel<true, true> : layernorm_bwd_cols_kernel<true, false>)
+                       : (fuse ? layernorm_bwd_cols_kernel<false, true> : layernorm_bwd_cols_kernel<false, false>);
+  launch_k(kcols, dim3(strips, slices), dim3(256), 0, st, dy, static_cast<const uint4*>(x),
+           static_cast<const float*>(mean), static_cast<const float*>(rstd),
+           static_cast<const uint4*>(dz), static_cast<float*>(dgamma), static_cast<float*>(dbeta),
+           static_cast<float*>(dbias), workspace, tickets, rows, h, rps, dy_slices, dy_slice_stride);
+  return check_launch("layernorm_bwd_cols_kernel");
 }
 
 // -------------------------------------------------------- bias + dropout + residual
 template <bool kF32In>
 __global__ void bias_dropout_add_kernel(const void* __restrict__ x, const uint4* __restrict__ bias,
                                         const uint4* __restrict__ res, uint4* __restrict__ out,
-                                        int rows, int cols, gx_dropout d) {
+                                        int rows, int cols, gx_dropout d, int x_slices,
+                                        int64_t x_stride) {
   pdl_enter();
   const int cchunks = cols >> 3;
   const int64_t n = static_cast<int64_t>(rows) * cchunks;
@@ -323,7 +419,7 @@ __global__ void bias_dropout_add_kernel(const void* __restrict__ x, const uint4*
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int r = static_cast<int>(i / cchunks), c = static_cast<int>(i % cchunks);
     float v[8], b[8], rr[8];
-    load8<kF32In>(x, i, v);
+    load8s<kF32In>(x, i, v, x_slices, x_stride);
     if (bias != nullptr) {
       unpack8(__ldg(bias + c), b);
 #pragma unroll
@@ -343,12 +439,16 @@ __global__ void bias_dropout_add_kernel(const void* __restrict__ x, const uint4*
 }
 
 int bias_dropout_add(const void* x, const void* bias, const void* residual, void* out, int rows,
-                     int cols, const gx_dropout& d, cudaStream_t st, bool x_f32) {
+                     int cols, const gx_dropout& d, cudaStream_t st, bool x_f32, int x_slices,
+                     int64_t slice_stride) {
   if (cols % 8) return set_error(kErrConfig, "bias_dropout_add: cols % 8 != 0");
+  if (x_slices < 1 || (x_slices > 1 && !x_f32))
+    return set_error(kErrConfig, "bias_dropout_add: slices need fp32 x");
   const int64_t n = static_cast<int64_t>(rows) * (cols / 8);
   launch_k(x_f32 ? bias_dropout_add_kernel<true> : bias_dropout_add_kernel<false>,
            dim3(grid_for(n, 256)), dim3(256), 0, st, x, static_cast<const uint4*>(bias),
-           static_cast<const uint4*>(residual), static_cast<uint4*>(out), rows, cols, d);
+           static_cast<const uint4*>(residual), static_cast<uint4*>(out), rows, cols, d, x_slices,
+           slice_stride);
   return check_launch("bias_dropout_add_kernel");
 }
 
@@ -433,9 +533,14 @@ int colsum(const void* x, int64_t ld, void* acc, int rows, int cols, cudaStream_
 }
 
 // ------------------------------------------------------------------------------ loss
-__global__ void mse_loss_kernel(const uint4* __restrict__ y, const uint4* __restrict__ t,
-                                uint4* __restrict__ dy, float* __restrict__ loss, int64_t n8,
-                                float inv) {
+// Deterministic: a fixed grid writes one partial per block; the last block to finish (ticket)
+// adds them in block order, so the loss is bit-reproducible run to run.
+__global__ void __launch_bounds__(256) mse_loss_kernel(const uint4* __restrict__ y,
+                                                       const uint4* __restrict__ t,
+                                                       uint4* __restrict__ dy,
+                                                       float* __restrict__ loss, int64_t n8,
+                                                       float inv, float* __restrict__ partials,
+                                                       unsigned int* __restrict__ ticket) {
   pdl_enter();
   float acc = 0.f;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n8;
@@ -452,62 +557,119 @@ __global__ void mse_loss_kernel(const uint4* __restrict__ y, const uint4* __rest
     dy[i] = pack8(g);
   }
   acc = warp_sum(acc);
-  __shared__ float s[32];
+  __shared__ float s[8];
+  __shared__ bool last;
   if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? s[threadIdx.x] : 0.f;
+  if (threadIdx.x == 0) {
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += s[w];
+    partials[blockIdx.x] = v;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x < 32) {
+    __threadfence();
+    float v = 0.f;
+    for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += 32)
+      v += *reinterpret_cast<volatile float*>(partials + b);
     v = warp_sum(v);
-    if (threadIdx.x == 0) atomicAdd(loss, v * inv);
+    if (threadIdx.x == 0) {
+      *loss += v * inv;
+      *ticket = 0u;  // ready for the next call (graph replays)
+    }
   }
 }
 
 int mse_loss(const void* y, const void* target, void* dy, void* loss, int64_t n, float inv_count,
-             cudaStream_t st) {
+             cudaStream_t st, float* workspace) {
   if (n % 8) return set_error(kErrConfig, "mse_loss: n % 8 != 0");
-  launch_k(mse_loss_kernel, dim3(grid_for(n / 8, 256)), dim3(256), 0, st,
-           static_cast<const uint4*>(y), static_cast<const uint4*>(target),
-           static_cast<uint4*>(dy), static_cast<float*>(loss), n / 8, inv_count);
+  int grid = grid_for(n / 8, 256);
+  if (grid > kLossBlocks) grid = kLossBlocks;
+  launch_k(mse_loss_kernel, dim3(grid), dim3(256), 0, st, static_cast<const uint4*>(y),
+           static_cast<const uint4*>(target), static_cast<uint4*>(dy), static_cast<float*>(loss),
+           n / 8, inv_count, workspace, reinterpret_cast<unsigned int*>(workspace + kLossBlocks));
   return check_launch("mse_loss_kernel");
 }
 
 // ------------------------------------------------------------------------------ AdamW
+// p <- p - lr * (m_hat / (sqrt(v_hat) + eps) + wd * p), restated with the bias corrections
+// folded into two per-launch scalars (step_size = lr / bc1, 1/sqrt(bc2)) so the per-element
+// work is FMAs, one sqrt and one fast divide: the kernel shares the SMs with the backward
+// GEMMs, so its issue cost matters as much as its 30 B/param of HBM traffic.
+struct AdamScalars {
+  float b1, b2, eps, step_size, inv_sqrt_bc2, lr_wd;
+};
+__device__ __forceinline__ AdamScalars adam_scalars(float lr, float b1, float b2, float eps,
+                                                    float wd, float bc1, float bc2) {
+  return AdamScalars{b1, b2, eps, lr / bc1, rsqrtf(bc2), lr * wd};
+}
+__device__ __forceinline__ void adam4(const AdamScalars& c, float4& p, const float4& g, float4& m,
+                                      float4& v) {
+  float* pf = &p.x;
+  const float* gf = &g.x;
+  float* mf = &m.x;
+  float* vf = &v.x;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    mf[j] = c.b1 * mf[j] + (1.f - c.b1) * gf[j];
+    vf[j] = c.b2 * vf[j] + (1.f - c.b2) * gf[j] * gf[j];
+    const float denom = sqrtf(vf[j]) * c.inv_sqrt_bc2 + c.eps;
+    pf[j] = pf[j] - c.step_size * __fdividef(mf[j], denom) - c.lr_wd * pf[j];
+  }
+}
+// two float4 per thread per iteration: 8 independent 16-byte loads in flight
+__device__ __forceinline__ void adam_range(const AdamScalars& c, float4* __restrict__ p,
+                                           const float4* __restrict__ g, float4* __restrict__ m,
+                                           float4* __restrict__ v, uint2* __restrict__ out,
+                                           int64_t n4) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  for (; i + stride < n4; i += 2 * stride) {
+    float4 p0 = p[i], p1 = p[i + stride];
+    const float4 g0 = g[i], g1 = g[i + stride];
+    float4 m0 = m[i], m1 = m[i + stride], v0 = v[i], v1 = v[i + stride];
+    adam4(c, p0, g0, m0, v0);
+    adam4(c, p1, g1, m1, v1);
+    p[i] = p0;
+    p[i + stride] = p1;
+    m[i] = m0;
+    m[i + stride] = m1;
+    v[i] = v0;
+    v[i + stride] = v1;
+    out[i] = make_uint2(pk(p0.x, p0.y), pk(p0.z, p0.w));
+    out[i + stride] = make_uint2(pk(p1.x, p1.y), pk(p1.z, p1.w));
+  }
+  if (i < n4) {
+    float4 p0 = p[i];
+    const float4 g0 = g[i];
+    float4 m0 = m[i], v0 = v[i];
+    adam4(c, p0, g0, m0, v0);
+    p[i] = p0;
+    m[i] = m0;
+    v[i] = v0;
+    out[i] = make_uint2(pk(p0.x, p0.y), pk(p0.z, p0.w));
+  }
+}
+
 __global__ void adamw_kernel(float4* __restrict__ p, const float4* __restrict__ g,
                              float4* __restrict__ m, float4* __restrict__ v,
                              uint2* __restrict__ out, int64_t n4, float lr, float b1, float b2,
                              float eps, float wd, float bc1, float bc2) {
   pdl_enter();
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    float4 pp = p[i];
-    const float4 gg = g[i];
-    float4 mm = m[i], vv = v[i];
-    float* pf = &pp.x;
-    const float* gf = &gg.x;
-    float* mf = &mm.x;
-    float* vf = &vv.x;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      mf[j] = b1 * mf[j] + (1.f - b1) * gf[j];
-      vf[j] = b2 * vf[j] + (1.f - b2) * gf[j] * gf[j];
-      const float mh = mf[j] / bc1, vh = vf[j] / bc2;
-      pf[j] = pf[j] - lr * (mh / (sqrtf(vh) + eps) + wd * pf[j]);
-    }
-    p[i] = pp;
-    m[i] = mm;
-    v[i] = vv;
-    out[i] = make_uint2(pk(pp.x, pp.y), pk(pp.z, pp.w));
-  }
+  adam_range(adam_scalars(lr, b1, b2, eps, wd, bc1, bc2), p, g, m, v, out, n4);
 }
 
 int adamw(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n, float lr,
           float beta1, float beta2, float eps, float wd, float bc1, float bc2, cudaStream_t st) {
   if (n % 4) return set_error(kErrConfig, "adamw: n % 4 != 0");
   if (n == 0) return kOk;
-  adamw_kernel<<<grid_for(n / 4, 256), 256, 0, st>>>(
-      static_cast<float4*>(master), static_cast<const float4*>(grad), static_cast<float4*>(m),
-      static_cast<float4*>(v), static_cast<uint2*>(bf16_out), n / 4, lr, beta1, beta2, eps, wd,
-      bc1, bc2);
+  launch_k(adamw_kernel, dim3(grid_for(n / 8, 256)), dim3(256), 0, st,
+           static_cast<float4*>(master), static_cast<const float4*>(grad), static_cast<float4*>(m),
+           static_cast<float4*>(v), static_cast<uint2*>(bf16_out), n / 4, lr, beta1, beta2, eps,
+           wd, bc1, bc2);
   return check_launch("adamw_kernel");
 }
 
@@ -518,28 +680,8 @@ __global__ void adamw_dev_kernel(float4* __restrict__ p, const float4* __restric
                                  float eps, float wd, const int64_t* __restrict__ step) {
   pdl_enter();
   const float t = static_cast<float>(*step);
-  const float bc1 = 1.f - powf(b1, t), bc2 = 1.f - powf(b2, t);
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    float4 pp = p[i];
-    const float4 gg = g[i];
-    float4 mm = m[i], vv = v[i];
-    float* pf = &pp.x;
-    const float* gf = &gg.x;
-    float* mf = &mm.x;
-    float* vf = &vv.x;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      mf[j] = b1 * mf[j] + (1.f - b1) * gf[j];
-      vf[j] = b2 * vf[j] + (1.f - b2) * gf[j] * gf[j];
-      const float mh = mf[j] / bc1, vh = vf[j] / bc2;
-      pf[j] = pf[j] - lr * (mh / (sqrtf(vh) + eps) + wd * pf[j]);
-    }
-    p[i] = pp;
-    m[i] = mm;
-    v[i] = vv;
-    out[i] = make_uint2(pk(pp.x, pp.y), pk(pp.z, pp.w));
-  }
+  adam_range(adam_scalars(lr, b1, b2, eps, wd, 1.f - powf(b1, t), 1.f - powf(b2, t)), p, g, m, v,
+             out, n4);
 }
 
 int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n,
@@ -547,7 +689,7 @@ int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, 
               cudaStream_t st, int max_blocks) {
   if (n % 4) return set_error(kErrConfig, "adamw: n % 4 != 0");
   if (n == 0) return kOk;
-  int blocks = grid_for(n / 4, 256);
+  int blocks = grid_for(n / 8, 256);
   if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
   launch_k(adamw_dev_kernel, dim3(blocks), dim3(256), 0, st,
            static_cast<float4*>(master), static_cast<const float4*>(grad),

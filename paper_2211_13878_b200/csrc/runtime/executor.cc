@@ -169,21 +169,28 @@ struct RankCtx {
   std::vector<RankLayer> layers;  // this stage's layers in order
   Arena arena;
   // scratch
-  bf16 *partial = nullptr, *dz = nullptr, *dpre = nullptr, *dc = nullptr, *dx1 = nullptr,
-       *dout = nullptr, *dctx = nullptr, *dqkv = nullptr, *da = nullptr;
+  bf16 *partial = nullptr, *dc = nullptr, *dx1 = nullptr, *dctx = nullptr, *da = nullptr;
+  // Gradients the weight-gradient GEMMs read, double-buffered by layer parity: layer l's
+  // wgrads run on the wgrad stream while layer l-1's data-gradient chain writes the other
+  // buffer.  wg_done[p] marks the last wgrad that read buffer set p.
+  bf16 *dzb[2] = {nullptr, nullptr}, *dpreb[2] = {nullptr, nullptr},
+       *doutb[2] = {nullptr, nullptr}, *dqkvb[2] = {nullptr, nullptr};
+  cudaEvent_t wg_done[2] = {nullptr, nullptr};
+  bool wg_pending[2] = {false, false};
   bf16* gbuf[2] = {nullptr, nullptr};
   float *dq_acc = nullptr, *dsum = nullptr;
   float* ln_ws = nullptr;  // LayerNorm-backward block partials
-  float* acc32 = nullptr;  // split-K fp32 reduction target [rows][h]
+  float* acc32 = nullptr;  // split-K fp32 slices [kMaxSplits][rows][h]
   bf16 *x_in = nullptr, *target = nullptr;  // [m micro-batches of this rank's rows][h]
   bf16* dx_out = nullptr;                   // first stage: input gradient per micro-batch
   float *loss = nullptr, *loss_dummy = nullptr;
+  float* loss_ws = nullptr;  // deterministic loss reduction: block partials + ticket
   int64_t* step = nullptr;
   uint64_t* seed_off = nullptr;
   int64_t in_rows_total = 0;
   std::vector<int64_t> in_row_off;  // per micro-batch offset (rows) into x_in / target
   int cur = 0;                      // index of gbuf holding the current dY
-  bool dc_f32 = false, da_f32 = false;  // split-K results pending in acc32
+  int dc_slices = 0, da_slices = 0;  // split-K slices pending in acc32 (0 = bf16 result)
 };
 
 // --------------------------------------------------------------------------------------
@@ -208,10 +215,14 @@ class ExecutorImpl final : public Executor {
     for (cudaEvent_t e : events_) cudaEventDestroy(e);
     for (cudaEvent_t e : fork_events_) cudaEventDestroy(e);
     if (join_event_ != nullptr) cudaEventDestroy(join_event_);
+    for (auto& r : ranks_)
+      for (cudaEvent_t e : r->wg_done)
+        if (e != nullptr) cudaEventDestroy(e);
     ranks_.clear();
     comm_.reset();
     if (stream_ != nullptr) cudaStreamDestroy(stream_);
     if (side_ != nullptr) cudaStreamDestroy(side_);
+    if (wg_ != nullptr) cudaStreamDestroy(wg_);
   }
 
  private:
@@ -302,8 +313,8 @@ class ExecutorImpl final : public Executor {
     return timed(kComm, 0, 1.0 * n * dtype_bytes(t),
                  [&] { return comm_->all_gather(g, rank, a, b, c, t, st); });
   }
-  // Split-K into r.acc32 (fp32 [M][N]) when it pays (small M*N, long K); returns the split
-  // count used, 1 meaning "not split" (nothing launched).
+  // Split-K into r.acc32 (fp32 slices [splits][M][N], summed in order by the consumer) when
+  // it pays (small M*N, long K); *used = split count, 1 meaning "not split" (nothing launched).
   int gemm_splitk(RankCtx& r, const void* a, int64_t lda, const void* b, int64_t ldb, bool bmn,
                   int M, int N, int K, int* used) {
     *used = 1;
@@ -311,12 +322,10 @@ class ExecutorImpl final : public Executor {
     int tile = 0;
     const int sp = splitk_plan(M, N, K, &tile);
     if (sp < 2) return kOk;
-    GX_TRY(cuda_check(cudaMemsetAsync(r.acc32, 0, static_cast<size_t>(M) * N * 4, stream_),
-                      "memset acc32"));
     gx_gemm_epilogue e{};
     e.alpha = 1.f;
     e.drop_scale = 1.f;
-    e.out_kind = kOutF32Accumulate;
+    e.out_kind = kOutF32Split;
     e.out = r.acc32;
     e.ldo = N;
     const double flops = 2.0 * M * N * K;
@@ -334,7 +343,7 @@ class ExecutorImpl final : public Executor {
     const double bytes = 2.0 * (static_cast<double>(M) * K + static_cast<double>(N) * K) +
                          (ep.out_kind == kOutBF16 ? 2.0 : 4.0) * M * N;
     return timed(kGemm, flops, bytes, [&] {
-      return gemm_bf16(GemmOperand{a, lda, amn}, GemmOperand{b, ldb, bmn}, M, N, K, ep, stream_);
+      return gemm_bf16(GemmOperand{a, lda, amn}, GemmOperand{b, ldb, bmn}, M, N, K, ep, ls_);
     });
   }
  public:
@@ -371,6 +380,35 @@ class ExecutorImpl final : public Executor {
   // AdamW of layer l runs on side_ while layer l-1's backward runs on stream_ (HBM-bound
   // optimizer under tensor-bound GEMMs); joined back before the step ends.
   cudaStream_t side_ = nullptr;
+  // Weight-gradient GEMMs (and the bias column sums) of the backward run on wg_, forked
+  // from stream_ as soon as their inputs exist, so they fill the SMs the data-gradient
+  // chain (the critical path) leaves idle.  ls_ is the stream gemm() launches on.
+  cudaStream_t wg_ = nullptr;
+  cudaStream_t ls_ = nullptr;
+  bool wgrad_stream_ = true;  // GX_WGRAD_STREAM=0 / "wgrad_stream": false disables
+  bool wg_active_ = false;    // this capture forks (off while profiling)
+  bool wg_used_ = false;
+  int fork(cudaStream_t from, cudaStream_t to) {
+    if (fork_events_.size() <= static_cast<size_t>(fork_used_)) {
+      cudaEvent_t e;
+      GX_TRY(cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event"));
+      fork_events_.push_back(e);
+    }
+    cudaEvent_t e = fork_events_[fork_used_++];
+    GX_TRY(cuda_check(cudaEventRecord(e, from), "fork record"));
+    return cuda_check(cudaStreamWaitEvent(to, e, 0), "fork wait");
+  }
+  // Runs f with launches on the wgrad stream (after everything already on stream_).
+  template <class F>
+  int on_wgrad(F&& f) {
+    if (!wg_active_) return f();
+    GX_TRY(fork(stream_, wg_));
+    wg_used_ = true;
+    ls_ = wg_;
+    const int rc = f();
+    ls_ = stream_;
+    return rc;
+  }
   std::vector<cudaEvent_t> fork_events_;
   cudaEvent_t join_event_ = nullptr;
   cudaGraph_t graph_ = nullptr;
@@ -421,6 +459,8 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     splitk_ = cfg.value("splitk", true);
     if (const char* e = std::getenv("GX_SPLITK")) splitk_ = e[0] != '0';
     opt_blocks_ = cfg.value("optimizer_blocks", 0);
+    wgrad_stream_ = cfg.value("wgrad_stream", true);
+    if (const char* e = std::getenv("GX_WGRAD_STREAM")) wgrad_stream_ = e[0] != '0';
     if (const char* e = std::getenv("GX_OPT_BLOCKS")) opt_blocks_ = std::atoi(e);
     thr_attn_ = threshold_of(p_attn_);
     thr_hidden_ = threshold_of(p_hidden_);
@@ -538,10 +578,16 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
       *err = "executor: side stream creation failed";
       return kErrCuda;
     }
-    if (cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking) != cudaSuccess) {
+    // the data-gradient chain gets the highest priority, the wgrad stream the next
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    if (cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, hi_prio) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&wg_, cudaStreamNonBlocking,
+                                     hi_prio < lo_prio ? hi_prio + 1 : lo_prio) != cudaSuccess) {
       *err = "executor: cudaStreamCreate failed";
       return kErrCuda;
     }
+    ls_ = stream_;
     for (int r : local) {
       auto rc = std::make_unique<RankCtx>();
       rc->rank = r;
@@ -689,27 +735,34 @@ int ExecutorImpl::allocate(RankCtx& r) {
     }
   }
   r.partial = A.a<bf16>(max_h);
-  r.dz = A.a<bf16>(max_h);
-  r.dpre = A.a<bf16>(max_f);
+  for (int p = 0; p < 2; ++p) {
+    r.dzb[p] = A.a<bf16>(max_h);
+    r.dpreb[p] = A.a<bf16>(max_f);
+    r.doutb[p] = A.a<bf16>(max_h);
+    r.dqkvb[p] = A.a<bf16>(max_q);
+    if (cudaEventCreateWithFlags(&r.wg_done[p], cudaEventDisableTiming) != cudaSuccess)
+      return set_error(kErrCuda, "executor: event creation failed");
+  }
   r.dc = A.a<bf16>(max_h);
   r.dx1 = A.a<bf16>(max_h);
-  r.dout = A.a<bf16>(max_h);
   r.dctx = A.a<bf16>(max_c);
-  r.dqkv = A.a<bf16>(max_q);
   r.da = A.a<bf16>(max_h);
   r.gbuf[0] = A.a<bf16>(max_h);
   r.gbuf[1] = A.a<bf16>(max_h);
   r.dq_acc = A.a<float>(max_c);
-  r.acc32 = A.a<float>(max_h);
+  r.acc32 = A.a<float>(static_cast<int64_t>(kMaxSplits) * max_h);
   {
     int64_t max_hdim = 0;
     for (const RankLayer& L : r.layers) max_hdim = std::max<int64_t>(max_hdim, L.sh.h);
-    r.ln_ws = A.a<float>(static_cast<int64_t>(layernorm_bwd_blocks(static_cast<int>(max_rows))) * 2 *
-                         max_hdim);
+    r.ln_ws = A.a<float>(layernorm_bwd_ws_floats(static_cast<int>(max_hdim)));
+    if (r.ln_ws != nullptr)
+      cudaMemset(r.ln_ws, 0, layernorm_bwd_ws_floats(static_cast<int>(max_hdim)) * sizeof(float));
   }
   r.dsum = A.a<float>(max_lse);
   r.loss = A.a<float>(1);
   r.loss_dummy = A.a<float>(1);
+  r.loss_ws = A.a<float>(kLossBlocks + 1);
+  if (r.loss_ws != nullptr) cudaMemset(r.loss_ws, 0, (kLossBlocks + 1) * sizeof(float));
   r.step = A.a<int64_t>(1);
   r.seed_off = A.a<uint64_t>(1);
   cudaMemset(r.step, 0, 8);
@@ -1005,7 +1058,8 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
         d.drop_ld = h;
         d.seed_offset = r.seed_off;
         return timed(kElementwise, 0, 8.0 * rows * h, [&] {
-          return bias_dropout_add(r.acc32, P + L.lay.b2.off, A.x1, A.y, rows, h, d, stream_, true);
+          return bias_dropout_add(r.acc32, P + L.lay.b2.off, A.x1, A.y, rows, h, d, stream_, true, sp,
+                                  static_cast<int64_t>(rows) * h);
         });
       }
       o.out = A.y;
@@ -1060,6 +1114,8 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
   bf16* dY = r.gbuf[r.cur];
   bf16* dX = r.gbuf[r.cur ^ 1];
   if (rows == 0) return kOk;
+  const int par = li & 1;
+  bf16 *dz = r.dzb[par], *dpre = r.dpreb[par], *dout = r.doutb[par], *dqkv = r.dqkvb[par];
   gx_dropout d{};
   d.threshold = thr_hidden_;
   d.scale = scale_of(p_hidden_);
@@ -1068,35 +1124,43 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
   d.drop_ld = h;
   d.seed_offset = r.seed_off;
   if (phase == 0) {
+    // this parity's buffers are free once the wgrads that last read them are done
+    if (r.wg_pending[par]) {
+      GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, r.wg_done[par], 0), "wgrad wait"));
+      r.wg_pending[par] = false;
+    }
     d.site = 3ull * l + 2;
-    GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(dY, r.dz, G + L.lay.b2.off, rows, h, d, stream_); }));
+    GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(dY, dz, G + L.lay.b2.off, rows, h, d, stream_); }));
     gx_gemm_epilogue w = epi();
     w.out_kind = wk;
     w.out = G + L.lay.w2.off;
     w.ldo = ft;
-    GX_TRY(gemm(r.dz, h, true, A.gel, ft, true, h, ft, rows, w));  // dW2 = dz^T gel
+    GX_TRY(on_wgrad([&] { return gemm(dz, h, true, A.gel, ft, true, h, ft, rows, w); }));  // dW2 = dz^T gel
     gx_gemm_epilogue e = epi();
     e.out_kind = kOutBF16;
-    e.out = r.dpre;
+    e.out = dpre;
     e.ldo = ft;
     e.gelu_bwd = 1;
     e.aux = A.pre;
     e.ld_aux = ft;
-    GX_TRY(gemm(r.dz, h, false, P + L.lay.w2.off, ft, true, rows, ft, h, e));  // dz W2 * gelu'
-    GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(r.dpre, ft, G + L.lay.b1.off, rows, ft, stream_); }));
-    w.out = G + L.lay.w1.off;
-    w.ldo = h;
-    GX_TRY(gemm(r.dpre, ft, true, A.ln2, h, true, ft, h, rows, w));  // dW1 = dpre^T ln2
+    GX_TRY(gemm(dz, h, false, P + L.lay.w2.off, ft, true, rows, ft, h, e));  // dz W2 * gelu'
+    GX_TRY(on_wgrad([&]() -> int {
+      GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dpre, ft, G + L.lay.b1.off, rows, ft, ls_); }));
+      gx_gemm_epilogue w1 = w;
+      w1.out = G + L.lay.w1.off;
+      w1.ldo = h;
+      return gemm(dpre, ft, true, A.ln2, h, true, ft, h, rows, w1);  // dW1 = dpre^T ln2
+    }));
     int sp_c = 1;
     if (t == 1)
-      GX_TRY(gemm_splitk(r, r.dpre, ft, P + L.lay.w1.off, h, true, rows, h, ft, &sp_c));
-    r.dc_f32 = sp_c > 1;
+      GX_TRY(gemm_splitk(r, dpre, ft, P + L.lay.w1.off, h, true, rows, h, ft, &sp_c));
+    r.dc_slices = sp_c > 1 ? sp_c : 0;
     if (sp_c == 1) {
       gx_gemm_epilogue c = epi();
       c.out_kind = kOutBF16;
       c.out = r.dc;
       c.ldo = h;
-      GX_TRY(gemm(r.dpre, ft, false, P + L.lay.w1.off, h, true, rows, h, ft, c));  // dpre W1
+      GX_TRY(gemm(dpre, ft, false, P + L.lay.w1.off, h, true, rows, h, ft, c));  // dpre W1
     }
     if (t > 1)
       return c_all_reduce(L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
@@ -1104,21 +1168,23 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     phase = 1;
   }
   if (phase == 1) {
-    const void* dc_in = r.dc_f32 ? static_cast<const void*>(r.acc32) : static_cast<const void*>(r.dc);
-    GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd(dc_in, A.x1, A.mean2, A.rstd2, P + L.lay.ln2g.off, dY, r.dx1,
-                         G + L.lay.ln2g.off, G + L.lay.ln2b.off, rows, h, r.ln_ws, stream_, r.dc_f32); }));
+    const void* dc_in = r.dc_slices ? static_cast<const void*>(r.acc32) : static_cast<const void*>(r.dc);
+    // LN2 backward with the out-projection's dropout backward + bias gradient fused in:
+    // dx1 = residual-stream gradient, dout = dropout_mask(dx1), dbo += colsum(dout)
     d.site = 3ull * l + 1;
-    GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(r.dx1, r.dout, G + L.lay.bo.off, rows, h, d, stream_); }));
+    GX_TRY(timed(kNorm, 0, 10.0 * rows * h, [&] { return layernorm_bwd(dc_in, A.x1, A.mean2, A.rstd2, P + L.lay.ln2g.off, dY, r.dx1,
+                         G + L.lay.ln2g.off, G + L.lay.ln2b.off, rows, h, r.ln_ws, stream_, r.dc_slices > 0,
+                         &d, dout, G + L.lay.bo.off, std::max(1, r.dc_slices), static_cast<int64_t>(rows) * h); }));
     gx_gemm_epilogue w = epi();
     w.out_kind = wk;
     w.out = G + L.lay.wo.off;
     w.ldo = ht;
-    GX_TRY(gemm(r.dout, h, true, A.ctx, ht, true, h, ht, rows, w));  // dWo = dout^T ctx
+    GX_TRY(on_wgrad([&] { return gemm(dout, h, true, A.ctx, ht, true, h, ht, rows, w); }));  // dWo = dout^T ctx
     gx_gemm_epilogue c = epi();
     c.out_kind = kOutBF16;
     c.out = r.dctx;
     c.ldo = ht;
-    GX_TRY(gemm(r.dout, h, false, P + L.lay.wo.off, ht, true, rows, ht, h, c));  // dout Wo
+    GX_TRY(gemm(dout, h, false, P + L.lay.wo.off, ht, true, rows, ht, h, c));  // dout Wo
     gx_attention_args at{};
     at.batch = A.samples;
     at.seq = s.seq;
@@ -1134,7 +1200,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     at.ld_ctx = ht;
     at.lse = A.lse;
     at.dctx = r.dctx;
-    at.dqkv = r.dqkv;
+    at.dqkv = dqkv;
     at.dq_accum = r.dq_acc;
     at.dsum = r.dsum;
     at.drop_threshold = thr_attn_;
@@ -1147,20 +1213,27 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       const double af = 10.0 * A.samples * (s.heads / t) * double(s.seq) * s.seq * s.hd;
       GX_TRY(timed(kAttnBwd, af, 2.0 * rows * 8 * ht, [&] { return attention_bwd(at, stream_); }));
     }
-    GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(r.dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, stream_); }));
-    w.out = G + L.lay.wqkv.off;
-    w.ldo = h;
-    GX_TRY(gemm(r.dqkv, 3 * ht, true, A.ln1, h, true, 3 * ht, h, rows, w));  // dWqkv
+    GX_TRY(on_wgrad([&]() -> int {
+      GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, ls_); }));
+      w.out = G + L.lay.wqkv.off;
+      w.ldo = h;
+      GX_TRY(gemm(dqkv, 3 * ht, true, A.ln1, h, true, 3 * ht, h, rows, w));  // dWqkv
+      if (wg_active_) {  // the last reader of this parity's buffers
+        GX_TRY(cuda_check(cudaEventRecord(r.wg_done[par], wg_), "wgrad done"));
+        r.wg_pending[par] = true;
+      }
+      return kOk;
+    }));
     int sp_a = 1;
     if (t == 1)
-      GX_TRY(gemm_splitk(r, r.dqkv, 3 * ht, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, &sp_a));
-    r.da_f32 = sp_a > 1;
+      GX_TRY(gemm_splitk(r, dqkv, 3 * ht, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, &sp_a));
+    r.da_slices = sp_a > 1 ? sp_a : 0;
     if (sp_a == 1) {
       gx_gemm_epilogue a = epi();
       a.out_kind = kOutBF16;
       a.out = r.da;
       a.ldo = h;
-      GX_TRY(gemm(r.dqkv, 3 * ht, false, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, a));
+      GX_TRY(gemm(dqkv, 3 * ht, false, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, a));
     }
     if (t > 1)
       return c_all_reduce(L.g_tp, r.rank, r.da, static_cast<size_t>(rows) * h, DType::kBF16,
@@ -1168,9 +1241,10 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     phase = 2;
   }
   if (phase == 2) {
-    const void* da_in = r.da_f32 ? static_cast<const void*>(r.acc32) : static_cast<const void*>(r.da);
+    const void* da_in = r.da_slices ? static_cast<const void*>(r.acc32) : static_cast<const void*>(r.da);
     GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd(da_in, A.x, A.mean1, A.rstd1, P + L.lay.ln1g.off, r.dx1, dX,
-                         G + L.lay.ln1g.off, G + L.lay.ln1b.off, rows, h, r.ln_ws, stream_, r.da_f32); }));
+                         G + L.lay.ln1g.off, G + L.lay.ln1b.off, rows, h, r.ln_ws, stream_, r.da_slices > 0,
+                         nullptr, nullptr, nullptr, std::max(1, r.da_slices), static_cast<int64_t>(rows) * h); }));
   }
   return kOk;
 }
@@ -1178,7 +1252,11 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
 // Gradient synchronisation + optimizer after the layer's last backward micro-batch.
 int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
   RankLayer& L = r.layers[li];
+  const int par = li & 1;
   if (phase == 0) {
+    // the gradient collectives read what this layer's wgrads (wgrad stream) wrote
+    if (wg_active_ && (L.d.sdp > 1 || L.d.dp > 1))
+      GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, r.wg_done[par], 0), "wgrad join"));
     if (L.d.sdp > 1)
       return c_reduce_scatter(L.g_sdp, r.rank, L.gfull, L.gshard,
                                    static_cast<size_t>(L.shard_n), DType::kF32, stream_);
@@ -1207,6 +1285,8 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
     cudaEvent_t e = fork_events_[fork_used_++];
     GX_TRY(cuda_check(cudaEventRecord(e, stream_), "fork record"));
     GX_TRY(cuda_check(cudaStreamWaitEvent(side_, e, 0), "fork wait"));
+    if (wg_active_)  // ... and for the weight gradients
+      GX_TRY(cuda_check(cudaStreamWaitEvent(side_, r.wg_done[par], 0), "fork wait wgrad"));
     side_used_ = true;
     return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_, wd_,
                      r.step, side_, opt_blocks_);
@@ -1406,6 +1486,10 @@ std::string ExecutorImpl::topology() const {
 int ExecutorImpl::step_once() {
   fork_used_ = 0;
   side_used_ = false;
+  wg_used_ = false;
+  wg_active_ = wgrad_stream_ && !profiling_;
+  ls_ = stream_;
+  for (auto& r : ranks_) r->wg_pending[0] = r->wg_pending[1] = false;
   auto in_stage = [&](int st) {
     std::vector<RankCtx*> v;
     for (auto& r : ranks_)
@@ -1460,7 +1544,7 @@ int ExecutorImpl::step_once() {
           if (n > 0)
             GX_TRY(mse_loss(a.y, r->target + off * Lz.sh.h, r->gbuf[0], Lz.tr == 0 ? r->loss
                                                                                       : r->loss_dummy,
-                            n, inv_count_, stream_));
+                            n, inv_count_, stream_, r->loss_ws));
         }
       }
       if (st + 1 < P_) {
@@ -1507,6 +1591,9 @@ int ExecutorImpl::step_once() {
         }
       }
     }
+  }
+  if (wg_used_) {  // join the wgrad stream
+    GX_TRY(fork(wg_, stream_));
   }
   if (side_used_) {  // join the optimizer stream before the step completes
     GX_TRY(cuda_check(cudaEventRecord(join_event_, side_), "join record"));

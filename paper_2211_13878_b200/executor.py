@@ -73,12 +73,13 @@ class PlanExecutor:
     def __init__(self, plan: dict, model: dict, world_size: int, local_ranks=None,
                  comm: str = "sim", nccl_id_hex: str = "", dropout_attn=0.0, dropout_hidden=0.0,
                  seed=1234, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0,
-                 optimizer=True, forward_only=False, splitk=True):
+                 optimizer=True, forward_only=False, splitk=True, **options):
         cfg = {"plan": plan, "model": model, "world_size": world_size, "comm": comm,
                "dropout_attn": dropout_attn, "dropout_hidden": dropout_hidden, "seed": seed,
                "lr": lr, "beta1": beta1, "beta2": beta2, "eps": eps,
                "weight_decay": weight_decay, "optimizer": optimizer,
                "forward_only": forward_only, "splitk": splitk}
+        cfg.update(options)  # executor knobs, e.g. wgrad_stream=False
         if local_ranks is not None:
             cfg["local_ranks"] = list(local_ranks)
         if comm == "nccl":
