@@ -544,6 +544,7 @@ static int attention_bwd_impl(const gx_attention_args& a, cudaStream_t st) {
 
 int attention_fwd(const gx_attention_args& a, cudaStream_t st) {
   if (a.seq <= 0 || a.batch <= 0 || a.heads <= 0) return set_error(kErrConfig, "attention: empty");
+  if (attention_tc_supported(a)) return attention_fwd_tc(a, st);
   switch (a.head_dim) {
     case 64: return attention_fwd_impl<64>(a, st);
     case 80: return attention_fwd_impl<80>(a, st);
@@ -554,6 +555,7 @@ int attention_fwd(const gx_attention_args& a, cudaStream_t st) {
 
 int attention_bwd(const gx_attention_args& a, cudaStream_t st) {
   if (a.seq <= 0 || a.batch <= 0 || a.heads <= 0) return set_error(kErrConfig, "attention: empty");
+  if (attention_tc_supported(a) && (a.ld_ctx % 8) == 0) return attention_bwd_tc(a, st);
   switch (a.head_dim) {
     case 64: return attention_bwd_impl<64>(a, st);
     case 80: return attention_bwd_impl<80>(a, st);

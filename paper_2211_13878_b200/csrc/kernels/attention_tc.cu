@@ -1,0 +1,675 @@
+// attention_tc.cu — attention forward on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+//   ctx = dropout(softmax(Q K^T * scale)) V        one CTA per (sample*head, 128-query tile)
+//
+// Same contract as attention.cu's forward (ctx, lse in log2 units, 16-bit keep masks with the
+// identical Philox call -> key mapping), restated for sm_100a with the whole key range of a
+// head resident on chip (seq <= 512, head_dim 64):
+//   1. one thread issues TMA loads of Q [128 x 64], K and V [NK x 64] (NK = seq rounded up to
+//      64; rows past the sample read as finite neighbours or zero fill and are masked) into
+//      128B-swizzled smem, then tcgen05.mma S = Q K^T into TMEM columns [0, NK) (fp32);
+//   2. eight warps (two per TMEM lane quarter, each half the key columns) read S back with
+//      tcgen05.ld: pass 1 row max, pass 2 exp2, row sum, Philox dropout, bf16 P written into
+//      smem in the UMMA K-major SWIZZLE_128B layout (over the dead Q/K tiles), keep bits to
+//      global for the backward;
+//   3. tcgen05.mma O = P V (V as an MN-major operand, straight from its TMA tile) into TMEM
+//      columns [0, 64), and the epilogue scales by 1/rowsum and stores bf16 ctx.
+// No online rescaling is needed: the full row of scores is in TMEM when the max is taken.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "gx_internal.h"
+#include "launch.cuh"
+#include "philox.cuh"
+#include "sm100.cuh"
+
+namespace gx {
+
+namespace {
+
+constexpr int kTcQ = 128;       // queries per CTA (UMMA M)
+constexpr int kTcHD = 64;       // head dim (one 128 B swizzle row)
+constexpr int kTcMaxKeys = 512; // TMEM columns
+constexpr int kTcThreads = 256;
+
+struct TcLayout {
+  int nk;          // keys rounded up to 64
+  int qk_bytes;    // Q + K tiles (P groups overlay them first)
+  int v_off;       // V tile
+  int p_hi_off;    // P groups that do not fit over Q + K
+  int p_lo_groups; // P groups placed at [0, qk_bytes)
+  int red_off;     // row max / row sum exchange [2][2][128] floats
+  int bar_off;
+  int bytes;
+};
+
+__host__ __device__ inline TcLayout tc_layout(int seq) {
+  TcLayout L{};
+  L.nk = (seq + 63) / 64 * 64;
+  L.qk_bytes = kTcQ * 128 + L.nk * 128;
+  L.v_off = L.qk_bytes;
+  const int groups = L.nk / 64;
+  L.p_lo_groups = L.qk_bytes / (16 * 1024);
+  if (L.p_lo_groups > groups) L.p_lo_groups = groups;
+  L.p_hi_off = L.v_off + L.nk * 128;
+  const int hi = groups - L.p_lo_groups;
+  L.red_off = L.p_hi_off + hi * 16 * 1024;
+  L.bar_off = L.red_off + 4 * kTcQ * 4;
+  L.bytes = L.bar_off + 64;
+  return L;
+}
+
+__device__ __forceinline__ uint32_t p_group_addr(const TcLayout& L, uint32_t base, int g) {
+  return g < L.p_lo_groups ? base + g * 16384 : base + L.p_hi_off + (g - L.p_lo_groups) * 16384;
+}
+
+__device__ __forceinline__ float ex2_ftz(float x) {  // MUFU.EX2, no denormal fix-up
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void fence_proxy_async_smem_tc() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void st_shared_v4_tc(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
+                                                uint32_t d) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+
+}  // namespace
+
+template <uint32_t kCols>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const gx_attention_args p) {
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-align by offsetting the shared array itself, so every access below stays in the
+  // shared state space (an integer-cast pointer would compile to generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int s = p.seq;
+  const TcLayout L = tc_layout(s);
+  const uint32_t sbase = smem_u32(smem);
+  float* red = reinterpret_cast<float*>(smem + L.red_off);  // [max|sum][half][128]
+  uint64_t* bar_qk = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+  uint64_t* bar_v = bar_qk + 1;
+  uint64_t* bar_s = bar_qk + 2;
+  uint64_t* bar_o = bar_qk + 3;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_qk + 4);
+
+  const int warp = static_cast<int>(warp_id());
+  const int lane = static_cast<int>(lane_id());
+  const int H = p.heads;
+  const int bh = blockIdx.y;
+  const int b = bh / H, h = bh % H;
+  const int q0 = blockIdx.x * kTcQ;
+  const int nk = L.nk;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_qkv);
+    mbar_init(bar_qk, 1);
+    mbar_init(bar_v, 1);
+    mbar_init(bar_s, 1);
+    mbar_init(bar_o, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<kCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_enter();
+
+  // ---------------------------------------------------------------- loads + S = Q K^T
+  if (threadIdx.x == 0) {
+    const int row0 = b * s;  // first token row of this sample
+    const int slot_q = h, slot_k = H + h, slot_v = 2 * H + h;
+    // 64-row boxes (128 B rows, 128B swizzle): Q 2 boxes, K and V nk/64 boxes each
+    mbar_expect_tx(bar_qk, (kTcQ + nk) * 128);
+    tma_load_3d(smem, &map_qkv, bar_qk, 0, slot_q, row0 + q0);
+    tma_load_3d(smem + 64 * 128, &map_qkv, bar_qk, 0, slot_q, row0 + q0 + 64);
+    for (int r = 0; r < nk; r += 64)
+      tma_load_3d(smem + kTcQ * 128 + r * 128, &map_qkv, bar_qk, 0, slot_k, row0 + r);
+    mbar_expect_tx(bar_v, nk * 128);
+    for (int r = 0; r < nk; r += 64)
+      tma_load_3d(smem + L.v_off + r * 128, &map_qkv, bar_v, 0, slot_v, row0 + r);
+    mbar_wait(bar_qk, 0);
+    tc_fence_after();
+    for (int n0 = 0; n0 < nk; n0 += 256) {
+      const int n = nk - n0 < 256 ? nk - n0 : 256;
+      const uint32_t idesc = idesc_bf16_f32(kTcQ, n, false, false);
+#pragma unroll
+      for (int k = 0; k < kTcHD / 16; ++k) {
+        const uint64_t ad = sdesc_sw128(sbase + k * 32, 16, 1024);
+        const uint64_t bd = sdesc_sw128(sbase + kTcQ * 128 + n0 * 128 + k * 32, 16, 1024);
+        umma_bf16(tmem + n0, ad, bd, idesc, k != 0 ? 1u : 0u);
+      }
+    }
+    umma_commit(bar_s);
+  }
+
+  // ---------------------------------------------------------------- softmax over TMEM rows
+  const int qd = warp & 3, hf = warp >> 2;
+  const int r = qd * 32 + lane;  // tile row == TMEM lane
+  const int q = q0 + r;
+  const int half = nk / 2;       // multiple of 32
+  const int c_begin = hf * half, c_end = c_begin + half;
+  const uint32_t trow = tmem + (static_cast<uint32_t>(qd * 32) << 16);
+  const float c2 = p.scale * 1.4426950408889634f;
+  mbar_wait(bar_s, 0);
+  tc_fence_after();
+
+  float mx = -INFINITY;
+  for (int c0 = c_begin; c0 < c_end; c0 += 32) {
+    uint32_t v[32];
+    tmem_ld32(trow + c0, v);
+    tmem_ld_wait();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float x = c0 + j < s ? __uint_as_float(v[j]) * c2 : -INFINITY;
+      mx = fmaxf(mx, x);
+    }
+  }
+  red[hf * kTcQ + r] = mx;
+  named_sync(1, kTcThreads);
+  const float m = fmaxf(red[r], red[kTcQ + r]);
+
+  const uint32_t thr = p.drop_threshold;
+  const float inv_keep = p.drop_scale;
+  const uint64_t seed = p.seed + (p.seed_offset != nullptr ? *p.seed_offset : 0ull);
+  const int nkb = (s + 63) / 64;
+  const uint64_t stream =
+      (static_cast<uint64_t>(p.sample_offset + b) * p.heads_total + (p.head_offset + h)) * s;
+  uint16_t* mask = static_cast<uint16_t*>(p.mask);
+  const bool row_ok = q < s;
+  float sum = 0.f;
+  int cached_kb = -1;
+  uint32_t bits[4] = {0u, 0u, 0u, 0u};
+  for (int c0 = c_begin; c0 < c_end; c0 += 32) {
+    uint32_t v[32];
+    tmem_ld32(trow + c0, v);
+    tmem_ld_wait();
+    float e[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      e[j] = c0 + j < s ? ex2_ftz(__uint_as_float(v[j]) * c2 - m) : 0.f;
+      sum += e[j];
+    }
+    const int kb = c0 >> 6;
+    if (thr != 0u) {
+      if (kb != cached_kb) {
+        cached_kb = kb;
+        const uint64_t call0 = ((stream + static_cast<uint64_t>(q)) * nkb + kb) * 4;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) bits[t] = keep16(seed, p.site, call0 + t, thr);
+        if (row_ok && kb < nkb) {
+          const uint64_t packed = static_cast<uint64_t>(bits[0]) |
+                                  (static_cast<uint64_t>(bits[1]) << 16) |
+                                  (static_cast<uint64_t>(bits[2]) << 32) |
+                                  (static_cast<uint64_t>(bits[3]) << 48);
+          *reinterpret_cast<uint64_t*>(mask + ((static_cast<int64_t>(bh) * s + q) * nkb + kb) * 4) =
+              packed;
+        }
+      }
+      // key i of this 32-key half: word t = (i/2)%4, bit 8*hb + 2*(i/8) + i%2
+      const int hb = (c0 >> 5) & 1;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const uint32_t bit = (bits[(i >> 1) & 3] >> (8 * hb + 2 * (i >> 3) + (i & 1))) & 1u;
+        e[i] = bit ? e[i] * inv_keep : 0.f;
+      }
+    }
+    // bf16 P row segment -> K-major SWIZZLE_128B tile of its 64-key group
+    const uint32_t g_addr = p_group_addr(L, sbase, kb) + r * 128;
+    const int chunk0 = (c0 & 63) >> 3;  // 0 or 4
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t sw = static_cast<uint32_t>((chunk0 + i) ^ (r & 7));
+      st_shared_v4_tc(g_addr + (sw << 4), pack_bf16(e[8 * i + 0], e[8 * i + 1]),
+                      pack_bf16(e[8 * i + 2], e[8 * i + 3]), pack_bf16(e[8 * i + 4], e[8 * i + 5]),
+                      pack_bf16(e[8 * i + 6], e[8 * i + 7]));
+    }
+  }
+  red[2 * kTcQ + hf * kTcQ + r] = sum;
+  fence_proxy_async_smem_tc();  // P (generic stores) -> visible to the tensor core
+  tc_fence_before();
+  named_sync(1, kTcThreads);
+  const float l = red[2 * kTcQ + r] + red[3 * kTcQ + r];
+
+  // ---------------------------------------------------------------- O = P V
+  if (threadIdx.x == 0) {
+    tc_fence_after();
+    mbar_wait(bar_v, 0);
+    const uint32_t idesc = idesc_bf16_f32(kTcQ, kTcHD, false, true);
+    for (int kk = 0; kk < nk / 16; ++kk) {
+      const uint64_t ad = sdesc_sw128(p_group_addr(L, sbase, kk >> 2) + (kk & 3) * 32, 16, 1024);
+      const uint64_t bd = sdesc_sw128(sbase + L.v_off + kk * 2048, nk * 128, 1024);
+      umma_bf16(tmem, ad, bd, idesc, kk != 0 ? 1u : 0u);
+    }
+    umma_commit(bar_o);
+  }
+  if (hf == 0 && row_ok) {
+    auto* lse = static_cast<float*>(p.lse);
+    lse[static_cast<int64_t>(bh) * s + q] = m + log2f(l);
+  }
+  mbar_wait(bar_o, 0);
+  tc_fence_after();
+  {
+    uint32_t o[32];
+    tmem_ld32(trow + hf * 32, o);
+    tmem_ld_wait();
+    if (row_ok) {
+      const float inv = 1.f / l;
+      auto* ctx = static_cast<__nv_bfloat16*>(p.ctx);
+      uint4* out = reinterpret_cast<uint4*>(ctx + (static_cast<int64_t>(b) * s + q) * p.ld_ctx +
+                                            h * kTcHD + hf * 32);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        out[i] = make_uint4(pack_bf16(__uint_as_float(o[8 * i + 0]) * inv, __uint_as_float(o[8 * i + 1]) * inv),
+                            pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv),
+                            pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv),
+                            pack_bf16(__uint_as_float(o[8 * i + 6]) * inv, __uint_as_float(o[8 * i + 7]) * inv));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<kCols>(tmem);
+  }
+}
+
+// ------------------------------------------------------------------------------ backward
+// One CTA per (sample*head, 128-key tile); the queries stream through in 128-row chunks
+// (double-buffered TMA).  Per chunk j, with K, V of the tile resident:
+//   S^T = K Q_j^T and dPd^T = V dO_j^T                 (tcgen05, TMEM cols [0,128) / [128,256))
+//   P = exp2(S*c2 - lse), Pd = drop(P), dP = drop(dPd), dS = P (dP - D)   (thread = key row)
+//   dV += Pd^T dO_j, dK += dS^T Q_j                     (TMEM cols [256,320) / [320,384))
+//   dQ_j = dS K  (dS^T's smem tile read as an MN-major A operand) -> fp32 partial per key tile
+// lse and the keep words of every query are staged in smem once; D = rowsum(dO * O) is
+// computed per chunk from the dO / O tiles in smem.  The key tiles of a head form one
+// thread-block cluster: after a cluster barrier, CTA t sums the dQ partials of query chunk t
+// over the key tiles in key-tile order, so the result is deterministic and the reduction is
+// spread over the cluster.
+namespace {
+struct BwdLayout {
+  static constexpr int kK = 0, kV = 16384, kQ = 32768, kDO = 65536, kO = 98304, kPd = 131072,
+                       kDS = 163840, kLse = 196608 /* [512] */, kD = kLse + 2048 /* [128] */,
+                       kMask = kD + 512 /* [512 q][2 kb][4] u16 */, kBar = kMask + 8192,
+                       kBytes = kBar + 128;
+};
+}  // namespace
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv,
+                       const __grid_constant__ CUtensorMap map_do,
+                       const __grid_constant__ CUtensorMap map_o, const gx_attention_args p) {
+  using BL = BwdLayout;
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-align by offsetting the shared array itself, so every access below stays in the
+  // shared state space (an integer-cast pointer would compile to generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sb = smem_u32(smem);
+  float* sLse = reinterpret_cast<float*>(smem + BL::kLse);
+  float* sD = reinterpret_cast<float*>(smem + BL::kD);
+  uint16_t* sMask = reinterpret_cast<uint16_t*>(smem + BL::kMask);  // [512 q][2 kb][4]
+  uint64_t* bar_kv = reinterpret_cast<uint64_t*>(smem + BL::kBar);
+  uint64_t* bar_ld = bar_kv + 1;  // [2]
+  uint64_t* bar_s = bar_kv + 3;
+  uint64_t* bar_mm = bar_kv + 4;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_kv + 5);
+
+  const int warp = static_cast<int>(warp_id());
+  const int lane = static_cast<int>(lane_id());
+  const int s = p.seq, H = p.heads;
+  const int bh = blockIdx.y;
+  const int b = bh / H, h = bh % H;
+  const int kt = blockIdx.x;  // key tile
+  const int nkt = gridDim.x;
+  const int nq = (s + kTcQ - 1) / kTcQ;
+  const int nkb = (s + 63) / 64;
+  const int row0 = b * s;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_qkv);
+    tma_prefetch(&map_do);
+    tma_prefetch(&map_o);
+    mbar_init(bar_kv, 1);
+    mbar_init(&bar_ld[0], 1);
+    mbar_init(&bar_ld[1], 1);
+    mbar_init(bar_s, 1);
+    mbar_init(bar_mm, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_enter();
+
+  auto load_chunk = [&](int j) {  // Q_j, dO_j, O_j -> buffer j & 1
+    const int bf = j & 1;
+    const int r = row0 + j * kTcQ;
+    mbar_expect_tx(&bar_ld[bf], 3 * kTcQ * 128);
+    for (int x = 0; x < 2; ++x) {
+      tma_load_3d(smem + BL::kQ + bf * 16384 + x * 8192, &map_qkv, &bar_ld[bf], 0, h, r + 64 * x);
+      tma_load_3d(smem + BL::kDO + bf * 16384 + x * 8192, &map_do, &bar_ld[bf], 0, h, r + 64 * x);
+      tma_load_3d(smem + BL::kO + bf * 16384 + x * 8192, &map_o, &bar_ld[bf], 0, h, r + 64 * x);
+    }
+  };
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(bar_kv, 2 * kTcQ * 128);
+    for (int x = 0; x < 2; ++x) {
+      tma_load_3d(smem + BL::kK + x * 8192, &map_qkv, bar_kv, 0, H + h, row0 + kt * 128 + 64 * x);
+      tma_load_3d(smem + BL::kV + x * 8192, &map_qkv, bar_kv, 0, 2 * H + h, row0 + kt * 128 + 64 * x);
+    }
+    load_chunk(0);
+  }
+  {  // lse and keep words of every query of the head (once; overlaps the TMA loads)
+    const float* lse_g = static_cast<const float*>(p.lse) + static_cast<int64_t>(bh) * s;
+    const uint16_t* mask_g = static_cast<const uint16_t*>(p.mask);
+    for (int q = threadIdx.x; q < s; q += kTcThreads) sLse[q] = lse_g[q];
+    for (int i = threadIdx.x; i < 2 * s; i += kTcThreads) {
+      const int q = i >> 1, kb = kt * 2 + (i & 1);
+      uint64_t w = 0;
+      if (p.drop_threshold != 0u && kb < nkb)
+        w = *reinterpret_cast<const uint64_t*>(mask_g + ((static_cast<int64_t>(bh) * s + q) * nkb + kb) * 4);
+      *reinterpret_cast<uint64_t*>(sMask + i * 4) = w;
+    }
+  }
+
+  const int qd = warp & 3, hf = warp >> 2;
+  const int kr = qd * 32 + lane;      // key row of the tile == TMEM lane (S^T, dV, dK)
+  const int key = kt * 128 + kr;
+  const uint32_t trow = tmem + (static_cast<uint32_t>(qd * 32) << 16);
+  const float c2 = p.scale * 1.4426950408889634f;
+  const uint32_t thr = p.drop_threshold;
+  const float inv_keep = p.drop_scale;
+  const int kbl = kr >> 6, kk = kr & 63;
+  const int mt = (kk >> 1) & 3, mbit = 2 * (kk >> 3) + (kk & 1);
+  float* part = static_cast<float*>(p.dq_accum);
+  const uint32_t idesc_s = idesc_bf16_f32(kTcQ, 128, false, false);
+  const uint32_t idesc_kv = idesc_bf16_f32(128, kTcHD, false, true);
+  const uint32_t idesc_q = idesc_bf16_f32(kTcQ, kTcHD, true, true);
+
+  for (int j = 0; j < nq; ++j) {
+    const int bf = j & 1;
+    const uint32_t ld_phase = (j >> 1) & 1;
+    if (threadIdx.x == 0) {
+      if (j + 1 < nq) load_chunk(j + 1);  // its buffer's readers (chunk j-1) are done
+      if (j == 0) mbar_wait(bar_kv, 0);
+      mbar_wait(&bar_ld[bf], ld_phase);
+      tc_fence_after();
+      const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
+#pragma unroll
+      for (int k = 0; k < kTcHD / 16; ++k) {
+        umma_bf16(tmem, sdesc_sw128(sb + BL::kK + k * 32, 16, 1024),
+                  sdesc_sw128(q_b + k * 32, 16, 1024), idesc_s, k != 0 ? 1u : 0u);
+        umma_bf16(tmem + 128, sdesc_sw128(sb + BL::kV + k * 32, 16, 1024),
+                  sdesc_sw128(do_b + k * 32, 16, 1024), idesc_s, k != 0 ? 1u : 0u);
+      }
+      umma_commit(bar_s);
+    }
+    // D = rowsum(dO * O), lse and keep words of this chunk's 128 queries -> smem
+    mbar_wait(&bar_ld[bf], ld_phase);
+    {
+      const int qi = threadIdx.x >> 1, hh = threadIdx.x & 1;
+      const int q = j * kTcQ + qi;
+      const uint8_t* dob = smem + BL::kDO + bf * 16384 + qi * 128;
+      const uint8_t* ob = smem + BL::kO + bf * 16384 + qi * 128;
+      float acc = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int cc = hh * 4 + c;
+        const int sw = (cc ^ (qi & 7)) << 4;
+        const uint4 a = *reinterpret_cast<const uint4*>(dob + sw);
+        const uint4 o = *reinterpret_cast<const uint4*>(ob + sw);
+        const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          acc += bf16_lo(aw[t]) * bf16_lo(ow[t]) + bf16_hi(aw[t]) * bf16_hi(ow[t]);
+      }
+      acc += __shfl_xor_sync(0xffffffff, acc, 1);
+      if (hh == 0) sD[qi] = acc;
+      (void)q;
+    }
+    named_sync(1, kTcThreads);
+    mbar_wait(bar_s, j & 1);
+    tc_fence_after();
+    // P, Pd, dS for key row kr x queries [hf*64, hf*64 + 64)
+#pragma unroll 1
+    for (int sc = 0; sc < 2; ++sc) {
+      const int c0 = hf * 64 + sc * 32;
+      uint32_t sv[32], dv[32];
+      tmem_ld32(trow + c0, sv);
+      tmem_ld32(trow + 128 + c0, dv);
+      tmem_ld_wait();
+      float pd[32], ds[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int qi = c0 + i;
+        const int qg = j * kTcQ + qi;
+        const bool valid = (qg < s) && (key < s);
+        const float pr = valid ? ex2_ftz(__uint_as_float(sv[i]) * c2 - sLse[qg]) : 0.f;
+        float dp = __uint_as_float(dv[i]);
+        float pdv = pr;
+        if (thr != 0u) {
+          const bool keep = valid && ((sMask[(qg * 2 + kbl) * 4 + mt] >> mbit) & 1u) != 0u;
+          pdv = keep ? pr * inv_keep : 0.f;
+          dp = keep ? dp * inv_keep : 0.f;
+        }
+        pd[i] = pdv;
+        ds[i] = pr * (dp - sD[qi]);
+      }
+      const uint32_t rowoff = static_cast<uint32_t>(hf * 16384 + kr * 128);
+      const int chunk0 = (c0 & 63) >> 3;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t sw = static_cast<uint32_t>((chunk0 + i) ^ (kr & 7)) << 4;
+        st_shared_v4_tc(sb + BL::kPd + rowoff + sw, pack_bf16(pd[8 * i], pd[8 * i + 1]),
+                        pack_bf16(pd[8 * i + 2], pd[8 * i + 3]), pack_bf16(pd[8 * i + 4], pd[8 * i + 5]),
+                        pack_bf16(pd[8 * i + 6], pd[8 * i + 7]));
+        st_shared_v4_tc(sb + BL::kDS + rowoff + sw, pack_bf16(ds[8 * i], ds[8 * i + 1]),
+                        pack_bf16(ds[8 * i + 2], ds[8 * i + 3]), pack_bf16(ds[8 * i + 4], ds[8 * i + 5]),
+                        pack_bf16(ds[8 * i + 6], ds[8 * i + 7]));
+      }
+    }
+    fence_proxy_async_smem_tc();
+    tc_fence_before();
+    named_sync(1, kTcThreads);
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+      const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
+#pragma unroll
+      for (int k = 0; k < kTcQ / 16; ++k) {  // K = 128 queries (dV, dK) / 128 keys (dQ)
+        const uint32_t a_kmaj = (k >> 2) * 16384 + (k & 3) * 32;
+        const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
+        umma_bf16(tmem + 256, sdesc_sw128(sb + BL::kPd + a_kmaj, 16, 1024),
+                  sdesc_sw128(do_b + k * 2048, 16384, 1024), idesc_kv, acc);
+        umma_bf16(tmem + 320, sdesc_sw128(sb + BL::kDS + a_kmaj, 16, 1024),
+                  sdesc_sw128(q_b + k * 2048, 16384, 1024), idesc_kv, acc);
+        umma_bf16(tmem + 384, sdesc_sw128(sb + BL::kDS + k * 2048, 16384, 1024),
+                  sdesc_sw128(sb + BL::kK + k * 2048, 16384, 1024), idesc_q, k > 0 ? 1u : 0u);
+      }
+      umma_commit(bar_mm);
+    }
+    mbar_wait(bar_mm, j & 1);
+    tc_fence_after();
+    {  // dQ_j partial (fp32): TMEM lane = query row of the chunk
+      uint32_t o[32];
+      tmem_ld32(trow + 384 + hf * 32, o);
+      tmem_ld_wait();
+      const int q = j * kTcQ + kr;
+      if (q < s) {
+        float4* dst = reinterpret_cast<float4*>(
+            part + ((static_cast<int64_t>(kt) * gridDim.y + bh) * s + q) * kTcHD + hf * 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
+                               __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
+      }
+    }
+    tc_fence_before();
+    named_sync(1, kTcThreads);  // TMEM dQ / S columns and the chunk buffer are free again
+  }
+  // dK (x scale), dV -> bf16 rows of dqkv
+  {
+    uint32_t dvv[32], dkv[32];
+    tmem_ld32(trow + 256 + hf * 32, dvv);
+    tmem_ld32(trow + 320 + hf * 32, dkv);
+    tmem_ld_wait();
+    if (key < s) {
+      auto* dq = static_cast<__nv_bfloat16*>(p.dqkv);
+      __nv_bfloat16* rowp = dq + (static_cast<int64_t>(row0) + key) * p.ld_qkv;
+      uint4* dvp = reinterpret_cast<uint4*>(rowp + (2 * H + h) * kTcHD + hf * 32);
+      uint4* dkp = reinterpret_cast<uint4*>(rowp + (H + h) * kTcHD + hf * 32);
+      const float sc = p.scale;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        dvp[i] = make_uint4(pack_bf16(__uint_as_float(dvv[8 * i]), __uint_as_float(dvv[8 * i + 1])),
+                            pack_bf16(__uint_as_float(dvv[8 * i + 2]), __uint_as_float(dvv[8 * i + 3])),
+                            pack_bf16(__uint_as_float(dvv[8 * i + 4]), __uint_as_float(dvv[8 * i + 5])),
+                            pack_bf16(__uint_as_float(dvv[8 * i + 6]), __uint_as_float(dvv[8 * i + 7])));
+        dkp[i] = make_uint4(pack_bf16(__uint_as_float(dkv[8 * i]) * sc, __uint_as_float(dkv[8 * i + 1]) * sc),
+                            pack_bf16(__uint_as_float(dkv[8 * i + 2]) * sc, __uint_as_float(dkv[8 * i + 3]) * sc),
+                            pack_bf16(__uint_as_float(dkv[8 * i + 4]) * sc, __uint_as_float(dkv[8 * i + 5]) * sc),
+                            pack_bf16(__uint_as_float(dkv[8 * i + 6]) * sc, __uint_as_float(dkv[8 * i + 7]) * sc));
+      }
+    }
+  }
+  tc_fence_before();
+  // every key tile's dQ partials are in global memory after the cluster barrier; CTA kt then
+  // owns query chunk kt and sums its partials in key-tile order
+  __threadfence();
+  cluster_sync();
+  {
+    auto* dq = static_cast<__nv_bfloat16*>(p.dqkv);
+    const float sc = p.scale;
+    const int q_lo = kt * kTcQ, q_hi = min(s, q_lo + kTcQ);
+    for (int idx = threadIdx.x; idx < (q_hi - q_lo) * (kTcHD / 8); idx += kTcThreads) {
+      const int q = q_lo + idx / (kTcHD / 8), c8 = idx % (kTcHD / 8);
+      float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int t = 0; t < nkt; ++t) {
+        const float4* src = reinterpret_cast<const float4*>(
+            part + ((static_cast<int64_t>(t) * gridDim.y + bh) * s + q) * kTcHD + c8 * 8);
+        const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
+        a[0] += x0.x; a[1] += x0.y; a[2] += x0.z; a[3] += x0.w;
+        a[4] += x1.x; a[5] += x1.y; a[6] += x1.z; a[7] += x1.w;
+      }
+      *reinterpret_cast<uint4*>(dq + (static_cast<int64_t>(row0) + q) * p.ld_qkv + h * kTcHD + c8 * 8) =
+          make_uint4(pack_bf16(a[0] * sc, a[1] * sc), pack_bf16(a[2] * sc, a[3] * sc),
+                     pack_bf16(a[4] * sc, a[5] * sc), pack_bf16(a[6] * sc, a[7] * sc));
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ------------------------------------------------------------------------------ host
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn_tc() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (fn == nullptr) {
+    cudaDriverEntryPointQueryResult qr;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qr) !=
+            cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+bool attention_tc_supported(const gx_attention_args& a) {
+  static const bool on = [] {
+    const char* e = std::getenv("GX_ATTN_TC");
+    return e == nullptr || e[0] != '0';
+  }();
+  return on && a.head_dim == kTcHD && a.seq >= 1 && a.seq <= kTcMaxKeys &&
+         (a.ld_qkv % 8) == 0 && (reinterpret_cast<uintptr_t>(a.qkv) % 16) == 0 &&
+         (a.ld_ctx % 8) == 0;
+}
+
+int attention_fwd_tc(const gx_attention_args& a, cudaStream_t st) {
+  auto fn = encode_fn_tc();
+  if (fn == nullptr) return set_error(kErrCuda, "attention_tc: no cuTensorMapEncodeTiled");
+  // qkv viewed as [rows][3*heads slots][64]: one 3-D map serves Q, K and V of every head
+  CUtensorMap map;
+  const uint64_t rows = static_cast<uint64_t>(a.batch) * a.seq;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(kTcHD), static_cast<cuuint64_t>(3 * a.heads), rows};
+  cuuint64_t strides[2] = {kTcHD * 2, static_cast<cuuint64_t>(a.ld_qkv) * 2};
+  cuuint32_t box[3] = {kTcHD, 1, 64};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const int nk = (a.seq + 63) / 64 * 64;
+  CUresult rc = fn(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.qkv), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (rc != CUDA_SUCCESS) return set_error(kErrCuda, "attention_tc: tensor map encode failed");
+  const TcLayout L = tc_layout(a.seq);
+  const int smem = L.bytes + 1024;
+  dim3 grid((a.seq + kTcQ - 1) / kTcQ, a.batch * a.heads);
+#define GX_ATTN_TC(C)                                                                      \
+  {                                                                                        \
+    static bool set = false;                                                               \
+    if (!set) {                                                                            \
+      cudaFuncSetAttribute(attn_fwd_tc_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           227 * 1024);                                                    \
+      set = true;                                                                          \
+    }                                                                                      \
+    launch_k(attn_fwd_tc_kernel<C>, grid, dim3(kTcThreads), smem, st, map, a);             \
+  }
+  if (nk <= 64) GX_ATTN_TC(64)
+  else if (nk <= 128) GX_ATTN_TC(128)
+  else if (nk <= 256) GX_ATTN_TC(256)
+  else GX_ATTN_TC(512)
+#undef GX_ATTN_TC
+  return check_launch("attn_fwd_tc_kernel");
+}
+
+
+static bool make_head_map(CUtensorMap* map, const void* base, int slots, uint64_t rows, int64_t ld) {
+  auto fn = encode_fn_tc();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(kTcHD), static_cast<cuuint64_t>(slots), rows};
+  cuuint64_t strides[2] = {kTcHD * 2, static_cast<cuuint64_t>(ld) * 2};
+  cuuint32_t box[3] = {kTcHD, 1, 64};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int attention_bwd_tc(const gx_attention_args& a, cudaStream_t st) {
+  const uint64_t rows = static_cast<uint64_t>(a.batch) * a.seq;
+  CUtensorMap mq, md, mo;
+  if (!make_head_map(&mq, a.qkv, 3 * a.heads, rows, a.ld_qkv) ||
+      !make_head_map(&md, a.dctx, a.heads, rows, a.ld_ctx) ||
+      !make_head_map(&mo, a.ctx, a.heads, rows, a.ld_ctx))
+    return set_error(kErrCuda, "attention_tc: tensor map encode failed");
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         BwdLayout::kBytes + 1024);
+    set = true;
+  }
+  dim3 grid((a.seq + 127) / 128, a.batch * a.heads);
+  // the key tiles of one head form a cluster (dQ reduction after a cluster barrier)
+  launch_k_cluster(attn_bwd_tc_kernel, grid, dim3(kTcThreads), BwdLayout::kBytes + 1024, st,
+                   static_cast<unsigned>(grid.x), mq, md, mo, a);
+  return check_launch("attn_bwd_tc_kernel");
+}
+
+}  // namespace gx

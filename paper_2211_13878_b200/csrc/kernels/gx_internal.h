@@ -51,6 +51,12 @@ constexpr int kMaxSplits = 8;
 int splitk_plan(int M, int N, int K, int* tile);
 
 int attention_fwd(const gx_attention_args& a, cudaStream_t st);
+// tcgen05/TMEM forward (attention_tc.cu): head_dim 64, seq <= 512; GX_ATTN_TC=0 disables
+bool attention_tc_supported(const gx_attention_args& a);
+int attention_fwd_tc(const gx_attention_args& a, cudaStream_t st);
+// tcgen05 backward: needs dq_accum >= ceil(seq/128) * batch*heads*seq*64 floats (per key-tile
+// dQ partials) and dsum >= batch*heads words zero-initialised once (tickets, left reset)
+int attention_bwd_tc(const gx_attention_args& a, cudaStream_t st);
 int attention_bwd(const gx_attention_args& a, cudaStream_t st);
 int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, void* mean,
                   void* rstd, int rows, int h, cudaStream_t st);

@@ -197,7 +197,7 @@ int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, v
 //           block of a strip (ticket counter) adds the slices in slice order.
 template <int NC, bool kF32Dy, bool kDrop>
 __global__ void __launch_bounds__(256) layernorm_bwd_rows_kernel(
-    const void* __restrict__ dy, const uint4* __restrict__ x, const float* __restrict__ mean,
+    const void* dy, const uint4* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, const uint4* __restrict__ gamma, const uint4* __restrict__ dres,
     uint4* __restrict__ dx, uint4* __restrict__ dz, gx_dropout d, int rows, int h, int dy_slices,
     int64_t dy_stride) {
@@ -209,13 +209,47 @@ __global__ void __launch_bounds__(256) layernorm_bwd_rows_kernel(
     const float mu = mean[r], rs = rstd[r];
     float xh[NC][8], dv[NC][8];
     float s1 = 0.f, s2 = 0.f;
+    // dy: slice-major so every slice's loads for the whole row are in flight together
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int ci = c * 32 + lane;
+      if (ci < chunks) {
+        load8<kF32Dy>(dy, static_cast<int64_t>(r) * chunks + ci, dv[c]);
+        unpack8(x[static_cast<int64_t>(r) * chunks + ci], xh[c]);
+      }
+    }
+    if constexpr (kF32Dy) {
+      for (int sl = 1; sl < dy_slices; ++sl) {
+        const float* base = static_cast<const float*>(dy) + sl * dy_stride;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const int ci = c * 32 + lane;
+          if (ci < chunks) {
+            float g8[8];
+            load8<true>(base, static_cast<int64_t>(r) * chunks + ci, g8);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) dv[c][j] += g8[j];
+          }
+        }
+      }
+      if (dy_slices > 1) {  // fold the split-K slices into slice 0 for the column pass
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const int ci = c * 32 + lane;
+          if (ci < chunks) {
+            float4* o = reinterpret_cast<float4*>(const_cast<void*>(dy)) +
+                        2 * (static_cast<int64_t>(r) * chunks + ci);
+            o[0] = make_float4(dv[c][0], dv[c][1], dv[c][2], dv[c][3]);
+            o[1] = make_float4(dv[c][4], dv[c][5], dv[c][6], dv[c][7]);
+          }
+        }
+      }
+    }
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int ci = c * 32 + lane;
       if (ci < chunks) {
         float gm[8];
-        unpack8(x[static_cast<int64_t>(r) * chunks + ci], xh[c]);
-        load8s<kF32Dy>(dy, static_cast<int64_t>(r) * chunks + ci, dv[c], dy_slices, dy_stride);
         unpack8(__ldg(gamma + ci), gm);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -402,7 +436,7 @@ int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* r
   launch_k(kcols, dim3(strips, slices), dim3(256), 0, st, dy, static_cast<const uint4*>(x),
            static_cast<const float*>(mean), static_cast<const float*>(rstd),
            static_cast<const uint4*>(dz), static_cast<float*>(dgamma), static_cast<float*>(dbeta),
-           static_cast<float*>(dbias), workspace, tickets, rows, h, rps, dy_slices, dy_slice_stride);
+           static_cast<float*>(dbias), workspace, tickets, rows, h, rps, 1, dy_slice_stride);
   return check_launch("layernorm_bwd_cols_kernel");
 }
 
@@ -620,29 +654,34 @@ __device__ __forceinline__ void adam4(const AdamScalars& c, float4& p, const flo
     pf[j] = pf[j] - c.step_size * __fdividef(mf[j], denom) - c.lr_wd * pf[j];
   }
 }
-// two float4 per thread per iteration: 8 independent 16-byte loads in flight
+// kU float4 per thread per iteration: 4*kU independent 16-byte loads in flight per thread, so
+// a small (SM-slot-frugal) grid still keeps HBM busy while the backward runs beside it
+template <int kU>
 __device__ __forceinline__ void adam_range(const AdamScalars& c, float4* __restrict__ p,
                                            const float4* __restrict__ g, float4* __restrict__ m,
                                            float4* __restrict__ v, uint2* __restrict__ out,
                                            int64_t n4) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  for (; i + stride < n4; i += 2 * stride) {
-    float4 p0 = p[i], p1 = p[i + stride];
-    const float4 g0 = g[i], g1 = g[i + stride];
-    float4 m0 = m[i], m1 = m[i + stride], v0 = v[i], v1 = v[i + stride];
-    adam4(c, p0, g0, m0, v0);
-    adam4(c, p1, g1, m1, v1);
-    p[i] = p0;
-    p[i + stride] = p1;
-    m[i] = m0;
-    m[i + stride] = m1;
-    v[i] = v0;
-    v[i + stride] = v1;
-    out[i] = make_uint2(pk(p0.x, p0.y), pk(p0.z, p0.w));
-    out[i + stride] = make_uint2(pk(p1.x, p1.y), pk(p1.z, p1.w));
+  for (; i + (kU - 1) * stride < n4; i += kU * stride) {
+    float4 pp[kU], gg[kU], mm[kU], vv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      pp[u] = p[i + u * stride];
+      gg[u] = g[i + u * stride];
+      mm[u] = m[i + u * stride];
+      vv[u] = v[i + u * stride];
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      adam4(c, pp[u], gg[u], mm[u], vv[u]);
+      p[i + u * stride] = pp[u];
+      m[i + u * stride] = mm[u];
+      v[i + u * stride] = vv[u];
+      out[i + u * stride] = make_uint2(pk(pp[u].x, pp[u].y), pk(pp[u].z, pp[u].w));
+    }
   }
-  if (i < n4) {
+  for (; i < n4; i += stride) {
     float4 p0 = p[i];
     const float4 g0 = g[i];
     float4 m0 = m[i], v0 = v[i];
@@ -659,7 +698,7 @@ __global__ void adamw_kernel(float4* __restrict__ p, const float4* __restrict__ 
                              uint2* __restrict__ out, int64_t n4, float lr, float b1, float b2,
                              float eps, float wd, float bc1, float bc2) {
   pdl_enter();
-  adam_range(adam_scalars(lr, b1, b2, eps, wd, bc1, bc2), p, g, m, v, out, n4);
+  adam_range<2>(adam_scalars(lr, b1, b2, eps, wd, bc1, bc2), p, g, m, v, out, n4);
 }
 
 int adamw(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n, float lr,
@@ -680,7 +719,7 @@ __global__ void adamw_dev_kernel(float4* __restrict__ p, const float4* __restric
                                  float eps, float wd, const int64_t* __restrict__ step) {
   pdl_enter();
   const float t = static_cast<float>(*step);
-  adam_range(adam_scalars(lr, b1, b2, eps, wd, 1.f - powf(b1, t), 1.f - powf(b2, t)), p, g, m, v,
+  adam_range<4>(adam_scalars(lr, b1, b2, eps, wd, 1.f - powf(b1, t), 1.f - powf(b2, t)), p, g, m, v,
              out, n4);
 }
 
@@ -689,7 +728,13 @@ int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, 
               cudaStream_t st, int max_blocks) {
   if (n % 4) return set_error(kErrConfig, "adamw: n % 4 != 0");
   if (n == 0) return kOk;
-  int blocks = grid_for(n / 8, 256);
+  // Short-lived blocks (one 4-float4 strip per thread, no grid-stride loop): the block
+  // scheduler can hand every SM freed by this kernel back to the higher-priority backward
+  // stream, instead of long-resident optimizer blocks pinning SMs for the whole update.
+  const int64_t per_block = 256 * 4;
+  int64_t nb = (n / 4 + per_block - 1) / per_block;
+  if (nb > (1ll << 30)) nb = 1ll << 30;
+  int blocks = static_cast<int>(nb);
   if (max_blocks > 0 && blocks > max_blocks) blocks = max_blocks;
   launch_k(adamw_dev_kernel, dim3(blocks), dim3(256), 0, st,
            static_cast<float4*>(master), static_cast<const float4*>(grad),

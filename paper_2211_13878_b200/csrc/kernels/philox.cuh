@@ -46,6 +46,20 @@ __host__ __device__ __forceinline__ uint32_t keep16(uint64_t seed, uint64_t site
                                   static_cast<uint32_t>(site), static_cast<uint32_t>(site >> 32),
                                   static_cast<uint32_t>(seed), static_cast<uint32_t>(seed >> 32));
   const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+#ifdef __CUDA_ARCH__
+  // SIMD byte compares: 0xFF per byte >= thr8, then one bit per byte (positions 0,8,16,24
+  // folded to 0..3) -- identical bits to the scalar loop below
+  const uint32_t t4 = thr8 * 0x01010101u;
+  uint32_t bits = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t x = __vcmpgeu4(words[k], t4) & 0x01010101u;
+    x |= x >> 7;
+    x |= x >> 14;
+    bits |= (x & 0xFu) << (4 * k);
+  }
+  return bits;
+#else
   uint32_t bits = 0;
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
@@ -53,6 +67,7 @@ __host__ __device__ __forceinline__ uint32_t keep16(uint64_t seed, uint64_t site
     bits |= (b >= thr8 ? 1u : 0u) << j;
   }
   return bits;
+#endif
 }
 
 }  // namespace gx

@@ -213,6 +213,7 @@ class ExecutorImpl final : public Executor {
     if (pgraph_exec_ != nullptr) cudaGraphExecDestroy(pgraph_exec_);
     if (pgraph_ != nullptr) cudaGraphDestroy(pgraph_);
     for (cudaEvent_t e : events_) cudaEventDestroy(e);
+    for (auto& t : tr_) cudaEventDestroy(t.second);
     for (cudaEvent_t e : fork_events_) cudaEventDestroy(e);
     if (join_event_ != nullptr) cudaEventDestroy(join_event_);
     for (auto& r : ranks_)
@@ -411,6 +412,22 @@ class ExecutorImpl final : public Executor {
   }
   std::vector<cudaEvent_t> fork_events_;
   cudaEvent_t join_event_ = nullptr;
+  // Eager-mode timeline (cfg "trace"): timing events recorded on the stream each mark names,
+  // reported by profile_report() as ms since the step's first mark.
+  bool trace_ = false;
+  std::vector<std::pair<std::string, cudaEvent_t>> tr_;
+  size_t tr_used_ = 0;
+  void tmark(const std::string& name, cudaStream_t st) {
+    if (!trace_ || capturing_) return;
+    if (tr_used_ == tr_.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      tr_.push_back({name, e});
+    }
+    tr_[tr_used_].first = name;
+    cudaEventRecord(tr_[tr_used_].second, st);
+    ++tr_used_;
+  }
   cudaGraph_t graph_ = nullptr;
   cudaGraphExec_t graph_exec_ = nullptr;
   cudaGraph_t pgraph_ = nullptr;  // instrumented (profiling) variant
@@ -460,6 +477,7 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     if (const char* e = std::getenv("GX_SPLITK")) splitk_ = e[0] != '0';
     opt_blocks_ = cfg.value("optimizer_blocks", 0);
     wgrad_stream_ = cfg.value("wgrad_stream", true);
+    trace_ = cfg.value("trace", false);
     if (const char* e = std::getenv("GX_WGRAD_STREAM")) wgrad_stream_ = e[0] != '0';
     if (const char* e = std::getenv("GX_OPT_BLOCKS")) opt_blocks_ = std::atoi(e);
     thr_attn_ = threshold_of(p_attn_);
@@ -749,7 +767,7 @@ int ExecutorImpl::allocate(RankCtx& r) {
   r.da = A.a<bf16>(max_h);
   r.gbuf[0] = A.a<bf16>(max_h);
   r.gbuf[1] = A.a<bf16>(max_h);
-  r.dq_acc = A.a<float>(max_c);
+  r.dq_acc = A.a<float>(4 * max_c);  // tcgen05 attention: one dQ partial per 128-key tile
   r.acc32 = A.a<float>(static_cast<int64_t>(kMaxSplits) * max_h);
   {
     int64_t max_hdim = 0;
@@ -759,6 +777,7 @@ int ExecutorImpl::allocate(RankCtx& r) {
       cudaMemset(r.ln_ws, 0, layernorm_bwd_ws_floats(static_cast<int>(max_hdim)) * sizeof(float));
   }
   r.dsum = A.a<float>(max_lse);
+  if (r.dsum != nullptr) cudaMemset(r.dsum, 0, max_lse * sizeof(float));  // attention tickets
   r.loss = A.a<float>(1);
   r.loss_dummy = A.a<float>(1);
   r.loss_ws = A.a<float>(kLossBlocks + 1);
@@ -1288,8 +1307,11 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
     if (wg_active_)  // ... and for the weight gradients
       GX_TRY(cuda_check(cudaStreamWaitEvent(side_, r.wg_done[par], 0), "fork wait wgrad"));
     side_used_ = true;
-    return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_, wd_,
-                     r.step, side_, opt_blocks_);
+    tmark("opt_begin L" + std::to_string(L.layer), side_);
+    GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_, wd_,
+                     r.step, side_, opt_blocks_));
+    tmark("opt_end L" + std::to_string(L.layer), side_);
+    return kOk;
   }
   return kOk;
 }
@@ -1485,6 +1507,8 @@ std::string ExecutorImpl::topology() const {
 // ------------------------------------------------------------------------- the step
 int ExecutorImpl::step_once() {
   fork_used_ = 0;
+  tr_used_ = 0;
+  tmark("step_begin", stream_);
   side_used_ = false;
   wg_used_ = false;
   wg_active_ = wgrad_stream_ && !profiling_;
@@ -1528,6 +1552,7 @@ int ExecutorImpl::step_once() {
       }
     }
   }
+  tmark("fwd_end", stream_);
   // --------------------------------------------------------------- backward (GPipe)
   for (int mb = m_ - 1; mb >= 0 && !forward_only_; --mb) {
     for (int st = P_ - 1; st >= 0; --st) {
@@ -1557,6 +1582,7 @@ int ExecutorImpl::step_once() {
         // SDP: the forward all-gather's copy stays resident through backward (B200 HBM
         // allows it), so the cost model's second gather (cost_model.cc:186-195) is elided.
         const int tp = R[0]->layers[li].d.tp;
+        tmark("bwd_begin L" + std::to_string(R[0]->layers[li].layer), stream_);
         if (tp > 1) {
           for (int ph = 0; ph < 3; ++ph)
             for (RankCtx* r : R) GX_TRY(bwd_phase(*r, li, mb, ph));
@@ -1599,6 +1625,7 @@ int ExecutorImpl::step_once() {
     GX_TRY(cuda_check(cudaEventRecord(join_event_, side_), "join record"));
     GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, join_event_, 0), "join wait"));
   }
+  tmark("step_end", stream_);
   for (auto& r : ranks_) GX_TRY(comm_->world_sum(r->rank, r->loss, stream_));
   // next step draws fresh dropout masks
   for (auto& r : ranks_) GX_TRY(bump_step(nullptr, r->seed_off, stream_));
@@ -1674,6 +1701,16 @@ std::string ExecutorImpl::profile_report() const {
   j["sum_ms"] = total;
   j["span_ms"] = span;
   j["gemm_launches"] = launches;
+  if (trace_ && tr_used_ > 0) {
+    cudaDeviceSynchronize();
+    json tl = json::array();
+    for (size_t i = 0; i < tr_used_; ++i) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, tr_[0].second, tr_[i].second);
+      tl.push_back({tr_[i].first, t});
+    }
+    j["trace"] = tl;
+  }
   return j.dump();
 }
 

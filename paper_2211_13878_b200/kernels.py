@@ -152,8 +152,11 @@ def attention_bwd(qkv, ctx, lse, dctx, batch, seq, heads, head_dim, p=0.0, seed=
                   mask=None, **kw):
     import torch
     dqkv = torch.zeros_like(qkv)
-    dq_acc = torch.empty(batch * heads * seq * head_dim, device=qkv.device, dtype=torch.float32)
-    dsum = torch.empty(batch * heads * seq, device=qkv.device, dtype=torch.float32)
+    # fp32 dQ partials (one slice per 128-key tile on the tcgen05 path) and D / ticket words
+    # (zero-initialised: the tcgen05 path keeps per-head tickets there)
+    dq_acc = torch.empty(((seq + 127) // 128) * batch * heads * seq * head_dim, device=qkv.device,
+                         dtype=torch.float32)
+    dsum = torch.zeros(batch * heads * seq, device=qkv.device, dtype=torch.float32)
     a = _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, **kw)
     a.ctx, a.ld_ctx, a.lse = _ptr(ctx), ctx.stride(0), _ptr(lse)
     a.dctx, a.dqkv, a.dq_accum, a.dsum = _ptr(dctx), _ptr(dqkv), _ptr(dq_acc), _ptr(dsum)
