@@ -401,48 +401,52 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t idesc_kv = idesc_bf16_f32(128, kTcHD, false, true);
   const uint32_t idesc_q = idesc_bf16_f32(kTcQ, kTcHD, true, true);
 
+  // S^T / dPd^T MMAs of chunk j (thread 0) and D of chunk j (all threads)
+  auto issue_s = [&](int j) {
+    const int bf = j & 1;
+    mbar_wait(&bar_ld[bf], (j >> 1) & 1);
+    tc_fence_after();
+    const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
+#pragma unroll
+    for (int k = 0; k < kTcHD / 16; ++k) {
+      umma_bf16(tmem, sdesc_sw128(sb + BL::kK + k * 32, 16, 1024),
+                sdesc_sw128(q_b + k * 32, 16, 1024), idesc_s, k != 0 ? 1u : 0u);
+      umma_bf16(tmem + 128, sdesc_sw128(sb + BL::kV + k * 32, 16, 1024),
+                sdesc_sw128(do_b + k * 32, 16, 1024), idesc_s, k != 0 ? 1u : 0u);
+    }
+    umma_commit(bar_s);
+  };
+  auto compute_d = [&](int j) {  // D = rowsum(dO * O) of chunk j's 128 queries -> sD
+    const int bf = j & 1;
+    mbar_wait(&bar_ld[bf], (j >> 1) & 1);
+    const int qi = threadIdx.x >> 1, hh = threadIdx.x & 1;
+    const uint8_t* dob = smem + BL::kDO + bf * 16384 + qi * 128;
+    const uint8_t* ob = smem + BL::kO + bf * 16384 + qi * 128;
+    float acc = 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int cc = hh * 4 + c;
+      const int sw = (cc ^ (qi & 7)) << 4;
+      const uint4 a = *reinterpret_cast<const uint4*>(dob + sw);
+      const uint4 o = *reinterpret_cast<const uint4*>(ob + sw);
+      const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        acc += bf16_lo(aw[t]) * bf16_lo(ow[t]) + bf16_hi(aw[t]) * bf16_hi(ow[t]);
+    }
+    acc += __shfl_xor_sync(0xffffffff, acc, 1);
+    if (hh == 0) sD[qi] = acc;
+  };
+  if (threadIdx.x == 0) {
+    if (nq > 1) load_chunk(1);
+    mbar_wait(bar_kv, 0);
+    issue_s(0);
+  }
+  compute_d(0);
+  named_sync(1, kTcThreads);
+
   for (int j = 0; j < nq; ++j) {
     const int bf = j & 1;
-    const uint32_t ld_phase = (j >> 1) & 1;
-    if (threadIdx.x == 0) {
-      if (j + 1 < nq) load_chunk(j + 1);  // its buffer's readers (chunk j-1) are done
-      if (j == 0) mbar_wait(bar_kv, 0);
-      mbar_wait(&bar_ld[bf], ld_phase);
-      tc_fence_after();
-      const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
-#pragma unroll
-      for (int k = 0; k < kTcHD / 16; ++k) {
-        umma_bf16(tmem, sdesc_sw128(sb + BL::kK + k * 32, 16, 1024),
-                  sdesc_sw128(q_b + k * 32, 16, 1024), idesc_s, k != 0 ? 1u : 0u);
-        umma_bf16(tmem + 128, sdesc_sw128(sb + BL::kV + k * 32, 16, 1024),
-                  sdesc_sw128(do_b + k * 32, 16, 1024), idesc_s, k != 0 ? 1u : 0u);
-      }
-      umma_commit(bar_s);
-    }
-    // D = rowsum(dO * O), lse and keep words of this chunk's 128 queries -> smem
-    mbar_wait(&bar_ld[bf], ld_phase);
-    {
-      const int qi = threadIdx.x >> 1, hh = threadIdx.x & 1;
-      const int q = j * kTcQ + qi;
-      const uint8_t* dob = smem + BL::kDO + bf * 16384 + qi * 128;
-      const uint8_t* ob = smem + BL::kO + bf * 16384 + qi * 128;
-      float acc = 0.f;
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int cc = hh * 4 + c;
-        const int sw = (cc ^ (qi & 7)) << 4;
-        const uint4 a = *reinterpret_cast<const uint4*>(dob + sw);
-        const uint4 o = *reinterpret_cast<const uint4*>(ob + sw);
-        const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, ow[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          acc += bf16_lo(aw[t]) * bf16_lo(ow[t]) + bf16_hi(aw[t]) * bf16_hi(ow[t]);
-      }
-      acc += __shfl_xor_sync(0xffffffff, acc, 1);
-      if (hh == 0) sD[qi] = acc;
-      (void)q;
-    }
-    named_sync(1, kTcThreads);
     mbar_wait(bar_s, j & 1);
     tc_fence_after();
     // P, Pd, dS for key row kr x queries [hf*64, hf*64 + 64)
@@ -501,7 +505,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                   sdesc_sw128(sb + BL::kK + k * 2048, 16384, 1024), idesc_q, k > 0 ? 1u : 0u);
       }
       umma_commit(bar_mm);
+      // the next chunk's scores queue behind (S / dPd columns were consumed above)
+      if (j + 1 < nq) issue_s(j + 1);
     }
+    if (j + 1 < nq) compute_d(j + 1);  // sD of chunk j was last read before the barrier
     mbar_wait(bar_mm, j & 1);
     tc_fence_after();
     {  // dQ_j partial (fp32): TMEM lane = query row of the chunk
@@ -518,6 +525,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                                __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
       }
     }
+    // chunk j's buffer is free once its MMAs are done: prefetch chunk j + 2 into it
+    if (threadIdx.x == 0 && j + 2 < nq) load_chunk(j + 2);
     tc_fence_before();
     named_sync(1, kTcThreads);  // TMEM dQ / S columns and the chunk buffer are free again
   }
@@ -555,6 +564,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     auto* dq = static_cast<__nv_bfloat16*>(p.dqkv);
     const float sc = p.scale;
     const int q_lo = kt * kTcQ, q_hi = min(s, q_lo + kTcQ);
+#pragma unroll 4
     for (int idx = threadIdx.x; idx < (q_hi - q_lo) * (kTcHD / 8); idx += kTcThreads) {
       const int q = q_lo + idx / (kTcHD / 8), c8 = idx % (kTcHD / 8);
       float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};

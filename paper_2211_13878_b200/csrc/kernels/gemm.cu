@@ -46,13 +46,31 @@ struct GemmCfg {
       kStages * kStageBytes + kStagingBytesDecl + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-__device__ __forceinline__ float gelu_erf(float x) {
-  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+// Exact-erf GeLU, x * Phi(x).  erf(z) for z = |x|/sqrt(2) uses the Abramowitz-Stegun 7.1.26
+// rational form (|error| < 1.5e-7, far below the bf16 rounding of the stored result): one
+// reciprocal, one exp2 and six FMAs instead of erff's branchy polynomial -- the GeLU epilogue
+// runs on the CUDA cores of a tensor-bound GEMM, so its instruction count is on the critical
+// path.  The same exp(-x^2/2) feeds the derivative Phi(x) + x phi(x).
+struct GeluTerms {
+  float phi_cdf;  // Phi(x) = 0.5 (1 + erf(x / sqrt 2))
+  float e;        // exp(-x^2 / 2)
+};
+__device__ __forceinline__ GeluTerms gelu_terms(float x) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  const float t = __frcp_rn(fmaf(0.3275911f, z, 1.f));
+  const float poly =
+      t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f),
+                       -0.284496736f), 0.254829592f);
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-z * z * 1.4426950408889634f));
+  const float erf_abs = 1.f - poly * e;
+  return GeluTerms{0.5f * (1.f + copysignf(erf_abs, x)), e};
 }
+__device__ __forceinline__ float gelu_erf(float x) { return x * gelu_terms(x).phi_cdf; }
 // d/dx [x * Phi(x)] = Phi(x) + x * phi(x)
 __device__ __forceinline__ float gelu_erf_grad(float x) {
-  return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) +
-         x * 0.3989422804014327f * __expf(-0.5f * x * x);
+  const GeluTerms g = gelu_terms(x);
+  return g.phi_cdf + x * 0.3989422804014327f * g.e;
 }
 
 // Epilogue math for 32 consecutive accumulator columns [n0, n0+32) of row `row`: v <- final
@@ -425,7 +443,8 @@ struct PairCfg {
   static constexpr int kBBytes = (BN / 2) * kBK * 2;   // this CTA's half of B
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = kSmemBudget / kStageBytes > 8 ? 8 : kSmemBudget / kStageBytes;
-  static constexpr int kTmemCols = 2 * BN;
+  // two accumulator buffers, rounded up to the power-of-two allocation granule
+  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
   static constexpr int kSmemBytes = kStages * kStageBytes + kStagingBytesDecl + 1024 + 256;
 };
 
@@ -720,14 +739,17 @@ static int launch_gemm_pair(const GemmOperand& a, const GemmOperand& b, int M, i
 
 // Picks the N tile that minimises the number of waves (ties -> larger tile).
 static int pick_bn(int M, int N);
-// Tile choice: CTA-pair (negative) when M >= 256, else the 1-CTA kernel.
-static int pick_tile(int M, int N) {
+// Tile choice: CTA-pair (negative) when M >= 256, else the 1-CTA kernel.  N tile 160 (K-major
+// B only: each CTA stages 80 B rows) fills one wave of pairs where 256 would leave SMs idle
+// and 128 would spill into a second wave (e.g. M = 512, N = 5120: 64 pairs vs 40 / 80).
+static int pick_tile(int M, int N, bool b_mn) {
   if (M < 256) return pick_bn(M, N);
   const int pairs = num_sms() / 2;
   int best = -256;
   double best_cost = 1e30;
-  for (int bn : {256, 128}) {
+  for (int bn : {256, 160, 128}) {
     if (bn == 256 && N <= 128) continue;
+    if (bn == 160 && (b_mn || N <= 128)) continue;
     const int tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
     const int waves = (tiles + pairs - 1) / pairs;
     const double cost = waves * (bn + 48.0);
@@ -799,7 +821,8 @@ int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
   // force_bn: >0 selects the 1-CTA kernel with that N tile, <0 the CTA-pair kernel with
   // N tile -force_bn, 0 = automatic (pair kernel whenever M spans at least one 256-row tile).
   int bn = force_bn;
-  if (bn == 0) bn = pick_tile(M, N);
+  if (bn == 0) bn = pick_tile(M, N, b.mn_major);
+  if (bn == -160 && b.mn_major) return set_error(kErrConfig, "gemm: N tile 160 needs K-major B");
 #define GX_GEMM_DISPATCH(BN_, LAUNCH)                                                        \
   if (bn == BN_) {                                                                           \
     if (!a.mn_major && !b.mn_major) return LAUNCH<BN_ < 0 ? -BN_ : BN_, false, false>(a, b, M, N, K, ep, stream, splits); \
@@ -812,6 +835,10 @@ int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
   GX_GEMM_DISPATCH(64, launch_gemm)
   GX_GEMM_DISPATCH(-256, launch_gemm_pair)
   GX_GEMM_DISPATCH(-128, launch_gemm_pair)
+  if (bn == -160) {
+    if (!a.mn_major) return launch_gemm_pair<160, false, false>(a, b, M, N, K, ep, stream, splits);
+    return launch_gemm_pair<160, true, false>(a, b, M, N, K, ep, stream, splits);
+  }
 #undef GX_GEMM_DISPATCH
   return set_error(kErrConfig, "gemm: unsupported N tile");
 }

@@ -17,9 +17,11 @@ def _rel(x, ref):
 @pytest.mark.parametrize("M,N,K", [(128, 128, 64), (512, 3840, 1280), (520, 480, 160),
                                    (1024, 1280, 5120), (256, 200, 72), (1280, 5120, 512),
                                    (776, 640, 1280)])
-@pytest.mark.parametrize("tile_n", [0, 64, 128, 256, -128, -256])
+@pytest.mark.parametrize("tile_n", [0, 64, 128, 256, -128, -256, -160])
 def test_gemm_layouts(cuda, a_mn, b_mn, M, N, K, tile_n):
     from paper_2211_13878_b200 import kernels
+    if tile_n == -160 and b_mn:
+        pytest.skip("N tile 160 is for K-major B only")
     g = torch.Generator(device="cpu").manual_seed(M * 7 + N * 3 + K)
     A = torch.randn(M, K, generator=g).to(cuda, torch.bfloat16)
     B = torch.randn(N, K, generator=g).to(cuda, torch.bfloat16)
