@@ -195,104 +195,92 @@ int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, v
 //  columns: dgamma += sum_r dy * xhat, dbeta += sum_r dy (and dbias += sum_r dz), computed by
 //           (64-column strip x row slice) blocks; each writes its partial sums and the last
 //           block of a strip (ticket counter) adds the slices in slice order.
-template <int NC, bool kF32Dy, bool kDrop>
-__global__ void __launch_bounds__(256) layernorm_bwd_rows_kernel(
+// One block per row, one thread per 8-element chunk (h / 8 threads, rounded up to whole
+// warps): every load of the row -- all split-K slices of dy included -- is issued at once,
+// which is what a latency-bound 512-row problem needs; the two row sums go through a
+// warp-shuffle + shared-memory reduction.
+template <bool kF32Dy, bool kDrop>
+__global__ void __launch_bounds__(512) layernorm_bwd_rows_kernel(
     const void* dy, const uint4* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, const uint4* __restrict__ gamma, const uint4* __restrict__ dres,
     uint4* __restrict__ dx, uint4* __restrict__ dz, gx_dropout d, int rows, int h, int dy_slices,
     int64_t dy_stride) {
   pdl_enter();
+  __shared__ float red[2][16];
   const int chunks = h >> 3;
-  const int lane = threadIdx.x & 31;
-  const int warps_total = gridDim.x * (blockDim.x >> 5);
-  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps_total) {
-    const float mu = mean[r], rs = rstd[r];
-    float xh[NC][8], dv[NC][8];
-    float s1 = 0.f, s2 = 0.f;
-    // dy: slice-major so every slice's loads for the whole row are in flight together
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ci = c * 32 + lane;
-      if (ci < chunks) {
-        load8<kF32Dy>(dy, static_cast<int64_t>(r) * chunks + ci, dv[c]);
-        unpack8(x[static_cast<int64_t>(r) * chunks + ci], xh[c]);
-      }
-    }
+  const int ci = threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int r = blockIdx.x;
+  const bool active = ci < chunks;
+  const int64_t i = static_cast<int64_t>(r) * chunks + ci;
+  const float mu = mean[r], rs = rstd[r];
+  float xh[8], dv[8], gm[8], rv[8];
+  float s1 = 0.f, s2 = 0.f;
+  if (active) {
+    load8<kF32Dy>(dy, i, dv);
     if constexpr (kF32Dy) {
-      for (int sl = 1; sl < dy_slices; ++sl) {
-        const float* base = static_cast<const float*>(dy) + sl * dy_stride;
+      float acc[kMaxSplits - 1][8];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const int ci = c * 32 + lane;
-          if (ci < chunks) {
-            float g8[8];
-            load8<true>(base, static_cast<int64_t>(r) * chunks + ci, g8);
+      for (int sl = 1; sl < kMaxSplits; ++sl)
+        if (sl < dy_slices) load8<true>(static_cast<const float*>(dy) + sl * dy_stride, i, acc[sl - 1]);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) dv[c][j] += g8[j];
-          }
+      for (int sl = 1; sl < kMaxSplits; ++sl)
+        if (sl < dy_slices) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) dv[j] += acc[sl - 1][j];
         }
-      }
       if (dy_slices > 1) {  // fold the split-K slices into slice 0 for the column pass
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          const int ci = c * 32 + lane;
-          if (ci < chunks) {
-            float4* o = reinterpret_cast<float4*>(const_cast<void*>(dy)) +
-                        2 * (static_cast<int64_t>(r) * chunks + ci);
-            o[0] = make_float4(dv[c][0], dv[c][1], dv[c][2], dv[c][3]);
-            o[1] = make_float4(dv[c][4], dv[c][5], dv[c][6], dv[c][7]);
-          }
-        }
+        float4* o = reinterpret_cast<float4*>(const_cast<void*>(dy)) + 2 * i;
+        o[0] = make_float4(dv[0], dv[1], dv[2], dv[3]);
+        o[1] = make_float4(dv[4], dv[5], dv[6], dv[7]);
       }
     }
+    unpack8(x[i], xh);
+    unpack8(__ldg(gamma + ci), gm);
+    if (dres != nullptr) {
+      unpack8(dres[i], rv);
+    } else {
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ci = c * 32 + lane;
-      if (ci < chunks) {
-        float gm[8];
-        unpack8(__ldg(gamma + ci), gm);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          xh[c][j] = (xh[c][j] - mu) * rs;
-          const float g = dv[c][j] * gm[j];
-          s1 += g;
-          s2 += g * xh[c][j];
-        }
-      }
+      for (int j = 0; j < 8; ++j) rv[j] = 0.f;
     }
-    const float m1 = warp_sum(s1) / static_cast<float>(h);
-    const float m2 = warp_sum(s2) / static_cast<float>(h);
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      const int ci = c * 32 + lane;
-      if (ci < chunks) {
-        const int64_t i = static_cast<int64_t>(r) * chunks + ci;
-        float gm[8], rv[8], o[8];
-        unpack8(__ldg(gamma + ci), gm);
-        if (dres != nullptr) {
-          unpack8(dres[i], rv);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) rv[j] = 0.f;
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = rs * (dv[c][j] * gm[j] - m1 - xh[c][j] * m2) + rv[j];
-        const uint4 ob = pack8(o);
-        dx[i] = ob;
-        if constexpr (kDrop) {
-          // identical arithmetic to dropout_bwd_colsum on the stored bf16 dx
-          float v[8];
-          unpack8(ob, v);
-          if (d.threshold != 0u) {
-            bool k[8];
-            keep8(d, static_cast<uint64_t>(d.row_offset + r) * d.drop_ld + d.col_offset + ci * 8, k);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = k[j] ? v[j] * d.scale : 0.f;
-          }
-          dz[i] = pack8(v);
-        }
-      }
+    for (int j = 0; j < 8; ++j) {
+      xh[j] = (xh[j] - mu) * rs;
+      const float g = dv[j] * gm[j];
+      s1 += g;
+      s2 += g * xh[j];
     }
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if (lane == 0) {
+    red[0][warp] = s1;
+    red[1][warp] = s2;
+  }
+  __syncthreads();
+  float t1 = 0.f, t2 = 0.f;
+  for (int w = 0; w < nwarps; ++w) {
+    t1 += red[0][w];
+    t2 += red[1][w];
+  }
+  if (!active) return;
+  const float m1 = t1 / static_cast<float>(h), m2 = t2 / static_cast<float>(h);
+  float o[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o[j] = rs * (dv[j] * gm[j] - m1 - xh[j] * m2) + rv[j];
+  const uint4 ob = pack8(o);
+  dx[i] = ob;
+  if constexpr (kDrop) {
+    // identical arithmetic to dropout_bwd_colsum on the stored bf16 dx
+    float v[8];
+    unpack8(ob, v);
+    if (d.threshold != 0u) {
+      bool k[8];
+      keep8(d, static_cast<uint64_t>(d.row_offset + r) * d.drop_ld + d.col_offset + ci * 8, k);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = k[j] ? v[j] * d.scale : 0.f;
+    }
+    dz[i] = pack8(v);
   }
 }
 
@@ -396,36 +384,20 @@ int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* r
                   int64_t dy_slice_stride) {
   if (h % 8 != 0 || h > 4096) return set_error(kErrConfig, "layernorm: h must be a multiple of 8, <= 4096");
   if (rows <= 0) return kOk;
-  if (dy_slices < 1 || (dy_slices > 1 && !dy_f32))
+  if (dy_slices < 1 || dy_slices > kMaxSplits || (dy_slices > 1 && !dy_f32))
     return set_error(kErrConfig, "layernorm_bwd: dy slices need fp32 dy");
   const bool fuse = drop != nullptr;
   if (fuse && (dz == nullptr || dbias == nullptr))
     return set_error(kErrConfig, "layernorm_bwd: fused dropout needs dz and dbias");
   const gx_dropout dd = fuse ? *drop : gx_dropout{};
-  int nc = (h / 8 + 31) / 32;
-  nc = nc <= 6 ? nc : (nc <= 8 ? 8 : (nc <= 10 ? 10 : (nc <= 12 ? 12 : 16)));
-  const int grid = grid_for(rows, 8);
-#define GX_LN_BWD_K(N, F32, DROP)                                                             \
-  launch_k(layernorm_bwd_rows_kernel<N, F32, DROP>, dim3(grid), dim3(256), 0, st, dy,         \
-           static_cast<const uint4*>(x), static_cast<const float*>(mean),                     \
-           static_cast<const float*>(rstd), static_cast<const uint4*>(gamma),                 \
-           static_cast<const uint4*>(dres), static_cast<uint4*>(dx), static_cast<uint4*>(dz), \
-           dd, rows, h, dy_slices, dy_slice_stride);
-#define GX_LN_BWD(N)                                                              \
-  case N:                                                                         \
-    if (dy_f32) {                                                                 \
-      if (fuse) GX_LN_BWD_K(N, true, true) else GX_LN_BWD_K(N, true, false)      \
-    } else {                                                                      \
-      if (fuse) GX_LN_BWD_K(N, false, true) else GX_LN_BWD_K(N, false, false)    \
-    }                                                                             \
-    break;
-  switch (nc) {
-    GX_LN_BWD(1) GX_LN_BWD(2) GX_LN_BWD(3) GX_LN_BWD(4) GX_LN_BWD(5) GX_LN_BWD(6)
-    GX_LN_BWD(8) GX_LN_BWD(10) GX_LN_BWD(12) GX_LN_BWD(16)
-    default: break;
-  }
-#undef GX_LN_BWD
-#undef GX_LN_BWD_K
+  const int threads = ((h / 8) + 31) / 32 * 32;  // <= 512 for h <= 4096
+  auto* krows = dy_f32 ? (fuse ? layernorm_bwd_rows_kernel<true, true> : layernorm_bwd_rows_kernel<true, false>)
+                       : (fuse ? layernorm_bwd_rows_kernel<false, true> : layernorm_bwd_rows_kernel<false, false>);
+  launch_k(krows, dim3(rows), dim3(threads), 0, st, dy, static_cast<const uint4*>(x),
+           static_cast<const float*>(mean), static_cast<const float*>(rstd),
+           static_cast<const uint4*>(gamma), static_cast<const uint4*>(dres),
+           static_cast<uint4*>(dx), static_cast<uint4*>(dz), dd, rows, h, dy_slices,
+           dy_slice_stride);
   GX_RC(check_launch("layernorm_bwd_rows_kernel"));
   int strips, slices, rps;
   ln_cols_grid(rows, h, &strips, &slices, &rps);
