@@ -32,7 +32,9 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 B = one swizzle span
 constexpr int kEpiWarps = 8;  // warps 4..11: two per TMEM lane quarter, each half the columns
 constexpr int kThreads = 128 + 32 * kEpiWarps;
-constexpr int kStagingBytesDecl = kEpiWarps * (4096 + 2048);      // epilogue staging (below)
+// epilogue staging per warp: out 4 KB + two 2 KB bf16 operand buffers + 256 B bias, plus the
+// operand-prefetch mbarriers (see kStagingBytes below)
+constexpr int kStagingBytesDecl = kEpiWarps * (4096 + 2048 + 2048 + 256) + kEpiWarps * 2 * 8;
 constexpr int kSmemBudget = 227 * 1024 - kStagingBytesDecl - 2048;  // left for the A/B ring
 
 template <int BN>
@@ -73,55 +75,30 @@ __device__ __forceinline__ float gelu_erf_grad(float x) {
   return g.phi_cdf + x * 0.3989422804014327f * g.e;
 }
 
-// Epilogue math for 32 consecutive accumulator columns [n0, n0+32) of row `row`: v <- final
-// values, pre <- bf16-rounded pre-activation (GeLU forward).  Operand reads are guarded for
-// rows >= M / columns >= N; the TMA store clips those elements.
-__device__ __forceinline__ void epilogue_math(const GemmEpilogue& ep, int64_t row, bool row_ok,
-                                              int n0, int N, const uint32_t (&acc)[32],
-                                              float (&v)[32], float (&pre)[32]) {
+// Epilogue math for 32 consecutive accumulator columns of one row (the lane's): v <- final
+// values, pre <- bf16-rounded pre-activation (GeLU forward).  bias_w / in_w hold the 32 bf16
+// bias values of these columns and the 32 bf16 of the row's epilogue operand (gelu_bwd's
+// pre-activation or the residual), both already staged on chip; out-of-range rows / columns
+// read as zero and the TMA store clips them.
+__device__ __forceinline__ void epilogue_math(const GemmEpilogue& ep, int64_t row, int n0,
+                                              const uint32_t (&acc)[32],
+                                              const uint32_t (&bias_w)[16],
+                                              const uint32_t (&in_w)[16], float (&v)[32],
+                                              float (&pre)[32]) {
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(acc[j]) * ep.alpha;
-  const bool full = row_ok && n0 + 32 <= N;
-  const __nv_bfloat16* bias = static_cast<const __nv_bfloat16*>(ep.bias);
-  const __nv_bfloat16* residual = static_cast<const __nv_bfloat16*>(ep.residual);
-  auto add_bf16x32 = [&](const __nv_bfloat16* src, bool ok_full, float scale_dummy) {
-    (void)scale_dummy;
-    if (ok_full) {
-      const uint4* sp = reinterpret_cast<const uint4*>(src);
+  if (ep.bias != nullptr) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 b = sp[q];
-        const uint32_t w[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          v[q * 8 + 2 * t] += bf16_lo(w[t]);
-          v[q * 8 + 2 * t + 1] += bf16_hi(w[t]);
-        }
-      }
-    } else if (row_ok) {
-      for (int j = 0; j < 32; ++j)
-        if (n0 + j < N) v[j] += __bfloat162float(src[j]);
+    for (int t = 0; t < 16; ++t) {
+      v[2 * t] += bf16_lo(bias_w[t]);
+      v[2 * t + 1] += bf16_hi(bias_w[t]);
     }
-  };
-  if (bias != nullptr) add_bf16x32(bias + n0, n0 + 32 <= N, 0.f);
-  if (ep.gelu_bwd) {
-    // dgrad epilogue of the MLP up-projection: v <- v * gelu'(pre)
-    const __nv_bfloat16* auxp = static_cast<const __nv_bfloat16*>(ep.aux) + row * ep.ld_aux + n0;
-    if (full) {
-      const uint4* ap = reinterpret_cast<const uint4*>(auxp);
+  }
+  if (ep.gelu_bwd) {  // dgrad epilogue of the MLP up-projection: v <- v * gelu'(pre)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 b = ap[q];
-        const uint32_t w[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          v[q * 8 + 2 * t] *= gelu_erf_grad(bf16_lo(w[t]));
-          v[q * 8 + 2 * t + 1] *= gelu_erf_grad(bf16_hi(w[t]));
-        }
-      }
-    } else if (row_ok) {
-      for (int j = 0; j < 32; ++j)
-        if (n0 + j < N) v[j] *= gelu_erf_grad(__bfloat162float(auxp[j]));
+    for (int t = 0; t < 16; ++t) {
+      v[2 * t] *= gelu_erf_grad(bf16_lo(in_w[t]));
+      v[2 * t + 1] *= gelu_erf_grad(bf16_hi(in_w[t]));
     }
   }
   if (ep.gelu) {
@@ -132,7 +109,7 @@ __device__ __forceinline__ void epilogue_math(const GemmEpilogue& ep, int64_t ro
       v[j] = gelu_erf(pre[j]);
     }
   }
-  if (residual != nullptr) {
+  if (ep.residual != nullptr) {
     // out = residual + dropout(v), dropout element index = (row_offset+row)*drop_ld + col
     const uint64_t grow = static_cast<uint64_t>(ep.row_offset + row);
     if (ep.drop_threshold != 0u) {
@@ -151,8 +128,10 @@ __device__ __forceinline__ void epilogue_math(const GemmEpilogue& ep, int64_t ro
     }
     // dropout output rounded to bf16 before the add, matching the unfused path
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));
-    add_bf16x32(residual + row * ep.ld_res + n0, full, 0.f);
+    for (int t = 0; t < 16; ++t) {
+      v[2 * t] = __bfloat162float(__float2bfloat16_rn(v[2 * t])) + bf16_lo(in_w[t]);
+      v[2 * t + 1] = __bfloat162float(__float2bfloat16_rn(v[2 * t + 1])) + bf16_hi(in_w[t]);
+    }
   }
 }
 
@@ -160,16 +139,31 @@ __device__ __forceinline__ void epilogue_math(const GemmEpilogue& ep, int64_t ro
 // Each epilogue warp owns 32 rows; a 32 x 32 block of results is written to a swizzled
 // staging buffer (64 B rows + SWIZZLE_64B for bf16, 128 B rows + SWIZZLE_128B for fp32:
 // conflict-free st.shared.v4 with one row per lane) and leaves through one TMA bulk
-// store (or bulk reduce-add for fp32 accumulation).  Two buffers per warp alternate, so
-// the store of block i overlaps the math of block i+1.
+// store (or bulk reduce-add for fp32 accumulation).
+// The epilogue's bf16 operand (gelu_bwd pre-activation or residual) arrives the same way in
+// reverse: TMA loads of 32 x 32 blocks into two per-warp buffers, the first issued before
+// the warp waits for the accumulator (so it overlaps the main loop) and each next one while
+// the current block is processed.  The bias slice of a tile is staged in shared memory
+// before the accumulator wait as well, so no global load latency is left in the epilogue.
 constexpr int kStageOutBytes = 4096;  // 32 x 32 fp32
-constexpr int kStageAuxBytes = 2048;  // 32 x 32 bf16
-constexpr int kStagingBytes = kEpiWarps * (kStageOutBytes + kStageAuxBytes);
+constexpr int kStageAuxBytes = 2048;  // 32 x 32 bf16 (gelu pre-activation out / operand in #0)
+constexpr int kStageInBytes = 2048;   // 32 x 32 bf16 (operand in #1)
+constexpr int kStageWarpBytes = kStageOutBytes + kStageAuxBytes + kStageInBytes;
+constexpr int kBiasWarpBytes = 256;   // up to 4 chunks x 32 bf16
+constexpr int kStagingBytes = kEpiWarps * (kStageWarpBytes + kBiasWarpBytes) + kEpiWarps * 2 * 8;
+static_assert(kStagingBytes == kStagingBytesDecl, "epilogue staging layout");
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
                                              uint32_t d) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
                "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ void ld_shared_v4(uint32_t addr, uint32_t& a, uint32_t& b, uint32_t& c,
+                                             uint32_t& d) {
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+               : "r"(addr)
                : "memory");
 }
 __device__ __forceinline__ void stage_bf16_row(uint32_t base, uint32_t r, const float (&v)[32]) {
@@ -179,6 +173,13 @@ __device__ __forceinline__ void stage_bf16_row(uint32_t base, uint32_t r, const 
     st_shared_v4(addr, pack_bf16(v[c * 8 + 0], v[c * 8 + 1]), pack_bf16(v[c * 8 + 2], v[c * 8 + 3]),
                  pack_bf16(v[c * 8 + 4], v[c * 8 + 5]), pack_bf16(v[c * 8 + 6], v[c * 8 + 7]));
   }
+}
+// the 32 bf16 of row r from a SWIZZLE_64B 32 x 32 block (inverse of stage_bf16_row)
+__device__ __forceinline__ void load_bf16_row(uint32_t base, uint32_t r, uint32_t (&w)[16]) {
+#pragma unroll
+  for (uint32_t c = 0; c < 4; ++c)
+    ld_shared_v4(base + r * 64 + ((c ^ ((r >> 1) & 3)) << 4), w[4 * c], w[4 * c + 1],
+                 w[4 * c + 2], w[4 * c + 3]);
 }
 __device__ __forceinline__ void stage_f32_row(uint32_t base, uint32_t r, const float (&v)[32]) {
 #pragma unroll
@@ -203,6 +204,14 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32
       "r"(src), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_u32(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                int32_t c0, int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -212,36 +221,95 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Per-warp epilogue state: staging buffers, operand-prefetch barriers and their use count.
+struct EpiWarp {
+  uint32_t out_buf, aux_buf, bias_buf;
+  uint32_t bar0;  // operand-prefetch barriers bar0, bar0 + 8
+  uint32_t blk;   // operand blocks consumed so far (buffer = blk & 1, phase = (blk >> 1) & 1)
+  // operand buffer b: buffer 0 is the aux staging (never live together with the gelu
+  // pre-activation output), buffer 1 follows it
+  __device__ __forceinline__ uint32_t in_buf(uint32_t b) const { return aux_buf + b * kStageAuxBytes; }
+  __device__ __forceinline__ uint32_t in_bar(uint32_t b) const { return bar0 + b * 8; }
+};
+
+__device__ __forceinline__ void epi_prefetch(const EpiWarp& w, const CUtensorMap* map_in,
+                                             uint32_t blk, int32_t col, int32_t row) {
+  if (lane_id() == 0) {
+    const uint32_t b = blk & 1;
+    fence_proxy_async_smem();  // this buffer's previous (generic) reads are complete
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(w.in_bar(b)),
+                 "r"(kStageInBytes)
+                 : "memory");
+    tma_load_2d_u32(w.in_buf(b), map_in, w.in_bar(b), col, row);
+  }
+}
+
+// Stage this warp's bias columns [n0 + c_lo*32, n0 + c_hi*32) of the tile in shared memory.
+__device__ __forceinline__ void epi_stage_bias(const GemmEpilogue& ep, const EpiWarp& w, int n0,
+                                               int N, int c_lo, int c_hi) {
+  if (ep.bias == nullptr) return;
+  const __nv_bfloat16* bias = static_cast<const __nv_bfloat16*>(ep.bias);
+  const int lane = static_cast<int>(lane_id());
+  const int ncols = (c_hi - c_lo) * 32;
+  for (int c = lane * 4; c < ncols; c += 128) {
+    uint32_t w0 = 0, w1 = 0;
+    const int col = n0 + c_lo * 32 + c;
+    if (col + 4 <= N) {
+      const uint2 v = *reinterpret_cast<const uint2*>(bias + col);
+      w0 = v.x;
+      w1 = v.y;
+    } else {
+      __nv_bfloat16 t[4];
+      for (int k = 0; k < 4; ++k) t[k] = col + k < N ? bias[col + k] : __float2bfloat16(0.f);
+      w0 = *reinterpret_cast<uint32_t*>(&t[0]);
+      w1 = *reinterpret_cast<uint32_t*>(&t[2]);
+    }
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(w.bias_buf + c * 2), "r"(w0), "r"(w1)
+                 : "memory");
+  }
+  __syncwarp();
+}
+
 // One 32 x 32 output block: math, staging, TMA store.  Executed by a whole epilogue warp.
 __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUtensorMap* map_out,
-                                               const CUtensorMap* map_aux, uint8_t* staging,
-                                               int q, uint32_t& block_ctr, int64_t m_base,
-                                               int32_t store_row, int n0, int M, int N,
+                                               const CUtensorMap* map_aux, EpiWarp& w,
+                                               bool has_in, int cb, int64_t m_base,
+                                               int32_t store_row, int n0,
                                                const uint32_t (&acc)[32]) {
   const uint32_t lane = lane_id();
   const int64_t row = m_base + lane;
+  uint32_t bias_w[16], in_w[16];
+  if (ep.bias != nullptr) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      ld_shared_v4(w.bias_buf + cb * 64 + c * 16, bias_w[4 * c], bias_w[4 * c + 1],
+                   bias_w[4 * c + 2], bias_w[4 * c + 3]);
+  }
+  if (has_in) {
+    const uint32_t b = w.blk & 1;
+    mbar_wait_addr(w.in_bar(b), (w.blk >> 1) & 1);
+    load_bf16_row(w.in_buf(b), lane, in_w);
+    ++w.blk;
+  }
   float v[32], pre[32];
-  epilogue_math(ep, row, row < M, n0, N, acc, v, pre);
-  ++block_ctr;
-  const uint32_t out_buf = smem_u32(staging) + q * (kStageOutBytes + kStageAuxBytes);
-  const uint32_t aux_buf = out_buf + kStageOutBytes;
-  if (lane == 0) bulk_wait_read0();  // the previous store from this buffer has read it
+  epilogue_math(ep, row, n0, acc, bias_w, in_w, v, pre);
+  if (lane == 0) bulk_wait_read0();  // the previous store from these buffers has read them
   __syncwarp();
   if (ep.out_kind == kOutBF16) {
-    stage_bf16_row(out_buf, lane, v);
+    stage_bf16_row(w.out_buf, lane, v);
   } else {
-    stage_f32_row(out_buf, lane, v);
+    stage_f32_row(w.out_buf, lane, v);
   }
-  if (ep.gelu) stage_bf16_row(aux_buf, lane, pre);
+  if (ep.gelu) stage_bf16_row(w.aux_buf, lane, pre);
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
     if (ep.out_kind == kOutF32Accumulate) {
-      tma_reduce_add_2d(map_out, out_buf, n0, store_row);
+      tma_reduce_add_2d(map_out, w.out_buf, n0, store_row);
     } else {
-      tma_store_2d(map_out, out_buf, n0, store_row);
+      tma_store_2d(map_out, w.out_buf, n0, store_row);
     }
-    if (ep.gelu) tma_store_2d(map_aux, aux_buf, n0, static_cast<int32_t>(m_base));
+    if (ep.gelu) tma_store_2d(map_aux, w.aux_buf, n0, static_cast<int32_t>(m_base));
     bulk_commit();
   }
 }
@@ -250,25 +318,60 @@ __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUt
 // All BN/32 chunks of one accumulator tile for one epilogue warp.  (A ping-pong variant
 // that keeps the next chunk's TMEM load in flight measured slower: the extra 32 live
 // registers cost more than the hidden LDTM latency.)
-// `ew` (0..kEpiWarps-1) selects the staging buffer and the column half this warp owns.
+// `ew` (0..kEpiWarps-1) selects the column half this warp owns.
 template <int BN>
-__device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const CUtensorMap* map_out,
-                                              const CUtensorMap* map_aux, uint8_t* staging, int ew,
-                                              uint32_t& block_ctr, uint32_t taddr, int64_t m_base,
-                                              int32_t store_row, int n0, int M, int N) {
+__device__ __forceinline__ void epilogue_chunks(int ew, int* c_lo, int* c_hi) {
   constexpr int NC = BN / 32;
   constexpr int kHalves = kEpiWarps / 4;
-  const int c_lo = (ew / 4) * NC / kHalves, c_hi = (ew / 4 + 1) * NC / kHalves;
-  const int q = ew;
+  *c_lo = (ew / 4) * NC / kHalves;
+  *c_hi = (ew / 4 + 1) * NC / kHalves;
+}
+template <int BN>
+__device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const CUtensorMap* map_out,
+                                              const CUtensorMap* map_aux, EpiWarp& w, int ew,
+                                              bool has_in, uint32_t taddr, int64_t m_base,
+                                              int32_t store_row, int n0, int M, int N) {
+  int c_lo, c_hi;
+  epilogue_chunks<BN>(ew, &c_lo, &c_hi);
 #pragma unroll 1
   for (int c = c_lo; c < c_hi; ++c) {
+    // next block of the operand streams in while this one is processed
+    if (has_in && c + 1 < c_hi)
+      epi_prefetch(w, map_aux, w.blk + 1, n0 + (c + 1) * 32, static_cast<int32_t>(m_base));
     uint32_t r[32];
     tmem_ld32(taddr + c * 32, r);
     tmem_ld_wait();
-    if (m_base < M && n0 + c * 32 < N)
-      epilogue_block(ep, map_out, map_aux, staging, q, block_ctr, m_base, store_row, n0 + c * 32,
-                     M, N, r);
+    if (m_base < M && n0 + c * 32 < N) {
+      epilogue_block(ep, map_out, map_aux, w, has_in, c - c_lo, m_base, store_row, n0 + c * 32, r);
+    } else if (has_in) {
+      // keep the operand pipeline in step: consume (wait for) the block even if unused
+      mbar_wait_addr(w.in_bar(w.blk & 1), (w.blk >> 1) & 1);
+      ++w.blk;
+    }
   }
+}
+
+// Before the accumulator wait of a tile: stage bias, start the first operand block.
+template <int BN>
+__device__ __forceinline__ void epilogue_tile_prologue(const GemmEpilogue& ep,
+                                                       const CUtensorMap* map_aux, EpiWarp& w,
+                                                       int ew, bool has_in, int64_t m_base,
+                                                       int n0, int N) {
+  int c_lo, c_hi;
+  epilogue_chunks<BN>(ew, &c_lo, &c_hi);
+  if (has_in) epi_prefetch(w, map_aux, w.blk, n0 + c_lo * 32, static_cast<int32_t>(m_base));
+  epi_stage_bias(ep, w, n0, N, c_lo, c_hi);
+}
+
+__device__ __forceinline__ EpiWarp epi_warp_init(uint8_t* staging, int ew) {
+  EpiWarp w;
+  const uint32_t base = smem_u32(staging);
+  w.out_buf = base + ew * kStageWarpBytes;
+  w.aux_buf = w.out_buf + kStageOutBytes;
+  w.bias_buf = base + kEpiWarps * kStageWarpBytes + ew * kBiasWarpBytes;
+  w.bar0 = base + kEpiWarps * (kStageWarpBytes + kBiasWarpBytes) + ew * 16;
+  w.blk = 0;
+  return w;
 }
 
 template <int BN, bool kAMN, bool kBMN>
@@ -311,6 +414,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[b], 1);
       mbar_init(&tempty_bar[b], 32 * kEpiWarps);
     }
+    for (int i = 0; i < 2 * kEpiWarps; ++i)  // epilogue operand-prefetch barriers
+      mbar_init(reinterpret_cast<uint64_t*>(staging + kEpiWarps * (kStageWarpBytes + kBiasWarpBytes)) + i, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -398,7 +503,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     // ---------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    uint32_t block_ctr = 0;
+    EpiWarp ew = epi_warp_init(staging, warp - 4);
+    const bool has_in = ep.gelu_bwd || ep.residual != nullptr;
     int local = 0;
     for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++local) {
       const int tile = unit % num_tiles;
@@ -406,13 +512,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t acc_phase = (local >> 1) & 1;
       const int m0 = (tile % num_m) * kBM;
       const int n0 = (tile / num_m) * BN;
+      const int64_t m_base = m0 + q * 32;
+      epilogue_tile_prologue<BN>(ep, &map_aux, ew, warp - 4, has_in, m_base, n0, N);
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
-      const int64_t m_base = m0 + q * 32;
       // split-K slices: split s stores rows [s*M, (s+1)*M) of the [splits*M][N] output
       const int32_t store_row = static_cast<int32_t>(
           m_base + (ep.out_kind == kOutF32Split ? static_cast<int64_t>(unit / num_tiles) * M : 0));
-      epilogue_tile<BN>(ep, &map_out, &map_aux, staging, warp - 4, block_ctr,
+      epilogue_tile<BN>(ep, &map_out, &map_aux, ew, warp - 4, has_in,
                         tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base,
                         store_row, n0, M, N);
       tc_fence_before();
@@ -492,6 +599,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[b], 1);  // the leader's multicast MMA commit
       mbar_init(&tempty_bar[b], 2 * kEpiWarps);  // epilogue warps x 2 CTAs (leader copy)
     }
+    for (int i = 0; i < 2 * kEpiWarps; ++i)  // epilogue operand-prefetch barriers
+      mbar_init(reinterpret_cast<uint64_t*>(staging + kEpiWarps * (kStageWarpBytes + kBiasWarpBytes)) + i, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_pair<Cfg::kTmemCols>(tmem_slot);
@@ -584,7 +693,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int q = warp & 3;
     const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
-    uint32_t block_ctr = 0;
+    EpiWarp ew = epi_warp_init(staging, warp - 4);
+    const bool has_in = ep.gelu_bwd || ep.residual != nullptr;
     int local = 0;
     for (int unit = pair; unit < num_units; unit += num_pairs, ++local) {
       const int tile = unit % num_tiles;
@@ -592,12 +702,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t acc_phase = (local >> 1) & 1;
       const int m0 = (tile % num_pm) * 256 + static_cast<int>(rank) * 128;
       const int n0 = (tile / num_pm) * BN;
+      const int64_t m_base = m0 + q * 32;
+      epilogue_tile_prologue<BN>(ep, &map_aux, ew, warp - 4, has_in, m_base, n0, N);
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
-      const int64_t m_base = m0 + q * 32;
       const int32_t store_row = static_cast<int32_t>(
           m_base + (ep.out_kind == kOutF32Split ? static_cast<int64_t>(unit / num_tiles) * M : 0));
-      epilogue_tile<BN>(ep, &map_out, &map_aux, staging, warp - 4, block_ctr,
+      epilogue_tile<BN>(ep, &map_out, &map_aux, ew, warp - 4, has_in,
                         tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base,
                         store_row, n0, M, N);
       tc_fence_before();
@@ -655,7 +766,10 @@ static bool make_epi_maps(const GemmEpilogue& ep, int M, int N, int splits, CUte
   const bool f32 = ep.out_kind != kOutBF16;
   const uint64_t rows = static_cast<uint64_t>(M) * (ep.out_kind == kOutF32Split ? splits : 1);
   if (!make_out_map(mo, ep.out, N, rows, ep.ldo, f32)) return false;
-  if (ep.gelu) return make_out_map(mx, ep.aux, N, M, ep.ld_aux, false);
+  // map_aux: the GeLU pre-activation (written by gelu, read by gelu_bwd) or the residual read
+  // by the epilogue's operand prefetch (never both in one GEMM)
+  if (ep.gelu || ep.gelu_bwd) return make_out_map(mx, ep.aux, N, M, ep.ld_aux, false);
+  if (ep.residual != nullptr) return make_out_map(mx, ep.residual, N, M, ep.ld_res, false);
   *mx = *mo;
   return true;
 }
@@ -813,6 +927,8 @@ int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
                      ep.gelu_bwd || ep.residual != nullptr || ep.alpha != 1.f))
     return set_error(kErrConfig, "gemm: split-K needs a plain fp32 accumulate / split epilogue");
   if (M <= 0 || N <= 0 || K <= 0) return set_error(kErrConfig, "gemm: empty problem");
+  if ((ep.gelu ? 1 : 0) + (ep.gelu_bwd ? 1 : 0) + (ep.residual != nullptr ? 1 : 0) > 1)
+    return set_error(kErrConfig, "gemm: gelu, gelu_bwd and residual epilogues are exclusive");
   // TMA: row strides must be 16-byte multiples; the epilogue's vector stores need ldo too.
   if ((a.ld % 8) != 0 || (b.ld % 8) != 0 || (ep.ldo % 8) != 0 || (ep.gelu && ep.ld_aux % 8 != 0))
     return set_error(kErrConfig, "gemm: lda, ldb, ldo and ld_aux must be multiples of 8 elements");
