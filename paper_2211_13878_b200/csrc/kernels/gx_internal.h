@@ -75,6 +75,12 @@ int64_t layernorm_bwd_ws_floats(int h);
 int bias_dropout_add(const void* x, const void* bias, const void* residual, void* out, int rows,
                      int cols, const gx_dropout& d, cudaStream_t st, bool x_f32 = false,
                      int x_slices = 1, int64_t slice_stride = 0);
+// y = residual + bf16(dropout(sum of split-K slices of x + bias)); with gamma: ln / mean /
+// rstd = LayerNorm(y) (fused consumer of a split-K GEMM; gamma NULL = no LayerNorm)
+int residual_layernorm(const float* x, int slices, int64_t slice_stride, const void* bias,
+                       const void* residual, void* y, const gx_dropout& d, const void* gamma,
+                       const void* beta, void* ln, void* mean, void* rstd, int rows, int h,
+                       cudaStream_t st);
 int dropout_bwd_colsum(const void* dy, void* dz, void* dbias, int rows, int cols,
                        const gx_dropout& d, cudaStream_t st);
 int colsum(const void* x, int64_t ld, void* acc, int rows, int cols, cudaStream_t st);

@@ -458,6 +458,112 @@ int bias_dropout_add(const void* x, const void* bias, const void* residual, void
   return check_launch("bias_dropout_add_kernel");
 }
 
+// ------------------------------------------- split-K sum + bias + dropout + residual + LN
+// y = residual + bf16(dropout(sum_s x_s + bias)) for one row per block (thread per 8-column
+// chunk), then -- when gamma is given -- the LayerNorm of the stored (bf16) y: ln, mean,
+// rstd.  Replaces bias_dropout_add + layernorm_fwd after a split-K GEMM (out-projection ->
+// LN2, MLP down-projection -> the next layer's LN1) with one pass over the row.
+__global__ void __launch_bounds__(512) residual_layernorm_kernel(
+    const float* __restrict__ x, int slices, int64_t stride, const uint4* __restrict__ bias,
+    const uint4* __restrict__ res, uint4* __restrict__ y, gx_dropout d,
+    const uint4* __restrict__ gamma, const uint4* __restrict__ beta, uint4* __restrict__ ln,
+    float* __restrict__ mean, float* __restrict__ rstd, int rows, int h) {
+  pdl_enter();
+  __shared__ float red[16];
+  const int chunks = h >> 3;
+  const int ci = threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int r = blockIdx.x;
+  const bool active = ci < chunks;
+  const int64_t i = static_cast<int64_t>(r) * chunks + ci;
+  float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (active) {
+    load8<true>(x, i, v);
+    float acc[kMaxSplits - 1][8];
+#pragma unroll
+    for (int sl = 1; sl < kMaxSplits; ++sl)
+      if (sl < slices) load8<true>(x + sl * stride, i, acc[sl - 1]);
+#pragma unroll
+    for (int sl = 1; sl < kMaxSplits; ++sl)
+      if (sl < slices) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] += acc[sl - 1][j];
+      }
+    float b[8], rr[8];
+    if (bias != nullptr) {
+      unpack8(__ldg(bias + ci), b);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] += b[j];
+    }
+    if (d.threshold != 0u) {
+      bool k[8];
+      keep8(d, static_cast<uint64_t>(d.row_offset + r) * d.drop_ld + d.col_offset + ci * 8, k);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = k[j] ? v[j] * d.scale : 0.f;
+    }
+    unpack8(res[i], rr);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(__float2bfloat16_rn(v[j])) + rr[j];
+    const uint4 yb = pack8(v);
+    y[i] = yb;
+    unpack8(yb, v);  // the LayerNorm sees the stored bf16 values
+  }
+  if (gamma == nullptr) return;
+  // mean, then variance about it (two-pass, as layernorm_fwd)
+  float s1 = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) s1 += v[j];
+  s1 = warp_sum(s1);
+  if (lane == 0) red[warp] = s1;
+  __syncthreads();
+  float t = 0.f;
+  for (int w = 0; w < nwarps; ++w) t += red[w];
+  const float mu = t / static_cast<float>(h);
+  float s2 = 0.f;
+  if (active) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float dd = v[j] - mu;
+      s2 += dd * dd;
+    }
+  }
+  s2 = warp_sum(s2);
+  __syncthreads();
+  if (lane == 0) red[warp] = s2;
+  __syncthreads();
+  float t2 = 0.f;
+  for (int w = 0; w < nwarps; ++w) t2 += red[w];
+  const float rs = rsqrtf(t2 / static_cast<float>(h) + kLnEps);
+  if (active) {
+    float gm[8], bt[8], o[8];
+    unpack8(__ldg(gamma + ci), gm);
+    unpack8(__ldg(beta + ci), bt);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = (v[j] - mu) * rs * gm[j] + bt[j];
+    ln[i] = pack8(o);
+  }
+  if (threadIdx.x == 0) {
+    mean[r] = mu;
+    rstd[r] = rs;
+  }
+}
+
+int residual_layernorm(const float* x, int slices, int64_t slice_stride, const void* bias,
+                       const void* residual, void* y, const gx_dropout& d, const void* gamma,
+                       const void* beta, void* ln, void* mean, void* rstd, int rows, int h,
+                       cudaStream_t st) {
+  if (h % 8 != 0 || h > 4096) return set_error(kErrConfig, "residual_layernorm: h % 8 != 0 or h > 4096");
+  if (slices < 1 || slices > kMaxSplits) return set_error(kErrConfig, "residual_layernorm: slices");
+  if (rows <= 0) return kOk;
+  const int threads = ((h / 8) + 31) / 32 * 32;
+  launch_k(residual_layernorm_kernel, dim3(rows), dim3(threads), 0, st, x, slices, slice_stride,
+           static_cast<const uint4*>(bias), static_cast<const uint4*>(residual),
+           static_cast<uint4*>(y), d, static_cast<const uint4*>(gamma),
+           static_cast<const uint4*>(beta), static_cast<uint4*>(ln), static_cast<float*>(mean),
+           static_cast<float*>(rstd), rows, h);
+  return check_launch("residual_layernorm_kernel");
+}
+
 // --------------------------------------------- dropout backward + bias-grad column sums
 // Block handles a strip of 64 columns (8 chunks) over a slice of rows; column partials are
 // reduced in shared memory then added to dbias with one atomic per column per block.

@@ -146,6 +146,7 @@ struct Acts {
        *ln2 = nullptr, *pre = nullptr, *gel = nullptr, *y = nullptr;
   float *lse = nullptr, *mean1 = nullptr, *rstd1 = nullptr, *mean2 = nullptr, *rstd2 = nullptr;
   uint16_t* amask = nullptr;  // attention dropout keep bits (fwd -> bwd)
+  bool ln1_ready = false;     // LN1 already produced by the previous layer's fused epilogue
 };
 
 enum class Xin { kSame, kSlice, kGather, kStageInput };
@@ -982,9 +983,11 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
   const int l = L.layer;
   const int64_t row_off = A.sample0 * s.seq;
   if (rows == 0) return kOk;
+  bool ln2_ready = false;
   if (phase == 0) {
-    GX_TRY(timed(kNorm, 0, 4.0 * rows * h, [&] { return layernorm_fwd(A.x, P + L.lay.ln1g.off, P + L.lay.ln1b.off, A.ln1, A.mean1, A.rstd1,
-                         rows, h, stream_); }));
+    if (!A.ln1_ready)
+      GX_TRY(timed(kNorm, 0, 4.0 * rows * h, [&] { return layernorm_fwd(A.x, P + L.lay.ln1g.off, P + L.lay.ln1b.off, A.ln1, A.mean1, A.rstd1,
+                           rows, h, stream_); }));
     gx_gemm_epilogue e = epi();
     e.out_kind = kOutBF16;
     e.out = A.qkv;
@@ -1019,18 +1022,38 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     o.out_kind = kOutBF16;
     o.ldo = h;
     if (t == 1) {
-      o.out = A.x1;
-      o.bias = P + L.lay.bo.off;
-      o.residual = A.x;
-      o.ld_res = h;
-      o.row_offset = row_off;
-      o.drop_ld = h;
-      o.drop_threshold = thr_hidden_;
-      o.drop_scale = scale_of(p_hidden_);
-      o.seed = seed_;
-      o.site = 3ull * l + 1;
-      o.seed_offset = r.seed_off;
-      GX_TRY(gemm(A.ctx, ht, false, P + L.lay.wo.off, ht, false, rows, h, ht, o));
+      // split-K out-projection -> one row pass: slice sum + bias + dropout + residual + LN2
+      int sp = 1;
+      GX_TRY(gemm_splitk(r, A.ctx, ht, P + L.lay.wo.off, ht, false, rows, h, ht, &sp));
+      if (sp > 1) {
+        gx_dropout d{};
+        d.threshold = thr_hidden_;
+        d.scale = scale_of(p_hidden_);
+        d.seed = seed_;
+        d.site = 3ull * l + 1;
+        d.row_offset = row_off;
+        d.drop_ld = h;
+        d.seed_offset = r.seed_off;
+        GX_TRY(timed(kNorm, 0, (4.0 * sp + 8.0) * rows * h, [&] {
+          return residual_layernorm(r.acc32, sp, static_cast<int64_t>(rows) * h, P + L.lay.bo.off,
+                                    A.x, A.x1, d, P + L.lay.ln2g.off, P + L.lay.ln2b.off, A.ln2,
+                                    A.mean2, A.rstd2, rows, h, stream_);
+        }));
+        ln2_ready = true;
+      } else {
+        o.out = A.x1;
+        o.bias = P + L.lay.bo.off;
+        o.residual = A.x;
+        o.ld_res = h;
+        o.row_offset = row_off;
+        o.drop_ld = h;
+        o.drop_threshold = thr_hidden_;
+        o.drop_scale = scale_of(p_hidden_);
+        o.seed = seed_;
+        o.site = 3ull * l + 1;
+        o.seed_offset = r.seed_off;
+        GX_TRY(gemm(A.ctx, ht, false, P + L.lay.wo.off, ht, false, rows, h, ht, o));
+      }
     } else {
       o.out = r.partial;
       GX_TRY(gemm(A.ctx, ht, false, P + L.lay.wo.off, ht, false, rows, h, ht, o));
@@ -1050,8 +1073,9 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
       d.seed_offset = r.seed_off;
       GX_TRY(timed(kElementwise, 0, 6.0 * rows * h, [&] { return bias_dropout_add(r.partial, P + L.lay.bo.off, A.x, A.x1, rows, h, d, stream_); }));
     }
-    GX_TRY(timed(kNorm, 0, 4.0 * rows * h, [&] { return layernorm_fwd(A.x1, P + L.lay.ln2g.off, P + L.lay.ln2b.off, A.ln2, A.mean2, A.rstd2,
-                         rows, h, stream_); }));
+    if (!ln2_ready)
+      GX_TRY(timed(kNorm, 0, 4.0 * rows * h, [&] { return layernorm_fwd(A.x1, P + L.lay.ln2g.off, P + L.lay.ln2b.off, A.ln2, A.mean2, A.rstd2,
+                           rows, h, stream_); }));
     gx_gemm_epilogue e = epi();
     e.out_kind = kOutBF16;
     e.out = A.gel;
@@ -1076,10 +1100,27 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
         d.row_offset = row_off;
         d.drop_ld = h;
         d.seed_offset = r.seed_off;
-        return timed(kElementwise, 0, 8.0 * rows * h, [&] {
-          return bias_dropout_add(r.acc32, P + L.lay.b2.off, A.x1, A.y, rows, h, d, stream_, true, sp,
-                                  static_cast<int64_t>(rows) * h);
-        });
+        // ... and the next layer's LN1 in the same row pass when its input aliases this
+        // output and its LayerNorm parameters are resident (no SDP gather pending)
+        Acts* nxt = nullptr;
+        const bf16* PN = nullptr;
+        if (li + 1 < static_cast<int>(r.layers.size())) {
+          RankLayer& N1 = r.layers[li + 1];
+          if (N1.xin == Xin::kSame && N1.d.sdp == 1 && N1.sh.h == h) {
+            nxt = &N1.acts[mb];
+            PN = N1.pfull;
+          }
+        }
+        GX_TRY(timed(kNorm, 0, (4.0 * sp + 8.0) * rows * h, [&] {
+          return residual_layernorm(r.acc32, sp, static_cast<int64_t>(rows) * h, P + L.lay.b2.off,
+                                    A.x1, A.y, d,
+                                    nxt ? PN + r.layers[li + 1].lay.ln1g.off : nullptr,
+                                    nxt ? PN + r.layers[li + 1].lay.ln1b.off : nullptr,
+                                    nxt ? nxt->ln1 : nullptr, nxt ? nxt->mean1 : nullptr,
+                                    nxt ? nxt->rstd1 : nullptr, rows, h, stream_);
+        }));
+        if (nxt != nullptr) nxt->ln1_ready = true;
+        return kOk;
       }
       o.out = A.y;
       o.bias = P + L.lay.b2.off;
@@ -1521,6 +1562,8 @@ int ExecutorImpl::step_once() {
     return v;
   };
   for (auto& r : ranks_) {
+    for (RankLayer& L : r->layers)
+      for (Acts& a : L.acts) a.ln1_ready = false;
     GX_TRY(bump_step(r->step, nullptr, stream_));
     GX_TRY(cuda_check(cudaMemsetAsync(r->loss, 0, 4, stream_), "memset loss"));
     for (RankLayer& L : r->layers)

@@ -119,3 +119,12 @@ def test_optimizer_step_moves_params(cuda):
             # the first AdamW step (no decay) moves each parameter by ~ -lr * sign(grad)
             assert (np.sign(delta[big]) == -np.sign(g[w][big])).mean() > 0.97, (l, w)
             assert np.allclose(np.abs(delta[big]), 1e-4, rtol=0.05), (l, w)
+
+
+@pytest.mark.parametrize("p_drop", [0.0, 0.1])
+def test_serial_splitk_row_fusions(cuda, p_drop):
+    """M = 512 tokens, h = 512: the out-projection and MLP-down GEMMs take the split-K path,
+    whose slices are reduced by the fused residual + LayerNorm row pass (LN2, and the next
+    layer's LN1 across the kSame boundary)."""
+    plan = gxe.make_plan(["", "", ""], 4)
+    _check(_run_case(plan, _small_model(L=3, h=512, heads=8, seq=128, ffn=2048), 1, p_drop))
