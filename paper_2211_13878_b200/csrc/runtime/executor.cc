@@ -147,6 +147,7 @@ struct Acts {
   float *lse = nullptr, *mean1 = nullptr, *rstd1 = nullptr, *mean2 = nullptr, *rstd2 = nullptr;
   uint16_t* amask = nullptr;  // attention dropout keep bits (fwd -> bwd)
   bool ln1_ready = false;     // LN1 already produced by the previous layer's fused epilogue
+  bool dz_ready = false;      // backward: dz / db2 already produced by the next layer's LN1 bwd
 };
 
 enum class Xin { kSame, kSlice, kGather, kStageInput };
@@ -388,6 +389,9 @@ class ExecutorImpl final : public Executor {
   cudaStream_t wg_ = nullptr;
   cudaStream_t ls_ = nullptr;
   bool wgrad_stream_ = true;  // GX_WGRAD_STREAM=0 / "wgrad_stream": false disables
+  bool fuse_dz_ = false;      // previous layer's dropout bwd inside LN1 bwd (GX_FUSE_DZ=1 on;
+                              // off by default: it moves the wgrad-buffer wait earlier)
+  int opt_stream_ = 1;        // AdamW on 0 = side stream, 1 = wgrad stream, 2 = main stream
   bool wg_active_ = false;    // this capture forks (off while profiling)
   bool wg_used_ = false;
   int fork(cudaStream_t from, cudaStream_t to) {
@@ -479,6 +483,10 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     opt_blocks_ = cfg.value("optimizer_blocks", 0);
     wgrad_stream_ = cfg.value("wgrad_stream", true);
     trace_ = cfg.value("trace", false);
+    fuse_dz_ = cfg.value("fuse_dz", false);
+    opt_stream_ = cfg.value("optimizer_stream", 1);
+    if (const char* e = std::getenv("GX_OPT_STREAM")) opt_stream_ = std::atoi(e);
+    if (const char* e = std::getenv("GX_FUSE_DZ")) fuse_dz_ = e[0] != '0';
     if (const char* e = std::getenv("GX_WGRAD_STREAM")) wgrad_stream_ = e[0] != '0';
     if (const char* e = std::getenv("GX_OPT_BLOCKS")) opt_blocks_ = std::atoi(e);
     thr_attn_ = threshold_of(p_attn_);
@@ -1190,7 +1198,8 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       r.wg_pending[par] = false;
     }
     d.site = 3ull * l + 2;
-    GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(dY, dz, G + L.lay.b2.off, rows, h, d, stream_); }));
+    if (!A.dz_ready)
+      GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(dY, dz, G + L.lay.b2.off, rows, h, d, stream_); }));
     gx_gemm_epilogue w = epi();
     w.out_kind = wk;
     w.out = G + L.lay.w2.off;
@@ -1302,9 +1311,37 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
   }
   if (phase == 2) {
     const void* da_in = r.da_slices ? static_cast<const void*>(r.acc32) : static_cast<const void*>(r.da);
+    // When this layer's input is the previous layer's output (same rows), the previous
+    // layer's MLP dropout backward rides along: dz_{l-1} = dropout_mask(dX), db2_{l-1} +=
+    // colsum(dz_{l-1}) -- its phase 0 then starts straight at the GEMMs.
+    Acts* prev = nullptr;
+    RankLayer* Lp = nullptr;
+    if (fuse_dz_ && li > 0 && L.xin == Xin::kSame && r.layers[li - 1].sh.h == h) {
+      Lp = &r.layers[li - 1];
+      prev = &Lp->acts[mb];
+    }
+    gx_dropout dp{};
+    bf16* dz_prev = nullptr;
+    if (prev != nullptr) {
+      const int pp = (li - 1) & 1;
+      if (r.wg_pending[pp]) {  // that parity's buffers are free once their wgrads are done
+        GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, r.wg_done[pp], 0), "wgrad wait"));
+        r.wg_pending[pp] = false;
+      }
+      dp.threshold = thr_hidden_;
+      dp.scale = scale_of(p_hidden_);
+      dp.seed = seed_;
+      dp.site = 3ull * Lp->layer + 2;
+      dp.row_offset = prev->sample0 * Lp->sh.seq;
+      dp.drop_ld = h;
+      dp.seed_offset = r.seed_off;
+      dz_prev = r.dzb[pp];
+    }
     GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd(da_in, A.x, A.mean1, A.rstd1, P + L.lay.ln1g.off, r.dx1, dX,
                          G + L.lay.ln1g.off, G + L.lay.ln1b.off, rows, h, r.ln_ws, stream_, r.da_slices > 0,
-                         nullptr, nullptr, nullptr, std::max(1, r.da_slices), static_cast<int64_t>(rows) * h); }));
+                         prev ? &dp : nullptr, dz_prev, prev ? Lp->gfull + Lp->lay.b2.off : nullptr,
+                         std::max(1, r.da_slices), static_cast<int64_t>(rows) * h); }));
+    if (prev != nullptr) prev->dz_ready = true;
   }
   return kOk;
 }
@@ -1332,7 +1369,7 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
     return kOk;
   }
   if (phase == 2 && optimizer_) {
-    if (profiling_)  // instrumented runs keep everything on one stream for clean event pairs
+    if (profiling_ || opt_stream_ == 2)  // instrumented runs keep everything on one stream
       return timed(kOptim, 0, 30.0 * L.shard_n, [&] {
         return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_,
                          wd_, r.step, stream_);
@@ -1341,6 +1378,14 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
       cudaEvent_t e;
       GX_TRY(cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event"));
       fork_events_.push_back(e);
+    }
+    if (opt_stream_ == 1 && wg_active_) {  // behind this layer's wgrads, in order
+      GX_TRY(fork(stream_, wg_));
+      tmark("opt_begin L" + std::to_string(L.layer), wg_);
+      GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_,
+                       wd_, r.step, wg_, opt_blocks_));
+      tmark("opt_end L" + std::to_string(L.layer), wg_);
+      return kOk;
     }
     cudaEvent_t e = fork_events_[fork_used_++];
     GX_TRY(cuda_check(cudaEventRecord(e, stream_), "fork record"));
@@ -1563,7 +1608,7 @@ int ExecutorImpl::step_once() {
   };
   for (auto& r : ranks_) {
     for (RankLayer& L : r->layers)
-      for (Acts& a : L.acts) a.ln1_ready = false;
+      for (Acts& a : L.acts) a.ln1_ready = a.dz_ready = false;
     GX_TRY(bump_step(r->step, nullptr, stream_));
     GX_TRY(cuda_check(cudaMemsetAsync(r->loss, 0, 4, stream_), "memset loss"));
     for (RankLayer& L : r->layers)
