@@ -41,6 +41,7 @@ extern "C" {
 #define GX_OUT_F32 1
 #define GX_OUT_F32_ACC 2
 #define GX_OUT_F32_SPLIT 3  /* split-K: out is [splits][M][ldo] fp32, split s stores slice s */
+#define GX_OUT_ADAMW 4      /* acc = final fp32 weight gradient, consumed by AdamW in place */
 
 /* ------------------------------------------------------------------ library */
 GX_API const char* gx_last_error(void);
@@ -178,6 +179,15 @@ typedef struct gx_gemm_epilogue {
   uint64_t site;
   int gelu_bwd;               /* out = acc * gelu'(aux) (aux = bf16 pre-activation, read) */
   const uint64_t* seed_offset;/* optional device counter added to seed (per-step masks) */
+  /* GX_OUT_ADAMW: the accumulator is the complete gradient of a weight slot; the epilogue
+   * applies AdamW to master/m/v (fp32) and writes the bf16 parameter, all [M][ldo] like
+   * `out` (which is unused): the gradient never reaches HBM. */
+  float* adam_master;
+  float* adam_m;
+  float* adam_v;
+  void* adam_param;
+  float lr, beta1, beta2, eps, weight_decay;
+  const int64_t* step;        /* device step counter (bias corrections) */
 } gx_gemm_epilogue;
 
 /* C[M,N] = A[M,K] * B[N,K]^T with the epilogue above.  a_mn_major: A stored [K][lda]

@@ -40,6 +40,9 @@ class GemmEpilogue(Structure):
         ("col_offset", c_int64), ("drop_ld", c_int64), ("drop_threshold", c_uint32),
         ("drop_scale", c_float), ("seed", c_uint64), ("site", c_uint64), ("gelu_bwd", c_int),
         ("seed_offset", c_void_p),
+        ("adam_master", c_void_p), ("adam_m", c_void_p), ("adam_v", c_void_p),
+        ("adam_param", c_void_p), ("lr", c_float), ("beta1", c_float), ("beta2", c_float),
+        ("eps", c_float), ("weight_decay", c_float), ("step", c_void_p),
     ]
 
 

@@ -29,7 +29,8 @@ enum OutKind : int {
   kOutBF16 = GX_OUT_BF16,
   kOutF32 = GX_OUT_F32,
   kOutF32Accumulate = GX_OUT_F32_ACC,
-  kOutF32Split = GX_OUT_F32_SPLIT
+  kOutF32Split = GX_OUT_F32_SPLIT,
+  kOutAdamW = GX_OUT_ADAMW
 };
 
 struct GemmOperand {

@@ -10,6 +10,7 @@
 
 #include "gx_internal.h"
 #include "launch.cuh"
+#include "adam.cuh"
 #include "philox.cuh"
 
 namespace gx {
@@ -711,27 +712,6 @@ int mse_loss(const void* y, const void* target, void* dy, void* loss, int64_t n,
 // folded into two per-launch scalars (step_size = lr / bc1, 1/sqrt(bc2)) so the per-element
 // work is FMAs, one sqrt and one fast divide: the kernel shares the SMs with the backward
 // GEMMs, so its issue cost matters as much as its 30 B/param of HBM traffic.
-struct AdamScalars {
-  float b1, b2, eps, step_size, inv_sqrt_bc2, lr_wd;
-};
-__device__ __forceinline__ AdamScalars adam_scalars(float lr, float b1, float b2, float eps,
-                                                    float wd, float bc1, float bc2) {
-  return AdamScalars{b1, b2, eps, lr / bc1, rsqrtf(bc2), lr * wd};
-}
-__device__ __forceinline__ void adam4(const AdamScalars& c, float4& p, const float4& g, float4& m,
-                                      float4& v) {
-  float* pf = &p.x;
-  const float* gf = &g.x;
-  float* mf = &m.x;
-  float* vf = &v.x;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    mf[j] = c.b1 * mf[j] + (1.f - c.b1) * gf[j];
-    vf[j] = c.b2 * vf[j] + (1.f - c.b2) * gf[j] * gf[j];
-    const float denom = sqrtf(vf[j]) * c.inv_sqrt_bc2 + c.eps;
-    pf[j] = pf[j] - c.step_size * __fdividef(mf[j], denom) - c.lr_wd * pf[j];
-  }
-}
 // kU float4 per thread per iteration: 4*kU independent 16-byte loads in flight per thread, so
 // a small (SM-slot-frugal) grid still keeps HBM busy while the backward runs beside it
 template <int kU>
@@ -796,8 +776,7 @@ __global__ void adamw_dev_kernel(float4* __restrict__ p, const float4* __restric
                                  uint2* __restrict__ out, int64_t n4, float lr, float b1, float b2,
                                  float eps, float wd, const int64_t* __restrict__ step) {
   pdl_enter();
-  const float t = static_cast<float>(*step);
-  adam_range<4>(adam_scalars(lr, b1, b2, eps, wd, 1.f - powf(b1, t), 1.f - powf(b2, t)), p, g, m, v,
+  adam_range<4>(adam_scalars_step(lr, b1, b2, eps, wd, step), p, g, m, v,
              out, n4);
 }
 

@@ -392,6 +392,15 @@ class ExecutorImpl final : public Executor {
   bool fuse_dz_ = false;      // previous layer's dropout bwd inside LN1 bwd (GX_FUSE_DZ=1 on;
                               // off by default: it moves the wgrad-buffer wait earlier)
   int opt_stream_ = 1;        // AdamW on 0 = side stream, 1 = wgrad stream, 2 = main stream
+  // AdamW inside the wgrad epilogues where legal (cfg "fused_adam" / GX_FUSED_ADAM=1).  Off by
+  // default: exact (tested against the standalone kernel) and 8 B/param less HBM traffic, but
+  // the row-per-lane state loads make the wgrad GEMMs hold SMs far longer (measured slower).
+  bool fused_adam_ = false;
+  // The weight gradients of L are final after its single wgrad GEMM: one micro-batch and no
+  // data-parallel reduction (TP shards own their weight gradients).
+  bool adam_fused(const RankLayer& L) const {
+    return fused_adam_ && optimizer_ && !forward_only_ && m_ == 1 && L.d.dp == 1 && L.d.sdp == 1;
+  }
   bool wg_active_ = false;    // this capture forks (off while profiling)
   bool wg_used_ = false;
   int fork(cudaStream_t from, cudaStream_t to) {
@@ -485,6 +494,8 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     trace_ = cfg.value("trace", false);
     fuse_dz_ = cfg.value("fuse_dz", false);
     opt_stream_ = cfg.value("optimizer_stream", 1);
+    fused_adam_ = cfg.value("fused_adam", false);
+    if (const char* e = std::getenv("GX_FUSED_ADAM")) fused_adam_ = e[0] != '0';
     if (const char* e = std::getenv("GX_OPT_STREAM")) opt_stream_ = std::atoi(e);
     if (const char* e = std::getenv("GX_FUSE_DZ")) fuse_dz_ = e[0] != '0';
     if (const char* e = std::getenv("GX_WGRAD_STREAM")) wgrad_stream_ = e[0] != '0';
@@ -1184,6 +1195,33 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
   if (rows == 0) return kOk;
   const int par = li & 1;
   bf16 *dz = r.dzb[par], *dpre = r.dpreb[par], *dout = r.doutb[par], *dqkv = r.dqkvb[par];
+  // Weight-gradient epilogue for a weight slot: fp32 gradient into G, or -- when the layer's
+  // gradient is complete after this one GEMM (one micro-batch, no data-parallel reduction) --
+  // AdamW applied in place by the epilogue, so the gradient never reaches HBM.  The fused
+  // form overwrites the bf16 weight, hence every wgrad below is issued after the dgrad GEMM
+  // that reads the same weight.
+  const bool fuse_adam = adam_fused(L);
+  auto wgrad_ep = [&](const Slot& slot, int64_t ldo) {
+    gx_gemm_epilogue w = epi();
+    w.ldo = ldo;
+    if (fuse_adam) {
+      w.out_kind = kOutAdamW;
+      w.adam_master = L.master + slot.off;
+      w.adam_m = L.m + slot.off;
+      w.adam_v = L.v + slot.off;
+      w.adam_param = L.pshard + slot.off;
+      w.lr = lr_;
+      w.beta1 = b1_;
+      w.beta2 = b2_;
+      w.eps = eps_;
+      w.weight_decay = wd_;
+      w.step = r.step;
+    } else {
+      w.out_kind = wk;
+      w.out = G + slot.off;
+    }
+    return w;
+  };
   gx_dropout d{};
   d.threshold = thr_hidden_;
   d.scale = scale_of(p_hidden_);
@@ -1200,11 +1238,9 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     d.site = 3ull * l + 2;
     if (!A.dz_ready)
       GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(dY, dz, G + L.lay.b2.off, rows, h, d, stream_); }));
-    gx_gemm_epilogue w = epi();
-    w.out_kind = wk;
-    w.out = G + L.lay.w2.off;
-    w.ldo = ft;
-    GX_TRY(on_wgrad([&] { return gemm(dz, h, true, A.gel, ft, true, h, ft, rows, w); }));  // dW2 = dz^T gel
+    const gx_gemm_epilogue w2 = wgrad_ep(L.lay.w2, ft);
+    auto wgrad2 = [&] { return on_wgrad([&] { return gemm(dz, h, true, A.gel, ft, true, h, ft, rows, w2); }); };  // dW2 = dz^T gel
+    if (!fuse_adam) GX_TRY(wgrad2());  // as early as its inputs exist
     gx_gemm_epilogue e = epi();
     e.out_kind = kOutBF16;
     e.out = dpre;
@@ -1213,13 +1249,15 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     e.aux = A.pre;
     e.ld_aux = ft;
     GX_TRY(gemm(dz, h, false, P + L.lay.w2.off, ft, true, rows, ft, h, e));  // dz W2 * gelu'
-    GX_TRY(on_wgrad([&]() -> int {
-      GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dpre, ft, G + L.lay.b1.off, rows, ft, ls_); }));
-      gx_gemm_epilogue w1 = w;
-      w1.out = G + L.lay.w1.off;
-      w1.ldo = h;
-      return gemm(dpre, ft, true, A.ln2, h, true, ft, h, rows, w1);  // dW1 = dpre^T ln2
-    }));
+    if (fuse_adam) GX_TRY(wgrad2());  // after the dgrad that reads W2
+    auto wgrad1 = [&] {
+      return on_wgrad([&]() -> int {
+        GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dpre, ft, G + L.lay.b1.off, rows, ft, ls_); }));
+        const gx_gemm_epilogue w1 = wgrad_ep(L.lay.w1, h);
+        return gemm(dpre, ft, true, A.ln2, h, true, ft, h, rows, w1);  // dW1 = dpre^T ln2
+      });
+    };
+    if (!fuse_adam) GX_TRY(wgrad1());
     int sp_c = 1;
     if (t == 1)
       GX_TRY(gemm_splitk(r, dpre, ft, P + L.lay.w1.off, h, true, rows, h, ft, &sp_c));
@@ -1231,6 +1269,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       c.ldo = h;
       GX_TRY(gemm(dpre, ft, false, P + L.lay.w1.off, h, true, rows, h, ft, c));  // dpre W1
     }
+    if (fuse_adam) GX_TRY(wgrad1());
     if (t > 1)
       return c_all_reduce(L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
                                stream_);
@@ -1244,16 +1283,15 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     GX_TRY(timed(kNorm, 0, 10.0 * rows * h, [&] { return layernorm_bwd(dc_in, A.x1, A.mean2, A.rstd2, P + L.lay.ln2g.off, dY, r.dx1,
                          G + L.lay.ln2g.off, G + L.lay.ln2b.off, rows, h, r.ln_ws, stream_, r.dc_slices > 0,
                          &d, dout, G + L.lay.bo.off, std::max(1, r.dc_slices), static_cast<int64_t>(rows) * h); }));
-    gx_gemm_epilogue w = epi();
-    w.out_kind = wk;
-    w.out = G + L.lay.wo.off;
-    w.ldo = ht;
-    GX_TRY(on_wgrad([&] { return gemm(dout, h, true, A.ctx, ht, true, h, ht, rows, w); }));  // dWo = dout^T ctx
+    const gx_gemm_epilogue wo = wgrad_ep(L.lay.wo, ht);
+    auto wgrado = [&] { return on_wgrad([&] { return gemm(dout, h, true, A.ctx, ht, true, h, ht, rows, wo); }); };  // dWo = dout^T ctx
+    if (!fuse_adam) GX_TRY(wgrado());
     gx_gemm_epilogue c = epi();
     c.out_kind = kOutBF16;
     c.out = r.dctx;
     c.ldo = ht;
     GX_TRY(gemm(dout, h, false, P + L.lay.wo.off, ht, true, rows, ht, h, c));  // dout Wo
+    if (fuse_adam) GX_TRY(wgrado());
     gx_attention_args at{};
     at.batch = A.samples;
     at.seq = s.seq;
@@ -1282,17 +1320,19 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       const double af = 10.0 * A.samples * (s.heads / t) * double(s.seq) * s.seq * s.hd;
       GX_TRY(timed(kAttnBwd, af, 2.0 * rows * 8 * ht, [&] { return attention_bwd(at, stream_); }));
     }
-    GX_TRY(on_wgrad([&]() -> int {
-      GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, ls_); }));
-      w.out = G + L.lay.wqkv.off;
-      w.ldo = h;
-      GX_TRY(gemm(dqkv, 3 * ht, true, A.ln1, h, true, 3 * ht, h, rows, w));  // dWqkv
-      if (wg_active_) {  // the last reader of this parity's buffers
-        GX_TRY(cuda_check(cudaEventRecord(r.wg_done[par], wg_), "wgrad done"));
-        r.wg_pending[par] = true;
-      }
-      return kOk;
-    }));
+    auto wgradq = [&] {
+      return on_wgrad([&]() -> int {
+        GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, ls_); }));
+        const gx_gemm_epilogue wq = wgrad_ep(L.lay.wqkv, h);
+        GX_TRY(gemm(dqkv, 3 * ht, true, A.ln1, h, true, 3 * ht, h, rows, wq));  // dWqkv
+        if (wg_active_) {  // the last reader of this parity's buffers
+          GX_TRY(cuda_check(cudaEventRecord(r.wg_done[par], wg_), "wgrad done"));
+          r.wg_pending[par] = true;
+        }
+        return kOk;
+      });
+    };
+    if (!fuse_adam) GX_TRY(wgradq());
     int sp_a = 1;
     if (t == 1)
       GX_TRY(gemm_splitk(r, dqkv, 3 * ht, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, &sp_a));
@@ -1304,6 +1344,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       a.ldo = h;
       GX_TRY(gemm(dqkv, 3 * ht, false, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, a));
     }
+    if (fuse_adam) GX_TRY(wgradq());
     if (t > 1)
       return c_all_reduce(L.g_tp, r.rank, r.da, static_cast<size_t>(rows) * h, DType::kBF16,
                                stream_);
@@ -1369,9 +1410,11 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
     return kOk;
   }
   if (phase == 2 && optimizer_) {
+    // with the AdamW-fused weight-gradient epilogues only the LayerNorm / bias prefix is left
+    const int64_t n_opt = adam_fused(L) ? L.lay.acc_end : L.shard_n;
     if (profiling_ || opt_stream_ == 2)  // instrumented runs keep everything on one stream
-      return timed(kOptim, 0, 30.0 * L.shard_n, [&] {
-        return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_,
+      return timed(kOptim, 0, 30.0 * n_opt, [&] {
+        return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, n_opt, lr_, b1_, b2_, eps_,
                          wd_, r.step, stream_);
       });
     if (fork_events_.size() <= static_cast<size_t>(fork_used_)) {
@@ -1382,7 +1425,7 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
     if (opt_stream_ == 1 && wg_active_) {  // behind this layer's wgrads, in order
       GX_TRY(fork(stream_, wg_));
       tmark("opt_begin L" + std::to_string(L.layer), wg_);
-      GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_,
+      GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, n_opt, lr_, b1_, b2_, eps_,
                        wd_, r.step, wg_, opt_blocks_));
       tmark("opt_end L" + std::to_string(L.layer), wg_);
       return kOk;
@@ -1394,7 +1437,7 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
       GX_TRY(cuda_check(cudaStreamWaitEvent(side_, r.wg_done[par], 0), "fork wait wgrad"));
     side_used_ = true;
     tmark("opt_begin L" + std::to_string(L.layer), side_);
-    GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_, wd_,
+    GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, n_opt, lr_, b1_, b2_, eps_, wd_,
                      r.step, side_, opt_blocks_));
     tmark("opt_end L" + std::to_string(L.layer), side_);
     return kOk;

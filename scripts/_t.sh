@@ -1,3 +1,3 @@
-for i in 1 2 3; do
-for o in 0 1 2; do GX_OPT_STREAM=$o timeout 200 python scripts/step_variants.py default | sed "s/^/opt$o /"; done
-done
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 200 python scripts/step_variants.py default no_optimizer
+GX_FUSED_ADAM=1 timeout 200 python scripts/step_variants.py default

@@ -128,3 +128,27 @@ def test_serial_splitk_row_fusions(cuda, p_drop):
     layer's LN1 across the kSame boundary)."""
     plan = gxe.make_plan(["", "", ""], 4)
     _check(_run_case(plan, _small_model(L=3, h=512, heads=8, seq=128, ffn=2048), 1, p_drop))
+
+
+def test_fused_adamw_epilogue_matches_standalone_optimizer(cuda):
+    """Serial plan, one micro-batch: the weight-gradient GEMMs apply AdamW in their epilogue
+    (the gradient never reaches HBM).  The updated parameters must equal the standalone
+    AdamW kernel's (same gradient bits, same update arithmetic)."""
+    plan = gxe.make_plan(["", ""], 2)
+    model = _small_model(L=2)
+    outs = []
+    for fused in (True, False):
+        ex = gxe.PlanExecutor(plan, model, 1, optimizer=True, lr=1e-3, weight_decay=0.01,
+                              fused_adam=fused)
+        ex.init_params(seed=11, std=0.02)
+        rng = np.random.default_rng(3)
+        rows = 2 * model["layers"][0]["shape"]["seq"]
+        xb = gxe.f32_to_bf16_bits(rng.standard_normal((rows, 256)).astype(np.float32))
+        for _ in range(2):
+            ex.step(xb, xb)
+        outs.append([ex.export_layer(l, "params") for l in range(2)])
+        ex.close()
+    for l in range(2):
+        for k, a in outs[0][l].items():
+            b = outs[1][l][k]
+            assert np.max(np.abs(a - b)) <= 1e-6 * max(1e-3, np.max(np.abs(b))), (l, k)
