@@ -43,6 +43,7 @@ class GemmEpilogue(Structure):
         ("adam_master", c_void_p), ("adam_m", c_void_p), ("adam_v", c_void_p),
         ("adam_param", c_void_p), ("lr", c_float), ("beta1", c_float), ("beta2", c_float),
         ("eps", c_float), ("weight_decay", c_float), ("step", c_void_p),
+        ("trace", c_void_p),
     ]
 
 

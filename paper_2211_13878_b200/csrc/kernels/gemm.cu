@@ -60,7 +60,8 @@ struct GeluTerms {
 };
 __device__ __forceinline__ GeluTerms gelu_terms(float x) {
   const float z = fabsf(x) * 0.70710678118654752f;
-  const float t = __frcp_rn(fmaf(0.3275911f, z, 1.f));
+  float t;  // MUFU.RCP (~1 ulp): __frcp_rn's IEEE slow path cost more than the whole rest
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.f)));
   const float poly =
       t * fmaf(t, fmaf(t, fmaf(t, fmaf(t, 1.061405429f, -1.453152027f), 1.421413741f),
                        -0.284496736f), 0.254829592f);
@@ -74,6 +75,12 @@ __device__ __forceinline__ float gelu_erf(float x) { return x * gelu_terms(x).ph
 __device__ __forceinline__ float gelu_erf_grad(float x) {
   const GeluTerms g = gelu_terms(x);
   return g.phi_cdf + x * 0.3989422804014327f * g.e;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 // Epilogue math for 32 consecutive accumulator columns of one row (the lane's): v <- final
@@ -217,6 +224,9 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
+__device__ __forceinline__ void bulk_wait_read1() {  // all but the most recent group read
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -228,6 +238,7 @@ struct EpiWarp {
   AdamScalars adam;  // GX_OUT_ADAMW only
   uint32_t bar0;  // operand-prefetch barriers bar0, bar0 + 8
   uint32_t blk;   // operand blocks consumed so far (buffer = blk & 1, phase = (blk >> 1) & 1)
+  uint32_t sblk;  // output blocks stored so far (staging buffer = sblk & 1)
   // operand buffer b: buffer 0 is the aux staging (never live together with the gelu
   // pre-activation output), buffer 1 follows it
   __device__ __forceinline__ uint32_t in_buf(uint32_t b) const { return aux_buf + b * kStageAuxBytes; }
@@ -354,23 +365,40 @@ __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUt
   }
   float v[32], pre[32];
   epilogue_math(ep, row, n0, acc, bias_w, in_w, v, pre);
-  if (lane == 0) bulk_wait_read0();  // the previous store from these buffers has read them
-  __syncwarp();
-  if (ep.out_kind == kOutBF16) {
-    stage_bf16_row(w.out_buf, lane, v);
-  } else {
-    stage_f32_row(w.out_buf, lane, v);
+  // Double-buffered staging, so block i+1's math overlaps block i's store: bf16 outputs use
+  // the two halves of the 4 KB out buffer; fp32 outputs (weight gradients: no operand, no
+  // aux) use the out buffer and the 4 KB operand/aux area; the GeLU pre-activation output
+  // alternates over the operand/aux area (gelu has no operand).
+  // (an fp32 output next to an operand or the GeLU output falls back to one buffer)
+  const uint32_t k = w.sblk & 1;
+  ++w.sblk;
+  const bool f32 = ep.out_kind != kOutBF16;
+  const bool dbl = !f32 || (!ep.gelu && !has_in);
+  const uint32_t obuf = !f32 ? w.out_buf + k * 2048 : (dbl && k ? w.aux_buf : w.out_buf);
+  const uint32_t abuf = w.aux_buf + k * kStageAuxBytes;
+  if (lane == 0) {  // the store that last used these buffers has read them
+    if (dbl) {
+      bulk_wait_read1();
+    } else {
+      bulk_wait_read0();
+    }
   }
-  if (ep.gelu) stage_bf16_row(w.aux_buf, lane, pre);
+  __syncwarp();
+  if (!f32) {
+    stage_bf16_row(obuf, lane, v);
+  } else {
+    stage_f32_row(obuf, lane, v);
+  }
+  if (ep.gelu) stage_bf16_row(abuf, lane, pre);
   fence_proxy_async_smem();
   __syncwarp();
   if (lane == 0) {
     if (ep.out_kind == kOutF32Accumulate) {
-      tma_reduce_add_2d(map_out, w.out_buf, n0, store_row);
+      tma_reduce_add_2d(map_out, obuf, n0, store_row);
     } else {
-      tma_store_2d(map_out, w.out_buf, n0, store_row);
+      tma_store_2d(map_out, obuf, n0, store_row);
     }
-    if (ep.gelu) tma_store_2d(map_aux, w.aux_buf, n0, static_cast<int32_t>(m_base));
+    if (ep.gelu) tma_store_2d(map_aux, abuf, n0, static_cast<int32_t>(m_base));
     bulk_commit();
   }
 }
@@ -433,6 +461,7 @@ __device__ __forceinline__ EpiWarp epi_warp_init(uint8_t* staging, int ew) {
   w.bias_buf = base + kEpiWarps * kStageWarpBytes + ew * kBiasWarpBytes;
   w.bar0 = base + kEpiWarps * (kStageWarpBytes + kBiasWarpBytes) + ew * 16;
   w.blk = 0;
+  w.sblk = 0;
   return w;
 }
 
@@ -652,6 +681,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int kb_total = (K + kBK - 1) / kBK;
   const int kb_per = (kb_total + splits - 1) / splits;
 
+  if (ep.trace != nullptr && threadIdx.x == 0) ep.trace[blockIdx.x * 8 + 0] = gtimer();
   if (warp == 0 && elect_one()) {
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
@@ -673,6 +703,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_enter();  // everything above overlapped the previous kernel's tail
+  if (ep.trace != nullptr && threadIdx.x == 0) ep.trace[blockIdx.x * 8 + 1] = gtimer();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -707,6 +738,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int c = 0; c < BN / 128; ++c)
               tma_load_2d_pair(b_dst + c * kBK * 128, &map_b, fb, nb0 + c * 64, k0);
           }
+          if (ep.trace != nullptr && unit == pair && kb == 0) ep.trace[blockIdx.x * 8 + 2] = gtimer();
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -731,6 +763,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
+          if (ep.trace != nullptr && local == 0 && kb == 0 && lane_id() == 0)
+            ep.trace[blockIdx.x * 8 + 3] = gtimer();
           if (elect_one()) {
             const uint32_t a_base = smem_u32(sA + stage * Cfg::kABytes);
             const uint32_t b_base = smem_u32(sB + stage * Cfg::kBBytes);
@@ -744,6 +778,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
             umma_commit_pair(&empty_bar[stage], 0x3);
             if (kb == num_kb - 1) umma_commit_pair(&tfull_bar[buf], 0x3);
+            if (ep.trace != nullptr && local == 0 && kb == num_kb - 1)
+              ep.trace[blockIdx.x * 8 + 4] = gtimer();
           }
           __syncwarp();
           if (++stage == S) {
@@ -772,6 +808,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       epilogue_tile_prologue<BN>(ep, &map_aux, ew, warp - 4, has_in, m_base, n0, N);
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
+      if (ep.trace != nullptr && local == 0 && warp == 4 && lane_id() == 0)
+        ep.trace[blockIdx.x * 8 + 5] = gtimer();
       const int32_t store_row = static_cast<int32_t>(
           m_base + (ep.out_kind == kOutF32Split ? static_cast<int64_t>(unit / num_tiles) * M : 0));
       epilogue_tile<BN, kAdam>(ep, &map_out, &map_aux, ew, warp - 4, has_in,
@@ -781,12 +819,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane_id() == 0) mbar_arrive_remote(leader_tempty0 + buf * 8);
     }
+    if (ep.trace != nullptr && warp == 4 && lane_id() == 0) ep.trace[blockIdx.x * 8 + 6] = gtimer();
     if (lane_id() == 0) bulk_wait_all();
     __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
   cluster_sync();
+  if (ep.trace != nullptr && threadIdx.x == 0) ep.trace[blockIdx.x * 8 + 7] = gtimer();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);

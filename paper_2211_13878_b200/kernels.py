@@ -33,8 +33,10 @@ def dropout_scale(p: float) -> float:
 
 def gemm(a, b, *, a_mn_major=False, b_mn_major=False, out=None, out_kind="bf16", bias=None,
          gelu_aux=None, residual=None, alpha=1.0, dropout_p=0.0, seed=0, site=0,
-         row_offset=0, col_offset=0, drop_ld=None, tile_n=0, stream=None, gelu_bwd_aux=None):
-    """C = A * B^T.  A is [M,K] (or [K,M] if a_mn_major); B is [N,K] (or [K,N])."""
+         row_offset=0, col_offset=0, drop_ld=None, tile_n=0, stream=None, gelu_bwd_aux=None,
+         trace=None):
+    """C = A * B^T.  A is [M,K] (or [K,M] if a_mn_major); B is [N,K] (or [K,N]).
+    trace: optional int64 device tensor [grid*8] receiving per-CTA %globaltimer stamps."""
     import torch
     M = a.shape[1] if a_mn_major else a.shape[0]
     K = a.shape[0] if a_mn_major else a.shape[1]
@@ -66,6 +68,7 @@ def gemm(a, b, *, a_mn_major=False, b_mn_major=False, out=None, out_kind="bf16",
     ep.drop_scale = dropout_scale(dropout_p)
     ep.seed = seed
     ep.site = site
+    ep.trace = _ptr(trace)
     _lib.check(_lib.lib().gx_k_gemm_bf16(
         _ptr(a), a.stride(0), int(a_mn_major), _ptr(b), b.stride(0), int(b_mn_major),
         M, N, K, ctypes.byref(ep), tile_n, _lib.stream_ptr(stream)))

@@ -1,3 +1,3 @@
 timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 200 python scripts/gemm_trace.py
 timeout 200 python scripts/step_variants.py default no_optimizer
-GX_FUSED_ADAM=1 timeout 200 python scripts/step_variants.py default

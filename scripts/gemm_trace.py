@@ -1,0 +1,36 @@
+"""Per-CTA phase timeline of one CTA-pair GEMM launch (globaltimer stamps, ns):
+entry, after-PDL, first-TMA, first-stage, last-MMA-issued, first-acc-ready, epi-done, exit."""
+import json, os, sys
+import torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2211_13878_b200 import kernels as K  # noqa: E402
+dev = torch.device("cuda:0")
+bf = torch.bfloat16
+names = ["entry", "pdl", "tma0", "stage0", "mma_last", "acc0", "epi_done", "exit"]
+shapes = {"up_fwd(gelu)": (512, 5120, 1280, False, "gelu"), "qkv_fwd": (512, 3840, 1280, False, None),
+          "dgrad_down(gelu_bwd)": (512, 5120, 1280, True, "gelu_bwd"), "out_fwd plain": (512, 1280, 1280, False, None),
+          "up_fwd plain": (512, 5120, 1280, False, None)}
+for name, (M, N, Kd, bmn, epi) in shapes.items():
+    A = (torch.randn(M, Kd, device=dev) * 0.5).to(bf)
+    B = (torch.randn(Kd, N, device=dev) if bmn else torch.randn(N, Kd, device=dev)).to(bf) * 0.05
+    aux = torch.randn(M, N, device=dev).to(bf)
+    bias = torch.randn(N, device=dev).to(bf)
+    tr = torch.zeros(148 * 8, dtype=torch.int64, device=dev)
+    kw = {}
+    if epi == "gelu":
+        kw = dict(bias=bias, gelu_aux=aux)
+    elif epi == "gelu_bwd":
+        kw = dict(gelu_bwd_aux=aux)
+    for i in range(4):
+        K.gemm(A, B, b_mn_major=bmn, trace=tr if i == 3 else None, **kw)
+    torch.cuda.synchronize()
+    t = tr.view(148, 8).cpu()
+    used = t[:, 0] > 0
+    t = t[used].double()
+    t0 = t[:, 0].min()
+    rel = (t - t0) / 1000.0  # us
+    med = rel.median(dim=0).values.tolist()
+    mx = rel.max(dim=0).values.tolist()
+    print(json.dumps({"gemm": name, "ctas": int(used.sum()),
+                      "median_us": {n: round(v, 2) for n, v in zip(names, med)},
+                      "max_us": {n: round(v, 2) for n, v in zip(names, mx)}}), flush=True)
