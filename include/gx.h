@@ -188,9 +188,10 @@ typedef struct gx_gemm_epilogue {
   void* adam_param;
   float lr, beta1, beta2, eps, weight_decay;
   const int64_t* step;        /* device step counter (bias corrections) */
-  /* debug: when set, CTA b writes %globaltimer stamps [b][0..7] (entry, after PDL wait,
+  /* debug: when set, CTA b writes %globaltimer stamps [b][0..15] (entry, after PDL wait,
    * first TMA issued, first stage landed, last MMA issued, first accumulator ready, epilogue
-   * done, exit) -- see scripts/gemm_trace.py */
+   * done, exit; then per epilogue chunk of warp 4: before / after its TMEM load) -- see
+   * scripts/gemm_trace.py */
   unsigned long long* trace;
 } gx_gemm_epilogue;
 

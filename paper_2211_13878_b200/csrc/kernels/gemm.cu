@@ -364,7 +364,10 @@ __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUt
     ++w.blk;
   }
   float v[32], pre[32];
+  const bool dstamp = ep.trace != nullptr && lane == 0 && (threadIdx.x >> 5) == 4 && w.sblk == 0;
+  if (dstamp) ep.trace[blockIdx.x * 16 + 12] = gtimer();
   epilogue_math(ep, row, n0, acc, bias_w, in_w, v, pre);
+  if (dstamp) ep.trace[blockIdx.x * 16 + 13] = gtimer();
   // Double-buffered staging, so block i+1's math overlaps block i's store: bf16 outputs use
   // the two halves of the 4 KB out buffer; fp32 outputs (weight gradients: no operand, no
   // aux) use the out buffer and the 4 KB operand/aux area; the GeLU pre-activation output
@@ -392,6 +395,7 @@ __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUt
   if (ep.gelu) stage_bf16_row(abuf, lane, pre);
   fence_proxy_async_smem();
   __syncwarp();
+  if (dstamp) ep.trace[blockIdx.x * 16 + 14] = gtimer();
   if (lane == 0) {
     if (ep.out_kind == kOutF32Accumulate) {
       tma_reduce_add_2d(map_out, obuf, n0, store_row);
@@ -401,6 +405,7 @@ __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUt
     if (ep.gelu) tma_store_2d(map_aux, abuf, n0, static_cast<int32_t>(m_base));
     bulk_commit();
   }
+  if (dstamp) ep.trace[blockIdx.x * 16 + 15] = gtimer();
 }
 
 
@@ -428,8 +433,11 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const CUte
     if (has_in && c + 1 < c_hi)
       epi_prefetch(w, map_aux, w.blk + 1, n0 + (c + 1) * 32, static_cast<int32_t>(m_base));
     uint32_t r[32];
+    const bool stamp = ep.trace != nullptr && ew == 0 && lane_id() == 0 && c - c_lo < 2;
+    if (stamp) ep.trace[blockIdx.x * 16 + 8 + 2 * (c - c_lo)] = gtimer();
     tmem_ld32(taddr + c * 32, r);
     tmem_ld_wait();
+    if (stamp) ep.trace[blockIdx.x * 16 + 9 + 2 * (c - c_lo)] = gtimer();
     if (m_base < M && n0 + c * 32 < N) {
       epilogue_block<kAdam>(ep, map_out, map_aux, w, has_in, c - c_lo, m_base, store_row, n0 + c * 32, M,
                      N, r);
@@ -681,7 +689,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int kb_total = (K + kBK - 1) / kBK;
   const int kb_per = (kb_total + splits - 1) / splits;
 
-  if (ep.trace != nullptr && threadIdx.x == 0) ep.trace[blockIdx.x * 8 + 0] = gtimer();
+  if (ep.trace != nullptr && threadIdx.x == 0) ep.trace[blockIdx.x * 16 + 0] = gtimer();
   if (warp == 0 && elect_one()) {
     tma_prefetch(&map_a);
     tma_prefetch(&map_b);
@@ -703,7 +711,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_enter();  // everything above overlapped the previous kernel's tail
-  if (ep.trace != nullptr && threadIdx.x == 0) ep.trace[blockIdx.x * 8 + 1] = gtimer();
+  if (ep.trace != nullptr && threadIdx.x == 0) ep.trace[blockIdx.x * 16 + 1] = gtimer();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -738,7 +746,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             for (int c = 0; c < BN / 128; ++c)
               tma_load_2d_pair(b_dst + c * kBK * 128, &map_b, fb, nb0 + c * 64, k0);
           }
-          if (ep.trace != nullptr && unit == pair && kb == 0) ep.trace[blockIdx.x * 8 + 2] = gtimer();
+          if (ep.trace != nullptr && unit == pair && kb == 0) ep.trace[blockIdx.x * 16 + 2] = gtimer();
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -764,7 +772,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           if (ep.trace != nullptr && local == 0 && kb == 0 && lane_id() == 0)
-            ep.trace[blockIdx.x * 8 + 3] = gtimer();
+            ep.trace[blockIdx.x * 16 + 3] = gtimer();
           if (elect_one()) {
             const uint32_t a_base = smem_u32(sA + stage * Cfg::kABytes);
             const uint32_t b_base = smem_u32(sB + stage * Cfg::kBBytes);
@@ -779,7 +787,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             umma_commit_pair(&empty_bar[stage], 0x3);
             if (kb == num_kb - 1) umma_commit_pair(&tfull_bar[buf], 0x3);
             if (ep.trace != nullptr && local == 0 && kb == num_kb - 1)
-              ep.trace[blockIdx.x * 8 + 4] = gtimer();
+              ep.trace[blockIdx.x * 16 + 4] = gtimer();
           }
           __syncwarp();
           if (++stage == S) {
@@ -809,7 +817,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
       if (ep.trace != nullptr && local == 0 && warp == 4 && lane_id() == 0)
-        ep.trace[blockIdx.x * 8 + 5] = gtimer();
+        ep.trace[blockIdx.x * 16 + 5] = gtimer();
       const int32_t store_row = static_cast<int32_t>(
           m_base + (ep.out_kind == kOutF32Split ? static_cast<int64_t>(unit / num_tiles) * M : 0));
       epilogue_tile<BN, kAdam>(ep, &map_out, &map_aux, ew, warp - 4, has_in,
@@ -817,16 +825,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                         store_row, n0, M, N);
       tc_fence_before();
       __syncwarp();
-      if (lane_id() == 0) mbar_arrive_remote(leader_tempty0 + buf * 8);
+      if (lane_id() == 0) mbar_arrive_remote_relaxed(leader_tempty0 + buf * 8);
     }
-    if (ep.trace != nullptr && warp == 4 && lane_id() == 0) ep.trace[blockIdx.x * 8 + 6] = gtimer();
+    if (ep.trace != nullptr && warp == 4 && lane_id() == 0) ep.trace[blockIdx.x * 16 + 6] = gtimer();
     if (lane_id() == 0) bulk_wait_all();
     __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
   cluster_sync();
-  if (ep.trace != nullptr && threadIdx.x == 0) ep.trace[blockIdx.x * 8 + 7] = gtimer();
+  if (ep.trace != nullptr && threadIdx.x == 0) ep.trace[blockIdx.x * 16 + 7] = gtimer();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc_pair<Cfg::kTmemCols>(tmem_base);

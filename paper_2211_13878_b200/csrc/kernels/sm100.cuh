@@ -188,6 +188,14 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// Relaxed remote arrive: orders nothing but the arrive itself.  Used where the only thing to
+// publish is TMEM reads (already ordered by tcgen05.wait::ld + fence::before_thread_sync), so
+// the release form's GPU-scope MEMBAR -- which waits for this thread's outstanding memory
+// traffic, e.g. the epilogue's TMA stores -- is avoided.
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(

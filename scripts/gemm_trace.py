@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2211_13878_b200 import kernels as K  # noqa: E402
 dev = torch.device("cuda:0")
 bf = torch.bfloat16
-names = ["entry", "pdl", "tma0", "stage0", "mma_last", "acc0", "epi_done", "exit"]
+names = ["entry", "pdl", "tma0", "stage0", "mma_last", "acc0", "epi_done", "exit", "c0", "c0ld", "c1", "c1ld", "blk0_math0", "blk0_math1", "blk0_staged", "blk0_stored"]
 shapes = {"up_fwd(gelu)": (512, 5120, 1280, False, "gelu"), "qkv_fwd": (512, 3840, 1280, False, None),
           "dgrad_down(gelu_bwd)": (512, 5120, 1280, True, "gelu_bwd"), "out_fwd plain": (512, 1280, 1280, False, None),
           "up_fwd plain": (512, 5120, 1280, False, None)}
@@ -15,7 +15,7 @@ for name, (M, N, Kd, bmn, epi) in shapes.items():
     B = (torch.randn(Kd, N, device=dev) if bmn else torch.randn(N, Kd, device=dev)).to(bf) * 0.05
     aux = torch.randn(M, N, device=dev).to(bf)
     bias = torch.randn(N, device=dev).to(bf)
-    tr = torch.zeros(148 * 8, dtype=torch.int64, device=dev)
+    tr = torch.zeros(148 * 16, dtype=torch.int64, device=dev)
     kw = {}
     if epi == "gelu":
         kw = dict(bias=bias, gelu_aux=aux)
@@ -24,13 +24,11 @@ for name, (M, N, Kd, bmn, epi) in shapes.items():
     for i in range(4):
         K.gemm(A, B, b_mn_major=bmn, trace=tr if i == 3 else None, **kw)
     torch.cuda.synchronize()
-    t = tr.view(148, 8).cpu()
+    t = tr.view(148, 16).cpu()
     used = t[:, 0] > 0
     t = t[used].double()
     t0 = t[:, 0].min()
     rel = (t - t0) / 1000.0  # us
-    med = rel.median(dim=0).values.tolist()
-    mx = rel.max(dim=0).values.tolist()
+    med = [float(rel[t[:, i] > 0, i].median()) if (t[:, i] > 0).any() else None for i in range(16)]
     print(json.dumps({"gemm": name, "ctas": int(used.sum()),
-                      "median_us": {n: round(v, 2) for n, v in zip(names, med)},
-                      "max_us": {n: round(v, 2) for n, v in zip(names, mx)}}), flush=True)
+                      "median_us": {n: round(v, 2) for n, v in zip(names, med) if v is not None}}), flush=True)
