@@ -72,6 +72,16 @@ int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* r
                   const gx_dropout* drop = nullptr, void* dz = nullptr, void* dbias = nullptr,
                   int dy_slices = 1, int64_t dy_slice_stride = 0);
 int64_t layernorm_bwd_ws_floats(int h);
+// The two passes separately (the executor runs the column pass on the weight-gradient
+// stream): rows writes dx (and dz), and -- with dy_fold -- the fp32 (slice-summed) dy that
+// the column pass then reads as its dy (dy_f32 = true).
+int layernorm_bwd_rows(const void* dy, const void* x, const void* mean, const void* rstd,
+                       const void* gamma, const void* dres, void* dx, int rows, int h,
+                       cudaStream_t st, bool dy_f32, const gx_dropout* drop, void* dz,
+                       int dy_slices, int64_t dy_slice_stride, float* dy_fold);
+int layernorm_bwd_cols(const void* dy, bool dy_f32, const void* x, const void* mean,
+                       const void* rstd, const void* dz, void* dgamma, void* dbeta, void* dbias,
+                       int rows, int h, float* workspace, cudaStream_t st);
 // x_f32: x is fp32, the sum of x_slices slices slice_stride elements apart (split-K output)
 int bias_dropout_add(const void* x, const void* bias, const void* residual, void* out, int rows,
                      int cols, const gx_dropout& d, cudaStream_t st, bool x_f32 = false,

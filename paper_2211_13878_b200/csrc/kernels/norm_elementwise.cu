@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(512) layernorm_bwd_rows_kernel(
     const void* dy, const uint4* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, const uint4* __restrict__ gamma, const uint4* __restrict__ dres,
     uint4* __restrict__ dx, uint4* __restrict__ dz, gx_dropout d, int rows, int h, int dy_slices,
-    int64_t dy_stride) {
+    int64_t dy_stride, float* __restrict__ dy_fold) {
   pdl_enter();
   __shared__ float red[2][16];
   const int chunks = h >> 3;
@@ -230,11 +230,16 @@ __global__ void __launch_bounds__(512) layernorm_bwd_rows_kernel(
 #pragma unroll
           for (int j = 0; j < 8; ++j) dv[j] += acc[sl - 1][j];
         }
-      if (dy_slices > 1) {  // fold the split-K slices into slice 0 for the column pass
+      if (dy_slices > 1 && dy_fold == nullptr) {  // fold the slices into slice 0 for the column pass
         float4* o = reinterpret_cast<float4*>(const_cast<void*>(dy)) + 2 * i;
         o[0] = make_float4(dv[0], dv[1], dv[2], dv[3]);
         o[1] = make_float4(dv[4], dv[5], dv[6], dv[7]);
       }
+    }
+    if (dy_fold != nullptr) {  // fp32 dy for a deferred column pass
+      float4* o = reinterpret_cast<float4*>(dy_fold) + 2 * i;
+      o[0] = make_float4(dv[0], dv[1], dv[2], dv[3]);
+      o[1] = make_float4(dv[4], dv[5], dv[6], dv[7]);
     }
     unpack8(x[i], xh);
     unpack8(__ldg(gamma + ci), gm);
@@ -378,18 +383,16 @@ int64_t layernorm_bwd_ws_floats(int h) {
   return static_cast<int64_t>(kLnBwdMaxSlices) * 3 * h + (h / 64 + 64);
 }
 
-int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
-                  const void* gamma, const void* dres, void* dx, void* dgamma, void* dbeta,
-                  int rows, int h, float* workspace, cudaStream_t st, bool dy_f32,
-                  const gx_dropout* drop, void* dz, void* dbias, int dy_slices,
-                  int64_t dy_slice_stride) {
+int layernorm_bwd_rows(const void* dy, const void* x, const void* mean, const void* rstd,
+                       const void* gamma, const void* dres, void* dx, int rows, int h,
+                       cudaStream_t st, bool dy_f32, const gx_dropout* drop, void* dz,
+                       int dy_slices, int64_t dy_slice_stride, float* dy_fold) {
   if (h % 8 != 0 || h > 4096) return set_error(kErrConfig, "layernorm: h must be a multiple of 8, <= 4096");
   if (rows <= 0) return kOk;
   if (dy_slices < 1 || dy_slices > kMaxSplits || (dy_slices > 1 && !dy_f32))
     return set_error(kErrConfig, "layernorm_bwd: dy slices need fp32 dy");
   const bool fuse = drop != nullptr;
-  if (fuse && (dz == nullptr || dbias == nullptr))
-    return set_error(kErrConfig, "layernorm_bwd: fused dropout needs dz and dbias");
+  if (fuse && dz == nullptr) return set_error(kErrConfig, "layernorm_bwd: fused dropout needs dz");
   const gx_dropout dd = fuse ? *drop : gx_dropout{};
   const int threads = ((h / 8) + 31) / 32 * 32;  // <= 512 for h <= 4096
   auto* krows = dy_f32 ? (fuse ? layernorm_bwd_rows_kernel<true, true> : layernorm_bwd_rows_kernel<true, false>)
@@ -398,8 +401,16 @@ int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* r
            static_cast<const float*>(mean), static_cast<const float*>(rstd),
            static_cast<const uint4*>(gamma), static_cast<const uint4*>(dres),
            static_cast<uint4*>(dx), static_cast<uint4*>(dz), dd, rows, h, dy_slices,
-           dy_slice_stride);
-  GX_RC(check_launch("layernorm_bwd_rows_kernel"));
+           dy_slice_stride, dy_fold);
+  return check_launch("layernorm_bwd_rows_kernel");
+}
+
+int layernorm_bwd_cols(const void* dy, bool dy_f32, const void* x, const void* mean,
+                       const void* rstd, const void* dz, void* dgamma, void* dbeta, void* dbias,
+                       int rows, int h, float* workspace, cudaStream_t st) {
+  if (rows <= 0) return kOk;
+  const bool fuse = dz != nullptr;
+  if (fuse && dbias == nullptr) return set_error(kErrConfig, "layernorm_bwd: dz needs dbias");
   int strips, slices, rps;
   ln_cols_grid(rows, h, &strips, &slices, &rps);
   unsigned int* tickets = reinterpret_cast<unsigned int*>(
@@ -409,8 +420,22 @@ int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* r
   launch_k(kcols, dim3(strips, slices), dim3(256), 0, st, dy, static_cast<const uint4*>(x),
            static_cast<const float*>(mean), static_cast<const float*>(rstd),
            static_cast<const uint4*>(dz), static_cast<float*>(dgamma), static_cast<float*>(dbeta),
-           static_cast<float*>(dbias), workspace, tickets, rows, h, rps, 1, dy_slice_stride);
+           static_cast<float*>(dbias), workspace, tickets, rows, h, rps, 1, int64_t{0});
   return check_launch("layernorm_bwd_cols_kernel");
+}
+
+int layernorm_bwd(const void* dy, const void* x, const void* mean, const void* rstd,
+                  const void* gamma, const void* dres, void* dx, void* dgamma, void* dbeta,
+                  int rows, int h, float* workspace, cudaStream_t st, bool dy_f32,
+                  const gx_dropout* drop, void* dz, void* dbias, int dy_slices,
+                  int64_t dy_slice_stride) {
+  if (drop != nullptr && (dz == nullptr || dbias == nullptr))
+    return set_error(kErrConfig, "layernorm_bwd: fused dropout needs dz and dbias");
+  GX_RC(layernorm_bwd_rows(dy, x, mean, rstd, gamma, dres, dx, rows, h, st, dy_f32, drop, dz,
+                           dy_slices, dy_slice_stride, nullptr));
+  // the column pass reads slice 0, into which the row pass folded the slices
+  return layernorm_bwd_cols(dy, dy_f32, x, mean, rstd, drop != nullptr ? dz : nullptr, dgamma,
+                            dbeta, dbias, rows, h, workspace, st);
 }
 
 // -------------------------------------------------------- bias + dropout + residual

@@ -177,6 +177,7 @@ struct RankCtx {
   // buffer.  wg_done[p] marks the last wgrad that read buffer set p.
   bf16 *dzb[2] = {nullptr, nullptr}, *dpreb[2] = {nullptr, nullptr},
        *doutb[2] = {nullptr, nullptr}, *dqkvb[2] = {nullptr, nullptr};
+  float* lnfold[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [parity][LN2, LN1] fp32 dy
   cudaEvent_t wg_done[2] = {nullptr, nullptr};
   bool wg_pending[2] = {false, false};
   bf16* gbuf[2] = {nullptr, nullptr};
@@ -778,6 +779,8 @@ int ExecutorImpl::allocate(RankCtx& r) {
     r.dpreb[p] = A.a<bf16>(max_f);
     r.doutb[p] = A.a<bf16>(max_h);
     r.dqkvb[p] = A.a<bf16>(max_q);
+    r.lnfold[p][0] = A.a<float>(max_h);
+    r.lnfold[p][1] = A.a<float>(max_h);
     if (cudaEventCreateWithFlags(&r.wg_done[p], cudaEventDisableTiming) != cudaSuccess)
       return set_error(kErrCuda, "executor: event creation failed");
   }
@@ -1279,10 +1282,17 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     const void* dc_in = r.dc_slices ? static_cast<const void*>(r.acc32) : static_cast<const void*>(r.dc);
     // LN2 backward with the out-projection's dropout backward + bias gradient fused in:
     // dx1 = residual-stream gradient, dout = dropout_mask(dx1), dbo += colsum(dout)
+    // (row pass on the critical path; the dgamma / dbeta / dbias column pass rides the wgrad
+    // stream from the row pass's fp32 copy of dy)
     d.site = 3ull * l + 1;
-    GX_TRY(timed(kNorm, 0, 10.0 * rows * h, [&] { return layernorm_bwd(dc_in, A.x1, A.mean2, A.rstd2, P + L.lay.ln2g.off, dY, r.dx1,
-                         G + L.lay.ln2g.off, G + L.lay.ln2b.off, rows, h, r.ln_ws, stream_, r.dc_slices > 0,
-                         &d, dout, G + L.lay.bo.off, std::max(1, r.dc_slices), static_cast<int64_t>(rows) * h); }));
+    float* fold2 = r.lnfold[par][0];
+    GX_TRY(timed(kNorm, 0, 10.0 * rows * h, [&] { return layernorm_bwd_rows(dc_in, A.x1, A.mean2, A.rstd2, P + L.lay.ln2g.off, dY, r.dx1,
+                         rows, h, stream_, r.dc_slices > 0, &d, dout, std::max(1, r.dc_slices),
+                         static_cast<int64_t>(rows) * h, fold2); }));
+    GX_TRY(on_wgrad([&] {
+      return timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd_cols(fold2, true, A.x1, A.mean2, A.rstd2, dout,
+                         G + L.lay.ln2g.off, G + L.lay.ln2b.off, G + L.lay.bo.off, rows, h, r.ln_ws, ls_); });
+    }));
     const gx_gemm_epilogue wo = wgrad_ep(L.lay.wo, ht);
     auto wgrado = [&] { return on_wgrad([&] { return gemm(dout, h, true, A.ctx, ht, true, h, ht, rows, wo); }); };  // dWo = dout^T ctx
     if (!fuse_adam) GX_TRY(wgrado());
@@ -1324,12 +1334,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       return on_wgrad([&]() -> int {
         GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, ls_); }));
         const gx_gemm_epilogue wq = wgrad_ep(L.lay.wqkv, h);
-        GX_TRY(gemm(dqkv, 3 * ht, true, A.ln1, h, true, 3 * ht, h, rows, wq));  // dWqkv
-        if (wg_active_) {  // the last reader of this parity's buffers
-          GX_TRY(cuda_check(cudaEventRecord(r.wg_done[par], wg_), "wgrad done"));
-          r.wg_pending[par] = true;
-        }
-        return kOk;
+        return gemm(dqkv, 3 * ht, true, A.ln1, h, true, 3 * ht, h, rows, wq);  // dWqkv
       });
     };
     if (!fuse_adam) GX_TRY(wgradq());
@@ -1378,10 +1383,20 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       dp.seed_offset = r.seed_off;
       dz_prev = r.dzb[pp];
     }
-    GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd(da_in, A.x, A.mean1, A.rstd1, P + L.lay.ln1g.off, r.dx1, dX,
-                         G + L.lay.ln1g.off, G + L.lay.ln1b.off, rows, h, r.ln_ws, stream_, r.da_slices > 0,
-                         prev ? &dp : nullptr, dz_prev, prev ? Lp->gfull + Lp->lay.b2.off : nullptr,
-                         std::max(1, r.da_slices), static_cast<int64_t>(rows) * h); }));
+    float* fold1 = r.lnfold[par][1];
+    GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd_rows(da_in, A.x, A.mean1, A.rstd1, P + L.lay.ln1g.off, r.dx1, dX,
+                         rows, h, stream_, r.da_slices > 0, prev ? &dp : nullptr, dz_prev,
+                         std::max(1, r.da_slices), static_cast<int64_t>(rows) * h, fold1); }));
+    GX_TRY(on_wgrad([&]() -> int {
+      GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd_cols(fold1, true, A.x, A.mean1, A.rstd1, dz_prev,
+                           G + L.lay.ln1g.off, G + L.lay.ln1b.off, prev ? Lp->gfull + Lp->lay.b2.off : nullptr,
+                           rows, h, r.ln_ws, ls_); }));
+      if (wg_active_) {  // the last reader of this parity's buffers
+        GX_TRY(cuda_check(cudaEventRecord(r.wg_done[par], wg_), "wgrad done"));
+        r.wg_pending[par] = true;
+      }
+      return kOk;
+    }));
     if (prev != nullptr) prev->dz_ready = true;
   }
   return kOk;
