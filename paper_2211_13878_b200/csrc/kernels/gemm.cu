@@ -33,6 +33,12 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;  // 64 bf16 = 128 B = one swizzle span
 constexpr int kEpiWarps = 8;  // warps 4..11: two per TMEM lane quarter, each half the columns
 constexpr int kThreads = 128 + 32 * kEpiWarps;
+// 384 threads x 128 registers = 48K of the SM's 64K: a GEMM CTA leaves room for a co-resident
+// block of another stream (the optimizer / column passes beside the data-gradient chain)
+#ifndef GX_GEMM_MAXREGS
+#define GX_GEMM_MAXREGS 128
+#endif
+constexpr int kGemmMaxRegs = GX_GEMM_MAXREGS;
 // epilogue staging per warp: out 4 KB + two 2 KB bf16 operand buffers + 256 B bias, plus the
 // operand-prefetch mbarriers (see kStagingBytes below)
 constexpr int kStagingBytesDecl = kEpiWarps * (4096 + 2048 + 2048 + 256) + kEpiWarps * 2 * 8;
@@ -474,7 +480,7 @@ __device__ __forceinline__ EpiWarp epi_warp_init(uint8_t* staging, int ew) {
 }
 
 template <int BN, bool kAMN, bool kBMN, bool kAdam = false>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __maxnreg__(kGemmMaxRegs)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_out,
@@ -657,7 +663,7 @@ struct PairCfg {
 };
 
 template <int BN, bool kAMN, bool kBMN, bool kAdam = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(kGemmMaxRegs)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                      const __grid_constant__ CUtensorMap map_b,
                      const __grid_constant__ CUtensorMap map_out,

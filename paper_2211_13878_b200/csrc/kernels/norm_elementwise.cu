@@ -796,12 +796,14 @@ int adamw(void* master, const void* grad, void* m, void* v, void* bf16_out, int6
 }
 
 // Same update with the step count read from device memory (CUDA-graph friendly).
-__global__ void adamw_dev_kernel(float4* __restrict__ p, const float4* __restrict__ g,
+// <= 64 registers (256 x 64 = 16K): a block fits beside a 128-register GEMM CTA (48K), so
+// the optimizer can share SMs with the backward instead of waiting for whole free SMs.
+__global__ void __launch_bounds__(256, 4) adamw_dev_kernel(float4* __restrict__ p, const float4* __restrict__ g,
                                  float4* __restrict__ m, float4* __restrict__ v,
                                  uint2* __restrict__ out, int64_t n4, float lr, float b1, float b2,
                                  float eps, float wd, const int64_t* __restrict__ step) {
   pdl_enter();
-  adam_range<4>(adam_scalars_step(lr, b1, b2, eps, wd, step), p, g, m, v,
+  adam_range<2>(adam_scalars_step(lr, b1, b2, eps, wd, step), p, g, m, v,
              out, n4);
 }
 
