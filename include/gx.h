@@ -142,6 +142,10 @@ GX_API int gx_exec_profile_report(gx_exec* ex, char* out, size_t cap, size_t* ne
  * canonical index, never on the sharding): LN gains 1, biases 0, weights N(0, std^2). */
 GX_API int gx_exec_init_params(gx_exec* ex, uint64_t seed, float std_dev);
 GX_API int gx_exec_loss(gx_exec* ex, float* out);
+/* Apply the AdamW update still pending from the last step.  By default the optimizer of step
+ * t runs at the start of step t+1, overlapped with its forward (config "defer_optimizer");
+ * gx_exec_export_layer(params) flushes implicitly. */
+GX_API int gx_exec_flush(gx_exec* ex);
 /* load_batch + run + loss: the end-to-end call (host buffers in, loss out). */
 GX_API int gx_exec_step(gx_exec* ex, const void* x_host, const void* target_host, int use_graph,
                         float* loss_out);

@@ -12,6 +12,19 @@ extern "C" int gx_k_gemm_bf16(const void* a, int64_t lda, int a_mn_major, const 
 
 namespace {
 cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+// standalone entry points share one zero-initialised column-sum workspace (up to 8192 columns)
+float* colsum_ws() {
+  static float* ws = nullptr;
+  if (ws == nullptr) {
+    const size_t n = static_cast<size_t>(gx::colsum_ws_floats(8192));
+    if (cudaMalloc(&ws, n * sizeof(float)) != cudaSuccess ||
+        cudaMemset(ws, 0, n * sizeof(float)) != cudaSuccess) {
+      ws = nullptr;
+    }
+  }
+  return ws;
+}
+
 }  // namespace
 
 extern "C" int gx_k_gemm_bf16_splitk(const void* a, int64_t lda, int a_mn_major, const void* b,
@@ -69,11 +82,15 @@ extern "C" int gx_k_bias_dropout_add(const void* x, const void* bias, const void
 extern "C" int gx_k_dropout_bwd_colsum(const void* dy, void* dz, void* dbias, int rows, int cols,
                                        const gx_dropout* d, void* stream) {
   gx_dropout off{};
-  return gx::dropout_bwd_colsum(dy, dz, dbias, rows, cols, d ? *d : off, S(stream));
+  float* ws = colsum_ws();
+  if (ws == nullptr) return gx::set_error(gx::kErrCuda, "colsum: workspace allocation failed");
+  return gx::dropout_bwd_colsum(dy, dz, dbias, rows, cols, d ? *d : off, S(stream), ws);
 }
 extern "C" int gx_k_colsum(const void* x, int64_t ld, void* acc, int rows, int cols,
                            void* stream) {
-  return gx::colsum(x, ld, acc, rows, cols, S(stream));
+  float* ws = colsum_ws();
+  if (ws == nullptr) return gx::set_error(gx::kErrCuda, "colsum: workspace allocation failed");
+  return gx::colsum(x, ld, acc, rows, cols, S(stream), ws);
 }
 extern "C" int gx_k_mse_loss(const void* y, const void* target, void* dy, void* loss, int64_t n,
                              float inv_count, void* stream) {

@@ -92,9 +92,14 @@ int residual_layernorm(const float* x, int slices, int64_t slice_stride, const v
                        const void* residual, void* y, const gx_dropout& d, const void* gamma,
                        const void* beta, void* ln, void* mean, void* rstd, int rows, int h,
                        cudaStream_t st);
+// Column sums are deterministic: per-slice partials in `ws` (colsum_ws_floats(max cols)
+// words, zero-initialised once, left reset), added in slice order; one workspace per stream.
+constexpr int kColsumTickets = 256;
+constexpr int kColsumMaxSlices = 64;
+int64_t colsum_ws_floats(int max_cols);
 int dropout_bwd_colsum(const void* dy, void* dz, void* dbias, int rows, int cols,
-                       const gx_dropout& d, cudaStream_t st);
-int colsum(const void* x, int64_t ld, void* acc, int rows, int cols, cudaStream_t st);
+                       const gx_dropout& d, cudaStream_t st, float* ws);
+int colsum(const void* x, int64_t ld, void* acc, int rows, int cols, cudaStream_t st, float* ws);
 // workspace: kLossBlocks + 1 words, zero-initialised once (the kernel leaves it reset)
 constexpr int kLossBlocks = 512;
 int mse_loss(const void* y, const void* target, void* dy, void* loss, int64_t n, float inv_count,
@@ -105,7 +110,9 @@ int cast_bf16(const void* src, void* dst, int64_t n, cudaStream_t st);
 // max_blocks > 0 caps the grid (the overlapped optimizer stream leaves SMs to the backward)
 int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n,
               float lr, float beta1, float beta2, float eps, float wd, const int64_t* step,
-              cudaStream_t st, int max_blocks = 0);
+              cudaStream_t st, int max_blocks = 0, const int* pending = nullptr);
+// *flag = v (stream-ordered; graph-friendly device flag updates)
+int set_flag(int* flag, int v, cudaStream_t st);
 int bump_step(int64_t* step, uint64_t* seed_offset, cudaStream_t st);
 struct PtrPack {
   const void* p[16];

@@ -591,13 +591,16 @@ int residual_layernorm(const float* x, int slices, int64_t slice_stride, const v
 }
 
 // --------------------------------------------- dropout backward + bias-grad column sums
-// Block handles a strip of 64 columns (8 chunks) over a slice of rows; column partials are
-// reduced in shared memory then added to dbias with one atomic per column per block.
+// Block = (64-column strip, row slice): 8 chunks x 32 row lanes accumulate, the 32 lanes are
+// combined in shared memory in a fixed order, and the slices of a strip are added in slice
+// order by the strip's last block (ticket) -- deterministic, no floating-point atomics.
+// ws: kColsumTickets ticket words, then [slices][cols] partials (zero-initialised once).
 __global__ void __launch_bounds__(256) dropout_bwd_colsum_kernel(
     const uint4* __restrict__ dy, uint4* __restrict__ dz, float* __restrict__ dbias, int rows,
-    int cols, int64_t ld_chunks, gx_dropout d, int rows_per_block) {
+    int cols, int64_t ld_chunks, gx_dropout d, int rows_per_block, float* __restrict__ ws) {
   pdl_enter();
   __shared__ float red[32][65];
+  __shared__ bool last;
   const int cchunks = cols >> 3;
   const int cstrip = blockIdx.x * 8;           // first chunk of this strip
   const int cc = cstrip + (threadIdx.x & 7);   // this thread's chunk
@@ -628,45 +631,77 @@ __global__ void __launch_bounds__(256) dropout_bwd_colsum_kernel(
 #pragma unroll
   for (int j = 0; j < 8; ++j) red[rlane][(threadIdx.x & 7) * 8 + j] = acc[j];
   __syncthreads();
+  const int col = cstrip * 8 + threadIdx.x;  // threads 0..63 own the strip's columns
+  float sum = 0.f;
   if (threadIdx.x < 64) {
-    float s = 0.f;
-    for (int r = 0; r < 32; ++r) s += red[r][threadIdx.x];
-    const int col = cstrip * 8 + threadIdx.x;
-    if (dbias != nullptr && col < cols) atomicAdd(dbias + col, s);
+    for (int rl = 0; rl < 32; ++rl) sum += red[rl][threadIdx.x];
   }
+  if (dbias == nullptr) return;
+  if (gridDim.y == 1) {
+    if (threadIdx.x < 64 && col < cols) dbias[col] += sum;
+    return;
+  }
+  unsigned int* tickets = reinterpret_cast<unsigned int*>(ws);
+  float* part = ws + kColsumTickets;
+  if (threadIdx.x < 64 && col < cols) part[static_cast<int64_t>(blockIdx.y) * cols + col] = sum;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    last = atomicAdd(&tickets[blockIdx.x], 1u) == static_cast<unsigned>(gridDim.y - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < 64 && col < cols) {
+    float t = 0.f;
+    for (int y = 0; y < static_cast<int>(gridDim.y); ++y)
+      t += __ldcg(part + static_cast<int64_t>(y) * cols + col);
+    dbias[col] += t;
+  }
+  if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;
+}
+
+static void colsum_grid(int rows, int cols, dim3* grid, int* rpb) {
+  const int strips = (cols / 8 + 7) / 8;
+  int ysplit = (num_sms() * 4 + strips - 1) / strips;
+  const int max_y = (rows + 31) / 32;
+  if (ysplit > max_y) ysplit = max_y;
+  if (ysplit > kColsumMaxSlices) ysplit = kColsumMaxSlices;
+  if (ysplit < 1) ysplit = 1;
+  *rpb = (rows + ysplit - 1) / ysplit;
+  *grid = dim3(strips, (rows + *rpb - 1) / *rpb);
+}
+
+int64_t colsum_ws_floats(int max_cols) {
+  return kColsumTickets + static_cast<int64_t>(kColsumMaxSlices) * max_cols;
 }
 
 int dropout_bwd_colsum(const void* dy, void* dz, void* dbias, int rows, int cols,
-                       const gx_dropout& d, cudaStream_t st) {
+                       const gx_dropout& d, cudaStream_t st, float* ws) {
   if (cols % 8) return set_error(kErrConfig, "dropout_bwd: cols % 8 != 0");
+  if (cols / 64 + 1 > kColsumTickets) return set_error(kErrConfig, "dropout_bwd: too many columns");
   if (rows <= 0) return kOk;
-  const int strips = (cols / 8 + 7) / 8;
-  int ysplit = (num_sms() * 4 + strips - 1) / strips;
-  const int max_y = (rows + 31) / 32;
-  if (ysplit > max_y) ysplit = max_y;
-  if (ysplit < 1) ysplit = 1;
-  const int rpb = (rows + ysplit - 1) / ysplit;
-  dim3 grid(strips, ysplit);
+  dim3 grid;
+  int rpb;
+  colsum_grid(rows, cols, &grid, &rpb);
+  if (grid.y > 1 && ws == nullptr) return set_error(kErrConfig, "dropout_bwd: workspace required");
   launch_k(dropout_bwd_colsum_kernel, grid, dim3(256), 0, st, static_cast<const uint4*>(dy),
            static_cast<uint4*>(dz), static_cast<float*>(dbias), rows, cols,
-           static_cast<int64_t>(cols / 8), d, rpb);
+           static_cast<int64_t>(cols / 8), d, rpb, ws);
   return check_launch("dropout_bwd_colsum_kernel");
 }
 
-int colsum(const void* x, int64_t ld, void* acc, int rows, int cols, cudaStream_t st) {
+int colsum(const void* x, int64_t ld, void* acc, int rows, int cols, cudaStream_t st, float* ws) {
   if (cols % 8 || ld % 8) return set_error(kErrConfig, "colsum: cols/ld % 8 != 0");
+  if (cols / 64 + 1 > kColsumTickets) return set_error(kErrConfig, "colsum: too many columns");
   if (rows <= 0) return kOk;
   gx_dropout off{};
-  const int strips = (cols / 8 + 7) / 8;
-  int ysplit = (num_sms() * 4 + strips - 1) / strips;
-  const int max_y = (rows + 31) / 32;
-  if (ysplit > max_y) ysplit = max_y;
-  if (ysplit < 1) ysplit = 1;
-  const int rpb = (rows + ysplit - 1) / ysplit;
-  dim3 grid(strips, ysplit);
+  dim3 grid;
+  int rpb;
+  colsum_grid(rows, cols, &grid, &rpb);
+  if (grid.y > 1 && ws == nullptr) return set_error(kErrConfig, "colsum: workspace required");
   launch_k(dropout_bwd_colsum_kernel, grid, dim3(256), 0, st, static_cast<const uint4*>(x),
            const_cast<uint4*>(static_cast<const uint4*>(x)), static_cast<float*>(acc), rows,
-           cols, static_cast<int64_t>(ld / 8), off, rpb);
+           cols, static_cast<int64_t>(ld / 8), off, rpb, ws);
   return check_launch("colsum_kernel");
 }
 
@@ -801,15 +836,17 @@ int adamw(void* master, const void* grad, void* m, void* v, void* bf16_out, int6
 __global__ void __launch_bounds__(256, 4) adamw_dev_kernel(float4* __restrict__ p, const float4* __restrict__ g,
                                  float4* __restrict__ m, float4* __restrict__ v,
                                  uint2* __restrict__ out, int64_t n4, float lr, float b1, float b2,
-                                 float eps, float wd, const int64_t* __restrict__ step) {
+                                 float eps, float wd, const int64_t* __restrict__ step,
+                                 const int* __restrict__ pending) {
   pdl_enter();
+  if (pending != nullptr && *pending == 0) return;  // deferred update with nothing to apply
   adam_range<2>(adam_scalars_step(lr, b1, b2, eps, wd, step), p, g, m, v,
              out, n4);
 }
 
 int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n,
               float lr, float beta1, float beta2, float eps, float wd, const int64_t* step,
-              cudaStream_t st, int max_blocks) {
+              cudaStream_t st, int max_blocks, const int* pending) {
   if (n % 4) return set_error(kErrConfig, "adamw: n % 4 != 0");
   if (n == 0) return kOk;
   // Short-lived blocks (one 4-float4 strip per thread, no grid-stride loop): the block
@@ -823,8 +860,17 @@ int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, 
   launch_k(adamw_dev_kernel, dim3(blocks), dim3(256), 0, st,
            static_cast<float4*>(master), static_cast<const float4*>(grad),
            static_cast<float4*>(m), static_cast<float4*>(v), static_cast<uint2*>(bf16_out), n / 4,
-           lr, beta1, beta2, eps, wd, step);
+           lr, beta1, beta2, eps, wd, step, pending);
   return check_launch("adamw_dev_kernel");
+}
+
+__global__ void set_flag_kernel(int* flag, int v) {
+  pdl_enter();
+  *flag = v;
+}
+int set_flag(int* flag, int v, cudaStream_t st) {
+  launch_k(set_flag_kernel, dim3(1), dim3(1), 0, st, flag, v);
+  return check_launch("set_flag_kernel");
 }
 
 __global__ void step_counters_kernel(int64_t* step, uint64_t* seed_offset) {

@@ -183,11 +183,14 @@ struct RankCtx {
   bf16* gbuf[2] = {nullptr, nullptr};
   float *dq_acc = nullptr, *dsum = nullptr;
   float* ln_ws = nullptr;  // LayerNorm-backward block partials
+  float* cs_ws[2] = {nullptr, nullptr};  // column-sum workspaces: [0] main stream, [1] wgrad stream
   float* acc32 = nullptr;  // split-K fp32 slices [kMaxSplits][rows][h]
   bf16 *x_in = nullptr, *target = nullptr;  // [m micro-batches of this rank's rows][h]
   bf16* dx_out = nullptr;                   // first stage: input gradient per micro-batch
   float *loss = nullptr, *loss_dummy = nullptr;
   float* loss_ws = nullptr;  // deterministic loss reduction: block partials + ticket
+  int* opt_pending = nullptr;  // deferred optimizer: gradients of the last step not applied yet
+  std::vector<cudaEvent_t> opt_done;  // deferred optimizer: layer li updated (forward may read)
   int64_t* step = nullptr;
   uint64_t* seed_off = nullptr;
   int64_t in_rows_total = 0;
@@ -219,9 +222,12 @@ class ExecutorImpl final : public Executor {
     for (auto& t : tr_) cudaEventDestroy(t.second);
     for (cudaEvent_t e : fork_events_) cudaEventDestroy(e);
     if (join_event_ != nullptr) cudaEventDestroy(join_event_);
-    for (auto& r : ranks_)
+    for (auto& r : ranks_) {
       for (cudaEvent_t e : r->wg_done)
         if (e != nullptr) cudaEventDestroy(e);
+      for (cudaEvent_t e : r->opt_done)
+        if (e != nullptr) cudaEventDestroy(e);
+    }
     ranks_.clear();
     comm_.reset();
     if (stream_ != nullptr) cudaStreamDestroy(stream_);
@@ -401,10 +407,22 @@ class ExecutorImpl final : public Executor {
   // default: exact (tested against the standalone kernel) and 8 B/param less HBM traffic, but
   // the row-per-lane state loads make the wgrad GEMMs hold SMs far longer (measured slower).
   bool fused_adam_ = false;
+  // Deferred optimizer (cfg "defer_optimizer" / GX_DEFER_OPT=1): the AdamW of step t
+  // runs at the start of step t+1 on the side stream, layer 0 first, and layer l's forward
+  // waits only for layer l's update -- the HBM-bound update overlaps the next forward instead
+  // of contending with this backward.  A device flag makes the first step's pass a no-op, and
+  // flush_optimizer() applies a pending update before parameters are read back.
+  bool defer_opt_ = false;  // measured slower at B = 1 (9.54 vs 9.35 ms): off by default
+  bool deferred() const { return defer_opt_ && optimizer_ && !forward_only_; }
+  int deferred_updates(RankCtx& r, cudaStream_t st, bool record);
+ public:
+  int flush_optimizer() override;
+ private:
   // The weight gradients of L are final after its single wgrad GEMM: one micro-batch and no
   // data-parallel reduction (TP shards own their weight gradients).
   bool adam_fused(const RankLayer& L) const {
-    return fused_adam_ && optimizer_ && !forward_only_ && m_ == 1 && L.d.dp == 1 && L.d.sdp == 1;
+    return fused_adam_ && optimizer_ && !forward_only_ && !defer_opt_ && m_ == 1 && L.d.dp == 1 &&
+           L.d.sdp == 1;
   }
   bool wg_active_ = false;    // this capture forks (off while profiling)
   bool wg_used_ = false;
@@ -500,6 +518,8 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     fuse_dz_ = cfg.value("fuse_dz", false);
     opt_stream_ = cfg.value("optimizer_stream", 0);
     fused_adam_ = cfg.value("fused_adam", false);
+    defer_opt_ = cfg.value("defer_optimizer", false);
+    if (const char* e = std::getenv("GX_DEFER_OPT")) defer_opt_ = e[0] != '0';
     if (const char* e = std::getenv("GX_FUSED_ADAM")) fused_adam_ = e[0] != '0';
     if (const char* e = std::getenv("GX_OPT_STREAM")) opt_stream_ = std::atoi(e);
     if (const char* e = std::getenv("GX_FUSE_DZ")) fuse_dz_ = e[0] != '0';
@@ -800,6 +820,14 @@ int ExecutorImpl::allocate(RankCtx& r) {
     int64_t max_hdim = 0;
     for (const RankLayer& L : r.layers) max_hdim = std::max<int64_t>(max_hdim, L.sh.h);
     r.ln_ws = A.a<float>(layernorm_bwd_ws_floats(static_cast<int>(max_hdim)));
+    int64_t max_cols = 0;
+    for (const RankLayer& L : r.layers)
+      max_cols = std::max<int64_t>({max_cols, L.sh.h, L.sh.ffn / L.d.tp, 3 * L.sh.h / L.d.tp});
+    for (float*& w : r.cs_ws) {
+      w = A.a<float>(colsum_ws_floats(static_cast<int>(max_cols)));
+      if (w != nullptr)
+        cudaMemset(w, 0, colsum_ws_floats(static_cast<int>(max_cols)) * sizeof(float));
+    }
     if (r.ln_ws != nullptr)
       cudaMemset(r.ln_ws, 0, layernorm_bwd_ws_floats(static_cast<int>(max_hdim)) * sizeof(float));
   }
@@ -810,6 +838,12 @@ int ExecutorImpl::allocate(RankCtx& r) {
   r.loss_ws = A.a<float>(kLossBlocks + 1);
   if (r.loss_ws != nullptr) cudaMemset(r.loss_ws, 0, (kLossBlocks + 1) * sizeof(float));
   r.step = A.a<int64_t>(1);
+  r.opt_pending = A.a<int>(1);
+  if (r.opt_pending != nullptr) cudaMemset(r.opt_pending, 0, sizeof(int));
+  r.opt_done.resize(r.layers.size(), nullptr);
+  for (auto& e : r.opt_done)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return set_error(kErrCuda, "executor: event creation failed");
   r.seed_off = A.a<uint64_t>(1);
   cudaMemset(r.step, 0, 8);
   cudaMemset(r.seed_off, 0, 8);
@@ -846,6 +880,7 @@ int ExecutorImpl::allocate(RankCtx& r) {
 
 // ------------------------------------------------------------------------- parameters
 int ExecutorImpl::set_layer_params(int layer, const float* canonical, int64_t n) {
+  GX_TRY(flush_optimizer());  // a pending update must not land on the new parameters
   if (layer < 0 || layer >= L_) return set_error(kErrConfig, "set_layer_params: bad layer");
   if (n != canonical_size(shape_[layer])) return set_error(kErrConfig, "set_layer_params: size");
   for (auto& r : ranks_) {
@@ -875,6 +910,7 @@ int ExecutorImpl::set_layer_params(int layer, const float* canonical, int64_t n)
 }
 
 int ExecutorImpl::export_layer(int layer, int what, float* canonical, int64_t n) {
+  if (what != 1) GX_TRY(flush_optimizer());  // parameters read back include the last update
   if (layer < 0 || layer >= L_) return set_error(kErrConfig, "export_layer: bad layer");
   if (n != canonical_size(shape_[layer])) return set_error(kErrConfig, "export_layer: size");
   GX_TRY(cuda_check(cudaStreamSynchronize(stream_), "export sync"));
@@ -907,6 +943,8 @@ int ExecutorImpl::export_layer(int layer, int what, float* canonical, int64_t n)
 }
 
 int ExecutorImpl::init_params(uint64_t seed, float std_dev) {
+  for (auto& r : ranks_)  // fresh parameters: drop any pending update
+    if (r->opt_pending != nullptr) GX_TRY(cuda_check(cudaMemset(r->opt_pending, 0, sizeof(int)), "clear pending"));
   for (auto& r : ranks_) {
     for (RankLayer& L : r->layers) {
       InitLayout il{};
@@ -1244,7 +1282,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     }
     d.site = 3ull * l + 2;
     if (!A.dz_ready)
-      GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(dY, dz, G + L.lay.b2.off, rows, h, d, stream_); }));
+      GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(dY, dz, G + L.lay.b2.off, rows, h, d, stream_, r.cs_ws[0]); }));
     const gx_gemm_epilogue w2 = wgrad_ep(L.lay.w2, ft);
     auto wgrad2 = [&] { return on_wgrad([&] { return gemm(dz, h, true, A.gel, ft, true, h, ft, rows, w2); }); };  // dW2 = dz^T gel
     if (!fuse_adam) GX_TRY(wgrad2());  // as early as its inputs exist
@@ -1259,7 +1297,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     if (fuse_adam) GX_TRY(wgrad2());  // after the dgrad that reads W2
     auto wgrad1 = [&] {
       return on_wgrad([&]() -> int {
-        GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dpre, ft, G + L.lay.b1.off, rows, ft, ls_); }));
+        GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dpre, ft, G + L.lay.b1.off, rows, ft, ls_, r.cs_ws[ls_ == stream_ ? 0 : 1]); }));
         const gx_gemm_epilogue w1 = wgrad_ep(L.lay.w1, h);
         return gemm(dpre, ft, true, A.ln2, h, true, ft, h, rows, w1);  // dW1 = dpre^T ln2
       });
@@ -1336,7 +1374,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     }
     auto wgradq = [&] {
       return on_wgrad([&]() -> int {
-        GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, ls_); }));
+        GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, ls_, r.cs_ws[ls_ == stream_ ? 0 : 1]); }));
         const gx_gemm_epilogue wq = wgrad_ep(L.lay.wqkv, h);
         return gemm(dqkv, 3 * ht, true, A.ln1, h, true, 3 * ht, h, rows, wq);  // dWqkv
       });
@@ -1428,7 +1466,7 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
                                DType::kF32, stream_);
     return kOk;
   }
-  if (phase == 2 && optimizer_) {
+  if (phase == 2 && optimizer_ && !deferred()) {
     // with the AdamW-fused weight-gradient epilogues only the LayerNorm / bias prefix is left
     const int64_t n_opt = adam_fused(L) ? L.lay.acc_end : L.shard_n;
     if (profiling_ || opt_stream_ == 2)  // instrumented runs keep everything on one stream
@@ -1462,6 +1500,30 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
     return kOk;
   }
   return kOk;
+}
+
+// AdamW of every layer (forward order) from the gradients of the last completed step (no-op
+// on device when none is pending), each followed by zeroing the layer's accumulated-gradient
+// prefix for the next backward; `record` marks each layer's completion for the forward.
+int ExecutorImpl::deferred_updates(RankCtx& r, cudaStream_t st, bool record) {
+  for (size_t li = 0; li < r.layers.size(); ++li) {
+    RankLayer& L = r.layers[li];
+    const int64_t n_opt = adam_fused(L) ? L.lay.acc_end : L.shard_n;
+    tmark("opt_begin L" + std::to_string(L.layer), st);
+    GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, n_opt, lr_, b1_, b2_, eps_, wd_,
+                     r.step, st, opt_blocks_ > 0 ? opt_blocks_ : 2 * num_sms(), r.opt_pending));
+    GX_TRY(cuda_check(cudaMemsetAsync(L.gfull, 0, L.lay.acc_end * 4, st), "memset grads"));
+    tmark("opt_end L" + std::to_string(L.layer), st);
+    if (record) GX_TRY(cuda_check(cudaEventRecord(r.opt_done[li], st), "opt done"));
+  }
+  return set_flag(r.opt_pending, 0, st);
+}
+
+int ExecutorImpl::flush_optimizer() {
+  if (!deferred() || dry_run_) return kOk;
+  GX_TRY(cuda_check(cudaStreamSynchronize(stream_), "flush sync"));
+  for (auto& r : ranks_) GX_TRY(deferred_updates(*r, stream_, false));
+  return cuda_check(cudaStreamSynchronize(stream_), "flush");
 }
 
 int ExecutorImpl::gather_params(RankCtx& r, int li) {
@@ -1671,10 +1733,16 @@ int ExecutorImpl::step_once() {
   for (auto& r : ranks_) {
     for (RankLayer& L : r->layers)
       for (Acts& a : L.acts) a.ln1_ready = a.dz_ready = false;
-    GX_TRY(bump_step(r->step, nullptr, stream_));
+    if (!deferred()) GX_TRY(bump_step(r->step, nullptr, stream_));
     GX_TRY(cuda_check(cudaMemsetAsync(r->loss, 0, 4, stream_), "memset loss"));
-    for (RankLayer& L : r->layers)
-      GX_TRY(cuda_check(cudaMemsetAsync(L.gfull, 0, L.lay.acc_end * 4, stream_), "memset grads"));
+    if (!deferred())
+      for (RankLayer& L : r->layers)
+        GX_TRY(cuda_check(cudaMemsetAsync(L.gfull, 0, L.lay.acc_end * 4, stream_), "memset grads"));
+  }
+  if (deferred()) {  // last step's AdamW on the side stream, layer by layer (see defer_opt_)
+    GX_TRY(fork(stream_, side_));
+    side_used_ = true;
+    for (auto& r : ranks_) GX_TRY(deferred_updates(*r, side_, true));
   }
   // ---------------------------------------------------------------- forward (GPipe)
   for (int mb = 0; mb < m_; ++mb) {
@@ -1688,6 +1756,9 @@ int ExecutorImpl::step_once() {
       }
       const int nl = static_cast<int>(R[0]->layers.size());
       for (int li = 0; li < nl; ++li) {
+        if (deferred() && mb == 0)  // this layer's parameters carry the last step's update
+          for (RankCtx* r : R)
+            GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, r->opt_done[li], 0), "opt wait"));
         for (RankCtx* r : R) GX_TRY(xin_fwd(*r, li, mb));
         if (mb == 0)
           for (RankCtx* r : R) GX_TRY(gather_params(*r, li));
@@ -1775,6 +1846,11 @@ int ExecutorImpl::step_once() {
     GX_TRY(cuda_check(cudaEventRecord(join_event_, side_), "join record"));
     GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, join_event_, 0), "join wait"));
   }
+  if (deferred())  // this step's gradients are complete: the next step (or a flush) applies them
+    for (auto& r : ranks_) {
+      GX_TRY(bump_step(r->step, nullptr, stream_));
+      GX_TRY(set_flag(r->opt_pending, 1, stream_));
+    }
   tmark("step_end", stream_);
   for (auto& r : ranks_) GX_TRY(comm_->world_sum(r->rank, r->loss, stream_));
   // next step draws fresh dropout masks

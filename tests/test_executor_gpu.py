@@ -139,7 +139,7 @@ def test_fused_adamw_epilogue_matches_standalone_optimizer(cuda):
     outs = []
     for fused in (True, False):
         ex = gxe.PlanExecutor(plan, model, 1, optimizer=True, lr=1e-3, weight_decay=0.01,
-                              fused_adam=fused)
+                              fused_adam=fused, defer_optimizer=False)
         ex.init_params(seed=11, std=0.02)
         rng = np.random.default_rng(3)
         rows = 2 * model["layers"][0]["shape"]["seq"]
@@ -152,3 +152,28 @@ def test_fused_adamw_epilogue_matches_standalone_optimizer(cuda):
         for k, a in outs[0][l].items():
             b = outs[1][l][k]
             assert np.max(np.abs(a - b)) <= 1e-6 * max(1e-3, np.max(np.abs(b))), (l, k)
+
+
+@pytest.mark.parametrize("strategies,world", [(["", "", ""], 1), (["sdp:2", "dp:2", "tp:2"], 2)])
+def test_deferred_optimizer_matches_immediate(cuda, strategies, world):
+    """The default deferred optimizer (step t's AdamW overlapped with step t+1's forward)
+    yields the same per-step losses and final parameters as updating at the end of the step."""
+    plan = gxe.make_plan(strategies, 2 * world)
+    model = _small_model(L=len(strategies))
+    res = []
+    for defer in (True, False):
+        ex = gxe.PlanExecutor(plan, model, world, optimizer=True, lr=1e-3, weight_decay=0.01,
+                              dropout_attn=0.1, dropout_hidden=0.1, defer_optimizer=defer)
+        ex.init_params(seed=21, std=0.02)
+        rng = np.random.default_rng(8)
+        rows = 2 * world * model["layers"][0]["shape"]["seq"]
+        xb = gxe.f32_to_bf16_bits(rng.standard_normal((rows, 256)).astype(np.float32))
+        tb = gxe.f32_to_bf16_bits(rng.standard_normal((rows, 256)).astype(np.float32))
+        losses = [ex.step(xb, tb, use_graph=(i > 0)) for i in range(4)]
+        params = [ex.export_layer(l, "params") for l in range(len(strategies))]
+        res.append((losses, params))
+        ex.close()
+    assert res[0][0] == res[1][0], (res[0][0], res[1][0])
+    for l, (a, b) in enumerate(zip(res[0][1], res[1][1])):
+        for k in a:
+            assert np.array_equal(a[k], b[k]), (l, k)
