@@ -111,6 +111,21 @@ int cast_bf16(const void* src, void* dst, int64_t n, cudaStream_t st);
 int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n,
               float lr, float beta1, float beta2, float eps, float wd, const int64_t* step,
               cudaStream_t st, int max_blocks = 0, const int* pending = nullptr);
+// AdamW over up to 8 (master, grad, m, v, bf16) segments in one launch
+struct AdamSeg {
+  void* p;
+  const void* g;
+  void* m;
+  void* v;
+  void* out;
+  int64_t n;
+};
+struct AdamSegs {
+  AdamSeg seg[8];
+  int n = 0;
+};
+int adamw_multi(const AdamSegs& segs, float lr, float beta1, float beta2, float eps, float wd,
+                const int64_t* step, cudaStream_t st, int blocks);
 // *flag = v (stream-ordered; graph-friendly device flag updates)
 int set_flag(int* flag, int v, cudaStream_t st);
 int bump_step(int64_t* step, uint64_t* seed_offset, cudaStream_t st);

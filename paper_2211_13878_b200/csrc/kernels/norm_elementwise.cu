@@ -864,6 +864,31 @@ int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, 
   return check_launch("adamw_dev_kernel");
 }
 
+// Several layers' updates in one launch (fewer forks / launches on the side stream): every
+// thread walks each segment with the grid stride.
+__global__ void __launch_bounds__(256, 4) adamw_multi_kernel(AdamSegs segs, float lr, float b1,
+                                                              float b2, float eps, float wd,
+                                                              const int64_t* __restrict__ step) {
+  pdl_enter();
+  const AdamScalars c = adam_scalars_step(lr, b1, b2, eps, wd, step);
+  for (int s = 0; s < segs.n; ++s) {
+    const AdamSeg& g = segs.seg[s];
+    adam_range<2>(c, static_cast<float4*>(g.p), static_cast<const float4*>(g.g),
+                  static_cast<float4*>(g.m), static_cast<float4*>(g.v), static_cast<uint2*>(g.out),
+                  g.n / 4);
+  }
+}
+
+int adamw_multi(const AdamSegs& segs, float lr, float beta1, float beta2, float eps, float wd,
+                const int64_t* step, cudaStream_t st, int blocks) {
+  for (int s = 0; s < segs.n; ++s)
+    if (segs.seg[s].n % 4) return set_error(kErrConfig, "adamw: n % 4 != 0");
+  if (segs.n == 0) return kOk;
+  launch_k(adamw_multi_kernel, dim3(blocks), dim3(256), 0, st, segs, lr, beta1, beta2, eps, wd,
+           step);
+  return check_launch("adamw_multi_kernel");
+}
+
 __global__ void set_flag_kernel(int* flag, int v) {
   pdl_enter();
   *flag = v;

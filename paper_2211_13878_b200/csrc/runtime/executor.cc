@@ -191,6 +191,7 @@ struct RankCtx {
   float* loss_ws = nullptr;  // deterministic loss reduction: block partials + ticket
   int* opt_pending = nullptr;  // deferred optimizer: gradients of the last step not applied yet
   std::vector<cudaEvent_t> opt_done;  // deferred optimizer: layer li updated (forward may read)
+  std::vector<int> opt_group;         // side-stream optimizer: layers waiting for a grouped launch
   int64_t* step = nullptr;
   uint64_t* seed_off = nullptr;
   int64_t in_rows_total = 0;
@@ -381,6 +382,7 @@ class ExecutorImpl final : public Executor {
   bool forward_only_ = false;  // profiler / debugging: skip loss, backward and optimizer
   bool splitk_ = true;         // split-K for long-K / small-MN GEMMs (GX_SPLITK=0 disables)
   int opt_blocks_ = 0;         // grid of the side-stream AdamW (GX_OPT_BLOCKS; 0 = 2 per SM)
+  int opt_group_ = 1;          // layers per side-stream AdamW launch (GX_OPT_GROUP, <= 8)
   bool dry_run_ = false;       // topology only: no device state (host-logic tests)
   float inv_count_ = 1.f;
 
@@ -513,6 +515,9 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     splitk_ = cfg.value("splitk", true);
     if (const char* e = std::getenv("GX_SPLITK")) splitk_ = e[0] != '0';
     opt_blocks_ = cfg.value("optimizer_blocks", 0);
+    opt_group_ = cfg.value("optimizer_group", 1);
+    if (const char* e = std::getenv("GX_OPT_GROUP")) opt_group_ = std::atoi(e);
+    opt_group_ = std::max(1, std::min(8, opt_group_));
     wgrad_stream_ = cfg.value("wgrad_stream", true);
     trace_ = cfg.value("trace", false);
     fuse_dz_ = cfg.value("fuse_dz", false);
@@ -1487,6 +1492,11 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
       tmark("opt_end L" + std::to_string(L.layer), wg_);
       return kOk;
     }
+    // Layers are updated in groups of opt_group_ (one fork + one multi-tensor launch); the
+    // stage's first layer (last in backward order) closes the final group.  The streams are
+    // in order, so waiting for the group's last layer covers the earlier ones.
+    r.opt_group.push_back(li);
+    if (static_cast<int>(r.opt_group.size()) < opt_group_ && li > 0) return kOk;
     cudaEvent_t e = fork_events_[fork_used_++];
     GX_TRY(cuda_check(cudaEventRecord(e, stream_), "fork record"));
     GX_TRY(cuda_check(cudaStreamWaitEvent(side_, e, 0), "fork wait"));
@@ -1494,8 +1504,15 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
       GX_TRY(cuda_check(cudaStreamWaitEvent(side_, r.wg_done[par], 0), "fork wait wgrad"));
     side_used_ = true;
     tmark("opt_begin L" + std::to_string(L.layer), side_);
-    GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, n_opt, lr_, b1_, b2_, eps_, wd_,
-                     r.step, side_, opt_blocks_ > 0 ? opt_blocks_ : 2 * num_sms()));
+    AdamSegs segs;
+    for (int lj : r.opt_group) {
+      RankLayer& Lg = r.layers[lj];
+      segs.seg[segs.n++] = AdamSeg{Lg.master, Lg.gshard, Lg.m, Lg.v, Lg.pshard,
+                                   adam_fused(Lg) ? Lg.lay.acc_end : Lg.shard_n};
+    }
+    r.opt_group.clear();
+    GX_TRY(adamw_multi(segs, lr_, b1_, b2_, eps_, wd_, r.step, side_,
+                       opt_blocks_ > 0 ? opt_blocks_ : 2 * num_sms()));
     tmark("opt_end L" + std::to_string(L.layer), side_);
     return kOk;
   }
@@ -1723,7 +1740,10 @@ int ExecutorImpl::step_once() {
   wg_used_ = false;
   wg_active_ = wgrad_stream_ && !profiling_;
   ls_ = stream_;
-  for (auto& r : ranks_) r->wg_pending[0] = r->wg_pending[1] = false;
+  for (auto& r : ranks_) {
+    r->wg_pending[0] = r->wg_pending[1] = false;
+    r->opt_group.clear();
+  }
   auto in_stage = [&](int st) {
     std::vector<RankCtx*> v;
     for (auto& r : ranks_)
