@@ -233,6 +233,7 @@ typedef struct gx_attention_args {
   const uint64_t* seed_offset; /* optional device counter added to seed */
   void* mask;                  /* uint16 keep bits [batch*heads][seq][ceil(seq/64)][4]:
                                   written by fwd, read by bwd (when dropout is on) */
+  unsigned long long* trace;   /* debug: per-CTA %globaltimer stamps (tcgen05 kernels), or NULL */
 } gx_attention_args;
 
 GX_API int gx_k_attention_fwd(const gx_attention_args* args, void* stream);

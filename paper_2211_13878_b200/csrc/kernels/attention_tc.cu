@@ -67,6 +67,17 @@ __device__ __forceinline__ uint32_t p_group_addr(const TcLayout& L, uint32_t bas
   return g < L.p_lo_groups ? base + g * 16384 : base + L.p_hi_off + (g - L.p_lo_groups) * 16384;
 }
 
+__device__ __forceinline__ unsigned long long gtimer_tc() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// debug stamps: slot i of CTA (blockIdx.y * gridDim.x + blockIdx.x), 32 slots per CTA
+#define GX_ATTN_STAMP(p, i)                                                                   \
+  do {                                                                                        \
+    if ((p).trace != nullptr && threadIdx.x == 0)                                             \
+      (p).trace[(blockIdx.y * gridDim.x + blockIdx.x) * 32 + (i)] = gtimer_tc();              \
+  } while (0)
 __device__ __forceinline__ float ex2_ftz(float x) {  // MUFU.EX2, no denormal fix-up
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -84,6 +95,18 @@ __device__ __forceinline__ void st_shared_v4_tc(uint32_t addr, uint32_t a, uint3
                "r"(d)
                : "memory");
 }
+
+// 32 lanes x 16 consecutive 32-bit TMEM columns
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+constexpr int kBwdThreads = 512;  // 16 warps: four per TMEM lane quarter, 32 queries each
 
 }  // namespace
 
@@ -308,7 +331,7 @@ struct BwdLayout {
 };
 }  // namespace
 
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv,
                        const __grid_constant__ CUtensorMap map_do,
                        const __grid_constant__ CUtensorMap map_o, const gx_attention_args p) {
@@ -354,7 +377,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  GX_ATTN_STAMP(p, 0);
   pdl_enter();
+  GX_ATTN_STAMP(p, 1);
 
   auto load_chunk = [&](int j) {  // Q_j, dO_j, O_j -> buffer j & 1
     const int bf = j & 1;
@@ -377,8 +402,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   {  // lse and keep words of every query of the head (once; overlaps the TMA loads)
     const float* lse_g = static_cast<const float*>(p.lse) + static_cast<int64_t>(bh) * s;
     const uint16_t* mask_g = static_cast<const uint16_t*>(p.mask);
-    for (int q = threadIdx.x; q < s; q += kTcThreads) sLse[q] = lse_g[q];
-    for (int i = threadIdx.x; i < 2 * s; i += kTcThreads) {
+    for (int q = threadIdx.x; q < s; q += kBwdThreads) sLse[q] = lse_g[q];
+    for (int i = threadIdx.x; i < 2 * s; i += kBwdThreads) {
       const int q = i >> 1, kb = kt * 2 + (i & 1);
       uint64_t w = 0;
       if (p.drop_threshold != 0u && kb < nkb)
@@ -387,7 +412,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   }
 
-  const int qd = warp & 3, hf = warp >> 2;
+  const int qd = warp & 3, cq = warp >> 2;  // TMEM lane quarter, 32-column quarter
   const int kr = qd * 32 + lane;      // key row of the tile == TMEM lane (S^T, dV, dK)
   const int key = kt * 128 + kr;
   const uint32_t trow = tmem + (static_cast<uint32_t>(qd * 32) << 16);
@@ -419,13 +444,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   auto compute_d = [&](int j) {  // D = rowsum(dO * O) of chunk j's 128 queries -> sD
     const int bf = j & 1;
     mbar_wait(&bar_ld[bf], (j >> 1) & 1);
-    const int qi = threadIdx.x >> 1, hh = threadIdx.x & 1;
+    const int qi = threadIdx.x >> 2, part4 = threadIdx.x & 3;  // 4 threads per query row
     const uint8_t* dob = smem + BL::kDO + bf * 16384 + qi * 128;
     const uint8_t* ob = smem + BL::kO + bf * 16384 + qi * 128;
     float acc = 0.f;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const int cc = hh * 4 + c;
+    for (int c = 0; c < 2; ++c) {
+      const int cc = part4 * 2 + c;
       const int sw = (cc ^ (qi & 7)) << 4;
       const uint4 a = *reinterpret_cast<const uint4*>(dob + sw);
       const uint4 o = *reinterpret_cast<const uint4*>(ob + sw);
@@ -435,7 +460,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         acc += bf16_lo(aw[t]) * bf16_lo(ow[t]) + bf16_hi(aw[t]) * bf16_hi(ow[t]);
     }
     acc += __shfl_xor_sync(0xffffffff, acc, 1);
-    if (hh == 0) sD[qi] = acc;
+    acc += __shfl_xor_sync(0xffffffff, acc, 2);
+    if (part4 == 0) sD[qi] = acc;
   };
   if (threadIdx.x == 0) {
     if (nq > 1) load_chunk(1);
@@ -443,53 +469,62 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     issue_s(0);
   }
   compute_d(0);
-  named_sync(1, kTcThreads);
+  named_sync(1, kBwdThreads);
+  GX_ATTN_STAMP(p, 2);
 
   for (int j = 0; j < nq; ++j) {
     const int bf = j & 1;
     mbar_wait(bar_s, j & 1);
     tc_fence_after();
-    // P, Pd, dS for key row kr x queries [hf*64, hf*64 + 64)
-#pragma unroll 1
-    for (int sc = 0; sc < 2; ++sc) {
-      const int c0 = hf * 64 + sc * 32;
+    GX_ATTN_STAMP(p, 4 + 5 * j);
+    // P, Pd, dS for key row kr x queries [cq*32, cq*32 + 32) of the chunk
+    {
+      const int c0 = cq * 32;
+      const int qg0 = j * kTcQ + c0;
+      const bool full = qg0 + 32 <= s && kt * 128 + 128 <= s;  // no tail masking needed
       uint32_t sv[32], dv[32];
       tmem_ld32(trow + c0, sv);
       tmem_ld32(trow + 128 + c0, dv);
       tmem_ld_wait();
-      float pd[32], ds[32];
+      uint32_t ppd[16], pds[16];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int qi = c0 + i;
-        const int qg = j * kTcQ + qi;
-        const bool valid = (qg < s) && (key < s);
-        const float pr = valid ? ex2_ftz(__uint_as_float(sv[i]) * c2 - sLse[qg]) : 0.f;
-        float dp = __uint_as_float(dv[i]);
-        float pdv = pr;
-        if (thr != 0u) {
-          const bool keep = valid && ((sMask[(qg * 2 + kbl) * 4 + mt] >> mbit) & 1u) != 0u;
-          pdv = keep ? pr * inv_keep : 0.f;
-          dp = keep ? dp * inv_keep : 0.f;
+      for (int i4 = 0; i4 < 8; ++i4) {
+        const float4 l4 = *reinterpret_cast<const float4*>(sLse + qg0 + 4 * i4);
+        const float4 d4 = *reinterpret_cast<const float4*>(sD + c0 + 4 * i4);
+        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dd[4] = {d4.x, d4.y, d4.z, d4.w};
+        float pd4[4], ds4[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int i = 4 * i4 + t;
+          const int qg = qg0 + i;
+          const bool valid = full || ((qg < s) && (key < s));
+          const float pr = valid ? ex2_ftz(__uint_as_float(sv[i]) * c2 - lv[t]) : 0.f;
+          float f = 1.f;  // dropout factor: inv_keep or 0
+          if (thr != 0u)
+            f = valid && ((sMask[(qg * 2 + kbl) * 4 + mt] >> mbit) & 1u) != 0u ? inv_keep : 0.f;
+          pd4[t] = pr * f;
+          ds4[t] = pr * (__uint_as_float(dv[i]) * f - dd[t]);
         }
-        pd[i] = pdv;
-        ds[i] = pr * (dp - sD[qi]);
+        ppd[2 * i4] = pack_bf16(pd4[0], pd4[1]);
+        ppd[2 * i4 + 1] = pack_bf16(pd4[2], pd4[3]);
+        pds[2 * i4] = pack_bf16(ds4[0], ds4[1]);
+        pds[2 * i4 + 1] = pack_bf16(ds4[2], ds4[3]);
       }
-      const uint32_t rowoff = static_cast<uint32_t>(hf * 16384 + kr * 128);
-      const int chunk0 = (c0 & 63) >> 3;
+      const uint32_t rowoff = static_cast<uint32_t>((cq >> 1) * 16384 + kr * 128);
+      const int chunk0 = (cq & 1) * 4;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint32_t sw = static_cast<uint32_t>((chunk0 + i) ^ (kr & 7)) << 4;
-        st_shared_v4_tc(sb + BL::kPd + rowoff + sw, pack_bf16(pd[8 * i], pd[8 * i + 1]),
-                        pack_bf16(pd[8 * i + 2], pd[8 * i + 3]), pack_bf16(pd[8 * i + 4], pd[8 * i + 5]),
-                        pack_bf16(pd[8 * i + 6], pd[8 * i + 7]));
-        st_shared_v4_tc(sb + BL::kDS + rowoff + sw, pack_bf16(ds[8 * i], ds[8 * i + 1]),
-                        pack_bf16(ds[8 * i + 2], ds[8 * i + 3]), pack_bf16(ds[8 * i + 4], ds[8 * i + 5]),
-                        pack_bf16(ds[8 * i + 6], ds[8 * i + 7]));
+        st_shared_v4_tc(sb + BL::kPd + rowoff + sw, ppd[4 * i], ppd[4 * i + 1], ppd[4 * i + 2],
+                        ppd[4 * i + 3]);
+        st_shared_v4_tc(sb + BL::kDS + rowoff + sw, pds[4 * i], pds[4 * i + 1], pds[4 * i + 2],
+                        pds[4 * i + 3]);
       }
     }
     fence_proxy_async_smem_tc();
     tc_fence_before();
-    named_sync(1, kTcThreads);
+    named_sync(1, kBwdThreads);
+    GX_ATTN_STAMP(p, 5 + 5 * j);
     if (threadIdx.x == 0) {
       tc_fence_after();
       const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
@@ -508,42 +543,45 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // the next chunk's scores queue behind (S / dPd columns were consumed above)
       if (j + 1 < nq) issue_s(j + 1);
     }
+    GX_ATTN_STAMP(p, 6 + 5 * j);
     if (j + 1 < nq) compute_d(j + 1);  // sD of chunk j was last read before the barrier
     mbar_wait(bar_mm, j & 1);
     tc_fence_after();
-    {  // dQ_j partial (fp32): TMEM lane = query row of the chunk
-      uint32_t o[32];
-      tmem_ld32(trow + 384 + hf * 32, o);
+    GX_ATTN_STAMP(p, 7 + 5 * j);
+    {  // dQ_j partial (fp32): TMEM lane = query row of the chunk, 16 columns per warp
+      uint32_t o[16];
+      tmem_ld16(trow + 384 + cq * 16, o);
       tmem_ld_wait();
       const int q = j * kTcQ + kr;
       if (q < s) {
         float4* dst = reinterpret_cast<float4*>(
-            part + ((static_cast<int64_t>(kt) * gridDim.y + bh) * s + q) * kTcHD + hf * 32);
+            part + ((static_cast<int64_t>(kt) * gridDim.y + bh) * s + q) * kTcHD + cq * 16);
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < 4; ++i)
           dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
                                __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
       }
     }
     // chunk j's buffer is free once its MMAs are done: prefetch chunk j + 2 into it
     if (threadIdx.x == 0 && j + 2 < nq) load_chunk(j + 2);
+    GX_ATTN_STAMP(p, 8 + 5 * j);
     tc_fence_before();
-    named_sync(1, kTcThreads);  // TMEM dQ / S columns and the chunk buffer are free again
+    named_sync(1, kBwdThreads);  // TMEM dQ / S columns and the chunk buffer are free again
   }
   // dK (x scale), dV -> bf16 rows of dqkv
   {
-    uint32_t dvv[32], dkv[32];
-    tmem_ld32(trow + 256 + hf * 32, dvv);
-    tmem_ld32(trow + 320 + hf * 32, dkv);
+    uint32_t dvv[16], dkv[16];
+    tmem_ld16(trow + 256 + cq * 16, dvv);
+    tmem_ld16(trow + 320 + cq * 16, dkv);
     tmem_ld_wait();
     if (key < s) {
       auto* dq = static_cast<__nv_bfloat16*>(p.dqkv);
       __nv_bfloat16* rowp = dq + (static_cast<int64_t>(row0) + key) * p.ld_qkv;
-      uint4* dvp = reinterpret_cast<uint4*>(rowp + (2 * H + h) * kTcHD + hf * 32);
-      uint4* dkp = reinterpret_cast<uint4*>(rowp + (H + h) * kTcHD + hf * 32);
+      uint4* dvp = reinterpret_cast<uint4*>(rowp + (2 * H + h) * kTcHD + cq * 16);
+      uint4* dkp = reinterpret_cast<uint4*>(rowp + (H + h) * kTcHD + cq * 16);
       const float sc = p.scale;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 2; ++i) {
         dvp[i] = make_uint4(pack_bf16(__uint_as_float(dvv[8 * i]), __uint_as_float(dvv[8 * i + 1])),
                             pack_bf16(__uint_as_float(dvv[8 * i + 2]), __uint_as_float(dvv[8 * i + 3])),
                             pack_bf16(__uint_as_float(dvv[8 * i + 4]), __uint_as_float(dvv[8 * i + 5])),
@@ -558,14 +596,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   tc_fence_before();
   // every key tile's dQ partials are in global memory after the cluster barrier; CTA kt then
   // owns query chunk kt and sums its partials in key-tile order
+  GX_ATTN_STAMP(p, 25);
   __threadfence();
   cluster_sync();
+  GX_ATTN_STAMP(p, 26);
   {
     auto* dq = static_cast<__nv_bfloat16*>(p.dqkv);
     const float sc = p.scale;
     const int q_lo = kt * kTcQ, q_hi = min(s, q_lo + kTcQ);
 #pragma unroll 4
-    for (int idx = threadIdx.x; idx < (q_hi - q_lo) * (kTcHD / 8); idx += kTcThreads) {
+    for (int idx = threadIdx.x; idx < (q_hi - q_lo) * (kTcHD / 8); idx += kBwdThreads) {
       const int q = q_lo + idx / (kTcHD / 8), c8 = idx % (kTcHD / 8);
       float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int t = 0; t < nkt; ++t) {
@@ -580,6 +620,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                      pack_bf16(a[4] * sc, a[5] * sc), pack_bf16(a[6] * sc, a[7] * sc));
     }
   }
+  GX_ATTN_STAMP(p, 27);
   __syncthreads();
   if (warp == 0) {
     tc_fence_after();
@@ -677,7 +718,7 @@ int attention_bwd_tc(const gx_attention_args& a, cudaStream_t st) {
   }
   dim3 grid((a.seq + 127) / 128, a.batch * a.heads);
   // the key tiles of one head form a cluster (dQ reduction after a cluster barrier)
-  launch_k_cluster(attn_bwd_tc_kernel, grid, dim3(kTcThreads), BwdLayout::kBytes + 1024, st,
+  launch_k_cluster(attn_bwd_tc_kernel, grid, dim3(kBwdThreads), BwdLayout::kBytes + 1024, st,
                    static_cast<unsigned>(grid.x), mq, md, mo, a);
   return check_launch("attn_bwd_tc_kernel");
 }

@@ -100,7 +100,8 @@ class _AttnArgs(ctypes.Structure):
                 ("dq_accum", ctypes.c_void_p), ("dsum", ctypes.c_void_p),
                 ("drop_threshold", ctypes.c_uint32), ("drop_scale", ctypes.c_float),
                 ("seed", ctypes.c_uint64), ("site", ctypes.c_uint64),
-                ("seed_offset", ctypes.c_void_p), ("mask", ctypes.c_void_p)]
+                ("seed_offset", ctypes.c_void_p), ("mask", ctypes.c_void_p),
+                ("trace", ctypes.c_void_p)]
 
 
 class Dropout(ctypes.Structure):
@@ -152,7 +153,7 @@ def attention_fwd(qkv, batch, seq, heads, head_dim, p=0.0, seed=0, site=0, mask=
 
 
 def attention_bwd(qkv, ctx, lse, dctx, batch, seq, heads, head_dim, p=0.0, seed=0, site=0,
-                  mask=None, **kw):
+                  mask=None, trace=None, **kw):
     import torch
     dqkv = torch.zeros_like(qkv)
     # fp32 dQ partials (one slice per 128-key tile on the tcgen05 path) and D / ticket words
@@ -164,6 +165,7 @@ def attention_bwd(qkv, ctx, lse, dctx, batch, seq, heads, head_dim, p=0.0, seed=
     a.ctx, a.ld_ctx, a.lse = _ptr(ctx), ctx.stride(0), _ptr(lse)
     a.dctx, a.dqkv, a.dq_accum, a.dsum = _ptr(dctx), _ptr(dqkv), _ptr(dq_acc), _ptr(dsum)
     a.mask = _ptr(mask)
+    a.trace = _ptr(trace)
     _lib.check(_lib.lib().gx_k_attention_bwd(ctypes.addressof(a), _lib.stream_ptr()))
     return dqkv
 

@@ -1,2 +1,4 @@
-timeout 600 python -m pytest tests/test_executor_gpu.py -x -q 2>&1 | tail -2
-for g in 1 2 4 8; do GX_OPT_GROUP=$g timeout 200 python scripts/step_variants.py default | sed "s/^/group$g /"; done
+timeout 300 python -m pytest tests/test_kernels_gpu.py -x -q 2>&1 | tail -1
+timeout 200 python scripts/attn_trace.py
+timeout 300 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+timeout 200 python scripts/step_variants.py default no_optimizer
