@@ -151,31 +151,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   pdl_enter();
 
   // ---------------------------------------------------------------- loads + S = Q K^T
-  if (threadIdx.x == 0) {
-    const int row0 = b * s;  // first token row of this sample
-    const int slot_q = h, slot_k = H + h, slot_v = 2 * H + h;
-    // 64-row boxes (128 B rows, 128B swizzle): Q 2 boxes, K and V nk/64 boxes each
-    mbar_expect_tx(bar_qk, (kTcQ + nk) * 128);
-    tma_load_3d(smem, &map_qkv, bar_qk, 0, slot_q, row0 + q0);
-    tma_load_3d(smem + 64 * 128, &map_qkv, bar_qk, 0, slot_q, row0 + q0 + 64);
-    for (int r = 0; r < nk; r += 64)
-      tma_load_3d(smem + kTcQ * 128 + r * 128, &map_qkv, bar_qk, 0, slot_k, row0 + r);
-    mbar_expect_tx(bar_v, nk * 128);
-    for (int r = 0; r < nk; r += 64)
-      tma_load_3d(smem + L.v_off + r * 128, &map_qkv, bar_v, 0, slot_v, row0 + r);
-    mbar_wait(bar_qk, 0);
-    tc_fence_after();
-    for (int n0 = 0; n0 < nk; n0 += 256) {
-      const int n = nk - n0 < 256 ? nk - n0 : 256;
-      const uint32_t idesc = idesc_bf16_f32(kTcQ, n, false, false);
+  if (warp == 0) {  // warp-uniform: lane 0 issues, the rest wait here
+    if (lane == 0) {
+      const int row0 = b * s;  // first token row of this sample
+      const int slot_q = h, slot_k = H + h, slot_v = 2 * H + h;
+      // 64-row boxes (128 B rows, 128B swizzle): Q 2 boxes, K and V nk/64 boxes each
+      mbar_expect_tx(bar_qk, (kTcQ + nk) * 128);
+      tma_load_3d(smem, &map_qkv, bar_qk, 0, slot_q, row0 + q0);
+      tma_load_3d(smem + 64 * 128, &map_qkv, bar_qk, 0, slot_q, row0 + q0 + 64);
+      for (int r = 0; r < nk; r += 64)
+        tma_load_3d(smem + kTcQ * 128 + r * 128, &map_qkv, bar_qk, 0, slot_k, row0 + r);
+      mbar_expect_tx(bar_v, nk * 128);
+      for (int r = 0; r < nk; r += 64)
+        tma_load_3d(smem + L.v_off + r * 128, &map_qkv, bar_v, 0, slot_v, row0 + r);
+      mbar_wait(bar_qk, 0);
+      tc_fence_after();
+      for (int n0 = 0; n0 < nk; n0 += 256) {
+        const int n = nk - n0 < 256 ? nk - n0 : 256;
+        const uint32_t idesc = idesc_bf16_f32(kTcQ, n, false, false);
 #pragma unroll
-      for (int k = 0; k < kTcHD / 16; ++k) {
-        const uint64_t ad = sdesc_sw128(sbase + k * 32, 16, 1024);
-        const uint64_t bd = sdesc_sw128(sbase + kTcQ * 128 + n0 * 128 + k * 32, 16, 1024);
-        umma_bf16(tmem + n0, ad, bd, idesc, k != 0 ? 1u : 0u);
+        for (int k = 0; k < kTcHD / 16; ++k) {
+          const uint64_t ad = sdesc_sw128(sbase + k * 32, 16, 1024);
+          const uint64_t bd = sdesc_sw128(sbase + kTcQ * 128 + n0 * 128 + k * 32, 16, 1024);
+          umma_bf16(tmem + n0, ad, bd, idesc, k != 0 ? 1u : 0u);
+        }
       }
+      umma_commit(bar_s);
     }
-    umma_commit(bar_s);
+    __syncwarp();
   }
 
   // ---------------------------------------------------------------- softmax over TMEM rows
@@ -267,16 +270,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const float l = red[2 * kTcQ + r] + red[3 * kTcQ + r];
 
   // ---------------------------------------------------------------- O = P V
-  if (threadIdx.x == 0) {
-    tc_fence_after();
-    mbar_wait(bar_v, 0);
-    const uint32_t idesc = idesc_bf16_f32(kTcQ, kTcHD, false, true);
-    for (int kk = 0; kk < nk / 16; ++kk) {
-      const uint64_t ad = sdesc_sw128(p_group_addr(L, sbase, kk >> 2) + (kk & 3) * 32, 16, 1024);
-      const uint64_t bd = sdesc_sw128(sbase + L.v_off + kk * 2048, nk * 128, 1024);
-      umma_bf16(tmem, ad, bd, idesc, kk != 0 ? 1u : 0u);
+  if (warp == 0) {  // warp-uniform: lane 0 issues, the rest wait here
+    if (lane == 0) {
+      tc_fence_after();
+      mbar_wait(bar_v, 0);
+      const uint32_t idesc = idesc_bf16_f32(kTcQ, kTcHD, false, true);
+      for (int kk = 0; kk < nk / 16; ++kk) {
+        const uint64_t ad = sdesc_sw128(p_group_addr(L, sbase, kk >> 2) + (kk & 3) * 32, 16, 1024);
+        const uint64_t bd = sdesc_sw128(sbase + L.v_off + kk * 2048, nk * 128, 1024);
+        umma_bf16(tmem, ad, bd, idesc, kk != 0 ? 1u : 0u);
+      }
+      umma_commit(bar_o);
     }
-    umma_commit(bar_o);
+    __syncwarp();
   }
   if (hf == 0 && row_ok) {
     auto* lse = static_cast<float*>(p.lse);
@@ -324,7 +330,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 // spread over the cluster.
 namespace {
 struct BwdLayout {
-  static constexpr int kK = 0, kV = 16384, kQ = 32768, kDO = 65536, kO = 98304, kPd = 131072,
+  // Q and dO stream through three 16 KB buffers each (chunk j in buffer j % 3)
+  static constexpr int kK = 0, kV = 16384, kQ = 32768, kDO = 81920, kPd = 131072,
                        kDS = 163840, kLse = 196608 /* [512] */, kD = kLse + 2048 /* [128] */,
                        kMask = kD + 512 /* [512 q][2 kb][4] u16 */, kBar = kMask + 8192,
                        kBytes = kBar + 128;
@@ -345,10 +352,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   float* sD = reinterpret_cast<float*>(smem + BL::kD);
   uint16_t* sMask = reinterpret_cast<uint16_t*>(smem + BL::kMask);  // [512 q][2 kb][4]
   uint64_t* bar_kv = reinterpret_cast<uint64_t*>(smem + BL::kBar);
-  uint64_t* bar_ld = bar_kv + 1;  // [2]
-  uint64_t* bar_s = bar_kv + 3;
-  uint64_t* bar_mm = bar_kv + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_kv + 5);
+  uint64_t* bar_ld = bar_kv + 1;  // [3]
+  uint64_t* bar_s = bar_kv + 4;
+  uint64_t* bar_mm = bar_kv + 5;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_kv + 6);
 
   const int warp = static_cast<int>(warp_id());
   const int lane = static_cast<int>(lane_id());
@@ -368,6 +375,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(bar_kv, 1);
     mbar_init(&bar_ld[0], 1);
     mbar_init(&bar_ld[1], 1);
+    mbar_init(&bar_ld[2], 1);
     mbar_init(bar_s, 1);
     mbar_init(bar_mm, 1);
     fence_barrier_init();
@@ -381,23 +389,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   pdl_enter();
   GX_ATTN_STAMP(p, 1);
 
-  auto load_chunk = [&](int j) {  // Q_j, dO_j, O_j -> buffer j & 1
-    const int bf = j & 1;
+  auto load_chunk = [&](int j) {  // Q_j, dO_j -> buffer j % 3
+    const int bf = j % 3;
     const int r = row0 + j * kTcQ;
-    mbar_expect_tx(&bar_ld[bf], 3 * kTcQ * 128);
+    mbar_expect_tx(&bar_ld[bf], 2 * kTcQ * 128);
     for (int x = 0; x < 2; ++x) {
       tma_load_3d(smem + BL::kQ + bf * 16384 + x * 8192, &map_qkv, &bar_ld[bf], 0, h, r + 64 * x);
       tma_load_3d(smem + BL::kDO + bf * 16384 + x * 8192, &map_do, &bar_ld[bf], 0, h, r + 64 * x);
-      tma_load_3d(smem + BL::kO + bf * 16384 + x * 8192, &map_o, &bar_ld[bf], 0, h, r + 64 * x);
     }
   };
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(bar_kv, 2 * kTcQ * 128);
-    for (int x = 0; x < 2; ++x) {
-      tma_load_3d(smem + BL::kK + x * 8192, &map_qkv, bar_kv, 0, H + h, row0 + kt * 128 + 64 * x);
-      tma_load_3d(smem + BL::kV + x * 8192, &map_qkv, bar_kv, 0, 2 * H + h, row0 + kt * 128 + 64 * x);
+  if (warp == 0) {  // warp-uniform: lane 0 issues, the rest wait here
+    if (lane == 0) {
+      mbar_expect_tx(bar_kv, 2 * kTcQ * 128);
+      for (int x = 0; x < 2; ++x) {
+        tma_load_3d(smem + BL::kK + x * 8192, &map_qkv, bar_kv, 0, H + h, row0 + kt * 128 + 64 * x);
+        tma_load_3d(smem + BL::kV + x * 8192, &map_qkv, bar_kv, 0, 2 * H + h, row0 + kt * 128 + 64 * x);
+      }
+      load_chunk(0);
     }
-    load_chunk(0);
+    __syncwarp();
   }
   {  // lse and keep words of every query of the head (once; overlaps the TMA loads)
     const float* lse_g = static_cast<const float*>(p.lse) + static_cast<int64_t>(bh) * s;
@@ -426,10 +436,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint32_t idesc_kv = idesc_bf16_f32(128, kTcHD, false, true);
   const uint32_t idesc_q = idesc_bf16_f32(kTcQ, kTcHD, true, true);
 
-  // S^T / dPd^T MMAs of chunk j (thread 0) and D of chunk j (all threads)
+  // S^T / dPd^T MMAs of chunk j (thread 0)
   auto issue_s = [&](int j) {
-    const int bf = j & 1;
-    mbar_wait(&bar_ld[bf], (j >> 1) & 1);
+    const int bf = j % 3;
+    mbar_wait(&bar_ld[bf], (j / 3) & 1);
     tc_fence_after();
     const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
 #pragma unroll
@@ -441,52 +451,95 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     umma_commit(bar_s);
   };
-  auto compute_d = [&](int j) {  // D = rowsum(dO * O) of chunk j's 128 queries -> sD
-    const int bf = j & 1;
-    mbar_wait(&bar_ld[bf], (j >> 1) & 1);
+  // dV += Pd^T dO_j, dK += dS^T Q_j, dQ_j = dS K (thread 0)
+  auto issue_grads = [&](int j) {
+    const int bf = j % 3;
+    const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
+#pragma unroll
+    for (int k = 0; k < kTcQ / 16; ++k) {  // K = 128 queries (dV, dK) / 128 keys (dQ)
+      const uint32_t a_kmaj = (k >> 2) * 16384 + (k & 3) * 32;
+      const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
+      umma_bf16(tmem + 256, sdesc_sw128(sb + BL::kPd + a_kmaj, 16, 1024),
+                sdesc_sw128(do_b + k * 2048, 16384, 1024), idesc_kv, acc);
+      umma_bf16(tmem + 320, sdesc_sw128(sb + BL::kDS + a_kmaj, 16, 1024),
+                sdesc_sw128(q_b + k * 2048, 16384, 1024), idesc_kv, acc);
+      umma_bf16(tmem + 384, sdesc_sw128(sb + BL::kDS + k * 2048, 16384, 1024),
+                sdesc_sw128(sb + BL::kK + k * 2048, 16384, 1024), idesc_q, k > 0 ? 1u : 0u);
+    }
+    umma_commit(bar_mm);
+  };
+  // D = rowsum(dO * O) of chunk j's 128 queries -> sD (dO from smem, O from global)
+  auto compute_d = [&](int j) {
+    const int bf = j % 3;
+    mbar_wait(&bar_ld[bf], (j / 3) & 1);
     const int qi = threadIdx.x >> 2, part4 = threadIdx.x & 3;  // 4 threads per query row
+    const int q = j * kTcQ + qi;
     const uint8_t* dob = smem + BL::kDO + bf * 16384 + qi * 128;
-    const uint8_t* ob = smem + BL::kO + bf * 16384 + qi * 128;
     float acc = 0.f;
+    if (q < s) {
+      const uint4* og = reinterpret_cast<const uint4*>(
+          static_cast<const __nv_bfloat16*>(p.ctx) + (static_cast<int64_t>(row0) + q) * p.ld_ctx +
+          h * kTcHD + part4 * 16);
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int cc = part4 * 2 + c;
-      const int sw = (cc ^ (qi & 7)) << 4;
-      const uint4 a = *reinterpret_cast<const uint4*>(dob + sw);
-      const uint4 o = *reinterpret_cast<const uint4*>(ob + sw);
-      const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, ow[4] = {o.x, o.y, o.z, o.w};
+      for (int c = 0; c < 2; ++c) {
+        const int cc = part4 * 2 + c;
+        const int sw = (cc ^ (qi & 7)) << 4;
+        const uint4 a = *reinterpret_cast<const uint4*>(dob + sw);
+        const uint4 o = og[c];
+        const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, ow[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
-        acc += bf16_lo(aw[t]) * bf16_lo(ow[t]) + bf16_hi(aw[t]) * bf16_hi(ow[t]);
+        for (int t = 0; t < 4; ++t)
+          acc += bf16_lo(aw[t]) * bf16_lo(ow[t]) + bf16_hi(aw[t]) * bf16_hi(ow[t]);
+      }
     }
     acc += __shfl_xor_sync(0xffffffff, acc, 1);
     acc += __shfl_xor_sync(0xffffffff, acc, 2);
     if (part4 == 0) sD[qi] = acc;
   };
-  if (threadIdx.x == 0) {
-    if (nq > 1) load_chunk(1);
-    mbar_wait(bar_kv, 0);
-    issue_s(0);
+  // dQ_j partial (fp32) out of TMEM (lane = query row of the chunk, 16 columns per warp)
+  auto store_dq = [&](int j) {
+    uint32_t o[16];
+    tmem_ld16(trow + 384 + cq * 16, o);
+    tmem_ld_wait();
+    const int q = j * kTcQ + kr;
+    if (q < s) {
+      float4* dst = reinterpret_cast<float4*>(
+          part + ((static_cast<int64_t>(kt) * gridDim.y + bh) * s + q) * kTcHD + cq * 16);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
+                             __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
+    }
+  };
+  if (warp == 0) {  // warp-uniform: lane 0 issues, the rest wait here
+    if (lane == 0) {
+      if (nq > 1) load_chunk(1);
+      if (nq > 2) load_chunk(2);
+      mbar_wait(bar_kv, 0);
+      issue_s(0);
+    }
+    __syncwarp();
   }
   compute_d(0);
   named_sync(1, kBwdThreads);
   GX_ATTN_STAMP(p, 2);
 
+  // Pipeline per chunk j: scores S(j) were issued one step earlier; the softmax math of j
+  // runs while the tensor core still does dV / dK / dQ of j-1, whose completion is awaited
+  // only right before Pd / dS(j) overwrite the smem those MMAs read.
   for (int j = 0; j < nq; ++j) {
-    const int bf = j & 1;
     mbar_wait(bar_s, j & 1);
     tc_fence_after();
     GX_ATTN_STAMP(p, 4 + 5 * j);
-    // P, Pd, dS for key row kr x queries [cq*32, cq*32 + 32) of the chunk
+    const int c0 = cq * 32;
+    const int qg0 = j * kTcQ + c0;
+    uint32_t ppd[16], pds[16];
     {
-      const int c0 = cq * 32;
-      const int qg0 = j * kTcQ + c0;
       const bool full = qg0 + 32 <= s && kt * 128 + 128 <= s;  // no tail masking needed
       uint32_t sv[32], dv[32];
       tmem_ld32(trow + c0, sv);
       tmem_ld32(trow + 128 + c0, dv);
       tmem_ld_wait();
-      uint32_t ppd[16], pds[16];
 #pragma unroll
       for (int i4 = 0; i4 < 8; ++i4) {
         const float4 l4 = *reinterpret_cast<const float4*>(sLse + qg0 + 4 * i4);
@@ -510,6 +563,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         pds[2 * i4] = pack_bf16(ds4[0], ds4[1]);
         pds[2 * i4 + 1] = pack_bf16(ds4[2], ds4[3]);
       }
+    }
+    GX_ATTN_STAMP(p, 5 + 5 * j);
+    if (j > 0) {  // chunk j-1's gradient MMAs: done reading Pd / dS; its dQ leaves TMEM
+      mbar_wait(bar_mm, (j - 1) & 1);
+      tc_fence_after();
+      store_dq(j - 1);
+      // chunk j-1's buffer is free: prefetch chunk j + 2 into it (chunks 0-2 came with the
+      // prologue)
+      if (warp == 0) {
+        if (lane == 0 && j + 2 < nq && j + 2 > 2) load_chunk(j + 2);
+        __syncwarp();
+      }
+    }
+    GX_ATTN_STAMP(p, 6 + 5 * j);
+    {
       const uint32_t rowoff = static_cast<uint32_t>((cq >> 1) * 16384 + kr * 128);
       const int chunk0 = (cq & 1) * 4;
 #pragma unroll
@@ -523,51 +591,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     fence_proxy_async_smem_tc();
     tc_fence_before();
-    named_sync(1, kBwdThreads);
-    GX_ATTN_STAMP(p, 5 + 5 * j);
-    if (threadIdx.x == 0) {
-      tc_fence_after();
-      const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
-#pragma unroll
-      for (int k = 0; k < kTcQ / 16; ++k) {  // K = 128 queries (dV, dK) / 128 keys (dQ)
-        const uint32_t a_kmaj = (k >> 2) * 16384 + (k & 3) * 32;
-        const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
-        umma_bf16(tmem + 256, sdesc_sw128(sb + BL::kPd + a_kmaj, 16, 1024),
-                  sdesc_sw128(do_b + k * 2048, 16384, 1024), idesc_kv, acc);
-        umma_bf16(tmem + 320, sdesc_sw128(sb + BL::kDS + a_kmaj, 16, 1024),
-                  sdesc_sw128(q_b + k * 2048, 16384, 1024), idesc_kv, acc);
-        umma_bf16(tmem + 384, sdesc_sw128(sb + BL::kDS + k * 2048, 16384, 1024),
-                  sdesc_sw128(sb + BL::kK + k * 2048, 16384, 1024), idesc_q, k > 0 ? 1u : 0u);
+    named_sync(1, kBwdThreads);  // Pd / dS(j) complete; S / dPd and dQ TMEM columns free
+    if (warp == 0) {  // warp-uniform: lane 0 issues, the rest wait here
+      if (lane == 0) {
+        tc_fence_after();
+        if (j + 1 < nq) issue_s(j + 1);  // scores of the next chunk first ...
+        issue_grads(j);                   // ... then this chunk's gradient products
       }
-      umma_commit(bar_mm);
-      // the next chunk's scores queue behind (S / dPd columns were consumed above)
-      if (j + 1 < nq) issue_s(j + 1);
+      __syncwarp();
     }
-    GX_ATTN_STAMP(p, 6 + 5 * j);
-    if (j + 1 < nq) compute_d(j + 1);  // sD of chunk j was last read before the barrier
-    mbar_wait(bar_mm, j & 1);
-    tc_fence_after();
     GX_ATTN_STAMP(p, 7 + 5 * j);
-    {  // dQ_j partial (fp32): TMEM lane = query row of the chunk, 16 columns per warp
-      uint32_t o[16];
-      tmem_ld16(trow + 384 + cq * 16, o);
-      tmem_ld_wait();
-      const int q = j * kTcQ + kr;
-      if (q < s) {
-        float4* dst = reinterpret_cast<float4*>(
-            part + ((static_cast<int64_t>(kt) * gridDim.y + bh) * s + q) * kTcHD + cq * 16);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
-                               __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
-      }
-    }
-    // chunk j's buffer is free once its MMAs are done: prefetch chunk j + 2 into it
-    if (threadIdx.x == 0 && j + 2 < nq) load_chunk(j + 2);
+    if (j + 1 < nq) compute_d(j + 1);  // sD(j) was last read before the barrier above
     GX_ATTN_STAMP(p, 8 + 5 * j);
-    tc_fence_before();
-    named_sync(1, kBwdThreads);  // TMEM dQ / S columns and the chunk buffer are free again
+    named_sync(1, kBwdThreads);        // sD(j+1) visible
   }
+  mbar_wait(bar_mm, (nq - 1) & 1);
+  tc_fence_after();
+  store_dq(nq - 1);
   // dK (x scale), dV -> bf16 rows of dqkv
   {
     uint32_t dvv[16], dkv[16];
