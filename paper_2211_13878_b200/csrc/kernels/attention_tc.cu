@@ -8,7 +8,7 @@
 //   1. one thread issues TMA loads of Q [128 x 64], K and V [NK x 64] (NK = seq rounded up to
 //      64; rows past the sample read as finite neighbours or zero fill and are masked) into
 //      128B-swizzled smem, then tcgen05.mma S = Q K^T into TMEM columns [0, NK) (fp32);
-//   2. eight warps (two per TMEM lane quarter, each half the key columns) read S back with
+//   2. sixteen warps (four per TMEM lane quarter, 64-key blocks round-robin) read S back with
 //      tcgen05.ld: pass 1 row max, pass 2 exp2, row sum, Philox dropout, bf16 P written into
 //      smem in the UMMA K-major SWIZZLE_128B layout (over the dead Q/K tiles), keep bits to
 //      global for the backward;
@@ -34,7 +34,6 @@ namespace {
 constexpr int kTcQ = 128;       // queries per CTA (UMMA M)
 constexpr int kTcHD = 64;       // head dim (one 128 B swizzle row)
 constexpr int kTcMaxKeys = 512; // TMEM columns
-constexpr int kTcThreads = 256;
 
 struct TcLayout {
   int nk;          // keys rounded up to 64
@@ -42,7 +41,7 @@ struct TcLayout {
   int v_off;       // V tile
   int p_hi_off;    // P groups that do not fit over Q + K
   int p_lo_groups; // P groups placed at [0, qk_bytes)
-  int red_off;     // row max / row sum exchange [2][2][128] floats
+  int red_off;     // row max / row sum exchange [2][4][128] floats
   int bar_off;
   int bytes;
 };
@@ -58,7 +57,7 @@ __host__ __device__ inline TcLayout tc_layout(int seq) {
   L.p_hi_off = L.v_off + L.nk * 128;
   const int hi = groups - L.p_lo_groups;
   L.red_off = L.p_hi_off + hi * 16 * 1024;
-  L.bar_off = L.red_off + 4 * kTcQ * 4;
+  L.bar_off = L.red_off + 8 * kTcQ * 4;  // [max | sum][4 column quarters][128 rows]
   L.bytes = L.bar_off + 64;
   return L;
 }
@@ -107,11 +106,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
       : "r"(taddr));
 }
 constexpr int kBwdThreads = 512;  // 16 warps: four per TMEM lane quarter, 32 queries each
+constexpr int kFwdThreads = 512;  // 16 warps: four per TMEM lane quarter
 
 }  // namespace
 
 template <uint32_t kCols>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const gx_attention_args p) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-align by offsetting the shared array itself, so every access below stays in the
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int s = p.seq;
   const TcLayout L = tc_layout(s);
   const uint32_t sbase = smem_u32(smem);
-  float* red = reinterpret_cast<float*>(smem + L.red_off);  // [max|sum][half][128]
+  float* red = reinterpret_cast<float*>(smem + L.red_off);  // [max|sum][quarter][128]
   uint64_t* bar_qk = reinterpret_cast<uint64_t*>(smem + L.bar_off);
   uint64_t* bar_v = bar_qk + 1;
   uint64_t* bar_s = bar_qk + 2;
@@ -182,30 +182,36 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 
   // ---------------------------------------------------------------- softmax over TMEM rows
-  const int qd = warp & 3, hf = warp >> 2;
+  // 16 warps: four per TMEM lane quarter; 64-key blocks go round-robin to the four column
+  // quarters (a block's two 32-key halves stay with one thread, so its Philox draws are
+  // shared), and the quarters exchange row max / row sum through shared memory.
+  const int qd = warp & 3, cq = warp >> 2;
   const int r = qd * 32 + lane;  // tile row == TMEM lane
   const int q = q0 + r;
-  const int half = nk / 2;       // multiple of 32
-  const int c_begin = hf * half, c_end = c_begin + half;
+  const int nblk = nk / 64;
   const uint32_t trow = tmem + (static_cast<uint32_t>(qd * 32) << 16);
   const float c2 = p.scale * 1.4426950408889634f;
   mbar_wait(bar_s, 0);
   tc_fence_after();
 
   float mx = -INFINITY;
-  for (int c0 = c_begin; c0 < c_end; c0 += 32) {
-    uint32_t v[32];
-    tmem_ld32(trow + c0, v);
-    tmem_ld_wait();
+  for (int kb = cq; kb < nblk; kb += 4) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float x = c0 + j < s ? __uint_as_float(v[j]) * c2 : -INFINITY;
-      mx = fmaxf(mx, x);
+    for (int hb = 0; hb < 2; ++hb) {
+      const int c0 = kb * 64 + hb * 32;
+      uint32_t v[32];
+      tmem_ld32(trow + c0, v);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float x = c0 + j < s ? __uint_as_float(v[j]) * c2 : -INFINITY;
+        mx = fmaxf(mx, x);
+      }
     }
   }
-  red[hf * kTcQ + r] = mx;
-  named_sync(1, kTcThreads);
-  const float m = fmaxf(red[r], red[kTcQ + r]);
+  red[cq * kTcQ + r] = mx;
+  named_sync(1, kFwdThreads);
+  const float m = fmaxf(fmaxf(red[r], red[kTcQ + r]), fmaxf(red[2 * kTcQ + r], red[3 * kTcQ + r]));
 
   const uint32_t thr = p.drop_threshold;
   const float inv_keep = p.drop_scale;
@@ -216,58 +222,59 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint16_t* mask = static_cast<uint16_t*>(p.mask);
   const bool row_ok = q < s;
   float sum = 0.f;
-  int cached_kb = -1;
-  uint32_t bits[4] = {0u, 0u, 0u, 0u};
-  for (int c0 = c_begin; c0 < c_end; c0 += 32) {
-    uint32_t v[32];
-    tmem_ld32(trow + c0, v);
-    tmem_ld_wait();
-    float e[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      e[j] = c0 + j < s ? ex2_ftz(__uint_as_float(v[j]) * c2 - m) : 0.f;
-      sum += e[j];
-    }
-    const int kb = c0 >> 6;
+  for (int kb = cq; kb < nblk; kb += 4) {
+    uint32_t bits[4] = {0u, 0u, 0u, 0u};
     if (thr != 0u) {
-      if (kb != cached_kb) {
-        cached_kb = kb;
-        const uint64_t call0 = ((stream + static_cast<uint64_t>(q)) * nkb + kb) * 4;
+      const uint64_t call0 = ((stream + static_cast<uint64_t>(q)) * nkb + kb) * 4;
 #pragma unroll
-        for (int t = 0; t < 4; ++t) bits[t] = keep16(seed, p.site, call0 + t, thr);
-        if (row_ok && kb < nkb) {
-          const uint64_t packed = static_cast<uint64_t>(bits[0]) |
-                                  (static_cast<uint64_t>(bits[1]) << 16) |
-                                  (static_cast<uint64_t>(bits[2]) << 32) |
-                                  (static_cast<uint64_t>(bits[3]) << 48);
-          *reinterpret_cast<uint64_t*>(mask + ((static_cast<int64_t>(bh) * s + q) * nkb + kb) * 4) =
-              packed;
-        }
-      }
-      // key i of this 32-key half: word t = (i/2)%4, bit 8*hb + 2*(i/8) + i%2
-      const int hb = (c0 >> 5) & 1;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const uint32_t bit = (bits[(i >> 1) & 3] >> (8 * hb + 2 * (i >> 3) + (i & 1))) & 1u;
-        e[i] = bit ? e[i] * inv_keep : 0.f;
+      for (int t = 0; t < 4; ++t) bits[t] = keep16(seed, p.site, call0 + t, thr);
+      if (row_ok && kb < nkb) {
+        const uint64_t packed = static_cast<uint64_t>(bits[0]) |
+                                (static_cast<uint64_t>(bits[1]) << 16) |
+                                (static_cast<uint64_t>(bits[2]) << 32) |
+                                (static_cast<uint64_t>(bits[3]) << 48);
+        *reinterpret_cast<uint64_t*>(mask + ((static_cast<int64_t>(bh) * s + q) * nkb + kb) * 4) =
+            packed;
       }
     }
-    // bf16 P row segment -> K-major SWIZZLE_128B tile of its 64-key group
     const uint32_t g_addr = p_group_addr(L, sbase, kb) + r * 128;
-    const int chunk0 = (c0 & 63) >> 3;  // 0 or 4
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t sw = static_cast<uint32_t>((chunk0 + i) ^ (r & 7));
-      st_shared_v4_tc(g_addr + (sw << 4), pack_bf16(e[8 * i + 0], e[8 * i + 1]),
-                      pack_bf16(e[8 * i + 2], e[8 * i + 3]), pack_bf16(e[8 * i + 4], e[8 * i + 5]),
-                      pack_bf16(e[8 * i + 6], e[8 * i + 7]));
+    for (int hb = 0; hb < 2; ++hb) {
+      const int c0 = kb * 64 + hb * 32;
+      uint32_t v[32];
+      tmem_ld32(trow + c0, v);
+      tmem_ld_wait();
+      uint32_t pk[16];
+#pragma unroll
+      for (int j2 = 0; j2 < 16; ++j2) {
+        float e2[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int i = 2 * j2 + u;
+          float e = c0 + i < s ? ex2_ftz(__uint_as_float(v[i]) * c2 - m) : 0.f;
+          sum += e;
+          if (thr != 0u) {
+            // key i of this 32-key half: word t = (i/2)%4, bit 8*hb + 2*(i/8) + i%2
+            const uint32_t bit = (bits[(i >> 1) & 3] >> (8 * hb + 2 * (i >> 3) + (i & 1))) & 1u;
+            e = bit ? e * inv_keep : 0.f;
+          }
+          e2[u] = e;
+        }
+        pk[j2] = pack_bf16(e2[0], e2[1]);
+      }
+      // bf16 P row segment -> K-major SWIZZLE_128B tile of its 64-key group
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t sw = static_cast<uint32_t>((hb * 4 + i) ^ (r & 7));
+        st_shared_v4_tc(g_addr + (sw << 4), pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      }
     }
   }
-  red[2 * kTcQ + hf * kTcQ + r] = sum;
+  red[4 * kTcQ + cq * kTcQ + r] = sum;
   fence_proxy_async_smem_tc();  // P (generic stores) -> visible to the tensor core
   tc_fence_before();
-  named_sync(1, kTcThreads);
-  const float l = red[2 * kTcQ + r] + red[3 * kTcQ + r];
+  named_sync(1, kFwdThreads);
+  const float l = red[4 * kTcQ + r] + red[5 * kTcQ + r] + red[6 * kTcQ + r] + red[7 * kTcQ + r];
 
   // ---------------------------------------------------------------- O = P V
   if (warp == 0) {  // warp-uniform: lane 0 issues, the rest wait here
@@ -284,23 +291,23 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     __syncwarp();
   }
-  if (hf == 0 && row_ok) {
+  if (cq == 0 && row_ok) {
     auto* lse = static_cast<float*>(p.lse);
     lse[static_cast<int64_t>(bh) * s + q] = m + log2f(l);
   }
   mbar_wait(bar_o, 0);
   tc_fence_after();
-  {
-    uint32_t o[32];
-    tmem_ld32(trow + hf * 32, o);
+  {  // O columns [cq*16, cq*16 + 16) of this row
+    uint32_t o[16];
+    tmem_ld16(trow + cq * 16, o);
     tmem_ld_wait();
     if (row_ok) {
       const float inv = 1.f / l;
       auto* ctx = static_cast<__nv_bfloat16*>(p.ctx);
       uint4* out = reinterpret_cast<uint4*>(ctx + (static_cast<int64_t>(b) * s + q) * p.ld_ctx +
-                                            h * kTcHD + hf * 32);
+                                            h * kTcHD + cq * 16);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
+      for (int i = 0; i < 2; ++i) {
         out[i] = make_uint4(pack_bf16(__uint_as_float(o[8 * i + 0]) * inv, __uint_as_float(o[8 * i + 1]) * inv),
                             pack_bf16(__uint_as_float(o[8 * i + 2]) * inv, __uint_as_float(o[8 * i + 3]) * inv),
                             pack_bf16(__uint_as_float(o[8 * i + 4]) * inv, __uint_as_float(o[8 * i + 5]) * inv),
@@ -720,7 +727,7 @@ int attention_fwd_tc(const gx_attention_args& a, cudaStream_t st) {
                            227 * 1024);                                                    \
       set = true;                                                                          \
     }                                                                                      \
-    launch_k(attn_fwd_tc_kernel<C>, grid, dim3(kTcThreads), smem, st, map, a);             \
+    launch_k(attn_fwd_tc_kernel<C>, grid, dim3(kFwdThreads), smem, st, map, a);             \
   }
   if (nk <= 64) GX_ATTN_TC(64)
   else if (nk <= 128) GX_ATTN_TC(128)
