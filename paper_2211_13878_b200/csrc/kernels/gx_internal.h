@@ -126,6 +126,12 @@ struct AdamSegs {
 };
 int adamw_multi(const AdamSegs& segs, float lr, float beta1, float beta2, float eps, float wd,
                 const int64_t* step, cudaStream_t st, int blocks);
+// Persistent AdamW over `count` layers (device table, processing order) on `ctas` SMs; layer i
+// starts once ready[i] >= *step (optimizer_stream.cu).  mark_ready publishes ready[i] = *step.
+int adamw_persistent(const AdamSeg* table_dev, int count, const int64_t* step,
+                     const int64_t* ready, float lr, float beta1, float beta2, float eps, float wd,
+                     int ctas, cudaStream_t st);
+int mark_ready(int64_t* ready, const int64_t* step, cudaStream_t st);
 // *flag = v (stream-ordered; graph-friendly device flag updates)
 int set_flag(int* flag, int v, cudaStream_t st);
 int bump_step(int64_t* step, uint64_t* seed_offset, cudaStream_t st);

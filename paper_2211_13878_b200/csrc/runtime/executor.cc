@@ -192,6 +192,9 @@ struct RankCtx {
   int* opt_pending = nullptr;  // deferred optimizer: gradients of the last step not applied yet
   std::vector<cudaEvent_t> opt_done;  // deferred optimizer: layer li updated (forward may read)
   std::vector<int> opt_group;         // side-stream optimizer: layers waiting for a grouped launch
+  // persistent optimizer: layer table in backward order + per-entry "gradients ready" flags
+  AdamSeg* opt_table = nullptr;
+  int64_t* opt_ready = nullptr;
   int64_t* step = nullptr;
   uint64_t* seed_off = nullptr;
   int64_t in_rows_total = 0;
@@ -383,6 +386,14 @@ class ExecutorImpl final : public Executor {
   bool splitk_ = true;         // split-K for long-K / small-MN GEMMs (GX_SPLITK=0 disables)
   int opt_blocks_ = 0;         // grid of the side-stream AdamW (GX_OPT_BLOCKS; 0 = 2 per SM)
   int opt_group_ = 1;          // layers per side-stream AdamW launch (GX_OPT_GROUP, <= 8)
+  // Persistent flag-driven AdamW on this many SMs (cfg "optimizer_sms" / GX_OPT_SMS; 0 = the
+  // per-layer side-stream launches): one kernel per step walks the layers in backward order
+  // as their gradients are marked ready (optimizer_stream.cu).
+  int opt_sms_ = 0;
+  bool persistent_opt() const {
+    return opt_sms_ > 0 && optimizer_ && !forward_only_ && !profiling_ && !deferred() &&
+           opt_stream_ == 0;
+  }
   bool dry_run_ = false;       // topology only: no device state (host-logic tests)
   float inv_count_ = 1.f;
 
@@ -518,6 +529,9 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     opt_group_ = cfg.value("optimizer_group", 1);
     if (const char* e = std::getenv("GX_OPT_GROUP")) opt_group_ = std::atoi(e);
     opt_group_ = std::max(1, std::min(8, opt_group_));
+    opt_sms_ = cfg.value("optimizer_sms", 0);
+    if (const char* e = std::getenv("GX_OPT_SMS")) opt_sms_ = std::atoi(e);
+    opt_sms_ = std::max(0, opt_sms_);
     wgrad_stream_ = cfg.value("wgrad_stream", true);
     trace_ = cfg.value("trace", false);
     fuse_dz_ = cfg.value("fuse_dz", false);
@@ -845,6 +859,18 @@ int ExecutorImpl::allocate(RankCtx& r) {
   r.step = A.a<int64_t>(1);
   r.opt_pending = A.a<int>(1);
   if (r.opt_pending != nullptr) cudaMemset(r.opt_pending, 0, sizeof(int));
+  r.opt_table = A.a<AdamSeg>(static_cast<int64_t>(r.layers.size()));
+  r.opt_ready = A.a<int64_t>(static_cast<int64_t>(r.layers.size()));
+  if (r.opt_ready != nullptr) cudaMemset(r.opt_ready, 0, r.layers.size() * sizeof(int64_t));
+  if (r.opt_table != nullptr) {  // backward order: entry i = local layer (n - 1 - i)
+    std::vector<AdamSeg> tab;
+    for (size_t i = 0; i < r.layers.size(); ++i) {
+      RankLayer& L = r.layers[r.layers.size() - 1 - i];
+      tab.push_back(AdamSeg{L.master, L.gshard, L.m, L.v, L.pshard,
+                            adam_fused(L) ? L.lay.acc_end : L.shard_n});
+    }
+    cudaMemcpy(r.opt_table, tab.data(), tab.size() * sizeof(AdamSeg), cudaMemcpyHostToDevice);
+  }
   r.opt_done.resize(r.layers.size(), nullptr);
   for (auto& e : r.opt_done)
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
@@ -1471,6 +1497,13 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
                                DType::kF32, stream_);
     return kOk;
   }
+  if (phase == 2 && optimizer_ && !deferred() && persistent_opt()) {
+    // the persistent optimizer (launched at the start of the backward) takes it from here
+    int64_t* flag = r.opt_ready + (static_cast<int>(r.layers.size()) - 1 - li);
+    if (wg_active_ && L.d.sdp == 1 && L.d.dp == 1)  // gradients complete on the wgrad stream
+      return on_wgrad([&] { return mark_ready(flag, r.step, ls_); });
+    return mark_ready(flag, r.step, stream_);
+  }
   if (phase == 2 && optimizer_ && !deferred()) {
     // with the AdamW-fused weight-gradient epilogues only the LayerNorm / bias prefix is left
     const int64_t n_opt = adam_fused(L) ? L.lay.acc_end : L.shard_n;
@@ -1794,6 +1827,14 @@ int ExecutorImpl::step_once() {
     }
   }
   tmark("fwd_end", stream_);
+  if (persistent_opt()) {  // one persistent AdamW per rank on a slice of the SMs
+    GX_TRY(fork(stream_, side_));
+    side_used_ = true;
+    const int ctas = std::max(1, std::min(opt_sms_, num_sms() / 2));
+    for (auto& r : ranks_)
+      GX_TRY(adamw_persistent(r->opt_table, static_cast<int>(r->layers.size()), r->step,
+                              r->opt_ready, lr_, b1_, b2_, eps_, wd_, ctas, side_));
+  }
   // --------------------------------------------------------------- backward (GPipe)
   for (int mb = m_ - 1; mb >= 0 && !forward_only_; --mb) {
     for (int st = P_ - 1; st >= 0; --st) {
