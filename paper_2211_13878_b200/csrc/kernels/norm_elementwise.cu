@@ -660,12 +660,13 @@ __global__ void __launch_bounds__(256) dropout_bwd_colsum_kernel(
   if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;
 }
 
+constexpr int kColsumSlicesUsed = 8;
 static void colsum_grid(int rows, int cols, dim3* grid, int* rpb) {
   const int strips = (cols / 8 + 7) / 8;
   int ysplit = (num_sms() * 4 + strips - 1) / strips;
   const int max_y = (rows + 31) / 32;
   if (ysplit > max_y) ysplit = max_y;
-  if (ysplit > kColsumMaxSlices) ysplit = kColsumMaxSlices;
+  if (ysplit > kColsumSlicesUsed) ysplit = kColsumSlicesUsed;  // fewer, longer slices measured best
   if (ysplit < 1) ysplit = 1;
   *rpb = (rows + ysplit - 1) / ysplit;
   *grid = dim3(strips, (rows + *rpb - 1) / *rpb);
