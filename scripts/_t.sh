@@ -1,1 +1,2 @@
-for c in 0 2 4 8; do GX_COLSUM_SLICES=$c timeout 200 python scripts/step_variants.py default no_optimizer | sed "s/^/cap$c /"; done
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+for i in 1 2; do timeout 200 python scripts/step_variants.py default no_optimizer; done
