@@ -311,7 +311,9 @@ def run_gx(args, rank, world, local_rank):
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
-            "memory": {"device_bytes_rank0": info["ranks"][0]["device_bytes"]},
+            "memory": {"device_bytes_rank0": info["ranks"][0]["device_bytes"],
+                       "plan_estimate_bytes_rank0": info["ranks"][0].get("plan_estimate_bytes"),
+                       "budget_bytes": int(args.budget_gib * (1 << 30))},
         }
         print(json.dumps(line), flush=True)
     ex.close()

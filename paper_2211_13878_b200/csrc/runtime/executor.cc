@@ -107,13 +107,22 @@ int64_t canon_index(const Shape& s, const Layout& L, int t, int tr, int64_t j) {
 }
 
 // ------------------------------------------------------------------ device allocations
+// Per-rank device arena with an optional byte cap (E15: the per-GPU memory budget E of the
+// plan).  Exceeding the cap fails the allocation like an OOM.
 class Arena {
  public:
   ~Arena() {
     for (void* p : ptrs_) cudaFree(p);
   }
+  void set_cap(size_t cap) { cap_ = cap; }
+  size_t cap() const { return cap_; }
+  bool over_cap() const { return over_cap_; }
   void* alloc(size_t bytes) {
     if (bytes == 0) return nullptr;
+    if (cap_ != 0 && bytes_ + bytes > cap_) {
+      failed_ = over_cap_ = true;
+      return nullptr;
+    }
     void* p = nullptr;
     if (cudaMalloc(&p, (bytes + 255) / 256 * 256) != cudaSuccess) {
       failed_ = true;
@@ -133,7 +142,8 @@ class Arena {
  private:
   std::vector<void*> ptrs_;
   size_t bytes_ = 0;
-  bool failed_ = false;
+  size_t cap_ = 0;
+  bool failed_ = false, over_cap_ = false;
 };
 
 using bf16 = __nv_bfloat16;
@@ -392,6 +402,7 @@ class ExecutorImpl final : public Executor {
   // per-layer side-stream launches): one kernel per step walks the layers in backward order
   // as their gradients are marked ready (optimizer_stream.cu).
   int opt_sms_ = 0;
+  int64_t mem_cap_ = 0;  // per-rank device-byte cap (cfg "memory_cap_bytes"; 0 = none)
   bool persistent_opt() const {
     return opt_sms_ > 0 && optimizer_ && !forward_only_ && !profiling_ && !deferred() &&
            opt_stream_ == 0;
@@ -534,6 +545,8 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     opt_sms_ = cfg.value("optimizer_sms", 0);
     if (const char* e = std::getenv("GX_OPT_SMS")) opt_sms_ = std::atoi(e);
     opt_sms_ = std::max(0, opt_sms_);
+    mem_cap_ = cfg.value("memory_cap_bytes", static_cast<int64_t>(0));
+    if (const char* e = std::getenv("GX_MEMORY_CAP")) mem_cap_ = std::atoll(e);
     wgrad_stream_ = cfg.value("wgrad_stream", true);
     trace_ = cfg.value("trace", false);
     fuse_dz_ = cfg.value("fuse_dz", false);
@@ -759,6 +772,7 @@ int ExecutorImpl::build_groups() {
 
 int ExecutorImpl::allocate(RankCtx& r) {
   Arena& A = r.arena;
+  A.set_cap(static_cast<size_t>(mem_cap_));
   int64_t max_rows = 0, max_h = 0, max_f = 0, max_q = 0, max_c = 0, max_lse = 0;
   for (size_t li = 0; li < r.layers.size(); ++li) {
     RankLayer& L = r.layers[li];
@@ -773,8 +787,8 @@ int ExecutorImpl::allocate(RankCtx& r) {
     L.gshard = L.d.sdp > 1 ? A.a<float>(L.shard_n) : L.gfull;
     L.pshard = A.a<bf16>(L.shard_n);
     L.pfull = L.d.sdp > 1 ? A.a<bf16>(L.lay.total) : L.pshard;
-    cudaMemset(L.m, 0, L.shard_n * 4);
-    cudaMemset(L.v, 0, L.shard_n * 4);
+    if (L.m != nullptr) cudaMemset(L.m, 0, L.shard_n * 4);
+    if (L.v != nullptr) cudaMemset(L.v, 0, L.shard_n * 4);
     L.acts.resize(m_);
     for (int mb = 0; mb < m_; ++mb) {
       Acts& a = L.acts[mb];
@@ -878,8 +892,8 @@ int ExecutorImpl::allocate(RankCtx& r) {
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
       return set_error(kErrCuda, "executor: event creation failed");
   r.seed_off = A.a<uint64_t>(1);
-  cudaMemset(r.step, 0, 8);
-  cudaMemset(r.seed_off, 0, 8);
+  if (r.step != nullptr) cudaMemset(r.step, 0, 8);
+  if (r.seed_off != nullptr) cudaMemset(r.seed_off, 0, 8);
   // stage input (first stage) / targets (last stage) for all micro-batches of this rank
   const RankLayer& first = r.layers.front();
   const RankLayer& last = r.layers.back();
@@ -907,6 +921,11 @@ int ExecutorImpl::allocate(RankCtx& r) {
     for (int mb = 0; mb < m_; ++mb) rows_all += last.acts[mb].rows;
     r.target = A.a<bf16>(rows_all * last.sh.h);
   }
+  if (A.failed()) (void)cudaGetLastError();  // no stale error for the next caller's checks
+  if (A.over_cap())
+    return set_error(kErrInfeasible, ("executor: rank " + std::to_string(r.rank) +
+                                      " needs more than its memory cap of " +
+                                      std::to_string(mem_cap_) + " bytes").c_str());
   if (A.failed()) return set_error(kErrCuda, "executor: out of device memory");
   return cuda_check(cudaDeviceSynchronize(), "executor allocate");
 }
@@ -2074,6 +2093,10 @@ std::string ExecutorImpl::info() const {
     jr["rank"] = r->rank;
     jr["stage"] = r->stage;
     jr["device_bytes"] = r->arena.bytes();
+    jr["memory_cap_bytes"] = r->arena.cap();
+    // the planner's per-device estimate for this rank's stage (EstimateMemory, A7)
+    if (plan_.contains("stages") && r->stage < static_cast<int>(plan_["stages"].size()))
+      jr["plan_estimate_bytes"] = plan_["stages"][r->stage].value("peak_memory_bytes", int64_t{0});
     int64_t params = 0, opt = 0, grads = 0;
     for (const RankLayer& L : r->layers) {
       params += L.shard_n * 4 + L.lay.total * 2;

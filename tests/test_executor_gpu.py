@@ -178,3 +178,21 @@ def test_deferred_optimizer_matches_immediate(cuda, strategies, world):
     for l, (a, b) in enumerate(zip(res[0][1], res[1][1])):
         for k in a:
             assert np.array_equal(a[k], b[k]), (l, k)
+
+
+def test_memory_cap_enforced_and_reported(cuda):
+    """E15: the per-rank arena honours a byte cap (plan infeasible beyond it) and info()
+    reports device bytes next to the planner's estimate for the rank's stage."""
+    from paper_2211_13878_b200 import _lib
+    plan = gxe.make_plan(["", ""], 2)
+    model = _small_model(L=2)
+    ex = gxe.PlanExecutor(plan, model, 1)
+    info = ex.info()["ranks"][0]
+    used = info["device_bytes"]
+    assert used > 0 and "plan_estimate_bytes" in info
+    ex.close()
+    with pytest.raises(_lib.GxError):
+        gxe.PlanExecutor(plan, model, 1, memory_cap_bytes=used // 2)
+    ok = gxe.PlanExecutor(plan, model, 1, memory_cap_bytes=used + (1 << 20))
+    assert ok.info()["ranks"][0]["memory_cap_bytes"] == used + (1 << 20)
+    ok.close()
