@@ -169,7 +169,7 @@ typedef struct gx_gemm_epilogue {
   int64_t ldo;
   float alpha;                /* acc scale */
   const void* bias;           /* bf16 [N] or NULL */
-  int gelu;                   /* out = gelu(acc + bias); aux = acc + bias (bf16) */
+  int gelu;                   /* out = gelu(acc + bias); aux = acc + bias (bf16); 2: aux = gelu'(acc + bias) */
   void* aux;
   int64_t ld_aux;
   const void* residual;       /* bf16 [M][ld_res]: out = residual + dropout(acc + bias) */
@@ -181,7 +181,7 @@ typedef struct gx_gemm_epilogue {
   float drop_scale;           /* 256 / (256 - thr8) */
   uint64_t seed;
   uint64_t site;
-  int gelu_bwd;               /* out = acc * gelu'(aux) (aux = bf16 pre-activation, read) */
+  int gelu_bwd;               /* out = acc * gelu'(aux) (aux = bf16 pre-activation, read); 2: out = acc * aux */
   const uint64_t* seed_offset;/* optional device counter added to seed (per-step masks) */
   /* GX_OUT_ADAMW: the accumulator is the complete gradient of a weight slot; the epilogue
    * applies AdamW to master/m/v (fp32) and writes the bf16 parameter, all [M][ldo] like

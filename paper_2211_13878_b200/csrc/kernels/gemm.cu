@@ -108,14 +108,30 @@ __device__ __forceinline__ void epilogue_math(const GemmEpilogue& ep, int64_t ro
       v[2 * t + 1] += bf16_hi(bias_w[t]);
     }
   }
-  if (ep.gelu_bwd) {  // dgrad epilogue of the MLP up-projection: v <- v * gelu'(pre)
+  if (ep.gelu_bwd == 2) {  // aux already holds gelu'(pre) (written by a gelu == 2 forward)
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      v[2 * t] *= bf16_lo(in_w[t]);
+      v[2 * t + 1] *= bf16_hi(in_w[t]);
+    }
+  } else if (ep.gelu_bwd) {  // dgrad epilogue of the MLP up-projection: v <- v * gelu'(pre)
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
       v[2 * t] *= gelu_erf_grad(bf16_lo(in_w[t]));
       v[2 * t + 1] *= gelu_erf_grad(bf16_hi(in_w[t]));
     }
   }
-  if (ep.gelu) {
+  if (ep.gelu == 2) {
+    // forward that also hands the backward its derivative: aux <- gelu'(pre), computed from
+    // the same erf / exp as the value, so the backward epilogue is a plain multiply
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float x = __bfloat162float(__float2bfloat16_rn(v[j]));
+      const GeluTerms g = gelu_terms(x);
+      v[j] = x * g.phi_cdf;
+      pre[j] = g.phi_cdf + x * 0.3989422804014327f * g.e;
+    }
+  } else if (ep.gelu) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       // GeLU is applied to the bf16-rounded pre-activation so forward and backward agree.

@@ -1197,7 +1197,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     e.out = A.gel;
     e.ldo = ft;
     e.bias = P + L.lay.b1.off;
-    e.gelu = 1;
+    e.gelu = 2;  // A.pre receives gelu'(pre-activation) for the backward's plain multiply
     e.aux = A.pre;
     e.ld_aux = ft;
     GX_TRY(gemm(A.ln2, h, false, P + L.lay.w1.off, h, false, rows, ft, h, e));
@@ -1342,7 +1342,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     e.out_kind = kOutBF16;
     e.out = dpre;
     e.ldo = ft;
-    e.gelu_bwd = 1;
+    e.gelu_bwd = 2;
     e.aux = A.pre;
     e.ld_aux = ft;
     GX_TRY(gemm(dz, h, false, P + L.lay.w2.off, ft, true, rows, ft, h, e));  // dz W2 * gelu'

@@ -34,9 +34,10 @@ def dropout_scale(p: float) -> float:
 def gemm(a, b, *, a_mn_major=False, b_mn_major=False, out=None, out_kind="bf16", bias=None,
          gelu_aux=None, residual=None, alpha=1.0, dropout_p=0.0, seed=0, site=0,
          row_offset=0, col_offset=0, drop_ld=None, tile_n=0, stream=None, gelu_bwd_aux=None,
-         trace=None):
+         trace=None, gelu_mode=1):
     """C = A * B^T.  A is [M,K] (or [K,M] if a_mn_major); B is [N,K] (or [K,N]).
-    trace: optional int64 device tensor [grid*8] receiving per-CTA %globaltimer stamps."""
+    trace: optional int64 device tensor [grid*16] receiving per-CTA %globaltimer stamps.
+    gelu_mode 2: gelu_aux receives gelu'(pre) (forward) / gelu_bwd_aux holds gelu'(pre) (backward)."""
     import torch
     M = a.shape[1] if a_mn_major else a.shape[0]
     K = a.shape[0] if a_mn_major else a.shape[1]
@@ -54,8 +55,8 @@ def gemm(a, b, *, a_mn_major=False, b_mn_major=False, out=None, out_kind="bf16",
     ep.ldo = out.stride(0)
     ep.alpha = alpha
     ep.bias = _ptr(bias)
-    ep.gelu = 1 if gelu_aux is not None else 0
-    ep.gelu_bwd = 1 if gelu_bwd_aux is not None else 0
+    ep.gelu = gelu_mode if gelu_aux is not None else 0
+    ep.gelu_bwd = gelu_mode if gelu_bwd_aux is not None else 0
     aux = gelu_aux if gelu_aux is not None else gelu_bwd_aux
     ep.aux = _ptr(aux)
     ep.ld_aux = aux.stride(0) if aux is not None else 0

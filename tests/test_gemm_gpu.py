@@ -65,6 +65,31 @@ def test_gemm_bias_gelu(cuda):
     assert _rel(y, ref) <= 1e-2
 
 
+def test_gemm_gelu_derivative_mode(cuda):
+    """gelu == 2 writes gelu'(pre) as the aux output; gelu_bwd == 2 multiplies by it."""
+    from paper_2211_13878_b200 import kernels
+    g = torch.Generator(device="cpu").manual_seed(16)
+    M, N, K = 512, 5120, 1280
+    X = torch.randn(M, K, generator=g).to(cuda, torch.bfloat16)
+    W = (0.03 * torch.randn(N, K, generator=g)).to(cuda, torch.bfloat16)
+    b = torch.randn(N, generator=g).to(cuda, torch.bfloat16)
+    dgel = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    y = kernels.gemm(X, W, bias=b, gelu_aux=dgel, gelu_mode=2)
+    pre = (X.float() @ W.float().t() + b.float()).to(torch.bfloat16).float().requires_grad_(True)
+    ref = torch.nn.functional.gelu(pre)
+    ref.backward(torch.ones_like(ref))
+    torch.cuda.synchronize()
+    assert _rel(y, ref.detach()) <= 1e-2
+    assert _rel(dgel, pre.grad) <= 1e-2
+    # backward: out = (dY W2-like product) * aux
+    dZ = torch.randn(M, 1280, generator=g).to(cuda, torch.bfloat16)
+    W2 = (0.03 * torch.randn(1280, N, generator=g)).to(cuda, torch.bfloat16)
+    out = kernels.gemm(dZ, W2, b_mn_major=True, gelu_bwd_aux=dgel, gelu_mode=2)
+    ref2 = (dZ.float() @ W2.float()) * dgel.float()
+    torch.cuda.synchronize()
+    assert _rel(out, ref2) <= 1e-2
+
+
 def test_gemm_residual_dropout(cuda):
     from paper_2211_13878_b200 import kernels
     g = torch.Generator(device="cpu").manual_seed(7)
