@@ -105,7 +105,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
-constexpr int kBwdThreads = 512;  // 16 warps: four per TMEM lane quarter, 32 queries each
+constexpr int kBwdSoftmax = 512;  // 16 softmax warps: four per TMEM lane quarter, 32 queries each
+constexpr int kBwdThreads = kBwdSoftmax + 32;  // + one producer / MMA-issue warp (warp 16)
+constexpr int kBwdMmaWarp = kBwdSoftmax / 32;
 constexpr int kFwdThreads = 512;  // 16 warps: four per TMEM lane quarter
 
 }  // namespace
@@ -148,7 +150,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  GX_ATTN_STAMP(p, 0);
   pdl_enter();
+  GX_ATTN_STAMP(p, 1);
 
   // ---------------------------------------------------------------- loads + S = Q K^T
   if (warp == 0) {  // warp-uniform: lane 0 issues, the rest wait here
@@ -193,6 +197,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const float c2 = p.scale * 1.4426950408889634f;
   mbar_wait(bar_s, 0);
   tc_fence_after();
+  GX_ATTN_STAMP(p, 2);
 
   float mx = -INFINITY;
   for (int kb = cq; kb < nblk; kb += 4) {
@@ -211,6 +216,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   }
   red[cq * kTcQ + r] = mx;
   named_sync(1, kFwdThreads);
+  GX_ATTN_STAMP(p, 3);
   const float m = fmaxf(fmaxf(red[r], red[kTcQ + r]), fmaxf(red[2 * kTcQ + r], red[3 * kTcQ + r]));
 
   const uint32_t thr = p.drop_threshold;
@@ -274,6 +280,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   fence_proxy_async_smem_tc();  // P (generic stores) -> visible to the tensor core
   tc_fence_before();
   named_sync(1, kFwdThreads);
+  GX_ATTN_STAMP(p, 4);
   const float l = red[4 * kTcQ + r] + red[5 * kTcQ + r] + red[6 * kTcQ + r] + red[7 * kTcQ + r];
 
   // ---------------------------------------------------------------- O = P V
@@ -297,6 +304,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   }
   mbar_wait(bar_o, 0);
   tc_fence_after();
+  GX_ATTN_STAMP(p, 5);
   {  // O columns [cq*16, cq*16 + 16) of this row
     uint32_t o[16];
     tmem_ld16(trow + cq * 16, o);
@@ -339,8 +347,8 @@ namespace {
 struct BwdLayout {
   // Q and dO stream through three 16 KB buffers each (chunk j in buffer j % 3)
   static constexpr int kK = 0, kV = 16384, kQ = 32768, kDO = 81920, kPd = 131072,
-                       kDS = 163840, kLse = 196608 /* [512] */, kD = kLse + 2048 /* [128] */,
-                       kMask = kD + 512 /* [512 q][2 kb][4] u16 */, kBar = kMask + 8192,
+                       kDS = 163840, kLse = 196608 /* [512] */, kD = kLse + 2048 /* [2][128] */,
+                       kMask = kD + 1024 /* [512 q][2 kb][4] u16 */, kBar = kMask + 8192,
                        kBytes = kBar + 128;
 };
 }  // namespace
@@ -362,7 +370,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* bar_ld = bar_kv + 1;  // [3]
   uint64_t* bar_s = bar_kv + 4;
   uint64_t* bar_mm = bar_kv + 5;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_kv + 6);
+  uint64_t* bar_pds = bar_kv + 6;  // Pd / dS of a chunk stored (all softmax threads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_kv + 7);
 
   const int warp = static_cast<int>(warp_id());
   const int lane = static_cast<int>(lane_id());
@@ -385,6 +394,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(&bar_ld[2], 1);
     mbar_init(bar_s, 1);
     mbar_init(bar_mm, 1);
+    mbar_init(bar_pds, kBwdSoftmax);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<512>(tmem_slot);
@@ -396,31 +406,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   pdl_enter();
   GX_ATTN_STAMP(p, 1);
 
-  auto load_chunk = [&](int j) {  // Q_j, dO_j -> buffer j % 3
-    const int bf = j % 3;
-    const int r = row0 + j * kTcQ;
-    mbar_expect_tx(&bar_ld[bf], 2 * kTcQ * 128);
-    for (int x = 0; x < 2; ++x) {
-      tma_load_3d(smem + BL::kQ + bf * 16384 + x * 8192, &map_qkv, &bar_ld[bf], 0, h, r + 64 * x);
-      tma_load_3d(smem + BL::kDO + bf * 16384 + x * 8192, &map_do, &bar_ld[bf], 0, h, r + 64 * x);
-    }
-  };
-  if (warp == 0) {  // warp-uniform: lane 0 issues, the rest wait here
-    if (lane == 0) {
-      mbar_expect_tx(bar_kv, 2 * kTcQ * 128);
-      for (int x = 0; x < 2; ++x) {
-        tma_load_3d(smem + BL::kK + x * 8192, &map_qkv, bar_kv, 0, H + h, row0 + kt * 128 + 64 * x);
-        tma_load_3d(smem + BL::kV + x * 8192, &map_qkv, bar_kv, 0, 2 * H + h, row0 + kt * 128 + 64 * x);
-      }
-      load_chunk(0);
-    }
-    __syncwarp();
-  }
-  {  // lse and keep words of every query of the head (once; overlaps the TMA loads)
+  const bool is_mma_warp = warp == kBwdMmaWarp;
+  if (!is_mma_warp) {  // lse and keep words of every query of the head (once)
     const float* lse_g = static_cast<const float*>(p.lse) + static_cast<int64_t>(bh) * s;
     const uint16_t* mask_g = static_cast<const uint16_t*>(p.mask);
-    for (int q = threadIdx.x; q < s; q += kBwdThreads) sLse[q] = lse_g[q];
-    for (int i = threadIdx.x; i < 2 * s; i += kBwdThreads) {
+    for (int q = threadIdx.x; q < s; q += kBwdSoftmax) sLse[q] = lse_g[q];
+    for (int i = threadIdx.x; i < 2 * s; i += kBwdSoftmax) {
       const int q = i >> 1, kb = kt * 2 + (i & 1);
       uint64_t w = 0;
       if (p.drop_threshold != 0u && kb < nkb)
@@ -429,7 +420,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   }
 
-  const int qd = warp & 3, cq = warp >> 2;  // TMEM lane quarter, 32-column quarter
+  const int qd = warp & 3, cq = (warp >> 2) & 3;  // TMEM lane quarter, 32-column quarter
   const int kr = qd * 32 + lane;      // key row of the tile == TMEM lane (S^T, dV, dK)
   const int key = kt * 128 + kr;
   const uint32_t trow = tmem + (static_cast<uint32_t>(qd * 32) << 16);
@@ -439,204 +430,216 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int kbl = kr >> 6, kk = kr & 63;
   const int mt = (kk >> 1) & 3, mbit = 2 * (kk >> 3) + (kk & 1);
   float* part = static_cast<float*>(p.dq_accum);
-  const uint32_t idesc_s = idesc_bf16_f32(kTcQ, 128, false, false);
-  const uint32_t idesc_kv = idesc_bf16_f32(128, kTcHD, false, true);
-  const uint32_t idesc_q = idesc_bf16_f32(kTcQ, kTcHD, true, true);
 
-  // S^T / dPd^T MMAs of chunk j (thread 0)
-  auto issue_s = [&](int j) {
-    const int bf = j % 3;
-    mbar_wait(&bar_ld[bf], (j / 3) & 1);
-    tc_fence_after();
-    const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
-#pragma unroll
-    for (int k = 0; k < kTcHD / 16; ++k) {
-      umma_bf16(tmem, sdesc_sw128(sb + BL::kK + k * 32, 16, 1024),
-                sdesc_sw128(q_b + k * 32, 16, 1024), idesc_s, k != 0 ? 1u : 0u);
-      umma_bf16(tmem + 128, sdesc_sw128(sb + BL::kV + k * 32, 16, 1024),
-                sdesc_sw128(do_b + k * 32, 16, 1024), idesc_s, k != 0 ? 1u : 0u);
-    }
-    umma_commit(bar_s);
-  };
-  // dV += Pd^T dO_j, dK += dS^T Q_j, dQ_j = dS K (thread 0)
-  auto issue_grads = [&](int j) {
-    const int bf = j % 3;
-    const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
-#pragma unroll
-    for (int k = 0; k < kTcQ / 16; ++k) {  // K = 128 queries (dV, dK) / 128 keys (dQ)
-      const uint32_t a_kmaj = (k >> 2) * 16384 + (k & 3) * 32;
-      const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
-      umma_bf16(tmem + 256, sdesc_sw128(sb + BL::kPd + a_kmaj, 16, 1024),
-                sdesc_sw128(do_b + k * 2048, 16384, 1024), idesc_kv, acc);
-      umma_bf16(tmem + 320, sdesc_sw128(sb + BL::kDS + a_kmaj, 16, 1024),
-                sdesc_sw128(q_b + k * 2048, 16384, 1024), idesc_kv, acc);
-      umma_bf16(tmem + 384, sdesc_sw128(sb + BL::kDS + k * 2048, 16384, 1024),
-                sdesc_sw128(sb + BL::kK + k * 2048, 16384, 1024), idesc_q, k > 0 ? 1u : 0u);
-    }
-    umma_commit(bar_mm);
-  };
-  // D = rowsum(dO * O) of chunk j's 128 queries -> sD (dO from smem, O from global)
-  auto compute_d = [&](int j) {
-    const int bf = j % 3;
-    mbar_wait(&bar_ld[bf], (j / 3) & 1);
-    const int qi = threadIdx.x >> 2, part4 = threadIdx.x & 3;  // 4 threads per query row
-    const int q = j * kTcQ + qi;
-    const uint8_t* dob = smem + BL::kDO + bf * 16384 + qi * 128;
-    float acc = 0.f;
-    if (q < s) {
-      const uint4* og = reinterpret_cast<const uint4*>(
-          static_cast<const __nv_bfloat16*>(p.ctx) + (static_cast<int64_t>(row0) + q) * p.ld_ctx +
-          h * kTcHD + part4 * 16);
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int cc = part4 * 2 + c;
-        const int sw = (cc ^ (qi & 7)) << 4;
-        const uint4 a = *reinterpret_cast<const uint4*>(dob + sw);
-        const uint4 o = og[c];
-        const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, ow[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          acc += bf16_lo(aw[t]) * bf16_lo(ow[t]) + bf16_hi(aw[t]) * bf16_hi(ow[t]);
-      }
-    }
-    acc += __shfl_xor_sync(0xffffffff, acc, 1);
-    acc += __shfl_xor_sync(0xffffffff, acc, 2);
-    if (part4 == 0) sD[qi] = acc;
-  };
-  // dQ_j partial (fp32) out of TMEM (lane = query row of the chunk, 16 columns per warp)
-  auto store_dq = [&](int j) {
-    uint32_t o[16];
-    tmem_ld16(trow + 384 + cq * 16, o);
-    tmem_ld_wait();
-    const int q = j * kTcQ + kr;
-    if (q < s) {
-      float4* dst = reinterpret_cast<float4*>(
-          part + ((static_cast<int64_t>(kt) * gridDim.y + bh) * s + q) * kTcHD + cq * 16);
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
-                             __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
-    }
-  };
-  if (warp == 0) {  // warp-uniform: lane 0 issues, the rest wait here
+  if (is_mma_warp) {
+    // ------------------------------------------------ producer / MMA issue (one lane)
+    // Softmax warps never wait on this warp directly: it consumes bar_pds (Pd / dS stored)
+    // and publishes bar_s (next scores) and bar_mm (gradient products), so the issue
+    // latency of ~30 MMAs per chunk overlaps the softmax math instead of stalling it.
     if (lane == 0) {
-      if (nq > 1) load_chunk(1);
-      if (nq > 2) load_chunk(2);
+      const uint32_t idesc_s = idesc_bf16_f32(kTcQ, 128, false, false);
+      const uint32_t idesc_kv = idesc_bf16_f32(128, kTcHD, false, true);
+      const uint32_t idesc_q = idesc_bf16_f32(kTcQ, kTcHD, true, true);
+      auto load_chunk = [&](int j) {  // Q_j, dO_j -> buffer j % 3
+        const int bf = j % 3;
+        const int r = row0 + j * kTcQ;
+        mbar_expect_tx(&bar_ld[bf], 2 * kTcQ * 128);
+        for (int x = 0; x < 2; ++x) {
+          tma_load_3d(smem + BL::kQ + bf * 16384 + x * 8192, &map_qkv, &bar_ld[bf], 0, h, r + 64 * x);
+          tma_load_3d(smem + BL::kDO + bf * 16384 + x * 8192, &map_do, &bar_ld[bf], 0, h, r + 64 * x);
+        }
+      };
+      auto issue_s = [&](int j) {  // S^T = K Q_j^T, dPd^T = V dO_j^T
+        const int bf = j % 3;
+        mbar_wait(&bar_ld[bf], (j / 3) & 1);
+        tc_fence_after();
+        const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
+#pragma unroll
+        for (int k = 0; k < kTcHD / 16; ++k) {
+          umma_bf16(tmem, sdesc_sw128(sb + BL::kK + k * 32, 16, 1024),
+                    sdesc_sw128(q_b + k * 32, 16, 1024), idesc_s, k != 0 ? 1u : 0u);
+          umma_bf16(tmem + 128, sdesc_sw128(sb + BL::kV + k * 32, 16, 1024),
+                    sdesc_sw128(do_b + k * 32, 16, 1024), idesc_s, k != 0 ? 1u : 0u);
+        }
+        umma_commit(bar_s);
+      };
+      auto issue_grads = [&](int j) {  // dV += Pd^T dO_j, dK += dS^T Q_j, dQ_j = dS K
+        const int bf = j % 3;
+        const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
+#pragma unroll
+        for (int k = 0; k < kTcQ / 16; ++k) {
+          const uint32_t a_kmaj = (k >> 2) * 16384 + (k & 3) * 32;
+          const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
+          umma_bf16(tmem + 256, sdesc_sw128(sb + BL::kPd + a_kmaj, 16, 1024),
+                    sdesc_sw128(do_b + k * 2048, 16384, 1024), idesc_kv, acc);
+          umma_bf16(tmem + 320, sdesc_sw128(sb + BL::kDS + a_kmaj, 16, 1024),
+                    sdesc_sw128(q_b + k * 2048, 16384, 1024), idesc_kv, acc);
+          umma_bf16(tmem + 384, sdesc_sw128(sb + BL::kDS + k * 2048, 16384, 1024),
+                    sdesc_sw128(sb + BL::kK + k * 2048, 16384, 1024), idesc_q, k > 0 ? 1u : 0u);
+        }
+        umma_commit(bar_mm);
+      };
+      mbar_expect_tx(bar_kv, 2 * kTcQ * 128);
+      for (int x = 0; x < 2; ++x) {
+        tma_load_3d(smem + BL::kK + x * 8192, &map_qkv, bar_kv, 0, H + h, row0 + kt * 128 + 64 * x);
+        tma_load_3d(smem + BL::kV + x * 8192, &map_qkv, bar_kv, 0, 2 * H + h, row0 + kt * 128 + 64 * x);
+      }
+      for (int j = 0; j < nq && j < 3; ++j) load_chunk(j);
       mbar_wait(bar_kv, 0);
       issue_s(0);
-    }
-    __syncwarp();
-  }
-  compute_d(0);
-  named_sync(1, kBwdThreads);
-  GX_ATTN_STAMP(p, 2);
-
-  // Pipeline per chunk j: scores S(j) were issued one step earlier; the softmax math of j
-  // runs while the tensor core still does dV / dK / dQ of j-1, whose completion is awaited
-  // only right before Pd / dS(j) overwrite the smem those MMAs read.
-  for (int j = 0; j < nq; ++j) {
-    mbar_wait(bar_s, j & 1);
-    tc_fence_after();
-    GX_ATTN_STAMP(p, 4 + 5 * j);
-    const int c0 = cq * 32;
-    const int qg0 = j * kTcQ + c0;
-    uint32_t ppd[16], pds[16];
-    {
-      const bool full = qg0 + 32 <= s && kt * 128 + 128 <= s;  // no tail masking needed
-      uint32_t sv[32], dv[32];
-      tmem_ld32(trow + c0, sv);
-      tmem_ld32(trow + 128 + c0, dv);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i4 = 0; i4 < 8; ++i4) {
-        const float4 l4 = *reinterpret_cast<const float4*>(sLse + qg0 + 4 * i4);
-        const float4 d4 = *reinterpret_cast<const float4*>(sD + c0 + 4 * i4);
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dd[4] = {d4.x, d4.y, d4.z, d4.w};
-        float pd4[4], ds4[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int i = 4 * i4 + t;
-          const int qg = qg0 + i;
-          const bool valid = full || ((qg < s) && (key < s));
-          const float pr = valid ? ex2_ftz(__uint_as_float(sv[i]) * c2 - lv[t]) : 0.f;
-          float f = 1.f;  // dropout factor: inv_keep or 0
-          if (thr != 0u)
-            f = valid && ((sMask[(qg * 2 + kbl) * 4 + mt] >> mbit) & 1u) != 0u ? inv_keep : 0.f;
-          pd4[t] = pr * f;
-          ds4[t] = pr * (__uint_as_float(dv[i]) * f - dd[t]);
-        }
-        ppd[2 * i4] = pack_bf16(pd4[0], pd4[1]);
-        ppd[2 * i4 + 1] = pack_bf16(pd4[2], pd4[3]);
-        pds[2 * i4] = pack_bf16(ds4[0], ds4[1]);
-        pds[2 * i4 + 1] = pack_bf16(ds4[2], ds4[3]);
-      }
-    }
-    GX_ATTN_STAMP(p, 5 + 5 * j);
-    if (j > 0) {  // chunk j-1's gradient MMAs: done reading Pd / dS; its dQ leaves TMEM
-      mbar_wait(bar_mm, (j - 1) & 1);
-      tc_fence_after();
-      store_dq(j - 1);
-      // chunk j-1's buffer is free: prefetch chunk j + 2 into it (chunks 0-2 came with the
-      // prologue)
-      if (warp == 0) {
-        if (lane == 0 && j + 2 < nq && j + 2 > 2) load_chunk(j + 2);
-        __syncwarp();
-      }
-    }
-    GX_ATTN_STAMP(p, 6 + 5 * j);
-    {
-      const uint32_t rowoff = static_cast<uint32_t>((cq >> 1) * 16384 + kr * 128);
-      const int chunk0 = (cq & 1) * 4;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t sw = static_cast<uint32_t>((chunk0 + i) ^ (kr & 7)) << 4;
-        st_shared_v4_tc(sb + BL::kPd + rowoff + sw, ppd[4 * i], ppd[4 * i + 1], ppd[4 * i + 2],
-                        ppd[4 * i + 3]);
-        st_shared_v4_tc(sb + BL::kDS + rowoff + sw, pds[4 * i], pds[4 * i + 1], pds[4 * i + 2],
-                        pds[4 * i + 3]);
-      }
-    }
-    fence_proxy_async_smem_tc();
-    tc_fence_before();
-    named_sync(1, kBwdThreads);  // Pd / dS(j) complete; S / dPd and dQ TMEM columns free
-    if (warp == 0) {  // warp-uniform: lane 0 issues, the rest wait here
-      if (lane == 0) {
+      for (int j = 0; j < nq; ++j) {
+        mbar_wait(bar_pds, j & 1);  // Pd / dS(j) in smem; S / dPd(j) and dQ(j-1) out of TMEM
         tc_fence_after();
-        if (j + 1 < nq) issue_s(j + 1);  // scores of the next chunk first ...
+        if (j + 1 < nq) issue_s(j + 1);  // next scores first ...
+        if (j >= 1) {  // chunk j-1's gradients (at most one bar_mm phase is ever pending here)
+          mbar_wait(bar_mm, (j - 1) & 1);
+          if (j + 2 < nq) load_chunk(j + 2);  // ... its Q / dO buffer takes chunk j + 2
+        }
         issue_grads(j);                   // ... then this chunk's gradient products
       }
-      __syncwarp();
     }
-    GX_ATTN_STAMP(p, 7 + 5 * j);
-    if (j + 1 < nq) compute_d(j + 1);  // sD(j) was last read before the barrier above
-    GX_ATTN_STAMP(p, 8 + 5 * j);
-    named_sync(1, kBwdThreads);        // sD(j+1) visible
-  }
-  mbar_wait(bar_mm, (nq - 1) & 1);
-  tc_fence_after();
-  store_dq(nq - 1);
-  // dK (x scale), dV -> bf16 rows of dqkv
-  {
-    uint32_t dvv[16], dkv[16];
-    tmem_ld16(trow + 256 + cq * 16, dvv);
-    tmem_ld16(trow + 320 + cq * 16, dkv);
-    tmem_ld_wait();
-    if (key < s) {
-      auto* dq = static_cast<__nv_bfloat16*>(p.dqkv);
-      __nv_bfloat16* rowp = dq + (static_cast<int64_t>(row0) + key) * p.ld_qkv;
-      uint4* dvp = reinterpret_cast<uint4*>(rowp + (2 * H + h) * kTcHD + cq * 16);
-      uint4* dkp = reinterpret_cast<uint4*>(rowp + (H + h) * kTcHD + cq * 16);
-      const float sc = p.scale;
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------ softmax warps (0..15)
+    // D = rowsum(dO * O) of chunk j's 128 queries -> sD[j & 1] (dO from smem, O from global)
+    auto compute_d = [&](int j) {
+      const int bf = j % 3;
+      mbar_wait(&bar_ld[bf], (j / 3) & 1);
+      const int qi = threadIdx.x >> 2, part4 = threadIdx.x & 3;  // 4 threads per query row
+      const int q = j * kTcQ + qi;
+      const uint8_t* dob = smem + BL::kDO + bf * 16384 + qi * 128;
+      float acc = 0.f;
+      if (q < s) {
+        const uint4* og = reinterpret_cast<const uint4*>(
+            static_cast<const __nv_bfloat16*>(p.ctx) + (static_cast<int64_t>(row0) + q) * p.ld_ctx +
+            h * kTcHD + part4 * 16);
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        dvp[i] = make_uint4(pack_bf16(__uint_as_float(dvv[8 * i]), __uint_as_float(dvv[8 * i + 1])),
-                            pack_bf16(__uint_as_float(dvv[8 * i + 2]), __uint_as_float(dvv[8 * i + 3])),
-                            pack_bf16(__uint_as_float(dvv[8 * i + 4]), __uint_as_float(dvv[8 * i + 5])),
-                            pack_bf16(__uint_as_float(dvv[8 * i + 6]), __uint_as_float(dvv[8 * i + 7])));
-        dkp[i] = make_uint4(pack_bf16(__uint_as_float(dkv[8 * i]) * sc, __uint_as_float(dkv[8 * i + 1]) * sc),
-                            pack_bf16(__uint_as_float(dkv[8 * i + 2]) * sc, __uint_as_float(dkv[8 * i + 3]) * sc),
-                            pack_bf16(__uint_as_float(dkv[8 * i + 4]) * sc, __uint_as_float(dkv[8 * i + 5]) * sc),
-                            pack_bf16(__uint_as_float(dkv[8 * i + 6]) * sc, __uint_as_float(dkv[8 * i + 7]) * sc));
+        for (int c = 0; c < 2; ++c) {
+          const int cc = part4 * 2 + c;
+          const int sw = (cc ^ (qi & 7)) << 4;
+          const uint4 a = *reinterpret_cast<const uint4*>(dob + sw);
+          const uint4 o = og[c];
+          const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            acc += bf16_lo(aw[t]) * bf16_lo(ow[t]) + bf16_hi(aw[t]) * bf16_hi(ow[t]);
+        }
+      }
+      acc += __shfl_xor_sync(0xffffffff, acc, 1);
+      acc += __shfl_xor_sync(0xffffffff, acc, 2);
+      if (part4 == 0) sD[(j & 1) * kTcQ + qi] = acc;
+    };
+    // dQ_j partial (fp32) out of TMEM (lane = query row of the chunk, 16 columns per warp)
+    auto store_dq = [&](int j) {
+      uint32_t o[16];
+      tmem_ld16(trow + 384 + cq * 16, o);
+      tmem_ld_wait();
+      const int q = j * kTcQ + kr;
+      if (q < s) {
+        float4* dst = reinterpret_cast<float4*>(
+            part + ((static_cast<int64_t>(kt) * gridDim.y + bh) * s + q) * kTcHD + cq * 16);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
+                               __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
+      }
+    };
+    compute_d(0);
+    named_sync(1, kBwdSoftmax);
+    GX_ATTN_STAMP(p, 2);
+    for (int j = 0; j < nq; ++j) {
+      mbar_wait(bar_s, j & 1);
+      tc_fence_after();
+      GX_ATTN_STAMP(p, 4 + 5 * j);
+      const int c0 = cq * 32;
+      const int qg0 = j * kTcQ + c0;
+      const float* sDj = sD + (j & 1) * kTcQ;
+      uint32_t ppd[16], pds[16];
+      {
+        const bool full = qg0 + 32 <= s && kt * 128 + 128 <= s;  // no tail masking needed
+        uint32_t sv[32], dv[32];
+        tmem_ld32(trow + c0, sv);
+        tmem_ld32(trow + 128 + c0, dv);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i4 = 0; i4 < 8; ++i4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(sLse + qg0 + 4 * i4);
+          const float4 d4 = *reinterpret_cast<const float4*>(sDj + c0 + 4 * i4);
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dd[4] = {d4.x, d4.y, d4.z, d4.w};
+          float pd4[4], ds4[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int i = 4 * i4 + t;
+            const int qg = qg0 + i;
+            const bool valid = full || ((qg < s) && (key < s));
+            const float pr = valid ? ex2_ftz(__uint_as_float(sv[i]) * c2 - lv[t]) : 0.f;
+            float f = 1.f;  // dropout factor: inv_keep or 0
+            if (thr != 0u)
+              f = valid && ((sMask[(qg * 2 + kbl) * 4 + mt] >> mbit) & 1u) != 0u ? inv_keep : 0.f;
+            pd4[t] = pr * f;
+            ds4[t] = pr * (__uint_as_float(dv[i]) * f - dd[t]);
+          }
+          ppd[2 * i4] = pack_bf16(pd4[0], pd4[1]);
+          ppd[2 * i4 + 1] = pack_bf16(pd4[2], pd4[3]);
+          pds[2 * i4] = pack_bf16(ds4[0], ds4[1]);
+          pds[2 * i4 + 1] = pack_bf16(ds4[2], ds4[3]);
+        }
+      }
+      GX_ATTN_STAMP(p, 5 + 5 * j);
+      if (j > 0) {  // chunk j-1's gradient MMAs: done reading Pd / dS; its dQ leaves TMEM
+        mbar_wait(bar_mm, (j - 1) & 1);
+        tc_fence_after();
+        store_dq(j - 1);
+      }
+      GX_ATTN_STAMP(p, 6 + 5 * j);
+      {
+        const uint32_t rowoff = static_cast<uint32_t>((cq >> 1) * 16384 + kr * 128);
+        const int chunk0 = (cq & 1) * 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t sw = static_cast<uint32_t>((chunk0 + i) ^ (kr & 7)) << 4;
+          st_shared_v4_tc(sb + BL::kPd + rowoff + sw, ppd[4 * i], ppd[4 * i + 1], ppd[4 * i + 2],
+                          ppd[4 * i + 3]);
+          st_shared_v4_tc(sb + BL::kDS + rowoff + sw, pds[4 * i], pds[4 * i + 1], pds[4 * i + 2],
+                          pds[4 * i + 3]);
+        }
+      }
+      fence_proxy_async_smem_tc();
+      tc_fence_before();
+      mbar_arrive(bar_pds);  // the MMA warp may issue S(j+1) and the gradients of j
+      GX_ATTN_STAMP(p, 7 + 5 * j);
+      // sD is double-buffered: sD[(j+1) & 1] was last read in chunk j-1, before every softmax
+      // warp passed the barrier that ended chunk j-1
+      if (j + 1 < nq) compute_d(j + 1);
+      named_sync(1, kBwdSoftmax);  // sD(j+1) visible
+      GX_ATTN_STAMP(p, 8 + 5 * j);
+    }
+    mbar_wait(bar_mm, (nq - 1) & 1);
+    tc_fence_after();
+    store_dq(nq - 1);
+    // dK (x scale), dV -> bf16 rows of dqkv
+    {
+      uint32_t dvv[16], dkv[16];
+      tmem_ld16(trow + 256 + cq * 16, dvv);
+      tmem_ld16(trow + 320 + cq * 16, dkv);
+      tmem_ld_wait();
+      if (key < s) {
+        auto* dq = static_cast<__nv_bfloat16*>(p.dqkv);
+        __nv_bfloat16* rowp = dq + (static_cast<int64_t>(row0) + key) * p.ld_qkv;
+        uint4* dvp = reinterpret_cast<uint4*>(rowp + (2 * H + h) * kTcHD + cq * 16);
+        uint4* dkp = reinterpret_cast<uint4*>(rowp + (H + h) * kTcHD + cq * 16);
+        const float sc = p.scale;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          dvp[i] = make_uint4(pack_bf16(__uint_as_float(dvv[8 * i]), __uint_as_float(dvv[8 * i + 1])),
+                              pack_bf16(__uint_as_float(dvv[8 * i + 2]), __uint_as_float(dvv[8 * i + 3])),
+                              pack_bf16(__uint_as_float(dvv[8 * i + 4]), __uint_as_float(dvv[8 * i + 5])),
+                              pack_bf16(__uint_as_float(dvv[8 * i + 6]), __uint_as_float(dvv[8 * i + 7])));
+          dkp[i] = make_uint4(pack_bf16(__uint_as_float(dkv[8 * i]) * sc, __uint_as_float(dkv[8 * i + 1]) * sc),
+                              pack_bf16(__uint_as_float(dkv[8 * i + 2]) * sc, __uint_as_float(dkv[8 * i + 3]) * sc),
+                              pack_bf16(__uint_as_float(dkv[8 * i + 4]) * sc, __uint_as_float(dkv[8 * i + 5]) * sc),
+                              pack_bf16(__uint_as_float(dkv[8 * i + 6]) * sc, __uint_as_float(dkv[8 * i + 7]) * sc));
+        }
       }
     }
   }

@@ -140,7 +140,8 @@ def attention_mask_buffer(batch, seq, heads, device):
                        dtype=torch.int16)
 
 
-def attention_fwd(qkv, batch, seq, heads, head_dim, p=0.0, seed=0, site=0, mask=None, **kw):
+def attention_fwd(qkv, batch, seq, heads, head_dim, p=0.0, seed=0, site=0, mask=None, trace=None,
+                  **kw):
     """Returns (ctx, lse, mask); mask (keep bits) feeds attention_bwd when p > 0."""
     import torch
     ctx = torch.empty(batch * seq, heads * head_dim, device=qkv.device, dtype=torch.bfloat16)
@@ -149,6 +150,7 @@ def attention_fwd(qkv, batch, seq, heads, head_dim, p=0.0, seed=0, site=0, mask=
         mask = attention_mask_buffer(batch, seq, heads, qkv.device)
     a = _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, **kw)
     a.ctx, a.ld_ctx, a.lse, a.mask = _ptr(ctx), ctx.stride(0), _ptr(lse), _ptr(mask)
+    a.trace = _ptr(trace)
     _lib.check(_lib.lib().gx_k_attention_fwd(ctypes.addressof(a), _lib.stream_ptr()))
     return ctx, lse, mask
 

@@ -27,3 +27,14 @@ for i, n in sorted(names.items()):
     if len(col):
         out[n] = round(float((col - t0).median()) / 1000, 2)
 print(json.dumps(out))
+
+# forward: stamps 0 entry, 1 pdl, 2 S ready, 3 row max exchanged, 4 P + sums done, 5 O ready
+nq = (s + 127) // 128
+trf = torch.zeros(nq * B * H * 32, dtype=torch.int64, device=dev)
+for i in range(4):
+    K.attention_fwd(qkv, B, s, H, d, p=0.1, seed=1, trace=trf if i == 3 else None)
+torch.cuda.synchronize()
+t = trf.view(-1, 32).cpu().double()
+t0 = t[:, 0][t[:, 0] > 0].min()
+print(json.dumps({n: round(float((t[:, i] - t0).median()) / 1000, 2) for i, n in
+                  enumerate(["entry", "pdl", "s_ready", "max_done", "p_done", "o_ready"])}))
