@@ -29,7 +29,10 @@ HDRS     := $(wildcard include/*.h include/parplan/*.h $(CSRC)/kernels/*.cuh $(C
 
 LIB      := $(PKG)/libgx.so
 
-all: $(LIB)
+CLI      := $(PKG)/parplan
+CLI_OBJS := $(BUILD)/tools/parplan_cli.o $(filter-out %plan_capi.o,$(filter $(BUILD)/parplan/%,$(CC_OBJS)))
+
+all: $(LIB) $(CLI)
 
 $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(dir $@)
@@ -43,10 +46,15 @@ $(LIB): $(CU_OBJS) $(CC_OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xlinker -rpath=$(NCCL_DIR)/lib \
 	    -L$(NCCL_DIR)/lib -l:libnccl.so.2 -lpthread
 
+# The `parplan` command line (reference proj/tools/parplan_main.cc): links the planner objects
+# statically and dlopens libgx.so (next to it) only for `run` / `profile`.
+$(CLI): $(CLI_OBJS)
+	$(CXX) -o $@ $^ -ldl -lpthread
+
 oracle:
 	$(MAKE) -C oracle
 
 clean:
-	rm -rf $(BUILD) $(LIB)
+	rm -rf $(BUILD) $(LIB) $(CLI)
 
 .PHONY: all oracle clean

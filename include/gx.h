@@ -118,7 +118,7 @@ GX_API const char* gx_plan_last_error(void);
  *    "world_size": N, "local_ranks": [...],            (default: all ranks -> sim mode)
  *    "comm": "sim" | "nccl", "nccl_id_hex": "<256 hex chars>" (nccl mode),
  *    "dropout_attn": p, "dropout_hidden": p, "seed": s, "optimizer": true,
- *    "lr", "beta1", "beta2", "eps", "weight_decay"}
+ *    "lr", "beta1", "beta2", "eps", "weight_decay", "device": cuda ordinal (optional)}
  * Parameters cross the boundary in the canonical unsharded fp32 order
  * ln1_g ln1_b ln2_g ln2_b b_qkv b_o b_1 b_2 w_qkv w_o w_1 w_2 (row-major, [out][in]); the
  * executor slices each rank's TP slice and SDP shard.  Batches are global bf16
@@ -135,6 +135,9 @@ GX_API int gx_exec_load_batch_device(gx_exec* ex, const void* x_dev, const void*
  * flags bit 0: replay as a CUDA graph (captured on first use); bit 1: instrumented run that
  * brackets every launch with CUDA events (read back with gx_exec_profile_report). */
 GX_API int gx_exec_run(gx_exec* ex, int flags);
+/* `warmup` untimed runs, then `steps` runs timed with CUDA events on the executor's stream;
+ * *ms_per_run = device time / steps (the parplan CLI's `run` and `profile`). */
+GX_API int gx_exec_time(gx_exec* ex, int flags, int warmup, int steps, double* ms_per_run);
 /* Per-category device time / launches / algorithmic flops+bytes of the last instrumented
  * run, plus per-GEMM-launch (ms, flops) pairs: the per-strategy profiler's raw data. */
 GX_API int gx_exec_profile_report(gx_exec* ex, char* out, size_t cap, size_t* needed);

@@ -21,8 +21,10 @@ extern "C" {
 int gx_exec_create(const char* config_json, gx_exec** out) {
   if (config_json == nullptr || out == nullptr) return bad("exec_create: NULL argument");
   std::string err;
-  auto impl = gx::create_executor(config_json, &err);
+  int code = gx::kOk;
+  auto impl = gx::create_executor(config_json, &err, &code);
   if (!impl) {
+    if (code == gx::kErrInfeasible) return gx::set_error(code, err.c_str());  // memory cap
     const bool nccl = err.find("nccl") != std::string::npos;
     const bool cuda = err.find("CUDA") != std::string::npos || err.find("cuda") != std::string::npos ||
                       err.find("memory") != std::string::npos;
@@ -60,6 +62,37 @@ int gx_exec_load_batch_device(gx_exec* ex, const void* x, const void* t) {
 int gx_exec_run(gx_exec* ex, int flags) {
   if (ex == nullptr) return bad("exec: NULL handle");
   return ex->impl->run2((flags & 1) != 0, (flags & 2) != 0);
+}
+
+int gx_exec_time(gx_exec* ex, int flags, int warmup, int steps, double* ms_per_run) {
+  if (ex == nullptr || ms_per_run == nullptr) return bad("exec_time: NULL argument");
+  if (steps <= 0 || warmup < 0) return bad("exec_time: steps must be > 0 and warmup >= 0");
+  for (int i = 0; i < warmup; ++i) {
+    const int rc = gx_exec_run(ex, flags);
+    if (rc != gx::kOk) return rc;
+  }
+  auto st = static_cast<cudaStream_t>(ex->impl->stream());
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) {
+    cudaGetLastError();
+    return gx::set_error(gx::kErrCuda, "exec_time: cudaEventCreate failed");
+  }
+  int rc = gx::kOk;
+  if (cudaStreamSynchronize(st) != cudaSuccess) rc = gx::check_launch("exec_time warm-up");
+  if (rc == gx::kOk) {
+    cudaEventRecord(a, st);
+    for (int i = 0; i < steps && rc == gx::kOk; ++i) rc = gx_exec_run(ex, flags);
+    cudaEventRecord(b, st);
+  }
+  float ms = 0.f;
+  if (rc == gx::kOk) {
+    if (cudaEventSynchronize(b) != cudaSuccess || cudaEventElapsedTime(&ms, a, b) != cudaSuccess)
+      rc = gx::set_error(gx::kErrCuda, "exec_time: event timing failed");
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (rc == gx::kOk) *ms_per_run = static_cast<double>(ms) / steps;
+  return rc;
 }
 
 int gx_exec_profile_report(gx_exec* ex, char* out, size_t cap, size_t* needed) {

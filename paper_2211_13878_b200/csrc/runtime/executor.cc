@@ -524,6 +524,15 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     model_ = cfg.at("model");
     world_ = cfg.at("world_size").get<int>();
     const std::string comm_kind = cfg.value("comm", std::string("sim"));
+    // one process per GPU without torch (the parplan CLI): the caller names its device
+    if (cfg.contains("device") && comm_kind != "dryrun") {
+      const int dev = cfg.at("device").get<int>();
+      if (cudaSetDevice(dev) != cudaSuccess) {
+        cudaGetLastError();
+        *err = "executor: cannot select CUDA device " + std::to_string(dev);
+        return kErrCuda;
+      }
+    }
     sim_ = comm_kind == "sim" || comm_kind == "dryrun";
     dry_run_ = comm_kind == "dryrun";
     p_attn_ = cfg.value("dropout_attn", 0.0f);
@@ -2114,16 +2123,22 @@ std::string ExecutorImpl::info() const {
 
 }  // namespace
 
-std::unique_ptr<Executor> create_executor(const std::string& config_json, std::string* err) {
+std::unique_ptr<Executor> create_executor(const std::string& config_json, std::string* err,
+                                          int* code) {
   json cfg;
   try {
     cfg = json::parse(config_json);
   } catch (const std::exception& e) {
     *err = std::string("executor: bad config json: ") + e.what();
+    if (code != nullptr) *code = kErrConfig;
     return nullptr;
   }
   auto ex = std::make_unique<ExecutorImpl>();
-  if (ex->init(cfg, err) != kOk) return nullptr;
+  const int rc = ex->init(cfg, err);
+  if (rc != kOk) {
+    if (code != nullptr) *code = rc;
+    return nullptr;
+  }
   return ex;
 }
 

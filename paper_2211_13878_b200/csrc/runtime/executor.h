@@ -52,7 +52,9 @@ Layout make_layout(const Shape& s, int tp, int sdp);
 int64_t canonical_size(const Shape& s);
 
 class Executor;
-std::unique_ptr<Executor> create_executor(const std::string& config_json, std::string* err);
+// On failure *err holds the message and *code (when non-null) the gx error code.
+std::unique_ptr<Executor> create_executor(const std::string& config_json, std::string* err,
+                                          int* code = nullptr);
 
 class Executor {
  public:

@@ -191,8 +191,9 @@ def test_memory_cap_enforced_and_reported(cuda):
     used = info["device_bytes"]
     assert used > 0 and "plan_estimate_bytes" in info
     ex.close()
-    with pytest.raises(_lib.GxError):
+    with pytest.raises(_lib.GxError) as ei:
         gxe.PlanExecutor(plan, model, 1, memory_cap_bytes=used // 2)
+    assert ei.value.code == 2  # GX_ERR_INFEASIBLE, like the planner's over-budget outcome
     ok = gxe.PlanExecutor(plan, model, 1, memory_cap_bytes=used + (1 << 20))
     assert ok.info()["ranks"][0]["memory_cap_bytes"] == used + (1 << 20)
     ok.close()

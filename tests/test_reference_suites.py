@@ -38,3 +38,16 @@ def test_reference_suite_passes(built, suite, impl):
         assert r.stdout.count("PASS") == 9
     else:
         assert " 0 failed" in r.stdout
+
+
+def test_reference_cli_suite_passes_against_parplan_binary(built):
+    """proj/tests/cli_test.cc (13 tests: plan JSON schema and budget, exit codes 1/2,
+    enumerate counts, estimate CSV ratio, sweep, PLANNER_THREADS invariance, oracle-plan)
+    compiled with PARPLAN_CLI_PATH = this repo's paper_2211_13878_b200/parplan."""
+    r = subprocess.run(["make", "-s", "-C", ROOT, "paper_2211_13878_b200/parplan"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    r = subprocess.run([os.path.join(built, "cli_test_gx")], capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stdout[-4000:]
+    assert "13 tests, 0 failed" in r.stdout
