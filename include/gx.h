@@ -213,7 +213,8 @@ GX_API int gx_k_gemm_bf16(const void* a, int64_t lda, int a_mn_major, const void
  * log2 domain); bwd reads qkv, ctx, lse, dctx and writes dqkv (qkv layout) using the fp32
  * workspaces dq_accum ([ceil(seq/128)][batch*heads*seq*d]: per-key-tile dQ partials) and
  * dsum ([batch*heads*seq], zero-initialised once by the caller; left reset).  head_dim 64 and
- * seq <= 512 run on tcgen05/TMEM (attention_tc.cu), other shapes on mma.sync.  Dropout
+ * seq <= 512 run on tcgen05/TMEM (attention_tc.cu), head_dim 32/80/128 on mma.sync.  Windowed
+ * (Swin) attention is this call with batch = samples * windows and seq = window.  Dropout
  * element (q,k) of global (sample_offset+b, head_offset+h) follows csrc/kernels/attention.cu. */
 typedef struct gx_attention_args {
   int batch, seq, heads, head_dim;

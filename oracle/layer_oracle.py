@@ -85,6 +85,11 @@ class LayerShape:
     heads: int
     seq: int
     ffn: int
+    window: int = 0  # > 0: Swin-style windowed attention over window-major token groups
+
+    @property
+    def att_seq(self):
+        return self.window or self.seq
 
     @property
     def head_dim(self):
@@ -167,9 +172,12 @@ def _attn_mask(drop: Dropout, site: int, samples: int, heads: int, seq: int, sam
 
 def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
                   drop: Dropout = Dropout(), sample_offset: int = 0):
-    """x: [samples*seq, h] float64.  Returns (y, cache)."""
-    h, H, d, s = shape.hidden, shape.heads, shape.head_dim, shape.seq
-    n = x.shape[0] // s
+    """x: [samples*seq, h] float64.  Returns (y, cache).  Attention runs per (attention
+    sequence, head); an attention sequence is a sample, or one window of a sample (window
+    layers: tokens stored window-major, so a window is `window` consecutive rows)."""
+    h, H, d, s = shape.hidden, shape.heads, shape.head_dim, shape.att_seq
+    n = x.shape[0] // s                      # attention sequences
+    nw = shape.seq // s                      # per sample
     a, ln1 = _ln_fwd(x, P["ln1_g"], P["ln1_b"])
     qkv = a @ P["w_qkv"].T + P["b_qkv"]
     q = qkv[:, :h].reshape(n, s, H, d).transpose(0, 2, 1, 3)
@@ -179,20 +187,20 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
     sc = sc - sc.max(-1, keepdims=True)
     pr = np.exp(sc)
     pr = pr / pr.sum(-1, keepdims=True)
-    am = _attn_mask(drop, 3 * layer_id, n, H, s, sample_offset)
+    am = _attn_mask(drop, 3 * layer_id, n, H, s, sample_offset * nw)
     ka = dropout_scale(drop.p_attn)
     pd = pr * am * ka
     ctx4 = pd @ v
     ctx = ctx4.transpose(0, 2, 1, 3).reshape(n * s, h)
     o = ctx @ P["w_o"].T + P["b_o"]
-    m1 = _hidden_mask(drop, 3 * layer_id + 1, n * s, h, sample_offset * s)
+    m1 = _hidden_mask(drop, 3 * layer_id + 1, n * s, h, sample_offset * shape.seq)
     kh = dropout_scale(drop.p_hidden)
     x1 = x + o * m1 * kh
     c, ln2 = _ln_fwd(x1, P["ln2_g"], P["ln2_b"])
     pre = c @ P["w_1"].T + P["b_1"]
     g = _gelu(pre)
     z = g @ P["w_2"].T + P["b_2"]
-    m2 = _hidden_mask(drop, 3 * layer_id + 2, n * s, h, sample_offset * s)
+    m2 = _hidden_mask(drop, 3 * layer_id + 2, n * s, h, sample_offset * shape.seq)
     y = x1 + z * m2 * kh
     cache = dict(x=x, a=a, ln1=ln1, q=q, k=k, v=v, pr=pr, am=am, ka=ka, pd=pd, ctx=ctx, m1=m1,
                  kh=kh, x1=x1, c=c, ln2=ln2, pre=pre, g=g, m2=m2, n=n)
@@ -201,7 +209,7 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
 
 def layer_backward(P: dict, dy: np.ndarray, cache: dict, shape: LayerShape):
     """Returns (dx, grads dict with the same keys as P)."""
-    h, H, d, s = shape.hidden, shape.heads, shape.head_dim, shape.seq
+    h, H, d, s = shape.hidden, shape.heads, shape.head_dim, shape.att_seq
     n = cache["n"]
     G = {}
     dz = dy * cache["m2"] * cache["kh"]

@@ -546,10 +546,11 @@ int attention_fwd(const gx_attention_args& a, cudaStream_t st) {
   if (a.seq <= 0 || a.batch <= 0 || a.heads <= 0) return set_error(kErrConfig, "attention: empty");
   if (attention_tc_supported(a)) return attention_fwd_tc(a, st);
   switch (a.head_dim) {
+    case 32: return attention_fwd_impl<32>(a, st);
     case 64: return attention_fwd_impl<64>(a, st);
     case 80: return attention_fwd_impl<80>(a, st);
     case 128: return attention_fwd_impl<128>(a, st);
-    default: return set_error(kErrConfig, "attention: head_dim must be 64, 80 or 128");
+    default: return set_error(kErrConfig, "attention: head_dim must be 32, 64, 80 or 128");
   }
 }
 
@@ -557,10 +558,11 @@ int attention_bwd(const gx_attention_args& a, cudaStream_t st) {
   if (a.seq <= 0 || a.batch <= 0 || a.heads <= 0) return set_error(kErrConfig, "attention: empty");
   if (attention_tc_supported(a) && (a.ld_ctx % 8) == 0) return attention_bwd_tc(a, st);
   switch (a.head_dim) {
+    case 32: return attention_bwd_impl<32>(a, st);
     case 64: return attention_bwd_impl<64>(a, st);
     case 80: return attention_bwd_impl<80>(a, st);
     case 128: return attention_bwd_impl<128>(a, st);
-    default: return set_error(kErrConfig, "attention: head_dim must be 64, 80 or 128");
+    default: return set_error(kErrConfig, "attention: head_dim must be 32, 64, 80 or 128");
   }
 }
 

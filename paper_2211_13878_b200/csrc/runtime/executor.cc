@@ -597,8 +597,19 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
       s.seq = sh.at("seq").get<int>();
       s.ffn = sh.at("ffn").get<int>();
       const std::string kind = sh.value("kind", std::string("encoder"));
-      if (kind != "encoder") {
-        *err = "executor: layer kind '" + kind + "' not supported yet (encoder only)";
+      // "window": Swin-style windowed self-attention -- the sample's seq tokens are stored
+      // window-major (window w holds tokens [w*win, (w+1)*win)) and attention runs inside
+      // each window; everything else is the encoder layer.
+      if (kind == "encoder") {
+        s.win = s.seq;
+      } else if (kind == "window") {
+        s.win = sh.value("window", 49);
+        if (s.win <= 0 || s.seq % s.win != 0) {
+          *err = "executor: window layer needs seq to be a multiple of window";
+          return kErrConfig;
+        }
+      } else {
+        *err = "executor: layer kind '" + kind + "' not supported (encoder, window)";
         return kErrConfig;
       }
       if (s.hd * s.heads != s.h) {
@@ -828,7 +839,7 @@ int ExecutorImpl::allocate(RankCtx& r) {
       a.lse = A.a<float>(static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq);
       if (thr_attn_ != 0u)
         a.amask = A.a<uint16_t>(static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq *
-                                ((s.seq + 63) / 64) * 4);
+                                ((s.win + 63) / 64) * 4);
       a.mean1 = A.a<float>(rows);
       a.rstd1 = A.a<float>(rows);
       a.mean2 = A.a<float>(rows);
@@ -1120,13 +1131,13 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     e.bias = P + L.lay.bqkv.off;
     GX_TRY(gemm(A.ln1, h, false, P + L.lay.wqkv.off, h, false, rows, 3 * ht, h, e));
     gx_attention_args at{};
-    at.batch = A.samples;
-    at.seq = s.seq;
+    at.batch = A.samples * s.windows();  // one attention sequence per window
+    at.seq = s.win;
     at.heads = s.heads / t;
     at.head_dim = s.hd;
     at.heads_total = s.heads;
     at.head_offset = L.tr * (s.heads / t);
-    at.sample_offset = A.sample0;
+    at.sample_offset = A.sample0 * s.windows();
     at.scale = 1.f / std::sqrt(static_cast<float>(s.hd));
     at.qkv = A.qkv;
     at.ld_qkv = 3 * ht;
@@ -1140,7 +1151,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     at.seed_offset = r.seed_off;
     at.mask = A.amask;
     {
-      const double af = 4.0 * A.samples * (s.heads / t) * double(s.seq) * s.seq * s.hd;
+      const double af = 4.0 * A.samples * (s.heads / t) * double(s.seq) * s.win * s.hd;
       GX_TRY(timed(kAttnFwd, af, 2.0 * rows * 4 * ht, [&] { return attention_fwd(at, stream_); }));
     }
     gx_gemm_epilogue o = epi();
@@ -1406,13 +1417,13 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     GX_TRY(gemm(dout, h, false, P + L.lay.wo.off, ht, true, rows, ht, h, c));  // dout Wo
     if (fuse_adam) GX_TRY(wgrado());
     gx_attention_args at{};
-    at.batch = A.samples;
-    at.seq = s.seq;
+    at.batch = A.samples * s.windows();  // one attention sequence per window
+    at.seq = s.win;
     at.heads = s.heads / t;
     at.head_dim = s.hd;
     at.heads_total = s.heads;
     at.head_offset = L.tr * (s.heads / t);
-    at.sample_offset = A.sample0;
+    at.sample_offset = A.sample0 * s.windows();
     at.scale = 1.f / std::sqrt(static_cast<float>(s.hd));
     at.qkv = A.qkv;
     at.ld_qkv = 3 * ht;
@@ -1430,7 +1441,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     at.seed_offset = r.seed_off;
     at.mask = A.amask;
     {
-      const double af = 10.0 * A.samples * (s.heads / t) * double(s.seq) * s.seq * s.hd;
+      const double af = 10.0 * A.samples * (s.heads / t) * double(s.seq) * s.win * s.hd;
       GX_TRY(timed(kAttnBwd, af, 2.0 * rows * 8 * ht, [&] { return attention_bwd(at, stream_); }));
     }
     auto wgradq = [&] {

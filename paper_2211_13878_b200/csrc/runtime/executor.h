@@ -34,6 +34,8 @@ struct Deg {
 
 struct Shape {
   int h = 0, heads = 0, hd = 0, seq = 0, ffn = 0;
+  int win = 0;  // tokens per attention window (kind "window"); == seq for full attention
+  int windows() const { return seq / win; }
 };
 
 // Offsets (elements) of one layer's tensors inside its flat per-rank parameter buffer.

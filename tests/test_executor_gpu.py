@@ -35,7 +35,8 @@ def _small_model(L=4, h=256, heads=4, seq=64, ffn=512):
 
 def _run_case(plan, model, world, p_drop=0.0, seed=11, optimizer=False):
     shp = model["layers"][0]["shape"]
-    oshape = lo.LayerShape(shp["hidden"], shp["heads"], shp["seq"], shp["ffn"])
+    oshape = lo.LayerShape(shp["hidden"], shp["heads"], shp["seq"], shp["ffn"],
+                           shp.get("window", 0) if shp.get("kind") == "window" else 0)
     L = len(model["layers"])
     B = plan["batch_size"]
     rng = np.random.default_rng(seed)
@@ -197,3 +198,34 @@ def test_memory_cap_enforced_and_reported(cuda):
     ok = gxe.PlanExecutor(plan, model, 1, memory_cap_bytes=used + (1 << 20))
     assert ok.info()["ranks"][0]["memory_cap_bytes"] == used + (1 << 20)
     ok.close()
+
+
+def _window_model(L, h, heads, seq, window, ffn):
+    m = _small_model(L, h, heads, seq, ffn)
+    for layer in m["layers"]:
+        layer["shape"].update(kind="window", window=window)
+    return m
+
+
+WINDOW_CASES = [
+    # (world, strategies, batch, hidden, heads, seq, window): Swin-style 7x7 windows with
+    # head_dim 32 (mma.sync path), and 64-token windows at head_dim 64 (tcgen05 path)
+    (1, ["", ""], 2, 128, 4, 98, 49),
+    (4, ["dp:4", "tp:2,sdp:2"], 4, 128, 4, 196, 49),
+    (2, ["sdp:2", "tp:2"], 2, 256, 4, 128, 64),
+]
+
+
+@pytest.mark.parametrize("case", WINDOW_CASES, ids=lambda c: f"N{c[0]}-{'|'.join(s or 'serial' for s in c[1])}-w{c[6]}-hd{c[3] // c[4]}")
+@pytest.mark.parametrize("p_drop", [0.0, 0.1])
+def test_window_attention_layers(cuda, case, p_drop):
+    """kind "window": attention inside each `window`-token group of a sample (Swin W-MSA)."""
+    world, strategies, B, h, heads, seq, window = case
+    model = _window_model(len(strategies), h, heads, seq, window, 2 * h)
+    _check(_run_case(gxe.make_plan(strategies, B), model, world, p_drop))
+
+
+def test_window_layer_rejects_ragged_windows(cuda):
+    model = _window_model(1, 128, 4, 100, 49, 256)
+    with pytest.raises(Exception, match="multiple of window"):
+        gxe.PlanExecutor(gxe.make_plan([""], 2), model, 1)

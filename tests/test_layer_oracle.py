@@ -38,29 +38,30 @@ def test_dropout_rate():
 
 
 def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0):
-    h, H, d, s = shape.hidden, shape.heads, shape.head_dim, shape.seq
+    h, H, d, s = shape.hidden, shape.heads, shape.head_dim, shape.att_seq
     n = x.shape[0] // s
+    nw, S = shape.seq // s, shape.seq
     ln = lambda t, g, b: torch.nn.functional.layer_norm(t, (h,), g, b, 1e-5)  # noqa: E731
     a = ln(x, P["ln1_g"], P["ln1_b"])
     qkv = a @ P["w_qkv"].T + P["b_qkv"]
     q, k, v = (qkv[:, i * h:(i + 1) * h].reshape(n, s, H, d).transpose(1, 2) for i in range(3))
     pr = torch.softmax(q @ k.transpose(-1, -2) / math.sqrt(d), -1)
-    am = torch.from_numpy(lo._attn_mask(drop, 3 * layer_id, n, H, s, sample_offset)).double()
+    am = torch.from_numpy(lo._attn_mask(drop, 3 * layer_id, n, H, s, sample_offset * nw)).double()
     ka = lo.dropout_scale(drop.p_attn)
     ctx = (pr * am * ka @ v).transpose(1, 2).reshape(n * s, h)
     kh = lo.dropout_scale(drop.p_hidden)
-    m1 = torch.from_numpy(lo._hidden_mask(drop, 3 * layer_id + 1, n * s, h, sample_offset * s)).double()
+    m1 = torch.from_numpy(lo._hidden_mask(drop, 3 * layer_id + 1, n * s, h, sample_offset * S)).double()
     x1 = x + (ctx @ P["w_o"].T + P["b_o"]) * m1 * kh
     c = ln(x1, P["ln2_g"], P["ln2_b"])
     g = torch.nn.functional.gelu(c @ P["w_1"].T + P["b_1"])
-    m2 = torch.from_numpy(lo._hidden_mask(drop, 3 * layer_id + 2, n * s, h, sample_offset * s)).double()
+    m2 = torch.from_numpy(lo._hidden_mask(drop, 3 * layer_id + 2, n * s, h, sample_offset * S)).double()
     return x1 + (g @ P["w_2"].T + P["b_2"]) * m2 * kh
 
 
-@pytest.mark.parametrize("p", [0.0, 0.1])
-def test_oracle_matches_autograd(p):
+@pytest.mark.parametrize("p,window", [(0.0, 0), (0.1, 0), (0.1, 4)])
+def test_oracle_matches_autograd(p, window):
     rng = np.random.default_rng(0)
-    shape = lo.LayerShape(hidden=64, heads=4, seq=12, ffn=128)
+    shape = lo.LayerShape(hidden=64, heads=4, seq=12, ffn=128, window=window)
     P = lo.init_layer_params(shape, rng, std=0.1)
     x = rng.standard_normal((2 * shape.seq, shape.hidden))
     dy = rng.standard_normal(x.shape)
