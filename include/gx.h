@@ -278,6 +278,12 @@ GX_API int gx_k_adamw(void* master, const void* grad, void* m, void* v, void* bf
                       float lr, float beta1, float beta2, float eps, float weight_decay,
                       float bc1, float bc2, void* stream);
 /* fp32 -> bf16 */
+/* Swin patch merging between window-major token layouts (window side window_side, input
+ * grid 2*grid_out, channels c in): backward = 0 gathers [samples*4*grid_out^2][c] into
+ * [samples*grid_out^2][4c] (2x2 neighbours in (dy,dx) order (0,0) (1,0) (0,1) (1,1));
+ * backward = 1 scatters the merged gradient back.  c % 8 == 0. */
+GX_API int gx_k_patch_merge(const void* src, void* dst, int samples, int grid_out,
+                            int window_side, int channels, int backward, void* stream);
 GX_API int gx_k_cast_bf16(const void* src, void* dst, int64_t n, void* stream);
 
 /* Split-K GEMM: out_f32[M,N] += A * B^T, each of `splits` K-slices reduce-adding its fp32

@@ -15,6 +15,9 @@ Layer (h hidden, H heads of d, f ffn; x is [tokens, h], tokens = samples * seq):
     x1  = x + drop_h1(ctx Wo^T + bo)
     c   = LN2(x1)
     y   = x1 + drop_h2(gelu(c W1^T + b1) W2^T + b2)  (exact erf GeLU)
+Window layers (Swin W-MSA, shape.window > 0): tokens are stored window-major and attention
+runs per window of `window` consecutive tokens.  Patch-merging layers (shape.merge) first map
+their input [4*seq, h/2] to x = LN_m(gather_2x2(input)) W_m^T ([seq, h]; merge_rows).
 Dropout uses the Philox4x32-10 byte scheme of csrc/kernels/philox.cuh: one call
 philox({c lo, c hi, site lo, site hi}, {seed lo, seed hi}) yields 16 bytes; an element is
 kept iff its byte >= thr8 = round(p * 256), kept values scale by 256 / (256 - thr8).
@@ -86,6 +89,7 @@ class LayerShape:
     seq: int
     ffn: int
     window: int = 0  # > 0: Swin-style windowed attention over window-major token groups
+    merge: bool = False  # Swin patch merging at the input: [4*seq, hidden/2] -> [seq, hidden]
 
     @property
     def att_seq(self):
@@ -96,9 +100,33 @@ class LayerShape:
         return self.hidden // self.heads
 
 
+def merge_rows(seq: int, window: int) -> np.ndarray:
+    """Patch merging index (csrc/kernels/patch_merge.cu): [seq, 4] input rows (within a
+    sample of 4*seq tokens) gathered for each output token.  Tokens are window-major: token
+    (y, x) of a G-grid with windows of side ws is row ((y//ws)*(G//ws) + x//ws)*ws^2 +
+    (y%ws)*ws + x%ws; output (y, x) takes inputs (2y+dy, 2x+dx), (dy, dx) = (0,0) (1,0) (0,1)
+    (1,1)."""
+    g, ws = math.isqrt(seq), math.isqrt(window)
+    assert g * g == seq and ws * ws == window and g % ws == 0
+
+    def row(y, x, grid):
+        return ((y // ws) * (grid // ws) + x // ws) * ws * ws + (y % ws) * ws + x % ws
+
+    out = np.empty((seq, 4), dtype=np.int64)
+    for y in range(g):
+        for x in range(g):
+            t = row(y, x, g)
+            for q, (dy, dx) in enumerate(((0, 0), (1, 0), (0, 1), (1, 1))):
+                out[t, q] = row(2 * y + dy, 2 * x + dx, 2 * g)
+    return out
+
+
 def init_layer_params(shape: LayerShape, rng: np.random.Generator, std=0.02) -> dict:
     h, f = shape.hidden, shape.ffn
-    return {
+    merge = {} if not shape.merge else {
+        "mln_g": 1.0 + 0.1 * rng.standard_normal(2 * h), "mln_b": 0.1 * rng.standard_normal(2 * h),
+        "w_m": std * rng.standard_normal((h, 2 * h))}
+    return merge | {
         "ln1_g": 1.0 + 0.1 * rng.standard_normal(h), "ln1_b": 0.1 * rng.standard_normal(h),
         "w_qkv": std * rng.standard_normal((3 * h, h)), "b_qkv": 0.02 * rng.standard_normal(3 * h),
         "w_o": std * rng.standard_normal((h, h)), "b_o": 0.02 * rng.standard_normal(h),
@@ -176,6 +204,15 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
     sequence, head); an attention sequence is a sample, or one window of a sample (window
     layers: tokens stored window-major, so a window is `window` consecutive rows)."""
     h, H, d, s = shape.hidden, shape.heads, shape.head_dim, shape.att_seq
+    mcache = {}
+    if shape.merge:  # patch merging: gather 2x2 -> LN(2h) -> x = mln W_m^T
+        idx = merge_rows(shape.seq, shape.window)
+        ns = x.shape[0] // (4 * shape.seq)
+        rows_in = (np.arange(ns)[:, None, None] * 4 * shape.seq + idx[None]).reshape(-1, 4)
+        mg = x[rows_in].reshape(ns * shape.seq, 2 * h)
+        mln, lnm = _ln_fwd(mg, P["mln_g"], P["mln_b"])
+        mcache = dict(rows_in=rows_in, mln=mln, lnm=lnm, x_in_shape=x.shape)
+        x = mln @ P["w_m"].T
     n = x.shape[0] // s                      # attention sequences
     nw = shape.seq // s                      # per sample
     a, ln1 = _ln_fwd(x, P["ln1_g"], P["ln1_b"])
@@ -203,7 +240,7 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
     m2 = _hidden_mask(drop, 3 * layer_id + 2, n * s, h, sample_offset * shape.seq)
     y = x1 + z * m2 * kh
     cache = dict(x=x, a=a, ln1=ln1, q=q, k=k, v=v, pr=pr, am=am, ka=ka, pd=pd, ctx=ctx, m1=m1,
-                 kh=kh, x1=x1, c=c, ln2=ln2, pre=pre, g=g, m2=m2, n=n)
+                 kh=kh, x1=x1, c=c, ln2=ln2, pre=pre, g=g, m2=m2, n=n, **mcache)
     return y, cache
 
 
@@ -242,6 +279,13 @@ def layer_backward(P: dict, dy: np.ndarray, cache: dict, shape: LayerShape):
     da = dqkv @ P["w_qkv"]
     dx_ln, G["ln1_g"], G["ln1_b"] = _ln_bwd(da, cache["ln1"], P["ln1_g"])
     dx = dx1 + dx_ln
+    if shape.merge:
+        G["w_m"] = dx.T @ cache["mln"]
+        dmln = dx @ P["w_m"]
+        dmg, G["mln_g"], G["mln_b"] = _ln_bwd(dmln, cache["lnm"], P["mln_g"])
+        dxin = np.zeros(cache["x_in_shape"])
+        dxin[cache["rows_in"].ravel()] = dmg.reshape(-1, h // 2)
+        dx = dxin
     return dx, G
 
 
@@ -249,17 +293,18 @@ def model_step(params: list, x: np.ndarray, target: np.ndarray, shape: LayerShap
                drop: Dropout = Dropout(), sample_offset: int = 0, count=None):
     """Forward through all layers, MSE loss = sum((y-t)^2)/count, backward.
     Returns (loss, y, dx, grads per layer)."""
+    shapes = shape if isinstance(shape, (list, tuple)) else [shape] * len(params)
     caches = []
     hcur = x
     for l, P in enumerate(params):
-        hcur, c = layer_forward(P, hcur, shape, l, drop, sample_offset)
+        hcur, c = layer_forward(P, hcur, shapes[l], l, drop, sample_offset)
         caches.append(c)
     count = count if count is not None else hcur.size
     loss = float(((hcur - target) ** 2).sum() / count)
     dcur = 2.0 * (hcur - target) / count
     grads = [None] * len(params)
     for l in reversed(range(len(params))):
-        dcur, grads[l] = layer_backward(params[l], dcur, caches[l], shape)
+        dcur, grads[l] = layer_backward(params[l], dcur, caches[l], shapes[l])
     return loss, hcur, dcur, grads
 
 

@@ -71,7 +71,8 @@ def _declare(L: ctypes.CDLL) -> None:
     L.gx_k_gemm_bf16_splitk.restype = c_int
     for name in ("gx_k_attention_fwd", "gx_k_attention_bwd", "gx_k_layernorm_fwd",
                  "gx_k_layernorm_bwd", "gx_k_bias_dropout_add", "gx_k_dropout_bwd_colsum",
-                 "gx_k_colsum", "gx_k_mse_loss", "gx_k_adamw", "gx_k_cast_bf16"):
+                 "gx_k_colsum", "gx_k_mse_loss", "gx_k_adamw", "gx_k_cast_bf16",
+                 "gx_k_patch_merge"):
         getattr(L, name).restype = c_int
     vp = c_void_p
     L.gx_k_attention_fwd.argtypes = [vp, vp]
@@ -85,6 +86,7 @@ def _declare(L: ctypes.CDLL) -> None:
     L.gx_k_adamw.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_float,
                              c_float, c_float, c_float, c_float, c_float, c_float, c_void_p]
     L.gx_k_cast_bf16.argtypes = [c_void_p, c_void_p, c_int64, c_void_p]
+    L.gx_k_patch_merge.argtypes = [vp, vp, c_int, c_int, c_int, c_int, c_int, vp]
     L.gx_exec_create.argtypes = [c_char_p, POINTER(c_void_p)]
     L.gx_exec_destroy.argtypes = [vp]
     L.gx_exec_set_layer_params.argtypes = [vp, c_int, vp, c_int64]

@@ -110,3 +110,8 @@ extern "C" int gx_k_adamw(void* master, const void* grad, void* m, void* v, void
 extern "C" int gx_k_cast_bf16(const void* src, void* dst, int64_t n, void* stream) {
   return gx::cast_bf16(src, dst, n, S(stream));
 }
+extern "C" int gx_k_patch_merge(const void* src, void* dst, int samples, int grid_out,
+                                int window_side, int channels, int backward, void* stream) {
+  return gx::patch_merge(src, dst, samples, grid_out, window_side, channels, backward != 0,
+                         S(stream));
+}

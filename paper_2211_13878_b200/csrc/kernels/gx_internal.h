@@ -140,15 +140,22 @@ struct PtrPack {
   int n;
 };
 int sum_ptrs(const PtrPack& srcs, void* out, int64_t n, bool bf16, cudaStream_t st);
-// Flat per-rank parameter layout (slot order ln1g ln1b ln2g ln2b bqkv bo b1 b2 wqkv wo w1 w2).
+// Flat per-rank parameter layout (slot order ln1g ln1b ln2g ln2b bqkv bo b1 b2 wqkv wo w1 w2,
+// then the patch-merging mlng mlnb wm, empty unless the layer merges).
 struct InitLayout {
-  int64_t off[12], n[12];
+  int64_t off[15], n[15];
   int64_t h, f;
   int t, tr;
   int64_t lo;  // first flat element of the shard
 };
 int init_params(float* master, int64_t n, const InitLayout& L, uint64_t seed, uint64_t layer,
                 float std_dev, cudaStream_t st);
+// Swin patch merging between window-major token layouts (window side ws, grid side
+// 2*grid_out -> grid_out, c channels in): forward gathers the 2x2 neighbours of every output
+// token into [rows_out][4c] (order (0,0) (1,0) (0,1) (1,1) in (dy, dx)); backward scatters
+// [rows_out][4c] back to [4*rows_out][c] (a permutation: every input row written once).
+int patch_merge(const void* src, void* dst, int samples, int grid_out, int ws, int c,
+                bool backward, cudaStream_t st);
 int num_sms();
 
 }  // namespace gx

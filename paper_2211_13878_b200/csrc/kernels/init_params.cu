@@ -2,7 +2,7 @@
 // the device (no host traffic for multi-GB models).  Every value is a function of
 // (seed, layer, canonical index) only, so any TP/SDP sharding of the same model holds
 // bit-identical parameters: LayerNorm gains 1, biases and LayerNorm shifts 0, weights
-// N(0, std^2) by Box-Muller over the Philox stream.
+// N(0, std^2) by Box-Muller over the Philox stream (patch-merging parameters included).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -17,8 +17,9 @@ __device__ int64_t canon_of(const InitLayout& L, int64_t j) {
   const int64_t c_ln1g = 0, c_ln1b = h, c_ln2g = 2 * h, c_ln2b = 3 * h, c_bqkv = 4 * h,
                 c_bo = 7 * h, c_b1 = 8 * h, c_b2 = 8 * h + f, c_wqkv = 9 * h + f,
                 c_wo = c_wqkv + 3 * h * h, c_w1 = c_wo + h * h, c_w2 = c_w1 + f * h;
+  const int64_t c_m = c_w2 + h * f;  // patch merging (mln_g, mln_b, w_m), unsharded
   int s = -1;
-  for (int i = 0; i < 12; ++i)
+  for (int i = 0; i < 15; ++i)
     if (j >= L.off[i] && j < L.off[i] + L.n[i]) s = i;
   if (s < 0) return -1;
   const int64_t k = j - L.off[s];
@@ -34,7 +35,10 @@ __device__ int64_t canon_of(const InitLayout& L, int64_t j) {
     case 8: return c_wqkv + ((k / h) / ht * h + tr * ht + (k / h) % ht) * h + k % h;
     case 9: return c_wo + (k / ht) * h + tr * ht + k % ht;
     case 10: return c_w1 + (tr * ft + k / h) * h + k % h;
-    default: return c_w2 + (k / ft) * f + tr * ft + k % ft;
+    case 11: return c_w2 + (k / ft) * f + tr * ft + k % ft;
+    case 12: return c_m + k;
+    case 13: return c_m + 2 * h + k;
+    default: return c_m + 4 * h + k;
   }
 }
 
@@ -45,9 +49,12 @@ __global__ void init_params_kernel(float* __restrict__ master, int64_t n, InitLa
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t c = canon_of(L, L.lo + i);
     float v = 0.f;
+    const int64_t c_m = 9 * h + f + 4 * h * h + 2 * h * f;  // first merge element
     if (c >= 0) {
-      if (c < h || (c >= 2 * h && c < 3 * h)) {
+      if (c < h || (c >= 2 * h && c < 3 * h) || (c >= c_m && c < c_m + 2 * h)) {
         v = 1.f;  // LayerNorm gains
+      } else if (c >= c_m && c < c_m + 4 * h) {
+        v = 0.f;  // merge LayerNorm shift
       } else if (c >= 9 * h + f) {
         const Philox4 w = philox4x32_10(static_cast<uint32_t>(c), static_cast<uint32_t>(c >> 32),
                                         static_cast<uint32_t>(layer), 0x5eedu,

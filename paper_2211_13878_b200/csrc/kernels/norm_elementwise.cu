@@ -2,7 +2,7 @@
 // dropout + residual, dropout backward with fused bias-gradient column sums, MSE loss,
 // AdamW, casts.  All are one pass over their operands with 16-byte vector accesses; grids
 // are sized in multiples of the SM count.  LayerNorm is one warp per row with the row held
-// in registers (h <= 4096), statistics reduced with warp shuffles.
+// in registers (h <= 8192), statistics reduced with warp shuffles.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -166,10 +166,10 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const uint4* __restr
 
 int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, void* mean,
                   void* rstd, int rows, int h, cudaStream_t st) {
-  if (h % 8 != 0 || h > 4096) return set_error(kErrConfig, "layernorm: h must be a multiple of 8, <= 4096");
+  if (h % 8 != 0 || h > 8192) return set_error(kErrConfig, "layernorm: h must be a multiple of 8, <= 8192");
   if (rows <= 0) return kOk;
   int nc = (h / 8 + 31) / 32;
-  nc = nc <= 6 ? nc : (nc <= 8 ? 8 : (nc <= 10 ? 10 : (nc <= 12 ? 12 : 16)));
+  nc = nc <= 6 ? nc : (nc <= 8 ? 8 : (nc <= 10 ? 10 : (nc <= 12 ? 12 : (nc <= 16 ? 16 : (nc <= 20 ? 20 : 32)))));
   const int grid = grid_for(rows, 8);
 #define GX_LN_FWD(N)                                                                         \
   case N:                                                                                    \
@@ -180,7 +180,7 @@ int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, v
     break;
   switch (nc) {
     GX_LN_FWD(1) GX_LN_FWD(2) GX_LN_FWD(3) GX_LN_FWD(4) GX_LN_FWD(5) GX_LN_FWD(6)
-    GX_LN_FWD(8) GX_LN_FWD(10) GX_LN_FWD(12) GX_LN_FWD(16)
+    GX_LN_FWD(8) GX_LN_FWD(10) GX_LN_FWD(12) GX_LN_FWD(16) GX_LN_FWD(20) GX_LN_FWD(32)
     default: break;
   }
 #undef GX_LN_FWD
@@ -200,14 +200,14 @@ int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, v
 // warps): every load of the row -- all split-K slices of dy included -- is issued at once,
 // which is what a latency-bound 512-row problem needs; the two row sums go through a
 // warp-shuffle + shared-memory reduction.
-template <bool kF32Dy, bool kDrop>
-__global__ void __launch_bounds__(512) layernorm_bwd_rows_kernel(
+template <bool kF32Dy, bool kDrop, int kMaxThreads = 512>
+__global__ void __launch_bounds__(kMaxThreads) layernorm_bwd_rows_kernel(
     const void* dy, const uint4* __restrict__ x, const float* __restrict__ mean,
     const float* __restrict__ rstd, const uint4* __restrict__ gamma, const uint4* __restrict__ dres,
     uint4* __restrict__ dx, uint4* __restrict__ dz, gx_dropout d, int rows, int h, int dy_slices,
     int64_t dy_stride, float* __restrict__ dy_fold) {
   pdl_enter();
-  __shared__ float red[2][16];
+  __shared__ float red[2][kMaxThreads / 32];
   const int chunks = h >> 3;
   const int ci = threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
@@ -387,16 +387,20 @@ int layernorm_bwd_rows(const void* dy, const void* x, const void* mean, const vo
                        const void* gamma, const void* dres, void* dx, int rows, int h,
                        cudaStream_t st, bool dy_f32, const gx_dropout* drop, void* dz,
                        int dy_slices, int64_t dy_slice_stride, float* dy_fold) {
-  if (h % 8 != 0 || h > 4096) return set_error(kErrConfig, "layernorm: h must be a multiple of 8, <= 4096");
+  if (h % 8 != 0 || h > 8192) return set_error(kErrConfig, "layernorm: h must be a multiple of 8, <= 8192");
   if (rows <= 0) return kOk;
   if (dy_slices < 1 || dy_slices > kMaxSplits || (dy_slices > 1 && !dy_f32))
     return set_error(kErrConfig, "layernorm_bwd: dy slices need fp32 dy");
   const bool fuse = drop != nullptr;
   if (fuse && dz == nullptr) return set_error(kErrConfig, "layernorm_bwd: fused dropout needs dz");
   const gx_dropout dd = fuse ? *drop : gx_dropout{};
-  const int threads = ((h / 8) + 31) / 32 * 32;  // <= 512 for h <= 4096
+  const int threads = ((h / 8) + 31) / 32 * 32;  // <= 512 for h <= 4096, <= 1024 for 8192
   auto* krows = dy_f32 ? (fuse ? layernorm_bwd_rows_kernel<true, true> : layernorm_bwd_rows_kernel<true, false>)
                        : (fuse ? layernorm_bwd_rows_kernel<false, true> : layernorm_bwd_rows_kernel<false, false>);
+  if (threads > 512) {  // wide rows (patch-merging LayerNorm over 4 x hidden/2 channels)
+    if (fuse || dy_f32) return set_error(kErrConfig, "layernorm_bwd: h > 4096 needs plain bf16 dy");
+    krows = layernorm_bwd_rows_kernel<false, false, 1024>;
+  }
   launch_k(krows, dim3(rows), dim3(threads), 0, st, dy, static_cast<const uint4*>(x),
            static_cast<const float*>(mean), static_cast<const float*>(rstd),
            static_cast<const uint4*>(gamma), static_cast<const uint4*>(dres),

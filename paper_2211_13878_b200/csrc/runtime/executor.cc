@@ -58,11 +58,15 @@ Layout make_layout(const Shape& s, int tp, int sdp) {
   put(L.bo, h);
   put(L.b1, f / tp);
   put(L.b2, h);
+  const int64_t mc = s.merge ? 2 * h : 0;  // merged channels (4 x h/2)
+  put(L.mlng, mc);
+  put(L.mlnb, mc);
   L.acc_end = off;
   put(L.wqkv, 3 * h / tp * h);
   put(L.wo, h * (h / tp));
   put(L.w1, f / tp * h);
   put(L.w2, h * (f / tp));
+  put(L.wm, s.merge ? h * mc : 0);  // replicated across TP ranks (identical gradients)
   const int64_t q = 64 * static_cast<int64_t>(sdp);
   L.total = (off + q - 1) / q * q;
   return L;
@@ -70,7 +74,8 @@ Layout make_layout(const Shape& s, int tp, int sdp) {
 
 int64_t canonical_size(const Shape& s) {
   const int64_t h = s.h, f = s.ffn;
-  return 4 * h + 3 * h + h + f + h + 3 * h * h + h * h + f * h + h * f;
+  const int64_t merge = s.merge ? 4 * h + 2 * h * h : 0;  // mln_g, mln_b (2h each), w_m [h][2h]
+  return 4 * h + 3 * h + h + f + h + 3 * h * h + h * h + f * h + h * f + merge;
 }
 
 namespace {
@@ -103,6 +108,10 @@ int64_t canon_index(const Shape& s, const Layout& L, int t, int tr, int64_t j) {
   if (in(L.w1, k)) return c_w1 + (tr * ft + k / h) * h + k % h;
   if (in(L.wo, k)) return c_wo + (k / ht) * h + tr * ht + k % ht;
   if (in(L.w2, k)) return c_w2 + (k / ft) * f + tr * ft + k % ft;
+  const int64_t c_m = c_w2 + h * f;  // patch merging, after w_2, unsharded by TP
+  if (in(L.mlng, k)) return c_m + k;
+  if (in(L.mlnb, k)) return c_m + 2 * h + k;
+  if (in(L.wm, k)) return c_m + 4 * h + k;
   return -1;
 }
 
@@ -156,6 +165,11 @@ struct Acts {
        *ln2 = nullptr, *pre = nullptr, *gel = nullptr, *y = nullptr;
   float *lse = nullptr, *mean1 = nullptr, *rstd1 = nullptr, *mean2 = nullptr, *rstd2 = nullptr;
   uint16_t* amask = nullptr;  // attention dropout keep bits (fwd -> bwd)
+  // patch merging (Shape::merge): xm = layer input [4*rows][h/2], mg = gathered [rows][2h],
+  // mln = LayerNorm(mg); x = mln Wm^T is then the residual-stream input of the block
+  bf16 *xm = nullptr, *mg = nullptr, *mln = nullptr;
+  float *meanm = nullptr, *rstdm = nullptr;
+  bf16* in() const { return xm != nullptr ? xm : x; }  // what the previous layer feeds
   bool ln1_ready = false;     // LN1 already produced by the previous layer's fused epilogue
   bool dz_ready = false;      // backward: dz / db2 already produced by the next layer's LN1 bwd
 };
@@ -193,6 +207,8 @@ struct RankCtx {
   bf16* gbuf[2] = {nullptr, nullptr};
   float *dq_acc = nullptr, *dsum = nullptr;
   float* ln_ws = nullptr;  // LayerNorm-backward block partials
+  float* ln_ws_m = nullptr;  // ... for the patch-merging LayerNorm (main stream only)
+  bf16 *dmg1 = nullptr, *dmg2 = nullptr;  // patch-merging backward scratch [rows][2h]
   float* cs_ws[2] = {nullptr, nullptr};  // column-sum workspaces: [0] main stream, [1] wgrad stream
   float* acc32 = nullptr;  // split-K fp32 slices [kMaxSplits][rows][h]
   bf16 *x_in = nullptr, *target = nullptr;  // [m micro-batches of this rank's rows][h]
@@ -270,6 +286,7 @@ class ExecutorImpl final : public Executor {
   // per-phase work
   int fwd_phase(RankCtx& r, int li, int mb, int phase);
   int bwd_phase(RankCtx& r, int li, int mb, int phase);
+  int merge_bwd(RankCtx& r, RankLayer& L, Acts& A, bf16* dX, const gx_gemm_epilogue& wm_ep);
   int sync_phase(RankCtx& r, int li, int phase);
   int xin_fwd(RankCtx& r, int li, int mb);
   int xin_bwd(RankCtx& r, int li, int mb);
@@ -612,6 +629,21 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
         *err = "executor: layer kind '" + kind + "' not supported (encoder, window)";
         return kErrConfig;
       }
+      s.merge = sh.value("merge", false);
+      if (s.merge) {
+        const int g = static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.seq))));
+        const int ws = static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.win))));
+        if (kind != "window" || g * g != s.seq || ws * ws != s.win || g % ws != 0 ||
+            (s.h / 2) % 8 != 0 || s.h % 2 != 0) {
+          *err = "executor: patch merging needs a window layer with a square token grid tiled by "
+                 "square windows and hidden/2 a multiple of 8";
+          return kErrConfig;
+        }
+        if (l == 0) {
+          *err = "executor: the first layer cannot merge patches (its input is the model input)";
+          return kErrConfig;
+        }
+      }
       if (s.hd * s.heads != s.h) {
         *err = "executor: heads * head_dim must equal hidden";
         return kErrConfig;
@@ -651,8 +683,10 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
         *err = "executor: more data replicas than samples per micro-batch";
         return kErrConfig;
       }
-      if (l > 0 && shape_[l].h != shape_[l - 1].h && stage_of_layer(l) == stage_of_layer(l - 1)) {
-        *err = "executor: hidden size changes between layers (patch merging) not supported yet";
+      if (l > 0 && (s.in_h() != shape_[l - 1].h || s.in_seq() != shape_[l - 1].seq)) {
+        *err = "executor: layer " + std::to_string(l) +
+               " input shape differs from the previous layer's output (only patch merging, "
+               "\"merge\": true, changes hidden and tokens between layers)";
         return kErrConfig;
       }
     }
@@ -793,7 +827,7 @@ int ExecutorImpl::build_groups() {
 int ExecutorImpl::allocate(RankCtx& r) {
   Arena& A = r.arena;
   A.set_cap(static_cast<size_t>(mem_cap_));
-  int64_t max_rows = 0, max_h = 0, max_f = 0, max_q = 0, max_c = 0, max_lse = 0;
+  int64_t max_rows = 0, max_h = 0, max_f = 0, max_q = 0, max_c = 0, max_lse = 0, max_m = 0;
   for (size_t li = 0; li < r.layers.size(); ++li) {
     RankLayer& L = r.layers[li];
     const Shape& s = L.sh;
@@ -819,15 +853,29 @@ int ExecutorImpl::allocate(RankCtx& r) {
       a.rows = a.samples * s.seq;
       const int64_t rows = a.rows;
       const int64_t h = s.h, ht = s.h / t, ft = s.ffn / t;
+      const int64_t in_rows = static_cast<int64_t>(a.samples) * s.in_seq();
       // layer input: alias into the previous layer's output where the relayout allows
+      bf16* xin = nullptr;
       if (L.xin == Xin::kSame) {
-        a.x = r.layers[li - 1].acts[mb].y;
+        xin = r.layers[li - 1].acts[mb].y;
       } else if (L.xin == Xin::kSlice) {
         const Acts& p = r.layers[li - 1].acts[mb];
-        a.x = p.y + (a.sample0 - p.sample0) * s.seq * h;
+        xin = p.y + (a.sample0 - p.sample0) * s.in_seq() * s.in_h();
       } else {
-        a.x = A.a<bf16>(rows * h);
+        xin = A.a<bf16>(in_rows * s.in_h());
       }
+      if (s.merge) {
+        a.xm = xin;
+        a.mg = A.a<bf16>(rows * 2 * h);
+        a.mln = A.a<bf16>(rows * 2 * h);
+        a.meanm = A.a<float>(rows);
+        a.rstdm = A.a<float>(rows);
+        a.x = A.a<bf16>(rows * h);
+        max_m = std::max(max_m, rows * 2 * h);
+      } else {
+        a.x = xin;
+      }
+      max_h = std::max(max_h, in_rows * s.in_h());  // gbuf also carries the input gradient
       a.ln1 = A.a<bf16>(rows * h);
       a.qkv = A.a<bf16>(rows * 3 * ht);
       a.ctx = A.a<bf16>(rows * ht);
@@ -875,6 +923,13 @@ int ExecutorImpl::allocate(RankCtx& r) {
     int64_t max_hdim = 0;
     for (const RankLayer& L : r.layers) max_hdim = std::max<int64_t>(max_hdim, L.sh.h);
     r.ln_ws = A.a<float>(layernorm_bwd_ws_floats(static_cast<int>(max_hdim)));
+    if (max_m > 0) {
+      r.ln_ws_m = A.a<float>(layernorm_bwd_ws_floats(static_cast<int>(2 * max_hdim)));
+      if (r.ln_ws_m != nullptr)
+        cudaMemset(r.ln_ws_m, 0, layernorm_bwd_ws_floats(static_cast<int>(2 * max_hdim)) * 4);
+      r.dmg1 = A.a<bf16>(max_m);
+      r.dmg2 = A.a<bf16>(max_m);
+    }
     int64_t max_cols = 0;
     for (const RankLayer& L : r.layers)
       max_cols = std::max<int64_t>({max_cols, L.sh.h, L.sh.ffn / L.d.tp, 3 * L.sh.h / L.d.tp});
@@ -1020,10 +1075,10 @@ int ExecutorImpl::init_params(uint64_t seed, float std_dev) {
   for (auto& r : ranks_) {
     for (RankLayer& L : r->layers) {
       InitLayout il{};
-      const Slot* slots[12] = {&L.lay.ln1g, &L.lay.ln1b, &L.lay.ln2g, &L.lay.ln2b, &L.lay.bqkv,
+      const Slot* slots[15] = {&L.lay.ln1g, &L.lay.ln1b, &L.lay.ln2g, &L.lay.ln2b, &L.lay.bqkv,
                                &L.lay.bo,   &L.lay.b1,   &L.lay.b2,   &L.lay.wqkv, &L.lay.wo,
-                               &L.lay.w1,   &L.lay.w2};
-      for (int i = 0; i < 12; ++i) {
+                               &L.lay.w1,   &L.lay.w2,   &L.lay.mlng, &L.lay.mlnb, &L.lay.wm};
+      for (int i = 0; i < 15; ++i) {
         il.off[i] = slots[i]->off;
         il.n[i] = slots[i]->n;
       }
@@ -1121,6 +1176,22 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
   if (rows == 0) return kOk;
   bool ln2_ready = false;
   if (phase == 0) {
+    if (s.merge) {  // Swin patch merging: gather 2x2 -> LayerNorm(2h) -> x = mln Wm^T
+      const int g = static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.seq))));
+      const int ws = static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.win))));
+      GX_TRY(timed(kElementwise, 0, 2.0 * rows * 2 * h * 2, [&] {
+        return patch_merge(A.xm, A.mg, A.samples, g, ws, h / 2, false, stream_);
+      }));
+      GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] {
+        return layernorm_fwd(A.mg, P + L.lay.mlng.off, P + L.lay.mlnb.off, A.mln, A.meanm,
+                             A.rstdm, rows, 2 * h, stream_);
+      }));
+      gx_gemm_epilogue e = epi();
+      e.out_kind = kOutBF16;
+      e.out = A.x;
+      e.ldo = h;
+      GX_TRY(gemm(A.mln, 2 * h, false, P + L.lay.wm.off, 2 * h, false, rows, h, 2 * h, e));
+    }
     if (!A.ln1_ready)
       GX_TRY(timed(kNorm, 0, 4.0 * rows * h, [&] { return layernorm_fwd(A.x, P + L.lay.ln1g.off, P + L.lay.ln1b.off, A.ln1, A.mean1, A.rstd1,
                            rows, h, stream_); }));
@@ -1512,8 +1583,35 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       return kOk;
     }));
     if (prev != nullptr) prev->dz_ready = true;
+    if (s.merge) GX_TRY(merge_bwd(r, L, A, dX, wgrad_ep(L.lay.wm, 2 * h)));
   }
   return kOk;
+}
+
+// Patch-merging backward (main stream, after LN1's backward left dL/dx in dX):
+// dmln = dX Wm, dWm = dX^T mln, LayerNorm(2h) backward, then the 2x2 scatter writes the input
+// gradient [4*rows][h/2] over dX (both readers of dX ran before it on this stream).
+int ExecutorImpl::merge_bwd(RankCtx& r, RankLayer& L, Acts& A, bf16* dX,
+                            const gx_gemm_epilogue& wm_ep) {
+  const Shape& s = L.sh;
+  const int rows = A.rows, h = s.h;
+  const bf16* P = L.pfull;
+  float* G = L.gfull;
+  gx_gemm_epilogue c = epi();
+  c.out_kind = kOutBF16;
+  c.out = r.dmg1;
+  c.ldo = 2 * h;
+  GX_TRY(gemm(dX, h, false, P + L.lay.wm.off, 2 * h, true, rows, 2 * h, h, c));  // dX Wm
+  GX_TRY(gemm(dX, h, true, A.mln, 2 * h, true, h, 2 * h, rows, wm_ep));          // dWm
+  GX_TRY(timed(kNorm, 0, 12.0 * rows * h, [&] {
+    return layernorm_bwd(r.dmg1, A.mg, A.meanm, A.rstdm, P + L.lay.mlng.off, nullptr, r.dmg2,
+                         G + L.lay.mlng.off, G + L.lay.mlnb.off, rows, 2 * h, r.ln_ws_m, stream_);
+  }));
+  const int g = static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.seq))));
+  const int ws = static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.win))));
+  return timed(kElementwise, 0, 2.0 * rows * 2 * h * 2, [&] {
+    return patch_merge(r.dmg2, dX, A.samples, g, ws, h / 2, true, stream_);
+  });
 }
 
 // Gradient synchronisation + optimizer after the layer's last backward micro-batch.
@@ -1635,9 +1733,9 @@ int ExecutorImpl::xin_fwd(RankCtx& r, int li, int mb) {
   for (int member : grp.ranks) {
     int64_t lo, hi;
     chunk(Pv.d, member % g_, mb, lo, hi);
-    counts.push_back(static_cast<size_t>((hi - lo) * L.sh.seq * L.sh.h));
+    counts.push_back(static_cast<size_t>((hi - lo) * L.sh.in_seq() * L.sh.in_h()));
   }
-  return c_all_gather(L.g_xin, r.rank, p.y, L.acts[mb].x, counts, DType::kBF16, stream_);
+  return c_all_gather(L.g_xin, r.rank, p.y, L.acts[mb].in(), counts, DType::kBF16, stream_);
 }
 
 // Backward relayout out of layer li: dX (gbuf[cur^1], layout li) -> dY of layer li-1 in
@@ -1647,7 +1745,7 @@ int ExecutorImpl::xin_bwd(RankCtx& r, int li, int mb) {
   const RankLayer& Pv = r.layers[li - 1];
   bf16* dX = r.gbuf[r.cur ^ 1];
   bf16* dYp = r.gbuf[r.cur];
-  const int64_t h = L.sh.h, seq = L.sh.seq;
+  const int64_t h = L.sh.in_h(), seq = L.sh.in_seq();  // the relayout moves layer li's input
   if (L.xin == Xin::kSame) {
     r.cur ^= 1;
     return kOk;
@@ -1714,14 +1812,15 @@ std::vector<ExecutorImpl::Xfer> ExecutorImpl::pp_plan(int stage, int idx, int mb
 int ExecutorImpl::pp_fwd(RankCtx& r, int mb, bool send) {
   const RankLayer& L = send ? r.layers.back() : r.layers.front();
   const Acts& my = L.acts[mb];
-  const int64_t hs = static_cast<int64_t>(L.sh.seq) * L.sh.h;
+  const int64_t hs = send ? static_cast<int64_t>(L.sh.seq) * L.sh.h
+                          : static_cast<int64_t>(L.sh.in_seq()) * L.sh.in_h();
   for (const Xfer& x : pp_plan(r.stage, r.idx, mb, send ? 0 : 1)) {
     const size_t bytes = static_cast<size_t>((x.hi - x.lo) * hs) * 2;
     const int64_t off = (x.lo - my.sample0) * hs;
     if (send) {
       GX_TRY(comm_->send(r.rank, x.peer, my.y + off, bytes, stream_));
     } else {
-      GX_TRY(comm_->recv(r.rank, x.peer, my.x + off, bytes, stream_));
+      GX_TRY(comm_->recv(r.rank, x.peer, my.in() + off, bytes, stream_));
     }
   }
   return kOk;
@@ -1732,7 +1831,8 @@ int ExecutorImpl::pp_fwd(RankCtx& r, int mb, bool send) {
 int ExecutorImpl::pp_bwd(RankCtx& r, int mb, bool send) {
   const RankLayer& L = send ? r.layers.front() : r.layers.back();
   const Acts& my = L.acts[mb];
-  const int64_t hs = static_cast<int64_t>(L.sh.seq) * L.sh.h;
+  const int64_t hs = send ? static_cast<int64_t>(L.sh.in_seq()) * L.sh.in_h()
+                          : static_cast<int64_t>(L.sh.seq) * L.sh.h;
   for (const Xfer& x : pp_plan(r.stage, r.idx, mb, send ? 2 : 3)) {
     const size_t bytes = static_cast<size_t>((x.hi - x.lo) * hs) * 2;
     const int64_t off = (x.lo - my.sample0) * hs;

@@ -36,6 +36,11 @@ struct Shape {
   int h = 0, heads = 0, hd = 0, seq = 0, ffn = 0;
   int win = 0;  // tokens per attention window (kind "window"); == seq for full attention
   int windows() const { return seq / win; }
+  // Swin patch merging at the layer input: the input is [4*seq, h/2] per sample (a grid of
+  // side 2G, window-major), 2x2 neighbours are concatenated, LayerNorm'd and projected to h.
+  bool merge = false;
+  int in_h() const { return merge ? h / 2 : h; }
+  int in_seq() const { return merge ? 4 * seq : seq; }
 };
 
 // Offsets (elements) of one layer's tensors inside its flat per-rank parameter buffer.
@@ -44,6 +49,7 @@ struct Slot {
 };
 struct Layout {
   Slot ln1g, ln1b, ln2g, ln2b, bqkv, bo, b1, b2, wqkv, wo, w1, w2;
+  Slot mlng, mlnb, wm;  // patch merging (empty unless Shape::merge): LN(2h) and [h][2h]
   int64_t acc_end = 0;  // [0, acc_end): params whose grads accumulate with atomics
   int64_t total = 0;    // padded to a multiple of 64 * sdp
   int64_t shard() const { return total; }

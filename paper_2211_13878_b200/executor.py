@@ -15,20 +15,23 @@ from . import _lib
 
 CANONICAL_ORDER = ("ln1_g", "ln1_b", "ln2_g", "ln2_b", "b_qkv", "b_o", "b_1", "b_2",
                    "w_qkv", "w_o", "w_1", "w_2")
+MERGE_ORDER = ("mln_g", "mln_b", "w_m")  # patch-merging layers only, after w_2
 
 
 def pack_canonical(P: dict) -> np.ndarray:
     """Layer parameter dict (oracle naming) -> canonical flat fp32 vector."""
-    return np.concatenate([np.asarray(P[k], dtype=np.float32).ravel() for k in CANONICAL_ORDER])
+    keys = CANONICAL_ORDER + (MERGE_ORDER if "w_m" in P else ())
+    return np.concatenate([np.asarray(P[k], dtype=np.float32).ravel() for k in keys])
 
 
-def unpack_canonical(flat: np.ndarray, hidden: int, ffn: int) -> dict:
+def unpack_canonical(flat: np.ndarray, hidden: int, ffn: int, merge: bool = False) -> dict:
     h, f = hidden, ffn
     shapes = {"ln1_g": (h,), "ln1_b": (h,), "ln2_g": (h,), "ln2_b": (h,), "b_qkv": (3 * h,),
               "b_o": (h,), "b_1": (f,), "b_2": (h,), "w_qkv": (3 * h, h), "w_o": (h, h),
-              "w_1": (f, h), "w_2": (h, f)}
+              "w_1": (f, h), "w_2": (h, f),
+              "mln_g": (2 * h,), "mln_b": (2 * h,), "w_m": (h, 2 * h)}
     out, off = {}, 0
-    for k in CANONICAL_ORDER:
+    for k in CANONICAL_ORDER + (MERGE_ORDER if merge else ()):
         n = int(np.prod(shapes[k]))
         out[k] = flat[off:off + n].reshape(shapes[k])
         off += n
@@ -104,7 +107,8 @@ class PlanExecutor:
         s = self.shapes[layer]
         n = ctypes.c_int64()
         _lib.lib().gx_exec_canonical_size(s["hidden"], s["ffn"], ctypes.byref(n))
-        return n.value
+        h = s["hidden"]
+        return n.value + (4 * h + 2 * h * h if s.get("merge") else 0)
 
     def set_layer_params(self, layer: int, P: dict):
         flat = np.ascontiguousarray(pack_canonical(P))
@@ -118,7 +122,7 @@ class PlanExecutor:
             self._h, layer, {"params": 0, "grads": 1, "bf16": 2}[what],
             out.ctypes.data_as(ctypes.c_void_p), n))
         s = self.shapes[layer]
-        return unpack_canonical(out, s["hidden"], s["ffn"])
+        return unpack_canonical(out, s["hidden"], s["ffn"], bool(s.get("merge")))
 
     @property
     def stream(self) -> int:

@@ -234,3 +234,16 @@ def adamw(p, g, m, v, out_bf16, lr, b1, b2, eps, wd, step):
         ctypes.c_float(b1), ctypes.c_float(b2), ctypes.c_float(eps), ctypes.c_float(wd),
         ctypes.c_float(1 - b1 ** step), ctypes.c_float(1 - b2 ** step),
         ctypes.c_void_p(_lib.stream_ptr())))
+
+
+def patch_merge(x, samples, grid_out, window_side, backward=False):
+    """Swin patch merging (gx_k_patch_merge): [samples*4*G^2, c] -> [samples*G^2, 4c], or the
+    scatter of a merged gradient back when backward=True."""
+    import torch
+    c = x.shape[1] // 4 if backward else x.shape[1]
+    rows_out = samples * grid_out * grid_out
+    out = torch.empty((4 * rows_out, c) if backward else (rows_out, 4 * c), dtype=x.dtype,
+                      device=x.device)
+    _lib.check(_lib.lib().gx_k_patch_merge(_ptr(x), _ptr(out), samples, grid_out, window_side,
+                                           c, int(backward), _lib.stream_ptr()))
+    return out

@@ -14,7 +14,10 @@ Planner numbers:
     SURVEY.md Appendix B (UniformModel of the paper's Table 2 totals).
 Executor shapes (not in the reference; chosen here): BERT-Huge h=1280 as 20 heads x 64,
 s=512, ffn 5120; BERT-base h=768, 12 x 64, s=128, ffn 3072; ViT-Huge h=1280, 16 x 80,
-s=257, ffn 5120; T5-Large encoder h=1024, 16 x 64, s=512, ffn 4096.
+s=257, ffn 5120; T5-Large encoder h=1024, 16 x 64, s=512, ffn 4096.  Swin-like (Swin-H at
+224 px, the fixture's 2/2/26/2 stages): hidden 320/640/1280/2560 as heads x 32, token grids
+56/28/14/7 stored window-major with 7x7 windows ("kind": "window", W-MSA), ffn 4h; the first
+layer of stages 2-4 starts with patch merging ("merge": true).
 """
 from __future__ import annotations
 
@@ -57,10 +60,15 @@ def _swin():
     ]
     layers = []
     for st, (n, h, p, a, t) in enumerate(spec):
+        grid = 56 >> st
         for i in range(n):
+            shape = _shape(h, h // 32, grid * grid, 4 * h, kind="window")
+            shape["window"] = 49
+            if st > 0 and i == 0:
+                shape["merge"] = True
             layers.append({"param_bytes": p, "activation_bytes_per_sample": a,
                            "fwd_time_per_sample_ms": t, "name": f"stage{st}.{i}",
-                           "shape": _shape(h, h // 32, 49, 4 * h, kind="window")})
+                           "shape": shape})
     return {"dtype_bytes": 4, "layers": layers}
 
 

@@ -33,19 +33,23 @@ def _small_model(L=4, h=256, heads=4, seq=64, ffn=512):
          "shape": dict(shape)} for _ in range(L)]}
 
 
+def _oshape(shp):
+    return lo.LayerShape(shp["hidden"], shp["heads"], shp["seq"], shp["ffn"],
+                         shp.get("window", 0) if shp.get("kind") == "window" else 0,
+                         bool(shp.get("merge", False)))
+
+
 def _run_case(plan, model, world, p_drop=0.0, seed=11, optimizer=False):
-    shp = model["layers"][0]["shape"]
-    oshape = lo.LayerShape(shp["hidden"], shp["heads"], shp["seq"], shp["ffn"],
-                           shp.get("window", 0) if shp.get("kind") == "window" else 0)
+    oshapes = [_oshape(layer["shape"]) for layer in model["layers"]]
+    oshape = oshapes[0]
     L = len(model["layers"])
     B = plan["batch_size"]
     rng = np.random.default_rng(seed)
-    params = [lo.init_layer_params(oshape, rng, std=0.05) for _ in range(L)]
+    params = [lo.init_layer_params(oshapes[l], rng, std=0.05) for l in range(L)]
     # round params to fp32 (what the executor stores) for the oracle
     params = [{k: v.astype(np.float32).astype(np.float64) for k, v in P.items()} for P in params]
-    rows = B * oshape.seq
-    x32 = rng.standard_normal((rows, oshape.hidden)).astype(np.float32)
-    t32 = rng.standard_normal((rows, oshape.hidden)).astype(np.float32)
+    x32 = rng.standard_normal((B * oshape.seq, oshape.hidden)).astype(np.float32)
+    t32 = rng.standard_normal((B * oshapes[-1].seq, oshapes[-1].hidden)).astype(np.float32)
     xb, tb = gxe.f32_to_bf16_bits(x32), gxe.f32_to_bf16_bits(t32)
     x = gxe.bf16_bits_to_f32(xb).astype(np.float64)
     t = gxe.bf16_bits_to_f32(tb).astype(np.float64)
@@ -55,7 +59,7 @@ def _run_case(plan, model, world, p_drop=0.0, seed=11, optimizer=False):
         ex.set_layer_params(l, params[l])
     loss = ex.step(xb, tb)
     drop = lo.Dropout(p_drop, p_drop, 77)
-    ref_loss, ref_y, ref_dx, ref_g = lo.model_step(params, x, t, oshape, drop)
+    ref_loss, ref_y, ref_dx, ref_g = lo.model_step(params, x, t, oshapes, drop)
     out = {"params0": params, "loss": (loss, ref_loss), "y": (ex.export_output("y"), ref_y),
            "dx": (ex.export_output("dx"), ref_dx), "grads": [], "ex": ex}
     for l in range(L):
@@ -229,3 +233,51 @@ def test_window_layer_rejects_ragged_windows(cuda):
     model = _window_model(1, 128, 4, 100, 49, 256)
     with pytest.raises(Exception, match="multiple of window"):
         gxe.PlanExecutor(gxe.make_plan([""], 2), model, 1)
+
+
+def _swin_like(h0=64, heads0=2, grid0=14, window=49, stages=(2, 2)):
+    """Window layers over a grid0 x grid0 token grid; each later stage starts with a
+    patch-merging layer (grid / 2, hidden x 2, heads x 2)."""
+    layers, h, heads, grid = [], h0, heads0, grid0
+    for st, n in enumerate(stages):
+        for i in range(n):
+            shape = {"hidden": h, "heads": heads, "head_dim": h // heads, "seq": grid * grid,
+                     "ffn": 2 * h, "kind": "window", "window": window}
+            if st > 0 and i == 0:
+                shape["merge"] = True
+            layers.append({"param_bytes": 1, "activation_bytes_per_sample": 1,
+                           "fwd_time_per_sample_ms": 0.1, "shape": shape})
+        h, heads, grid = 2 * h, 2 * heads, grid // 2
+    return {"dtype_bytes": 4, "layers": layers}
+
+
+SWIN_CASES = [
+    # (world, strategies, batch, pp, micro_batches, stage bounds)
+    (1, ["", "", "", ""], 2, 1, 1, None),
+    (4, ["dp:4", "sdp:4", "tp:2,sdp:2", "tp:2,dp:2"], 4, 1, 1, None),
+    (2, ["", "", "", ""], 2, 2, 2, [0, 2, 4]),      # the merging layer starts stage 1
+    (4, ["dp:2", "tp:2", "sdp:2", "dp:2"], 4, 2, 2, [0, 2, 4]),
+]
+
+
+@pytest.mark.parametrize("case", SWIN_CASES, ids=lambda c: f"N{c[0]}-{'|'.join(s or 'serial' for s in c[1])}-P{c[3]}")
+@pytest.mark.parametrize("p_drop", [0.0, 0.1])
+def test_swin_patch_merging_plans(cuda, case, p_drop):
+    """Swin-style stages: window attention + patch merging (hidden 64 -> 128, grid 14 -> 7)
+    under heterogeneous per-layer strategies, Slice-Gather relayouts and PP boundaries."""
+    world, strategies, B, P, m, bounds = case
+    plan = gxe.make_plan(strategies, B, P, m, bounds)
+    out = _run_case(plan, _swin_like(), world, p_drop)
+    _check(out)
+    assert set(out["grads"][2][1]) >= {"mln_g", "mln_b", "w_m"}
+
+
+def test_patch_merging_rejects_bad_shapes(cuda):
+    m = _swin_like()
+    m["layers"][0]["shape"]["merge"] = True
+    with pytest.raises(Exception, match="first layer cannot merge"):
+        gxe.PlanExecutor(gxe.make_plan([""] * 4, 2), m, 1)
+    m = _swin_like()
+    m["layers"][2]["shape"]["merge"] = False
+    with pytest.raises(Exception, match="input shape differs"):
+        gxe.PlanExecutor(gxe.make_plan([""] * 4, 2), m, 1)

@@ -37,7 +37,25 @@ def test_dropout_rate():
     assert abs(1.0 - m.mean() - 26 / 256) < 0.005
 
 
+def _torch_merge(x, P, shape):
+    """Swin PatchMerging written with reshapes (independent of lo.merge_rows): window-major
+    -> raster grid, x0..x3 = x[0::2,0::2], x[1::2,0::2], x[0::2,1::2], x[1::2,1::2], concat,
+    raster -> window-major, LayerNorm, projection."""
+    h = shape.hidden
+    c, g2 = h // 2, math.isqrt(shape.seq)
+    g, ws = 2 * g2, math.isqrt(shape.window)
+    n = x.shape[0] // (g * g)
+    r = x.reshape(n, g // ws, g // ws, ws, ws, c).permute(0, 1, 3, 2, 4, 5).reshape(n, g, g, c)
+    m = torch.cat([r[:, 0::2, 0::2], r[:, 1::2, 0::2], r[:, 0::2, 1::2], r[:, 1::2, 1::2]], -1)
+    m = m.reshape(n, g2 // ws, ws, g2 // ws, ws, 4 * c).permute(0, 1, 3, 2, 4, 5)
+    m = m.reshape(n * g2 * g2, 4 * c)
+    m = torch.nn.functional.layer_norm(m, (4 * c,), P["mln_g"], P["mln_b"], 1e-5)
+    return m @ P["w_m"].T
+
+
 def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0):
+    if shape.merge:
+        x = _torch_merge(x, P, shape)
     h, H, d, s = shape.hidden, shape.heads, shape.head_dim, shape.att_seq
     n = x.shape[0] // s
     nw, S = shape.seq // s, shape.seq
@@ -58,13 +76,15 @@ def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0):
     return x1 + (g @ P["w_2"].T + P["b_2"]) * m2 * kh
 
 
-@pytest.mark.parametrize("p,window", [(0.0, 0), (0.1, 0), (0.1, 4)])
-def test_oracle_matches_autograd(p, window):
+@pytest.mark.parametrize("p,window,seq,merge", [(0.0, 0, 12, False), (0.1, 0, 12, False),
+                                                (0.1, 4, 12, False), (0.1, 4, 16, True),
+                                                (0.0, 9, 36, True)])
+def test_oracle_matches_autograd(p, window, seq, merge):
     rng = np.random.default_rng(0)
-    shape = lo.LayerShape(hidden=64, heads=4, seq=12, ffn=128, window=window)
+    shape = lo.LayerShape(hidden=64, heads=4, seq=seq, ffn=128, window=window, merge=merge)
     P = lo.init_layer_params(shape, rng, std=0.1)
-    x = rng.standard_normal((2 * shape.seq, shape.hidden))
-    dy = rng.standard_normal(x.shape)
+    x = rng.standard_normal((2 * shape.seq * (4 if merge else 1), shape.hidden // (2 if merge else 1)))
+    dy = rng.standard_normal((2 * shape.seq, shape.hidden))
     drop = lo.Dropout(p_attn=p, p_hidden=p, seed=99)
     y, cache = lo.layer_forward(P, x, shape, 0, drop, sample_offset=3)
     dx, G = lo.layer_backward(P, dy, cache, shape)
