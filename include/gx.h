@@ -130,6 +130,8 @@ GX_API int gx_exec_set_layer_params(gx_exec* ex, int layer, const float* canonic
 /* what: 0 = fp32 master params, 1 = synchronised fp32 gradients of the last step. */
 GX_API int gx_exec_export_layer(gx_exec* ex, int layer, int what, float* canonical, int64_t n);
 GX_API int gx_exec_load_batch(gx_exec* ex, const void* x_host, const void* target_host);
+/* Device-resident batch: the copies are ordered after the legacy default stream; buffers
+ * written on any other stream must be complete (synchronised) before the call. */
 GX_API int gx_exec_load_batch_device(gx_exec* ex, const void* x_dev, const void* target_dev);
 /* One training step (fwd + loss + bwd + grad sync + AdamW) on the loaded batch.
  * flags bit 0: replay as a CUDA graph (captured on first use); bit 1: instrumented run that

@@ -379,8 +379,11 @@ static void ln_cols_grid(int rows, int h, int* strips, int* slices, int* rows_pe
   *slices = (rows + *rows_per_slice - 1) / *rows_per_slice;
 }
 
+// Workspace: kLnBwdTickets ticket words first (a fixed offset, so one workspace serves
+// LayerNorms of different widths -- Swin stages), then [slices][3][h] fp32 partials.
+constexpr int kLnBwdTickets = 256;  // one per 64-column strip: h <= 16384
 int64_t layernorm_bwd_ws_floats(int h) {
-  return static_cast<int64_t>(kLnBwdMaxSlices) * 3 * h + (h / 64 + 64);
+  return kLnBwdTickets + static_cast<int64_t>(kLnBwdMaxSlices) * 3 * h;
 }
 
 int layernorm_bwd_rows(const void* dy, const void* x, const void* mean, const void* rstd,
@@ -417,14 +420,14 @@ int layernorm_bwd_cols(const void* dy, bool dy_f32, const void* x, const void* m
   if (fuse && dbias == nullptr) return set_error(kErrConfig, "layernorm_bwd: dz needs dbias");
   int strips, slices, rps;
   ln_cols_grid(rows, h, &strips, &slices, &rps);
-  unsigned int* tickets = reinterpret_cast<unsigned int*>(
-      workspace + static_cast<int64_t>(kLnBwdMaxSlices) * 3 * h);
+  unsigned int* tickets = reinterpret_cast<unsigned int*>(workspace);
   auto* kcols = dy_f32 ? (fuse ? layernorm_bwd_cols_kernel<true, true> : layernorm_bwd_cols_kernel<true, false>)
                        : (fuse ? layernorm_bwd_cols_kernel<false, true> : layernorm_bwd_cols_kernel<false, false>);
   launch_k(kcols, dim3(strips, slices), dim3(256), 0, st, dy, static_cast<const uint4*>(x),
            static_cast<const float*>(mean), static_cast<const float*>(rstd),
            static_cast<const uint4*>(dz), static_cast<float*>(dgamma), static_cast<float*>(dbeta),
-           static_cast<float*>(dbias), workspace, tickets, rows, h, rps, 1, int64_t{0});
+           static_cast<float*>(dbias), workspace + kLnBwdTickets, tickets, rows, h, rps, 1,
+           int64_t{0});
   return check_launch("layernorm_bwd_cols_kernel");
 }
 

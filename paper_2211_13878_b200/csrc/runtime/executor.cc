@@ -139,6 +139,13 @@ class Arena {
     }
     ptrs_.push_back(p);
     bytes_ += bytes;
+    // GX_POISON=1 (debug): fill fresh allocations with NaN bit patterns, so a read of memory
+    // the step never wrote shows up as a NaN instead of depending on what was there before
+    static const bool poison = [] {
+      const char* e = std::getenv("GX_POISON");
+      return e != nullptr && e[0] == '1';
+    }();
+    if (poison) cudaMemset(p, 0xFF, (bytes + 255) / 256 * 256);
     return p;
   }
   template <typename T>
@@ -226,6 +233,8 @@ struct RankCtx {
   int64_t in_rows_total = 0;
   std::vector<int64_t> in_row_off;  // per micro-batch offset (rows) into x_in / target
   int cur = 0;                      // index of gbuf holding the current dY
+  bool idle_chunks = false;  // some (layer, micro-batch) chunk of this rank has no samples:
+                             // gradients are zeroed whole each step and always accumulated
   int dc_slices = 0, da_slices = 0;  // split-K slices pending in acc32 (0 = bf16 result)
 };
 
@@ -463,6 +472,11 @@ class ExecutorImpl final : public Executor {
  private:
   // The weight gradients of L are final after its single wgrad GEMM: one micro-batch and no
   // data-parallel reduction (TP shards own their weight gradients).
+  // gradient bytes cleared before a step: the atomically accumulated head of the buffer, or
+  // all of it when some chunk of the rank is empty (its weight-gradient GEMMs may not run)
+  static size_t grad_zero_bytes(const RankCtx& r, const RankLayer& L) {
+    return static_cast<size_t>(r.idle_chunks ? L.lay.total : L.lay.acc_end) * 4;
+  }
   bool adam_fused(const RankLayer& L) const {
     return fused_adam_ && optimizer_ && !forward_only_ && !defer_opt_ && m_ == 1 && L.d.dp == 1 &&
            L.d.sdp == 1;
@@ -679,10 +693,9 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
         *err = "executor: hidden/tp and ffn/tp must be multiples of 8";
         return kErrConfig;
       }
-      if (d.data() > Bm_) {
-        *err = "executor: more data replicas than samples per micro-batch";
-        return kErrConfig;
-      }
+      // d.data() > Bm_ is allowed: GPipe splits each micro-batch over the data replicas, so
+      // with the planner's 1-sample micro-batches (A14, planner.cc:343-349) some replicas
+      // idle for a micro-batch; their gradients enter the reductions as zeros.
       if (l > 0 && (s.in_h() != shape_[l - 1].h || s.in_seq() != shape_[l - 1].seq)) {
         *err = "executor: layer " + std::to_string(l) +
                " input shape differs from the previous layer's output (only patch merging, "
@@ -851,6 +864,7 @@ int ExecutorImpl::allocate(RankCtx& r) {
       a.sample0 = lo;
       a.samples = static_cast<int>(hi - lo);
       a.rows = a.samples * s.seq;
+      if (a.rows == 0) r.idle_chunks = true;
       const int64_t rows = a.rows;
       const int64_t h = s.h, ht = s.h / t, ft = s.ffn / t;
       const int64_t in_rows = static_cast<int64_t>(a.samples) * s.in_seq();
@@ -1130,6 +1144,17 @@ int ExecutorImpl::load_batch(const void* x_host, const void* target_host) {
 }
 
 int ExecutorImpl::load_batch_device(const void* x_dev, const void* target_dev) {
+  // The caller produced the buffers on its own stream; our streams are non-blocking, so order
+  // the copies after the legacy default stream explicitly (callers on other streams must
+  // synchronise them first -- the Python wrapper does).
+  {
+    cudaEvent_t ev = nullptr;
+    GX_TRY(cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "load event"));
+    cudaError_t e = cudaEventRecord(ev, cudaStreamLegacy);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(stream_, ev, 0);
+    cudaEventDestroy(ev);
+    GX_TRY(cuda_check(e, "load_batch_device order"));
+  }
   for (auto& rp : ranks_) {
     RankCtx& r = *rp;
     for (int mb = 0; mb < m_; ++mb) {
@@ -1377,7 +1402,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
   const int l = L.layer;
   const int64_t row_off = A.sample0 * s.seq;
   const bool first_mb = mb == m_ - 1;  // backward visits micro-batches in reverse
-  const int wk = first_mb ? kOutF32 : kOutF32Accumulate;
+  const int wk = first_mb && !r.idle_chunks ? kOutF32 : kOutF32Accumulate;
   bf16* dY = r.gbuf[r.cur];
   bf16* dX = r.gbuf[r.cur ^ 1];
   if (rows == 0) return kOk;
@@ -1701,7 +1726,7 @@ int ExecutorImpl::deferred_updates(RankCtx& r, cudaStream_t st, bool record) {
     tmark("opt_begin L" + std::to_string(L.layer), st);
     GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, n_opt, lr_, b1_, b2_, eps_, wd_,
                      r.step, st, opt_blocks_ > 0 ? opt_blocks_ : 2 * num_sms(), r.opt_pending));
-    GX_TRY(cuda_check(cudaMemsetAsync(L.gfull, 0, L.lay.acc_end * 4, st), "memset grads"));
+    GX_TRY(cuda_check(cudaMemsetAsync(L.gfull, 0, grad_zero_bytes(r, L), st), "memset grads"));
     tmark("opt_end L" + std::to_string(L.layer), st);
     if (record) GX_TRY(cuda_check(cudaEventRecord(r.opt_done[li], st), "opt done"));
   }
@@ -1931,7 +1956,7 @@ int ExecutorImpl::step_once() {
     GX_TRY(cuda_check(cudaMemsetAsync(r->loss, 0, 4, stream_), "memset loss"));
     if (!deferred())
       for (RankLayer& L : r->layers)
-        GX_TRY(cuda_check(cudaMemsetAsync(L.gfull, 0, L.lay.acc_end * 4, stream_), "memset grads"));
+        GX_TRY(cuda_check(cudaMemsetAsync(L.gfull, 0, grad_zero_bytes(*r, L), stream_), "memset grads"));
   }
   if (deferred()) {  // last step's AdamW on the side stream, layer by layer (see defer_opt_)
     GX_TRY(fork(stream_, side_));

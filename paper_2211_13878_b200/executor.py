@@ -135,6 +135,10 @@ class PlanExecutor:
         _lib.check(_lib.lib().gx_exec_load_batch(self._h, _host_ptr(x_host), _host_ptr(target_host)))
 
     def load_batch_device(self, x_dev, target_dev):
+        import torch
+        for t in (x_dev, target_dev):  # produced on torch's stream; the executor's is separate
+            if t is not None:
+                torch.cuda.current_stream(t.device).synchronize()
         _lib.check(_lib.lib().gx_exec_load_batch_device(
             self._h, x_dev.data_ptr() if x_dev is not None else None,
             target_dev.data_ptr() if target_dev is not None else None))

@@ -90,6 +90,11 @@ CASES = [
     (4, ["tp:4", "tp:2,sdp:2", "sdp:4", "dp:4"], 6, 1, 1),        # uneven sample splits
     (8, ["tp:2,dp:2", "sdp:4", "dp:2,tp:2", "tp:4"], 8, 2, 2),    # PP x hybrid
     (4, ["dp:2", "tp:2", "sdp:2", "dp:2"], 8, 2, 4),              # PP, 4 micro-batches
+    # the planner's 1-sample micro-batches (A14) under data parallelism: replicas idle per
+    # micro-batch (T5-Large-48's searched plan is P=2, m=8, B=8 over dp:4 / sdp:4)
+    (4, ["dp:4", "sdp:4", "dp:4", "sdp:4"], 4, 1, 4),
+    (8, ["dp:4", "sdp:4", "tp:2,sdp:2", "sdp:4"], 4, 2, 4),
+    (4, ["sdp:4", "dp:2,tp:2", "tp:4", "dp:4"], 2, 1, 1),         # B < D: idle every step
 ]
 
 
