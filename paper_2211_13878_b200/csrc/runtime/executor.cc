@@ -2116,6 +2116,8 @@ int ExecutorImpl::run2(bool use_graph, bool profile) {
     }
     GX_TRY(cuda_check(e, "end capture"));
     graph = g;
+    // Node priorities (cudaGraphInstantiateFlagUseNodePriority) were measured slower: the
+    // weight-gradient stream starves and the data-gradient chain then waits on its buffers.
     GX_TRY(cuda_check(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate"));
     if (profile) prof_recs_ = recs_;
   }

@@ -12,7 +12,14 @@ rows, h = B * sh["seq"], sh["hidden"]
 x = torch.randn(rows, h).to(torch.bfloat16)
 variants = [("default", {}), ("no_optimizer", {"optimizer": False}),
             ("forward_only", {"forward_only": True}), ("no_wgrad_stream", {"wgrad_stream": False}),
-            ("no_splitk", {"splitk": False})]
+            ("no_splitk", {"splitk": False}),
+            ("opt_blocks_148", {"optimizer_blocks": 148}),
+            ("opt_blocks_592", {"optimizer_blocks": 592}),
+            ("opt_blocks_1184", {"optimizer_blocks": 1184}),
+            ("opt_blocks_4736", {"optimizer_blocks": 4736}),
+            ("opt_blocks_16384", {"optimizer_blocks": 16384}),
+            ("opt_group2_4736", {"optimizer_blocks": 4736, "optimizer_group": 2}),
+            ("defer_4736", {"optimizer_blocks": 4736, "defer_optimizer": True})]
 for name in (sys.argv[1:] or [v[0] for v in variants]):
     kw = dict(variants)[name]
     ex = gxe.PlanExecutor(plan, model, 1, dropout_attn=0.1, dropout_hidden=0.1, **kw)
