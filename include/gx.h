@@ -240,6 +240,7 @@ typedef struct gx_attention_args {
   void* mask;                  /* uint16 keep bits [batch*heads][seq][ceil(seq/64)][4]:
                                   written by fwd, read by bwd (when dropout is on) */
   unsigned long long* trace;   /* debug: per-CTA %globaltimer stamps (tcgen05 kernels), or NULL */
+  int causal;                  /* 1: query q attends keys k <= q only (decoder self-attention) */
 } gx_attention_args;
 
 GX_API int gx_k_attention_fwd(const gx_attention_args* args, void* stream);

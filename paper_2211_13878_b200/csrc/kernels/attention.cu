@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_a
       for (int j = 0; j < 4; ++j) {
         const int key = kb * kBlk + nb * 8 + 2 * t + (j & 1);
         float v = sacc[nb][j] * c2;
-        if (key >= s) v = -INFINITY;
+        if (key >= s || (p.causal && key > q0 + warp * 16 + g + 8 * (j >> 1))) v = -INFINITY;
         sacc[nb][j] = v;
         mx[j >> 1] = fmaxf(mx[j >> 1], v);
       }
@@ -389,7 +389,8 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
         const int ql = nb * 8 + 2 * t + (j & 1);
         const int q = q0 + ql;
         const int key = k0 + warp * 16 + g + 8 * (j >> 1);
-        float P = (q < s && key < s) ? exp2f(st[nb][j] * c2 - sL[ql]) : 0.f;
+        float P = (q < s && key < s && !(p.causal && key > q)) ? exp2f(st[nb][j] * c2 - sL[ql])
+                                                                : 0.f;
         float keep = 1.f;
         if (thr != 0u) {
           const int kk = key - k0;  // 0..63 within this CTA's key block

@@ -199,6 +199,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_after();
   GX_ATTN_STAMP(p, 2);
 
+  // keys [0, lim) exist for this row: the sequence, and with a causal mask only k <= q
+  const int lim = p.causal ? (q + 1 < s ? q + 1 : s) : s;
   float mx = -INFINITY;
   for (int kb = cq; kb < nblk; kb += 4) {
 #pragma unroll
@@ -209,7 +211,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       tmem_ld_wait();
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const float x = c0 + j < s ? __uint_as_float(v[j]) * c2 : -INFINITY;
+        const float x = c0 + j < lim ? __uint_as_float(v[j]) * c2 : -INFINITY;
         mx = fmaxf(mx, x);
       }
     }
@@ -257,7 +259,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           const int i = 2 * j2 + u;
-          float e = c0 + i < s ? ex2_ftz(__uint_as_float(v[i]) * c2 - m) : 0.f;
+          float e = c0 + i < lim ? ex2_ftz(__uint_as_float(v[i]) * c2 - m) : 0.f;
           sum += e;
           if (thr != 0u) {
             // key i of this 32-key half: word t = (i/2)%4, bit 8*hb + 2*(i/8) + i%2
@@ -556,7 +558,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const float* sDj = sD + (j & 1) * kTcQ;
       uint32_t ppd[16], pds[16];
       {
-        const bool full = qg0 + 32 <= s && kt * 128 + 128 <= s;  // no tail masking needed
+        // no tail / causal masking needed for this 32-query x 128-key block
+        const bool full = qg0 + 32 <= s && kt * 128 + 128 <= s && (!p.causal || kt * 128 + 127 <= qg0);
         uint32_t sv[32], dv[32];
         tmem_ld32(trow + c0, sv);
         tmem_ld32(trow + 128 + c0, dv);
@@ -571,7 +574,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int t = 0; t < 4; ++t) {
             const int i = 4 * i4 + t;
             const int qg = qg0 + i;
-            const bool valid = full || ((qg < s) && (key < s));
+            const bool valid = full || ((qg < s) && (key < s) && !(p.causal && key > qg));
             const float pr = valid ? ex2_ftz(__uint_as_float(sv[i]) * c2 - lv[t]) : 0.f;
             float f = 1.f;  // dropout factor: inv_keep or 0
             if (thr != 0u)

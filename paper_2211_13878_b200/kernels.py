@@ -102,7 +102,7 @@ class _AttnArgs(ctypes.Structure):
                 ("drop_threshold", ctypes.c_uint32), ("drop_scale", ctypes.c_float),
                 ("seed", ctypes.c_uint64), ("site", ctypes.c_uint64),
                 ("seed_offset", ctypes.c_void_p), ("mask", ctypes.c_void_p),
-                ("trace", ctypes.c_void_p)]
+                ("trace", ctypes.c_void_p), ("causal", ctypes.c_int)]
 
 
 class Dropout(ctypes.Structure):
@@ -121,8 +121,9 @@ def make_dropout(p, seed, site, row_offset=0, col_offset=0, drop_ld=0):
 
 
 def _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, heads_total=None, head_offset=0,
-               sample_offset=0):
+               sample_offset=0, causal=False):
     a = _AttnArgs()
+    a.causal = int(causal)
     a.batch, a.seq, a.heads, a.head_dim = batch, seq, heads, head_dim
     a.heads_total = heads_total or heads
     a.head_offset, a.sample_offset = head_offset, sample_offset
