@@ -90,6 +90,8 @@ class LayerShape:
     ffn: int
     window: int = 0  # > 0: Swin-style windowed attention over window-major token groups
     merge: bool = False  # Swin patch merging at the input: [4*seq, hidden/2] -> [seq, hidden]
+    causal: bool = False  # decoder self-attention: query q sees keys k <= q
+    cross: bool = False   # T5 decoder: + cross-attention sublayer over the memory
 
     @property
     def att_seq(self):
@@ -126,6 +128,12 @@ def init_layer_params(shape: LayerShape, rng: np.random.Generator, std=0.02) -> 
     merge = {} if not shape.merge else {
         "mln_g": 1.0 + 0.1 * rng.standard_normal(2 * h), "mln_b": 0.1 * rng.standard_normal(2 * h),
         "w_m": std * rng.standard_normal((h, 2 * h))}
+    if shape.cross:
+        merge = {
+            "ln3_g": 1.0 + 0.1 * rng.standard_normal(h), "ln3_b": 0.1 * rng.standard_normal(h),
+            "w_q2": std * rng.standard_normal((h, h)), "b_q2": 0.02 * rng.standard_normal(h),
+            "w_kv2": std * rng.standard_normal((2 * h, h)), "b_kv2": 0.02 * rng.standard_normal(2 * h),
+            "w_o2": std * rng.standard_normal((h, h)), "b_o2": 0.02 * rng.standard_normal(h)}
     return merge | {
         "ln1_g": 1.0 + 0.1 * rng.standard_normal(h), "ln1_b": 0.1 * rng.standard_normal(h),
         "w_qkv": std * rng.standard_normal((3 * h, h)), "b_qkv": 0.02 * rng.standard_normal(3 * h),
@@ -198,8 +206,42 @@ def _attn_mask(drop: Dropout, site: int, samples: int, heads: int, seq: int, sam
     return keep_bytes(drop.seed, site, call, j, drop.p_attn)
 
 
+def _attention(q2, k2, v2, n, s, H, d, am, ka, causal):
+    """softmax(q k^T / sqrt(d)) (keys k > q masked when causal), dropout, times v."""
+    q = q2.reshape(n, s, H, d).transpose(0, 2, 1, 3)
+    k = k2.reshape(n, s, H, d).transpose(0, 2, 1, 3)
+    v = v2.reshape(n, s, H, d).transpose(0, 2, 1, 3)
+    sc = q @ k.transpose(0, 1, 3, 2) / math.sqrt(d)
+    if causal:
+        sc = np.where(np.triu(np.ones((s, s), dtype=bool), 1), -np.inf, sc)
+    sc = sc - sc.max(-1, keepdims=True)
+    pr = np.exp(sc)
+    pr = pr / pr.sum(-1, keepdims=True)
+    pd = pr * am * ka
+    ctx = (pd @ v).transpose(0, 2, 1, 3).reshape(n * s, H * d)
+    return ctx, dict(q=q, k=k, v=v, pr=pr, am=am, ka=ka, pd=pd)
+
+
+def _attention_bwd(dctx, c, n, s, H, d):
+    """-> dq, dk, dv as [n*s, H*d]."""
+    dctx4 = dctx.reshape(n, s, H, d).transpose(0, 2, 1, 3)
+    dv = c["pd"].transpose(0, 1, 3, 2) @ dctx4
+    dpd = dctx4 @ c["v"].transpose(0, 1, 3, 2)
+    dpr = dpd * c["am"] * c["ka"]
+    pr = c["pr"]
+    dsc = pr * (dpr - (dpr * pr).sum(-1, keepdims=True)) / math.sqrt(d)
+    to2 = lambda t: t.transpose(0, 2, 1, 3).reshape(n * s, H * d)  # noqa: E731
+    return to2(dsc @ c["k"]), to2(dsc.transpose(0, 1, 3, 2) @ c["q"]), to2(dv)
+
+
+def cross_sites(layer_id: int, n_layers: int):
+    """Philox sites of a decoder layer's cross sublayer (after every layer's 3l+0..2)."""
+    return 3 * n_layers + 2 * layer_id, 3 * n_layers + 2 * layer_id + 1
+
+
 def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
-                  drop: Dropout = Dropout(), sample_offset: int = 0):
+                  drop: Dropout = Dropout(), sample_offset: int = 0, memory=None,
+                  n_layers: int = 0):
     """x: [samples*seq, h] float64.  Returns (y, cache).  Attention runs per (attention
     sequence, head); an attention sequence is a sample, or one window of a sample (window
     layers: tokens stored window-major, so a window is `window` consecutive rows)."""
@@ -221,6 +263,8 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
     k = qkv[:, h:2 * h].reshape(n, s, H, d).transpose(0, 2, 1, 3)
     v = qkv[:, 2 * h:].reshape(n, s, H, d).transpose(0, 2, 1, 3)
     sc = q @ k.transpose(0, 1, 3, 2) / math.sqrt(d)
+    if shape.causal:
+        sc = np.where(np.triu(np.ones((s, s), dtype=bool), 1), -np.inf, sc)
     sc = sc - sc.max(-1, keepdims=True)
     pr = np.exp(sc)
     pr = pr / pr.sum(-1, keepdims=True)
@@ -233,14 +277,26 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
     m1 = _hidden_mask(drop, 3 * layer_id + 1, n * s, h, sample_offset * shape.seq)
     kh = dropout_scale(drop.p_hidden)
     x1 = x + o * m1 * kh
-    c, ln2 = _ln_fwd(x1, P["ln2_g"], P["ln2_b"])
+    xcache = {}
+    xr = x1
+    if shape.cross:  # cross sublayer: q from LN3(x1), k / v from the memory
+        sa, sh = cross_sites(layer_id, n_layers)
+        c3, ln3 = _ln_fwd(x1, P["ln3_g"], P["ln3_b"])
+        q2 = c3 @ P["w_q2"].T + P["b_q2"]
+        kv2 = memory @ P["w_kv2"].T + P["b_kv2"]
+        am2 = _attn_mask(drop, sa, n, H, s, sample_offset)
+        ctx2, ac = _attention(q2, kv2[:, :h], kv2[:, h:], n, s, H, d, am2, ka, False)
+        m3 = _hidden_mask(drop, sh, n * s, h, sample_offset * shape.seq)
+        xr = x1 + (ctx2 @ P["w_o2"].T + P["b_o2"]) * m3 * kh
+        xcache = dict(c3=c3, ln3=ln3, ctx2=ctx2, ac=ac, m3=m3, memory=memory, x2=xr)
+    c, ln2 = _ln_fwd(xr, P["ln2_g"], P["ln2_b"])
     pre = c @ P["w_1"].T + P["b_1"]
     g = _gelu(pre)
     z = g @ P["w_2"].T + P["b_2"]
     m2 = _hidden_mask(drop, 3 * layer_id + 2, n * s, h, sample_offset * shape.seq)
-    y = x1 + z * m2 * kh
+    y = xr + z * m2 * kh
     cache = dict(x=x, a=a, ln1=ln1, q=q, k=k, v=v, pr=pr, am=am, ka=ka, pd=pd, ctx=ctx, m1=m1,
-                 kh=kh, x1=x1, c=c, ln2=ln2, pre=pre, g=g, m2=m2, n=n, **mcache)
+                 kh=kh, x1=x1, c=c, ln2=ln2, pre=pre, g=g, m2=m2, n=n, **mcache, **xcache)
     return y, cache
 
 
@@ -259,6 +315,18 @@ def layer_backward(P: dict, dy: np.ndarray, cache: dict, shape: LayerShape):
     dc = dpre @ P["w_1"]
     dx1_ln, G["ln2_g"], G["ln2_b"] = _ln_bwd(dc, cache["ln2"], P["ln2_g"])
     dx1 = dy + dx1_ln
+    if shape.cross:  # dx1 so far is dL/dx2: back through the cross sublayer
+        dx2 = dx1
+        do2 = dx2 * cache["m3"] * cache["kh"]
+        G["b_o2"] = do2.sum(0)
+        G["w_o2"] = do2.T @ cache["ctx2"]
+        dq2, dk2, dv2 = _attention_bwd(do2 @ P["w_o2"], cache["ac"], cache["n"], s, H, d)
+        dkv2 = np.concatenate([dk2, dv2], axis=1)
+        G["b_q2"], G["w_q2"] = dq2.sum(0), dq2.T @ cache["c3"]
+        G["b_kv2"], G["w_kv2"] = dkv2.sum(0), dkv2.T @ cache["memory"]
+        G["_dmem"] = dkv2 @ P["w_kv2"]
+        dx1_3, G["ln3_g"], G["ln3_b"] = _ln_bwd(dq2 @ P["w_q2"], cache["ln3"], P["ln3_g"])
+        dx1 = dx2 + dx1_3
     do = dx1 * cache["m1"] * cache["kh"]
     G["b_o"] = do.sum(0)
     G["w_o"] = do.T @ cache["ctx"]
@@ -294,17 +362,25 @@ def model_step(params: list, x: np.ndarray, target: np.ndarray, shape: LayerShap
     """Forward through all layers, MSE loss = sum((y-t)^2)/count, backward.
     Returns (loss, y, dx, grads per layer)."""
     shapes = shape if isinstance(shape, (list, tuple)) else [shape] * len(params)
+    dec0 = next((l for l, sh in enumerate(shapes) if sh.cross), None)
     caches = []
     hcur = x
+    memory = None
     for l, P in enumerate(params):
-        hcur, c = layer_forward(P, hcur, shapes[l], l, drop, sample_offset)
+        if l == dec0:
+            memory = hcur  # the first decoder layer's input is every decoder layer's memory
+        hcur, c = layer_forward(P, hcur, shapes[l], l, drop, sample_offset, memory, len(params))
         caches.append(c)
     count = count if count is not None else hcur.size
     loss = float(((hcur - target) ** 2).sum() / count)
     dcur = 2.0 * (hcur - target) / count
     grads = [None] * len(params)
+    dmem = 0.0
     for l in reversed(range(len(params))):
         dcur, grads[l] = layer_backward(params[l], dcur, caches[l], shapes[l])
+        dmem = dmem + grads[l].pop("_dmem", 0.0)
+        if l == dec0:
+            dcur = dcur + dmem
     return loss, hcur, dcur, grads
 
 

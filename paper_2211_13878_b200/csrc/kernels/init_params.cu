@@ -19,7 +19,7 @@ __device__ int64_t canon_of(const InitLayout& L, int64_t j) {
                 c_wo = c_wqkv + 3 * h * h, c_w1 = c_wo + h * h, c_w2 = c_w1 + f * h;
   const int64_t c_m = c_w2 + h * f;  // patch merging (mln_g, mln_b, w_m), unsharded
   int s = -1;
-  for (int i = 0; i < 15; ++i)
+  for (int i = 0; i < 23; ++i)
     if (j >= L.off[i] && j < L.off[i] + L.n[i]) s = i;
   if (s < 0) return -1;
   const int64_t k = j - L.off[s];
@@ -38,7 +38,16 @@ __device__ int64_t canon_of(const InitLayout& L, int64_t j) {
     case 11: return c_w2 + (k / ft) * f + tr * ft + k % ft;
     case 12: return c_m + k;
     case 13: return c_m + 2 * h + k;
-    default: return c_m + 4 * h + k;
+    case 14: return c_m + 4 * h + k;
+    // cross-attention (c_m is also its base: a layer merges or cross-attends, never both)
+    case 15: return c_m + k;                                              // ln3_g
+    case 16: return c_m + h + k;                                          // ln3_b
+    case 17: return c_m + 2 * h + tr * ht + k;                            // b_q2
+    case 18: return c_m + 3 * h + (k / ht) * h + tr * ht + k % ht;        // b_kv2
+    case 19: return c_m + 5 * h + k;                                      // b_o2
+    case 20: return c_m + 6 * h + (tr * ht + k / h) * h + k % h;          // w_q2
+    case 21: return c_m + 6 * h + h * h + ((k / h) / ht * h + tr * ht + (k / h) % ht) * h + k % h;
+    default: return c_m + 6 * h + 3 * h * h + (k / ht) * h + tr * ht + k % ht;  // w_o2
   }
 }
 
@@ -49,12 +58,14 @@ __global__ void init_params_kernel(float* __restrict__ master, int64_t n, InitLa
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t c = canon_of(L, L.lo + i);
     float v = 0.f;
-    const int64_t c_m = 9 * h + f + 4 * h * h + 2 * h * f;  // first merge element
+    const int64_t c_m = 9 * h + f + 4 * h * h + 2 * h * f;  // first merge / cross element
+    const int64_t gains = L.extra == 1 ? 2 * h : h;              // merge LN(2h) / LN3(h)
+    const int64_t zeros = L.extra == 1 ? 4 * h : 6 * h;          // ... then shifts, biases
     if (c >= 0) {
-      if (c < h || (c >= 2 * h && c < 3 * h) || (c >= c_m && c < c_m + 2 * h)) {
+      if (c < h || (c >= 2 * h && c < 3 * h) || (L.extra != 0 && c >= c_m && c < c_m + gains)) {
         v = 1.f;  // LayerNorm gains
-      } else if (c >= c_m && c < c_m + 4 * h) {
-        v = 0.f;  // merge LayerNorm shift
+      } else if (L.extra != 0 && c >= c_m && c < c_m + zeros) {
+        v = 0.f;  // LayerNorm shifts and biases of the extra sublayer
       } else if (c >= 9 * h + f) {
         const Philox4 w = philox4x32_10(static_cast<uint32_t>(c), static_cast<uint32_t>(c >> 32),
                                         static_cast<uint32_t>(layer), 0x5eedu,

@@ -61,12 +61,21 @@ Layout make_layout(const Shape& s, int tp, int sdp) {
   const int64_t mc = s.merge ? 2 * h : 0;  // merged channels (4 x h/2)
   put(L.mlng, mc);
   put(L.mlnb, mc);
+  const int64_t xh = s.cross ? h : 0, xht = s.cross ? h / tp : 0;
+  put(L.ln3g, xh);
+  put(L.ln3b, xh);
+  put(L.bq2, xht);
+  put(L.bkv2, 2 * xht);
+  put(L.bo2, xh);
   L.acc_end = off;
   put(L.wqkv, 3 * h / tp * h);
   put(L.wo, h * (h / tp));
   put(L.w1, f / tp * h);
   put(L.w2, h * (f / tp));
   put(L.wm, s.merge ? h * mc : 0);  // replicated across TP ranks (identical gradients)
+  put(L.wq2, xht * h);
+  put(L.wkv2, 2 * xht * h);
+  put(L.wo2, h * xht);
   const int64_t q = 64 * static_cast<int64_t>(sdp);
   L.total = (off + q - 1) / q * q;
   return L;
@@ -75,7 +84,9 @@ Layout make_layout(const Shape& s, int tp, int sdp) {
 int64_t canonical_size(const Shape& s) {
   const int64_t h = s.h, f = s.ffn;
   const int64_t merge = s.merge ? 4 * h + 2 * h * h : 0;  // mln_g, mln_b (2h each), w_m [h][2h]
-  return 4 * h + 3 * h + h + f + h + 3 * h * h + h * h + f * h + h * f + merge;
+  // ln3_g ln3_b b_q2 b_kv2(2h) b_o2, w_q2 [h][h], w_kv2 [2h][h], w_o2 [h][h]
+  const int64_t cross = s.cross ? 6 * h + 4 * h * h : 0;
+  return 4 * h + 3 * h + h + f + h + 3 * h * h + h * h + f * h + h * f + merge + cross;
 }
 
 namespace {
@@ -112,6 +123,17 @@ int64_t canon_index(const Shape& s, const Layout& L, int t, int tr, int64_t j) {
   if (in(L.mlng, k)) return c_m + k;
   if (in(L.mlnb, k)) return c_m + 2 * h + k;
   if (in(L.wm, k)) return c_m + 4 * h + k;
+  if (in(L.ln3g, k)) return c_m + k;  // cross-attention shares the base (never both)
+  if (in(L.ln3b, k)) return c_m + h + k;
+  if (in(L.bq2, k)) return c_m + 2 * h + tr * ht + k;
+  if (in(L.bkv2, k)) return c_m + 3 * h + (k / ht) * h + tr * ht + k % ht;
+  if (in(L.bo2, k)) return c_m + 5 * h + k;
+  if (in(L.wq2, k)) return c_m + 6 * h + (tr * ht + k / h) * h + k % h;
+  if (in(L.wkv2, k)) {
+    const int64_t row = k / h, col = k % h;
+    return c_m + 6 * h + h * h + ((row / ht) * h + tr * ht + row % ht) * h + col;
+  }
+  if (in(L.wo2, k)) return c_m + 6 * h + 3 * h * h + (k / ht) * h + tr * ht + k % ht;
   return -1;
 }
 
@@ -177,6 +199,10 @@ struct Acts {
   bf16 *xm = nullptr, *mg = nullptr, *mln = nullptr;
   float *meanm = nullptr, *rstdm = nullptr;
   bf16* in() const { return xm != nullptr ? xm : x; }  // what the previous layer feeds
+  // decoder cross-attention sublayer: x2 = x1 + drop(attn(LN3(x1) Wq2, mem Wkv2) Wo2 + bo2)
+  bf16 *x2 = nullptr, *ln3 = nullptr, *qkv2 = nullptr, *ctx2 = nullptr;
+  float *lse2 = nullptr, *mean3 = nullptr, *rstd3 = nullptr;
+  uint16_t* amask2 = nullptr;
   bool ln1_ready = false;     // LN1 already produced by the previous layer's fused epilogue
   bool dz_ready = false;      // backward: dz / db2 already produced by the next layer's LN1 bwd
 };
@@ -215,7 +241,14 @@ struct RankCtx {
   float *dq_acc = nullptr, *dsum = nullptr;
   float* ln_ws = nullptr;  // LayerNorm-backward block partials
   float* ln_ws_m = nullptr;  // ... for the patch-merging LayerNorm (main stream only)
+  float* ln_ws_x = nullptr;  // ... for the decoder's LN3 (main stream only)
   bf16 *dmg1 = nullptr, *dmg2 = nullptr;  // patch-merging backward scratch [rows][2h]
+  // decoder backward: the cross sublayer's dropout-masked output gradient, its dqkv, and the
+  // memory gradient accumulated over the decoder layers (fp32, added to the first decoder
+  // layer's input gradient)
+  bf16 *dout2 = nullptr, *dqkv2 = nullptr;
+  float* dmem = nullptr;
+  int dec_li = -1;  // local index of the model's first decoder layer on this rank, or -1
   float* cs_ws[2] = {nullptr, nullptr};  // column-sum workspaces: [0] main stream, [1] wgrad stream
   float* acc32 = nullptr;  // split-K fp32 slices [kMaxSplits][rows][h]
   bf16 *x_in = nullptr, *target = nullptr;  // [m micro-batches of this rank's rows][h]
@@ -296,6 +329,10 @@ class ExecutorImpl final : public Executor {
   int fwd_phase(RankCtx& r, int li, int mb, int phase);
   int bwd_phase(RankCtx& r, int li, int mb, int phase);
   int merge_bwd(RankCtx& r, RankLayer& L, Acts& A, bf16* dX, const gx_gemm_epilogue& wm_ep);
+  int cross_fwd(RankCtx& r, int li, int mb, bool ln3_ready);
+  int cross_bwd(RankCtx& r, int li, int mb, bf16* dout,
+                const std::function<gx_gemm_epilogue(const Slot&, int64_t)>& wgrad_ep);
+  gx_attention_args cross_args(RankCtx& r, const RankLayer& L, const Acts& A) const;
   int sync_phase(RankCtx& r, int li, int phase);
   int xin_fwd(RankCtx& r, int li, int mb);
   int xin_bwd(RankCtx& r, int li, int mb);
@@ -429,6 +466,7 @@ class ExecutorImpl final : public Executor {
   // as their gradients are marked ready (optimizer_stream.cu).
   int opt_sms_ = 0;
   int64_t mem_cap_ = 0;  // per-rank device-byte cap (cfg "memory_cap_bytes"; 0 = none)
+  int dec0_ = -1;         // first decoder (cross-attention) layer, or -1
   bool persistent_opt() const {
     return opt_sms_ > 0 && optimizer_ && !forward_only_ && !profiling_ && !deferred() &&
            opt_stream_ == 0;
@@ -631,8 +669,10 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
       // "window": Swin-style windowed self-attention -- the sample's seq tokens are stored
       // window-major (window w holds tokens [w*win, (w+1)*win)) and attention runs inside
       // each window; everything else is the encoder layer.
-      if (kind == "encoder") {
+      if (kind == "encoder" || kind == "causal" || kind == "decoder") {
         s.win = s.seq;
+        s.causal = kind != "encoder";
+        s.cross = kind == "decoder";
       } else if (kind == "window") {
         s.win = sh.value("window", 49);
         if (s.win <= 0 || s.seq % s.win != 0) {
@@ -640,7 +680,7 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
           return kErrConfig;
         }
       } else {
-        *err = "executor: layer kind '" + kind + "' not supported (encoder, window)";
+        *err = "executor: layer kind '" + kind + "' not supported (encoder, causal, decoder, window)";
         return kErrConfig;
       }
       s.merge = sh.value("merge", false);
@@ -696,6 +736,23 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
       // d.data() > Bm_ is allowed: GPipe splits each micro-batch over the data replicas, so
       // with the planner's 1-sample micro-batches (A14, planner.cc:343-349) some replicas
       // idle for a micro-batch; their gradients enter the reductions as zeros.
+      if (s.cross) {  // T5 decoder layers (SPEC.md:67 flattens encoder + decoder)
+        if (dec0_ < 0) dec0_ = l;
+        if (d.tp != 1) {
+          *err = "executor: decoder (cross-attention) layers run without tensor parallelism";
+          return kErrConfig;
+        }
+        const Shape& s0 = shape_[dec0_];
+        if (stage_of_layer(l) != stage_of_layer(dec0_) || d.data() != deg_[dec0_].data() ||
+            s.h != s0.h || s.seq != s0.seq) {
+          *err = "executor: decoder layers must share one pipeline stage, data degree and "
+                 "shape (the memory is the first decoder layer's input)";
+          return kErrConfig;
+        }
+      } else if (dec0_ >= 0) {
+        *err = "executor: decoder layers must be the model's last layers";
+        return kErrConfig;
+      }
       if (l > 0 && (s.in_h() != shape_[l - 1].h || s.in_seq() != shape_[l - 1].seq)) {
         *err = "executor: layer " + std::to_string(l) +
                " input shape differs from the previous layer's output (only patch merging, "
@@ -840,7 +897,8 @@ int ExecutorImpl::build_groups() {
 int ExecutorImpl::allocate(RankCtx& r) {
   Arena& A = r.arena;
   A.set_cap(static_cast<size_t>(mem_cap_));
-  int64_t max_rows = 0, max_h = 0, max_f = 0, max_q = 0, max_c = 0, max_lse = 0, max_m = 0;
+  int64_t max_rows = 0, max_h = 0, max_f = 0, max_q = 0, max_c = 0, max_lse = 0, max_m = 0,
+          max_x = 0;
   for (size_t li = 0; li < r.layers.size(); ++li) {
     RankLayer& L = r.layers[li];
     const Shape& s = L.sh;
@@ -898,6 +956,19 @@ int ExecutorImpl::allocate(RankCtx& r) {
       a.pre = A.a<bf16>(rows * ft);
       a.gel = A.a<bf16>(rows * ft);
       a.y = A.a<bf16>(rows * h);
+      if (s.cross) {
+        a.x2 = A.a<bf16>(rows * h);
+        a.ln3 = A.a<bf16>(rows * h);
+        a.qkv2 = A.a<bf16>(rows * 3 * ht);
+        a.ctx2 = A.a<bf16>(rows * ht);
+        a.lse2 = A.a<float>(static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq);
+        if (thr_attn_ != 0u)
+          a.amask2 = A.a<uint16_t>(static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq *
+                                   ((s.seq + 63) / 64) * 4);
+        a.mean3 = A.a<float>(rows);
+        a.rstd3 = A.a<float>(rows);
+        max_x = std::max(max_x, rows * h);
+      }
       a.lse = A.a<float>(static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq);
       if (thr_attn_ != 0u)
         a.amask = A.a<uint16_t>(static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq *
@@ -932,6 +1003,18 @@ int ExecutorImpl::allocate(RankCtx& r) {
   r.gbuf[0] = A.a<bf16>(max_h);
   r.gbuf[1] = A.a<bf16>(max_h);
   r.dq_acc = A.a<float>(4 * max_c);  // tcgen05 attention: one dQ partial per 128-key tile
+  if (max_x > 0) {
+    int64_t hx = 0;
+    for (const RankLayer& L : r.layers) hx = std::max<int64_t>(hx, L.sh.h);
+    r.ln_ws_x = A.a<float>(layernorm_bwd_ws_floats(static_cast<int>(hx)));
+    if (r.ln_ws_x != nullptr)
+      cudaMemset(r.ln_ws_x, 0, layernorm_bwd_ws_floats(static_cast<int>(hx)) * sizeof(float));
+    r.dout2 = A.a<bf16>(max_x);
+    r.dqkv2 = A.a<bf16>(3 * max_x);
+    r.dmem = A.a<float>(max_x);
+    for (size_t i = 0; i < r.layers.size(); ++i)
+      if (r.layers[i].layer == dec0_) r.dec_li = static_cast<int>(i);
+  }
   r.acc32 = A.a<float>(static_cast<int64_t>(kMaxSplits) * max_h);
   {
     int64_t max_hdim = 0;
@@ -1089,10 +1172,13 @@ int ExecutorImpl::init_params(uint64_t seed, float std_dev) {
   for (auto& r : ranks_) {
     for (RankLayer& L : r->layers) {
       InitLayout il{};
-      const Slot* slots[15] = {&L.lay.ln1g, &L.lay.ln1b, &L.lay.ln2g, &L.lay.ln2b, &L.lay.bqkv,
+      const Slot* slots[23] = {&L.lay.ln1g, &L.lay.ln1b, &L.lay.ln2g, &L.lay.ln2b, &L.lay.bqkv,
                                &L.lay.bo,   &L.lay.b1,   &L.lay.b2,   &L.lay.wqkv, &L.lay.wo,
-                               &L.lay.w1,   &L.lay.w2,   &L.lay.mlng, &L.lay.mlnb, &L.lay.wm};
-      for (int i = 0; i < 15; ++i) {
+                               &L.lay.w1,   &L.lay.w2,   &L.lay.mlng, &L.lay.mlnb, &L.lay.wm,
+                               &L.lay.ln3g, &L.lay.ln3b, &L.lay.bq2,  &L.lay.bkv2, &L.lay.bo2,
+                               &L.lay.wq2,  &L.lay.wkv2, &L.lay.wo2};
+      il.extra = L.sh.merge ? 1 : (L.sh.cross ? 2 : 0);
+      for (int i = 0; i < 23; ++i) {
         il.off[i] = slots[i]->off;
         il.n[i] = slots[i]->n;
       }
@@ -1199,7 +1285,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
   const int l = L.layer;
   const int64_t row_off = A.sample0 * s.seq;
   if (rows == 0) return kOk;
-  bool ln2_ready = false;
+  bool ln2_ready = false, ln3_ready = false;
   if (phase == 0) {
     if (s.merge) {  // Swin patch merging: gather 2x2 -> LayerNorm(2h) -> x = mln Wm^T
       const int g = static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.seq))));
@@ -1246,6 +1332,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     at.site = 3ull * l;
     at.seed_offset = r.seed_off;
     at.mask = A.amask;
+    at.causal = s.causal ? 1 : 0;
     {
       const double af = 4.0 * A.samples * (s.heads / t) * double(s.seq) * s.win * s.hd;
       GX_TRY(timed(kAttnFwd, af, 2.0 * rows * 4 * ht, [&] { return attention_fwd(at, stream_); }));
@@ -1266,12 +1353,15 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
         d.row_offset = row_off;
         d.drop_ld = h;
         d.seed_offset = r.seed_off;
+        // (decoder layers: the LayerNorm that follows is the cross sublayer's LN3)
         GX_TRY(timed(kNorm, 0, (4.0 * sp + 8.0) * rows * h, [&] {
           return residual_layernorm(r.acc32, sp, static_cast<int64_t>(rows) * h, P + L.lay.bo.off,
-                                    A.x, A.x1, d, P + L.lay.ln2g.off, P + L.lay.ln2b.off, A.ln2,
-                                    A.mean2, A.rstd2, rows, h, stream_);
+                                    A.x, A.x1, d, P + (s.cross ? L.lay.ln3g : L.lay.ln2g).off,
+                                    P + (s.cross ? L.lay.ln3b : L.lay.ln2b).off,
+                                    s.cross ? A.ln3 : A.ln2, s.cross ? A.mean3 : A.mean2,
+                                    s.cross ? A.rstd3 : A.rstd2, rows, h, stream_);
         }));
-        ln2_ready = true;
+        (s.cross ? ln3_ready : ln2_ready) = true;
       } else {
         o.out = A.x1;
         o.bias = P + L.lay.bo.off;
@@ -1293,6 +1383,8 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
                                DType::kBF16, stream_);
     }
   }
+  // the MLP's residual-stream input: x1, or -- after a decoder's cross sublayer -- x2
+  bf16* const xr = s.cross ? A.x2 : A.x1;
   if ((t == 1 && phase == 0) || (t > 1 && phase == 1)) {
     if (t > 1) {
       gx_dropout d{};
@@ -1305,8 +1397,9 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
       d.seed_offset = r.seed_off;
       GX_TRY(timed(kElementwise, 0, 6.0 * rows * h, [&] { return bias_dropout_add(r.partial, P + L.lay.bo.off, A.x, A.x1, rows, h, d, stream_); }));
     }
+    if (s.cross) GX_TRY(cross_fwd(r, li, mb, ln3_ready));
     if (!ln2_ready)
-      GX_TRY(timed(kNorm, 0, 4.0 * rows * h, [&] { return layernorm_fwd(A.x1, P + L.lay.ln2g.off, P + L.lay.ln2b.off, A.ln2, A.mean2, A.rstd2,
+      GX_TRY(timed(kNorm, 0, 4.0 * rows * h, [&] { return layernorm_fwd(xr, P + L.lay.ln2g.off, P + L.lay.ln2b.off, A.ln2, A.mean2, A.rstd2,
                            rows, h, stream_); }));
     gx_gemm_epilogue e = epi();
     e.out_kind = kOutBF16;
@@ -1345,7 +1438,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
         }
         GX_TRY(timed(kNorm, 0, (4.0 * sp + 8.0) * rows * h, [&] {
           return residual_layernorm(r.acc32, sp, static_cast<int64_t>(rows) * h, P + L.lay.b2.off,
-                                    A.x1, A.y, d,
+                                    xr, A.y, d,
                                     nxt ? PN + r.layers[li + 1].lay.ln1g.off : nullptr,
                                     nxt ? PN + r.layers[li + 1].lay.ln1b.off : nullptr,
                                     nxt ? nxt->ln1 : nullptr, nxt ? nxt->mean1 : nullptr,
@@ -1356,7 +1449,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
       }
       o.out = A.y;
       o.bias = P + L.lay.b2.off;
-      o.residual = A.x1;
+      o.residual = xr;
       o.ld_res = h;
       o.row_offset = row_off;
       o.drop_ld = h;
@@ -1382,7 +1475,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     d.drop_ld = h;
     d.seed_offset = r.seed_off;
     return timed(kElementwise, 0, 6.0 * rows * h, [&] {
-      return bias_dropout_add(r.partial, P + L.lay.b2.off, A.x1, A.y, rows, h, d, stream_);
+      return bias_dropout_add(r.partial, P + L.lay.b2.off, xr, A.y, rows, h, d, stream_);
     });
   }
   return kOk;
@@ -1494,15 +1587,24 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     // dx1 = residual-stream gradient, dout = dropout_mask(dx1), dbo += colsum(dout)
     // (row pass on the critical path; the dgamma / dbeta / dbias column pass rides the wgrad
     // stream from the row pass's fp32 copy of dy)
-    d.site = 3ull * l + 1;
+    // (decoder layers: LN2 sits on x2 and the dropout below it is the cross sublayer's)
+    const bool xd = s.cross;
+    d.site = xd ? 3ull * L_ + 2ull * l + 1 : 3ull * l + 1;
+    bf16* const xr = xd ? A.x2 : A.x1;
+    bf16* const dz2 = xd ? r.dout2 : dout;
     float* fold2 = r.lnfold[par][0];
-    GX_TRY(timed(kNorm, 0, 10.0 * rows * h, [&] { return layernorm_bwd_rows(dc_in, A.x1, A.mean2, A.rstd2, P + L.lay.ln2g.off, dY, r.dx1,
-                         rows, h, stream_, r.dc_slices > 0, &d, dout, std::max(1, r.dc_slices),
+    GX_TRY(timed(kNorm, 0, 10.0 * rows * h, [&] { return layernorm_bwd_rows(dc_in, xr, A.mean2, A.rstd2, P + L.lay.ln2g.off, dY, r.dx1,
+                         rows, h, stream_, r.dc_slices > 0, &d, dz2, std::max(1, r.dc_slices),
                          static_cast<int64_t>(rows) * h, fold2); }));
     GX_TRY(on_wgrad([&] {
-      return timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd_cols(fold2, true, A.x1, A.mean2, A.rstd2, dout,
-                         G + L.lay.ln2g.off, G + L.lay.ln2b.off, G + L.lay.bo.off, rows, h, r.ln_ws, ls_); });
+      return timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd_cols(fold2, true, xr, A.mean2, A.rstd2, dz2,
+                         G + L.lay.ln2g.off, G + L.lay.ln2b.off, G + (xd ? L.lay.bo2 : L.lay.bo).off, rows, h, r.ln_ws, ls_); });
     }));
+    if (xd) {
+      // the wgrad-stream LN2 column pass above reads dout2 / fold2: let it finish first
+      if (wg_active_) GX_TRY(fork(wg_, stream_));
+      GX_TRY(cross_bwd(r, li, mb, dout, wgrad_ep));
+    }
     const gx_gemm_epilogue wo = wgrad_ep(L.lay.wo, ht);
     auto wgrado = [&] { return on_wgrad([&] { return gemm(dout, h, true, A.ctx, ht, true, h, ht, rows, wo); }); };  // dWo = dout^T ctx
     if (!fuse_adam) GX_TRY(wgrado());
@@ -1536,6 +1638,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     at.site = 3ull * l;
     at.seed_offset = r.seed_off;
     at.mask = A.amask;
+    at.causal = s.causal ? 1 : 0;
     {
       const double af = 10.0 * A.samples * (s.heads / t) * double(s.seq) * s.win * s.hd;
       GX_TRY(timed(kAttnBwd, af, 2.0 * rows * 8 * ht, [&] { return attention_bwd(at, stream_); }));
@@ -1609,8 +1712,142 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     }));
     if (prev != nullptr) prev->dz_ready = true;
     if (s.merge) GX_TRY(merge_bwd(r, L, A, dX, wgrad_ep(L.lay.wm, 2 * h)));
+    if (li == r.dec_li) {  // this input is also every decoder layer's memory: dX += dL/dmem
+      gx_dropout off{};
+      GX_TRY(timed(kElementwise, 0, 8.0 * rows * h, [&] {
+        return bias_dropout_add(r.dmem, nullptr, dX, dX, rows, h, off, stream_, true);
+      }));
+    }
   }
   return kOk;
+}
+
+// Decoder cross-attention sublayer, forward (tp == 1): x2 = x1 + drop(attn(q, k, v) Wo2 + bo2)
+// with q = LN3(x1) Wq2 + bq2 and k, v = mem Wkv2 + bkv2, mem = the input of the model's first
+// decoder layer (the encoder output).  q and kv are written side by side into one
+// [rows][3h] buffer so the self-attention kernels serve unchanged (non-causal).
+int ExecutorImpl::cross_fwd(RankCtx& r, int li, int mb, bool ln3_ready) {
+  RankLayer& L = r.layers[li];
+  Acts& A = L.acts[mb];
+  const Shape& s = L.sh;
+  const int rows = A.rows, h = s.h;
+  const bf16* P = L.pfull;
+  const int l = L.layer;
+  const bf16* mem = r.layers[r.dec_li].acts[mb].x;
+  if (!ln3_ready)
+    GX_TRY(timed(kNorm, 0, 4.0 * rows * h, [&] {
+      return layernorm_fwd(A.x1, P + L.lay.ln3g.off, P + L.lay.ln3b.off, A.ln3, A.mean3, A.rstd3,
+                           rows, h, stream_);
+    }));
+  gx_gemm_epilogue e = epi();
+  e.out_kind = kOutBF16;
+  e.out = A.qkv2;
+  e.ldo = 3 * h;
+  e.bias = P + L.lay.bq2.off;
+  GX_TRY(gemm(A.ln3, h, false, P + L.lay.wq2.off, h, false, rows, h, h, e));  // q2
+  e.out = A.qkv2 + h;
+  e.bias = P + L.lay.bkv2.off;
+  GX_TRY(gemm(mem, h, false, P + L.lay.wkv2.off, h, false, rows, 2 * h, h, e));  // k2 v2
+  gx_attention_args at = cross_args(r, L, A);
+  GX_TRY(timed(kAttnFwd, 4.0 * A.samples * s.heads * double(s.seq) * s.seq * s.hd,
+               2.0 * rows * 4 * h, [&] { return attention_fwd(at, stream_); }));
+  gx_gemm_epilogue o = epi();
+  o.out_kind = kOutBF16;
+  o.ldo = h;
+  o.out = A.x2;
+  o.bias = P + L.lay.bo2.off;
+  o.residual = A.x1;
+  o.ld_res = h;
+  o.row_offset = A.sample0 * s.seq;
+  o.drop_ld = h;
+  o.drop_threshold = thr_hidden_;
+  o.drop_scale = scale_of(p_hidden_);
+  o.seed = seed_;
+  o.site = 3ull * L_ + 2ull * l + 1;
+  o.seed_offset = r.seed_off;
+  return gemm(A.ctx2, h, false, P + L.lay.wo2.off, h, false, rows, h, h, o);
+}
+
+gx_attention_args ExecutorImpl::cross_args(RankCtx& r, const RankLayer& L, const Acts& A) const {
+  const Shape& s = L.sh;
+  gx_attention_args at{};
+  at.batch = A.samples;
+  at.seq = s.seq;
+  at.heads = s.heads;
+  at.head_dim = s.hd;
+  at.heads_total = s.heads;
+  at.head_offset = 0;
+  at.sample_offset = A.sample0;
+  at.scale = 1.f / std::sqrt(static_cast<float>(s.hd));
+  at.qkv = A.qkv2;
+  at.ld_qkv = 3 * s.h;
+  at.ctx = A.ctx2;
+  at.ld_ctx = s.h;
+  at.lse = A.lse2;
+  at.drop_threshold = thr_attn_;
+  at.drop_scale = scale_of(p_attn_);
+  at.seed = seed_;
+  at.site = 3ull * L_ + 2ull * L.layer;
+  at.seed_offset = r.seed_off;
+  at.mask = A.amask2;
+  at.dq_accum = r.dq_acc;
+  at.dsum = r.dsum;
+  return at;
+}
+
+// Decoder cross-attention sublayer, backward (main stream).  In: r.dx1 = dL/dx2 (the residual
+// gradient below the MLP), r.dout2 = its dropout-masked copy (bo2's gradient already taken).
+// Out: r.dx1 = dL/dx1, dout = dL/d(self-attention out-projection) with bo's gradient, and
+// dL/dmem accumulated into r.dmem.
+int ExecutorImpl::cross_bwd(RankCtx& r, int li, int mb, bf16* dout,
+                            const std::function<gx_gemm_epilogue(const Slot&, int64_t)>& wgrad_ep) {
+  RankLayer& L = r.layers[li];
+  Acts& A = L.acts[mb];
+  const Shape& s = L.sh;
+  const int rows = A.rows, h = s.h;
+  const bf16* P = L.pfull;
+  float* G = L.gfull;
+  const int l = L.layer;
+  const bf16* mem = r.layers[r.dec_li].acts[mb].x;
+  gx_gemm_epilogue c = epi();
+  c.out_kind = kOutBF16;
+  c.out = r.dctx;
+  c.ldo = h;
+  GX_TRY(gemm(r.dout2, h, false, P + L.lay.wo2.off, h, true, rows, h, h, c));  // dout2 Wo2
+  GX_TRY(gemm(r.dout2, h, true, A.ctx2, h, true, h, h, rows, wgrad_ep(L.lay.wo2, h)));
+  gx_attention_args at = cross_args(r, L, A);
+  at.dctx = r.dctx;
+  at.dqkv = r.dqkv2;
+  GX_TRY(timed(kAttnBwd, 10.0 * A.samples * s.heads * double(s.seq) * s.seq * s.hd,
+               2.0 * rows * 8 * h, [&] { return attention_bwd(at, stream_); }));
+  // weight / bias gradients of the q and kv projections
+  GX_TRY(colsum(r.dqkv2, 3 * h, G + L.lay.bq2.off, rows, h, stream_, r.cs_ws[0]));
+  GX_TRY(gemm(r.dqkv2, 3 * h, true, A.ln3, h, true, h, h, rows, wgrad_ep(L.lay.wq2, h)));
+  GX_TRY(colsum(r.dqkv2 + h, 3 * h, G + L.lay.bkv2.off, rows, 2 * h, stream_, r.cs_ws[0]));
+  GX_TRY(gemm(r.dqkv2 + h, 3 * h, true, mem, h, true, 2 * h, h, rows, wgrad_ep(L.lay.wkv2, h)));
+  // memory gradient: the last decoder layer (first in backward) starts the sum
+  gx_gemm_epilogue m = epi();
+  m.out_kind = li + 1 == static_cast<int>(r.layers.size()) ? kOutF32 : kOutF32Accumulate;
+  m.out = r.dmem;
+  m.ldo = h;
+  GX_TRY(gemm(r.dqkv2 + h, 3 * h, false, P + L.lay.wkv2.off, h, true, rows, h, 2 * h, m));
+  c.out = r.dc;
+  GX_TRY(gemm(r.dqkv2, 3 * h, false, P + L.lay.wq2.off, h, true, rows, h, h, c));  // dq Wq2
+  // LN3 backward: dx1 = dx2 + LN3'(dc3), with the self-attention out-projection's dropout
+  // backward and bias gradient fused in (as LN2's backward does for non-decoder layers)
+  gx_dropout d{};
+  d.threshold = thr_hidden_;
+  d.scale = scale_of(p_hidden_);
+  d.seed = seed_;
+  d.site = 3ull * l + 1;
+  d.row_offset = A.sample0 * s.seq;
+  d.drop_ld = h;
+  d.seed_offset = r.seed_off;
+  return timed(kNorm, 0, 18.0 * rows * h, [&] {
+    return layernorm_bwd(r.dc, A.x1, A.mean3, A.rstd3, P + L.lay.ln3g.off, r.dx1, r.dx1,
+                         G + L.lay.ln3g.off, G + L.lay.ln3b.off, rows, h, r.ln_ws_x, stream_,
+                         false, &d, dout, G + L.lay.bo.off);
+  });
 }
 
 // Patch-merging backward (main stream, after LN1's backward left dL/dx in dX):

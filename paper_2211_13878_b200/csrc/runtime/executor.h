@@ -39,6 +39,9 @@ struct Shape {
   // Swin patch merging at the layer input: the input is [4*seq, h/2] per sample (a grid of
   // side 2G, window-major), 2x2 neighbours are concatenated, LayerNorm'd and projected to h.
   bool merge = false;
+  // decoder layers: causal self-attention (kind "causal", "decoder"); "decoder" adds a
+  // cross-attention sublayer over the memory (the input of the model's first decoder layer)
+  bool causal = false, cross = false;
   int in_h() const { return merge ? h / 2 : h; }
   int in_seq() const { return merge ? 4 * seq : seq; }
 };
@@ -50,6 +53,8 @@ struct Slot {
 struct Layout {
   Slot ln1g, ln1b, ln2g, ln2b, bqkv, bo, b1, b2, wqkv, wo, w1, w2;
   Slot mlng, mlnb, wm;  // patch merging (empty unless Shape::merge): LN(2h) and [h][2h]
+  // cross-attention (empty unless Shape::cross): LN3, q / kv / out projections
+  Slot ln3g, ln3b, bq2, bkv2, bo2, wq2, wkv2, wo2;
   int64_t acc_end = 0;  // [0, acc_end): params whose grads accumulate with atomics
   int64_t total = 0;    // padded to a multiple of 64 * sdp
   int64_t shard() const { return total; }

@@ -16,22 +16,27 @@ from . import _lib
 CANONICAL_ORDER = ("ln1_g", "ln1_b", "ln2_g", "ln2_b", "b_qkv", "b_o", "b_1", "b_2",
                    "w_qkv", "w_o", "w_1", "w_2")
 MERGE_ORDER = ("mln_g", "mln_b", "w_m")  # patch-merging layers only, after w_2
+CROSS_ORDER = ("ln3_g", "ln3_b", "b_q2", "b_kv2", "b_o2", "w_q2", "w_kv2", "w_o2")  # decoders
 
 
 def pack_canonical(P: dict) -> np.ndarray:
     """Layer parameter dict (oracle naming) -> canonical flat fp32 vector."""
-    keys = CANONICAL_ORDER + (MERGE_ORDER if "w_m" in P else ())
+    keys = CANONICAL_ORDER + (MERGE_ORDER if "w_m" in P else ()) + \
+        (CROSS_ORDER if "w_q2" in P else ())
     return np.concatenate([np.asarray(P[k], dtype=np.float32).ravel() for k in keys])
 
 
-def unpack_canonical(flat: np.ndarray, hidden: int, ffn: int, merge: bool = False) -> dict:
+def unpack_canonical(flat: np.ndarray, hidden: int, ffn: int, merge: bool = False,
+                     cross: bool = False) -> dict:
     h, f = hidden, ffn
     shapes = {"ln1_g": (h,), "ln1_b": (h,), "ln2_g": (h,), "ln2_b": (h,), "b_qkv": (3 * h,),
               "b_o": (h,), "b_1": (f,), "b_2": (h,), "w_qkv": (3 * h, h), "w_o": (h, h),
               "w_1": (f, h), "w_2": (h, f),
-              "mln_g": (2 * h,), "mln_b": (2 * h,), "w_m": (h, 2 * h)}
+              "mln_g": (2 * h,), "mln_b": (2 * h,), "w_m": (h, 2 * h),
+              "ln3_g": (h,), "ln3_b": (h,), "b_q2": (h,), "b_kv2": (2 * h,), "b_o2": (h,),
+              "w_q2": (h, h), "w_kv2": (2 * h, h), "w_o2": (h, h)}
     out, off = {}, 0
-    for k in CANONICAL_ORDER + (MERGE_ORDER if merge else ()):
+    for k in CANONICAL_ORDER + (MERGE_ORDER if merge else ()) + (CROSS_ORDER if cross else ()):
         n = int(np.prod(shapes[k]))
         out[k] = flat[off:off + n].reshape(shapes[k])
         off += n
@@ -108,7 +113,8 @@ class PlanExecutor:
         n = ctypes.c_int64()
         _lib.lib().gx_exec_canonical_size(s["hidden"], s["ffn"], ctypes.byref(n))
         h = s["hidden"]
-        return n.value + (4 * h + 2 * h * h if s.get("merge") else 0)
+        return n.value + (4 * h + 2 * h * h if s.get("merge") else 0) + \
+            (6 * h + 4 * h * h if s.get("kind") == "decoder" else 0)
 
     def set_layer_params(self, layer: int, P: dict):
         flat = np.ascontiguousarray(pack_canonical(P))
@@ -122,7 +128,8 @@ class PlanExecutor:
             self._h, layer, {"params": 0, "grads": 1, "bf16": 2}[what],
             out.ctypes.data_as(ctypes.c_void_p), n))
         s = self.shapes[layer]
-        return unpack_canonical(out, s["hidden"], s["ffn"], bool(s.get("merge")))
+        return unpack_canonical(out, s["hidden"], s["ffn"], bool(s.get("merge")),
+                                s.get("kind") == "decoder")
 
     @property
     def stream(self) -> int:

@@ -14,7 +14,8 @@ Planner numbers:
     SURVEY.md Appendix B (UniformModel of the paper's Table 2 totals).
 Executor shapes (not in the reference; chosen here): BERT-Huge h=1280 as 20 heads x 64,
 s=512, ffn 5120; BERT-base h=768, 12 x 64, s=128, ffn 3072; ViT-Huge h=1280, 16 x 80,
-s=257, ffn 5120; T5-Large encoder h=1024, 16 x 64, s=512, ffn 4096.  Swin-like (Swin-H at
+s=257, ffn 5120; T5-Large h=1024, 16 x 64, s=512, ffn 4096, 24 encoder + 24 decoder layers
+("kind": "decoder": causal self-attention + cross-attention).  Swin-like (Swin-H at
 224 px, the fixture's 2/2/26/2 stages): hidden 320/640/1280/2560 as heads x 32, token grids
 56/28/14/7 stored window-major with 7x7 windows ("kind": "window", W-MSA), ffn 4h; the first
 layer of stages 2-4 starts with patch merging ("merge": true).
@@ -51,6 +52,16 @@ def layer_param_count(shape) -> int:
     return 3 * h * h + 3 * h + h * h + h + h * f + f + f * h + h + 4 * h
 
 
+def _t5(n, param_bytes, act_bytes, fwd_ms, shape):
+    """T5 flattened into one layer list: n/2 encoder layers, then n/2 decoder
+    layers (causal self-attention + cross-attention over the encoder output + MLP).  The
+    planner numbers stay uniform, as in the paper's Table 2 totals."""
+    m = _uniform(n, param_bytes, act_bytes, fwd_ms, shape)
+    for layer in m["layers"][n // 2:]:
+        layer["shape"]["kind"] = "decoder"
+    return m
+
+
 def _swin():
     spec = [  # (count, hidden, param_bytes, act_bytes, fwd_ms) per reference fixture stage
         (2, 320, 4915200, 78142034, 0.9),
@@ -77,8 +88,8 @@ _CATALOG = {
     "bert-huge-32": lambda: _uniform(32, 84000000, 103199211, 1.5, _shape(1280, 20, 512, 5120)),
     "vit-huge-32": lambda: _uniform(32, 632e6 * 4 / 32, 646.5 * MiB / 32, 1.5,
                                     _shape(1280, 16, 257, 5120)),
-    "t5-large-48": lambda: _uniform(48, 737e6 * 4 / 48, 6107.75 * MiB / 48, 1.5,
-                                    _shape(1024, 16, 512, 4096)),
+    "t5-large-48": lambda: _t5(48, 737e6 * 4 / 48, 6107.75 * MiB / 48, 1.5,
+                               _shape(1024, 16, 512, 4096)),
     "swin-like": _swin,
 }
 

@@ -34,9 +34,11 @@ def _small_model(L=4, h=256, heads=4, seq=64, ffn=512):
 
 
 def _oshape(shp):
+    kind = shp.get("kind", "encoder")
     return lo.LayerShape(shp["hidden"], shp["heads"], shp["seq"], shp["ffn"],
-                         shp.get("window", 0) if shp.get("kind") == "window" else 0,
-                         bool(shp.get("merge", False)))
+                         shp.get("window", 0) if kind == "window" else 0,
+                         bool(shp.get("merge", False)), kind in ("causal", "decoder"),
+                         kind == "decoder")
 
 
 def _run_case(plan, model, world, p_drop=0.0, seed=11, optimizer=False):
@@ -285,4 +287,53 @@ def test_patch_merging_rejects_bad_shapes(cuda):
     m = _swin_like()
     m["layers"][2]["shape"]["merge"] = False
     with pytest.raises(Exception, match="input shape differs"):
+        gxe.PlanExecutor(gxe.make_plan([""] * 4, 2), m, 1)
+
+
+def _t5_like(n_enc=2, n_dec=2, h=256, heads=4, seq=64, ffn=512, dec_kind="decoder"):
+    """Flattened encoder-decoder: encoder layers, then decoder layers whose
+    cross-attention reads the first decoder layer's input (the encoder output)."""
+    m = _small_model(n_enc + n_dec, h, heads, seq, ffn)
+    for layer in m["layers"][n_enc:]:
+        layer["shape"]["kind"] = dec_kind
+    return m
+
+
+T5_CASES = [
+    # (world, strategies, batch, pp, micro_batches, stage bounds)
+    (1, ["", "", "", ""], 2, 1, 1, None),
+    (2, ["dp:2", "tp:2", "sdp:2", "dp:2"], 4, 1, 1, None),
+    (4, ["tp:2,sdp:2", "dp:4", "sdp:4", "dp:4"], 4, 1, 2, None),
+    (2, ["", "", "", ""], 4, 2, 2, [0, 2, 4]),          # decoder = stage 1 (searched T5 split)
+    (8, ["dp:4", "sdp:4", "dp:4", "sdp:4"], 8, 2, 8, [0, 2, 4]),  # 1-sample micro-batches
+]
+
+
+@pytest.mark.parametrize("case", T5_CASES, ids=lambda c: f"N{c[0]}-{'|'.join(s or 'serial' for s in c[1])}-P{c[3]}m{c[4]}")
+@pytest.mark.parametrize("p_drop", [0.0, 0.1])
+def test_t5_decoder_plans(cuda, case, p_drop):
+    """T5 decoder layers: causal self-attention, cross-attention over the memory, MLP; the
+    memory gradient summed over the decoder layers flows into the encoder."""
+    world, strategies, B, P, m, bounds = case
+    out = _run_case(gxe.make_plan(strategies, B, P, m, bounds), _t5_like(), world, p_drop)
+    _check(out)
+    assert {"w_q2", "w_kv2", "w_o2", "ln3_g"} <= set(out["grads"][2][1])
+
+
+@pytest.mark.parametrize("strategies,world", [(["", "", ""], 1), (["tp:2", "sdp:2", "tp:2"], 2)])
+def test_causal_decoder_only_layers(cuda, strategies, world):
+    """kind "causal": GPT-style decoder-only layers (causal self-attention), TP included."""
+    m = _t5_like(0, 3, dec_kind="causal")
+    _check(_run_case(gxe.make_plan(strategies, 2), m, world, 0.1))
+
+
+def test_decoder_plan_restrictions(cuda):
+    with pytest.raises(Exception, match="without tensor parallelism"):
+        gxe.PlanExecutor(gxe.make_plan(["dp:2", "dp:2", "tp:2", "tp:2"], 2), _t5_like(), 2)
+    with pytest.raises(Exception, match="share one pipeline stage"):
+        gxe.PlanExecutor(gxe.make_plan([""] * 4, 2, 2, 2, [0, 3, 4]), _t5_like(), 2)
+    m = _t5_like()
+    m["layers"][1]["shape"]["kind"] = "decoder"
+    m["layers"][2]["shape"]["kind"] = "encoder"
+    with pytest.raises(Exception, match="last layers"):
         gxe.PlanExecutor(gxe.make_plan([""] * 4, 2), m, 1)

@@ -53,7 +53,16 @@ def _torch_merge(x, P, shape):
     return m @ P["w_m"].T
 
 
-def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0):
+def _torch_mha(q2, k2, v2, n, s, H, d, am, ka, causal):
+    q, k, v = (t.reshape(n, s, H, d).transpose(1, 2) for t in (q2, k2, v2))
+    sc = q @ k.transpose(-1, -2) / math.sqrt(d)
+    if causal:
+        sc = sc.masked_fill(torch.ones(s, s, dtype=torch.bool).triu(1), -math.inf)
+    pr = torch.softmax(sc, -1)
+    return (pr * am * ka @ v).transpose(1, 2).reshape(n * s, H * d)
+
+
+def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0, memory=None, n_layers=0):
     if shape.merge:
         x = _torch_merge(x, P, shape)
     h, H, d, s = shape.hidden, shape.heads, shape.head_dim, shape.att_seq
@@ -62,14 +71,20 @@ def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0):
     ln = lambda t, g, b: torch.nn.functional.layer_norm(t, (h,), g, b, 1e-5)  # noqa: E731
     a = ln(x, P["ln1_g"], P["ln1_b"])
     qkv = a @ P["w_qkv"].T + P["b_qkv"]
-    q, k, v = (qkv[:, i * h:(i + 1) * h].reshape(n, s, H, d).transpose(1, 2) for i in range(3))
-    pr = torch.softmax(q @ k.transpose(-1, -2) / math.sqrt(d), -1)
     am = torch.from_numpy(lo._attn_mask(drop, 3 * layer_id, n, H, s, sample_offset * nw)).double()
     ka = lo.dropout_scale(drop.p_attn)
-    ctx = (pr * am * ka @ v).transpose(1, 2).reshape(n * s, h)
+    ctx = _torch_mha(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], n, s, H, d, am, ka, shape.causal)
     kh = lo.dropout_scale(drop.p_hidden)
     m1 = torch.from_numpy(lo._hidden_mask(drop, 3 * layer_id + 1, n * s, h, sample_offset * S)).double()
     x1 = x + (ctx @ P["w_o"].T + P["b_o"]) * m1 * kh
+    if shape.cross:
+        sa, sh = lo.cross_sites(layer_id, n_layers)
+        q2 = ln(x1, P["ln3_g"], P["ln3_b"]) @ P["w_q2"].T + P["b_q2"]
+        kv2 = memory @ P["w_kv2"].T + P["b_kv2"]
+        am2 = torch.from_numpy(lo._attn_mask(drop, sa, n, H, s, sample_offset)).double()
+        ctx2 = _torch_mha(q2, kv2[:, :h], kv2[:, h:], n, s, H, d, am2, ka, False)
+        m3 = torch.from_numpy(lo._hidden_mask(drop, sh, n * s, h, sample_offset * S)).double()
+        x1 = x1 + (ctx2 @ P["w_o2"].T + P["b_o2"]) * m3 * kh
     c = ln(x1, P["ln2_g"], P["ln2_b"])
     g = torch.nn.functional.gelu(c @ P["w_1"].T + P["b_1"])
     m2 = torch.from_numpy(lo._hidden_mask(drop, 3 * layer_id + 2, n * s, h, sample_offset * S)).double()
@@ -111,3 +126,36 @@ def test_golden_vectors():
     assert np.allclose(dx, z["dx"], rtol=0, atol=1e-12)
     for k in G:
         assert np.allclose(G[k], z["G_" + k], rtol=0, atol=1e-12)
+
+
+
+@pytest.mark.parametrize("p", [0.0, 0.1])
+def test_t5_encoder_decoder_model_matches_autograd(p):
+    """Encoder + causal decoder layers with cross-attention over the memory (the first decoder
+    layer's input), MSE loss: loss, dx and every parameter gradient vs torch.autograd."""
+    rng = np.random.default_rng(5)
+    enc = lo.LayerShape(hidden=32, heads=2, seq=8, ffn=64)
+    dec = lo.LayerShape(hidden=32, heads=2, seq=8, ffn=64, causal=True, cross=True)
+    shapes = [enc, enc, dec, dec]
+    params = [lo.init_layer_params(sh, rng, std=0.2) for sh in shapes]
+    x = rng.standard_normal((3 * 8, 32))
+    t = rng.standard_normal((3 * 8, 32))
+    drop = lo.Dropout(p, p, 21)
+    loss, y, dx, grads = lo.model_step(params, x, t, shapes, drop, sample_offset=2)
+
+    tP = [{k: torch.tensor(v, requires_grad=True) for k, v in P.items()} for P in params]
+    tx = torch.tensor(x, requires_grad=True)
+    hcur, mem = tx, None
+    for l, sh in enumerate(shapes):
+        if sh.cross and mem is None:
+            mem = hcur
+        hcur = _torch_layer(tP[l], hcur, sh, drop, l, 2, mem, len(shapes))
+    tl = ((hcur - torch.tensor(t)) ** 2).sum() / hcur.numel()
+    tl.backward()
+    assert abs(loss - tl.item()) <= 1e-10 * abs(loss)
+    assert np.allclose(y, hcur.detach().numpy(), rtol=1e-10, atol=1e-12)
+    assert np.allclose(dx, tx.grad.numpy(), rtol=1e-8, atol=1e-12)
+    for l in range(len(shapes)):
+        assert set(grads[l]) == set(params[l])
+        for k in params[l]:
+            assert np.allclose(grads[l][k], tP[l][k].grad.numpy(), rtol=1e-8, atol=1e-12), (l, k)
