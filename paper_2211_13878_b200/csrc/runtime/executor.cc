@@ -249,6 +249,13 @@ struct RankCtx {
   bf16 *dout2 = nullptr, *dqkv2 = nullptr;
   float* dmem = nullptr;
   int dec_li = -1;  // local index of the model's first decoder layer on this rank, or -1
+  // stages after the first decoder layer's: the memory received with each micro-batch's
+  // activations, and whether dL/dmem arrives from the next (decoder) stage in backward
+  std::vector<bf16*> mem_in;
+  bool dmem_from_next = false;
+  const bf16* mem(int mb) const {
+    return dec_li >= 0 ? layers[dec_li].acts[mb].x : mem_in[mb];
+  }
   float* cs_ws[2] = {nullptr, nullptr};  // column-sum workspaces: [0] main stream, [1] wgrad stream
   float* acc32 = nullptr;  // split-K fp32 slices [kMaxSplits][rows][h]
   bf16 *x_in = nullptr, *target = nullptr;  // [m micro-batches of this rank's rows][h]
@@ -743,10 +750,11 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
           return kErrConfig;
         }
         const Shape& s0 = shape_[dec0_];
-        if (stage_of_layer(l) != stage_of_layer(dec0_) || d.data() != deg_[dec0_].data() ||
-            s.h != s0.h || s.seq != s0.seq) {
-          *err = "executor: decoder layers must share one pipeline stage, data degree and "
-                 "shape (the memory is the first decoder layer's input)";
+        // the memory (the first decoder layer's input) travels with the activations across
+        // the decoder's stage boundaries, chunked like them: one data degree and shape
+        if (d.data() != deg_[dec0_].data() || s.h != s0.h || s.seq != s0.seq) {
+          *err = "executor: decoder layers must share one data degree and shape (the memory "
+                 "is the first decoder layer's input)";
           return kErrConfig;
         }
       } else if (dec0_ >= 0) {
@@ -1014,6 +1022,14 @@ int ExecutorImpl::allocate(RankCtx& r) {
     r.dmem = A.a<float>(max_x);
     for (size_t i = 0; i < r.layers.size(); ++i)
       if (r.layers[i].layer == dec0_) r.dec_li = static_cast<int>(i);
+    const int s0 = stage_of_layer(dec0_);
+    r.dmem_from_next = r.stage >= s0 && r.stage + 1 < P_;
+    if (r.stage > s0) {
+      r.mem_in.resize(m_);
+      for (int mb = 0; mb < m_; ++mb)
+        r.mem_in[mb] = A.a<bf16>(static_cast<int64_t>(r.layers.front().acts[mb].rows) *
+                                 r.layers.front().sh.h);
+    }
   }
   r.acc32 = A.a<float>(static_cast<int64_t>(kMaxSplits) * max_h);
   {
@@ -1733,7 +1749,7 @@ int ExecutorImpl::cross_fwd(RankCtx& r, int li, int mb, bool ln3_ready) {
   const int rows = A.rows, h = s.h;
   const bf16* P = L.pfull;
   const int l = L.layer;
-  const bf16* mem = r.layers[r.dec_li].acts[mb].x;
+  const bf16* mem = r.mem(mb);
   if (!ln3_ready)
     GX_TRY(timed(kNorm, 0, 4.0 * rows * h, [&] {
       return layernorm_fwd(A.x1, P + L.lay.ln3g.off, P + L.lay.ln3b.off, A.ln3, A.mean3, A.rstd3,
@@ -1808,7 +1824,7 @@ int ExecutorImpl::cross_bwd(RankCtx& r, int li, int mb, bf16* dout,
   const bf16* P = L.pfull;
   float* G = L.gfull;
   const int l = L.layer;
-  const bf16* mem = r.layers[r.dec_li].acts[mb].x;
+  const bf16* mem = r.mem(mb);
   gx_gemm_epilogue c = epi();
   c.out_kind = kOutBF16;
   c.out = r.dctx;
@@ -1827,7 +1843,8 @@ int ExecutorImpl::cross_bwd(RankCtx& r, int li, int mb, bf16* dout,
   GX_TRY(gemm(r.dqkv2 + h, 3 * h, true, mem, h, true, 2 * h, h, rows, wgrad_ep(L.lay.wkv2, h)));
   // memory gradient: the last decoder layer (first in backward) starts the sum
   gx_gemm_epilogue m = epi();
-  m.out_kind = li + 1 == static_cast<int>(r.layers.size()) ? kOutF32 : kOutF32Accumulate;
+  m.out_kind = li + 1 == static_cast<int>(r.layers.size()) && !r.dmem_from_next
+                   ? kOutF32 : kOutF32Accumulate;
   m.out = r.dmem;
   m.ldo = h;
   GX_TRY(gemm(r.dqkv2 + h, 3 * h, false, P + L.lay.wkv2.off, h, true, rows, h, 2 * h, m));
@@ -2084,6 +2101,11 @@ int ExecutorImpl::pp_fwd(RankCtx& r, int mb, bool send) {
     } else {
       GX_TRY(comm_->recv(r.rank, x.peer, my.in() + off, bytes, stream_));
     }
+    // decoder stages: the memory follows, same rows (decoders share data degree and shape)
+    if (send && dec0_ >= 0 && r.stage >= stage_of_layer(dec0_))
+      GX_TRY(comm_->send(r.rank, x.peer, r.mem(mb) + off, bytes, stream_));
+    if (!send && !r.mem_in.empty())
+      GX_TRY(comm_->recv(r.rank, x.peer, r.mem_in[mb] + off, bytes, stream_));
   }
   return kOk;
 }
@@ -2103,6 +2125,11 @@ int ExecutorImpl::pp_bwd(RankCtx& r, int mb, bool send) {
     } else {
       GX_TRY(comm_->recv(r.rank, x.peer, r.gbuf[r.cur] + off, bytes, stream_));
     }
+    // decoder stages: dL/dmemory summed over this stage's decoder layers goes back (fp32)
+    if (send && !r.mem_in.empty())
+      GX_TRY(comm_->send(r.rank, x.peer, r.dmem + off, bytes * 2, stream_));
+    if (!send && r.dmem_from_next)
+      GX_TRY(comm_->recv(r.rank, x.peer, r.dmem + off, bytes * 2, stream_));
   }
   return kOk;
 }

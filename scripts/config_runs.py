@@ -3,7 +3,7 @@
   config 3  ViT-Huge-32 (s 257, 16 x 80 heads): hand plan [tp:2,sdp:4] x32
   config 4  T5-Large-48 (24 encoder + 24 decoder layers, flattened per SPEC.md:67): the
             searched 8-GPU / 8 GiB plan (P=2, m=8, decoder = stage 1) and hand P=4 / P=8 splits
-            (decoder layers there as causal self-attention: cross-attention needs one stage)
+            (the memory travels with the activations across the decoder's stage boundaries)
   config 5  Swin fixture: the searched [dp:8] x6 | [sdp:8] x24 | [tp:2,sdp:4] x2 (B=64)
 
 Every rank of the world runs in this process on cuda:0 (comm "sim"), so ms/step is the sum
@@ -30,21 +30,15 @@ from paper_2211_13878_b200 import models, planner  # noqa: E402
 def _runs():
     api = planner.api()
     t5 = models.model("t5-large-48")
-    # cross-attention layers must share one pipeline stage (the memory is not forwarded
-    # between stages yet): P=4 / P=8 split the decoder, so run its layers without cross
-    t5c = models.model("t5-large-48")
-    for layer in t5c["layers"]:
-        if layer["shape"]["kind"] == "decoder":
-            layer["shape"]["kind"] = "causal"
     swin = models.model("swin-like")
     return {
         "vit": ("config 3: ViT-Huge-32", models.model("vit-huge-32"),
                 gxe.make_plan(["tp:2,sdp:4"] * 32, 8), 8),
         "t5p2": ("config 4: T5-Large-48 searched (8 GPUs, 8 GiB)", t5,
                  api.optimize(t5, models.cluster(8, 8)).plan, 8),
-        "t5p4": ("config 4: T5-Large-48 P=4 (decoders as causal self-attention only)", t5c,
+        "t5p4": ("config 4: T5-Large-48 P=4", t5,
                  gxe.make_plan(["sdp:2"] * 48, 8, pp_degree=4, micro_batches=8), 8),
-        "t5p8": ("config 4: T5-Large-48 P=8 (decoders as causal self-attention only)", t5c,
+        "t5p8": ("config 4: T5-Large-48 P=8", t5,
                  gxe.make_plan([""] * 48, 8, pp_degree=8, micro_batches=8), 8),
         "swin": ("config 5: Swin fixture searched (8 GPUs, 8 GiB)", swin,
                  api.optimize(swin, models.cluster(8, 8)).plan, 8),

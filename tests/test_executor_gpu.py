@@ -306,6 +306,10 @@ T5_CASES = [
     (4, ["tp:2,sdp:2", "dp:4", "sdp:4", "dp:4"], 4, 1, 2, None),
     (2, ["", "", "", ""], 4, 2, 2, [0, 2, 4]),          # decoder = stage 1 (searched T5 split)
     (8, ["dp:4", "sdp:4", "dp:4", "sdp:4"], 8, 2, 8, [0, 2, 4]),  # 1-sample micro-batches
+    # decoder split over stages: the memory travels with the activations, dL/dmem back
+    (2, ["", "", "", ""], 2, 2, 2, [0, 3, 4]),
+    (4, ["", "", "", ""], 4, 4, 4, [0, 1, 2, 3, 4]),
+    (8, ["dp:4", "sdp:4", "sdp:4", "dp:4"], 8, 2, 4, [0, 3, 4]),
 ]
 
 
@@ -330,8 +334,10 @@ def test_causal_decoder_only_layers(cuda, strategies, world):
 def test_decoder_plan_restrictions(cuda):
     with pytest.raises(Exception, match="without tensor parallelism"):
         gxe.PlanExecutor(gxe.make_plan(["dp:2", "dp:2", "tp:2", "tp:2"], 2), _t5_like(), 2)
-    with pytest.raises(Exception, match="share one pipeline stage"):
-        gxe.PlanExecutor(gxe.make_plan([""] * 4, 2, 2, 2, [0, 3, 4]), _t5_like(), 2)
+    m = _t5_like()
+    m["layers"][3]["shape"].update(hidden=128, head_dim=32)
+    with pytest.raises(Exception, match="share one data degree and shape"):
+        gxe.PlanExecutor(gxe.make_plan([""] * 4, 2), m, 1)
     m = _t5_like()
     m["layers"][1]["shape"]["kind"] = "decoder"
     m["layers"][2]["shape"]["kind"] = "encoder"
