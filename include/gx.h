@@ -241,6 +241,10 @@ typedef struct gx_attention_args {
                                   written by fwd, read by bwd (when dropout is on) */
   unsigned long long* trace;   /* debug: per-CTA %globaltimer stamps (tcgen05 kernels), or NULL */
   int causal;                  /* 1: query q attends keys k <= q only (decoder self-attention) */
+  /* Swin shifted windows (SW-MSA): with win_shift > 0 the batch is samples x (grid/side)^2
+   * windows of side win_side over a win_grid-wide grid rolled by win_shift; q and k attend
+   * only when they come from the same region of the unrolled grid (mma.sync path). */
+  int win_grid, win_side, win_shift;
 } gx_attention_args;
 
 GX_API int gx_k_attention_fwd(const gx_attention_args* args, void* stream);
@@ -287,6 +291,10 @@ GX_API int gx_k_adamw(void* master, const void* grad, void* m, void* v, void* bf
  * backward = 1 scatters the merged gradient back.  c % 8 == 0. */
 GX_API int gx_k_patch_merge(const void* src, void* dst, int samples, int grid_out,
                             int window_side, int channels, int backward, void* stream);
+/* Swin cyclic shift between window-major layouts of a grid x grid token grid: inverse = 0
+ * rolls by -shift in both axes (torch.roll(x, (-shift, -shift))), inverse = 1 rolls back. */
+GX_API int gx_k_window_roll(const void* src, void* dst, int samples, int grid, int window_side,
+                            int shift, int channels, int inverse, void* stream);
 GX_API int gx_k_cast_bf16(const void* src, void* dst, int64_t n, void* stream);
 
 /* Split-K GEMM: out_f32[M,N] += A * B^T, each of `splits` K-slices reduce-adding its fp32

@@ -16,7 +16,9 @@ Layer (h hidden, H heads of d, f ffn; x is [tokens, h], tokens = samples * seq):
     c   = LN2(x1)
     y   = x1 + drop_h2(gelu(c W1^T + b1) W2^T + b2)  (exact erf GeLU)
 Window layers (Swin W-MSA, shape.window > 0): tokens are stored window-major and attention
-runs per window of `window` consecutive tokens.  Patch-merging layers (shape.merge) first map
+runs per window of `window` consecutive tokens; shape.shift > 0 (SW-MSA) rolls LN1's output by
+-shift in both grid axes first (roll_rows), masks q-k pairs from different regions of the rolled
+grid (shift_regions) and rolls the attention output back.  Patch-merging layers (shape.merge) first map
 their input [4*seq, h/2] to x = LN_m(gather_2x2(input)) W_m^T ([seq, h]; merge_rows).
 Dropout uses the Philox4x32-10 byte scheme of csrc/kernels/philox.cuh: one call
 philox({c lo, c hi, site lo, site hi}, {seed lo, seed hi}) yields 16 bytes; an element is
@@ -92,6 +94,7 @@ class LayerShape:
     merge: bool = False  # Swin patch merging at the input: [4*seq, hidden/2] -> [seq, hidden]
     causal: bool = False  # decoder self-attention: query q sees keys k <= q
     cross: bool = False   # T5 decoder: + cross-attention sublayer over the memory
+    shift: int = 0        # Swin SW-MSA: tokens rolled by -shift around the window attention
 
     @property
     def att_seq(self):
@@ -121,6 +124,33 @@ def merge_rows(seq: int, window: int) -> np.ndarray:
             for q, (dy, dx) in enumerate(((0, 0), (1, 0), (0, 1), (1, 1))):
                 out[t, q] = row(2 * y + dy, 2 * x + dx, 2 * g)
     return out
+
+
+def _wm_row(y, x, grid, ws):
+    return ((y // ws) * (grid // ws) + x // ws) * ws * ws + (y % ws) * ws + x % ws
+
+
+def roll_rows(seq: int, window: int, shift: int) -> np.ndarray:
+    """Window-major row permutation of torch.roll(grid, (-shift, -shift)): out[t] = in[perm[t]]
+    (csrc/kernels/patch_merge.cu window_roll)."""
+    g, ws = math.isqrt(seq), math.isqrt(window)
+    perm = np.empty(seq, dtype=np.int64)
+    for y in range(g):
+        for x in range(g):
+            perm[_wm_row(y, x, g, ws)] = _wm_row((y + shift) % g, (x + shift) % g, g, ws)
+    return perm
+
+
+def shift_regions(seq: int, window: int, shift: int) -> np.ndarray:
+    """[windows, window] region id (0..8) of each token of the rolled grid; SW-MSA lets q
+    and k attend only within one region."""
+    g, ws = math.isqrt(seq), math.isqrt(window)
+    reg = np.empty(seq, dtype=np.int64)
+    band = lambda v: 0 if v < g - ws else (1 if v < g - shift else 2)  # noqa: E731
+    for y in range(g):
+        for x in range(g):
+            reg[_wm_row(y, x, g, ws)] = 3 * band(y) + band(x)
+    return reg.reshape(seq // window, window)
 
 
 def init_layer_params(shape: LayerShape, rng: np.random.Generator, std=0.02) -> dict:
@@ -258,13 +288,21 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
     n = x.shape[0] // s                      # attention sequences
     nw = shape.seq // s                      # per sample
     a, ln1 = _ln_fwd(x, P["ln1_g"], P["ln1_b"])
-    qkv = a @ P["w_qkv"].T + P["b_qkv"]
+    ar, perm = a, None
+    if shape.shift:  # SW-MSA: roll the tokens (per sample), attend in windows, roll back
+        ns = n // nw
+        perm = (np.arange(ns)[:, None] * shape.seq + roll_rows(shape.seq, s, shape.shift)[None]).ravel()
+        ar = a[perm]
+    qkv = ar @ P["w_qkv"].T + P["b_qkv"]
     q = qkv[:, :h].reshape(n, s, H, d).transpose(0, 2, 1, 3)
     k = qkv[:, h:2 * h].reshape(n, s, H, d).transpose(0, 2, 1, 3)
     v = qkv[:, 2 * h:].reshape(n, s, H, d).transpose(0, 2, 1, 3)
     sc = q @ k.transpose(0, 1, 3, 2) / math.sqrt(d)
     if shape.causal:
         sc = np.where(np.triu(np.ones((s, s), dtype=bool), 1), -np.inf, sc)
+    if shape.shift:
+        reg = np.tile(shift_regions(shape.seq, s, shape.shift), (n // nw, 1))  # [n, s]
+        sc = np.where((reg[:, :, None] != reg[:, None, :])[:, None], -np.inf, sc)
     sc = sc - sc.max(-1, keepdims=True)
     pr = np.exp(sc)
     pr = pr / pr.sum(-1, keepdims=True)
@@ -273,6 +311,10 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
     pd = pr * am * ka
     ctx4 = pd @ v
     ctx = ctx4.transpose(0, 2, 1, 3).reshape(n * s, h)
+    if perm is not None:
+        ctx_u = np.empty_like(ctx)
+        ctx_u[perm] = ctx
+        ctx = ctx_u
     o = ctx @ P["w_o"].T + P["b_o"]
     m1 = _hidden_mask(drop, 3 * layer_id + 1, n * s, h, sample_offset * shape.seq)
     kh = dropout_scale(drop.p_hidden)
@@ -295,7 +337,7 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
     z = g @ P["w_2"].T + P["b_2"]
     m2 = _hidden_mask(drop, 3 * layer_id + 2, n * s, h, sample_offset * shape.seq)
     y = xr + z * m2 * kh
-    cache = dict(x=x, a=a, ln1=ln1, q=q, k=k, v=v, pr=pr, am=am, ka=ka, pd=pd, ctx=ctx, m1=m1,
+    cache = dict(x=x, a=ar, ln1=ln1, perm=perm, q=q, k=k, v=v, pr=pr, am=am, ka=ka, pd=pd, ctx=ctx, m1=m1,
                  kh=kh, x1=x1, c=c, ln2=ln2, pre=pre, g=g, m2=m2, n=n, **mcache, **xcache)
     return y, cache
 
@@ -331,6 +373,9 @@ def layer_backward(P: dict, dy: np.ndarray, cache: dict, shape: LayerShape):
     G["b_o"] = do.sum(0)
     G["w_o"] = do.T @ cache["ctx"]
     dctx = do @ P["w_o"]
+    perm = cache["perm"]
+    if perm is not None:
+        dctx = dctx[perm]
     dctx4 = dctx.reshape(n, s, H, d).transpose(0, 2, 1, 3)
     dv = cache["pd"].transpose(0, 1, 3, 2) @ dctx4
     dpd = dctx4 @ cache["v"].transpose(0, 1, 3, 2)
@@ -345,6 +390,10 @@ def layer_backward(P: dict, dy: np.ndarray, cache: dict, shape: LayerShape):
     G["b_qkv"] = dqkv.sum(0)
     G["w_qkv"] = dqkv.T @ cache["a"]
     da = dqkv @ P["w_qkv"]
+    if perm is not None:
+        da_u = np.empty_like(da)
+        da_u[perm] = da
+        da = da_u
     dx_ln, G["ln1_g"], G["ln1_b"] = _ln_bwd(da, cache["ln1"], P["ln1_g"])
     dx = dx1 + dx_ln
     if shape.merge:

@@ -81,6 +81,18 @@ __device__ __forceinline__ void load_tile(__nv_bfloat16* dst, const __nv_bfloat1
   }
 }
 
+// Swin shifted-window region (0..8) of token `tok` of attention sequence (window) `b`: the
+// window's position in the rolled grid gives the token's (y, x); rows / columns within
+// `side` of the far edge came from the other side of the grid (SW-MSA attention mask).
+__device__ __forceinline__ int swin_region(const gx_attention_args& p, int b, int tok) {
+  const int nw = p.win_grid / p.win_side;
+  const int w = b % (nw * nw);
+  const int y = (w / nw) * p.win_side + tok / p.win_side;
+  const int x = (w % nw) * p.win_side + tok % p.win_side;
+  const int l0 = p.win_grid - p.win_side, l1 = p.win_grid - p.win_shift;
+  return (y < l0 ? 0 : (y < l1 ? 1 : 2)) * 3 + (x < l0 ? 0 : (x < l1 ? 1 : 2));
+}
+
 }  // namespace
 
 // --------------------------------------------------------------------------- forward
@@ -166,7 +178,11 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_a
       for (int j = 0; j < 4; ++j) {
         const int key = kb * kBlk + nb * 8 + 2 * t + (j & 1);
         float v = sacc[nb][j] * c2;
-        if (key >= s || (p.causal && key > q0 + warp * 16 + g + 8 * (j >> 1))) v = -INFINITY;
+        const int qrow = q0 + warp * 16 + g + 8 * (j >> 1);
+        if (key >= s || (p.causal && key > qrow) ||
+            (p.win_shift > 0 && key < s && qrow < s &&
+             swin_region(p, b, qrow) != swin_region(p, b, key)))
+          v = -INFINITY;
         sacc[nb][j] = v;
         mx[j >> 1] = fmaxf(mx[j >> 1], v);
       }
@@ -389,8 +405,9 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
         const int ql = nb * 8 + 2 * t + (j & 1);
         const int q = q0 + ql;
         const int key = k0 + warp * 16 + g + 8 * (j >> 1);
-        float P = (q < s && key < s && !(p.causal && key > q)) ? exp2f(st[nb][j] * c2 - sL[ql])
-                                                                : 0.f;
+        const bool keep_pk = q < s && key < s && !(p.causal && key > q) &&
+                             !(p.win_shift > 0 && swin_region(p, b, q) != swin_region(p, b, key));
+        float P = keep_pk ? exp2f(st[nb][j] * c2 - sL[ql]) : 0.f;
         float keep = 1.f;
         if (thr != 0u) {
           const int kk = key - k0;  // 0..63 within this CTA's key block

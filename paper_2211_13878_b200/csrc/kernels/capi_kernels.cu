@@ -115,3 +115,9 @@ extern "C" int gx_k_patch_merge(const void* src, void* dst, int samples, int gri
   return gx::patch_merge(src, dst, samples, grid_out, window_side, channels, backward != 0,
                          S(stream));
 }
+extern "C" int gx_k_window_roll(const void* src, void* dst, int samples, int grid,
+                                int window_side, int shift, int channels, int inverse,
+                                void* stream) {
+  return gx::window_roll(src, dst, samples, grid, window_side, shift, channels, inverse != 0,
+                         S(stream));
+}

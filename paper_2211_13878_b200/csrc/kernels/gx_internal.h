@@ -157,6 +157,10 @@ int init_params(float* master, int64_t n, const InitLayout& L, uint64_t seed, ui
 // [rows_out][4c] back to [4*rows_out][c] (a permutation: every input row written once).
 int patch_merge(const void* src, void* dst, int samples, int grid_out, int ws, int c,
                 bool backward, cudaStream_t st);
+// Swin cyclic shift (torch.roll by -shift in both grid axes) between window-major layouts;
+// inverse rolls back.  A row permutation: every row copied once.
+int window_roll(const void* src, void* dst, int samples, int grid, int ws, int shift, int c,
+                bool inverse, cudaStream_t st);
 int num_sms();
 
 }  // namespace gx

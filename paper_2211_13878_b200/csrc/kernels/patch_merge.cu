@@ -52,7 +52,44 @@ __global__ void patch_merge_kernel(const uint4* __restrict__ src, uint4* __restr
   }
 }
 
+__global__ void window_roll_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                   int64_t total, int seq, int grid, int ws, int shift, int cv,
+                                   bool inverse) {
+  pdl_enter();
+  const int win = ws * ws, wpr = grid / ws;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int v = static_cast<int>(i % cv);
+    const int64_t row = i / cv;
+    const int64_t b = row / seq;
+    const int t = static_cast<int>(row % seq);
+    const int w = t / win, p = t % win;
+    const int y = (w / wpr) * ws + p / ws, x = (w % wpr) * ws + p % ws;
+    // output token (y, x) takes the input token shifted by +shift (roll by -shift) or by
+    // -shift (the inverse roll)
+    const int d = inverse ? grid - shift : shift;
+    const int64_t src_row = b * seq + wm_row((y + d) % grid, (x + d) % grid, grid, ws);
+    dst[i] = src[src_row * cv + v];
+  }
+}
+
 }  // namespace
+
+int window_roll(const void* src, void* dst, int samples, int grid, int ws, int shift, int c,
+                bool inverse, cudaStream_t st) {
+  if (c % 8 != 0 || ws <= 0 || grid % ws != 0 || shift <= 0 || shift >= ws)
+    return set_error(kErrConfig, "window_roll: channels % 8, grid tiled by windows, 0 < shift < side");
+  const int seq = grid * grid;
+  const int cv = c / 8;
+  const int64_t total = static_cast<int64_t>(samples) * seq * cv;
+  if (total == 0) return kOk;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > num_sms() * 8) blocks = num_sms() * 8;
+  launch_k(window_roll_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st,
+           static_cast<const uint4*>(src), static_cast<uint4*>(dst), total, seq, grid, ws, shift,
+           cv, inverse);
+  return check_launch("window_roll_kernel");
+}
 
 int patch_merge(const void* src, void* dst, int samples, int grid_out, int ws, int c,
                 bool backward, cudaStream_t st) {

@@ -199,6 +199,7 @@ struct Acts {
   bf16 *xm = nullptr, *mg = nullptr, *mln = nullptr;
   float *meanm = nullptr, *rstdm = nullptr;
   bf16* in() const { return xm != nullptr ? xm : x; }  // what the previous layer feeds
+  bf16 *ln1r = nullptr, *ctxr = nullptr;  // SW-MSA: LN1 output / context in rolled order
   // decoder cross-attention sublayer: x2 = x1 + drop(attn(LN3(x1) Wq2, mem Wkv2) Wo2 + bo2)
   bf16 *x2 = nullptr, *ln3 = nullptr, *qkv2 = nullptr, *ctx2 = nullptr;
   float *lse2 = nullptr, *mean3 = nullptr, *rstd3 = nullptr;
@@ -247,6 +248,7 @@ struct RankCtx {
   // memory gradient accumulated over the decoder layers (fp32, added to the first decoder
   // layer's input gradient)
   bf16 *dout2 = nullptr, *dqkv2 = nullptr;
+  bf16 *dctxr = nullptr, *rollbuf = nullptr;  // SW-MSA backward scratch (rolled dctx, da)
   float* dmem = nullptr;
   int dec_li = -1;  // local index of the model's first decoder layer on this rank, or -1
   // stages after the first decoder layer's: the memory received with each micro-batch's
@@ -336,6 +338,19 @@ class ExecutorImpl final : public Executor {
   int fwd_phase(RankCtx& r, int li, int mb, int phase);
   int bwd_phase(RankCtx& r, int li, int mb, int phase);
   int merge_bwd(RankCtx& r, RankLayer& L, Acts& A, bf16* dX, const gx_gemm_epilogue& wm_ep);
+  static int grid_of(const Shape& s) {
+    return static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.seq))));
+  }
+  static int side_of(const Shape& s) {
+    return static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.win))));
+  }
+  static void set_window_mask(gx_attention_args& at, const Shape& s) {
+    if (s.shift > 0) {
+      at.win_grid = grid_of(s);
+      at.win_side = side_of(s);
+      at.win_shift = s.shift;
+    }
+  }
   int cross_fwd(RankCtx& r, int li, int mb, bool ln3_ready);
   int cross_bwd(RankCtx& r, int li, int mb, bf16* dout,
                 const std::function<gx_gemm_epilogue(const Slot&, int64_t)>& wgrad_ep);
@@ -690,6 +705,15 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
         *err = "executor: layer kind '" + kind + "' not supported (encoder, causal, decoder, window)";
         return kErrConfig;
       }
+      if (kind == "window" && sh.value("shift", false)) {  // SW-MSA (Swin's odd blocks)
+        const int g = static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.seq))));
+        const int ws = static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.win))));
+        if (g * g != s.seq || ws * ws != s.win || g % ws != 0) {
+          *err = "executor: shifted windows need a square token grid tiled by square windows";
+          return kErrConfig;
+        }
+        s.shift = g > ws ? ws / 2 : 0;  // one window covers the grid: Swin skips the shift
+      }
       s.merge = sh.value("merge", false);
       if (s.merge) {
         const int g = static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.seq))));
@@ -907,6 +931,7 @@ int ExecutorImpl::allocate(RankCtx& r) {
   A.set_cap(static_cast<size_t>(mem_cap_));
   int64_t max_rows = 0, max_h = 0, max_f = 0, max_q = 0, max_c = 0, max_lse = 0, max_m = 0,
           max_x = 0;
+  bool any_shift = false;
   for (size_t li = 0; li < r.layers.size(); ++li) {
     RankLayer& L = r.layers[li];
     const Shape& s = L.sh;
@@ -977,6 +1002,11 @@ int ExecutorImpl::allocate(RankCtx& r) {
         a.rstd3 = A.a<float>(rows);
         max_x = std::max(max_x, rows * h);
       }
+      if (s.shift > 0) {
+        a.ln1r = A.a<bf16>(rows * h);
+        a.ctxr = A.a<bf16>(rows * ht);
+        any_shift = true;
+      }
       a.lse = A.a<float>(static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq);
       if (thr_attn_ != 0u)
         a.amask = A.a<uint16_t>(static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq *
@@ -1011,6 +1041,10 @@ int ExecutorImpl::allocate(RankCtx& r) {
   r.gbuf[0] = A.a<bf16>(max_h);
   r.gbuf[1] = A.a<bf16>(max_h);
   r.dq_acc = A.a<float>(4 * max_c);  // tcgen05 attention: one dQ partial per 128-key tile
+  if (any_shift) {
+    r.dctxr = A.a<bf16>(max_c);
+    r.rollbuf = A.a<bf16>(max_h);
+  }
   if (max_x > 0) {
     int64_t hx = 0;
     for (const RankLayer& L : r.layers) hx = std::max<int64_t>(hx, L.sh.h);
@@ -1322,12 +1356,20 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     if (!A.ln1_ready)
       GX_TRY(timed(kNorm, 0, 4.0 * rows * h, [&] { return layernorm_fwd(A.x, P + L.lay.ln1g.off, P + L.lay.ln1b.off, A.ln1, A.mean1, A.rstd1,
                            rows, h, stream_); }));
+    const bf16* qkv_in = A.ln1;
+    if (s.shift > 0) {  // SW-MSA: roll the (per-token) LN1 output, attend, roll the context back
+      GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] {
+        return window_roll(A.ln1, A.ln1r, A.samples, grid_of(s), side_of(s), s.shift, h, false,
+                           stream_);
+      }));
+      qkv_in = A.ln1r;
+    }
     gx_gemm_epilogue e = epi();
     e.out_kind = kOutBF16;
     e.out = A.qkv;
     e.ldo = 3 * ht;
     e.bias = P + L.lay.bqkv.off;
-    GX_TRY(gemm(A.ln1, h, false, P + L.lay.wqkv.off, h, false, rows, 3 * ht, h, e));
+    GX_TRY(gemm(qkv_in, h, false, P + L.lay.wqkv.off, h, false, rows, 3 * ht, h, e));
     gx_attention_args at{};
     at.batch = A.samples * s.windows();  // one attention sequence per window
     at.seq = s.win;
@@ -1339,9 +1381,10 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     at.scale = 1.f / std::sqrt(static_cast<float>(s.hd));
     at.qkv = A.qkv;
     at.ld_qkv = 3 * ht;
-    at.ctx = A.ctx;
+    at.ctx = s.shift > 0 ? A.ctxr : A.ctx;
     at.ld_ctx = ht;
     at.lse = A.lse;
+    set_window_mask(at, s);
     at.drop_threshold = thr_attn_;
     at.drop_scale = scale_of(p_attn_);
     at.seed = seed_;
@@ -1353,6 +1396,11 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
       const double af = 4.0 * A.samples * (s.heads / t) * double(s.seq) * s.win * s.hd;
       GX_TRY(timed(kAttnFwd, af, 2.0 * rows * 4 * ht, [&] { return attention_fwd(at, stream_); }));
     }
+    if (s.shift > 0)
+      GX_TRY(timed(kElementwise, 0, 4.0 * rows * ht, [&] {
+        return window_roll(A.ctxr, A.ctx, A.samples, grid_of(s), side_of(s), s.shift, ht, true,
+                           stream_);
+      }));
     gx_gemm_epilogue o = epi();
     o.out_kind = kOutBF16;
     o.ldo = h;
@@ -1639,12 +1687,18 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     at.head_offset = L.tr * (s.heads / t);
     at.sample_offset = A.sample0 * s.windows();
     at.scale = 1.f / std::sqrt(static_cast<float>(s.hd));
+    if (s.shift > 0)  // the attention saw rolled tokens: roll its output gradient likewise
+      GX_TRY(timed(kElementwise, 0, 4.0 * rows * ht, [&] {
+        return window_roll(r.dctx, r.dctxr, A.samples, grid_of(s), side_of(s), s.shift, ht,
+                           false, stream_);
+      }));
     at.qkv = A.qkv;
     at.ld_qkv = 3 * ht;
-    at.ctx = A.ctx;
+    at.ctx = s.shift > 0 ? A.ctxr : A.ctx;
     at.ld_ctx = ht;
     at.lse = A.lse;
-    at.dctx = r.dctx;
+    set_window_mask(at, s);
+    at.dctx = s.shift > 0 ? r.dctxr : r.dctx;
     at.dqkv = dqkv;
     at.dq_accum = r.dq_acc;
     at.dsum = r.dsum;
@@ -1663,12 +1717,13 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       return on_wgrad([&]() -> int {
         GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, ls_, r.cs_ws[ls_ == stream_ ? 0 : 1]); }));
         const gx_gemm_epilogue wq = wgrad_ep(L.lay.wqkv, h);
-        return gemm(dqkv, 3 * ht, true, A.ln1, h, true, 3 * ht, h, rows, wq);  // dWqkv
+        return gemm(dqkv, 3 * ht, true, s.shift > 0 ? A.ln1r : A.ln1, h, true, 3 * ht, h, rows,
+                    wq);  // dWqkv
       });
     };
     if (!fuse_adam) GX_TRY(wgradq());
     int sp_a = 1;
-    if (t == 1)
+    if (t == 1 && s.shift == 0)  // (SW-MSA rolls dA back before LN1: keep it bf16)
       GX_TRY(gemm_splitk(r, dqkv, 3 * ht, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, &sp_a));
     r.da_slices = sp_a > 1 ? sp_a : 0;
     if (sp_a == 1) {
@@ -1677,6 +1732,15 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       a.out = r.da;
       a.ldo = h;
       GX_TRY(gemm(dqkv, 3 * ht, false, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, a));
+      if (s.shift > 0) {  // LN1 (and the residual) live in the unrolled order
+        GX_TRY(timed(kElementwise, 0, 8.0 * rows * h, [&] {
+          return window_roll(r.da, r.rollbuf, A.samples, grid_of(s), side_of(s), s.shift, h, true,
+                             stream_);
+        }));
+        GX_TRY(cuda_check(cudaMemcpyAsync(r.da, r.rollbuf, static_cast<size_t>(rows) * h * 2,
+                                          cudaMemcpyDeviceToDevice, stream_),
+                          "sw-msa da"));
+      }
     }
     if (fuse_adam) GX_TRY(wgradq());
     if (t > 1)

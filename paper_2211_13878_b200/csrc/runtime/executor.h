@@ -42,6 +42,7 @@ struct Shape {
   // decoder layers: causal self-attention (kind "causal", "decoder"); "decoder" adds a
   // cross-attention sublayer over the memory (the input of the model's first decoder layer)
   bool causal = false, cross = false;
+  int shift = 0;  // Swin SW-MSA: tokens rolled by -shift in both grid axes around attention
   int in_h() const { return merge ? h / 2 : h; }
   int in_seq() const { return merge ? 4 * seq : seq; }
 };

@@ -102,7 +102,8 @@ class _AttnArgs(ctypes.Structure):
                 ("drop_threshold", ctypes.c_uint32), ("drop_scale", ctypes.c_float),
                 ("seed", ctypes.c_uint64), ("site", ctypes.c_uint64),
                 ("seed_offset", ctypes.c_void_p), ("mask", ctypes.c_void_p),
-                ("trace", ctypes.c_void_p), ("causal", ctypes.c_int)]
+                ("trace", ctypes.c_void_p), ("causal", ctypes.c_int),
+                ("win_grid", ctypes.c_int), ("win_side", ctypes.c_int), ("win_shift", ctypes.c_int)]
 
 
 class Dropout(ctypes.Structure):
@@ -121,9 +122,11 @@ def make_dropout(p, seed, site, row_offset=0, col_offset=0, drop_ld=0):
 
 
 def _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, heads_total=None, head_offset=0,
-               sample_offset=0, causal=False):
+               sample_offset=0, causal=False, win=None):
     a = _AttnArgs()
     a.causal = int(causal)
+    if win is not None:  # (grid, side, shift): Swin shifted-window region mask
+        a.win_grid, a.win_side, a.win_shift = win
     a.batch, a.seq, a.heads, a.head_dim = batch, seq, heads, head_dim
     a.heads_total = heads_total or heads
     a.head_offset, a.sample_offset = head_offset, sample_offset
@@ -247,4 +250,13 @@ def patch_merge(x, samples, grid_out, window_side, backward=False):
                       device=x.device)
     _lib.check(_lib.lib().gx_k_patch_merge(_ptr(x), _ptr(out), samples, grid_out, window_side,
                                            c, int(backward), _lib.stream_ptr()))
+    return out
+
+
+def window_roll(x, samples, grid, window_side, shift, inverse=False):
+    """Swin cyclic shift of window-major tokens (gx_k_window_roll)."""
+    import torch
+    out = torch.empty_like(x)
+    _lib.check(_lib.lib().gx_k_window_roll(_ptr(x), _ptr(out), samples, grid, window_side, shift,
+                                           x.shape[1], int(inverse), _lib.stream_ptr()))
     return out

@@ -17,8 +17,9 @@ s=512, ffn 5120; BERT-base h=768, 12 x 64, s=128, ffn 3072; ViT-Huge h=1280, 16 
 s=257, ffn 5120; T5-Large h=1024, 16 x 64, s=512, ffn 4096, 24 encoder + 24 decoder layers
 ("kind": "decoder": causal self-attention + cross-attention).  Swin-like (Swin-H at
 224 px, the fixture's 2/2/26/2 stages): hidden 320/640/1280/2560 as heads x 32, token grids
-56/28/14/7 stored window-major with 7x7 windows ("kind": "window", W-MSA), ffn 4h; the first
-layer of stages 2-4 starts with patch merging ("merge": true).
+56/28/14/7 stored window-major with 7x7 windows ("kind": "window", W-MSA; odd blocks
+"shift": true, SW-MSA), ffn 4h; the first layer of stages 2-4 starts with patch merging
+("merge": true).
 """
 from __future__ import annotations
 
@@ -77,6 +78,8 @@ def _swin():
             shape["window"] = 49
             if st > 0 and i == 0:
                 shape["merge"] = True
+            if i % 2 == 1:
+                shape["shift"] = True  # SW-MSA on odd blocks (the 7x7 last stage skips it)
             layers.append({"param_bytes": p, "activation_bytes_per_sample": a,
                            "fwd_time_per_sample_ms": t, "name": f"stage{st}.{i}",
                            "shape": shape})

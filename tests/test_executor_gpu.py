@@ -7,6 +7,8 @@ seeds, inputs and Philox dropout masks.
 Tolerance (bf16 storage, fp32 accumulation): ||got - ref||_2 / ||ref||_2 <= 3e-2 for the
 output and every gradient tensor; loss within 1e-2 relative.
 """
+import math
+
 import numpy as np
 import pytest
 
@@ -35,10 +37,14 @@ def _small_model(L=4, h=256, heads=4, seq=64, ffn=512):
 
 def _oshape(shp):
     kind = shp.get("kind", "encoder")
+    shift = 0
+    if kind == "window" and shp.get("shift"):
+        g, ws = math.isqrt(shp["seq"]), math.isqrt(shp.get("window", 49))
+        shift = ws // 2 if g > ws else 0
     return lo.LayerShape(shp["hidden"], shp["heads"], shp["seq"], shp["ffn"],
                          shp.get("window", 0) if kind == "window" else 0,
                          bool(shp.get("merge", False)), kind in ("causal", "decoder"),
-                         kind == "decoder")
+                         kind == "decoder", shift)
 
 
 def _run_case(plan, model, world, p_drop=0.0, seed=11, optimizer=False):
@@ -242,7 +248,7 @@ def test_window_layer_rejects_ragged_windows(cuda):
         gxe.PlanExecutor(gxe.make_plan([""], 2), model, 1)
 
 
-def _swin_like(h0=64, heads0=2, grid0=14, window=49, stages=(2, 2)):
+def _swin_like(h0=64, heads0=2, grid0=14, window=49, stages=(2, 2), shifted=True):
     """Window layers over a grid0 x grid0 token grid; each later stage starts with a
     patch-merging layer (grid / 2, hidden x 2, heads x 2)."""
     layers, h, heads, grid = [], h0, heads0, grid0
@@ -252,6 +258,8 @@ def _swin_like(h0=64, heads0=2, grid0=14, window=49, stages=(2, 2)):
                      "ffn": 2 * h, "kind": "window", "window": window}
             if st > 0 and i == 0:
                 shape["merge"] = True
+            if i % 2 == 1 and shifted:
+                shape["shift"] = True  # Swin's odd blocks: SW-MSA
             layers.append({"param_bytes": 1, "activation_bytes_per_sample": 1,
                            "fwd_time_per_sample_ms": 0.1, "shape": shape})
         h, heads, grid = 2 * h, 2 * heads, grid // 2
@@ -343,3 +351,13 @@ def test_decoder_plan_restrictions(cuda):
     m["layers"][2]["shape"]["kind"] = "encoder"
     with pytest.raises(Exception, match="last layers"):
         gxe.PlanExecutor(gxe.make_plan([""] * 4, 2), m, 1)
+
+
+
+@pytest.mark.parametrize("p_drop", [0.0, 0.1])
+@pytest.mark.parametrize("strategies,world", [(["", ""], 1), (["tp:2", "sdp:2"], 2)])
+def test_swin_shifted_windows(cuda, strategies, world, p_drop):
+    """SW-MSA: a 28x28 grid (4x4 windows of 7x7, shift 3) with W-MSA / SW-MSA blocks."""
+    m = _swin_like(h0=64, heads0=2, grid0=28, stages=(2,))
+    assert m["layers"][1]["shape"]["shift"]
+    _check(_run_case(gxe.make_plan(strategies, 2), m, world, p_drop))

@@ -53,11 +53,36 @@ def _torch_merge(x, P, shape):
     return m @ P["w_m"].T
 
 
-def _torch_mha(q2, k2, v2, n, s, H, d, am, ka, causal):
+def _wm_to_raster(t, g, ws):
+    c = t.shape[-1]
+    n = t.shape[0] // (g * g)
+    return t.reshape(n, g // ws, g // ws, ws, ws, c).permute(0, 1, 3, 2, 4, 5).reshape(n, g, g, c)
+
+
+def _raster_to_wm(t, ws):
+    n, g, _, c = t.shape
+    return t.reshape(n, g // ws, ws, g // ws, ws, c).permute(0, 1, 3, 2, 4, 5).reshape(n * g * g, c)
+
+
+def _swin_attn_mask(g, ws, sh):
+    """Swin's SW-MSA mask, built the way the Swin reference does (img_mask slices)."""
+    img = torch.zeros(1, g, g, 1)
+    cnt = 0
+    for hs in (slice(0, -ws), slice(-ws, -sh), slice(-sh, None)):
+        for wsl in (slice(0, -ws), slice(-ws, -sh), slice(-sh, None)):
+            img[:, hs, wsl, :] = cnt
+            cnt += 1
+    mw = _raster_to_wm(img, ws).reshape(-1, ws * ws)
+    return mw[:, None, :] != mw[:, :, None]  # [nW, win, win] True = masked
+
+
+def _torch_mha(q2, k2, v2, n, s, H, d, am, ka, causal, mask=None):
     q, k, v = (t.reshape(n, s, H, d).transpose(1, 2) for t in (q2, k2, v2))
     sc = q @ k.transpose(-1, -2) / math.sqrt(d)
     if causal:
         sc = sc.masked_fill(torch.ones(s, s, dtype=torch.bool).triu(1), -math.inf)
+    if mask is not None:
+        sc = sc.masked_fill(mask[:, None], -math.inf)
     pr = torch.softmax(sc, -1)
     return (pr * am * ka @ v).transpose(1, 2).reshape(n * s, H * d)
 
@@ -73,7 +98,16 @@ def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0, memory=None, n_
     qkv = a @ P["w_qkv"].T + P["b_qkv"]
     am = torch.from_numpy(lo._attn_mask(drop, 3 * layer_id, n, H, s, sample_offset * nw)).double()
     ka = lo.dropout_scale(drop.p_attn)
-    ctx = _torch_mha(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], n, s, H, d, am, ka, shape.causal)
+    mask = None
+    if shape.shift:
+        g, ws, sh = math.isqrt(S), math.isqrt(s), shape.shift
+        a = _raster_to_wm(torch.roll(_wm_to_raster(a, g, ws), (-sh, -sh), (1, 2)), ws)
+        qkv = a @ P["w_qkv"].T + P["b_qkv"]
+        mask = _swin_attn_mask(g, ws, sh).repeat(n // nw, 1, 1)
+    ctx = _torch_mha(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], n, s, H, d, am, ka, shape.causal,
+                     mask)
+    if shape.shift:
+        ctx = _raster_to_wm(torch.roll(_wm_to_raster(ctx, g, ws), (sh, sh), (1, 2)), ws)
     kh = lo.dropout_scale(drop.p_hidden)
     m1 = torch.from_numpy(lo._hidden_mask(drop, 3 * layer_id + 1, n * s, h, sample_offset * S)).double()
     x1 = x + (ctx @ P["w_o"].T + P["b_o"]) * m1 * kh
@@ -91,12 +125,13 @@ def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0, memory=None, n_
     return x1 + (g @ P["w_2"].T + P["b_2"]) * m2 * kh
 
 
-@pytest.mark.parametrize("p,window,seq,merge", [(0.0, 0, 12, False), (0.1, 0, 12, False),
-                                                (0.1, 4, 12, False), (0.1, 4, 16, True),
-                                                (0.0, 9, 36, True)])
-def test_oracle_matches_autograd(p, window, seq, merge):
+@pytest.mark.parametrize("p,window,seq,merge,shift", [
+    (0.0, 0, 12, False, 0), (0.1, 0, 12, False, 0), (0.1, 4, 12, False, 0), (0.1, 4, 16, True, 0),
+    (0.0, 9, 36, True, 0), (0.1, 9, 36, False, 1), (0.0, 16, 64, False, 2), (0.1, 4, 16, True, 1)])
+def test_oracle_matches_autograd(p, window, seq, merge, shift):
     rng = np.random.default_rng(0)
-    shape = lo.LayerShape(hidden=64, heads=4, seq=seq, ffn=128, window=window, merge=merge)
+    shape = lo.LayerShape(hidden=64, heads=4, seq=seq, ffn=128, window=window, merge=merge,
+                          shift=shift)
     P = lo.init_layer_params(shape, rng, std=0.1)
     x = rng.standard_normal((2 * shape.seq * (4 if merge else 1), shape.hidden // (2 if merge else 1)))
     dy = rng.standard_normal((2 * shape.seq, shape.hidden))
