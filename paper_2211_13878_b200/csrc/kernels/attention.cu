@@ -96,7 +96,8 @@ __device__ __forceinline__ int swin_region(const gx_attention_args& p, int b, in
 }  // namespace
 
 // --------------------------------------------------------------------------- forward
-template <int HD>
+// kMask: causal / shifted-window masking compiled in only when used (register pressure)
+template <int HD, bool kMask>
 __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_args p) {
   pdl_enter();
   constexpr int LDS = HD + 8;
@@ -179,9 +180,9 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_a
         const int key = kb * kBlk + nb * 8 + 2 * t + (j & 1);
         float v = sacc[nb][j] * c2;
         const int qrow = q0 + warp * 16 + g + 8 * (j >> 1);
-        if (key >= s || (p.causal && key > qrow) ||
-            (p.win_shift > 0 && key < s && qrow < s &&
-             swin_region(p, b, qrow) != swin_region(p, b, key)))
+        if (key >= s || (kMask && ((p.causal && key > qrow) ||
+                                   (p.win_shift > 0 && key < s && qrow < s &&
+                                    swin_region(p, b, qrow) != swin_region(p, b, key)))))
           v = -INFINITY;
         sacc[nb][j] = v;
         mx[j >> 1] = fmaxf(mx[j >> 1], v);
@@ -297,7 +298,7 @@ __global__ void attn_bwd_prep_kernel(const gx_attention_args p) {
 }
 
 // --------------------------------------------------------------------------- backward
-template <int HD>
+template <int HD, bool kMask>
 __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_args p) {
   pdl_enter();
   constexpr int LDS = HD + 8;
@@ -405,8 +406,10 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
         const int ql = nb * 8 + 2 * t + (j & 1);
         const int q = q0 + ql;
         const int key = k0 + warp * 16 + g + 8 * (j >> 1);
-        const bool keep_pk = q < s && key < s && !(p.causal && key > q) &&
-                             !(p.win_shift > 0 && swin_region(p, b, q) != swin_region(p, b, key));
+        const bool keep_pk = q < s && key < s &&
+                             !(kMask && ((p.causal && key > q) ||
+                                         (p.win_shift > 0 &&
+                                          swin_region(p, b, q) != swin_region(p, b, key))));
         float P = keep_pk ? exp2f(st[nb][j] * c2 - sL[ql]) : 0.f;
         float keep = 1.f;
         if (thr != 0u) {
@@ -530,11 +533,15 @@ static int attention_fwd_impl(const gx_attention_args& a, cudaStream_t st) {
   const int smem = 5 * kBlk * LDS * 2;
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(attn_fwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_fwd_kernel<HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_fwd_kernel<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     set = true;
   }
   dim3 grid((a.seq + kBlk - 1) / kBlk, a.batch * a.heads);
-  launch_k(attn_fwd_kernel<HD>, grid, dim3(kThreads), smem, st, a);
+  if (a.causal || a.win_shift > 0)
+    launch_k(attn_fwd_kernel<HD, true>, grid, dim3(kThreads), smem, st, a);
+  else
+    launch_k(attn_fwd_kernel<HD, false>, grid, dim3(kThreads), smem, st, a);
   return check_launch("attn_fwd_kernel");
 }
 
@@ -544,14 +551,18 @@ static int attention_bwd_impl(const gx_attention_args& a, cudaStream_t st) {
   const int smem = 4 * kBlk * LDS * 2 + kBlk * (kBlk + 8) * 2 + 2 * kBlk * 4 + kBlk * 4 * 2;
   static bool set = false;
   if (!set) {
-    cudaFuncSetAttribute(attn_bwd_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_bwd_kernel<HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_bwd_kernel<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     set = true;
   }
   const int rows = a.batch * a.heads * a.seq;
   launch_k(attn_bwd_prep_kernel<HD>, dim3((rows + 7) / 8), dim3(256), 0, st, a);
   if (int rc = check_launch("attn_bwd_prep_kernel")) return rc;
   dim3 grid((a.seq + kBlk - 1) / kBlk, a.batch * a.heads);
-  launch_k(attn_bwd_kernel<HD>, grid, dim3(kThreads), smem, st, a);
+  if (a.causal || a.win_shift > 0)
+    launch_k(attn_bwd_kernel<HD, true>, grid, dim3(kThreads), smem, st, a);
+  else
+    launch_k(attn_bwd_kernel<HD, false>, grid, dim3(kThreads), smem, st, a);
   if (int rc = check_launch("attn_bwd_kernel")) return rc;
   const int64_t work = static_cast<int64_t>(rows) * (HD / 2);
   int blocks = static_cast<int>((work + 255) / 256);
