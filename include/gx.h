@@ -122,7 +122,7 @@ GX_API const char* gx_plan_last_error(void);
  * Layer "shape": {"hidden", "heads", "head_dim", "seq", "ffn", "kind"} with kind
  *   "encoder" (pre-LN BERT/ViT layer), "causal" (decoder-only self-attention),
  *   "decoder" (T5: causal self-attention + cross-attention over the first decoder layer's
- *   input + MLP; decoder layers are the model's suffix, tp 1) or "window" (Swin: "window"
+ *   input + MLP; decoder layers are the model's suffix) or "window" (Swin: "window"
  *   tokens per attention window, window-major; "shift": true = SW-MSA; "merge": true = patch
  *   merging of a [4*seq, hidden/2] input first).
  * Parameters cross the boundary in the canonical unsharded fp32 order

@@ -281,6 +281,8 @@ struct RankCtx {
 };
 
 // --------------------------------------------------------------------------------------
+float scale_of(float p);  // dropout keep-scale for probability p (defined below)
+
 class ExecutorImpl final : public Executor {
  public:
   int init(const json& cfg, std::string* err);
@@ -338,6 +340,25 @@ class ExecutorImpl final : public Executor {
   int fwd_phase(RankCtx& r, int li, int mb, int phase);
   int bwd_phase(RankCtx& r, int li, int mb, int phase);
   int merge_bwd(RankCtx& r, RankLayer& L, Acts& A, bf16* dX, const gx_gemm_epilogue& wm_ep);
+  // phases of a layer's forward / backward: TP splits them at its all-reduces (a decoder's
+  // cross sublayer adds one)
+  int tp_phases(const RankLayer& L) const {
+    return L.d.tp > 1 ? (L.sh.cross ? 4 : 3) : 1;
+  }
+  int tp_bwd_phases(const RankLayer& L) const {
+    return L.d.tp > 1 ? (L.sh.cross ? (L.layer == dec0_ ? 5 : 4) : 3) : 1;
+  }
+  gx_dropout hidden_drop(const RankCtx& r, uint64_t site, int64_t row_off, int ld) const {
+    gx_dropout d{};
+    d.threshold = thr_hidden_;
+    d.scale = scale_of(p_hidden_);
+    d.seed = seed_;
+    d.site = site;
+    d.row_offset = row_off;
+    d.drop_ld = ld;
+    d.seed_offset = r.seed_off;
+    return d;
+  }
   static int grid_of(const Shape& s) {
     return static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.seq))));
   }
@@ -352,8 +373,9 @@ class ExecutorImpl final : public Executor {
     }
   }
   int cross_fwd(RankCtx& r, int li, int mb, bool ln3_ready);
-  int cross_bwd(RankCtx& r, int li, int mb, bf16* dout,
-                const std::function<gx_gemm_epilogue(const Slot&, int64_t)>& wgrad_ep);
+  int cross_bwd_attn(RankCtx& r, int li, int mb,
+                     const std::function<gx_gemm_epilogue(const Slot&, int64_t)>& wgrad_ep);
+  int cross_bwd_ln3(RankCtx& r, int li, int mb, bf16* dout);
   gx_attention_args cross_args(RankCtx& r, const RankLayer& L, const Acts& A) const;
   int sync_phase(RankCtx& r, int li, int phase);
   int xin_fwd(RankCtx& r, int li, int mb);
@@ -769,10 +791,6 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
       // idle for a micro-batch; their gradients enter the reductions as zeros.
       if (s.cross) {  // T5 decoder layers (SPEC.md:67 flattens encoder + decoder)
         if (dec0_ < 0) dec0_ = l;
-        if (d.tp != 1) {
-          *err = "executor: decoder (cross-attention) layers run without tensor parallelism";
-          return kErrConfig;
-        }
         const Shape& s0 = shape_[dec0_];
         // the memory (the first decoder layer's input) travels with the activations across
         // the decoder's stage boundaries, chunked like them: one data degree and shape
@@ -1449,19 +1467,29 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
   }
   // the MLP's residual-stream input: x1, or -- after a decoder's cross sublayer -- x2
   bf16* const xr = s.cross ? A.x2 : A.x1;
-  if ((t == 1 && phase == 0) || (t > 1 && phase == 1)) {
-    if (t > 1) {
-      gx_dropout d{};
-      d.threshold = thr_hidden_;
-      d.scale = scale_of(p_hidden_);
-      d.seed = seed_;
-      d.site = 3ull * l + 1;
-      d.row_offset = row_off;
-      d.drop_ld = h;
-      d.seed_offset = r.seed_off;
-      GX_TRY(timed(kElementwise, 0, 6.0 * rows * h, [&] { return bias_dropout_add(r.partial, P + L.lay.bo.off, A.x, A.x1, rows, h, d, stream_); }));
+  // TP phases: [attention] [cross (decoders)] [MLP] [final residual]
+  const int mlp_ph = t > 1 ? (s.cross ? 2 : 1) : 0;
+  if (t > 1 && s.cross && phase == 1) {
+    GX_TRY(timed(kElementwise, 0, 6.0 * rows * h, [&] {
+      return bias_dropout_add(r.partial, P + L.lay.bo.off, A.x, A.x1, rows, h,
+                              hidden_drop(r, 3ull * l + 1, row_off, h), stream_);
+    }));
+    GX_TRY(cross_fwd(r, li, mb, false));  // leaves the out-projection partial in r.partial
+    return c_all_reduce(L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h, DType::kBF16,
+                        stream_);
+  }
+  if (phase == mlp_ph) {
+    if (t > 1) {  // the all-reduced sublayer output below the MLP: + bias, dropout, residual
+      const bool xd = s.cross;
+      GX_TRY(timed(kElementwise, 0, 6.0 * rows * h, [&] {
+        return bias_dropout_add(r.partial, P + (xd ? L.lay.bo2 : L.lay.bo).off, xd ? A.x1 : A.x,
+                                xr, rows, h,
+                                hidden_drop(r, xd ? 3ull * L_ + 2ull * l + 1 : 3ull * l + 1,
+                                            row_off, h),
+                                stream_);
+      }));
     }
-    if (s.cross) GX_TRY(cross_fwd(r, li, mb, ln3_ready));
+    if (s.cross && t == 1) GX_TRY(cross_fwd(r, li, mb, ln3_ready));
     if (!ln2_ready)
       GX_TRY(timed(kNorm, 0, 4.0 * rows * h, [&] { return layernorm_fwd(xr, P + L.lay.ln2g.off, P + L.lay.ln2b.off, A.ln2, A.mean2, A.rstd2,
                            rows, h, stream_); }));
@@ -1529,15 +1557,8 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     return c_all_reduce(L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h,
                              DType::kBF16, stream_);
   }
-  if (t > 1 && phase == 2) {
-    gx_dropout d{};
-    d.threshold = thr_hidden_;
-    d.scale = scale_of(p_hidden_);
-    d.seed = seed_;
-    d.site = 3ull * l + 2;
-    d.row_offset = row_off;
-    d.drop_ld = h;
-    d.seed_offset = r.seed_off;
+  if (t > 1 && phase == mlp_ph + 1) {
+    gx_dropout d = hidden_drop(r, 3ull * l + 2, row_off, h);
     return timed(kElementwise, 0, 6.0 * rows * h, [&] {
       return bias_dropout_add(r.partial, P + L.lay.b2.off, xr, A.y, rows, h, d, stream_);
     });
@@ -1645,7 +1666,13 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
                                stream_);
     phase = 1;
   }
-  if (phase == 1) {
+  // TP decoder layers: [MLP] [LN2 + cross attention] [LN3 + self-attention] [LN1] (+ [dmem
+  // all-reduce] [dmem add] on the first decoder layer); every other layer: [MLP] [LN2 +
+  // self-attention] [LN1]
+  const bool xtp = s.cross && t > 1;
+  const int ln1_ph = xtp ? 3 : 2;
+  if (phase == 1 || (xtp && phase == 2)) {
+   if (phase == 1) {
     const void* dc_in = r.dc_slices ? static_cast<const void*>(r.acc32) : static_cast<const void*>(r.dc);
     // LN2 backward with the out-projection's dropout backward + bias gradient fused in:
     // dx1 = residual-stream gradient, dout = dropout_mask(dx1), dbo += colsum(dout)
@@ -1667,8 +1694,13 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     if (xd) {
       // the wgrad-stream LN2 column pass above reads dout2 / fold2: let it finish first
       if (wg_active_) GX_TRY(fork(wg_, stream_));
-      GX_TRY(cross_bwd(r, li, mb, dout, wgrad_ep));
+      GX_TRY(cross_bwd_attn(r, li, mb, wgrad_ep));  // -> dc3 (TP: partial) in r.dc
+      if (t > 1)
+        return c_all_reduce(L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
+                            stream_);
     }
+   }
+    if (s.cross) GX_TRY(cross_bwd_ln3(r, li, mb, dout));  // dx1, dout (self-attention)
     const gx_gemm_epilogue wo = wgrad_ep(L.lay.wo, ht);
     auto wgrado = [&] { return on_wgrad([&] { return gemm(dout, h, true, A.ctx, ht, true, h, ht, rows, wo); }); };  // dWo = dout^T ctx
     if (!fuse_adam) GX_TRY(wgrado());
@@ -1748,7 +1780,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
                                stream_);
     phase = 2;
   }
-  if (phase == 2) {
+  if (phase == ln1_ph) {
     const void* da_in = r.da_slices ? static_cast<const void*>(r.acc32) : static_cast<const void*>(r.da);
     // When this layer's input is the previous layer's output (same rows), the previous
     // layer's MLP dropout backward rides along: dz_{l-1} = dropout_mask(dX), db2_{l-1} +=
@@ -1792,12 +1824,17 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     }));
     if (prev != nullptr) prev->dz_ready = true;
     if (s.merge) GX_TRY(merge_bwd(r, L, A, dX, wgrad_ep(L.lay.wm, 2 * h)));
-    if (li == r.dec_li) {  // this input is also every decoder layer's memory: dX += dL/dmem
-      gx_dropout off{};
-      GX_TRY(timed(kElementwise, 0, 8.0 * rows * h, [&] {
-        return bias_dropout_add(r.dmem, nullptr, dX, dX, rows, h, off, stream_, true);
-      }));
-    }
+    if (li == r.dec_li && t > 1)  // TP ranks hold per-head partial sums of dL/dmem
+      return c_all_reduce(L.g_tp, r.rank, r.dmem, static_cast<size_t>(rows) * h, DType::kF32,
+                          stream_);
+    phase = ln1_ph + 1;
+  }
+  if (phase == ln1_ph + 1 && li == r.dec_li) {
+    // this input is also every decoder layer's memory: dX += dL/dmem
+    gx_dropout off{};
+    GX_TRY(timed(kElementwise, 0, 8.0 * rows * h, [&] {
+      return bias_dropout_add(r.dmem, nullptr, dX, dX, rows, h, off, stream_, true);
+    }));
   }
   return kOk;
 }
@@ -1810,7 +1847,7 @@ int ExecutorImpl::cross_fwd(RankCtx& r, int li, int mb, bool ln3_ready) {
   RankLayer& L = r.layers[li];
   Acts& A = L.acts[mb];
   const Shape& s = L.sh;
-  const int rows = A.rows, h = s.h;
+  const int rows = A.rows, h = s.h, t = L.d.tp, ht = h / t;
   const bf16* P = L.pfull;
   const int l = L.layer;
   const bf16* mem = r.mem(mb);
@@ -1819,21 +1856,26 @@ int ExecutorImpl::cross_fwd(RankCtx& r, int li, int mb, bool ln3_ready) {
       return layernorm_fwd(A.x1, P + L.lay.ln3g.off, P + L.lay.ln3b.off, A.ln3, A.mean3, A.rstd3,
                            rows, h, stream_);
     }));
+  // (TP: this rank's heads -- q2 / kv2 column-parallel, the out-projection row-parallel)
   gx_gemm_epilogue e = epi();
   e.out_kind = kOutBF16;
   e.out = A.qkv2;
-  e.ldo = 3 * h;
+  e.ldo = 3 * ht;
   e.bias = P + L.lay.bq2.off;
-  GX_TRY(gemm(A.ln3, h, false, P + L.lay.wq2.off, h, false, rows, h, h, e));  // q2
-  e.out = A.qkv2 + h;
+  GX_TRY(gemm(A.ln3, h, false, P + L.lay.wq2.off, h, false, rows, ht, h, e));  // q2
+  e.out = A.qkv2 + ht;
   e.bias = P + L.lay.bkv2.off;
-  GX_TRY(gemm(mem, h, false, P + L.lay.wkv2.off, h, false, rows, 2 * h, h, e));  // k2 v2
+  GX_TRY(gemm(mem, h, false, P + L.lay.wkv2.off, h, false, rows, 2 * ht, h, e));  // k2 v2
   gx_attention_args at = cross_args(r, L, A);
-  GX_TRY(timed(kAttnFwd, 4.0 * A.samples * s.heads * double(s.seq) * s.seq * s.hd,
-               2.0 * rows * 4 * h, [&] { return attention_fwd(at, stream_); }));
+  GX_TRY(timed(kAttnFwd, 4.0 * A.samples * (s.heads / t) * double(s.seq) * s.seq * s.hd,
+               2.0 * rows * 4 * ht, [&] { return attention_fwd(at, stream_); }));
   gx_gemm_epilogue o = epi();
   o.out_kind = kOutBF16;
   o.ldo = h;
+  if (t > 1) {  // partial sums; the caller all-reduces and adds bias + dropout + residual
+    o.out = r.partial;
+    return gemm(A.ctx2, ht, false, P + L.lay.wo2.off, ht, false, rows, h, ht, o);
+  }
   o.out = A.x2;
   o.bias = P + L.lay.bo2.off;
   o.residual = A.x1;
@@ -1850,19 +1892,20 @@ int ExecutorImpl::cross_fwd(RankCtx& r, int li, int mb, bool ln3_ready) {
 
 gx_attention_args ExecutorImpl::cross_args(RankCtx& r, const RankLayer& L, const Acts& A) const {
   const Shape& s = L.sh;
+  const int t = L.d.tp;
   gx_attention_args at{};
   at.batch = A.samples;
   at.seq = s.seq;
-  at.heads = s.heads;
+  at.heads = s.heads / t;
   at.head_dim = s.hd;
   at.heads_total = s.heads;
-  at.head_offset = 0;
+  at.head_offset = L.tr * (s.heads / t);
   at.sample_offset = A.sample0;
   at.scale = 1.f / std::sqrt(static_cast<float>(s.hd));
   at.qkv = A.qkv2;
-  at.ld_qkv = 3 * s.h;
+  at.ld_qkv = 3 * s.h / t;
   at.ctx = A.ctx2;
-  at.ld_ctx = s.h;
+  at.ld_ctx = s.h / t;
   at.lse = A.lse2;
   at.drop_threshold = thr_attn_;
   at.drop_scale = scale_of(p_attn_);
@@ -1879,8 +1922,46 @@ gx_attention_args ExecutorImpl::cross_args(RankCtx& r, const RankLayer& L, const
 // gradient below the MLP), r.dout2 = its dropout-masked copy (bo2's gradient already taken).
 // Out: r.dx1 = dL/dx1, dout = dL/d(self-attention out-projection) with bo's gradient, and
 // dL/dmem accumulated into r.dmem.
-int ExecutorImpl::cross_bwd(RankCtx& r, int li, int mb, bf16* dout,
-                            const std::function<gx_gemm_epilogue(const Slot&, int64_t)>& wgrad_ep) {
+int ExecutorImpl::cross_bwd_attn(RankCtx& r, int li, int mb,
+                                 const std::function<gx_gemm_epilogue(const Slot&, int64_t)>& wgrad_ep) {
+  RankLayer& L = r.layers[li];
+  Acts& A = L.acts[mb];
+  const Shape& s = L.sh;
+  const int rows = A.rows, h = s.h, t = L.d.tp, ht = h / t;
+  const bf16* P = L.pfull;
+  float* G = L.gfull;
+  const bf16* mem = r.mem(mb);
+  gx_gemm_epilogue c = epi();
+  c.out_kind = kOutBF16;
+  c.out = r.dctx;
+  c.ldo = ht;
+  GX_TRY(gemm(r.dout2, h, false, P + L.lay.wo2.off, ht, true, rows, ht, h, c));  // dout2 Wo2
+  GX_TRY(gemm(r.dout2, h, true, A.ctx2, ht, true, h, ht, rows, wgrad_ep(L.lay.wo2, ht)));
+  gx_attention_args at = cross_args(r, L, A);
+  at.dctx = r.dctx;
+  at.dqkv = r.dqkv2;
+  GX_TRY(timed(kAttnBwd, 10.0 * A.samples * (s.heads / t) * double(s.seq) * s.seq * s.hd,
+               2.0 * rows * 8 * ht, [&] { return attention_bwd(at, stream_); }));
+  // weight / bias gradients of the q and kv projections (this rank's heads)
+  GX_TRY(colsum(r.dqkv2, 3 * ht, G + L.lay.bq2.off, rows, ht, stream_, r.cs_ws[0]));
+  GX_TRY(gemm(r.dqkv2, 3 * ht, true, A.ln3, h, true, ht, h, rows, wgrad_ep(L.lay.wq2, h)));
+  GX_TRY(colsum(r.dqkv2 + ht, 3 * ht, G + L.lay.bkv2.off, rows, 2 * ht, stream_, r.cs_ws[0]));
+  GX_TRY(gemm(r.dqkv2 + ht, 3 * ht, true, mem, h, true, 2 * ht, h, rows, wgrad_ep(L.lay.wkv2, h)));
+  // memory gradient (TP: partial over heads): the last decoder layer starts the sum
+  gx_gemm_epilogue m = epi();
+  m.out_kind = li + 1 == static_cast<int>(r.layers.size()) && !r.dmem_from_next
+                   ? kOutF32 : kOutF32Accumulate;
+  m.out = r.dmem;
+  m.ldo = h;
+  GX_TRY(gemm(r.dqkv2 + ht, 3 * ht, false, P + L.lay.wkv2.off, h, true, rows, h, 2 * ht, m));
+  c.out = r.dc;
+  c.ldo = h;
+  return gemm(r.dqkv2, 3 * ht, false, P + L.lay.wq2.off, h, true, rows, h, ht, c);  // dq Wq2
+}
+
+// LN3 backward: dx1 = dx2 + LN3'(dc3), with the self-attention out-projection's dropout
+// backward and bias gradient fused in (as LN2's backward does for non-decoder layers).
+int ExecutorImpl::cross_bwd_ln3(RankCtx& r, int li, int mb, bf16* dout) {
   RankLayer& L = r.layers[li];
   Acts& A = L.acts[mb];
   const Shape& s = L.sh;
@@ -1888,34 +1969,6 @@ int ExecutorImpl::cross_bwd(RankCtx& r, int li, int mb, bf16* dout,
   const bf16* P = L.pfull;
   float* G = L.gfull;
   const int l = L.layer;
-  const bf16* mem = r.mem(mb);
-  gx_gemm_epilogue c = epi();
-  c.out_kind = kOutBF16;
-  c.out = r.dctx;
-  c.ldo = h;
-  GX_TRY(gemm(r.dout2, h, false, P + L.lay.wo2.off, h, true, rows, h, h, c));  // dout2 Wo2
-  GX_TRY(gemm(r.dout2, h, true, A.ctx2, h, true, h, h, rows, wgrad_ep(L.lay.wo2, h)));
-  gx_attention_args at = cross_args(r, L, A);
-  at.dctx = r.dctx;
-  at.dqkv = r.dqkv2;
-  GX_TRY(timed(kAttnBwd, 10.0 * A.samples * s.heads * double(s.seq) * s.seq * s.hd,
-               2.0 * rows * 8 * h, [&] { return attention_bwd(at, stream_); }));
-  // weight / bias gradients of the q and kv projections
-  GX_TRY(colsum(r.dqkv2, 3 * h, G + L.lay.bq2.off, rows, h, stream_, r.cs_ws[0]));
-  GX_TRY(gemm(r.dqkv2, 3 * h, true, A.ln3, h, true, h, h, rows, wgrad_ep(L.lay.wq2, h)));
-  GX_TRY(colsum(r.dqkv2 + h, 3 * h, G + L.lay.bkv2.off, rows, 2 * h, stream_, r.cs_ws[0]));
-  GX_TRY(gemm(r.dqkv2 + h, 3 * h, true, mem, h, true, 2 * h, h, rows, wgrad_ep(L.lay.wkv2, h)));
-  // memory gradient: the last decoder layer (first in backward) starts the sum
-  gx_gemm_epilogue m = epi();
-  m.out_kind = li + 1 == static_cast<int>(r.layers.size()) && !r.dmem_from_next
-                   ? kOutF32 : kOutF32Accumulate;
-  m.out = r.dmem;
-  m.ldo = h;
-  GX_TRY(gemm(r.dqkv2 + h, 3 * h, false, P + L.lay.wkv2.off, h, true, rows, h, 2 * h, m));
-  c.out = r.dc;
-  GX_TRY(gemm(r.dqkv2, 3 * h, false, P + L.lay.wq2.off, h, true, rows, h, h, c));  // dq Wq2
-  // LN3 backward: dx1 = dx2 + LN3'(dc3), with the self-attention out-projection's dropout
-  // backward and bias gradient fused in (as LN2's backward does for non-decoder layers)
   gx_dropout d{};
   d.threshold = thr_hidden_;
   d.scale = scale_of(p_hidden_);
@@ -2309,7 +2362,7 @@ int ExecutorImpl::step_once() {
         for (RankCtx* r : R) GX_TRY(xin_fwd(*r, li, mb));
         if (mb == 0)
           for (RankCtx* r : R) GX_TRY(gather_params(*r, li));
-        const int phases = R[0]->layers[li].d.tp > 1 ? 3 : 1;
+        const int phases = tp_phases(R[0]->layers[li]);
         for (int ph = 0; ph < phases; ++ph)
           for (RankCtx* r : R) GX_TRY(fwd_phase(*r, li, mb, ph));
       }
@@ -2360,7 +2413,7 @@ int ExecutorImpl::step_once() {
         const int tp = R[0]->layers[li].d.tp;
         tmark("bwd_begin L" + std::to_string(R[0]->layers[li].layer), stream_);
         if (tp > 1) {
-          for (int ph = 0; ph < 3; ++ph)
+          for (int ph = 0; ph < tp_bwd_phases(R[0]->layers[li]); ++ph)
             for (RankCtx* r : R) GX_TRY(bwd_phase(*r, li, mb, ph));
         } else {
           for (RankCtx* r : R) GX_TRY(bwd_phase(*r, li, mb, 0));

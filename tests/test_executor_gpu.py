@@ -318,6 +318,10 @@ T5_CASES = [
     (2, ["", "", "", ""], 2, 2, 2, [0, 3, 4]),
     (4, ["", "", "", ""], 4, 4, 4, [0, 1, 2, 3, 4]),
     (8, ["dp:4", "sdp:4", "sdp:4", "dp:4"], 8, 2, 4, [0, 3, 4]),
+    # tensor-parallel decoders: cross-attention heads split, dL/dmem partials all-reduced
+    (2, ["tp:2", "tp:2", "tp:2", "tp:2"], 2, 1, 1, None),
+    (4, ["tp:2,dp:2", "dp:2,tp:2", "tp:2,sdp:2", "sdp:2,tp:2"], 4, 1, 1, None),
+    (4, ["tp:2", "tp:2", "tp:2", "tp:2"], 4, 2, 2, [0, 3, 4]),
 ]
 
 
@@ -340,8 +344,6 @@ def test_causal_decoder_only_layers(cuda, strategies, world):
 
 
 def test_decoder_plan_restrictions(cuda):
-    with pytest.raises(Exception, match="without tensor parallelism"):
-        gxe.PlanExecutor(gxe.make_plan(["dp:2", "dp:2", "tp:2", "tp:2"], 2), _t5_like(), 2)
     m = _t5_like()
     m["layers"][3]["shape"].update(hidden=128, head_dim=32)
     with pytest.raises(Exception, match="share one data degree and shape"):
