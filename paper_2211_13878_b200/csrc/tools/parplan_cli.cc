@@ -654,27 +654,32 @@ int cmd_run(const Args& a) {
   return kOk;
 }
 
-// Time one layer of `shape` (serial strategy, `batch` samples, graph replay).
-double time_layer(const json& shape, int batch, bool forward_only, int warmup, int steps, int device) {
-  const json model = {{"dtype_bytes", 4},
-                      {"layers", json::array({{{"param_bytes", 1},
-                                               {"activation_bytes_per_sample", 1},
-                                               {"fwd_time_per_sample_ms", 1.0},
-                                               {"shape", shape}}})}};
+// Time `shapes` run in sequence (serial strategy, `batch` samples, graph replay).
+double time_layers(const std::vector<json>& shapes, int batch, bool forward_only, int warmup,
+                   int steps, int device) {
+  json layers = json::array(), plan_layers = json::array();
+  for (size_t i = 0; i < shapes.size(); ++i) {
+    layers.push_back({{"param_bytes", 1}, {"activation_bytes_per_sample", 1},
+                      {"fwd_time_per_sample_ms", 1.0}, {"shape", shapes[i]}});
+    plan_layers.push_back({{"id", static_cast<int>(i)}, {"strategy", ""}});
+  }
+  const int n = static_cast<int>(shapes.size());
+  const json model = {{"dtype_bytes", 4}, {"layers", layers}};
   const json plan = {{"pp_degree", 1},
                      {"micro_batches", 1},
                      {"batch_size", batch},
-                     {"stages", json::array({{{"layer_range", {0, 1}},
-                                              {"layers", json::array({{{"id", 0}, {"strategy", ""}}})}}})}};
+                     {"stages", json::array({{{"layer_range", {0, n}}, {"layers", plan_layers}}})}};
   const json cfg = {{"plan", plan},         {"model", model},        {"world_size", 1},
                     {"comm", "sim"},        {"forward_only", forward_only}, {"optimizer", false},
                     {"dropout_attn", 0.1},  {"dropout_hidden", 0.1}, {"device", device}};
   Executor ex(cfg);
   const GxLib& L = GxLib::get();
   gx_check(L.init_params(ex.get(), 1, 0.02f), "init_params");
-  const size_t n = static_cast<size_t>(batch) * shape.at("seq").get<int>() * shape.at("hidden").get<int>();
-  const auto x = synthetic_bf16(n, 3);
-  gx_check(L.load_batch(ex.get(), x.data(), x.data()), "load_batch");
+  const json& f = shapes.front();
+  const json& z = shapes.back();
+  const auto x = synthetic_bf16(static_cast<size_t>(batch) * f.at("seq").get<int>() * f.at("hidden").get<int>(), 3);
+  const auto y = synthetic_bf16(static_cast<size_t>(batch) * z.at("seq").get<int>() * z.at("hidden").get<int>(), 4);
+  gx_check(L.load_batch(ex.get(), x.data(), y.data()), "load_batch");
   double ms = 0;
   gx_check(L.time(ex.get(), 1, warmup, steps, &ms), "gx_exec_time");
   return ms;
@@ -699,17 +704,24 @@ int cmd_profile(const Args& a) {
   std::map<std::string, std::pair<double, double>> measured;  // shape -> (fwd, fwd+bwd) ms
   std::vector<std::string> order;
   json raw = json::array();
+  json prev;  // the previous layer's shape: a patch-merging layer is timed behind it
+  auto time_layer = [&](const json& shape, bool fwd_only) {
+    if (!shape.value("merge", false)) return time_layers({shape}, batch, fwd_only, warmup, steps, device);
+    return time_layers({prev, shape}, batch, fwd_only, warmup, steps, device) -
+           time_layers({prev}, batch, fwd_only, warmup, steps, device);
+  };
   for (json& layer : model.at("layers")) {
     const std::string key = layer.at("shape").dump();
     if (measured.count(key) == 0) {
-      const double fwd = time_layer(layer.at("shape"), batch, true, warmup, steps, device);
-      const double full = time_layer(layer.at("shape"), batch, false, warmup, steps, device);
+      const double fwd = time_layer(layer.at("shape"), true);
+      const double full = time_layer(layer.at("shape"), false);
       measured[key] = {fwd, full};
       order.push_back(key);
       raw.push_back({{"shape", layer.at("shape")}, {"batch", batch}, {"fwd_ms", fwd}, {"fwd_bwd_ms", full}});
       std::printf("shape %s  batch %d  fwd %.4f ms  fwd+bwd %.4f ms\n", key.c_str(), batch, fwd, full);
     }
     layer["fwd_time_per_sample_ms"] = round_to(measured[key].first / batch, 6);
+    prev = layer.at("shape");
   }
   double sum = 0;
   int cnt = 0;

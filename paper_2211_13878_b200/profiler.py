@@ -26,18 +26,21 @@ from . import executor as gxe
 from . import models
 
 
-def _time_layer(shape: dict, batch: int, forward_only: bool, steps: int = 20, warmup: int = 3) -> float:
-    """ms per replay of one layer (serial plan) at `batch` samples."""
+def _time_layers(shapes: list, batch: int, forward_only: bool, steps: int = 20,
+                 warmup: int = 3) -> float:
+    """ms per replay of these layers in sequence (serial plan) at `batch` samples."""
     import torch
     m = {"dtype_bytes": 4, "layers": [{"param_bytes": 1, "activation_bytes_per_sample": 1,
-                                        "fwd_time_per_sample_ms": 1.0, "shape": dict(shape)}]}
-    plan = gxe.make_plan([""], batch)
+                                        "fwd_time_per_sample_ms": 1.0, "shape": dict(sh)}
+                                       for sh in shapes]}
+    plan = gxe.make_plan([""] * len(shapes), batch)
     ex = gxe.PlanExecutor(plan, m, 1, forward_only=forward_only, optimizer=False,
                           dropout_attn=0.1, dropout_hidden=0.1)
     ex.init_params(seed=1, std=0.02)
-    rows = batch * shape["seq"]
-    x = torch.randn(rows, shape["hidden"], device="cuda").to(torch.bfloat16)
-    ex.load_batch_device(x, x)
+    first, last = shapes[0], shapes[-1]
+    x = torch.randn(batch * first["seq"], first["hidden"], device="cuda").to(torch.bfloat16)
+    y = torch.randn(batch * last["seq"], last["hidden"], device="cuda").to(torch.bfloat16)
+    ex.load_batch_device(x, y)
     stream = torch.cuda.ExternalStream(ex.stream)
     for _ in range(warmup):
         ex.run(use_graph=True)
@@ -52,20 +55,33 @@ def _time_layer(shape: dict, batch: int, forward_only: bool, steps: int = 20, wa
     return a.elapsed_time(b) / steps
 
 
+def _time_layer(shape: dict, batch: int, forward_only: bool, prev: Optional[dict] = None) -> float:
+    """ms of one layer.  A patch-merging layer cannot start a model (its input is the
+    previous stage's grid), so it is timed behind its predecessor and the predecessor's own
+    time is subtracted."""
+    if not shape.get("merge"):
+        return _time_layers([shape], batch, forward_only)
+    assert prev is not None, "a merging layer needs its predecessor's shape"
+    return (_time_layers([prev, shape], batch, forward_only)
+            - _time_layers([prev], batch, forward_only))
+
+
 def profile_model(model: dict, batch: int = 4) -> tuple[dict, dict, dict]:
     """Returns (model with measured fwd_time_per_sample_ms, profile json, raw measurements)."""
     out = copy.deepcopy(model)
     cache: dict = {}
     raw = []
+    prev = None
     for layer in out["layers"]:
         key = json.dumps(layer["shape"], sort_keys=True)
         if key not in cache:
-            fwd = _time_layer(layer["shape"], batch, True)
-            full = _time_layer(layer["shape"], batch, False)
+            fwd = _time_layer(layer["shape"], batch, True, prev)
+            full = _time_layer(layer["shape"], batch, False, prev)
             cache[key] = (fwd, full)
             raw.append({"shape": layer["shape"], "batch": batch, "fwd_ms": fwd, "fwd_bwd_ms": full})
         fwd, full = cache[key]
         layer["fwd_time_per_sample_ms"] = round(fwd / batch, 6)
+        prev = layer["shape"]
     ratios = [(full - fwd) / fwd for fwd, full in cache.values() if fwd > 0]
     profile = {"backward_multiplier": round(sum(ratios) / len(ratios), 4)}
     return out, profile, {"layers": raw}

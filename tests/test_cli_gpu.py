@@ -143,3 +143,48 @@ def test_profile_feeds_the_search(tmp_path):
     code, so, se = _run("plan", "--model", om, "--cluster", c, "--profile", op, "--batches", "8,16")
     assert code == 0, se
     assert "throughput" in so
+
+
+def _swin_small():
+    layers = []
+    for st, (h, heads, grid) in enumerate(((64, 2, 14), (128, 4, 7))):
+        for i in range(2):
+            sh = {"hidden": h, "heads": heads, "head_dim": 32, "seq": grid * grid, "ffn": 2 * h,
+                  "kind": "window", "window": 49}
+            if st == 1 and i == 0:
+                sh["merge"] = True
+            if i == 1:
+                sh["shift"] = True
+            layers.append({"param_bytes": 4 * (12 * h * h + 13 * h),
+                           "activation_bytes_per_sample": 4 * grid * grid * h * 20,
+                           "fwd_time_per_sample_ms": 0.05, "shape": sh})
+    return {"dtype_bytes": 4, "layers": layers}
+
+
+def _t5_small():
+    m = _model(L=4)
+    for layer in m["layers"][2:]:
+        layer["shape"]["kind"] = "decoder"
+    return m
+
+
+@pytest.mark.parametrize("name", ["swin", "t5"])
+def test_run_and_profile_other_layer_families(tmp_path, name):
+    """`run` executes Swin (windows, SW-MSA, merging) and T5 (decoder) models; `profile`
+    times a merging layer behind its predecessor and writes planner-loadable inputs."""
+    model = _swin_small() if name == "swin" else _t5_small()
+    m = _dump(tmp_path, "m.json", model)
+    c = _dump(tmp_path, "c.json", _cluster(2))
+    rep = tmp_path / "rep.json"
+    code, so, se = _run("run", "--model", m, "--cluster", c, "--batches", "2,4", "--steps", 2,
+                        "--warmup", 1, "--dropout", 0.1, "--report", rep)
+    assert code == 0, se
+    assert math.isfinite(json.loads(rep.read_text())["loss"])
+    om, op = tmp_path / "mm.json", tmp_path / "pp.json"
+    code, so, se = _run("profile", "--model", m, "--batch", 2, "--steps", 3, "--warmup", 1,
+                        "--out-model", om, "--out-profile", op)
+    assert code == 0, se
+    times = [l["fwd_time_per_sample_ms"] for l in json.loads(om.read_text())["layers"]]
+    assert all(t > 0 for t in times), times
+    code, _, se = _run("plan", "--model", om, "--cluster", c, "--profile", op, "--batches", "2,4")
+    assert code == 0, se

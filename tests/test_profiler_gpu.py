@@ -59,3 +59,12 @@ def test_nccl_world_of_one_matches_sim(cuda):
         ex.close()
     assert outs[0][0] == outs[1][0]
     assert np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_profile_swin_merging_layer(cuda):
+    """A patch-merging layer is timed behind its predecessor (minus the predecessor)."""
+    from tests.test_cli_gpu import _swin_small
+    m, prof, raw = profiler.profile_model(_swin_small(), batch=2)
+    times = [l["fwd_time_per_sample_ms"] for l in m["layers"]]
+    assert all(t > 0 for t in times), times
+    assert 0.3 < prof["backward_multiplier"] < 10
