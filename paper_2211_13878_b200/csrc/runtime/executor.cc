@@ -315,6 +315,7 @@ class ExecutorImpl final : public Executor {
     comm_.reset();
     if (stream_ != nullptr) cudaStreamDestroy(stream_);
     if (side_ != nullptr) cudaStreamDestroy(side_);
+    if (cs_ != nullptr) cudaStreamDestroy(cs_);
     if (wg_ != nullptr) cudaStreamDestroy(wg_);
   }
 
@@ -524,6 +525,13 @@ class ExecutorImpl final : public Executor {
   // AdamW of layer l runs on side_ while layer l-1's backward runs on stream_ (HBM-bound
   // optimizer under tensor-bound GEMMs); joined back before the step ends.
   cudaStream_t side_ = nullptr;
+  // Gradient collectives (DP all-reduce, SDP reduce-scatter) of layer l run on cs_ beside
+  // layer l-1's backward (the overlap EstimateLayerCost models, cost_model.cc:200-206); the
+  // optimizer of layer l waits for them.  comm_stream_ = false keeps them on stream_.
+  cudaStream_t cs_ = nullptr;
+  bool comm_stream_ = true, cs_used_ = false;
+  std::vector<char> synced_on_cs_;  // per local layer index: this step's sync ran on cs_
+  bool comm_on_cs() const { return comm_stream_ && !profiling_ && cs_ != nullptr; }
   // Weight-gradient GEMMs (and the bias column sums) of the backward run on wg_, forked
   // from stream_ as soon as their inputs exist, so they fill the SMs the data-gradient
   // chain (the critical path) leaves idle.  ls_ is the stream gemm() launches on.
@@ -670,6 +678,8 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     mem_cap_ = cfg.value("memory_cap_bytes", static_cast<int64_t>(0));
     if (const char* e = std::getenv("GX_MEMORY_CAP")) mem_cap_ = std::atoll(e);
     wgrad_stream_ = cfg.value("wgrad_stream", true);
+    comm_stream_ = cfg.value("comm_stream", true);
+    if (const char* e = std::getenv("GX_COMM_STREAM")) comm_stream_ = e[0] != '0';
     trace_ = cfg.value("trace", false);
     fuse_dz_ = cfg.value("fuse_dz", false);
     opt_stream_ = cfg.value("optimizer_stream", 0);
@@ -854,6 +864,8 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
     if (cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, hi_prio) != cudaSuccess ||
         cudaStreamCreateWithPriority(&wg_, cudaStreamNonBlocking,
+                                     hi_prio < lo_prio ? hi_prio + 1 : lo_prio) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&cs_, cudaStreamNonBlocking,
                                      hi_prio < lo_prio ? hi_prio + 1 : lo_prio) != cudaSuccess) {
       *err = "executor: cudaStreamCreate failed";
       return kErrCuda;
@@ -2014,39 +2026,50 @@ int ExecutorImpl::merge_bwd(RankCtx& r, RankLayer& L, Acts& A, bf16* dX,
 int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
   RankLayer& L = r.layers[li];
   const int par = li & 1;
+  const bool syncs = L.d.sdp > 1 || L.d.dp > 1;
+  if (synced_on_cs_.size() < r.layers.size()) synced_on_cs_.assign(r.layers.size(), 0);
+  cudaStream_t cst = syncs && comm_on_cs() ? cs_ : stream_;
   if (phase == 0) {
-    // the gradient collectives read what this layer's wgrads (wgrad stream) wrote
-    if (wg_active_ && (L.d.sdp > 1 || L.d.dp > 1))
-      GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, r.wg_done[par], 0), "wgrad join"));
+    if (syncs && cst == cs_) {  // after everything the gradients came from on stream_ ...
+      GX_TRY(fork(stream_, cs_));
+      cs_used_ = true;
+    }
+    synced_on_cs_[li] = cst == cs_;
+    // ... and on the wgrad stream
+    if (wg_active_ && syncs)
+      GX_TRY(cuda_check(cudaStreamWaitEvent(cst, r.wg_done[par], 0), "wgrad join"));
     if (L.d.sdp > 1)
       return c_reduce_scatter(L.g_sdp, r.rank, L.gfull, L.gshard,
-                                   static_cast<size_t>(L.shard_n), DType::kF32, stream_);
+                                   static_cast<size_t>(L.shard_n), DType::kF32, cst);
     if (L.d.dp > 1)
       return c_all_reduce(L.g_dp, r.rank, L.gfull, static_cast<size_t>(L.lay.total),
-                               DType::kF32, stream_);
+                               DType::kF32, cst);
     return kOk;
   }
   if (phase == 1) {
     if (L.d.sdp > 1 && L.d.dp > 1)
       return c_all_reduce(L.g_dp, r.rank, L.gshard, static_cast<size_t>(L.shard_n),
-                               DType::kF32, stream_);
+                               DType::kF32, cst);
     return kOk;
   }
+  const bool on_cs = synced_on_cs_[li] != 0;
   if (phase == 2 && optimizer_ && !deferred() && persistent_opt()) {
     // the persistent optimizer (launched at the start of the backward) takes it from here
     int64_t* flag = r.opt_ready + (static_cast<int>(r.layers.size()) - 1 - li);
     if (wg_active_ && L.d.sdp == 1 && L.d.dp == 1)  // gradients complete on the wgrad stream
       return on_wgrad([&] { return mark_ready(flag, r.step, ls_); });
-    return mark_ready(flag, r.step, stream_);
+    return mark_ready(flag, r.step, on_cs ? cs_ : stream_);
   }
   if (phase == 2 && optimizer_ && !deferred()) {
     // with the AdamW-fused weight-gradient epilogues only the LayerNorm / bias prefix is left
     const int64_t n_opt = adam_fused(L) ? L.lay.acc_end : L.shard_n;
-    if (profiling_ || opt_stream_ == 2)  // instrumented runs keep everything on one stream
+    if (profiling_ || opt_stream_ == 2) {  // instrumented runs keep everything on one stream
+      if (on_cs) GX_TRY(fork(cs_, stream_));
       return timed(kOptim, 0, 30.0 * n_opt, [&] {
         return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, n_opt, lr_, b1_, b2_, eps_,
                          wd_, r.step, stream_);
       });
+    }
     if (fork_events_.size() <= static_cast<size_t>(fork_used_)) {
       cudaEvent_t e;
       GX_TRY(cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event"));
@@ -2054,6 +2077,7 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
     }
     if (opt_stream_ == 1 && wg_active_) {  // behind this layer's wgrads, in order
       GX_TRY(fork(stream_, wg_));
+      if (on_cs) GX_TRY(fork(cs_, wg_));
       tmark("opt_begin L" + std::to_string(L.layer), wg_);
       GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, n_opt, lr_, b1_, b2_, eps_,
                        wd_, r.step, wg_, opt_blocks_));
@@ -2070,6 +2094,7 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
     GX_TRY(cuda_check(cudaStreamWaitEvent(side_, e, 0), "fork wait"));
     if (wg_active_)  // ... and for the weight gradients
       GX_TRY(cuda_check(cudaStreamWaitEvent(side_, r.wg_done[par], 0), "fork wait wgrad"));
+    if (on_cs) GX_TRY(fork(cs_, side_));  // ... and their collectives
     side_used_ = true;
     tmark("opt_begin L" + std::to_string(L.layer), side_);
     AdamSegs segs;
@@ -2318,6 +2343,7 @@ int ExecutorImpl::step_once() {
   tmark("step_begin", stream_);
   side_used_ = false;
   wg_used_ = false;
+  cs_used_ = false;
   wg_active_ = wgrad_stream_ && !profiling_;
   ls_ = stream_;
   for (auto& r : ranks_) {
@@ -2450,6 +2476,7 @@ int ExecutorImpl::step_once() {
   if (wg_used_) {  // join the wgrad stream
     GX_TRY(fork(wg_, stream_));
   }
+  if (cs_used_) GX_TRY(fork(cs_, stream_));  // ... and the gradient-collective stream
   if (side_used_) {  // join the optimizer stream before the step completes
     GX_TRY(cuda_check(cudaEventRecord(join_event_, side_), "join record"));
     GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, join_event_, 0), "join wait"));
