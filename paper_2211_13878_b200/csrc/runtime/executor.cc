@@ -266,6 +266,7 @@ struct RankCtx {
   float* loss_ws = nullptr;  // deterministic loss reduction: block partials + ticket
   int* opt_pending = nullptr;  // deferred optimizer: gradients of the last step not applied yet
   std::vector<cudaEvent_t> opt_done;  // deferred optimizer: layer li updated (forward may read)
+  std::vector<cudaEvent_t> gath_ev;   // SDP parameter all-gather of layer li done (prefetch)
   std::vector<int> opt_group;         // side-stream optimizer: layers waiting for a grouped launch
   // persistent optimizer: layer table in backward order + per-entry "gradients ready" flags
   AdamSeg* opt_table = nullptr;
@@ -309,6 +310,8 @@ class ExecutorImpl final : public Executor {
       for (cudaEvent_t e : r->wg_done)
         if (e != nullptr) cudaEventDestroy(e);
       for (cudaEvent_t e : r->opt_done)
+        if (e != nullptr) cudaEventDestroy(e);
+      for (cudaEvent_t e : r->gath_ev)
         if (e != nullptr) cudaEventDestroy(e);
     }
     ranks_.clear();
@@ -381,7 +384,8 @@ class ExecutorImpl final : public Executor {
   int sync_phase(RankCtx& r, int li, int phase);
   int xin_fwd(RankCtx& r, int li, int mb);
   int xin_bwd(RankCtx& r, int li, int mb);
-  int gather_params(RankCtx& r, int li);
+  int gather_params(RankCtx& r, int li, cudaStream_t st);
+  bool prefetched_ = false;  // the current layer's SDP gather was prefetched on cs_
   int pp_fwd(RankCtx& r, int mb, bool send);
   int pp_bwd(RankCtx& r, int mb, bool send);
   struct Xfer {
@@ -1141,6 +1145,10 @@ int ExecutorImpl::allocate(RankCtx& r) {
   }
   r.opt_done.resize(r.layers.size(), nullptr);
   for (auto& e : r.opt_done)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+      return set_error(kErrCuda, "executor: event creation failed");
+  r.gath_ev.resize(r.layers.size(), nullptr);
+  for (auto& e : r.gath_ev)
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
       return set_error(kErrCuda, "executor: event creation failed");
   r.seed_off = A.a<uint64_t>(1);
@@ -2136,11 +2144,11 @@ int ExecutorImpl::flush_optimizer() {
   return cuda_check(cudaStreamSynchronize(stream_), "flush");
 }
 
-int ExecutorImpl::gather_params(RankCtx& r, int li) {
+int ExecutorImpl::gather_params(RankCtx& r, int li, cudaStream_t st) {
   RankLayer& L = r.layers[li];
   if (L.d.sdp <= 1) return kOk;
   std::vector<size_t> counts(L.d.sdp, static_cast<size_t>(L.shard_n));
-  return c_all_gather(L.g_sdp, r.rank, L.pshard, L.pfull, counts, DType::kBF16, stream_);
+  return c_all_gather(L.g_sdp, r.rank, L.pshard, L.pfull, counts, DType::kBF16, st);
 }
 
 // Forward relayout into layer li (same stage): only the all-gather case moves data.
@@ -2386,8 +2394,32 @@ int ExecutorImpl::step_once() {
           for (RankCtx* r : R)
             GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, r->opt_done[li], 0), "opt wait"));
         for (RankCtx* r : R) GX_TRY(xin_fwd(*r, li, mb));
-        if (mb == 0)
-          for (RankCtx* r : R) GX_TRY(gather_params(*r, li));
+        if (mb == 0) {
+          // SDP parameters: gathered on stream_ for the stage's first layer, prefetched on
+          // cs_ one layer ahead for the rest (the all-gather overlaps the previous layer)
+          const bool pre = li > 0 && prefetched_;
+          for (RankCtx* r : R) {
+            if (r->layers[li].d.sdp <= 1) continue;
+            if (pre)
+              GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, r->gath_ev[li], 0), "gather wait"));
+            else
+              GX_TRY(gather_params(*r, li, stream_));
+          }
+          prefetched_ = false;
+          if (comm_on_cs() && li + 1 < nl && R[0]->layers[li + 1].d.sdp > 1) {
+            GX_TRY(fork(stream_, cs_));
+            cs_used_ = true;
+            for (RankCtx* r : R) {
+              if (deferred())  // the next layer's shard carries the last step's update
+                GX_TRY(cuda_check(cudaStreamWaitEvent(cs_, r->opt_done[li + 1], 0), "opt wait"));
+              GX_TRY(gather_params(*r, li + 1, cs_));
+            }
+            // recorded after every rank posted: a simulated collective runs at the last post
+            for (RankCtx* r : R)
+              GX_TRY(cuda_check(cudaEventRecord(r->gath_ev[li + 1], cs_), "gather done"));
+            prefetched_ = true;
+          }
+        }
         const int phases = tp_phases(R[0]->layers[li]);
         for (int ph = 0; ph < phases; ++ph)
           for (RankCtx* r : R) GX_TRY(fwd_phase(*r, li, mb, ph));
