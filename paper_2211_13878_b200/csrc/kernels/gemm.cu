@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <algorithm>
 #include <cstdio>
 
@@ -1013,6 +1014,15 @@ static int pick_tile(int M, int N, bool b_mn) {
       best = -bn;
     }
   }
+  // One CTA per 128 x 64 tile when that still fits one wave: at M = 512, N = 1280 (the
+  // out-projection forward and data-gradient) 80 CTAs beat 20 CTA pairs of 256 x 128
+  // (measured 9.6 vs 11.3 us and 8.3 vs 8.8 us, scripts/tile_sweep.py).
+  static const bool tile64 = [] {
+    const char* e = std::getenv("GX_TILE64");
+    return e == nullptr || e[0] != '0';
+  }();
+  const int tiles64 = ((M + 127) / 128) * ((N + 63) / 64);
+  if (tile64 && tiles64 <= num_sms() && 64 + 48.0 < best_cost - 1e-9) best = 64;
   return best;
 }
 
