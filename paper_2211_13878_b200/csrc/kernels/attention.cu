@@ -93,6 +93,14 @@ __device__ __forceinline__ int swin_region(const gx_attention_args& p, int b, in
   return (y < l0 ? 0 : (y < l1 ? 1 : 2)) * 3 + (x < l0 ? 0 : (x < l1 ? 1 : 2));
 }
 
+// Relative-position bias of (q, k) inside a side x side window (log2 units, head h).
+__device__ __forceinline__ float rpb_bias(const gx_attention_args& p, int h, int q, int k) {
+  const int w = p.rpb_side, n = 2 * w - 1;
+  const int e = (q / w - k / w + w - 1) * n + (q % w - k % w + w - 1);
+  return __bfloat162float(static_cast<const __nv_bfloat16*>(p.rpb)[h * n * n + e]) *
+         1.4426950408889634f;
+}
+
 }  // namespace
 
 // --------------------------------------------------------------------------- forward
@@ -180,6 +188,7 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_a
         const int key = kb * kBlk + nb * 8 + 2 * t + (j & 1);
         float v = sacc[nb][j] * c2;
         const int qrow = q0 + warp * 16 + g + 8 * (j >> 1);
+        if (kMask && p.rpb != nullptr && key < s && qrow < s) v += rpb_bias(p, h, qrow, key);
         if (key >= s || (kMask && ((p.causal && key > qrow) ||
                                    (p.win_shift > 0 && key < s && qrow < s &&
                                     swin_region(p, b, qrow) != swin_region(p, b, key)))))
@@ -410,7 +419,10 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
                              !(kMask && ((p.causal && key > q) ||
                                          (p.win_shift > 0 &&
                                           swin_region(p, b, q) != swin_region(p, b, key))));
-        float P = keep_pk ? exp2f(st[nb][j] * c2 - sL[ql]) : 0.f;
+        float P = keep_pk ? exp2f(st[nb][j] * c2 +
+                                  (kMask && p.rpb != nullptr ? rpb_bias(p, h, q, key) : 0.f) -
+                                  sL[ql])
+                          : 0.f;
         float keep = 1.f;
         if (thr != 0u) {
           const int kk = key - k0;  // 0..63 within this CTA's key block
@@ -419,6 +431,9 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
         }
         pd[nb][j] = P * keep;
         st[nb][j] = P * (dpt[nb][j] * keep - sD[ql]);  // dS^T
+        if (kMask && p.rpb_dpart != nullptr && q < s && key < s)  // dL/d(bias) per (q, k)
+          static_cast<float*>(p.rpb_dpart)[(static_cast<int64_t>(bh) * s + q) * s + key] =
+              st[nb][j];
       }
     }
     // dV += Pd^T dO ; dK += dS^T Q   (k-dim = queries)
@@ -538,7 +553,7 @@ static int attention_fwd_impl(const gx_attention_args& a, cudaStream_t st) {
     set = true;
   }
   dim3 grid((a.seq + kBlk - 1) / kBlk, a.batch * a.heads);
-  if (a.causal || a.win_shift > 0)
+  if (a.causal || a.win_shift > 0 || a.rpb != nullptr)
     launch_k(attn_fwd_kernel<HD, true>, grid, dim3(kThreads), smem, st, a);
   else
     launch_k(attn_fwd_kernel<HD, false>, grid, dim3(kThreads), smem, st, a);
@@ -559,7 +574,7 @@ static int attention_bwd_impl(const gx_attention_args& a, cudaStream_t st) {
   launch_k(attn_bwd_prep_kernel<HD>, dim3((rows + 7) / 8), dim3(256), 0, st, a);
   if (int rc = check_launch("attn_bwd_prep_kernel")) return rc;
   dim3 grid((a.seq + kBlk - 1) / kBlk, a.batch * a.heads);
-  if (a.causal || a.win_shift > 0)
+  if (a.causal || a.win_shift > 0 || a.rpb != nullptr)
     launch_k(attn_bwd_kernel<HD, true>, grid, dim3(kThreads), smem, st, a);
   else
     launch_k(attn_bwd_kernel<HD, false>, grid, dim3(kThreads), smem, st, a);
@@ -569,6 +584,41 @@ static int attention_bwd_impl(const gx_attention_args& a, cudaStream_t st) {
   if (blocks > 148 * 16) blocks = 148 * 16;
   launch_k(attn_bwd_dq_kernel<HD>, dim3(blocks), dim3(256), 0, st, a);
   return check_launch("attn_bwd_dq_kernel");
+}
+
+// grad[h][e] (+)= sum_b sum_{(q,k): offset e} dpart[b*heads + h][q][k]: one block per (h, e),
+// threads stride over b, fixed-order tree reduction (deterministic).
+__global__ void rpb_grad_kernel(const float* __restrict__ dpart, int batch, int heads, int side,
+                                float* __restrict__ grad, bool accumulate) {
+  pdl_enter();
+  const int n = 2 * side - 1, ne = n * n, s = side * side;
+  const int h = blockIdx.x / ne, e = blockIdx.x % ne;
+  const int dy = e / n - (side - 1), dx = e % n - (side - 1);
+  float acc = 0.f;
+  for (int b = threadIdx.x; b < batch; b += blockDim.x) {
+    const float* src = dpart + (static_cast<int64_t>(b) * heads + h) * s * s;
+    for (int q = 0; q < s; ++q) {
+      const int yk = q / side - dy, xk = q % side - dx;
+      if (yk >= 0 && yk < side && xk >= 0 && xk < side) acc += src[q * s + yk * side + xk];
+    }
+  }
+  __shared__ float red[256];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (static_cast<int>(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) grad[h * ne + e] = (accumulate ? grad[h * ne + e] : 0.f) + red[0];
+}
+
+int rpb_grad(const float* dpart, int batch, int heads, int side, float* grad, bool accumulate,
+             cudaStream_t st) {
+  if (batch <= 0) return kOk;
+  const int n = 2 * side - 1;
+  launch_k(rpb_grad_kernel, dim3(heads * n * n), dim3(256), 0, st, dpart, batch, heads, side,
+           grad, accumulate);
+  return check_launch("rpb_grad_kernel");
 }
 
 int attention_fwd(const gx_attention_args& a, cudaStream_t st) {

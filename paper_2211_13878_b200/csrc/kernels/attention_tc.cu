@@ -702,7 +702,7 @@ bool attention_tc_supported(const gx_attention_args& a) {
     const char* e = std::getenv("GX_ATTN_TC");
     return e == nullptr || e[0] != '0';
   }();
-  return on && a.head_dim == kTcHD && a.seq >= 1 && a.seq <= kTcMaxKeys && a.win_shift == 0 &&
+  return on && a.head_dim == kTcHD && a.seq >= 1 && a.seq <= kTcMaxKeys && a.win_shift == 0 && a.rpb == nullptr &&
          (a.ld_qkv % 8) == 0 && (reinterpret_cast<uintptr_t>(a.qkv) % 16) == 0 &&
          (a.ld_ctx % 8) == 0;
 }

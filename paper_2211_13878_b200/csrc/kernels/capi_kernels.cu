@@ -121,3 +121,8 @@ extern "C" int gx_k_window_roll(const void* src, void* dst, int samples, int gri
   return gx::window_roll(src, dst, samples, grid, window_side, shift, channels, inverse != 0,
                          S(stream));
 }
+extern "C" int gx_k_rpb_grad(const void* dpart, int batch, int heads, int side, void* grad,
+                             int accumulate, void* stream) {
+  return gx::rpb_grad(static_cast<const float*>(dpart), batch, heads, side,
+                      static_cast<float*>(grad), accumulate != 0, S(stream));
+}

@@ -161,6 +161,10 @@ int patch_merge(const void* src, void* dst, int samples, int grid_out, int ws, i
 // inverse rolls back.  A row permutation: every row copied once.
 int window_roll(const void* src, void* dst, int samples, int grid, int ws, int shift, int c,
                 bool inverse, cudaStream_t st);
+// Swin relative-position bias gradient (attention.cu): grad[h][e] (+)= fixed-order sum over
+// b < batch and the (q, k) pairs of offset e of dpart[b * heads + h][q][k]
+int rpb_grad(const float* dpart, int batch, int heads, int side, float* grad, bool accumulate,
+             cudaStream_t st);
 int num_sms();
 
 }  // namespace gx

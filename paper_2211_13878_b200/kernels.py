@@ -103,7 +103,8 @@ class _AttnArgs(ctypes.Structure):
                 ("seed", ctypes.c_uint64), ("site", ctypes.c_uint64),
                 ("seed_offset", ctypes.c_void_p), ("mask", ctypes.c_void_p),
                 ("trace", ctypes.c_void_p), ("causal", ctypes.c_int),
-                ("win_grid", ctypes.c_int), ("win_side", ctypes.c_int), ("win_shift", ctypes.c_int)]
+                ("win_grid", ctypes.c_int), ("win_side", ctypes.c_int), ("win_shift", ctypes.c_int),
+                ("rpb", ctypes.c_void_p), ("rpb_dpart", ctypes.c_void_p), ("rpb_side", ctypes.c_int)]
 
 
 class Dropout(ctypes.Structure):
@@ -122,9 +123,12 @@ def make_dropout(p, seed, site, row_offset=0, col_offset=0, drop_ld=0):
 
 
 def _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, heads_total=None, head_offset=0,
-               sample_offset=0, causal=False, win=None):
+               sample_offset=0, causal=False, win=None, rpb=None, rpb_dpart=None):
     a = _AttnArgs()
     a.causal = int(causal)
+    if rpb is not None:  # Swin relative-position bias table [heads][(2 side - 1)^2] (bf16)
+        a.rpb, a.rpb_side = _ptr(rpb), int(round(seq ** 0.5))
+        a.rpb_dpart = _ptr(rpb_dpart) if rpb_dpart is not None else None
     if win is not None:  # (grid, side, shift): Swin shifted-window region mask
         a.win_grid, a.win_side, a.win_shift = win
     a.batch, a.seq, a.heads, a.head_dim = batch, seq, heads, head_dim
@@ -260,3 +264,11 @@ def window_roll(x, samples, grid, window_side, shift, inverse=False):
     _lib.check(_lib.lib().gx_k_window_roll(_ptr(x), _ptr(out), samples, grid, window_side, shift,
                                            x.shape[1], int(inverse), _lib.stream_ptr()))
     return out
+
+
+def rpb_grad(dpart, batch, heads, side, grad, accumulate=True):
+    """Relative-position-bias gradient: fixed-order sum of the per-(window, head) score
+    gradients into grad (fp32 [heads][(2 side - 1)^2])."""
+    _lib.check(_lib.lib().gx_k_rpb_grad(_ptr(dpart), batch, heads, side, _ptr(grad),
+                                        int(accumulate), _lib.stream_ptr()))
+    return grad
