@@ -123,12 +123,14 @@ GX_API const char* gx_plan_last_error(void);
  *   "encoder" (pre-LN BERT/ViT layer), "causal" (decoder-only self-attention),
  *   "decoder" (T5: causal self-attention + cross-attention over the first decoder layer's
  *   input + MLP; decoder layers are the model's suffix) or "window" (Swin: "window"
- *   tokens per attention window, window-major; "shift": true = SW-MSA; "merge": true = patch
- *   merging of a [4*seq, hidden/2] input first).
+ *   tokens per attention window, window-major; "shift": true = SW-MSA; "rel_pos": true =
+ *   learned relative-position bias; "merge": true = patch merging of a [4*seq, hidden/2]
+ *   input first).
  * Parameters cross the boundary in the canonical unsharded fp32 order
  * ln1_g ln1_b ln2_g ln2_b b_qkv b_o b_1 b_2 w_qkv w_o w_1 w_2 (row-major, [out][in]), then
  * mln_g mln_b w_m (merging layers) or ln3_g ln3_b b_q2 b_kv2 b_o2 w_q2 w_kv2 w_o2 (decoder
- * layers); the executor slices each rank's TP slice and SDP shard.  Batches are global bf16
+ * layers), then rpb [heads][(2 side - 1)^2] (rel_pos window layers); the executor slices each
+ * rank's TP slice and SDP shard.  Batches are global bf16
  * [batch*seq][hidden] arrays; each rank copies only its own rows. */
 typedef struct gx_exec gx_exec;
 GX_API int gx_exec_create(const char* config_json, gx_exec** out);

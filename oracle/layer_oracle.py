@@ -95,6 +95,7 @@ class LayerShape:
     causal: bool = False  # decoder self-attention: query q sees keys k <= q
     cross: bool = False   # T5 decoder: + cross-attention sublayer over the memory
     shift: int = 0        # Swin SW-MSA: tokens rolled by -shift around the window attention
+    rpb: bool = False     # Swin relative-position bias table [heads][(2 side - 1)^2]
 
     @property
     def att_seq(self):
@@ -153,8 +154,21 @@ def shift_regions(seq: int, window: int, shift: int) -> np.ndarray:
     return reg.reshape(seq // window, window)
 
 
+def rel_index(window: int) -> np.ndarray:
+    """[window, window] relative-position index of (q, k) in a side x side window (Swin's
+    relative_position_index): (dy + side - 1) * (2 side - 1) + dx + side - 1."""
+    w = math.isqrt(window)
+    y, x = np.arange(window) // w, np.arange(window) % w
+    return (y[:, None] - y[None] + w - 1) * (2 * w - 1) + (x[:, None] - x[None] + w - 1)
+
+
 def init_layer_params(shape: LayerShape, rng: np.random.Generator, std=0.02) -> dict:
     h, f = shape.hidden, shape.ffn
+    if shape.rpb:
+        n2 = (2 * math.isqrt(shape.window) - 1) ** 2
+        rp = {"rpb": 0.5 * rng.standard_normal((shape.heads, n2))}
+    else:
+        rp = {}
     merge = {} if not shape.merge else {
         "mln_g": 1.0 + 0.1 * rng.standard_normal(2 * h), "mln_b": 0.1 * rng.standard_normal(2 * h),
         "w_m": std * rng.standard_normal((h, 2 * h))}
@@ -164,7 +178,7 @@ def init_layer_params(shape: LayerShape, rng: np.random.Generator, std=0.02) -> 
             "w_q2": std * rng.standard_normal((h, h)), "b_q2": 0.02 * rng.standard_normal(h),
             "w_kv2": std * rng.standard_normal((2 * h, h)), "b_kv2": 0.02 * rng.standard_normal(2 * h),
             "w_o2": std * rng.standard_normal((h, h)), "b_o2": 0.02 * rng.standard_normal(h)}
-    return merge | {
+    return rp | merge | {
         "ln1_g": 1.0 + 0.1 * rng.standard_normal(h), "ln1_b": 0.1 * rng.standard_normal(h),
         "w_qkv": std * rng.standard_normal((3 * h, h)), "b_qkv": 0.02 * rng.standard_normal(3 * h),
         "w_o": std * rng.standard_normal((h, h)), "b_o": 0.02 * rng.standard_normal(h),
@@ -298,6 +312,8 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
     k = qkv[:, h:2 * h].reshape(n, s, H, d).transpose(0, 2, 1, 3)
     v = qkv[:, 2 * h:].reshape(n, s, H, d).transpose(0, 2, 1, 3)
     sc = q @ k.transpose(0, 1, 3, 2) / math.sqrt(d)
+    if shape.rpb:
+        sc = sc + P["rpb"][:, rel_index(s)][None]
     if shape.causal:
         sc = np.where(np.triu(np.ones((s, s), dtype=bool), 1), -np.inf, sc)
     if shape.shift:
@@ -382,6 +398,11 @@ def layer_backward(P: dict, dy: np.ndarray, cache: dict, shape: LayerShape):
     dpr = dpd * cache["am"] * cache["ka"]
     pr = cache["pr"]
     dsc = pr * (dpr - (dpr * pr).sum(-1, keepdims=True))
+    if shape.rpb:
+        idx = rel_index(s).ravel()
+        tot = dsc.sum(0).reshape(H, -1)  # [H, s*s]
+        G["rpb"] = np.stack([np.bincount(idx, weights=tot[hh], minlength=P["rpb"].shape[1])
+                             for hh in range(H)])
     dsc = dsc / math.sqrt(d)
     dq = dsc @ cache["k"]
     dk = dsc.transpose(0, 1, 3, 2) @ cache["q"]

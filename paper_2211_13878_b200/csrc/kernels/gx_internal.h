@@ -143,7 +143,7 @@ int sum_ptrs(const PtrPack& srcs, void* out, int64_t n, bool bf16, cudaStream_t 
 // Flat per-rank parameter layout (slot order ln1g ln1b ln2g ln2b bqkv bo b1 b2 wqkv wo w1 w2,
 // then the patch-merging mlng mlnb wm, empty unless the layer merges).
 struct InitLayout {
-  int64_t off[23], n[23];  // + cross-attention ln3g ln3b bq2 bkv2 bo2 wq2 wkv2 wo2
+  int64_t off[24], n[24];  // + cross-attention ln3g ln3b bq2 bkv2 bo2 wq2 wkv2 wo2, rpb
   int64_t h, f;
   int extra;               // 0 none, 1 patch merging, 2 cross-attention (after w_2)
   int t, tr;

@@ -67,6 +67,7 @@ Layout make_layout(const Shape& s, int tp, int sdp) {
   put(L.bq2, xht);
   put(L.bkv2, 2 * xht);
   put(L.bo2, xh);
+  put(L.rpb, s.rpb ? static_cast<int64_t>(s.heads / tp) * s.rpb_n() : 0);
   L.acc_end = off;
   put(L.wqkv, 3 * h / tp * h);
   put(L.wo, h * (h / tp));
@@ -86,7 +87,8 @@ int64_t canonical_size(const Shape& s) {
   const int64_t merge = s.merge ? 4 * h + 2 * h * h : 0;  // mln_g, mln_b (2h each), w_m [h][2h]
   // ln3_g ln3_b b_q2 b_kv2(2h) b_o2, w_q2 [h][h], w_kv2 [2h][h], w_o2 [h][h]
   const int64_t cross = s.cross ? 6 * h + 4 * h * h : 0;
-  return 4 * h + 3 * h + h + f + h + 3 * h * h + h * h + f * h + h * f + merge + cross;
+  const int64_t rpb = s.rpb ? static_cast<int64_t>(s.heads) * s.rpb_n() : 0;
+  return 4 * h + 3 * h + h + f + h + 3 * h * h + h * h + f * h + h * f + merge + cross + rpb;
 }
 
 namespace {
@@ -134,6 +136,7 @@ int64_t canon_index(const Shape& s, const Layout& L, int t, int tr, int64_t j) {
     return c_m + 6 * h + h * h + ((row / ht) * h + tr * ht + row % ht) * h + col;
   }
   if (in(L.wo2, k)) return c_m + 6 * h + 3 * h * h + (k / ht) * h + tr * ht + k % ht;
+  if (in(L.rpb, k)) return c_m + (s.merge ? 4 * h + 2 * h * h : 0) + tr * L.rpb.n + k;
   return -1;
 }
 
@@ -249,6 +252,7 @@ struct RankCtx {
   // layer's input gradient)
   bf16 *dout2 = nullptr, *dqkv2 = nullptr;
   bf16 *dctxr = nullptr, *rollbuf = nullptr;  // SW-MSA backward scratch (rolled dctx, da)
+  float* rpb_part = nullptr;  // relative-position bias: per-(window, head) score gradients
   float* dmem = nullptr;
   int dec_li = -1;  // local index of the model's first decoder layer on this rank, or -1
   // stages after the first decoder layer's: the memory received with each micro-batch's
@@ -750,6 +754,7 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
         }
         s.shift = g > ws ? ws / 2 : 0;  // one window covers the grid: Swin skips the shift
       }
+      s.rpb = kind == "window" && sh.value("rel_pos", false);
       s.merge = sh.value("merge", false);
       if (s.merge) {
         const int g = static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.seq))));
@@ -966,6 +971,7 @@ int ExecutorImpl::allocate(RankCtx& r) {
   int64_t max_rows = 0, max_h = 0, max_f = 0, max_q = 0, max_c = 0, max_lse = 0, max_m = 0,
           max_x = 0;
   bool any_shift = false;
+  int64_t max_rpb = 0;
   for (size_t li = 0; li < r.layers.size(); ++li) {
     RankLayer& L = r.layers[li];
     const Shape& s = L.sh;
@@ -1036,6 +1042,9 @@ int ExecutorImpl::allocate(RankCtx& r) {
         a.rstd3 = A.a<float>(rows);
         max_x = std::max(max_x, rows * h);
       }
+      if (s.rpb)
+        max_rpb = std::max<int64_t>(max_rpb, static_cast<int64_t>(a.samples) * (s.heads / t) *
+                                                 s.seq * s.win);
       if (s.shift > 0) {
         a.ln1r = A.a<bf16>(rows * h);
         a.ctxr = A.a<bf16>(rows * ht);
@@ -1079,6 +1088,7 @@ int ExecutorImpl::allocate(RankCtx& r) {
     r.dctxr = A.a<bf16>(max_c);
     r.rollbuf = A.a<bf16>(max_h);
   }
+  if (max_rpb > 0) r.rpb_part = A.a<float>(max_rpb);
   if (max_x > 0) {
     int64_t hx = 0;
     for (const RankLayer& L : r.layers) hx = std::max<int64_t>(hx, L.sh.h);
@@ -1260,13 +1270,13 @@ int ExecutorImpl::init_params(uint64_t seed, float std_dev) {
   for (auto& r : ranks_) {
     for (RankLayer& L : r->layers) {
       InitLayout il{};
-      const Slot* slots[23] = {&L.lay.ln1g, &L.lay.ln1b, &L.lay.ln2g, &L.lay.ln2b, &L.lay.bqkv,
+      const Slot* slots[24] = {&L.lay.ln1g, &L.lay.ln1b, &L.lay.ln2g, &L.lay.ln2b, &L.lay.bqkv,
                                &L.lay.bo,   &L.lay.b1,   &L.lay.b2,   &L.lay.wqkv, &L.lay.wo,
                                &L.lay.w1,   &L.lay.w2,   &L.lay.mlng, &L.lay.mlnb, &L.lay.wm,
                                &L.lay.ln3g, &L.lay.ln3b, &L.lay.bq2,  &L.lay.bkv2, &L.lay.bo2,
-                               &L.lay.wq2,  &L.lay.wkv2, &L.lay.wo2};
+                               &L.lay.wq2,  &L.lay.wkv2, &L.lay.wo2,  &L.lay.rpb};
       il.extra = L.sh.merge ? 1 : (L.sh.cross ? 2 : 0);
-      for (int i = 0; i < 23; ++i) {
+      for (int i = 0; i < 24; ++i) {
         il.off[i] = slots[i]->off;
         il.n[i] = slots[i]->n;
       }
@@ -1423,6 +1433,10 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     at.ld_ctx = ht;
     at.lse = A.lse;
     set_window_mask(at, s);
+    if (s.rpb) {
+      at.rpb = P + L.lay.rpb.off;
+      at.rpb_side = side_of(s);
+    }
     at.drop_threshold = thr_attn_;
     at.drop_scale = scale_of(p_attn_);
     at.seed = seed_;
@@ -1750,6 +1764,11 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     at.ld_ctx = ht;
     at.lse = A.lse;
     set_window_mask(at, s);
+    if (s.rpb) {
+      at.rpb = P + L.lay.rpb.off;
+      at.rpb_side = side_of(s);
+      at.rpb_dpart = r.rpb_part;
+    }
     at.dctx = s.shift > 0 ? r.dctxr : r.dctx;
     at.dqkv = dqkv;
     at.dq_accum = r.dq_acc;
@@ -1765,6 +1784,11 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       const double af = 10.0 * A.samples * (s.heads / t) * double(s.seq) * s.win * s.hd;
       GX_TRY(timed(kAttnBwd, af, 2.0 * rows * 8 * ht, [&] { return attention_bwd(at, stream_); }));
     }
+    if (s.rpb)  // table gradient: fixed-order sum of the per-window score gradients
+      GX_TRY(timed(kElementwise, 0, 4.0 * A.samples * (s.heads / t) * double(s.seq) * s.win, [&] {
+        return rpb_grad(r.rpb_part, A.samples * s.windows(), s.heads / t, side_of(s),
+                        G + L.lay.rpb.off, true, stream_);
+      }));
     auto wgradq = [&] {
       return on_wgrad([&]() -> int {
         GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, ls_, r.cs_ws[ls_ == stream_ ? 0 : 1]); }));

@@ -43,6 +43,12 @@ struct Shape {
   // cross-attention sublayer over the memory (the input of the model's first decoder layer)
   bool causal = false, cross = false;
   int shift = 0;  // Swin SW-MSA: tokens rolled by -shift in both grid axes around attention
+  bool rpb = false;  // Swin relative-position bias table [heads][(2 side - 1)^2]
+  int rpb_n() const {  // table entries per head
+    int w = 1;
+    while (w * w < win) ++w;
+    return (2 * w - 1) * (2 * w - 1);
+  }
   int in_h() const { return merge ? h / 2 : h; }
   int in_seq() const { return merge ? 4 * seq : seq; }
 };
@@ -56,6 +62,7 @@ struct Layout {
   Slot mlng, mlnb, wm;  // patch merging (empty unless Shape::merge): LN(2h) and [h][2h]
   // cross-attention (empty unless Shape::cross): LN3, q / kv / out projections
   Slot ln3g, ln3b, bq2, bkv2, bo2, wq2, wkv2, wo2;
+  Slot rpb;  // Swin relative-position bias, this rank's heads (gradient accumulated)
   int64_t acc_end = 0;  // [0, acc_end): params whose grads accumulate with atomics
   int64_t total = 0;    // padded to a multiple of 64 * sdp
   int64_t shard() const { return total; }

@@ -22,12 +22,13 @@ CROSS_ORDER = ("ln3_g", "ln3_b", "b_q2", "b_kv2", "b_o2", "w_q2", "w_kv2", "w_o2
 def pack_canonical(P: dict) -> np.ndarray:
     """Layer parameter dict (oracle naming) -> canonical flat fp32 vector."""
     keys = CANONICAL_ORDER + (MERGE_ORDER if "w_m" in P else ()) + \
-        (CROSS_ORDER if "w_q2" in P else ())
+        (CROSS_ORDER if "w_q2" in P else ()) + (("rpb",) if "rpb" in P else ())
     return np.concatenate([np.asarray(P[k], dtype=np.float32).ravel() for k in keys])
 
 
 def unpack_canonical(flat: np.ndarray, hidden: int, ffn: int, merge: bool = False,
-                     cross: bool = False) -> dict:
+                     cross: bool = False, rpb=None) -> dict:
+    """rpb: (heads, entries per head) of a relative-position-bias table, or None."""
     h, f = hidden, ffn
     shapes = {"ln1_g": (h,), "ln1_b": (h,), "ln2_g": (h,), "ln2_b": (h,), "b_qkv": (3 * h,),
               "b_o": (h,), "b_1": (f,), "b_2": (h,), "w_qkv": (3 * h, h), "w_o": (h, h),
@@ -36,7 +37,10 @@ def unpack_canonical(flat: np.ndarray, hidden: int, ffn: int, merge: bool = Fals
               "ln3_g": (h,), "ln3_b": (h,), "b_q2": (h,), "b_kv2": (2 * h,), "b_o2": (h,),
               "w_q2": (h, h), "w_kv2": (2 * h, h), "w_o2": (h, h)}
     out, off = {}, 0
-    for k in CANONICAL_ORDER + (MERGE_ORDER if merge else ()) + (CROSS_ORDER if cross else ()):
+    if rpb is not None:
+        shapes["rpb"] = tuple(rpb)
+    for k in CANONICAL_ORDER + (MERGE_ORDER if merge else ()) + (CROSS_ORDER if cross else ()) + \
+            (("rpb",) if rpb is not None else ()):
         n = int(np.prod(shapes[k]))
         out[k] = flat[off:off + n].reshape(shapes[k])
         off += n
@@ -113,8 +117,17 @@ class PlanExecutor:
         n = ctypes.c_int64()
         _lib.lib().gx_exec_canonical_size(s["hidden"], s["ffn"], ctypes.byref(n))
         h = s["hidden"]
+        rp = self._rpb_shape(s)
         return n.value + (4 * h + 2 * h * h if s.get("merge") else 0) + \
-            (6 * h + 4 * h * h if s.get("kind") == "decoder" else 0)
+            (6 * h + 4 * h * h if s.get("kind") == "decoder" else 0) + \
+            (rp[0] * rp[1] if rp else 0)
+
+    @staticmethod
+    def _rpb_shape(s):
+        if s.get("kind") != "window" or not s.get("rel_pos"):
+            return None
+        side = int(round(s.get("window", 49) ** 0.5))
+        return (s["heads"], (2 * side - 1) ** 2)
 
     def set_layer_params(self, layer: int, P: dict):
         flat = np.ascontiguousarray(pack_canonical(P))
@@ -129,7 +142,7 @@ class PlanExecutor:
             out.ctypes.data_as(ctypes.c_void_p), n))
         s = self.shapes[layer]
         return unpack_canonical(out, s["hidden"], s["ffn"], bool(s.get("merge")),
-                                s.get("kind") == "decoder")
+                                s.get("kind") == "decoder", self._rpb_shape(s))
 
     @property
     def stream(self) -> int:

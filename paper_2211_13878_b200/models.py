@@ -80,6 +80,7 @@ def _swin():
                 shape["merge"] = True
             if i % 2 == 1:
                 shape["shift"] = True  # SW-MSA on odd blocks (the 7x7 last stage skips it)
+            shape["rel_pos"] = True    # learned relative-position bias per head
             layers.append({"param_bytes": p, "activation_bytes_per_sample": a,
                            "fwd_time_per_sample_ms": t, "name": f"stage{st}.{i}",
                            "shape": shape})

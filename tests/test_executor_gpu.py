@@ -44,7 +44,8 @@ def _oshape(shp):
     return lo.LayerShape(shp["hidden"], shp["heads"], shp["seq"], shp["ffn"],
                          shp.get("window", 0) if kind == "window" else 0,
                          bool(shp.get("merge", False)), kind in ("causal", "decoder"),
-                         kind == "decoder", shift)
+                         kind == "decoder", shift,
+                         bool(kind == "window" and shp.get("rel_pos", False)))
 
 
 def _run_case(plan, model, world, p_drop=0.0, seed=11, optimizer=False):
@@ -248,7 +249,7 @@ def test_window_layer_rejects_ragged_windows(cuda):
         gxe.PlanExecutor(gxe.make_plan([""], 2), model, 1)
 
 
-def _swin_like(h0=64, heads0=2, grid0=14, window=49, stages=(2, 2), shifted=True):
+def _swin_like(h0=64, heads0=2, grid0=14, window=49, stages=(2, 2), shifted=True, rel_pos=True):
     """Window layers over a grid0 x grid0 token grid; each later stage starts with a
     patch-merging layer (grid / 2, hidden x 2, heads x 2)."""
     layers, h, heads, grid = [], h0, heads0, grid0
@@ -260,6 +261,8 @@ def _swin_like(h0=64, heads0=2, grid0=14, window=49, stages=(2, 2), shifted=True
                 shape["merge"] = True
             if i % 2 == 1 and shifted:
                 shape["shift"] = True  # Swin's odd blocks: SW-MSA
+            if rel_pos:
+                shape["rel_pos"] = True
             layers.append({"param_bytes": 1, "activation_bytes_per_sample": 1,
                            "fwd_time_per_sample_ms": 0.1, "shape": shape})
         h, heads, grid = 2 * h, 2 * heads, grid // 2

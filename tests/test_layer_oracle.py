@@ -76,9 +76,11 @@ def _swin_attn_mask(g, ws, sh):
     return mw[:, None, :] != mw[:, :, None]  # [nW, win, win] True = masked
 
 
-def _torch_mha(q2, k2, v2, n, s, H, d, am, ka, causal, mask=None):
+def _torch_mha(q2, k2, v2, n, s, H, d, am, ka, causal, mask=None, bias=None):
     q, k, v = (t.reshape(n, s, H, d).transpose(1, 2) for t in (q2, k2, v2))
     sc = q @ k.transpose(-1, -2) / math.sqrt(d)
+    if bias is not None:
+        sc = sc + bias[None]
     if causal:
         sc = sc.masked_fill(torch.ones(s, s, dtype=torch.bool).triu(1), -math.inf)
     if mask is not None:
@@ -99,13 +101,20 @@ def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0, memory=None, n_
     am = torch.from_numpy(lo._attn_mask(drop, 3 * layer_id, n, H, s, sample_offset * nw)).double()
     ka = lo.dropout_scale(drop.p_attn)
     mask = None
+    bias = None
+    if shape.rpb:  # Swin's relative_position_index, built the Swin way (coords meshgrid)
+        w = math.isqrt(s)
+        coords = torch.stack(torch.meshgrid(torch.arange(w), torch.arange(w), indexing="ij")).flatten(1)
+        rel = (coords[:, :, None] - coords[:, None, :]).permute(1, 2, 0) + (w - 1)
+        rpi = rel[:, :, 0] * (2 * w - 1) + rel[:, :, 1]
+        bias = P["rpb"][:, rpi]  # [H, s, s]
     if shape.shift:
         g, ws, sh = math.isqrt(S), math.isqrt(s), shape.shift
         a = _raster_to_wm(torch.roll(_wm_to_raster(a, g, ws), (-sh, -sh), (1, 2)), ws)
         qkv = a @ P["w_qkv"].T + P["b_qkv"]
         mask = _swin_attn_mask(g, ws, sh).repeat(n // nw, 1, 1)
     ctx = _torch_mha(qkv[:, :h], qkv[:, h:2 * h], qkv[:, 2 * h:], n, s, H, d, am, ka, shape.causal,
-                     mask)
+                     mask, bias)
     if shape.shift:
         ctx = _raster_to_wm(torch.roll(_wm_to_raster(ctx, g, ws), (sh, sh), (1, 2)), ws)
     kh = lo.dropout_scale(drop.p_hidden)
@@ -125,13 +134,15 @@ def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0, memory=None, n_
     return x1 + (g @ P["w_2"].T + P["b_2"]) * m2 * kh
 
 
-@pytest.mark.parametrize("p,window,seq,merge,shift", [
-    (0.0, 0, 12, False, 0), (0.1, 0, 12, False, 0), (0.1, 4, 12, False, 0), (0.1, 4, 16, True, 0),
-    (0.0, 9, 36, True, 0), (0.1, 9, 36, False, 1), (0.0, 16, 64, False, 2), (0.1, 4, 16, True, 1)])
-def test_oracle_matches_autograd(p, window, seq, merge, shift):
+@pytest.mark.parametrize("p,window,seq,merge,shift,rpb", [
+    (0.0, 0, 12, False, 0, False), (0.1, 0, 12, False, 0, False), (0.1, 4, 12, False, 0, False),
+    (0.1, 4, 16, True, 0, False), (0.0, 9, 36, True, 0, False), (0.1, 9, 36, False, 1, False),
+    (0.0, 16, 64, False, 2, False), (0.1, 4, 16, True, 1, False), (0.1, 9, 36, False, 1, True),
+    (0.0, 4, 16, True, 0, True)])
+def test_oracle_matches_autograd(p, window, seq, merge, shift, rpb):
     rng = np.random.default_rng(0)
     shape = lo.LayerShape(hidden=64, heads=4, seq=seq, ffn=128, window=window, merge=merge,
-                          shift=shift)
+                          shift=shift, rpb=rpb)
     P = lo.init_layer_params(shape, rng, std=0.1)
     x = rng.standard_normal((2 * shape.seq * (4 if merge else 1), shape.hidden // (2 if merge else 1)))
     dy = rng.standard_normal((2 * shape.seq, shape.hidden))
