@@ -256,8 +256,9 @@ typedef struct gx_attention_args {
   int win_grid, win_side, win_shift;
   /* Swin relative-position bias (mma.sync path, seq = rpb_side^2 window tokens): scores get
    * rpb[head][(dy + side - 1) * (2 side - 1) + dx + side - 1] (bf16 [heads][(2 side - 1)^2],
-   * this call's heads); bwd writes dL/dscore per (batch*head, q, k) to rpb_dpart (fp32
-   * [batch*heads][seq][seq]) for gx::rpb_grad to reduce.  rpb NULL = no bias. */
+   * this call's heads); bwd writes each (window, head)'s table gradient to rpb_dpart (fp32
+   * [batch*heads][(2 side - 1)^2], seq <= 64) for gx_k_rpb_grad to sum over the batch in
+   * order.  rpb NULL = no bias. */
   const void* rpb;
   void* rpb_dpart;
   int rpb_side;
@@ -309,8 +310,8 @@ GX_API int gx_k_patch_merge(const void* src, void* dst, int samples, int grid_ou
                             int window_side, int channels, int backward, void* stream);
 /* Swin cyclic shift between window-major layouts of a grid x grid token grid: inverse = 0
  * rolls by -shift in both axes (torch.roll(x, (-shift, -shift))), inverse = 1 rolls back. */
-/* Swin relative-position-bias gradient: grad[h][e] (+)= sum over b and over the (q, k) pairs
- * of relative offset e of dpart[b*heads + h][q][k] (fixed order: deterministic). */
+/* Swin relative-position-bias gradient: grad[h][e] (+)= sum over b of dpart[b*heads + h][e]
+ * (fixed order: deterministic). */
 GX_API int gx_k_rpb_grad(const void* dpart, int batch, int heads, int side, void* grad,
                          int accumulate, void* stream);
 GX_API int gx_k_window_roll(const void* src, void* dst, int samples, int grid, int window_side,

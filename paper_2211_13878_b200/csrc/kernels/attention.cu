@@ -93,12 +93,27 @@ __device__ __forceinline__ int swin_region(const gx_attention_args& p, int b, in
   return (y < l0 ? 0 : (y < l1 ? 1 : 2)) * 3 + (x < l0 ? 0 : (x < l1 ? 1 : 2));
 }
 
-// Relative-position bias of (q, k) inside a side x side window (log2 units, head h).
-__device__ __forceinline__ float rpb_bias(const gx_attention_args& p, int h, int q, int k) {
+// Relative-position bias staged in shared memory per CTA (one head): the head's table in log2
+// units and each window token's (y, x), so a score's bias is two byte loads and one table load.
+constexpr int kRpbMaxTab = 15 * 15;  // (2 * 8 - 1)^2: windows of up to 8 x 8 tokens
+struct RpbSmem {
+  float tab[kRpbMaxTab];
+  int8_t y[64], x[64];
+};
+__device__ __forceinline__ void rpb_stage(const gx_attention_args& p, int h, RpbSmem* r) {
   const int w = p.rpb_side, n = 2 * w - 1;
-  const int e = (q / w - k / w + w - 1) * n + (q % w - k % w + w - 1);
-  return __bfloat162float(static_cast<const __nv_bfloat16*>(p.rpb)[h * n * n + e]) *
-         1.4426950408889634f;
+  const auto* t = static_cast<const __nv_bfloat16*>(p.rpb) + h * n * n;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x)
+    r->tab[e] = __bfloat162float(t[e]) * 1.4426950408889634f;
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+    r->y[i] = static_cast<int8_t>(i / w);
+    r->x[i] = static_cast<int8_t>(i % w);
+  }
+}
+__device__ __forceinline__ float rpb_bias(const gx_attention_args& p, const RpbSmem* r, int q,
+                                          int k) {
+  const int w = p.rpb_side;
+  return r->tab[(r->y[q] - r->y[k] + w - 1) * (2 * w - 1) + (r->x[q] - r->x[k] + w - 1)];
 }
 
 }  // namespace
@@ -113,12 +128,14 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_a
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
   __nv_bfloat16* sK = sQ + kBlk * LDS;        // [2][64][LDS]
   __nv_bfloat16* sV = sK + 2 * kBlk * LDS;    // [2][64][LDS]
+  RpbSmem* sRp = reinterpret_cast<RpbSmem*>(sV + 2 * kBlk * LDS);  // (kMask, rpb)
 
   const int s = p.seq;
   const int H = p.heads;
   const int bh = blockIdx.y;
   const int b = bh / H, h = bh % H;
   const int q0 = blockIdx.x * kBlk;
+  if (kMask && p.rpb != nullptr) rpb_stage(p, h, sRp);  // visible after the first tile barrier
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
 
@@ -188,7 +205,7 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_a
         const int key = kb * kBlk + nb * 8 + 2 * t + (j & 1);
         float v = sacc[nb][j] * c2;
         const int qrow = q0 + warp * 16 + g + 8 * (j >> 1);
-        if (kMask && p.rpb != nullptr && key < s && qrow < s) v += rpb_bias(p, h, qrow, key);
+        if (kMask && p.rpb != nullptr && key < s && qrow < s) v += rpb_bias(p, sRp, qrow, key);
         if (key >= s || (kMask && ((p.causal && key > qrow) ||
                                    (p.win_shift > 0 && key < s && qrow < s &&
                                     swin_region(p, b, qrow) != swin_region(p, b, key)))))
@@ -321,6 +338,8 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
   float* sL = reinterpret_cast<float*>(sdS + kBlk * LDP);             // lse [64]
   float* sD = sL + kBlk;                                              // D   [64]
   uint16_t* sM = reinterpret_cast<uint16_t*>(sD + kBlk);              // keep bits [64][4]
+  float* sRB = reinterpret_cast<float*>(sM + kBlk * 4);  // rel-pos bias: dS tile [64][64] (kMask)
+  RpbSmem* sRp = reinterpret_cast<RpbSmem*>(sRB + kBlk * kBlk);
 
   const int s = p.seq, H = p.heads;
   const int bh = blockIdx.y;
@@ -328,6 +347,7 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
   const int k0 = blockIdx.x * kBlk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
+  if (kMask && p.rpb != nullptr) rpb_stage(p, h, sRp);  // visible after the first tile barrier
 
   const auto* qkv = static_cast<const __nv_bfloat16*>(p.qkv);
   const int64_t ld = p.ld_qkv;
@@ -420,7 +440,7 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
                                          (p.win_shift > 0 &&
                                           swin_region(p, b, q) != swin_region(p, b, key))));
         float P = keep_pk ? exp2f(st[nb][j] * c2 +
-                                  (kMask && p.rpb != nullptr ? rpb_bias(p, h, q, key) : 0.f) -
+                                  (kMask && p.rpb != nullptr ? rpb_bias(p, sRp, q, key) : 0.f) -
                                   sL[ql])
                           : 0.f;
         float keep = 1.f;
@@ -432,8 +452,7 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
         pd[nb][j] = P * keep;
         st[nb][j] = P * (dpt[nb][j] * keep - sD[ql]);  // dS^T
         if (kMask && p.rpb_dpart != nullptr && q < s && key < s)  // dL/d(bias) per (q, k)
-          static_cast<float*>(p.rpb_dpart)[(static_cast<int64_t>(bh) * s + q) * s + key] =
-              st[nb][j];
+          sRB[q * kBlk + key] = st[nb][j];  // (s <= 64: one query and one key block)
       }
     }
     // dV += Pd^T dO ; dK += dS^T Q   (k-dim = queries)
@@ -502,6 +521,20 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
     }
     __syncthreads();
   }
+  if (kMask && p.rpb_dpart != nullptr) {
+    // this (window, head)'s bias-table gradient: entry e sums the dS of every (q, k) at relative
+    // offset e, in a fixed order; the batch sum follows in rpb_grad
+    const int w = p.rpb_side, n = 2 * w - 1;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int dy = e / n - (w - 1), dx = e % n - (w - 1);
+      float acc = 0.f;
+      for (int q = 0; q < s; ++q) {
+        const int yk = q / w - dy, xk = q % w - dx;
+        if (yk >= 0 && yk < w && xk >= 0 && xk < w) acc += sRB[q * kBlk + yk * w + xk];
+      }
+      static_cast<float*>(p.rpb_dpart)[static_cast<int64_t>(bh) * n * n + e] = acc;
+    }
+  }
   // write dK, dV (scaled) into dqkv
   auto* dqkv = static_cast<__nv_bfloat16*>(p.dqkv);
 #pragma unroll
@@ -546,15 +579,18 @@ template <int HD>
 static int attention_fwd_impl(const gx_attention_args& a, cudaStream_t st) {
   constexpr int LDS = HD + 8;
   const int smem = 5 * kBlk * LDS * 2;
+  const int smem_m = smem + static_cast<int>(sizeof(RpbSmem));
+  if (a.rpb != nullptr && (a.rpb_side < 1 || a.rpb_side > 8 || a.seq != a.rpb_side * a.rpb_side))
+    return set_error(kErrConfig, "attention: relative-position bias needs square windows of <= 8x8");
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(attn_fwd_kernel<HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attn_fwd_kernel<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_fwd_kernel<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_m);
     set = true;
   }
   dim3 grid((a.seq + kBlk - 1) / kBlk, a.batch * a.heads);
   if (a.causal || a.win_shift > 0 || a.rpb != nullptr)
-    launch_k(attn_fwd_kernel<HD, true>, grid, dim3(kThreads), smem, st, a);
+    launch_k(attn_fwd_kernel<HD, true>, grid, dim3(kThreads), smem_m, st, a);
   else
     launch_k(attn_fwd_kernel<HD, false>, grid, dim3(kThreads), smem, st, a);
   return check_launch("attn_fwd_kernel");
@@ -564,10 +600,14 @@ template <int HD>
 static int attention_bwd_impl(const gx_attention_args& a, cudaStream_t st) {
   constexpr int LDS = HD + 8;
   const int smem = 4 * kBlk * LDS * 2 + kBlk * (kBlk + 8) * 2 + 2 * kBlk * 4 + kBlk * 4 * 2;
+  // + the relative-position-bias dS tile and staged table
+  const int smem_m = smem + kBlk * kBlk * 4 + static_cast<int>(sizeof(RpbSmem));
+  if (a.rpb_dpart != nullptr && a.seq > kBlk)
+    return set_error(kErrConfig, "attention: relative-position bias needs windows of <= 64 tokens");
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(attn_bwd_kernel<HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    cudaFuncSetAttribute(attn_bwd_kernel<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(attn_bwd_kernel<HD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_m);
     set = true;
   }
   const int rows = a.batch * a.heads * a.seq;
@@ -575,7 +615,7 @@ static int attention_bwd_impl(const gx_attention_args& a, cudaStream_t st) {
   if (int rc = check_launch("attn_bwd_prep_kernel")) return rc;
   dim3 grid((a.seq + kBlk - 1) / kBlk, a.batch * a.heads);
   if (a.causal || a.win_shift > 0 || a.rpb != nullptr)
-    launch_k(attn_bwd_kernel<HD, true>, grid, dim3(kThreads), smem, st, a);
+    launch_k(attn_bwd_kernel<HD, true>, grid, dim3(kThreads), smem_m, st, a);
   else
     launch_k(attn_bwd_kernel<HD, false>, grid, dim3(kThreads), smem, st, a);
   if (int rc = check_launch("attn_bwd_kernel")) return rc;
@@ -588,35 +628,30 @@ static int attention_bwd_impl(const gx_attention_args& a, cudaStream_t st) {
 
 // grad[h][e] (+)= sum_b sum_{(q,k): offset e} dpart[b*heads + h][q][k]: one block per (h, e),
 // threads stride over b, fixed-order tree reduction (deterministic).
-__global__ void rpb_grad_kernel(const float* __restrict__ dpart, int batch, int heads, int side,
+// grad[h][e] (+)= sum_b dpart[b*heads + h][e]: one block per (h, e); threads stride over b
+// and a shared-memory tree adds their sums in a fixed order (deterministic).
+__global__ void rpb_grad_kernel(const float* __restrict__ dpart, int batch, int heads, int ne,
                                 float* __restrict__ grad, bool accumulate) {
   pdl_enter();
-  const int n = 2 * side - 1, ne = n * n, s = side * side;
-  const int h = blockIdx.x / ne, e = blockIdx.x % ne;
-  const int dy = e / n - (side - 1), dx = e % n - (side - 1);
+  const int i = blockIdx.x;  // h * ne + e
   float acc = 0.f;
-  for (int b = threadIdx.x; b < batch; b += blockDim.x) {
-    const float* src = dpart + (static_cast<int64_t>(b) * heads + h) * s * s;
-    for (int q = 0; q < s; ++q) {
-      const int yk = q / side - dy, xk = q % side - dx;
-      if (yk >= 0 && yk < side && xk >= 0 && xk < side) acc += src[q * s + yk * side + xk];
-    }
-  }
-  __shared__ float red[256];
+  for (int b = threadIdx.x; b < batch; b += blockDim.x)
+    acc += dpart[static_cast<int64_t>(b) * heads * ne + i];
+  __shared__ float red[128];
   red[threadIdx.x] = acc;
   __syncthreads();
   for (int w = blockDim.x / 2; w > 0; w >>= 1) {
     if (static_cast<int>(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
     __syncthreads();
   }
-  if (threadIdx.x == 0) grad[h * ne + e] = (accumulate ? grad[h * ne + e] : 0.f) + red[0];
+  if (threadIdx.x == 0) grad[i] = (accumulate ? grad[i] : 0.f) + red[0];
 }
 
 int rpb_grad(const float* dpart, int batch, int heads, int side, float* grad, bool accumulate,
              cudaStream_t st) {
   if (batch <= 0) return kOk;
   const int n = 2 * side - 1;
-  launch_k(rpb_grad_kernel, dim3(heads * n * n), dim3(256), 0, st, dpart, batch, heads, side,
+  launch_k(rpb_grad_kernel, dim3(heads * n * n), dim3(128), 0, st, dpart, batch, heads, n * n,
            grad, accumulate);
   return check_launch("rpb_grad_kernel");
 }

@@ -1043,8 +1043,8 @@ int ExecutorImpl::allocate(RankCtx& r) {
         max_x = std::max(max_x, rows * h);
       }
       if (s.rpb)
-        max_rpb = std::max<int64_t>(max_rpb, static_cast<int64_t>(a.samples) * (s.heads / t) *
-                                                 s.seq * s.win);
+        max_rpb = std::max<int64_t>(max_rpb, static_cast<int64_t>(a.samples) * s.windows() *
+                                                 (s.heads / t) * s.rpb_n());
       if (s.shift > 0) {
         a.ln1r = A.a<bf16>(rows * h);
         a.ctxr = A.a<bf16>(rows * ht);
@@ -1785,7 +1785,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       GX_TRY(timed(kAttnBwd, af, 2.0 * rows * 8 * ht, [&] { return attention_bwd(at, stream_); }));
     }
     if (s.rpb)  // table gradient: fixed-order sum of the per-window score gradients
-      GX_TRY(timed(kElementwise, 0, 4.0 * A.samples * (s.heads / t) * double(s.seq) * s.win, [&] {
+      GX_TRY(timed(kElementwise, 0, 4.0 * A.samples * s.windows() * (s.heads / t) * s.rpb_n(), [&] {
         return rpb_grad(r.rpb_part, A.samples * s.windows(), s.heads / t, side_of(s),
                         G + L.lay.rpb.off, true, stream_);
       }));

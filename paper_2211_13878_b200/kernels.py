@@ -267,8 +267,8 @@ def window_roll(x, samples, grid, window_side, shift, inverse=False):
 
 
 def rpb_grad(dpart, batch, heads, side, grad, accumulate=True):
-    """Relative-position-bias gradient: fixed-order sum of the per-(window, head) score
-    gradients into grad (fp32 [heads][(2 side - 1)^2])."""
+    """Relative-position-bias gradient: fixed-order batch sum of the per-(window, head) table
+    gradients (attention_bwd's rpb_dpart) into grad (fp32 [heads][(2 side - 1)^2])."""
     _lib.check(_lib.lib().gx_k_rpb_grad(_ptr(dpart), batch, heads, side, _ptr(grad),
                                         int(accumulate), _lib.stream_ptr()))
     return grad
