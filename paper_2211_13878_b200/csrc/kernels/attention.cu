@@ -98,17 +98,24 @@ __device__ __forceinline__ int swin_region(const gx_attention_args& p, int b, in
 constexpr int kRpbMaxTab = 15 * 15;  // (2 * 8 - 1)^2: windows of up to 8 x 8 tokens
 struct RpbSmem {
   float tab[kRpbMaxTab];
-  int8_t y[64], x[64];
+  int8_t y[64], x[64];  // token -> (row, column) inside its window (rel-pos bias)
+  int8_t reg[64];       // token -> shifted-window region of this CTA's window (SW-MSA mask)
 };
-__device__ __forceinline__ void rpb_stage(const gx_attention_args& p, int h, RpbSmem* r) {
-  const int w = p.rpb_side, n = 2 * w - 1;
-  const auto* t = static_cast<const __nv_bfloat16*>(p.rpb) + h * n * n;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x)
-    r->tab[e] = __bfloat162float(t[e]) * 1.4426950408889634f;
-  for (int i = threadIdx.x; i < 64; i += blockDim.x) {
-    r->y[i] = static_cast<int8_t>(i / w);
-    r->x[i] = static_cast<int8_t>(i % w);
+// Per-CTA staging of the window masks / bias: attention sequence b (one window), head h.
+__device__ __forceinline__ void win_stage(const gx_attention_args& p, int b, int h, RpbSmem* r) {
+  if (p.rpb != nullptr) {
+    const int w = p.rpb_side, n = 2 * w - 1;
+    const auto* t = static_cast<const __nv_bfloat16*>(p.rpb) + h * n * n;
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x)
+      r->tab[e] = __bfloat162float(t[e]) * 1.4426950408889634f;
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
+      r->y[i] = static_cast<int8_t>(i / w);
+      r->x[i] = static_cast<int8_t>(i % w);
+    }
   }
+  if (p.win_shift > 0)
+    for (int i = threadIdx.x; i < 64; i += blockDim.x)
+      r->reg[i] = static_cast<int8_t>(i < p.seq ? swin_region(p, b, i) : 0);
 }
 __device__ __forceinline__ float rpb_bias(const gx_attention_args& p, const RpbSmem* r, int q,
                                           int k) {
@@ -128,14 +135,14 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_a
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_raw);
   __nv_bfloat16* sK = sQ + kBlk * LDS;        // [2][64][LDS]
   __nv_bfloat16* sV = sK + 2 * kBlk * LDS;    // [2][64][LDS]
-  RpbSmem* sRp = reinterpret_cast<RpbSmem*>(sV + 2 * kBlk * LDS);  // (kMask, rpb)
+  RpbSmem* sRp = reinterpret_cast<RpbSmem*>(sV + 2 * kBlk * LDS);  // (kMask: shift / rpb)
 
   const int s = p.seq;
   const int H = p.heads;
   const int bh = blockIdx.y;
   const int b = bh / H, h = bh % H;
   const int q0 = blockIdx.x * kBlk;
-  if (kMask && p.rpb != nullptr) rpb_stage(p, h, sRp);  // visible after the first tile barrier
+  if (kMask) win_stage(p, b, h, sRp);  // visible after the first tile barrier
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
 
@@ -208,7 +215,7 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(const gx_attention_a
         if (kMask && p.rpb != nullptr && key < s && qrow < s) v += rpb_bias(p, sRp, qrow, key);
         if (key >= s || (kMask && ((p.causal && key > qrow) ||
                                    (p.win_shift > 0 && key < s && qrow < s &&
-                                    swin_region(p, b, qrow) != swin_region(p, b, key)))))
+                                    sRp->reg[qrow] != sRp->reg[key]))))
           v = -INFINITY;
         sacc[nb][j] = v;
         mx[j >> 1] = fmaxf(mx[j >> 1], v);
@@ -347,7 +354,7 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
   const int k0 = blockIdx.x * kBlk;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  if (kMask && p.rpb != nullptr) rpb_stage(p, h, sRp);  // visible after the first tile barrier
+  if (kMask) win_stage(p, b, h, sRp);  // visible after the first tile barrier
 
   const auto* qkv = static_cast<const __nv_bfloat16*>(p.qkv);
   const int64_t ld = p.ld_qkv;
@@ -438,7 +445,7 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
         const bool keep_pk = q < s && key < s &&
                              !(kMask && ((p.causal && key > q) ||
                                          (p.win_shift > 0 &&
-                                          swin_region(p, b, q) != swin_region(p, b, key))));
+                                          sRp->reg[q] != sRp->reg[key])));
         float P = keep_pk ? exp2f(st[nb][j] * c2 +
                                   (kMask && p.rpb != nullptr ? rpb_bias(p, sRp, q, key) : 0.f) -
                                   sL[ql])
@@ -529,7 +536,7 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_kernel(const gx_attention_a
       const int dy = e / n - (w - 1), dx = e % n - (w - 1);
       float acc = 0.f;
       for (int q = 0; q < s; ++q) {
-        const int yk = q / w - dy, xk = q % w - dx;
+        const int yk = sRp->y[q] - dy, xk = sRp->x[q] - dx;
         if (yk >= 0 && yk < w && xk >= 0 && xk < w) acc += sRB[q * kBlk + yk * w + xk];
       }
       static_cast<float*>(p.rpb_dpart)[static_cast<int64_t>(bh) * n * n + e] = acc;
@@ -582,6 +589,8 @@ static int attention_fwd_impl(const gx_attention_args& a, cudaStream_t st) {
   const int smem_m = smem + static_cast<int>(sizeof(RpbSmem));
   if (a.rpb != nullptr && (a.rpb_side < 1 || a.rpb_side > 8 || a.seq != a.rpb_side * a.rpb_side))
     return set_error(kErrConfig, "attention: relative-position bias needs square windows of <= 8x8");
+  if (a.win_shift > 0 && a.seq > kBlk)
+    return set_error(kErrConfig, "attention: shifted windows of <= 64 tokens");
   static bool set = false;
   if (!set) {
     cudaFuncSetAttribute(attn_fwd_kernel<HD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
