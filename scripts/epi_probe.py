@@ -1,18 +1,19 @@
-"""Per-chunk epilogue cost probe: one tile, K=64, N = 32..256 valid columns."""
-import json, sys
+"""Out-projection GEMM epilogue cost by stage (bias, residual, Philox dropout) at M = 512..8192."""
+import json, os, sys
+sys.path.insert(0, "/root/repo")
 import torch
-sys.path.insert(0, ".")
-from paper_2211_13878_b200 import kernels
-from scripts.bench_gemm import timeit
-dev = torch.device("cuda:0")
-for tn, M in ((-256, 256), (256, 128)):
-    row = []
-    for N in (32, 64, 128, 256):
-        A = torch.randn(M, 64, device=dev).bfloat16()
-        B = torch.randn(N, 64, device=dev).bfloat16()
-        out = torch.empty(M, N, device=dev, dtype=torch.bfloat16)
-        row.append(round(timeit(lambda: kernels.gemm(A, B, out=out, tile_n=tn)) * 1e3, 2))
-    print(json.dumps({"tile": tn, "M": M, "us_for_N_32_64_128_256": row}))
-# empty-ish kernels for reference: torch fill of small tensor
-x = torch.empty(16, device=dev)
-print(json.dumps({"torch_fill_us": round(timeit(lambda: x.fill_(1.0)) * 1e3, 2)}))
+from paper_2211_13878_b200 import kernels as K
+from scripts.tile_sweep import timeit
+dev, bf = torch.device("cuda:0"), torch.bfloat16
+h = 1280
+for M in (512, 2048, 8192):
+    r = lambda *s: torch.randn(*s, device=dev).to(bf)
+    ctx, wo, x, oh = r(M, h), r(h, h), r(M, h), r(M, h)
+    bh = torch.zeros(h, device=dev).to(bf)
+    cur = torch.cuda.current_stream
+    res = {}
+    res["plain"] = timeit(lambda: K.gemm(ctx, wo, out=oh, stream=cur()))
+    res["bias"] = timeit(lambda: K.gemm(ctx, wo, out=oh, bias=bh, stream=cur()))
+    res["bias+res"] = timeit(lambda: K.gemm(ctx, wo, out=oh, bias=bh, residual=x, stream=cur()))
+    res["bias+res+drop"] = timeit(lambda: K.gemm(ctx, wo, out=oh, bias=bh, residual=x, dropout_p=0.1, seed=1, site=1, stream=cur()))
+    print(json.dumps({"M": M, **{k: round(v, 2) for k, v in res.items()}}), flush=True)
