@@ -366,3 +366,27 @@ def test_swin_shifted_windows(cuda, strategies, world, p_drop):
     m = _swin_like(h0=64, heads0=2, grid0=28, stages=(2,))
     assert m["layers"][1]["shape"]["shift"]
     _check(_run_case(gxe.make_plan(strategies, 2), m, world, p_drop))
+
+
+@pytest.mark.parametrize("family", ["t5", "swin"])
+def test_instrumented_run_other_families(cuda, family):
+    """The per-launch instrumented replay (gx_exec_run flags=2, the profiler's raw data) covers
+    the decoder and window layers: every category timed, and the step's numbers unchanged."""
+    import torch
+    model = _t5_like() if family == "t5" else _swin_like()
+    plan = gxe.make_plan(["dp:2", "dp:2", "sdp:2", "sdp:2"], 4)
+    # no dropout (each step draws fresh masks) and no optimizer: two steps compute the same loss
+    ex = gxe.PlanExecutor(plan, model, 2, optimizer=False)
+    ex.init_params(seed=3, std=0.02)
+    f, z = model["layers"][0]["shape"], model["layers"][-1]["shape"]
+    x = torch.randn(4 * f["seq"], f["hidden"]).to(torch.bfloat16).view(torch.int16).numpy()
+    t = torch.randn(4 * z["seq"], z["hidden"]).to(torch.bfloat16).view(torch.int16).numpy()
+    ex.load_batch(x, t)
+    ex.run(use_graph=False)
+    plain = ex.loss()
+    ex.run(use_graph=False, profile=True)
+    rep = ex.profile_report()
+    assert ex.loss() == plain
+    cats = rep["categories"] if "categories" in rep else rep
+    assert any("gemm" in str(k) for k in cats)
+    ex.close()
