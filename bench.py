@@ -152,14 +152,27 @@ def run_reference(args, rank):
         from oracle import ref_planner
         from paper_2211_13878_b200 import models
         if ref_planner.available():
+            from paper_2211_13878_b200 import planner as gx_planner
             m = models.model(args.model)
             c = models.cluster(args.gpus, args.budget_gib, 13.0)
-            t0 = time.perf_counter()
             o = ref_planner.api().optimize(m, c)
+            batches = None
             if o.plan is None:
-                o = ref_planner.api().optimize(m, c, None, list(range(1, 513)))
-            extra["reference_planner_optimize_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+                batches = list(range(1, 513))
+                o = ref_planner.api().optimize(m, c, None, batches)
             extra["reference_plan_predicted_samples_per_s"] = o.plan["throughput_samples_per_s"] if o.plan else None
+
+            def med7(api, threads):  # median of 7, PLANNER_THREADS = 1 and = nproc
+                ts = []
+                for _ in range(7):
+                    t0 = time.perf_counter()
+                    api.optimize(m, c, None, batches, num_threads=threads)
+                    ts.append((time.perf_counter() - t0) * 1e3)
+                return round(statistics.median(ts), 3)
+            extra["reference_planner_optimize_ms"] = {"threads_1": med7(ref_planner.api(), 1),
+                                                      f"threads_{cores}": med7(ref_planner.api(), cores)}
+            extra["gx_planner_optimize_ms"] = {"threads_1": med7(gx_planner.api(), 1),
+                                               f"threads_{cores}": med7(gx_planner.api(), cores)}
     except Exception as e:  # the planner timing is informational only
         extra["reference_planner_error"] = str(e)[:200]
     sample = (f"1 {args.model} layer fwd+bwd at 1 sample (numpy fp32, dropout {args.dropout}) per step, "
