@@ -41,7 +41,6 @@ extern "C" {
 #define GX_OUT_F32 1
 #define GX_OUT_F32_ACC 2
 #define GX_OUT_F32_SPLIT 3  /* split-K: out is [splits][M][ldo] fp32, split s stores slice s */
-#define GX_OUT_ADAMW 4      /* acc = final fp32 weight gradient, consumed by AdamW in place */
 
 /* ------------------------------------------------------------------ library */
 GX_API const char* gx_last_error(void);
@@ -156,10 +155,6 @@ GX_API int gx_exec_profile_report(gx_exec* ex, char* out, size_t cap, size_t* ne
  * canonical index, never on the sharding): LN gains 1, biases 0, weights N(0, std^2). */
 GX_API int gx_exec_init_params(gx_exec* ex, uint64_t seed, float std_dev);
 GX_API int gx_exec_loss(gx_exec* ex, float* out);
-/* Apply the AdamW update still pending from the last step.  By default the optimizer of step
- * t runs at the start of step t+1, overlapped with its forward (config "defer_optimizer");
- * gx_exec_export_layer(params) flushes implicitly. */
-GX_API int gx_exec_flush(gx_exec* ex);
 /* load_batch + run + loss: the end-to-end call (host buffers in, loss out). */
 GX_API int gx_exec_step(gx_exec* ex, const void* x_host, const void* target_host, int use_graph,
                         float* loss_out);
@@ -197,15 +192,6 @@ typedef struct gx_gemm_epilogue {
   uint64_t site;
   int gelu_bwd;               /* out = acc * gelu'(aux) (aux = bf16 pre-activation, read); 2: out = acc * aux */
   const uint64_t* seed_offset;/* optional device counter added to seed (per-step masks) */
-  /* GX_OUT_ADAMW: the accumulator is the complete gradient of a weight slot; the epilogue
-   * applies AdamW to master/m/v (fp32) and writes the bf16 parameter, all [M][ldo] like
-   * `out` (which is unused): the gradient never reaches HBM. */
-  float* adam_master;
-  float* adam_m;
-  float* adam_v;
-  void* adam_param;
-  float lr, beta1, beta2, eps, weight_decay;
-  const int64_t* step;        /* device step counter (bias corrections) */
   /* debug: when set, CTA b writes %globaltimer stamps [b][0..15] (entry, after PDL wait,
    * first TMA issued, first stage landed, last MMA issued, first accumulator ready, epilogue
    * done, exit; then per epilogue chunk of warp 4: before / after its TMEM load) -- see

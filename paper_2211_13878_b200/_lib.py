@@ -40,9 +40,6 @@ class GemmEpilogue(Structure):
         ("col_offset", c_int64), ("drop_ld", c_int64), ("drop_threshold", c_uint32),
         ("drop_scale", c_float), ("seed", c_uint64), ("site", c_uint64), ("gelu_bwd", c_int),
         ("seed_offset", c_void_p),
-        ("adam_master", c_void_p), ("adam_m", c_void_p), ("adam_v", c_void_p),
-        ("adam_param", c_void_p), ("lr", c_float), ("beta1", c_float), ("beta2", c_float),
-        ("eps", c_float), ("weight_decay", c_float), ("step", c_void_p),
         ("trace", c_void_p),
     ]
 
@@ -97,7 +94,6 @@ def _declare(L: ctypes.CDLL) -> None:
     L.gx_exec_load_batch_device.argtypes = [vp, vp, vp]
     L.gx_exec_run.argtypes = [vp, c_int]
     L.gx_exec_loss.argtypes = [vp, POINTER(c_float)]
-    L.gx_exec_flush.argtypes = [vp]
     L.gx_exec_step.argtypes = [vp, vp, vp, c_int, POINTER(c_float)]
     L.gx_exec_export_output.argtypes = [vp, c_int, vp]
     L.gx_exec_stream.argtypes = [vp, POINTER(c_void_p)]
@@ -106,7 +102,7 @@ def _declare(L: ctypes.CDLL) -> None:
     L.gx_nccl_unique_id.argtypes = [c_char_p, c_size_t]
     for name in ("gx_exec_create", "gx_exec_destroy", "gx_exec_set_layer_params",
                  "gx_exec_export_layer", "gx_exec_load_batch", "gx_exec_load_batch_device",
-                 "gx_exec_run", "gx_exec_loss", "gx_exec_flush", "gx_exec_step", "gx_exec_export_output",
+                 "gx_exec_run", "gx_exec_loss", "gx_exec_step", "gx_exec_export_output",
                  "gx_exec_stream", "gx_exec_info", "gx_exec_canonical_size",
                  "gx_nccl_unique_id"):
         getattr(L, name).restype = c_int

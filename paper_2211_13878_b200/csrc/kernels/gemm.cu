@@ -24,7 +24,6 @@
 
 #include "gx_internal.h"
 #include "launch.cuh"
-#include "adam.cuh"
 #include "philox.cuh"
 #include "sm100.cuh"
 
@@ -258,7 +257,6 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // Per-warp epilogue state: staging buffers, operand-prefetch barriers and their use count.
 struct EpiWarp {
   uint32_t out_buf, aux_buf, bias_buf;
-  AdamScalars adam;  // GX_OUT_ADAMW only
   uint32_t bar0;  // operand-prefetch barriers bar0, bar0 + 8
   uint32_t blk;   // operand blocks consumed so far (buffer = blk & 1, phase = (blk >> 1) & 1)
   uint32_t sblk;  // output blocks stored so far (staging buffer = sblk & 1)
@@ -306,62 +304,7 @@ __device__ __forceinline__ void epi_stage_bias(const GemmEpilogue& ep, const Epi
   __syncwarp();
 }
 
-// GX_OUT_ADAMW: the lane's 32 gradient values (row `row`, columns [n0, n0+32)) update the
-// weight slot in place -- master / m / v fp32 read and written, bf16 parameter written.
-__device__ __forceinline__ void epilogue_adamw(const GemmEpilogue& ep, const AdamScalars& c,
-                                               int64_t row, int M, int n0, int N,
-                                               const uint32_t (&acc)[32]) {
-  if (row >= M) return;
-  const int64_t base = row * ep.ldo + n0;
-  float* pm = ep.adam_master + base;
-  float* mm = ep.adam_m + base;
-  float* vm = ep.adam_v + base;
-  uint32_t* pb = reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(ep.adam_param) + base);
-  if (n0 + 32 <= N) {
-#pragma unroll
-    for (int hh = 0; hh < 4; ++hh) {  // 8 columns: six 16-byte loads in flight
-      float4 P[2], Mv[2], V[2];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        P[q] = reinterpret_cast<const float4*>(pm + 8 * hh)[q];
-        Mv[q] = reinterpret_cast<const float4*>(mm + 8 * hh)[q];
-        V[q] = reinterpret_cast<const float4*>(vm + 8 * hh)[q];
-      }
-      uint32_t bw[4];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int j = 8 * hh + 4 * q;
-        const float4 g = make_float4(__uint_as_float(acc[j]) * ep.alpha,
-                                     __uint_as_float(acc[j + 1]) * ep.alpha,
-                                     __uint_as_float(acc[j + 2]) * ep.alpha,
-                                     __uint_as_float(acc[j + 3]) * ep.alpha);
-        adam4(c, P[q], g, Mv[q], V[q]);
-        reinterpret_cast<float4*>(pm + 8 * hh)[q] = P[q];
-        reinterpret_cast<float4*>(mm + 8 * hh)[q] = Mv[q];
-        reinterpret_cast<float4*>(vm + 8 * hh)[q] = V[q];
-        bw[2 * q] = pack_bf16(P[q].x, P[q].y);
-        bw[2 * q + 1] = pack_bf16(P[q].z, P[q].w);
-      }
-      reinterpret_cast<uint4*>(pb + 4 * hh)[0] = make_uint4(bw[0], bw[1], bw[2], bw[3]);
-    }
-  } else {
-    __nv_bfloat16* pbh = reinterpret_cast<__nv_bfloat16*>(pb);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      if (n0 + j >= N) continue;
-      float p = pm[j], m = mm[j], v = vm[j];
-      adam1(c, p, __uint_as_float(acc[j]) * ep.alpha, m, v);
-      pm[j] = p;
-      mm[j] = m;
-      vm[j] = v;
-      pbh[j] = __float2bfloat16_rn(p);
-    }
-  }
-}
-
 // One 32 x 32 output block: math, staging, TMA store.  Executed by a whole epilogue warp.
-// kAdam: the GX_OUT_ADAMW instantiation (kept out of the other kernels' register budget).
-template <bool kAdam>
 __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUtensorMap* map_out,
                                                const CUtensorMap* map_aux, EpiWarp& w,
                                                bool has_in, int cb, int64_t m_base,
@@ -369,10 +312,6 @@ __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUt
                                                const uint32_t (&acc)[32]) {
   const uint32_t lane = lane_id();
   const int64_t row = m_base + lane;
-  if constexpr (kAdam) {
-    epilogue_adamw(ep, w.adam, row, M, n0, N, acc);
-    return;
-  }
   uint32_t bias_w[16], in_w[16];
   if (ep.bias != nullptr) {
 #pragma unroll
@@ -443,7 +382,7 @@ __device__ __forceinline__ void epilogue_chunks(int ew, int* c_lo, int* c_hi) {
   *c_lo = (ew / 4) * NC / kHalves;
   *c_hi = (ew / 4 + 1) * NC / kHalves;
 }
-template <int BN, bool kAdam>
+template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const CUtensorMap* map_out,
                                               const CUtensorMap* map_aux, EpiWarp& w, int ew,
                                               bool has_in, uint32_t taddr, int64_t m_base,
@@ -462,7 +401,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const CUte
     tmem_ld_wait();
     if (stamp) ep.trace[blockIdx.x * 16 + 9 + 2 * (c - c_lo)] = gtimer();
     if (m_base < M && n0 + c * 32 < N) {
-      epilogue_block<kAdam>(ep, map_out, map_aux, w, has_in, c - c_lo, m_base, store_row, n0 + c * 32, M,
+      epilogue_block(ep, map_out, map_aux, w, has_in, c - c_lo, m_base, store_row, n0 + c * 32, M,
                      N, r);
     } else if (has_in) {
       // keep the operand pipeline in step: consume (wait for) the block even if unused
@@ -496,7 +435,7 @@ __device__ __forceinline__ EpiWarp epi_warp_init(uint8_t* staging, int ew) {
   return w;
 }
 
-template <int BN, bool kAMN, bool kBMN, bool kAdam = false>
+template <int BN, bool kAMN, bool kBMN>
 __global__ void __maxnreg__(kGemmMaxRegs)
     gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
@@ -626,8 +565,6 @@ __global__ void __maxnreg__(kGemmMaxRegs)
     // ---------------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     EpiWarp ew = epi_warp_init(staging, warp - 4);
-    if constexpr (kAdam)
-      ew.adam = adam_scalars_step(ep.lr, ep.beta1, ep.beta2, ep.eps, ep.weight_decay, ep.step);
     const bool has_in = ep.gelu_bwd || ep.residual != nullptr;
     int local = 0;
     for (int unit = blockIdx.x; unit < num_units; unit += gridDim.x, ++local) {
@@ -643,7 +580,7 @@ __global__ void __maxnreg__(kGemmMaxRegs)
       // split-K slices: split s stores rows [s*M, (s+1)*M) of the [splits*M][N] output
       const int32_t store_row = static_cast<int32_t>(
           m_base + (ep.out_kind == kOutF32Split ? static_cast<int64_t>(unit / num_tiles) * M : 0));
-      epilogue_tile<BN, kAdam>(ep, &map_out, &map_aux, ew, warp - 4, has_in,
+      epilogue_tile<BN>(ep, &map_out, &map_aux, ew, warp - 4, has_in,
                         tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base,
                         store_row, n0, M, N);
       tc_fence_before();
@@ -679,7 +616,7 @@ struct PairCfg {
   static constexpr int kSmemBytes = kStages * kStageBytes + kStagingBytesDecl + 1024 + 256;
 };
 
-template <int BN, bool kAMN, bool kBMN, bool kAdam = false>
+template <int BN, bool kAMN, bool kBMN>
 __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(kGemmMaxRegs)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                      const __grid_constant__ CUtensorMap map_b,
@@ -825,8 +762,6 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(kGemmMaxRegs)
     const int q = warp & 3;
     const uint32_t leader_tempty0 = mapa_shared(smem_u32(&tempty_bar[0]), 0);
     EpiWarp ew = epi_warp_init(staging, warp - 4);
-    if constexpr (kAdam)
-      ew.adam = adam_scalars_step(ep.lr, ep.beta1, ep.beta2, ep.eps, ep.weight_decay, ep.step);
     const bool has_in = ep.gelu_bwd || ep.residual != nullptr;
     int local = 0;
     for (int unit = pair; unit < num_units; unit += num_pairs, ++local) {
@@ -843,7 +778,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(kGemmMaxRegs)
         ep.trace[blockIdx.x * 16 + 5] = gtimer();
       const int32_t store_row = static_cast<int32_t>(
           m_base + (ep.out_kind == kOutF32Split ? static_cast<int64_t>(unit / num_tiles) * M : 0));
-      epilogue_tile<BN, kAdam>(ep, &map_out, &map_aux, ew, warp - 4, has_in,
+      epilogue_tile<BN>(ep, &map_out, &map_aux, ew, warp - 4, has_in,
                         tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base,
                         store_row, n0, M, N);
       tc_fence_before();
@@ -900,11 +835,6 @@ static bool make_out_map(CUtensorMap* map, const void* ptr, uint64_t cols, uint6
 
 static bool make_epi_maps(const GemmEpilogue& ep, int M, int N, int splits, CUtensorMap* mo,
                           CUtensorMap* mx) {
-  if (ep.out_kind == kOutAdamW) {  // nothing is stored through a map; keep valid descriptors
-    if (!make_out_map(mo, ep.adam_master, N, M, ep.ldo, true)) return false;
-    *mx = *mo;
-    return true;
-  }
   const bool f32 = ep.out_kind != kOutBF16;
   const uint64_t rows = static_cast<uint64_t>(M) * (ep.out_kind == kOutF32Split ? splits : 1);
   if (!make_out_map(mo, ep.out, N, rows, ep.ldo, f32)) return false;
@@ -944,7 +874,7 @@ int num_sms() {
   return n;
 }
 
-template <int BN, bool kAMN, bool kBMN, bool kAdam = false>
+template <int BN, bool kAMN, bool kBMN>
 static int launch_gemm(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
                        const GemmEpilogue& ep, cudaStream_t stream, int splits) {
   using Cfg = GemmCfg<BN>;
@@ -957,18 +887,18 @@ static int launch_gemm(const GemmOperand& a, const GemmOperand& b, int M, int N,
   if (!ok) return set_error(kErrCuda, "gemm: cuTensorMapEncodeTiled failed");
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, kAMN, kBMN, kAdam>,
+    cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, kAMN, kBMN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     attr_set = true;
   }
   const int units = ((M + kBM - 1) / kBM) * ((N + BN - 1) / BN) * splits;
   const int grid = units < num_sms() ? units : num_sms();
-  launch_k(gemm_tcgen05_kernel<BN, kAMN, kBMN, kAdam>, dim3(grid), dim3(kThreads), Cfg::kSmemBytes,
+  launch_k(gemm_tcgen05_kernel<BN, kAMN, kBMN>, dim3(grid), dim3(kThreads), Cfg::kSmemBytes,
            stream, ma, mb, mo, mx, M, N, K, splits, ep);
   return check_launch("gemm_tcgen05_kernel");
 }
 
-template <int BN, bool kAMN, bool kBMN, bool kAdam = false>
+template <int BN, bool kAMN, bool kBMN>
 static int launch_gemm_pair(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
                             const GemmEpilogue& ep, cudaStream_t stream, int splits) {
   using Cfg = PairCfg<BN>;
@@ -982,13 +912,13 @@ static int launch_gemm_pair(const GemmOperand& a, const GemmOperand& b, int M, i
   if (!ok) return set_error(kErrCuda, "gemm: cuTensorMapEncodeTiled failed");
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_pair_kernel<BN, kAMN, kBMN, kAdam>,
+    cudaFuncSetAttribute(gemm_pair_kernel<BN, kAMN, kBMN>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmemBytes);
     attr_set = true;
   }
   const int units = ((M + 255) / 256) * ((N + BN - 1) / BN) * splits;
   const int pairs = units < num_sms() / 2 ? units : num_sms() / 2;
-  launch_k(gemm_pair_kernel<BN, kAMN, kBMN, kAdam>, dim3(2 * pairs), dim3(kThreads), Cfg::kSmemBytes,
+  launch_k(gemm_pair_kernel<BN, kAMN, kBMN>, dim3(2 * pairs), dim3(kThreads), Cfg::kSmemBytes,
            stream, ma, mb, mo, mx, M, N, K, splits, ep);
   return check_launch("gemm_pair_kernel");
 }
@@ -1080,11 +1010,6 @@ int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
   if (M <= 0 || N <= 0 || K <= 0) return set_error(kErrConfig, "gemm: empty problem");
   if ((ep.gelu ? 1 : 0) + (ep.gelu_bwd ? 1 : 0) + (ep.residual != nullptr ? 1 : 0) > 1)
     return set_error(kErrConfig, "gemm: gelu, gelu_bwd and residual epilogues are exclusive");
-  if (ep.out_kind == kOutAdamW &&
-      (splits > 1 || ep.bias != nullptr || ep.gelu || ep.gelu_bwd || ep.residual != nullptr ||
-       ep.adam_master == nullptr || ep.adam_m == nullptr || ep.adam_v == nullptr ||
-       ep.adam_param == nullptr || ep.step == nullptr || (ep.ldo % 4) != 0))
-    return set_error(kErrConfig, "gemm: AdamW epilogue needs plain fp32 gradients and state");
   // TMA: row strides must be 16-byte multiples; the epilogue's vector stores need ldo too.
   if ((a.ld % 8) != 0 || (b.ld % 8) != 0 || (ep.ldo % 8) != 0 || (ep.gelu && ep.ld_aux % 8 != 0))
     return set_error(kErrConfig, "gemm: lda, ldb, ldo and ld_aux must be multiples of 8 elements");
@@ -1094,13 +1019,6 @@ int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
   // N tile -force_bn, 0 = automatic (pair kernel whenever M spans at least one 256-row tile).
   int bn = force_bn;
   if (bn == 0) bn = pick_tile(M, N, b.mn_major);
-  if (ep.out_kind == kOutAdamW) {
-    if (!a.mn_major || !b.mn_major)
-      return set_error(kErrConfig, "gemm: AdamW epilogue is for weight gradients (MN-major A and B)");
-    if (bn == -256) return launch_gemm_pair<256, true, true, true>(a, b, M, N, K, ep, stream, splits);
-    if (bn == -128) return launch_gemm_pair<128, true, true, true>(a, b, M, N, K, ep, stream, splits);
-    return launch_gemm<128, true, true, true>(a, b, M, N, K, ep, stream, splits);
-  }
   if (bn == -160 && b.mn_major) return set_error(kErrConfig, "gemm: N tile 160 needs K-major B");
 #define GX_GEMM_DISPATCH(BN_, LAUNCH)                                                        \
   if (bn == BN_) {                                                                           \

@@ -30,7 +30,6 @@ enum OutKind : int {
   kOutF32 = GX_OUT_F32,
   kOutF32Accumulate = GX_OUT_F32_ACC,
   kOutF32Split = GX_OUT_F32_SPLIT,
-  kOutAdamW = GX_OUT_ADAMW
 };
 
 struct GemmOperand {
@@ -110,30 +109,7 @@ int cast_bf16(const void* src, void* dst, int64_t n, cudaStream_t st);
 // max_blocks > 0 caps the grid (the overlapped optimizer stream leaves SMs to the backward)
 int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n,
               float lr, float beta1, float beta2, float eps, float wd, const int64_t* step,
-              cudaStream_t st, int max_blocks = 0, const int* pending = nullptr);
-// AdamW over up to 8 (master, grad, m, v, bf16) segments in one launch
-struct AdamSeg {
-  void* p;
-  const void* g;
-  void* m;
-  void* v;
-  void* out;
-  int64_t n;
-};
-struct AdamSegs {
-  AdamSeg seg[8];
-  int n = 0;
-};
-int adamw_multi(const AdamSegs& segs, float lr, float beta1, float beta2, float eps, float wd,
-                const int64_t* step, cudaStream_t st, int blocks);
-// Persistent AdamW over `count` layers (device table, processing order) on `ctas` SMs; layer i
-// starts once ready[i] >= *step (optimizer_stream.cu).  mark_ready publishes ready[i] = *step.
-int adamw_persistent(const AdamSeg* table_dev, int count, const int64_t* step,
-                     const int64_t* ready, float lr, float beta1, float beta2, float eps, float wd,
-                     int ctas, cudaStream_t st);
-int mark_ready(int64_t* ready, const int64_t* step, cudaStream_t st);
-// *flag = v (stream-ordered; graph-friendly device flag updates)
-int set_flag(int* flag, int v, cudaStream_t st);
+              cudaStream_t st, int max_blocks = 0);
 int bump_step(int64_t* step, uint64_t* seed_offset, cudaStream_t st);
 struct PtrPack {
   const void* p[16];

@@ -844,17 +844,15 @@ int adamw(void* master, const void* grad, void* m, void* v, void* bf16_out, int6
 __global__ void __launch_bounds__(256, 4) adamw_dev_kernel(float4* __restrict__ p, const float4* __restrict__ g,
                                  float4* __restrict__ m, float4* __restrict__ v,
                                  uint2* __restrict__ out, int64_t n4, float lr, float b1, float b2,
-                                 float eps, float wd, const int64_t* __restrict__ step,
-                                 const int* __restrict__ pending) {
+                                 float eps, float wd, const int64_t* __restrict__ step) {
   pdl_enter();
-  if (pending != nullptr && *pending == 0) return;  // deferred update with nothing to apply
   adam_range<2>(adam_scalars_step(lr, b1, b2, eps, wd, step), p, g, m, v,
              out, n4);
 }
 
 int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, int64_t n,
               float lr, float beta1, float beta2, float eps, float wd, const int64_t* step,
-              cudaStream_t st, int max_blocks, const int* pending) {
+              cudaStream_t st, int max_blocks) {
   if (n % 4) return set_error(kErrConfig, "adamw: n % 4 != 0");
   if (n == 0) return kOk;
   // Short-lived blocks (one 4-float4 strip per thread, no grid-stride loop): the block
@@ -868,42 +866,8 @@ int adamw_dev(void* master, const void* grad, void* m, void* v, void* bf16_out, 
   launch_k(adamw_dev_kernel, dim3(blocks), dim3(256), 0, st,
            static_cast<float4*>(master), static_cast<const float4*>(grad),
            static_cast<float4*>(m), static_cast<float4*>(v), static_cast<uint2*>(bf16_out), n / 4,
-           lr, beta1, beta2, eps, wd, step, pending);
+           lr, beta1, beta2, eps, wd, step);
   return check_launch("adamw_dev_kernel");
-}
-
-// Several layers' updates in one launch (fewer forks / launches on the side stream): every
-// thread walks each segment with the grid stride.
-__global__ void __launch_bounds__(256, 4) adamw_multi_kernel(AdamSegs segs, float lr, float b1,
-                                                              float b2, float eps, float wd,
-                                                              const int64_t* __restrict__ step) {
-  pdl_enter();
-  const AdamScalars c = adam_scalars_step(lr, b1, b2, eps, wd, step);
-  for (int s = 0; s < segs.n; ++s) {
-    const AdamSeg& g = segs.seg[s];
-    adam_range<2>(c, static_cast<float4*>(g.p), static_cast<const float4*>(g.g),
-                  static_cast<float4*>(g.m), static_cast<float4*>(g.v), static_cast<uint2*>(g.out),
-                  g.n / 4);
-  }
-}
-
-int adamw_multi(const AdamSegs& segs, float lr, float beta1, float beta2, float eps, float wd,
-                const int64_t* step, cudaStream_t st, int blocks) {
-  for (int s = 0; s < segs.n; ++s)
-    if (segs.seg[s].n % 4) return set_error(kErrConfig, "adamw: n % 4 != 0");
-  if (segs.n == 0) return kOk;
-  launch_k(adamw_multi_kernel, dim3(blocks), dim3(256), 0, st, segs, lr, beta1, beta2, eps, wd,
-           step);
-  return check_launch("adamw_multi_kernel");
-}
-
-__global__ void set_flag_kernel(int* flag, int v) {
-  pdl_enter();
-  *flag = v;
-}
-int set_flag(int* flag, int v, cudaStream_t st) {
-  launch_k(set_flag_kernel, dim3(1), dim3(1), 0, st, flag, v);
-  return check_launch("set_flag_kernel");
 }
 
 __global__ void step_counters_kernel(int64_t* step, uint64_t* seed_offset) {

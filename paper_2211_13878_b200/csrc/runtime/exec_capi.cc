@@ -115,11 +115,6 @@ int gx_exec_loss(gx_exec* ex, float* out) {
   return ex->impl->loss(out);
 }
 
-int gx_exec_flush(gx_exec* ex) {
-  if (ex == nullptr) return bad("exec: NULL handle");
-  return ex->impl->flush_optimizer();
-}
-
 int gx_exec_step(gx_exec* ex, const void* x, const void* t, int use_graph, float* loss_out) {
   if (ex == nullptr) return bad("exec: NULL handle");
   int rc = ex->impl->load_batch(x, t);

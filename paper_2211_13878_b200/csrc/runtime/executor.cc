@@ -268,13 +268,7 @@ struct RankCtx {
   bf16* dx_out = nullptr;                   // first stage: input gradient per micro-batch
   float *loss = nullptr, *loss_dummy = nullptr;
   float* loss_ws = nullptr;  // deterministic loss reduction: block partials + ticket
-  int* opt_pending = nullptr;  // deferred optimizer: gradients of the last step not applied yet
-  std::vector<cudaEvent_t> opt_done;  // deferred optimizer: layer li updated (forward may read)
   std::vector<cudaEvent_t> gath_ev;   // SDP parameter all-gather of layer li done (prefetch)
-  std::vector<int> opt_group;         // side-stream optimizer: layers waiting for a grouped launch
-  // persistent optimizer: layer table in backward order + per-entry "gradients ready" flags
-  AdamSeg* opt_table = nullptr;
-  int64_t* opt_ready = nullptr;
   int64_t* step = nullptr;
   uint64_t* seed_off = nullptr;
   int64_t in_rows_total = 0;
@@ -312,8 +306,6 @@ class ExecutorImpl final : public Executor {
     if (join_event_ != nullptr) cudaEventDestroy(join_event_);
     for (auto& r : ranks_) {
       for (cudaEvent_t e : r->wg_done)
-        if (e != nullptr) cudaEventDestroy(e);
-      for (cudaEvent_t e : r->opt_done)
         if (e != nullptr) cudaEventDestroy(e);
       for (cudaEvent_t e : r->gath_ev)
         if (e != nullptr) cudaEventDestroy(e);
@@ -511,19 +503,9 @@ class ExecutorImpl final : public Executor {
   float lr_ = 1e-4f, b1_ = 0.9f, b2_ = 0.999f, eps_ = 1e-8f, wd_ = 0.f;
   bool optimizer_ = true;
   bool forward_only_ = false;  // profiler / debugging: skip loss, backward and optimizer
-  bool splitk_ = true;         // split-K for long-K / small-MN GEMMs (GX_SPLITK=0 disables)
-  int opt_blocks_ = 0;         // grid of the side-stream AdamW (GX_OPT_BLOCKS; 0 = 2 per SM)
-  int opt_group_ = 1;          // layers per side-stream AdamW launch (GX_OPT_GROUP, <= 8)
-  // Persistent flag-driven AdamW on this many SMs (cfg "optimizer_sms" / GX_OPT_SMS; 0 = the
-  // per-layer side-stream launches): one kernel per step walks the layers in backward order
-  // as their gradients are marked ready (optimizer_stream.cu).
-  int opt_sms_ = 0;
+  bool splitk_ = true;         // split-K for long-K / small-MN GEMMs (cfg "splitk")
   int64_t mem_cap_ = 0;  // per-rank device-byte cap (cfg "memory_cap_bytes"; 0 = none)
   int dec0_ = -1;         // first decoder (cross-attention) layer, or -1
-  bool persistent_opt() const {
-    return opt_sms_ > 0 && optimizer_ && !forward_only_ && !profiling_ && !deferred() &&
-           opt_stream_ == 0;
-  }
   bool dry_run_ = false;       // topology only: no device state (host-logic tests)
   float inv_count_ = 1.f;
 
@@ -545,39 +527,15 @@ class ExecutorImpl final : public Executor {
   // chain (the critical path) leaves idle.  ls_ is the stream gemm() launches on.
   cudaStream_t wg_ = nullptr;
   cudaStream_t ls_ = nullptr;
-  bool wgrad_stream_ = true;  // GX_WGRAD_STREAM=0 / "wgrad_stream": false disables
-  bool fuse_dz_ = false;      // previous layer's dropout bwd inside LN1 bwd (GX_FUSE_DZ=1 on;
-                              // off by default: it moves the wgrad-buffer wait earlier)
-  // AdamW on 0 = side stream (default), 1 = wgrad stream, 2 = main stream.  On the side stream
-  // it runs as a resident grid of 2 blocks per SM (64-register blocks): measured best at B = 1
-  // (9.4 ms/step vs 9.9 unbounded / on the wgrad stream) -- enough HBM parallelism without
-  // crowding the backward's GEMMs off their SMs.
-  int opt_stream_ = 0;
-  // AdamW inside the wgrad epilogues where legal (cfg "fused_adam" / GX_FUSED_ADAM=1).  Off by
-  // default: exact (tested against the standalone kernel) and 8 B/param less HBM traffic, but
-  // the row-per-lane state loads make the wgrad GEMMs hold SMs far longer (measured slower).
-  bool fused_adam_ = false;
-  // Deferred optimizer (cfg "defer_optimizer" / GX_DEFER_OPT=1): the AdamW of step t
-  // runs at the start of step t+1 on the side stream, layer 0 first, and layer l's forward
-  // waits only for layer l's update -- the HBM-bound update overlaps the next forward instead
-  // of contending with this backward.  A device flag makes the first step's pass a no-op, and
-  // flush_optimizer() applies a pending update before parameters are read back.
-  bool defer_opt_ = false;  // measured slower at B = 1 (9.54 vs 9.35 ms): off by default
-  bool deferred() const { return defer_opt_ && optimizer_ && !forward_only_; }
-  int deferred_updates(RankCtx& r, cudaStream_t st, bool record);
- public:
-  int flush_optimizer() override;
- private:
-  // The weight gradients of L are final after its single wgrad GEMM: one micro-batch and no
-  // data-parallel reduction (TP shards own their weight gradients).
+  bool wgrad_stream_ = true;  // cfg "wgrad_stream": false keeps the wgrads on stream_
+  bool fuse_dz_ = false;      // previous layer's dropout bwd inside LN1 bwd (cfg "fuse_dz")
+  // AdamW of each layer runs on the side stream as a resident grid of 2 blocks per SM
+  // (64-register blocks): enough HBM parallelism without crowding the backward's GEMMs off
+  // their SMs (DESIGN.md §7.2 lists the placements measured and rejected).
   // gradient bytes cleared before a step: the atomically accumulated head of the buffer, or
   // all of it when some chunk of the rank is empty (its weight-gradient GEMMs may not run)
   static size_t grad_zero_bytes(const RankCtx& r, const RankLayer& L) {
     return static_cast<size_t>(r.idle_chunks ? L.lay.total : L.lay.acc_end) * 4;
-  }
-  bool adam_fused(const RankLayer& L) const {
-    return fused_adam_ && optimizer_ && !forward_only_ && !defer_opt_ && m_ == 1 && L.d.dp == 1 &&
-           L.d.sdp == 1;
   }
   bool wg_active_ = false;    // this capture forks (off while profiling)
   bool wg_used_ = false;
@@ -675,30 +633,11 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     optimizer_ = cfg.value("optimizer", true);
     forward_only_ = cfg.value("forward_only", false);
     splitk_ = cfg.value("splitk", true);
-    if (const char* e = std::getenv("GX_SPLITK")) splitk_ = e[0] != '0';
-    opt_blocks_ = cfg.value("optimizer_blocks", 0);
-    opt_group_ = cfg.value("optimizer_group", 1);
-    if (const char* e = std::getenv("GX_OPT_GROUP")) opt_group_ = std::atoi(e);
-    opt_group_ = std::max(1, std::min(8, opt_group_));
-    opt_sms_ = cfg.value("optimizer_sms", 0);
-    if (const char* e = std::getenv("GX_OPT_SMS")) opt_sms_ = std::atoi(e);
-    opt_sms_ = std::max(0, opt_sms_);
     mem_cap_ = cfg.value("memory_cap_bytes", static_cast<int64_t>(0));
-    if (const char* e = std::getenv("GX_MEMORY_CAP")) mem_cap_ = std::atoll(e);
     wgrad_stream_ = cfg.value("wgrad_stream", true);
     comm_stream_ = cfg.value("comm_stream", true);
-    if (const char* e = std::getenv("GX_COMM_STREAM")) comm_stream_ = e[0] != '0';
     trace_ = cfg.value("trace", false);
     fuse_dz_ = cfg.value("fuse_dz", false);
-    opt_stream_ = cfg.value("optimizer_stream", 0);
-    fused_adam_ = cfg.value("fused_adam", false);
-    defer_opt_ = cfg.value("defer_optimizer", false);
-    if (const char* e = std::getenv("GX_DEFER_OPT")) defer_opt_ = e[0] != '0';
-    if (const char* e = std::getenv("GX_FUSED_ADAM")) fused_adam_ = e[0] != '0';
-    if (const char* e = std::getenv("GX_OPT_STREAM")) opt_stream_ = std::atoi(e);
-    if (const char* e = std::getenv("GX_FUSE_DZ")) fuse_dz_ = e[0] != '0';
-    if (const char* e = std::getenv("GX_WGRAD_STREAM")) wgrad_stream_ = e[0] != '0';
-    if (const char* e = std::getenv("GX_OPT_BLOCKS")) opt_blocks_ = std::atoi(e);
     thr_attn_ = threshold_of(p_attn_);
     thr_hidden_ = threshold_of(p_hidden_);
 
@@ -1139,24 +1078,6 @@ int ExecutorImpl::allocate(RankCtx& r) {
   r.loss_ws = A.a<float>(kLossBlocks + 1);
   if (r.loss_ws != nullptr) cudaMemset(r.loss_ws, 0, (kLossBlocks + 1) * sizeof(float));
   r.step = A.a<int64_t>(1);
-  r.opt_pending = A.a<int>(1);
-  if (r.opt_pending != nullptr) cudaMemset(r.opt_pending, 0, sizeof(int));
-  r.opt_table = A.a<AdamSeg>(static_cast<int64_t>(r.layers.size()));
-  r.opt_ready = A.a<int64_t>(static_cast<int64_t>(r.layers.size()));
-  if (r.opt_ready != nullptr) cudaMemset(r.opt_ready, 0, r.layers.size() * sizeof(int64_t));
-  if (r.opt_table != nullptr) {  // backward order: entry i = local layer (n - 1 - i)
-    std::vector<AdamSeg> tab;
-    for (size_t i = 0; i < r.layers.size(); ++i) {
-      RankLayer& L = r.layers[r.layers.size() - 1 - i];
-      tab.push_back(AdamSeg{L.master, L.gshard, L.m, L.v, L.pshard,
-                            adam_fused(L) ? L.lay.acc_end : L.shard_n});
-    }
-    cudaMemcpy(r.opt_table, tab.data(), tab.size() * sizeof(AdamSeg), cudaMemcpyHostToDevice);
-  }
-  r.opt_done.resize(r.layers.size(), nullptr);
-  for (auto& e : r.opt_done)
-    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
-      return set_error(kErrCuda, "executor: event creation failed");
   r.gath_ev.resize(r.layers.size(), nullptr);
   for (auto& e : r.gath_ev)
     if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
@@ -1202,7 +1123,6 @@ int ExecutorImpl::allocate(RankCtx& r) {
 
 // ------------------------------------------------------------------------- parameters
 int ExecutorImpl::set_layer_params(int layer, const float* canonical, int64_t n) {
-  GX_TRY(flush_optimizer());  // a pending update must not land on the new parameters
   if (layer < 0 || layer >= L_) return set_error(kErrConfig, "set_layer_params: bad layer");
   if (n != canonical_size(shape_[layer])) return set_error(kErrConfig, "set_layer_params: size");
   for (auto& r : ranks_) {
@@ -1232,7 +1152,6 @@ int ExecutorImpl::set_layer_params(int layer, const float* canonical, int64_t n)
 }
 
 int ExecutorImpl::export_layer(int layer, int what, float* canonical, int64_t n) {
-  if (what != 1) GX_TRY(flush_optimizer());  // parameters read back include the last update
   if (layer < 0 || layer >= L_) return set_error(kErrConfig, "export_layer: bad layer");
   if (n != canonical_size(shape_[layer])) return set_error(kErrConfig, "export_layer: size");
   GX_TRY(cuda_check(cudaStreamSynchronize(stream_), "export sync"));
@@ -1265,8 +1184,6 @@ int ExecutorImpl::export_layer(int layer, int what, float* canonical, int64_t n)
 }
 
 int ExecutorImpl::init_params(uint64_t seed, float std_dev) {
-  for (auto& r : ranks_)  // fresh parameters: drop any pending update
-    if (r->opt_pending != nullptr) GX_TRY(cuda_check(cudaMemset(r->opt_pending, 0, sizeof(int)), "clear pending"));
   for (auto& r : ranks_) {
     for (RankLayer& L : r->layers) {
       InitLayout il{};
@@ -1620,31 +1537,13 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
   if (rows == 0) return kOk;
   const int par = li & 1;
   bf16 *dz = r.dzb[par], *dpre = r.dpreb[par], *dout = r.doutb[par], *dqkv = r.dqkvb[par];
-  // Weight-gradient epilogue for a weight slot: fp32 gradient into G, or -- when the layer's
-  // gradient is complete after this one GEMM (one micro-batch, no data-parallel reduction) --
-  // AdamW applied in place by the epilogue, so the gradient never reaches HBM.  The fused
-  // form overwrites the bf16 weight, hence every wgrad below is issued after the dgrad GEMM
-  // that reads the same weight.
-  const bool fuse_adam = adam_fused(L);
+  // Weight-gradient epilogue for a weight slot: fp32 gradient into G (written on the first
+  // backward micro-batch, accumulated on the others).
   auto wgrad_ep = [&](const Slot& slot, int64_t ldo) {
     gx_gemm_epilogue w = epi();
     w.ldo = ldo;
-    if (fuse_adam) {
-      w.out_kind = kOutAdamW;
-      w.adam_master = L.master + slot.off;
-      w.adam_m = L.m + slot.off;
-      w.adam_v = L.v + slot.off;
-      w.adam_param = L.pshard + slot.off;
-      w.lr = lr_;
-      w.beta1 = b1_;
-      w.beta2 = b2_;
-      w.eps = eps_;
-      w.weight_decay = wd_;
-      w.step = r.step;
-    } else {
-      w.out_kind = wk;
-      w.out = G + slot.off;
-    }
+    w.out_kind = wk;
+    w.out = G + slot.off;
     return w;
   };
   gx_dropout d{};
@@ -1664,8 +1563,8 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     if (!A.dz_ready)
       GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(dY, dz, G + L.lay.b2.off, rows, h, d, stream_, r.cs_ws[0]); }));
     const gx_gemm_epilogue w2 = wgrad_ep(L.lay.w2, ft);
-    auto wgrad2 = [&] { return on_wgrad([&] { return gemm(dz, h, true, A.gel, ft, true, h, ft, rows, w2); }); };  // dW2 = dz^T gel
-    if (!fuse_adam) GX_TRY(wgrad2());  // as early as its inputs exist
+    // dW2 = dz^T gel, as early as its inputs exist
+    GX_TRY(on_wgrad([&] { return gemm(dz, h, true, A.gel, ft, true, h, ft, rows, w2); }));
     gx_gemm_epilogue e = epi();
     e.out_kind = kOutBF16;
     e.out = dpre;
@@ -1674,15 +1573,11 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     e.aux = A.pre;
     e.ld_aux = ft;
     GX_TRY(gemm(dz, h, false, P + L.lay.w2.off, ft, true, rows, ft, h, e));  // dz W2 * gelu'
-    if (fuse_adam) GX_TRY(wgrad2());  // after the dgrad that reads W2
-    auto wgrad1 = [&] {
-      return on_wgrad([&]() -> int {
-        GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dpre, ft, G + L.lay.b1.off, rows, ft, ls_, r.cs_ws[ls_ == stream_ ? 0 : 1]); }));
-        const gx_gemm_epilogue w1 = wgrad_ep(L.lay.w1, h);
-        return gemm(dpre, ft, true, A.ln2, h, true, ft, h, rows, w1);  // dW1 = dpre^T ln2
-      });
-    };
-    if (!fuse_adam) GX_TRY(wgrad1());
+    GX_TRY(on_wgrad([&]() -> int {
+      GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dpre, ft, G + L.lay.b1.off, rows, ft, ls_, r.cs_ws[ls_ == stream_ ? 0 : 1]); }));
+      const gx_gemm_epilogue w1 = wgrad_ep(L.lay.w1, h);
+      return gemm(dpre, ft, true, A.ln2, h, true, ft, h, rows, w1);  // dW1 = dpre^T ln2
+    }));
     int sp_c = 1;
     if (t == 1)
       GX_TRY(gemm_splitk(r, dpre, ft, P + L.lay.w1.off, h, true, rows, h, ft, &sp_c));
@@ -1694,7 +1589,6 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       c.ldo = h;
       GX_TRY(gemm(dpre, ft, false, P + L.lay.w1.off, h, true, rows, h, ft, c));  // dpre W1
     }
-    if (fuse_adam) GX_TRY(wgrad1());
     if (t > 1)
       return c_all_reduce(L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
                                stream_);
@@ -1736,14 +1630,13 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
    }
     if (s.cross) GX_TRY(cross_bwd_ln3(r, li, mb, dout));  // dx1, dout (self-attention)
     const gx_gemm_epilogue wo = wgrad_ep(L.lay.wo, ht);
-    auto wgrado = [&] { return on_wgrad([&] { return gemm(dout, h, true, A.ctx, ht, true, h, ht, rows, wo); }); };  // dWo = dout^T ctx
-    if (!fuse_adam) GX_TRY(wgrado());
+    // dWo = dout^T ctx
+    GX_TRY(on_wgrad([&] { return gemm(dout, h, true, A.ctx, ht, true, h, ht, rows, wo); }));
     gx_gemm_epilogue c = epi();
     c.out_kind = kOutBF16;
     c.out = r.dctx;
     c.ldo = ht;
     GX_TRY(gemm(dout, h, false, P + L.lay.wo.off, ht, true, rows, ht, h, c));  // dout Wo
-    if (fuse_adam) GX_TRY(wgrado());
     gx_attention_args at{};
     at.batch = A.samples * s.windows();  // one attention sequence per window
     at.seq = s.win;
@@ -1789,15 +1682,12 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
         return rpb_grad(r.rpb_part, A.samples * s.windows(), s.heads / t, side_of(s),
                         G + L.lay.rpb.off, true, stream_);
       }));
-    auto wgradq = [&] {
-      return on_wgrad([&]() -> int {
-        GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, ls_, r.cs_ws[ls_ == stream_ ? 0 : 1]); }));
-        const gx_gemm_epilogue wq = wgrad_ep(L.lay.wqkv, h);
-        return gemm(dqkv, 3 * ht, true, s.shift > 0 ? A.ln1r : A.ln1, h, true, 3 * ht, h, rows,
-                    wq);  // dWqkv
-      });
-    };
-    if (!fuse_adam) GX_TRY(wgradq());
+    GX_TRY(on_wgrad([&]() -> int {
+      GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dqkv, 3 * ht, G + L.lay.bqkv.off, rows, 3 * ht, ls_, r.cs_ws[ls_ == stream_ ? 0 : 1]); }));
+      const gx_gemm_epilogue wq = wgrad_ep(L.lay.wqkv, h);
+      return gemm(dqkv, 3 * ht, true, s.shift > 0 ? A.ln1r : A.ln1, h, true, 3 * ht, h, rows,
+                  wq);  // dWqkv
+    }));
     int sp_a = 1;
     if (t == 1 && s.shift == 0)  // (SW-MSA rolls dA back before LN1: keep it bf16)
       GX_TRY(gemm_splitk(r, dqkv, 3 * ht, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, &sp_a));
@@ -1818,7 +1708,6 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
                           "sw-msa da"));
       }
     }
-    if (fuse_adam) GX_TRY(wgradq());
     if (t > 1)
       return c_all_reduce(L.g_tp, r.rank, r.da, static_cast<size_t>(rows) * h, DType::kBF16,
                                stream_);
@@ -2085,87 +1974,27 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
     return kOk;
   }
   const bool on_cs = synced_on_cs_[li] != 0;
-  if (phase == 2 && optimizer_ && !deferred() && persistent_opt()) {
-    // the persistent optimizer (launched at the start of the backward) takes it from here
-    int64_t* flag = r.opt_ready + (static_cast<int>(r.layers.size()) - 1 - li);
-    if (wg_active_ && L.d.sdp == 1 && L.d.dp == 1)  // gradients complete on the wgrad stream
-      return on_wgrad([&] { return mark_ready(flag, r.step, ls_); });
-    return mark_ready(flag, r.step, on_cs ? cs_ : stream_);
-  }
-  if (phase == 2 && optimizer_ && !deferred()) {
-    // with the AdamW-fused weight-gradient epilogues only the LayerNorm / bias prefix is left
-    const int64_t n_opt = adam_fused(L) ? L.lay.acc_end : L.shard_n;
-    if (profiling_ || opt_stream_ == 2) {  // instrumented runs keep everything on one stream
+  if (phase == 2 && optimizer_) {
+    if (profiling_) {  // instrumented runs keep everything on one stream
       if (on_cs) GX_TRY(fork(cs_, stream_));
-      return timed(kOptim, 0, 30.0 * n_opt, [&] {
-        return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, n_opt, lr_, b1_, b2_, eps_,
+      return timed(kOptim, 0, 30.0 * L.shard_n, [&] {
+        return adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_,
                          wd_, r.step, stream_);
       });
     }
-    if (fork_events_.size() <= static_cast<size_t>(fork_used_)) {
-      cudaEvent_t e;
-      GX_TRY(cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event"));
-      fork_events_.push_back(e);
-    }
-    if (opt_stream_ == 1 && wg_active_) {  // behind this layer's wgrads, in order
-      GX_TRY(fork(stream_, wg_));
-      if (on_cs) GX_TRY(fork(cs_, wg_));
-      tmark("opt_begin L" + std::to_string(L.layer), wg_);
-      GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, n_opt, lr_, b1_, b2_, eps_,
-                       wd_, r.step, wg_, opt_blocks_));
-      tmark("opt_end L" + std::to_string(L.layer), wg_);
-      return kOk;
-    }
-    // Layers are updated in groups of opt_group_ (one fork + one multi-tensor launch); the
-    // stage's first layer (last in backward order) closes the final group.  The streams are
-    // in order, so waiting for the group's last layer covers the earlier ones.
-    r.opt_group.push_back(li);
-    if (static_cast<int>(r.opt_group.size()) < opt_group_ && li > 0) return kOk;
-    cudaEvent_t e = fork_events_[fork_used_++];
-    GX_TRY(cuda_check(cudaEventRecord(e, stream_), "fork record"));
-    GX_TRY(cuda_check(cudaStreamWaitEvent(side_, e, 0), "fork wait"));
-    if (wg_active_)  // ... and for the weight gradients
+    // side stream, after this layer's data-gradient chain, its weight gradients and their
+    // collectives
+    GX_TRY(fork(stream_, side_));
+    if (wg_active_)
       GX_TRY(cuda_check(cudaStreamWaitEvent(side_, r.wg_done[par], 0), "fork wait wgrad"));
-    if (on_cs) GX_TRY(fork(cs_, side_));  // ... and their collectives
+    if (on_cs) GX_TRY(fork(cs_, side_));
     side_used_ = true;
     tmark("opt_begin L" + std::to_string(L.layer), side_);
-    AdamSegs segs;
-    for (int lj : r.opt_group) {
-      RankLayer& Lg = r.layers[lj];
-      segs.seg[segs.n++] = AdamSeg{Lg.master, Lg.gshard, Lg.m, Lg.v, Lg.pshard,
-                                   adam_fused(Lg) ? Lg.lay.acc_end : Lg.shard_n};
-    }
-    r.opt_group.clear();
-    GX_TRY(adamw_multi(segs, lr_, b1_, b2_, eps_, wd_, r.step, side_,
-                       opt_blocks_ > 0 ? opt_blocks_ : 2 * num_sms()));
+    GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_, wd_,
+                     r.step, side_, 2 * num_sms()));
     tmark("opt_end L" + std::to_string(L.layer), side_);
-    return kOk;
   }
   return kOk;
-}
-
-// AdamW of every layer (forward order) from the gradients of the last completed step (no-op
-// on device when none is pending), each followed by zeroing the layer's accumulated-gradient
-// prefix for the next backward; `record` marks each layer's completion for the forward.
-int ExecutorImpl::deferred_updates(RankCtx& r, cudaStream_t st, bool record) {
-  for (size_t li = 0; li < r.layers.size(); ++li) {
-    RankLayer& L = r.layers[li];
-    const int64_t n_opt = adam_fused(L) ? L.lay.acc_end : L.shard_n;
-    tmark("opt_begin L" + std::to_string(L.layer), st);
-    GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, n_opt, lr_, b1_, b2_, eps_, wd_,
-                     r.step, st, opt_blocks_ > 0 ? opt_blocks_ : 2 * num_sms(), r.opt_pending));
-    GX_TRY(cuda_check(cudaMemsetAsync(L.gfull, 0, grad_zero_bytes(r, L), st), "memset grads"));
-    tmark("opt_end L" + std::to_string(L.layer), st);
-    if (record) GX_TRY(cuda_check(cudaEventRecord(r.opt_done[li], st), "opt done"));
-  }
-  return set_flag(r.opt_pending, 0, st);
-}
-
-int ExecutorImpl::flush_optimizer() {
-  if (!deferred() || dry_run_) return kOk;
-  GX_TRY(cuda_check(cudaStreamSynchronize(stream_), "flush sync"));
-  for (auto& r : ranks_) GX_TRY(deferred_updates(*r, stream_, false));
-  return cuda_check(cudaStreamSynchronize(stream_), "flush");
 }
 
 int ExecutorImpl::gather_params(RankCtx& r, int li, cudaStream_t st) {
@@ -2378,10 +2207,7 @@ int ExecutorImpl::step_once() {
   cs_used_ = false;
   wg_active_ = wgrad_stream_ && !profiling_;
   ls_ = stream_;
-  for (auto& r : ranks_) {
-    r->wg_pending[0] = r->wg_pending[1] = false;
-    r->opt_group.clear();
-  }
+  for (auto& r : ranks_) r->wg_pending[0] = r->wg_pending[1] = false;
   auto in_stage = [&](int st) {
     std::vector<RankCtx*> v;
     for (auto& r : ranks_)
@@ -2391,16 +2217,10 @@ int ExecutorImpl::step_once() {
   for (auto& r : ranks_) {
     for (RankLayer& L : r->layers)
       for (Acts& a : L.acts) a.ln1_ready = a.dz_ready = false;
-    if (!deferred()) GX_TRY(bump_step(r->step, nullptr, stream_));
+    GX_TRY(bump_step(r->step, nullptr, stream_));
     GX_TRY(cuda_check(cudaMemsetAsync(r->loss, 0, 4, stream_), "memset loss"));
-    if (!deferred())
-      for (RankLayer& L : r->layers)
-        GX_TRY(cuda_check(cudaMemsetAsync(L.gfull, 0, grad_zero_bytes(*r, L), stream_), "memset grads"));
-  }
-  if (deferred()) {  // last step's AdamW on the side stream, layer by layer (see defer_opt_)
-    GX_TRY(fork(stream_, side_));
-    side_used_ = true;
-    for (auto& r : ranks_) GX_TRY(deferred_updates(*r, side_, true));
+    for (RankLayer& L : r->layers)
+      GX_TRY(cuda_check(cudaMemsetAsync(L.gfull, 0, grad_zero_bytes(*r, L), stream_), "memset grads"));
   }
   // ---------------------------------------------------------------- forward (GPipe)
   for (int mb = 0; mb < m_; ++mb) {
@@ -2414,9 +2234,6 @@ int ExecutorImpl::step_once() {
       }
       const int nl = static_cast<int>(R[0]->layers.size());
       for (int li = 0; li < nl; ++li) {
-        if (deferred() && mb == 0)  // this layer's parameters carry the last step's update
-          for (RankCtx* r : R)
-            GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, r->opt_done[li], 0), "opt wait"));
         for (RankCtx* r : R) GX_TRY(xin_fwd(*r, li, mb));
         if (mb == 0) {
           // SDP parameters: gathered on stream_ for the stage's first layer, prefetched on
@@ -2433,11 +2250,7 @@ int ExecutorImpl::step_once() {
           if (comm_on_cs() && li + 1 < nl && R[0]->layers[li + 1].d.sdp > 1) {
             GX_TRY(fork(stream_, cs_));
             cs_used_ = true;
-            for (RankCtx* r : R) {
-              if (deferred())  // the next layer's shard carries the last step's update
-                GX_TRY(cuda_check(cudaStreamWaitEvent(cs_, r->opt_done[li + 1], 0), "opt wait"));
-              GX_TRY(gather_params(*r, li + 1, cs_));
-            }
+            for (RankCtx* r : R) GX_TRY(gather_params(*r, li + 1, cs_));
             // recorded after every rank posted: a simulated collective runs at the last post
             for (RankCtx* r : R)
               GX_TRY(cuda_check(cudaEventRecord(r->gath_ev[li + 1], cs_), "gather done"));
@@ -2456,14 +2269,6 @@ int ExecutorImpl::step_once() {
     }
   }
   tmark("fwd_end", stream_);
-  if (persistent_opt()) {  // one persistent AdamW per rank on a slice of the SMs
-    GX_TRY(fork(stream_, side_));
-    side_used_ = true;
-    const int ctas = std::max(1, std::min(opt_sms_, num_sms() / 2));
-    for (auto& r : ranks_)
-      GX_TRY(adamw_persistent(r->opt_table, static_cast<int>(r->layers.size()), r->step,
-                              r->opt_ready, lr_, b1_, b2_, eps_, wd_, ctas, side_));
-  }
   // --------------------------------------------------------------- backward (GPipe)
   for (int mb = m_ - 1; mb >= 0 && !forward_only_; --mb) {
     for (int st = P_ - 1; st >= 0; --st) {
@@ -2537,11 +2342,6 @@ int ExecutorImpl::step_once() {
     GX_TRY(cuda_check(cudaEventRecord(join_event_, side_), "join record"));
     GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, join_event_, 0), "join wait"));
   }
-  if (deferred())  // this step's gradients are complete: the next step (or a flush) applies them
-    for (auto& r : ranks_) {
-      GX_TRY(bump_step(r->step, nullptr, stream_));
-      GX_TRY(set_flag(r->opt_pending, 1, stream_));
-    }
   tmark("step_end", stream_);
   for (auto& r : ranks_) GX_TRY(comm_->world_sum(r->rank, r->loss, stream_));
   // next step draws fresh dropout masks

@@ -93,8 +93,6 @@ class Executor {
   virtual int run2(bool use_graph, bool profile) = 0;
   virtual std::string profile_report() const = 0;
   virtual int init_params(uint64_t seed, float std_dev) = 0;
-  // apply an optimizer update still pending from the last step (deferred-optimizer mode)
-  virtual int flush_optimizer() = 0;
   // Groups, data chunks and pipeline transfers of the local ranks (no device state needed).
   virtual std::string topology() const = 0;
 };

@@ -542,26 +542,44 @@ int env_int(const char* name, int dflt) {
   return e == nullptr || *e == '\0' ? dflt : std::atoi(e);
 }
 
-// Rank 0 creates the NCCL id and publishes it through a file; the other ranks poll for it,
-// ignoring files older than a minute before they started (a leftover of a failed launch).
+// Rank 0 creates the NCCL id and publishes it through a file as "<launch id> <hex>"; the other
+// ranks poll for a file carrying THEIR launch id, so a leftover of an earlier (e.g. crashed)
+// launch on the same path is never read.  The launch id is shared by every rank of one launch:
+// $PARPLAN_LAUNCH_ID, else torchrun's $TORCHELASTIC_RUN_ID.  Without either, only a file
+// written after this process started (minus a few seconds of launch skew) is accepted.
 // Rank 0 removes the file once its communicator exists (NCCL init is collective, so every rank
 // has read it by then).
+std::string launch_id() {
+  for (const char* name : {"PARPLAN_LAUNCH_ID", "TORCHELASTIC_RUN_ID"}) {
+    const char* e = std::getenv(name);
+    if (e != nullptr && *e != '\0') return e;
+  }
+  return "-";
+}
+
+const auto kProcessStart = std::filesystem::file_time_type::clock::now();
+
 std::string exchange_nccl_id(const std::string& path, int rank) {
+  const std::string nonce = launch_id();
   if (rank == 0) {
     char hex[257];
     gx_check(GxLib::get().nccl_id(hex, sizeof(hex)), "gx_nccl_unique_id");
+    std::error_code ec;
+    std::filesystem::remove(path, ec);  // a stale id must not outlive this launch's start
     const std::string tmp = path + ".tmp";
-    write_text(tmp, hex);
+    write_text(tmp, nonce + " " + hex);
     std::filesystem::rename(tmp, path);
     return hex;
   }
-  const auto not_before = std::filesystem::file_time_type::clock::now() - std::chrono::seconds(60);
+  const auto not_before = kProcessStart - std::chrono::seconds(5);
   for (int i = 0; i < 1200; ++i) {
     std::error_code ec;
     const auto mtime = std::filesystem::last_write_time(path, ec);
     std::ifstream f(path);
-    std::string hex;
-    if (!ec && mtime >= not_before && f && (f >> hex) && hex.size() == 256) return hex;
+    std::string tag, hex;
+    if (!ec && f && (f >> tag >> hex) && hex.size() == 256 && tag == nonce &&
+        (nonce != "-" || mtime >= not_before))
+      return hex;
     std::this_thread::sleep_for(std::chrono::milliseconds(50));
   }
   throw parplan::ValidationError("timed out waiting for the NCCL id in " + path);

@@ -176,10 +176,6 @@ class PlanExecutor:
     def init_params(self, seed=1, std=0.02):
         _lib.check(_lib.lib().gx_exec_init_params(self._h, seed, std))
 
-    def flush(self):
-        """Apply the optimizer update still pending from the last step (deferred optimizer)."""
-        _lib.check(_lib.lib().gx_exec_flush(self._h))
-
     def loss(self) -> float:
         v = ctypes.c_float()
         _lib.check(_lib.lib().gx_exec_loss(self._h, ctypes.byref(v)))

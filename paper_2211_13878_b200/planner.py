@@ -61,13 +61,17 @@ class PlanAPI:
             raise _lib.GuardError(code, msg)
         raise _lib.ValidationError(code, msg)
 
+    _BUF = 1 << 20  # plan JSON of a 96-layer model is ~40 KB: one call nearly always fits
+
     def _call_text(self, name, *args) -> tuple[int, str]:
+        """One C call into a generously sized buffer (the search runs once); only an output
+        longer than the buffer costs a second call with the exact size."""
         needed = ctypes.c_size_t(0)
-        code = self._fn(name)(*args, None, 0, ctypes.byref(needed))
-        if code not in (0, 2):
-            self._raise(code)
-        buf = ctypes.create_string_buffer(needed.value)
-        code = self._fn(name)(*args, buf, needed.value, ctypes.byref(needed))
+        buf = ctypes.create_string_buffer(self._BUF)
+        code = self._fn(name)(*args, buf, self._BUF, ctypes.byref(needed))
+        if code not in (0, 2) and needed.value > self._BUF:
+            buf = ctypes.create_string_buffer(needed.value)
+            code = self._fn(name)(*args, buf, needed.value, ctypes.byref(needed))
         if code not in (0, 2):
             self._raise(code)
         return code, buf.value.decode()

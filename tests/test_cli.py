@@ -284,9 +284,12 @@ def test_run_nccl_id_rendezvous_between_two_processes(cli, tmp_path):
          "shape": {"hidden": 256, "heads": 4, "seq": 64, "ffn": 1024}}] * 2})
     c = dump(tmp_path, "c.json", models.cluster(2, 8))
     idf = tmp_path / "nccl.id"
+    # a leftover id of an earlier launch on the same path must never be read
+    idf.write_text("earlier-launch " + "0" * 256)
     procs = []
     for rank in (1, 0):
-        env = dict(os.environ, WORLD_SIZE="2", RANK=str(rank), LOCAL_RANK=str(rank))
+        env = dict(os.environ, WORLD_SIZE="2", RANK=str(rank), LOCAL_RANK=str(rank),
+                   PARPLAN_LAUNCH_ID="this-launch")
         procs.append(subprocess.Popen([cli, "run", "--model", m, "--cluster", c, "--batches", "4",
                                        "--nccl-id-file", str(idf)], env=env,
                                       stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True))
@@ -295,7 +298,8 @@ def test_run_nccl_id_rendezvous_between_two_processes(cli, tmp_path):
         assert p.returncode == 1
         assert "gx_exec_create" in se and "timed out" not in se
     assert "[dp:2] x2" in outs[1][0] and outs[0][0] == ""  # only rank 0 prints
-    assert len(idf.read_text()) == 256  # left in place: the communicator never formed
+    tag, hex_id = idf.read_text().split()  # left in place: the communicator never formed
+    assert tag == "this-launch" and len(hex_id) == 256 and hex_id != "0" * 256
     # WORLD_SIZE must agree with the cluster
     env = dict(os.environ, WORLD_SIZE="4", RANK="0")
     r = subprocess.run([cli, "run", "--model", m, "--cluster", c, "--batches", "4"], env=env,
