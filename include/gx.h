@@ -155,6 +155,11 @@ GX_API int gx_exec_profile_report(gx_exec* ex, char* out, size_t cap, size_t* ne
  * canonical index, never on the sharding): LN gains 1, biases 0, weights N(0, std^2). */
 GX_API int gx_exec_init_params(gx_exec* ex, uint64_t seed, float std_dev);
 GX_API int gx_exec_loss(gx_exec* ex, float* out);
+/* Wait for the step(s) in flight, polling the NCCL communicators' asynchronous errors; after
+ * timeout_ms (<= 0: none) or on a communicator error the communicators are aborted and
+ * GX_ERR_NCCL returned instead of hanging (ncclCommGetAsyncError / ncclCommAbort).
+ * gx_exec_loss and gx_exec_step use it with config "sync_timeout_ms" (default 600000). */
+GX_API int gx_exec_sync(gx_exec* ex, int64_t timeout_ms);
 /* load_batch + run + loss: the end-to-end call (host buffers in, loss out). */
 GX_API int gx_exec_step(gx_exec* ex, const void* x_host, const void* target_host, int use_graph,
                         float* loss_out);

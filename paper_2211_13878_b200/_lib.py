@@ -94,6 +94,7 @@ def _declare(L: ctypes.CDLL) -> None:
     L.gx_exec_load_batch_device.argtypes = [vp, vp, vp]
     L.gx_exec_run.argtypes = [vp, c_int]
     L.gx_exec_loss.argtypes = [vp, POINTER(c_float)]
+    L.gx_exec_sync.argtypes = [vp, c_int64]
     L.gx_exec_step.argtypes = [vp, vp, vp, c_int, POINTER(c_float)]
     L.gx_exec_export_output.argtypes = [vp, c_int, vp]
     L.gx_exec_stream.argtypes = [vp, POINTER(c_void_p)]
@@ -102,7 +103,7 @@ def _declare(L: ctypes.CDLL) -> None:
     L.gx_nccl_unique_id.argtypes = [c_char_p, c_size_t]
     for name in ("gx_exec_create", "gx_exec_destroy", "gx_exec_set_layer_params",
                  "gx_exec_export_layer", "gx_exec_load_batch", "gx_exec_load_batch_device",
-                 "gx_exec_run", "gx_exec_loss", "gx_exec_step", "gx_exec_export_output",
+                 "gx_exec_run", "gx_exec_loss", "gx_exec_sync", "gx_exec_step", "gx_exec_export_output",
                  "gx_exec_stream", "gx_exec_info", "gx_exec_canonical_size",
                  "gx_nccl_unique_id"):
         getattr(L, name).restype = c_int

@@ -2,6 +2,8 @@
 #include "comm.h"
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cstring>
 #include <deque>
 
@@ -183,13 +185,16 @@ ncclDataType_t nccl_type(DType t) { return t == DType::kBF16 ? ncclBfloat16 : nc
 
 class NcclComm final : public Comm {
  public:
-  NcclComm(int world, int rank) : world_size_(world), rank_(rank) {}
+  NcclComm(int world, int rank, const NcclOptions& opt)
+      : world_size_(world), rank_(rank), opt_(opt) {}
   ~NcclComm() override {
     for (ncclComm_t c : comms_)
       if (c != nullptr) ncclCommDestroy(c);
     if (world_ != nullptr) ncclCommDestroy(world_);
   }
 
+  // Nonblocking communicators: creation returns at once and is polled with a deadline, so a
+  // rank whose peers never arrive fails with an error instead of hanging the job.
   int init(const std::string& id_bytes, std::string* err) {
     ncclUniqueId id;
     if (id_bytes.size() != sizeof(id.internal)) {
@@ -197,9 +202,17 @@ class NcclComm final : public Comm {
       return kErrConfig;
     }
     std::memcpy(id.internal, id_bytes.data(), sizeof(id.internal));
-    const ncclResult_t r = ncclCommInitRank(&world_, world_size_, id, rank_);
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.blocking = 0;
+    if (opt_.min_ctas > 0) cfg.minCTAs = opt_.min_ctas;
+    if (opt_.max_ctas > 0) cfg.maxCTAs = opt_.max_ctas;
+    ncclResult_t r = ncclCommInitRankConfig(&world_, world_size_, id, rank_, &cfg);
+    if (r == ncclSuccess || r == ncclInProgress) r = wait_ready(world_);
     if (r != ncclSuccess) {
-      *err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      *err = std::string("ncclCommInitRankConfig: ") + ncclGetErrorString(r) +
+             (r == ncclInProgress ? " (timed out waiting for the other ranks)" : "");
+      if (world_ != nullptr) ncclCommAbort(world_);
+      world_ = nullptr;
       return kErrNccl;
     }
     return kOk;
@@ -211,8 +224,11 @@ class NcclComm final : public Comm {
       if (groups_[g].ranks.size() <= 1) continue;
       const int idx = groups_[g].index_of(rank_);
       ncclComm_t c = nullptr;
-      const ncclResult_t r = ncclCommSplit(world_, idx >= 0 ? 0 : NCCL_SPLIT_NOCOLOR,
-                                           idx >= 0 ? idx : 0, &c, nullptr);
+      // the child inherits the parent's config (nonblocking, CTA budget)
+      ncclResult_t r = ncclCommSplit(world_, idx >= 0 ? 0 : NCCL_SPLIT_NOCOLOR,
+                                     idx >= 0 ? idx : 0, &c, nullptr);
+      if (r == ncclInProgress) r = wait_ready(world_);
+      if (r == ncclSuccess && c != nullptr) r = wait_ready(c);
       if (r != ncclSuccess) return nccl_fail(r, "ncclCommSplit");
       comms_[g] = c;
     }
@@ -221,8 +237,8 @@ class NcclComm final : public Comm {
 
   int all_reduce(int gid, int, void* buf, size_t count, DType t, cudaStream_t s) override {
     if (groups_[gid].ranks.size() <= 1) return kOk;
-    return nccl_ok(ncclAllReduce(buf, buf, count, nccl_type(t), ncclSum, comms_[gid], s),
-                   "ncclAllReduce");
+    return done(comms_[gid], ncclAllReduce(buf, buf, count, nccl_type(t), ncclSum, comms_[gid], s),
+                "ncclAllReduce");
   }
 
   int reduce_scatter(int gid, int, const void* send, void* recv, size_t count, DType t,
@@ -233,9 +249,9 @@ class NcclComm final : public Comm {
                                      s),
                      "reduce_scatter copy");
     }
-    return nccl_ok(
-        ncclReduceScatter(send, recv, count, nccl_type(t), ncclSum, comms_[gid], s),
-        "ncclReduceScatter");
+    return done(comms_[gid],
+                ncclReduceScatter(send, recv, count, nccl_type(t), ncclSum, comms_[gid], s),
+                "ncclReduceScatter");
   }
 
   int all_gather(int gid, int rank, const void* send, void* recv,
@@ -250,8 +266,8 @@ class NcclComm final : public Comm {
     const bool equal = std::all_of(counts.begin(), counts.end(),
                                    [&](size_t c) { return c == counts[0]; });
     if (equal)
-      return nccl_ok(ncclAllGather(send, recv, counts[0], nccl_type(t), comms_[gid], s),
-                     "ncclAllGather");
+      return done(comms_[gid], ncclAllGather(send, recv, counts[0], nccl_type(t), comms_[gid], s),
+                  "ncclAllGather");
     const int me = g.index_of(rank);
     ncclGroupStart();
     size_t displ = 0;
@@ -260,26 +276,51 @@ class NcclComm final : public Comm {
       const void* src = static_cast<int>(j) == me ? send : dst;
       const ncclResult_t r =
           ncclBroadcast(src, dst, counts[j], nccl_type(t), static_cast<int>(j), comms_[gid], s);
-      if (r != ncclSuccess) {
+      if (r != ncclSuccess && r != ncclInProgress) {
         ncclGroupEnd();
         return nccl_fail(r, "ncclBroadcast");
       }
       displ += counts[j];
     }
-    return nccl_ok(ncclGroupEnd(), "ncclGroupEnd");
+    return done(comms_[gid], ncclGroupEnd(), "ncclGroupEnd");
   }
 
   int send(int, int peer, const void* buf, size_t bytes, cudaStream_t s) override {
-    return nccl_ok(ncclSend(buf, bytes, ncclUint8, peer, world_, s), "ncclSend");
+    return done(world_, ncclSend(buf, bytes, ncclUint8, peer, world_, s), "ncclSend");
   }
   int recv(int, int peer, void* buf, size_t bytes, cudaStream_t s) override {
-    return nccl_ok(ncclRecv(buf, bytes, ncclUint8, peer, world_, s), "ncclRecv");
+    return done(world_, ncclRecv(buf, bytes, ncclUint8, peer, world_, s), "ncclRecv");
   }
   int group_start() override { return nccl_ok(ncclGroupStart(), "ncclGroupStart"); }
-  int group_end() override { return nccl_ok(ncclGroupEnd(), "ncclGroupEnd"); }
+  int group_end() override { return done(world_, ncclGroupEnd(), "ncclGroupEnd"); }
 
   int world_sum(int, float* v, cudaStream_t s) override {
-    return nccl_ok(ncclAllReduce(v, v, 1, ncclFloat32, ncclSum, world_, s), "ncclAllReduce(loss)");
+    return done(world_, ncclAllReduce(v, v, 1, ncclFloat32, ncclSum, world_, s),
+                "ncclAllReduce(loss)");
+  }
+
+  int poll_async() override {
+    auto check = [](ncclComm_t c) {
+      ncclResult_t a = ncclSuccess;
+      if (c != nullptr && ncclCommGetAsyncError(c, &a) == ncclSuccess && a != ncclSuccess &&
+          a != ncclInProgress)
+        return nccl_fail(a, "NCCL asynchronous error");
+      return static_cast<int>(kOk);
+    };
+    int rc = check(world_);
+    for (ncclComm_t c : comms_)
+      if (rc == kOk) rc = check(c);
+    return rc;
+  }
+
+  void abort() override {
+    for (ncclComm_t& c : comms_)
+      if (c != nullptr) {
+        ncclCommAbort(c);
+        c = nullptr;
+      }
+    if (world_ != nullptr) ncclCommAbort(world_);
+    world_ = nullptr;
   }
 
  private:
@@ -289,20 +330,59 @@ class NcclComm final : public Comm {
   static int nccl_ok(ncclResult_t r, const char* what) {
     return r == ncclSuccess ? kOk : nccl_fail(r, what);
   }
+  // Nonblocking communicator: poll until the communicator leaves ncclInProgress (or the
+  // deadline passes, reported as ncclInProgress).
+  ncclResult_t wait_ready(ncclComm_t c) const {
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      ncclResult_t a = ncclSuccess;
+      const ncclResult_t q = ncclCommGetAsyncError(c, &a);
+      if (q != ncclSuccess) return q;
+      if (a != ncclInProgress) return a;
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(opt_.timeout_ms))
+        return ncclInProgress;
+      std::this_thread::yield();
+    }
+  }
+  // An enqueue on a nonblocking communicator may return ncclInProgress: wait for it.
+  int done(ncclComm_t c, ncclResult_t r, const char* what) const {
+    if (r == ncclInProgress) r = wait_ready(c);
+    return nccl_ok(r, what);
+  }
   int world_size_, rank_;
+  NcclOptions opt_;
   ncclComm_t world_ = nullptr;
   std::vector<ncclComm_t> comms_;
 };
 
+// =========================================================== no-op world (per-GPU proxy)
+class NullComm final : public Comm {
+ public:
+  int finalize() override { return kOk; }
+  int all_reduce(int, int, void*, size_t, DType, cudaStream_t) override { return kOk; }
+  int reduce_scatter(int, int, const void*, void*, size_t, DType, cudaStream_t) override {
+    return kOk;
+  }
+  int all_gather(int, int, const void*, void*, const std::vector<size_t>&, DType,
+                 cudaStream_t) override {
+    return kOk;
+  }
+  int send(int, int, const void*, size_t, cudaStream_t) override { return kOk; }
+  int recv(int, int, void*, size_t, cudaStream_t) override { return kOk; }
+  int world_sum(int, float*, cudaStream_t) override { return kOk; }
+};
+
 }  // namespace
+
+std::unique_ptr<Comm> make_null_comm(int) { return std::make_unique<NullComm>(); }
 
 std::unique_ptr<Comm> make_sim_comm(int world_size) {
   return std::make_unique<SimComm>(world_size);
 }
 
 std::unique_ptr<Comm> make_nccl_comm(int world_size, int rank, const std::string& unique_id,
-                                     std::string* err) {
-  auto c = std::make_unique<NcclComm>(world_size, rank);
+                                     const NcclOptions& opt, std::string* err) {
+  auto c = std::make_unique<NcclComm>(world_size, rank, opt);
   if (c->init(unique_id, err) != kOk) return nullptr;
   return c;
 }

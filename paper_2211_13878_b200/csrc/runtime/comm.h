@@ -61,14 +61,29 @@ class Comm {
   virtual int group_end() { return 0; }
   // Scalar fp32 sum over the world (loss reporting).
   virtual int world_sum(int rank, float* dev_scalar, cudaStream_t s) = 0;
+  // Failure detection: an asynchronous communicator error (a peer died, a
+  // network fault) as kErrNccl, else kOk.  abort() tears every communicator down so kernels
+  // blocked on a dead peer return and the process can exit instead of hanging.
+  virtual int poll_async() { return 0; }
+  virtual void abort() {}
 
  protected:
   std::vector<CommGroup> groups_;
 };
 
 std::unique_ptr<Comm> make_sim_comm(int world_size);
+// Every collective and transfer is a no-op: one rank of a larger world run alone on one GPU
+// (bench.py's per-GPU proxy of an N-GPU plan).
+std::unique_ptr<Comm> make_null_comm(int world_size);
+// NCCL communicator options (E13): a CTA budget so collectives overlapped with GEMMs leave
+// SMs to them, and a timeout for communicator creation (nonblocking init, polled).
+struct NcclOptions {
+  int min_ctas = 0;        // 0 = NCCL default
+  int max_ctas = 16;       // per collective; NVSwitch (NVLS) needs few CTAs for full bandwidth
+  int timeout_ms = 120000;  // init / split / in-progress polling limit
+};
 // unique_id: the 128-byte ncclUniqueId shared by all ranks (rank 0 creates it).
 std::unique_ptr<Comm> make_nccl_comm(int world_size, int rank, const std::string& unique_id,
-                                     std::string* err);
+                                     const NcclOptions& opt, std::string* err);
 
 }  // namespace gx

@@ -115,6 +115,11 @@ int gx_exec_loss(gx_exec* ex, float* out) {
   return ex->impl->loss(out);
 }
 
+int gx_exec_sync(gx_exec* ex, int64_t timeout_ms) {
+  if (ex == nullptr) return bad("exec: NULL handle");
+  return ex->impl->sync(timeout_ms);
+}
+
 int gx_exec_step(gx_exec* ex, const void* x, const void* t, int use_graph, float* loss_out) {
   if (ex == nullptr) return bad("exec: NULL handle");
   int rc = ex->impl->load_batch(x, t);

@@ -12,6 +12,8 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
+#include <thread>
 #include <functional>
 #include <sstream>
 
@@ -266,6 +268,11 @@ struct RankCtx {
   float* acc32 = nullptr;  // split-K fp32 slices [kMaxSplits][rows][h]
   bf16 *x_in = nullptr, *target = nullptr;  // [m micro-batches of this rank's rows][h]
   bf16* dx_out = nullptr;                   // first stage: input gradient per micro-batch
+  // stages > 0: the input gradient (and dL/dmemory) each backward micro-batch sends to the
+  // previous stage, copied out of the ping-pong gradient buffers so the send (on the pipeline
+  // stream) overlaps the next micro-batch's backward instead of fencing it
+  bf16* pp_dx_send = nullptr;
+  float* pp_dmem_send = nullptr;
   float *loss = nullptr, *loss_dummy = nullptr;
   float* loss_ws = nullptr;  // deterministic loss reduction: block partials + ticket
   std::vector<cudaEvent_t> gath_ev;   // SDP parameter all-gather of layer li done (prefetch)
@@ -292,6 +299,7 @@ class ExecutorImpl final : public Executor {
   int run(bool use_graph) override { return run2(use_graph, false); }
   int run2(bool use_graph, bool profile) override;
   int loss(float* out) override;
+  int sync(int64_t timeout_ms) override;
   int export_output(void* host_bf16, int what) override;
   cudaStream_t stream() const override { return stream_; }
   std::string info() const override;
@@ -315,6 +323,7 @@ class ExecutorImpl final : public Executor {
     if (stream_ != nullptr) cudaStreamDestroy(stream_);
     if (side_ != nullptr) cudaStreamDestroy(side_);
     if (cs_ != nullptr) cudaStreamDestroy(cs_);
+    if (pp_ != nullptr) cudaStreamDestroy(pp_);
     if (wg_ != nullptr) cudaStreamDestroy(wg_);
   }
 
@@ -382,8 +391,37 @@ class ExecutorImpl final : public Executor {
   int xin_bwd(RankCtx& r, int li, int mb);
   int gather_params(RankCtx& r, int li, cudaStream_t st);
   bool prefetched_ = false;  // the current layer's SDP gather was prefetched on cs_
-  int pp_fwd(RankCtx& r, int mb, bool send);
-  int pp_bwd(RankCtx& r, int mb, bool send);
+  int pp_fwd(RankCtx& r, int mb, bool send, cudaStream_t st);
+  int pp_bwd(RankCtx& r, int mb, bool send, cudaStream_t st);
+  // One pipeline-boundary exchange of every rank in R on the pipeline stream pp_ (E12/E13):
+  // forked after the producer's work on stream_; receives are joined back before the
+  // consumer runs, sends (of activations / private gradient copies that nothing overwrites
+  // within the step) only at the step end.
+  int pp_exchange(const std::vector<RankCtx*>& R, int mb, bool fwd, bool send) {
+    const bool side = pp_ != nullptr && !profiling_;
+    cudaStream_t st = side ? pp_ : stream_;
+    if (side) GX_TRY(fork(stream_, pp_));
+    double bytes = 0;  // rows this exchange moves (send or receive side), bf16
+    for (RankCtx* r : R) {
+      const bool out = fwd == send;  // the stage's output rows (else its input rows)
+      const RankLayer& L = out ? r->layers.back() : r->layers.front();
+      const double hs = out ? 1.0 * L.sh.seq * L.sh.h : 1.0 * L.sh.in_seq() * L.sh.in_h();
+      for (const Xfer& x : pp_plan(r->stage, r->idx, mb, fwd ? (send ? 0 : 1) : (send ? 2 : 3)))
+        bytes += 2.0 * hs * static_cast<double>(x.hi - x.lo);
+    }
+    return timed(kComm, 0, bytes, [&]() -> int {
+      GX_TRY(comm_->group_start());
+      for (RankCtx* r : R) GX_TRY(fwd ? pp_fwd(*r, mb, send, st) : pp_bwd(*r, mb, send, st));
+      GX_TRY(comm_->group_end());
+      if (side) {
+        pp_used_ = true;
+        if (!send) GX_TRY(fork(pp_, stream_));
+      }
+      return kOk;
+    }, kPpSendRecv, bytes);
+  }
+  cudaStream_t pp_ = nullptr;
+  bool pp_used_ = false;
   struct Xfer {
     int peer;
     int64_t lo, hi;  // global sample range within the iteration
@@ -401,19 +439,24 @@ class ExecutorImpl final : public Executor {
   // the events become external event-record nodes, so a replay of the instrumented graph
   // yields per-launch device durations of exactly the kernels the plain graph runs.
   enum Cat { kGemm, kAttnFwd, kAttnBwd, kNorm, kElementwise, kOptim, kComm, kNumCats };
+  // collective classes of the plan, reported with their NCCL bus bytes
+  enum CommKind { kTpAllReduce, kSdpAllGather, kSdpReduceScatter, kDpAllReduce, kRelayout,
+                  kPpSendRecv, kNumCommKinds };
   struct Rec {
     int cat;
     double flops, bytes;
     cudaEvent_t a, b;
+    int kind = -1;      // CommKind of a kComm record
+    double bus = 0.0;   // NCCL bus bytes (ring convention, cost_model.cc:97-117)
   };
   template <class F>
-  int timed(int cat, double flops, double bytes, F&& f) {
+  int timed(int cat, double flops, double bytes, F&& f, int kind = -1, double bus = 0.0) {
     if (!profiling_) return f();
     cudaEvent_t a = next_event(), b = next_event();
     record_event(a);
     const int rc = f();
     record_event(b);
-    recs_.push_back(Rec{cat, flops, bytes, a, b});
+    recs_.push_back(Rec{cat, flops, bytes, a, b, kind, bus});
     return rc;
   }
   cudaEvent_t next_event() {
@@ -430,20 +473,28 @@ class ExecutorImpl final : public Executor {
     else
       cudaEventRecord(e, stream_);
   }
-  int c_all_reduce(int g, int rank, void* buf, size_t n, DType t, cudaStream_t st) {
-    return timed(kComm, 0, 2.0 * n * dtype_bytes(t),
-                 [&] { return comm_->all_reduce(g, rank, buf, n, t, st); });
+  int c_all_reduce(int kind, int g, int rank, void* buf, size_t n, DType t, cudaStream_t st) {
+    const double d = static_cast<double>(comm_->group(g).ranks.size());
+    const double bytes = 1.0 * n * dtype_bytes(t);
+    return timed(kComm, 0, 2.0 * bytes, [&] { return comm_->all_reduce(g, rank, buf, n, t, st); },
+                 kind, 2.0 * (d - 1.0) / d * bytes);
   }
-  int c_reduce_scatter(int g, int rank, const void* a, void* b, size_t n, DType t, cudaStream_t st) {
-    return timed(kComm, 0, 1.0 * n * dtype_bytes(t) * comm_->group(g).ranks.size(),
-                 [&] { return comm_->reduce_scatter(g, rank, a, b, n, t, st); });
+  int c_reduce_scatter(int kind, int g, int rank, const void* a, void* b, size_t n, DType t,
+                       cudaStream_t st) {
+    const double d = static_cast<double>(comm_->group(g).ranks.size());
+    const double bytes = 1.0 * n * dtype_bytes(t) * d;
+    return timed(kComm, 0, bytes,
+                 [&] { return comm_->reduce_scatter(g, rank, a, b, n, t, st); }, kind,
+                 (d - 1.0) / d * bytes);
   }
-  int c_all_gather(int g, int rank, const void* a, void* b, const std::vector<size_t>& c, DType t,
-                   cudaStream_t st) {
+  int c_all_gather(int kind, int g, int rank, const void* a, void* b, const std::vector<size_t>& c,
+                   DType t, cudaStream_t st) {
     size_t n = 0;
     for (size_t x : c) n += x;
-    return timed(kComm, 0, 1.0 * n * dtype_bytes(t),
-                 [&] { return comm_->all_gather(g, rank, a, b, c, t, st); });
+    const double d = static_cast<double>(comm_->group(g).ranks.size());
+    const double bytes = 1.0 * n * dtype_bytes(t);
+    return timed(kComm, 0, bytes, [&] { return comm_->all_gather(g, rank, a, b, c, t, st); },
+                 kind, (d - 1.0) / d * bytes);
   }
   // Split-K into r.acc32 (fp32 slices [splits][M][N], summed in order by the consumer) when
   // it pays (small M*N, long K); *used = split count, 1 meaning "not split" (nothing launched).
@@ -497,6 +548,7 @@ class ExecutorImpl final : public Executor {
   std::vector<Deg> deg_;
   std::vector<Shape> shape_;
   bool sim_ = true;
+  std::string comm_kind_ = "sim";
   float p_attn_ = 0.f, p_hidden_ = 0.f;
   uint32_t thr_attn_ = 0, thr_hidden_ = 0;
   uint64_t seed_ = 1234;
@@ -505,6 +557,7 @@ class ExecutorImpl final : public Executor {
   bool forward_only_ = false;  // profiler / debugging: skip loss, backward and optimizer
   bool splitk_ = true;         // split-K for long-K / small-MN GEMMs (cfg "splitk")
   int64_t mem_cap_ = 0;  // per-rank device-byte cap (cfg "memory_cap_bytes"; 0 = none)
+  int64_t sync_timeout_ms_ = 600000;  // loss() / step(): watchdog limit (cfg "sync_timeout_ms")
   int dec0_ = -1;         // first decoder (cross-attention) layer, or -1
   bool dry_run_ = false;       // topology only: no device state (host-logic tests)
   float inv_count_ = 1.f;
@@ -621,6 +674,11 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
       }
     }
     sim_ = comm_kind == "sim" || comm_kind == "dryrun";
+    comm_kind_ = comm_kind;
+    if (comm_kind != "sim" && comm_kind != "dryrun" && comm_kind != "nccl" && comm_kind != "null") {
+      *err = "executor: comm must be sim, nccl, null or dryrun";
+      return kErrConfig;
+    }
     dry_run_ = comm_kind == "dryrun";
     p_attn_ = cfg.value("dropout_attn", 0.0f);
     p_hidden_ = cfg.value("dropout_hidden", 0.0f);
@@ -634,6 +692,7 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     forward_only_ = cfg.value("forward_only", false);
     splitk_ = cfg.value("splitk", true);
     mem_cap_ = cfg.value("memory_cap_bytes", static_cast<int64_t>(0));
+    sync_timeout_ms_ = cfg.value("sync_timeout_ms", sync_timeout_ms_);
     wgrad_stream_ = cfg.value("wgrad_stream", true);
     comm_stream_ = cfg.value("comm_stream", true);
     trace_ = cfg.value("trace", false);
@@ -778,6 +837,14 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     }
     if (sim_) {
       comm_ = make_sim_comm(world_);
+    } else if (comm_kind == "null") {
+      // per-GPU proxy: one rank's share of a world_-rank plan on this device, every
+      // collective / transfer a no-op (timing of the rank's compute only; values are junk)
+      if (local.size() != 1) {
+        *err = "executor: null comm drives exactly one local rank";
+        return kErrConfig;
+      }
+      comm_ = make_null_comm(world_);
     } else {
       if (local.size() != 1) {
         *err = "executor: nccl mode drives exactly one local rank";
@@ -787,7 +854,11 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
       std::string id(hex.size() / 2, '\0');
       for (size_t i = 0; i < id.size(); ++i)
         id[i] = static_cast<char>(std::stoi(hex.substr(2 * i, 2), nullptr, 16));
-      comm_ = make_nccl_comm(world_, local[0], id, err);
+      NcclOptions no;
+      no.min_ctas = cfg.value("nccl_min_ctas", no.min_ctas);
+      no.max_ctas = cfg.value("nccl_max_ctas", no.max_ctas);
+      no.timeout_ms = cfg.value("nccl_timeout_ms", no.timeout_ms);
+      comm_ = make_nccl_comm(world_, local[0], id, no, err);
       if (!comm_) return kErrNccl;
     }
     if (dry_run_) {
@@ -814,7 +885,8 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
         cudaStreamCreateWithPriority(&wg_, cudaStreamNonBlocking,
                                      hi_prio < lo_prio ? hi_prio + 1 : lo_prio) != cudaSuccess ||
         cudaStreamCreateWithPriority(&cs_, cudaStreamNonBlocking,
-                                     hi_prio < lo_prio ? hi_prio + 1 : lo_prio) != cudaSuccess) {
+                                     hi_prio < lo_prio ? hi_prio + 1 : lo_prio) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&pp_, cudaStreamNonBlocking, hi_prio) != cudaSuccess) {
       *err = "executor: cudaStreamCreate failed";
       return kErrCuda;
     }
@@ -1111,6 +1183,15 @@ int ExecutorImpl::allocate(RankCtx& r) {
     int64_t rows_all = 0;
     for (int mb = 0; mb < m_; ++mb) rows_all += last.acts[mb].rows;
     r.target = A.a<bf16>(rows_all * last.sh.h);
+  }
+  if (r.stage > 0) {
+    int64_t in_all = 0, rows_all = 0;
+    for (int mb = 0; mb < m_; ++mb) {
+      in_all += static_cast<int64_t>(first.acts[mb].samples) * first.sh.in_seq() * first.sh.in_h();
+      rows_all += first.acts[mb].rows;
+    }
+    r.pp_dx_send = A.a<bf16>(in_all);
+    if (!r.mem_in.empty()) r.pp_dmem_send = A.a<float>(rows_all * first.sh.h);
   }
   if (A.failed()) (void)cudaGetLastError();  // no stale error for the next caller's checks
   if (A.over_cap())
@@ -1412,7 +1493,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     } else {
       o.out = r.partial;
       GX_TRY(gemm(A.ctx, ht, false, P + L.lay.wo.off, ht, false, rows, h, ht, o));
-      return c_all_reduce(L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h,
+      return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h,
                                DType::kBF16, stream_);
     }
   }
@@ -1426,7 +1507,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
                               hidden_drop(r, 3ull * l + 1, row_off, h), stream_);
     }));
     GX_TRY(cross_fwd(r, li, mb, false));  // leaves the out-projection partial in r.partial
-    return c_all_reduce(L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h, DType::kBF16,
+    return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h, DType::kBF16,
                         stream_);
   }
   if (phase == mlp_ph) {
@@ -1505,7 +1586,7 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     }
     o.out = r.partial;
     GX_TRY(gemm(A.gel, ft, false, P + L.lay.w2.off, ft, false, rows, h, ft, o));
-    return c_all_reduce(L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h,
+    return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.partial, static_cast<size_t>(rows) * h,
                              DType::kBF16, stream_);
   }
   if (t > 1 && phase == mlp_ph + 1) {
@@ -1590,7 +1671,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       GX_TRY(gemm(dpre, ft, false, P + L.lay.w1.off, h, true, rows, h, ft, c));  // dpre W1
     }
     if (t > 1)
-      return c_all_reduce(L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
+      return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
                                stream_);
     phase = 1;
   }
@@ -1624,7 +1705,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       if (wg_active_) GX_TRY(fork(wg_, stream_));
       GX_TRY(cross_bwd_attn(r, li, mb, wgrad_ep));  // -> dc3 (TP: partial) in r.dc
       if (t > 1)
-        return c_all_reduce(L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
+        return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
                             stream_);
     }
    }
@@ -1709,7 +1790,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       }
     }
     if (t > 1)
-      return c_all_reduce(L.g_tp, r.rank, r.da, static_cast<size_t>(rows) * h, DType::kBF16,
+      return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.da, static_cast<size_t>(rows) * h, DType::kBF16,
                                stream_);
     phase = 2;
   }
@@ -1758,7 +1839,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     if (prev != nullptr) prev->dz_ready = true;
     if (s.merge) GX_TRY(merge_bwd(r, L, A, dX, wgrad_ep(L.lay.wm, 2 * h)));
     if (li == r.dec_li && t > 1)  // TP ranks hold per-head partial sums of dL/dmem
-      return c_all_reduce(L.g_tp, r.rank, r.dmem, static_cast<size_t>(rows) * h, DType::kF32,
+      return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.dmem, static_cast<size_t>(rows) * h, DType::kF32,
                           stream_);
     phase = ln1_ph + 1;
   }
@@ -1960,16 +2041,16 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
     if (wg_active_ && syncs)
       GX_TRY(cuda_check(cudaStreamWaitEvent(cst, r.wg_done[par], 0), "wgrad join"));
     if (L.d.sdp > 1)
-      return c_reduce_scatter(L.g_sdp, r.rank, L.gfull, L.gshard,
+      return c_reduce_scatter(kSdpReduceScatter, L.g_sdp, r.rank, L.gfull, L.gshard,
                                    static_cast<size_t>(L.shard_n), DType::kF32, cst);
     if (L.d.dp > 1)
-      return c_all_reduce(L.g_dp, r.rank, L.gfull, static_cast<size_t>(L.lay.total),
+      return c_all_reduce(kDpAllReduce, L.g_dp, r.rank, L.gfull, static_cast<size_t>(L.lay.total),
                                DType::kF32, cst);
     return kOk;
   }
   if (phase == 1) {
     if (L.d.sdp > 1 && L.d.dp > 1)
-      return c_all_reduce(L.g_dp, r.rank, L.gshard, static_cast<size_t>(L.shard_n),
+      return c_all_reduce(kDpAllReduce, L.g_dp, r.rank, L.gshard, static_cast<size_t>(L.shard_n),
                                DType::kF32, cst);
     return kOk;
   }
@@ -2001,7 +2082,7 @@ int ExecutorImpl::gather_params(RankCtx& r, int li, cudaStream_t st) {
   RankLayer& L = r.layers[li];
   if (L.d.sdp <= 1) return kOk;
   std::vector<size_t> counts(L.d.sdp, static_cast<size_t>(L.shard_n));
-  return c_all_gather(L.g_sdp, r.rank, L.pshard, L.pfull, counts, DType::kBF16, st);
+  return c_all_gather(kSdpAllGather, L.g_sdp, r.rank, L.pshard, L.pfull, counts, DType::kBF16, st);
 }
 
 // Forward relayout into layer li (same stage): only the all-gather case moves data.
@@ -2017,7 +2098,7 @@ int ExecutorImpl::xin_fwd(RankCtx& r, int li, int mb) {
     chunk(Pv.d, member % g_, mb, lo, hi);
     counts.push_back(static_cast<size_t>((hi - lo) * L.sh.in_seq() * L.sh.in_h()));
   }
-  return c_all_gather(L.g_xin, r.rank, p.y, L.acts[mb].in(), counts, DType::kBF16, stream_);
+  return c_all_gather(kRelayout, L.g_xin, r.rank, p.y, L.acts[mb].in(), counts, DType::kBF16, stream_);
 }
 
 // Backward relayout out of layer li: dX (gbuf[cur^1], layout li) -> dY of layer li-1 in
@@ -2050,7 +2131,7 @@ int ExecutorImpl::xin_bwd(RankCtx& r, int li, int mb) {
     chunk(L.d, member % g_, mb, lo, hi);
     counts.push_back(static_cast<size_t>((hi - lo) * seq * h));
   }
-  return c_all_gather(L.g_xin, r.rank, dX, dYp, counts, DType::kBF16, stream_);
+  return c_all_gather(kRelayout, L.g_xin, r.rank, dX, dYp, counts, DType::kBF16, stream_);
 }
 
 // Pipeline-boundary transfer lists (pure functions of the plan, shared by the executor and
@@ -2091,7 +2172,7 @@ std::vector<ExecutorImpl::Xfer> ExecutorImpl::pp_plan(int stage, int idx, int mb
 }
 
 // Forward boundary: send this stage's last layer output / receive the first layer input.
-int ExecutorImpl::pp_fwd(RankCtx& r, int mb, bool send) {
+int ExecutorImpl::pp_fwd(RankCtx& r, int mb, bool send, cudaStream_t st) {
   const RankLayer& L = send ? r.layers.back() : r.layers.front();
   const Acts& my = L.acts[mb];
   const int64_t hs = send ? static_cast<int64_t>(L.sh.seq) * L.sh.h
@@ -2100,39 +2181,58 @@ int ExecutorImpl::pp_fwd(RankCtx& r, int mb, bool send) {
     const size_t bytes = static_cast<size_t>((x.hi - x.lo) * hs) * 2;
     const int64_t off = (x.lo - my.sample0) * hs;
     if (send) {
-      GX_TRY(comm_->send(r.rank, x.peer, my.y + off, bytes, stream_));
+      GX_TRY(comm_->send(r.rank, x.peer, my.y + off, bytes, st));
     } else {
-      GX_TRY(comm_->recv(r.rank, x.peer, my.in() + off, bytes, stream_));
+      GX_TRY(comm_->recv(r.rank, x.peer, my.in() + off, bytes, st));
     }
     // decoder stages: the memory follows, same rows (decoders share data degree and shape)
     if (send && dec0_ >= 0 && r.stage >= stage_of_layer(dec0_))
-      GX_TRY(comm_->send(r.rank, x.peer, r.mem(mb) + off, bytes, stream_));
+      GX_TRY(comm_->send(r.rank, x.peer, r.mem(mb) + off, bytes, st));
     if (!send && !r.mem_in.empty())
-      GX_TRY(comm_->recv(r.rank, x.peer, r.mem_in[mb] + off, bytes, stream_));
+      GX_TRY(comm_->recv(r.rank, x.peer, r.mem_in[mb] + off, bytes, st));
   }
   return kOk;
 }
 
 // Backward boundary: send the first layer's input gradient (gbuf[cur ^ 1]) / receive the
 // last layer's output gradient into gbuf[cur].
-int ExecutorImpl::pp_bwd(RankCtx& r, int mb, bool send) {
+int ExecutorImpl::pp_bwd(RankCtx& r, int mb, bool send, cudaStream_t st) {
   const RankLayer& L = send ? r.layers.front() : r.layers.back();
   const Acts& my = L.acts[mb];
   const int64_t hs = send ? static_cast<int64_t>(L.sh.in_seq()) * L.sh.in_h()
                           : static_cast<int64_t>(L.sh.seq) * L.sh.h;
+  bf16* dx_src = nullptr;
+  float* dmem_src = nullptr;
+  if (send) {  // private per-micro-batch copies (stream_), read by the send on `st`
+    int64_t off_in = 0, off_rows = 0;
+    for (int k = 0; k < mb; ++k) {
+      off_in += static_cast<int64_t>(L.acts[k].samples) * hs;
+      off_rows += L.acts[k].rows;
+    }
+    dx_src = r.pp_dx_send + off_in;
+    if (my.samples > 0)
+      GX_TRY(cuda_check(cudaMemcpyAsync(dx_src, r.gbuf[r.cur ^ 1], static_cast<size_t>(my.samples) * hs * 2,
+                                        cudaMemcpyDeviceToDevice, stream_), "pp dx copy"));
+    if (!r.mem_in.empty()) {
+      dmem_src = r.pp_dmem_send + off_rows * L.sh.h;
+      if (my.rows > 0)
+        GX_TRY(cuda_check(cudaMemcpyAsync(dmem_src, r.dmem, static_cast<size_t>(my.rows) * L.sh.h * 4,
+                                          cudaMemcpyDeviceToDevice, stream_), "pp dmem copy"));
+    }
+  }
   for (const Xfer& x : pp_plan(r.stage, r.idx, mb, send ? 2 : 3)) {
     const size_t bytes = static_cast<size_t>((x.hi - x.lo) * hs) * 2;
     const int64_t off = (x.lo - my.sample0) * hs;
     if (send) {
-      GX_TRY(comm_->send(r.rank, x.peer, r.gbuf[r.cur ^ 1] + off, bytes, stream_));
+      GX_TRY(comm_->send(r.rank, x.peer, dx_src + off, bytes, st));
     } else {
-      GX_TRY(comm_->recv(r.rank, x.peer, r.gbuf[r.cur] + off, bytes, stream_));
+      GX_TRY(comm_->recv(r.rank, x.peer, r.gbuf[r.cur] + off, bytes, st));
     }
     // decoder stages: dL/dmemory summed over this stage's decoder layers goes back (fp32)
-    if (send && !r.mem_in.empty())
-      GX_TRY(comm_->send(r.rank, x.peer, r.dmem + off, bytes * 2, stream_));
+    if (send && dmem_src != nullptr)
+      GX_TRY(comm_->send(r.rank, x.peer, dmem_src + off, bytes * 2, st));
     if (!send && r.dmem_from_next)
-      GX_TRY(comm_->recv(r.rank, x.peer, r.dmem + off, bytes * 2, stream_));
+      GX_TRY(comm_->recv(r.rank, x.peer, r.dmem + off, bytes * 2, st));
   }
   return kOk;
 }
@@ -2205,6 +2305,7 @@ int ExecutorImpl::step_once() {
   side_used_ = false;
   wg_used_ = false;
   cs_used_ = false;
+  pp_used_ = false;
   wg_active_ = wgrad_stream_ && !profiling_;
   ls_ = stream_;
   for (auto& r : ranks_) r->wg_pending[0] = r->wg_pending[1] = false;
@@ -2227,11 +2328,7 @@ int ExecutorImpl::step_once() {
     for (int st = 0; st < P_; ++st) {
       auto R = in_stage(st);
       if (R.empty()) continue;
-      if (st > 0) {
-        GX_TRY(comm_->group_start());
-        for (RankCtx* r : R) GX_TRY(pp_fwd(*r, mb, false));
-        GX_TRY(comm_->group_end());
-      }
+      if (st > 0) GX_TRY(pp_exchange(R, mb, true, false));
       const int nl = static_cast<int>(R[0]->layers.size());
       for (int li = 0; li < nl; ++li) {
         for (RankCtx* r : R) GX_TRY(xin_fwd(*r, li, mb));
@@ -2261,11 +2358,7 @@ int ExecutorImpl::step_once() {
         for (int ph = 0; ph < phases; ++ph)
           for (RankCtx* r : R) GX_TRY(fwd_phase(*r, li, mb, ph));
       }
-      if (st + 1 < P_) {
-        GX_TRY(comm_->group_start());
-        for (RankCtx* r : R) GX_TRY(pp_fwd(*r, mb, true));
-        GX_TRY(comm_->group_end());
-      }
+      if (st + 1 < P_) GX_TRY(pp_exchange(R, mb, true, true));
     }
   }
   tmark("fwd_end", stream_);
@@ -2288,11 +2381,7 @@ int ExecutorImpl::step_once() {
                             n, inv_count_, stream_, r->loss_ws));
         }
       }
-      if (st + 1 < P_) {
-        GX_TRY(comm_->group_start());
-        for (RankCtx* r : R) GX_TRY(pp_bwd(*r, mb, false));
-        GX_TRY(comm_->group_end());
-      }
+      if (st + 1 < P_) GX_TRY(pp_exchange(R, mb, false, false));
       const int nl = static_cast<int>(R[0]->layers.size());
       for (int li = nl - 1; li >= 0; --li) {
         // SDP: the forward all-gather's copy stays resident through backward (B200 HBM
@@ -2317,9 +2406,7 @@ int ExecutorImpl::step_once() {
       }
       for (RankCtx* r : R) r->cur ^= 1;  // pp_bwd(send) / export read gbuf[cur ^ 1]
       if (st > 0) {
-        GX_TRY(comm_->group_start());
-        for (RankCtx* r : R) GX_TRY(pp_bwd(*r, mb, true));
-        GX_TRY(comm_->group_end());
+        GX_TRY(pp_exchange(R, mb, false, true));
       } else {
         for (RankCtx* r : R) {
           const RankLayer& F = r->layers.front();
@@ -2338,6 +2425,7 @@ int ExecutorImpl::step_once() {
     GX_TRY(fork(wg_, stream_));
   }
   if (cs_used_) GX_TRY(fork(cs_, stream_));  // ... and the gradient-collective stream
+  if (pp_used_) GX_TRY(fork(pp_, stream_));  // ... and the pipeline stream
   if (side_used_) {  // join the optimizer stream before the step completes
     GX_TRY(cuda_check(cudaEventRecord(join_event_, side_), "join record"));
     GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, join_event_, 0), "join wait"));
@@ -2399,6 +2487,11 @@ std::string ExecutorImpl::profile_report() const {
   double ms[kNumCats] = {}, fl[kNumCats] = {}, by[kNumCats] = {};
   int64_t n[kNumCats] = {};
   json launches = json::array();
+  static const char* kKinds[kNumCommKinds] = {"tp_all_reduce", "sdp_all_gather",
+                                              "sdp_reduce_scatter", "dp_all_reduce",
+                                              "relayout_all_gather", "pp_send_recv"};
+  double kms[kNumCommKinds] = {}, kby[kNumCommKinds] = {}, kbus[kNumCommKinds] = {};
+  int64_t kn[kNumCommKinds] = {};
   for (const Rec& r : recs_) {
     float t = 0.f;
     if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) continue;
@@ -2407,6 +2500,12 @@ std::string ExecutorImpl::profile_report() const {
     by[r.cat] += r.bytes;
     n[r.cat] += 1;
     if (r.cat == kGemm) launches.push_back({t, r.flops});
+    if (r.cat == kComm && r.kind >= 0) {
+      kms[r.kind] += t;
+      kby[r.kind] += r.bytes;
+      kbus[r.kind] += r.bus;
+      kn[r.kind] += 1;
+    }
   }
   json j;
   double total = 0;
@@ -2420,6 +2519,11 @@ std::string ExecutorImpl::profile_report() const {
   j["sum_ms"] = total;
   j["span_ms"] = span;
   j["gemm_launches"] = launches;
+  j["comm_kinds"] = json::object();
+  for (int k = 0; k < kNumCommKinds; ++k)
+    if (kn[k] > 0)
+      j["comm_kinds"][kKinds[k]] = {{"ms", kms[k]}, {"bytes", kby[k]}, {"bus_bytes", kbus[k]},
+                                    {"launches", kn[k]}};
   if (trace_ && tr_used_ > 0) {
     cudaDeviceSynchronize();
     json tl = json::array();
@@ -2433,11 +2537,38 @@ std::string ExecutorImpl::profile_report() const {
   return j.dump();
 }
 
+// Waits for the executor stream like cudaStreamSynchronize, but polls the communicators'
+// asynchronous errors meanwhile and gives up after timeout_ms: a dead or hung peer aborts the
+// communicators (NCCL kernels blocked on it return) and surfaces as GX_ERR_NCCL instead of a
+// hang (SURVEY.md §5 failure detection).
+int ExecutorImpl::sync(int64_t timeout_ms) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t e = cudaStreamQuery(stream_);
+    if (e == cudaSuccess) return kOk;
+    if (e != cudaErrorNotReady) return cuda_check(e, "executor sync");
+    if (comm_ != nullptr) {
+      const int rc = comm_->poll_async();
+      if (rc != kOk) {
+        comm_->abort();
+        return rc;
+      }
+    }
+    if (timeout_ms > 0 &&
+        std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(timeout_ms)) {
+      if (comm_ != nullptr) comm_->abort();
+      return set_error(kErrNccl, ("executor: step did not complete within " +
+                                  std::to_string(timeout_ms) + " ms (communicators aborted)").c_str());
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+}
+
 int ExecutorImpl::loss(float* out) {
   float v = 0.f;
   GX_TRY(cuda_check(cudaMemcpyAsync(&v, ranks_.front()->loss, 4, cudaMemcpyDeviceToHost, stream_),
                     "loss d2h"));
-  GX_TRY(cuda_check(cudaStreamSynchronize(stream_), "loss sync"));
+  GX_TRY(sync(sync_timeout_ms_));
   *out = v;
   return kOk;
 }
@@ -2495,7 +2626,7 @@ std::string ExecutorImpl::info() const {
   j["pp_degree"] = P_;
   j["micro_batches"] = m_;
   j["batch_size"] = B_;
-  j["comm"] = sim_ ? "sim" : "nccl";
+  j["comm"] = comm_kind_;
   j["launches_per_step"] = launches_per_step_;
   j["steps_run"] = steps_run_;
   json ranks = json::array();
@@ -2505,6 +2636,13 @@ std::string ExecutorImpl::info() const {
     jr["stage"] = r->stage;
     jr["device_bytes"] = r->arena.bytes();
     jr["memory_cap_bytes"] = r->arena.cap();
+    int64_t in_rows = 0, tgt_rows = 0;  // rows of this rank's host batch slice (load_batch)
+    for (int mb = 0; mb < m_; ++mb) {
+      if (r->stage == 0) in_rows += r->layers.front().acts[mb].samples * r->layers.front().sh.in_seq();
+      if (r->stage == P_ - 1) tgt_rows += r->layers.back().acts[mb].rows;
+    }
+    jr["input_rows"] = in_rows;
+    jr["target_rows"] = tgt_rows;
     // the planner's per-device estimate for this rank's stage (EstimateMemory, A7)
     if (plan_.contains("stages") && r->stage < static_cast<int>(plan_["stages"].size()))
       jr["plan_estimate_bytes"] = plan_["stages"][r->stage].value("peak_memory_bytes", int64_t{0});

@@ -86,6 +86,8 @@ class Executor {
   virtual int load_batch_device(const void* x_dev, const void* target_dev) = 0;
   virtual int run(bool use_graph) = 0;
   virtual int loss(float* out) = 0;
+  // stream synchronisation with communicator failure detection (timeout_ms <= 0: no limit)
+  virtual int sync(int64_t timeout_ms) = 0;
   virtual int export_output(void* host_bf16, int what) = 0;  // 0 final y, 1 input grad dx
   virtual cudaStream_t stream() const = 0;
   virtual std::string info() const = 0;

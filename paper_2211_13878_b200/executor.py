@@ -176,6 +176,10 @@ class PlanExecutor:
     def init_params(self, seed=1, std=0.02):
         _lib.check(_lib.lib().gx_exec_init_params(self._h, seed, std))
 
+    def sync(self, timeout_ms: int = 600000):
+        """Wait for the executor's stream; a communicator failure or hang raises GxError."""
+        _lib.check(_lib.lib().gx_exec_sync(self._h, int(timeout_ms)))
+
     def loss(self) -> float:
         v = ctypes.c_float()
         _lib.check(_lib.lib().gx_exec_loss(self._h, ctypes.byref(v)))
