@@ -1,26 +1,38 @@
-// attention_tc.cu — attention forward on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+// attention_tc.cu — attention forward and backward on the 5th-generation tensor cores
+// (tcgen05 + TMEM + TMA) for every attention shape of the BASELINE configs:
 //
-//   ctx = dropout(softmax(Q K^T * scale)) V        one CTA per (sample*head, 128-query tile)
+//   ctx = dropout(softmax(Q K^T * scale + bias, masked)) V
 //
-// Same contract as attention.cu's forward (ctx, lse in log2 units, 16-bit keep masks with the
-// identical Philox call -> key mapping), restated for sm_100a with the whole key range of a
-// head resident on chip (seq <= 512, head_dim 64):
-//   1. one thread issues TMA loads of Q [128 x 64], K and V [NK x 64] (NK = seq rounded up to
-//      64; rows past the sample read as finite neighbours or zero fill and are masked) into
-//      128B-swizzled smem, then tcgen05.mma S = Q K^T into TMEM columns [0, NK) (fp32);
-//   2. sixteen warps (four per TMEM lane quarter, 64-key blocks round-robin) read S back with
-//      tcgen05.ld: pass 1 row max, pass 2 exp2, row sum, Philox dropout, bf16 P written into
-//      smem in the UMMA K-major SWIZZLE_128B layout (over the dead Q/K tiles), keep bits to
-//      global for the backward;
-//   3. tcgen05.mma O = P V (V as an MN-major operand, straight from its TMA tile) into TMEM
-//      columns [0, 64), and the epilogue scales by 1/rowsum and stores bf16 ctx.
-// No online rescaling is needed: the full row of scores is in TMEM when the max is taken.
+//   * head_dim 32 / 64 / 80 (any multiple of 16 up to 80): each head row is staged as one or
+//     two 64-column SWIZZLE_128B panels by 2-D TMA boxes at column slot*hd + panel*64; the MMAs
+//     use exactly hd/16 K-steps (hd as the K dimension) or N = hd (hd as the N dimension), so
+//     the neighbouring head's columns a second panel drags in are never read;
+//   * sequences of up to 512 keys, tail-masked (ViT-Huge: 257 tokens);
+//   * short sequences (Swin's 49-token windows) packed wpt = 128 / seq per tile, with a
+//     block-diagonal mask -- one CTA attends several windows instead of idling 60% of its rows;
+//   * causal masking (decoder self-attention), Swin's shifted-window region mask (SW-MSA) and
+//     its learned relative-position bias (forward bias, backward table gradient).
+// Contract (identical to attention.cu's mma.sync kernels, which remain only for shapes outside
+// the list above): ctx bf16, lse in log2 units [batch*heads][seq], 16-bit keep masks with the
+// Philox call -> key mapping of oracle/layer_oracle.py::_attn_mask.
+//
+// Forward CTA = (tile of wpt sequences x head, 128-query block), 16 warps (four per TMEM lane
+// quarter):
+//   1. one thread issues the TMA loads of Q [128 x hd] and K, V [nk x hd] (nk = the tile's
+//      keys rounded up to 64) and tcgen05.mma S = Q K^T into TMEM columns [0, nk) (fp32);
+//   2. the 16 warps read S back with tcgen05.ld (64-key blocks round-robin over four column
+//      quarters): pass 1 row max, pass 2 exp2, row sum, Philox dropout, bf16 P written into smem
+//      in the UMMA K-major SWIZZLE_128B layout over the dead Q / K tiles, keep bits to global;
+//   3. tcgen05.mma O = P V (V as an MN-major operand straight from its TMA tile) into TMEM
+//      columns [0, hd); the epilogue scales by 1 / rowsum and stores bf16 ctx.
+// No online rescaling: the whole row of scores is in TMEM when its max is taken.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "gx_internal.h"
 #include "launch.cuh"
@@ -31,39 +43,112 @@ namespace gx {
 
 namespace {
 
-constexpr int kTcQ = 128;       // queries per CTA (UMMA M)
-constexpr int kTcHD = 64;       // head dim (one 128 B swizzle row)
-constexpr int kTcMaxKeys = 512; // TMEM columns
+constexpr int kTcQ = 128;        // queries per CTA (UMMA M)
+constexpr int kTcMaxKeys = 512;  // TMEM columns
+constexpr int kTcMaxHd = 80;     // backward TMEM budget: 256 + 3 * hd <= 512
+constexpr int kMaxSide = 8;      // relative-position tables of up to (2*8 - 1)^2 entries
+constexpr int kTabMax = (2 * kMaxSide - 1) * (2 * kMaxSide - 1);
 
-struct TcLayout {
-  int nk;          // keys rounded up to 64
-  int qk_bytes;    // Q + K tiles (P groups overlay them first)
-  int v_off;       // V tile
-  int p_hi_off;    // P groups that do not fit over Q + K
-  int p_lo_groups; // P groups placed at [0, qk_bytes)
-  int red_off;     // row max / row sum exchange [2][4][128] floats
-  int bar_off;
-  int bytes;
+// Geometry of one call, computed on the host and passed by value.
+struct Geom {
+  int hd;     // head dim (multiple of 16, <= 80)
+  int np;     // 64-column panels per head row
+  int wpt;    // attention sequences (units) per tile: 1, or 128 / seq for seq <= 64
+  int vseq;   // rows (= keys) of a tile's virtual sequence: wpt * seq
+  int nk;     // keys staged per forward CTA: vseq rounded up to 64
+  int tiles;  // ceil(batch / wpt)
+  int gmask;  // the general masked path: windows packed, causal, shifted regions or bias
 };
 
-__host__ __device__ inline TcLayout tc_layout(int seq) {
-  TcLayout L{};
-  L.nk = (seq + 63) / 64 * 64;
-  L.qk_bytes = kTcQ * 128 + L.nk * 128;
-  L.v_off = L.qk_bytes;
-  const int groups = L.nk / 64;
-  L.p_lo_groups = L.qk_bytes / (16 * 1024);
-  if (L.p_lo_groups > groups) L.p_lo_groups = groups;
-  L.p_hi_off = L.v_off + L.nk * 128;
-  const int hi = groups - L.p_lo_groups;
-  L.red_off = L.p_hi_off + hi * 16 * 1024;
-  L.bar_off = L.red_off + 8 * kTcQ * 4;  // [max | sum][4 column quarters][128 rows]
-  L.bytes = L.bar_off + 64;
+Geom make_geom(const gx_attention_args& a) {
+  Geom g{};
+  g.hd = a.head_dim;
+  g.np = (a.head_dim + 63) / 64;
+  g.wpt = a.seq <= 64 ? kTcQ / a.seq : 1;
+  g.vseq = g.wpt * a.seq;
+  g.nk = (g.vseq + 63) / 64 * 64;
+  g.tiles = (a.batch + g.wpt - 1) / g.wpt;
+  g.gmask = (g.wpt > 1 || a.causal || a.win_shift > 0 || a.rpb != nullptr) ? 1 : 0;
+  return g;
+}
+
+// Per-tile window metadata staged in smem: token (in-window) coordinates, shifted-window
+// region and the head's bias table (log2 units).
+struct WinSmem {
+  float tab[kTabMax];
+  int8_t ty[kTcQ], tx[kTcQ], reg[kTcQ];
+};
+
+// Swin shifted-window region (0..8) of token `tok` of attention sequence (window) `u`: the
+// window's position in the rolled grid gives the token's (y, x); rows / columns within
+// `side` of the far edge came from the other side of the grid (SW-MSA mask).
+__device__ __forceinline__ int swin_region_tc(const gx_attention_args& p, int u, int tok) {
+  const int nw = p.win_grid / p.win_side;
+  const int w = u % (nw * nw);
+  const int y = (w / nw) * p.win_side + tok / p.win_side;
+  const int x = (w % nw) * p.win_side + tok % p.win_side;
+  const int l0 = p.win_grid - p.win_side, l1 = p.win_grid - p.win_shift;
+  return (y < l0 ? 0 : (y < l1 ? 1 : 2)) * 3 + (x < l0 ? 0 : (x < l1 ? 1 : 2));
+}
+
+__device__ __forceinline__ void win_stage_tc(const gx_attention_args& p, const Geom& g, int vb,
+                                             int h, WinSmem* w, int nthreads) {
+  const int s = p.seq;
+  if (p.rpb != nullptr) {
+    const int n = 2 * p.rpb_side - 1;
+    const auto* t = static_cast<const __nv_bfloat16*>(p.rpb) + h * n * n;
+    for (int e = threadIdx.x; e < n * n; e += nthreads)
+      w->tab[e] = __bfloat162float(t[e]) * 1.4426950408889634f;
+  }
+  for (int v = threadIdx.x; v < kTcQ; v += nthreads) {
+    const int tok = v % s, u = vb * g.wpt + v / s;
+    w->ty[v] = static_cast<int8_t>(p.rpb_side > 0 ? tok / p.rpb_side : 0);
+    w->tx[v] = static_cast<int8_t>(p.rpb_side > 0 ? tok % p.rpb_side : 0);
+    w->reg[v] = static_cast<int8_t>(p.win_shift > 0 && v < g.vseq && u < p.batch
+                                        ? swin_region_tc(p, u, tok) : 0);
+  }
+}
+
+// Is the (virtual query, virtual key) pair attended?  (general path; both < vseq checked)
+__device__ __forceinline__ bool pair_ok(const gx_attention_args& p, const WinSmem* w, int s,
+                                        int vq, int vk) {
+  if (vq / s != vk / s) return false;  // different packed sequences
+  if (p.causal && vk % s > vq % s) return false;
+  if (p.win_shift > 0 && w->reg[vq] != w->reg[vk]) return false;
+  return true;
+}
+__device__ __forceinline__ float pair_bias(const gx_attention_args& p, const WinSmem* w, int vq,
+                                           int vk) {
+  if (p.rpb == nullptr) return 0.f;
+  const int side = p.rpb_side;
+  return w->tab[(w->ty[vq] - w->ty[vk] + side - 1) * (2 * side - 1) + (w->tx[vq] - w->tx[vk] + side - 1)];
+}
+
+// keep bit of real key kk (0..63) of a 64-key block: word (kk/2)%4, bit 2*(kk/8) + kk%2
+__device__ __forceinline__ uint32_t keep_bit(const uint32_t (&w)[4], int kk) {
+  return (w[(kk >> 1) & 3] >> (2 * (kk >> 3) + (kk & 1))) & 1u;
+}
+
+struct FwdLayout {
+  int kq, kv, p_lo, p_hi, win, red, bar, bytes;
+};
+__host__ __device__ inline FwdLayout fwd_layout(int np, int nk) {
+  FwdLayout L{};
+  L.kq = np * kTcQ * 128;
+  L.kv = L.kq + np * nk * 128;
+  const int groups = nk / 64;
+  L.p_lo = L.kv / (16 * 1024);  // P groups that fit over the dead Q + K tiles
+  if (L.p_lo > groups) L.p_lo = groups;
+  L.p_hi = L.kv + np * nk * 128;
+  L.win = L.p_hi + (groups - L.p_lo) * 16 * 1024;
+  L.red = L.win + static_cast<int>((sizeof(WinSmem) + 15) / 16 * 16);
+  L.bar = L.red + 8 * kTcQ * 4;  // [max | sum][4 column quarters][128 rows]
+  L.bytes = L.bar + 64;
   return L;
 }
 
-__device__ __forceinline__ uint32_t p_group_addr(const TcLayout& L, uint32_t base, int g) {
-  return g < L.p_lo_groups ? base + g * 16384 : base + L.p_hi_off + (g - L.p_lo_groups) * 16384;
+__device__ __forceinline__ uint32_t p_group_addr(const FwdLayout& L, uint32_t base, int g) {
+  return g < L.p_lo ? base + g * 16384 : base + L.p_hi + (g - L.p_lo) * 16384;
 }
 
 __device__ __forceinline__ unsigned long long gtimer_tc() {
@@ -94,6 +179,11 @@ __device__ __forceinline__ void st_shared_v4_tc(uint32_t addr, uint32_t a, uint3
                "r"(d)
                : "memory");
 }
+// TMA load of a 64 x 64 bf16 box of a 2-D [rows][ld] map (inner coordinate c0, row c1)
+__device__ __forceinline__ void tma_box(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                        int c1) {
+  tma_load_2d(dst, map, bar, c0, c1);
+}
 
 // 32 lanes x 16 consecutive 32-bit TMEM columns
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
@@ -112,18 +202,20 @@ constexpr int kFwdThreads = 512;  // 16 warps: four per TMEM lane quarter
 
 }  // namespace
 
-template <uint32_t kCols>
+template <uint32_t kCols, bool kGen>
 __global__ void __launch_bounds__(kFwdThreads, 1)
-    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const gx_attention_args p) {
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const gx_attention_args p,
+                       const Geom g) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-align by offsetting the shared array itself, so every access below stays in the
   // shared state space (an integer-cast pointer would compile to generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int s = p.seq;
-  const TcLayout L = tc_layout(s);
+  const FwdLayout L = fwd_layout(g.np, g.nk);
   const uint32_t sbase = smem_u32(smem);
-  float* red = reinterpret_cast<float*>(smem + L.red_off);  // [max|sum][quarter][128]
-  uint64_t* bar_qk = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+  float* red = reinterpret_cast<float*>(smem + L.red);  // [max|sum][quarter][128]
+  WinSmem* win = reinterpret_cast<WinSmem*>(smem + L.win);
+  uint64_t* bar_qk = reinterpret_cast<uint64_t*>(smem + L.bar);
   uint64_t* bar_v = bar_qk + 1;
   uint64_t* bar_s = bar_qk + 2;
   uint64_t* bar_o = bar_qk + 3;
@@ -131,11 +223,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   const int warp = static_cast<int>(warp_id());
   const int lane = static_cast<int>(lane_id());
-  const int H = p.heads;
-  const int bh = blockIdx.y;
-  const int b = bh / H, h = bh % H;
+  const int H = p.heads, hd = g.hd, nk = g.nk, np = g.np;
+  const int vb = blockIdx.y / H, h = blockIdx.y % H;
   const int q0 = blockIdx.x * kTcQ;
-  const int nk = L.nk;
+  const int row0 = vb * g.wpt * s;  // first token row of this tile's sequences
 
   if (threadIdx.x == 0) {
     tma_prefetch(&map_qkv);
@@ -157,33 +248,36 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   // ---------------------------------------------------------------- loads + S = Q K^T
   if (warp == 0) {  // warp-uniform: lane 0 issues, the rest wait here
     if (lane == 0) {
-      const int row0 = b * s;  // first token row of this sample
-      const int slot_q = h, slot_k = H + h, slot_v = 2 * H + h;
-      // 64-row boxes (128 B rows, 128B swizzle): Q 2 boxes, K and V nk/64 boxes each
-      mbar_expect_tx(bar_qk, (kTcQ + nk) * 128);
-      tma_load_3d(smem, &map_qkv, bar_qk, 0, slot_q, row0 + q0);
-      tma_load_3d(smem + 64 * 128, &map_qkv, bar_qk, 0, slot_q, row0 + q0 + 64);
-      for (int r = 0; r < nk; r += 64)
-        tma_load_3d(smem + kTcQ * 128 + r * 128, &map_qkv, bar_qk, 0, slot_k, row0 + r);
-      mbar_expect_tx(bar_v, nk * 128);
-      for (int r = 0; r < nk; r += 64)
-        tma_load_3d(smem + L.v_off + r * 128, &map_qkv, bar_v, 0, slot_v, row0 + r);
+      const int cq = h * hd, ck = (H + h) * hd, cv = (2 * H + h) * hd;  // column of each slot
+      // 64 x 64 boxes (128 B rows, 128B swizzle): Q 2 per panel, K and V nk/64 per panel
+      mbar_expect_tx(bar_qk, np * (kTcQ + nk) * 128);
+      for (int pn = 0; pn < np; ++pn) {
+        tma_box(smem + pn * kTcQ * 128, &map_qkv, bar_qk, cq + pn * 64, row0 + q0);
+        tma_box(smem + pn * kTcQ * 128 + 64 * 128, &map_qkv, bar_qk, cq + pn * 64, row0 + q0 + 64);
+        for (int r = 0; r < nk; r += 64)
+          tma_box(smem + L.kq + pn * nk * 128 + r * 128, &map_qkv, bar_qk, ck + pn * 64, row0 + r);
+      }
+      mbar_expect_tx(bar_v, np * nk * 128);
+      for (int pn = 0; pn < np; ++pn)
+        for (int r = 0; r < nk; r += 64)
+          tma_box(smem + L.kv + pn * nk * 128 + r * 128, &map_qkv, bar_v, cv + pn * 64, row0 + r);
       mbar_wait(bar_qk, 0);
       tc_fence_after();
       for (int n0 = 0; n0 < nk; n0 += 256) {
         const int n = nk - n0 < 256 ? nk - n0 : 256;
         const uint32_t idesc = idesc_bf16_f32(kTcQ, n, false, false);
-#pragma unroll
-        for (int k = 0; k < kTcHD / 16; ++k) {
-          const uint64_t ad = sdesc_sw128(sbase + k * 32, 16, 1024);
-          const uint64_t bd = sdesc_sw128(sbase + kTcQ * 128 + n0 * 128 + k * 32, 16, 1024);
-          umma_bf16(tmem + n0, ad, bd, idesc, k != 0 ? 1u : 0u);
+        for (int ks = 0; ks < hd / 16; ++ks) {
+          const int pn = ks >> 2, k = ks & 3;
+          const uint64_t ad = sdesc_sw128(sbase + pn * kTcQ * 128 + k * 32, 16, 1024);
+          const uint64_t bd = sdesc_sw128(sbase + L.kq + pn * nk * 128 + n0 * 128 + k * 32, 16, 1024);
+          umma_bf16(tmem + n0, ad, bd, idesc, ks != 0 ? 1u : 0u);
         }
       }
       umma_commit(bar_s);
     }
     __syncwarp();
   }
+  if (kGen) win_stage_tc(p, g, vb, h, win, kFwdThreads);  // visible after the barrier below
 
   // ---------------------------------------------------------------- softmax over TMEM rows
   // 16 warps: four per TMEM lane quarter; 64-key blocks go round-robin to the four column
@@ -191,48 +285,68 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   // shared), and the quarters exchange row max / row sum through shared memory.
   const int qd = warp & 3, cq = warp >> 2;
   const int r = qd * 32 + lane;  // tile row == TMEM lane
-  const int q = q0 + r;
+  const int vq = q0 + r;         // virtual query
+  const int u = vb * g.wpt + vq / s;  // its attention sequence (unit)
+  const int q = vq % s;               // real query index
+  const bool row_ok = vq < g.vseq && u < p.batch;
   const int nblk = nk / 64;
   const uint32_t trow = tmem + (static_cast<uint32_t>(qd * 32) << 16);
   const float c2 = p.scale * 1.4426950408889634f;
   mbar_wait(bar_s, 0);
   tc_fence_after();
+  if (kGen) named_sync(1, kFwdThreads);  // window metadata staged
   GX_ATTN_STAMP(p, 2);
 
-  // keys [0, lim) exist for this row: the sequence, and with a causal mask only k <= q
-  const int lim = p.causal ? (q + 1 < s ? q + 1 : s) : s;
+  // fast path: keys [0, lim) exist for this row
+  const int lim = kGen ? 0 : s;
   float mx = -INFINITY;
   for (int kb = cq; kb < nblk; kb += 4) {
+    uint32_t v[64];
+    tmem_ld32(trow + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+    tmem_ld32(trow + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+    tmem_ld_wait();
 #pragma unroll
-    for (int hb = 0; hb < 2; ++hb) {
-      const int c0 = kb * 64 + hb * 32;
-      uint32_t v[32];
-      tmem_ld32(trow + c0, v);
-      tmem_ld_wait();
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float x = c0 + j < lim ? __uint_as_float(v[j]) * c2 : -INFINITY;
-        mx = fmaxf(mx, x);
+    for (int j = 0; j < 64; ++j) {
+      const int c = kb * 64 + j;
+      float x;
+      if (kGen) {
+        x = c < g.vseq && pair_ok(p, win, s, vq, c)
+                ? __uint_as_float(v[j]) * c2 + pair_bias(p, win, vq, c) : -INFINITY;
+      } else {
+        x = c < lim ? __uint_as_float(v[j]) * c2 : -INFINITY;
       }
+      mx = fmaxf(mx, x);
     }
   }
   red[cq * kTcQ + r] = mx;
   named_sync(1, kFwdThreads);
   GX_ATTN_STAMP(p, 3);
-  const float m = fmaxf(fmaxf(red[r], red[kTcQ + r]), fmaxf(red[2 * kTcQ + r], red[3 * kTcQ + r]));
+  float m = fmaxf(fmaxf(red[r], red[kTcQ + r]), fmaxf(red[2 * kTcQ + r], red[3 * kTcQ + r]));
+  if (m == -INFINITY) m = 0.f;  // an empty row (padding) keeps finite arithmetic
 
   const uint32_t thr = p.drop_threshold;
   const float inv_keep = p.drop_scale;
   const uint64_t seed = p.seed + (p.seed_offset != nullptr ? *p.seed_offset : 0ull);
-  const int nkb = (s + 63) / 64;
+  const int nkb = (s + 63) / 64;  // real 64-key blocks per query
   const uint64_t stream =
-      (static_cast<uint64_t>(p.sample_offset + b) * p.heads_total + (p.head_offset + h)) * s;
+      (static_cast<uint64_t>(p.sample_offset + u) * p.heads_total + (p.head_offset + h)) * s;
   uint16_t* mask = static_cast<uint16_t*>(p.mask);
-  const bool row_ok = q < s;
+  const int64_t bh_real = static_cast<int64_t>(u) * H + h;
+  // packed short sequences: one 64-key real block per query, drawn once per row
+  uint32_t wrow[4] = {0u, 0u, 0u, 0u};
+  if (kGen && g.wpt > 1 && thr != 0u) {
+    const uint64_t call0 = (stream + static_cast<uint64_t>(q)) * nkb * 4;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) wrow[t] = keep16(seed, p.site, call0 + t, thr);
+    if (row_ok && cq == 0)
+      *reinterpret_cast<uint64_t*>(mask + (bh_real * s + q) * nkb * 4) =
+          static_cast<uint64_t>(wrow[0]) | (static_cast<uint64_t>(wrow[1]) << 16) |
+          (static_cast<uint64_t>(wrow[2]) << 32) | (static_cast<uint64_t>(wrow[3]) << 48);
+  }
   float sum = 0.f;
   for (int kb = cq; kb < nblk; kb += 4) {
-    uint32_t bits[4] = {0u, 0u, 0u, 0u};
-    if (thr != 0u) {
+    uint32_t bits[4] = {wrow[0], wrow[1], wrow[2], wrow[3]};
+    if (thr != 0u && g.wpt == 1) {
       const uint64_t call0 = ((stream + static_cast<uint64_t>(q)) * nkb + kb) * 4;
 #pragma unroll
       for (int t = 0; t < 4; ++t) bits[t] = keep16(seed, p.site, call0 + t, thr);
@@ -241,8 +355,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                                 (static_cast<uint64_t>(bits[1]) << 16) |
                                 (static_cast<uint64_t>(bits[2]) << 32) |
                                 (static_cast<uint64_t>(bits[3]) << 48);
-        *reinterpret_cast<uint64_t*>(mask + ((static_cast<int64_t>(bh) * s + q) * nkb + kb) * 4) =
-            packed;
+        *reinterpret_cast<uint64_t*>(mask + ((bh_real * s + q) * nkb + kb) * 4) = packed;
       }
     }
     const uint32_t g_addr = p_group_addr(L, sbase, kb) + r * 128;
@@ -257,16 +370,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int j2 = 0; j2 < 16; ++j2) {
         float e2[2];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int i = 2 * j2 + u;
-          float e = c0 + i < lim ? ex2_ftz(__uint_as_float(v[i]) * c2 - m) : 0.f;
-          sum += e;
-          if (thr != 0u) {
-            // key i of this 32-key half: word t = (i/2)%4, bit 8*hb + 2*(i/8) + i%2
-            const uint32_t bit = (bits[(i >> 1) & 3] >> (8 * hb + 2 * (i >> 3) + (i & 1))) & 1u;
-            e = bit ? e * inv_keep : 0.f;
+        for (int uu = 0; uu < 2; ++uu) {
+          const int i = 2 * j2 + uu;
+          const int c = c0 + i;
+          float e;
+          int kk;  // the key's position in its real 64-key block (dropout bit)
+          if (kGen) {
+            const bool ok = row_ok && c < g.vseq && pair_ok(p, win, s, vq, c);
+            e = ok ? ex2_ftz(__uint_as_float(v[i]) * c2 + pair_bias(p, win, vq, c) - m) : 0.f;
+            kk = g.wpt > 1 ? c % s : (c & 63);
+          } else {
+            e = c < lim ? ex2_ftz(__uint_as_float(v[i]) * c2 - m) : 0.f;
+            kk = c & 63;
           }
-          e2[u] = e;
+          sum += e;
+          if (thr != 0u) e = keep_bit(bits, kk) ? e * inv_keep : 0.f;
+          e2[uu] = e;
         }
         pk[j2] = pack_bf16(e2[0], e2[1]);
       }
@@ -290,10 +409,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (lane == 0) {
       tc_fence_after();
       mbar_wait(bar_v, 0);
-      const uint32_t idesc = idesc_bf16_f32(kTcQ, kTcHD, false, true);
+      const uint32_t idesc = idesc_bf16_f32(kTcQ, hd, false, true);
       for (int kk = 0; kk < nk / 16; ++kk) {
         const uint64_t ad = sdesc_sw128(p_group_addr(L, sbase, kk >> 2) + (kk & 3) * 32, 16, 1024);
-        const uint64_t bd = sdesc_sw128(sbase + L.v_off + kk * 2048, nk * 128, 1024);
+        // V as MN-major B (N = hd): 64-column chunks are the panels, nk * 128 B apart
+        const uint64_t bd = sdesc_sw128(sbase + L.kv + kk * 2048, nk * 128, 1024);
         umma_bf16(tmem, ad, bd, idesc, kk != 0 ? 1u : 0u);
       }
       umma_commit(bar_o);
@@ -302,20 +422,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   }
   if (cq == 0 && row_ok) {
     auto* lse = static_cast<float*>(p.lse);
-    lse[static_cast<int64_t>(bh) * s + q] = m + log2f(l);
+    lse[bh_real * s + q] = m + log2f(l);
   }
   mbar_wait(bar_o, 0);
   tc_fence_after();
   GX_ATTN_STAMP(p, 5);
-  {  // O columns [cq*16, cq*16 + 16) of this row
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  auto* ctx = static_cast<__nv_bfloat16*>(p.ctx);
+  for (int c16 = cq; c16 < hd / 16; c16 += 4) {  // O columns [16 c16, 16 c16 + 16) of this row
     uint32_t o[16];
-    tmem_ld16(trow + cq * 16, o);
+    tmem_ld16(trow + c16 * 16, o);
     tmem_ld_wait();
     if (row_ok) {
-      const float inv = 1.f / l;
-      auto* ctx = static_cast<__nv_bfloat16*>(p.ctx);
-      uint4* out = reinterpret_cast<uint4*>(ctx + (static_cast<int64_t>(b) * s + q) * p.ld_ctx +
-                                            h * kTcHD + cq * 16);
+      uint4* out = reinterpret_cast<uint4*>(ctx + (static_cast<int64_t>(row0) + vq) * p.ld_ctx +
+                                            h * hd + c16 * 16);
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         out[i] = make_uint4(pack_bf16(__uint_as_float(o[8 * i + 0]) * inv, __uint_as_float(o[8 * i + 1]) * inv),
@@ -334,41 +454,60 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 }
 
 // ------------------------------------------------------------------------------ backward
-// One CTA per (sample*head, 128-key tile); the queries stream through in 128-row chunks
-// (double-buffered TMA).  Per chunk j, with K, V of the tile resident:
-//   S^T = K Q_j^T and dPd^T = V dO_j^T                 (tcgen05, TMEM cols [0,128) / [128,256))
-//   P = exp2(S*c2 - lse), Pd = drop(P), dP = drop(dPd), dS = P (dP - D)   (thread = key row)
-//   dV += Pd^T dO_j, dK += dS^T Q_j                     (TMEM cols [256,320) / [320,384))
-//   dQ_j = dS K  (dS^T's smem tile read as an MN-major A operand) -> fp32 partial per key tile
+// One CTA per (tile x head, 128-key block); the queries stream through in 128-row chunks.
+// Per chunk j, with K, V of the key block resident:
+//   S^T = K Q_j^T and dPd^T = V dO_j^T                (tcgen05, TMEM cols [0,128) / [128,256))
+//   P = exp2(S*c2 + bias - lse), Pd = drop(P), dP = drop(dPd), dS = P (dP - D)  (thread = key)
+//   dV += Pd^T dO_j, dK += dS^T Q_j                    (TMEM cols 256 + [0, hd) / [hd, 2hd))
+//   dQ_j = dS K  (dS^T's smem tile read as an MN-major A operand) -> fp32 partial per key block
 // lse and the keep words of every query are staged in smem once; D = rowsum(dO * O) is
-// computed per chunk from the dO / O tiles in smem.  The key tiles of a head form one
-// thread-block cluster: after a cluster barrier, CTA t sums the dQ partials of query chunk t
-// over the key tiles in key-tile order, so the result is deterministic and the reduction is
-// spread over the cluster.
+// computed per chunk from the dO tile in smem and O in global memory.  The key blocks of a
+// head form one thread-block cluster: after a cluster barrier, CTA t sums the dQ partials of
+// query chunk t over the key blocks in order, so the result is deterministic.
+// Relative-position bias: the tile's fp32 dS is kept in smem and each (window, table entry)
+// sums its (q, k) pairs in a fixed order into rpb_dpart (the batch sum follows in rpb_grad).
 namespace {
 struct BwdLayout {
-  // Q and dO stream through three 16 KB buffers each (chunk j in buffer j % 3)
-  static constexpr int kK = 0, kV = 16384, kQ = 32768, kDO = 81920, kPd = 131072,
-                       kDS = 163840, kLse = 196608 /* [512] */, kD = kLse + 2048 /* [2][128] */,
-                       kMask = kD + 1024 /* [512 q][2 kb][4] u16 */, kBar = kMask + 8192,
-                       kBytes = kBar + 128;
+  int nb;  // Q / dO chunk buffers (3: prefetch two chunks ahead; 1 when smem is short)
+  int k, v, q, d_o, pd, ds, lse, dd, mask, win, ds32, bar, bytes;
 };
+__host__ __device__ inline BwdLayout bwd_layout(int np, bool rpb) {
+  BwdLayout L{};
+  L.nb = (np == 1 && !rpb) ? 3 : 1;
+  const int tile = np * kTcQ * 128;  // one 128-row head tile
+  L.k = 0;
+  L.v = L.k + tile;
+  L.q = L.v + tile;
+  L.d_o = L.q + L.nb * tile;
+  L.pd = L.d_o + L.nb * tile;
+  L.ds = L.pd + 32768;
+  L.lse = L.ds + 32768;                  // [512] floats
+  L.dd = L.lse + 2048;                   // [2][128] floats
+  L.mask = L.dd + 1024;                  // [512 q][2 blocks][4] u16
+  L.win = L.mask + 8192;
+  L.ds32 = L.win + static_cast<int>((sizeof(WinSmem) + 15) / 16 * 16);
+  L.bar = L.ds32 + (rpb ? kTcQ * kTcQ * 4 : 0);  // fp32 dS [128 q][128 k] (bias gradient)
+  L.bytes = L.bar + 128;
+  return L;
+}
 }  // namespace
 
+template <int HD, bool kGen>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv,
-                       const __grid_constant__ CUtensorMap map_do,
-                       const __grid_constant__ CUtensorMap map_o, const gx_attention_args p) {
-  using BL = BwdLayout;
+                       const __grid_constant__ CUtensorMap map_do, const gx_attention_args p,
+                       const Geom g) {
   extern __shared__ uint8_t smem_raw[];
-  // 1024-align by offsetting the shared array itself, so every access below stays in the
-  // shared state space (an integer-cast pointer would compile to generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sb = smem_u32(smem);
-  float* sLse = reinterpret_cast<float*>(smem + BL::kLse);
-  float* sD = reinterpret_cast<float*>(smem + BL::kD);
-  uint16_t* sMask = reinterpret_cast<uint16_t*>(smem + BL::kMask);  // [512 q][2 kb][4]
-  uint64_t* bar_kv = reinterpret_cast<uint64_t*>(smem + BL::kBar);
+  const bool has_rpb = kGen && p.rpb_dpart != nullptr;
+  const BwdLayout BL = bwd_layout((HD + 63) / 64, has_rpb);
+  float* sLse = reinterpret_cast<float*>(smem + BL.lse);
+  float* sD = reinterpret_cast<float*>(smem + BL.dd);
+  uint16_t* sMask = reinterpret_cast<uint16_t*>(smem + BL.mask);  // [512 q][2 kb][4]
+  WinSmem* win = reinterpret_cast<WinSmem*>(smem + BL.win);
+  float* sDs = reinterpret_cast<float*>(smem + BL.ds32);
+  uint64_t* bar_kv = reinterpret_cast<uint64_t*>(smem + BL.bar);
   uint64_t* bar_ld = bar_kv + 1;  // [3]
   uint64_t* bar_s = bar_kv + 4;
   uint64_t* bar_mm = bar_kv + 5;
@@ -377,19 +516,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   const int warp = static_cast<int>(warp_id());
   const int lane = static_cast<int>(lane_id());
-  const int s = p.seq, H = p.heads;
-  const int bh = blockIdx.y;
-  const int b = bh / H, h = bh % H;
-  const int kt = blockIdx.x;  // key tile
+  constexpr int hd = HD, np = (HD + 63) / 64;
+  const int s = p.seq, H = p.heads, NB = BL.nb;
+  const int vb = blockIdx.y / H, h = blockIdx.y % H;
+  const int kt = blockIdx.x;  // key block
   const int nkt = gridDim.x;
-  const int nq = (s + kTcQ - 1) / kTcQ;
+  const int nq = (g.vseq + kTcQ - 1) / kTcQ;
   const int nkb = (s + 63) / 64;
-  const int row0 = b * s;
+  const int row0 = vb * g.wpt * s;
+  const int tile = np * kTcQ * 128;
+  // TMEM columns (hd is a multiple of 16): S^T, dPd^T, then dV, dK, dQ -- 256 + 3 hd <= 512
+  const uint32_t t_dv = 256, t_dk = 256 + hd, t_dq = 256 + 2 * hd;
 
   if (threadIdx.x == 0) {
     tma_prefetch(&map_qkv);
     tma_prefetch(&map_do);
-    tma_prefetch(&map_o);
     mbar_init(bar_kv, 1);
     mbar_init(&bar_ld[0], 1);
     mbar_init(&bar_ld[1], 1);
@@ -409,27 +550,39 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   GX_ATTN_STAMP(p, 1);
 
   const bool is_mma_warp = warp == kBwdMmaWarp;
-  if (!is_mma_warp) {  // lse and keep words of every query of the head (once)
-    const float* lse_g = static_cast<const float*>(p.lse) + static_cast<int64_t>(bh) * s;
+  if (!is_mma_warp) {  // lse and keep words of every query of the tile (once)
+    const float* lse_g = static_cast<const float*>(p.lse);
     const uint16_t* mask_g = static_cast<const uint16_t*>(p.mask);
-    for (int q = threadIdx.x; q < s; q += kBwdSoftmax) sLse[q] = lse_g[q];
-    for (int i = threadIdx.x; i < 2 * s; i += kBwdSoftmax) {
-      const int q = i >> 1, kb = kt * 2 + (i & 1);
+    for (int v = threadIdx.x; v < g.vseq; v += kBwdSoftmax) {
+      const int u = vb * g.wpt + v / s;
+      sLse[v] = u < p.batch ? lse_g[(static_cast<int64_t>(u) * H + h) * s + v % s] : 0.f;
+    }
+    for (int i = threadIdx.x; i < 2 * g.vseq; i += kBwdSoftmax) {
+      const int v = i >> 1, u = vb * g.wpt + v / s;
+      // packed sequences: every query's keys lie in real block 0 (slot 0); else the key
+      // block's two 64-key halves
+      const int kb = g.wpt > 1 ? 0 : kt * 2 + (i & 1);
       uint64_t w = 0;
-      if (p.drop_threshold != 0u && kb < nkb)
-        w = *reinterpret_cast<const uint64_t*>(mask_g + ((static_cast<int64_t>(bh) * s + q) * nkb + kb) * 4);
+      if (p.drop_threshold != 0u && kb < nkb && u < p.batch && (g.wpt == 1 || (i & 1) == 0))
+        w = *reinterpret_cast<const uint64_t*>(
+            mask_g + (((static_cast<int64_t>(u) * H + h) * s + v % s) * nkb + kb) * 4);
       *reinterpret_cast<uint64_t*>(sMask + i * 4) = w;
     }
+    if (kGen) win_stage_tc(p, g, vb, h, win, kBwdSoftmax);
   }
 
   const int qd = warp & 3, cq = (warp >> 2) & 3;  // TMEM lane quarter, 32-column quarter
-  const int kr = qd * 32 + lane;      // key row of the tile == TMEM lane (S^T, dV, dK)
-  const int key = kt * 128 + kr;
+  const int kr = qd * 32 + lane;      // key row of the block == TMEM lane (S^T, dV, dK)
+  const int key = kt * 128 + kr;      // virtual key
+  const int ku = vb * g.wpt + key / s;  // its unit
+  const bool key_ok = key < g.vseq && ku < p.batch;
   const uint32_t trow = tmem + (static_cast<uint32_t>(qd * 32) << 16);
   const float c2 = p.scale * 1.4426950408889634f;
   const uint32_t thr = p.drop_threshold;
   const float inv_keep = p.drop_scale;
-  const int kbl = kr >> 6, kk = kr & 63;
+  // keep-word slot and bit of this key: real key kk in its 64-key block
+  const int kslot = g.wpt > 1 ? 0 : (kr >> 6);
+  const int kk = g.wpt > 1 ? key % s : (kr & 63);
   const int mt = (kk >> 1) & 3, mbit = 2 * (kk >> 3) + (kk & 1);
   float* part = static_cast<float*>(p.dq_accum);
 
@@ -437,67 +590,84 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ------------------------------------------------ producer / MMA issue (one lane)
     // Softmax warps never wait on this warp directly: it consumes bar_pds (Pd / dS stored)
     // and publishes bar_s (next scores) and bar_mm (gradient products), so the issue
-    // latency of ~30 MMAs per chunk overlaps the softmax math instead of stalling it.
+    // latency of the MMAs per chunk overlaps the softmax math instead of stalling it.
     if (lane == 0) {
       const uint32_t idesc_s = idesc_bf16_f32(kTcQ, 128, false, false);
-      const uint32_t idesc_kv = idesc_bf16_f32(128, kTcHD, false, true);
-      const uint32_t idesc_q = idesc_bf16_f32(kTcQ, kTcHD, true, true);
-      auto load_chunk = [&](int j) {  // Q_j, dO_j -> buffer j % 3
-        const int bf = j % 3;
+      const uint32_t idesc_kv = idesc_bf16_f32(128, hd, false, true);
+      const uint32_t idesc_q = idesc_bf16_f32(kTcQ, hd, true, true);
+      const int cqs = h * hd, cks = (H + h) * hd, cvs = (2 * H + h) * hd, cdo = h * hd;
+      auto load_chunk = [&](int j) {  // Q_j, dO_j -> buffer j % NB
+        const int bf = j % NB;
         const int r = row0 + j * kTcQ;
-        mbar_expect_tx(&bar_ld[bf], 2 * kTcQ * 128);
-        for (int x = 0; x < 2; ++x) {
-          tma_load_3d(smem + BL::kQ + bf * 16384 + x * 8192, &map_qkv, &bar_ld[bf], 0, h, r + 64 * x);
-          tma_load_3d(smem + BL::kDO + bf * 16384 + x * 8192, &map_do, &bar_ld[bf], 0, h, r + 64 * x);
-        }
+        mbar_expect_tx(&bar_ld[bf], 2 * tile);
+        for (int pn = 0; pn < np; ++pn)
+          for (int x = 0; x < 2; ++x) {
+            tma_box(smem + BL.q + bf * tile + pn * 16384 + x * 8192, &map_qkv, &bar_ld[bf],
+                    cqs + pn * 64, r + 64 * x);
+            tma_box(smem + BL.d_o + bf * tile + pn * 16384 + x * 8192, &map_do, &bar_ld[bf],
+                    cdo + pn * 64, r + 64 * x);
+          }
       };
       auto issue_s = [&](int j) {  // S^T = K Q_j^T, dPd^T = V dO_j^T
-        const int bf = j % 3;
-        mbar_wait(&bar_ld[bf], (j / 3) & 1);
+        const int bf = j % NB;
+        mbar_wait(&bar_ld[bf], (j / NB) & 1);
         tc_fence_after();
-        const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
-#pragma unroll
-        for (int k = 0; k < kTcHD / 16; ++k) {
-          umma_bf16(tmem, sdesc_sw128(sb + BL::kK + k * 32, 16, 1024),
-                    sdesc_sw128(q_b + k * 32, 16, 1024), idesc_s, k != 0 ? 1u : 0u);
-          umma_bf16(tmem + 128, sdesc_sw128(sb + BL::kV + k * 32, 16, 1024),
-                    sdesc_sw128(do_b + k * 32, 16, 1024), idesc_s, k != 0 ? 1u : 0u);
+        const uint32_t q_b = sb + BL.q + bf * tile, do_b = sb + BL.d_o + bf * tile;
+        for (int ks = 0; ks < hd / 16; ++ks) {
+          const uint32_t o = (ks >> 2) * 16384 + (ks & 3) * 32;
+          umma_bf16(tmem, sdesc_sw128(sb + BL.k + o, 16, 1024), sdesc_sw128(q_b + o, 16, 1024),
+                    idesc_s, ks != 0 ? 1u : 0u);
+          umma_bf16(tmem + 128, sdesc_sw128(sb + BL.v + o, 16, 1024),
+                    sdesc_sw128(do_b + o, 16, 1024), idesc_s, ks != 0 ? 1u : 0u);
         }
         umma_commit(bar_s);
       };
       auto issue_grads = [&](int j) {  // dV += Pd^T dO_j, dK += dS^T Q_j, dQ_j = dS K
-        const int bf = j % 3;
-        const uint32_t q_b = sb + BL::kQ + bf * 16384, do_b = sb + BL::kDO + bf * 16384;
+        const int bf = j % NB;
+        const uint32_t q_b = sb + BL.q + bf * tile, do_b = sb + BL.d_o + bf * tile;
 #pragma unroll
         for (int k = 0; k < kTcQ / 16; ++k) {
           const uint32_t a_kmaj = (k >> 2) * 16384 + (k & 3) * 32;
           const uint32_t acc = (j > 0 || k > 0) ? 1u : 0u;
-          umma_bf16(tmem + 256, sdesc_sw128(sb + BL::kPd + a_kmaj, 16, 1024),
+          // MN-major B operands (N = hd): the 64-column chunks are the panels, 16 KB apart
+          umma_bf16(tmem + t_dv, sdesc_sw128(sb + BL.pd + a_kmaj, 16, 1024),
                     sdesc_sw128(do_b + k * 2048, 16384, 1024), idesc_kv, acc);
-          umma_bf16(tmem + 320, sdesc_sw128(sb + BL::kDS + a_kmaj, 16, 1024),
+          umma_bf16(tmem + t_dk, sdesc_sw128(sb + BL.ds + a_kmaj, 16, 1024),
                     sdesc_sw128(q_b + k * 2048, 16384, 1024), idesc_kv, acc);
-          umma_bf16(tmem + 384, sdesc_sw128(sb + BL::kDS + k * 2048, 16384, 1024),
-                    sdesc_sw128(sb + BL::kK + k * 2048, 16384, 1024), idesc_q, k > 0 ? 1u : 0u);
+          umma_bf16(tmem + t_dq, sdesc_sw128(sb + BL.ds + k * 2048, 16384, 1024),
+                    sdesc_sw128(sb + BL.k + k * 2048, 16384, 1024), idesc_q, k > 0 ? 1u : 0u);
         }
         umma_commit(bar_mm);
       };
-      mbar_expect_tx(bar_kv, 2 * kTcQ * 128);
-      for (int x = 0; x < 2; ++x) {
-        tma_load_3d(smem + BL::kK + x * 8192, &map_qkv, bar_kv, 0, H + h, row0 + kt * 128 + 64 * x);
-        tma_load_3d(smem + BL::kV + x * 8192, &map_qkv, bar_kv, 0, 2 * H + h, row0 + kt * 128 + 64 * x);
-      }
-      for (int j = 0; j < nq && j < 3; ++j) load_chunk(j);
+      mbar_expect_tx(bar_kv, 2 * tile);
+      for (int pn = 0; pn < np; ++pn)
+        for (int x = 0; x < 2; ++x) {
+          tma_box(smem + BL.k + pn * 16384 + x * 8192, &map_qkv, bar_kv, cks + pn * 64,
+                  row0 + kt * 128 + 64 * x);
+          tma_box(smem + BL.v + pn * 16384 + x * 8192, &map_qkv, bar_kv, cvs + pn * 64,
+                  row0 + kt * 128 + 64 * x);
+        }
+      for (int j = 0; j < nq && j < NB; ++j) load_chunk(j);
       mbar_wait(bar_kv, 0);
       issue_s(0);
       for (int j = 0; j < nq; ++j) {
         mbar_wait(bar_pds, j & 1);  // Pd / dS(j) in smem; S / dPd(j) and dQ(j-1) out of TMEM
         tc_fence_after();
-        if (j + 1 < nq) issue_s(j + 1);  // next scores first ...
-        if (j >= 1) {  // chunk j-1's gradients (at most one bar_mm phase is ever pending here)
-          mbar_wait(bar_mm, (j - 1) & 1);
-          if (j + 2 < nq) load_chunk(j + 2);  // ... its Q / dO buffer takes chunk j + 2
+        if (NB == 3) {
+          if (j + 1 < nq) issue_s(j + 1);  // next scores first ...
+          if (j >= 1) {  // chunk j-1's gradients (at most one bar_mm phase is ever pending here)
+            mbar_wait(bar_mm, (j - 1) & 1);
+            if (j + 2 < nq) load_chunk(j + 2);  // ... its Q / dO buffer takes chunk j + 2
+          }
+          issue_grads(j);                     // ... then this chunk's gradient products
+        } else {  // one buffer: chunk j's products finish before chunk j + 1 loads into it
+          issue_grads(j);
+          if (j + 1 < nq) {
+            mbar_wait(bar_mm, j & 1);
+            load_chunk(j + 1);
+            issue_s(j + 1);
+          }
         }
-        issue_grads(j);                   // ... then this chunk's gradient products
       }
     }
     __syncwarp();
@@ -505,22 +675,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // ------------------------------------------------------------ softmax warps (0..15)
     // D = rowsum(dO * O) of chunk j's 128 queries -> sD[j & 1] (dO from smem, O from global)
     auto compute_d = [&](int j) {
-      const int bf = j % 3;
-      mbar_wait(&bar_ld[bf], (j / 3) & 1);
+      const int bf = j % NB;
+      mbar_wait(&bar_ld[bf], (j / NB) & 1);
       const int qi = threadIdx.x >> 2, part4 = threadIdx.x & 3;  // 4 threads per query row
-      const int q = j * kTcQ + qi;
-      const uint8_t* dob = smem + BL::kDO + bf * 16384 + qi * 128;
+      const int v = j * kTcQ + qi;
+      const uint8_t* dob = smem + BL.d_o + bf * tile + qi * 128;
       float acc = 0.f;
-      if (q < s) {
-        const uint4* og = reinterpret_cast<const uint4*>(
-            static_cast<const __nv_bfloat16*>(p.ctx) + (static_cast<int64_t>(row0) + q) * p.ld_ctx +
-            h * kTcHD + part4 * 16);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int cc = part4 * 2 + c;
-          const int sw = (cc ^ (qi & 7)) << 4;
-          const uint4 a = *reinterpret_cast<const uint4*>(dob + sw);
-          const uint4 o = og[c];
+      if (v < g.vseq && vb * g.wpt + v / s < p.batch) {
+        const __nv_bfloat16* og = static_cast<const __nv_bfloat16*>(p.ctx) +
+                                  (static_cast<int64_t>(row0) + v) * p.ld_ctx + h * hd;
+        for (int cc = part4; cc < hd / 8; cc += 4) {  // 8-column chunks
+          const int sw = ((cc & 7) ^ (qi & 7)) << 4;
+          const uint4 a = *reinterpret_cast<const uint4*>(dob + (cc >> 3) * 16384 + sw);
+          const uint4 o = *reinterpret_cast<const uint4*>(og + cc * 8);
           const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, ow[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
           for (int t = 0; t < 4; ++t)
@@ -531,19 +698,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       acc += __shfl_xor_sync(0xffffffff, acc, 2);
       if (part4 == 0) sD[(j & 1) * kTcQ + qi] = acc;
     };
-    // dQ_j partial (fp32) out of TMEM (lane = query row of the chunk, 16 columns per warp)
+    // dQ_j partial (fp32) out of TMEM (lane = query row of the chunk, 16 columns per load)
     auto store_dq = [&](int j) {
-      uint32_t o[16];
-      tmem_ld16(trow + 384 + cq * 16, o);
-      tmem_ld_wait();
-      const int q = j * kTcQ + kr;
-      if (q < s) {
-        float4* dst = reinterpret_cast<float4*>(
-            part + ((static_cast<int64_t>(kt) * gridDim.y + bh) * s + q) * kTcHD + cq * 16);
+      const int v = j * kTcQ + kr;
+      for (int c16 = cq; c16 < hd / 16; c16 += 4) {
+        uint32_t o[16];
+        tmem_ld16(trow + t_dq + c16 * 16, o);
+        tmem_ld_wait();
+        if (v < g.vseq) {
+          float4* dst = reinterpret_cast<float4*>(
+              part + ((static_cast<int64_t>(kt) * gridDim.y + blockIdx.y) * g.vseq + v) * hd + c16 * 16);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
-                               __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
+                                 __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
+        }
       }
     };
     compute_d(0);
@@ -554,12 +723,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_after();
       GX_ATTN_STAMP(p, 4 + 5 * j);
       const int c0 = cq * 32;
-      const int qg0 = j * kTcQ + c0;
+      const int qg0 = j * kTcQ + c0;  // first virtual query of this warp's 32
       const float* sDj = sD + (j & 1) * kTcQ;
       uint32_t ppd[16], pds[16];
       {
-        // no tail / causal masking needed for this 32-query x 128-key block
-        const bool full = qg0 + 32 <= s && kt * 128 + 128 <= s && (!p.causal || kt * 128 + 127 <= qg0);
+        // no masking needed for this 32-query x 128-key block
+        const bool full = !kGen && qg0 + 32 <= s && kt * 128 + 128 <= s;
         uint32_t sv[32], dv[32];
         tmem_ld32(trow + c0, sv);
         tmem_ld32(trow + 128 + c0, dv);
@@ -574,13 +743,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int t = 0; t < 4; ++t) {
             const int i = 4 * i4 + t;
             const int qg = qg0 + i;
-            const bool valid = full || ((qg < s) && (key < s) && !(p.causal && key > qg));
-            const float pr = valid ? ex2_ftz(__uint_as_float(sv[i]) * c2 - lv[t]) : 0.f;
+            bool valid;
+            float bias = 0.f;
+            if (kGen) {
+              valid = key_ok && qg < g.vseq && pair_ok(p, win, s, qg, key);
+              if (valid) bias = pair_bias(p, win, qg, key);
+            } else {
+              valid = full || (qg < s && key < s);
+            }
+            const float pr = valid ? ex2_ftz(__uint_as_float(sv[i]) * c2 + bias - lv[t]) : 0.f;
             float f = 1.f;  // dropout factor: inv_keep or 0
             if (thr != 0u)
-              f = valid && ((sMask[(qg * 2 + kbl) * 4 + mt] >> mbit) & 1u) != 0u ? inv_keep : 0.f;
+              f = valid && ((sMask[(qg * 2 + kslot) * 4 + mt] >> mbit) & 1u) != 0u ? inv_keep : 0.f;
             pd4[t] = pr * f;
             ds4[t] = pr * (__uint_as_float(dv[i]) * f - dd[t]);
+            if (has_rpb) sDs[qg * kTcQ + kr] = ds4[t];
           }
           ppd[2 * i4] = pack_bf16(pd4[0], pd4[1]);
           ppd[2 * i4 + 1] = pack_bf16(pd4[2], pd4[3]);
@@ -601,9 +778,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const uint32_t sw = static_cast<uint32_t>((chunk0 + i) ^ (kr & 7)) << 4;
-          st_shared_v4_tc(sb + BL::kPd + rowoff + sw, ppd[4 * i], ppd[4 * i + 1], ppd[4 * i + 2],
+          st_shared_v4_tc(sb + BL.pd + rowoff + sw, ppd[4 * i], ppd[4 * i + 1], ppd[4 * i + 2],
                           ppd[4 * i + 3]);
-          st_shared_v4_tc(sb + BL::kDS + rowoff + sw, pds[4 * i], pds[4 * i + 1], pds[4 * i + 2],
+          st_shared_v4_tc(sb + BL.ds + rowoff + sw, pds[4 * i], pds[4 * i + 1], pds[4 * i + 2],
                           pds[4 * i + 3]);
         }
       }
@@ -614,24 +791,42 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // sD is double-buffered: sD[(j+1) & 1] was last read in chunk j-1, before every softmax
       // warp passed the barrier that ended chunk j-1
       if (j + 1 < nq) compute_d(j + 1);
-      named_sync(1, kBwdSoftmax);  // sD(j+1) visible
+      named_sync(1, kBwdSoftmax);  // sD(j+1) visible (and, last chunk, the fp32 dS tile)
       GX_ATTN_STAMP(p, 8 + 5 * j);
+    }
+    if (has_rpb) {
+      // each (window of the tile, bias-table entry e) sums dS over its (q, k) pairs at
+      // relative offset e in a fixed order (vseq <= 128: one key block, one query chunk)
+      const int side = p.rpb_side, n = 2 * side - 1;
+      for (int task = threadIdx.x; task < g.wpt * n * n; task += kBwdSoftmax) {
+        const int wl = task / (n * n), e = task % (n * n);
+        const int u = vb * g.wpt + wl;
+        if (u >= p.batch) continue;
+        const int dy = e / n - (side - 1), dx = e % n - (side - 1);
+        float acc = 0.f;
+        for (int qi = 0; qi < s; ++qi) {
+          const int yk = qi / side - dy, xk = qi % side - dx;
+          if (yk >= 0 && yk < side && xk >= 0 && xk < side)
+            acc += sDs[(wl * s + qi) * kTcQ + wl * s + yk * side + xk];
+        }
+        static_cast<float*>(p.rpb_dpart)[(static_cast<int64_t>(u) * H + h) * n * n + e] = acc;
+      }
     }
     mbar_wait(bar_mm, (nq - 1) & 1);
     tc_fence_after();
     store_dq(nq - 1);
     // dK (x scale), dV -> bf16 rows of dqkv
-    {
+    auto* dqkv = static_cast<__nv_bfloat16*>(p.dqkv);
+    __nv_bfloat16* rowp = dqkv + (static_cast<int64_t>(row0) + key) * p.ld_qkv;
+    const float sc = p.scale;
+    for (int c16 = cq; c16 < hd / 16; c16 += 4) {
       uint32_t dvv[16], dkv[16];
-      tmem_ld16(trow + 256 + cq * 16, dvv);
-      tmem_ld16(trow + 320 + cq * 16, dkv);
+      tmem_ld16(trow + t_dv + c16 * 16, dvv);
+      tmem_ld16(trow + t_dk + c16 * 16, dkv);
       tmem_ld_wait();
-      if (key < s) {
-        auto* dq = static_cast<__nv_bfloat16*>(p.dqkv);
-        __nv_bfloat16* rowp = dq + (static_cast<int64_t>(row0) + key) * p.ld_qkv;
-        uint4* dvp = reinterpret_cast<uint4*>(rowp + (2 * H + h) * kTcHD + cq * 16);
-        uint4* dkp = reinterpret_cast<uint4*>(rowp + (H + h) * kTcHD + cq * 16);
-        const float sc = p.scale;
+      if (key_ok) {
+        uint4* dvp = reinterpret_cast<uint4*>(rowp + (2 * H + h) * hd + c16 * 16);
+        uint4* dkp = reinterpret_cast<uint4*>(rowp + (H + h) * hd + c16 * 16);
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           dvp[i] = make_uint4(pack_bf16(__uint_as_float(dvv[8 * i]), __uint_as_float(dvv[8 * i + 1])),
@@ -647,8 +842,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   }
   tc_fence_before();
-  // every key tile's dQ partials are in global memory after the cluster barrier; CTA kt then
-  // owns query chunk kt and sums its partials in key-tile order
+  // every key block's dQ partials are in global memory after the cluster barrier; CTA kt then
+  // owns query chunk kt and sums its partials in key-block order
   GX_ATTN_STAMP(p, 25);
   __threadfence();
   cluster_sync();
@@ -656,19 +851,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   {
     auto* dq = static_cast<__nv_bfloat16*>(p.dqkv);
     const float sc = p.scale;
-    const int q_lo = kt * kTcQ, q_hi = min(s, q_lo + kTcQ);
+    const int q_lo = kt * kTcQ, q_hi = min(g.vseq, q_lo + kTcQ);
+    const int c8n = hd / 8;
 #pragma unroll 4
-    for (int idx = threadIdx.x; idx < (q_hi - q_lo) * (kTcHD / 8); idx += kBwdThreads) {
-      const int q = q_lo + idx / (kTcHD / 8), c8 = idx % (kTcHD / 8);
+    for (int idx = threadIdx.x; idx < (q_hi - q_lo) * c8n; idx += kBwdThreads) {
+      const int v = q_lo + idx / c8n, c8 = idx % c8n;
+      if (vb * g.wpt + v / s >= p.batch) continue;
       float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       for (int t = 0; t < nkt; ++t) {
         const float4* src = reinterpret_cast<const float4*>(
-            part + ((static_cast<int64_t>(t) * gridDim.y + bh) * s + q) * kTcHD + c8 * 8);
+            part + ((static_cast<int64_t>(t) * gridDim.y + blockIdx.y) * g.vseq + v) * hd + c8 * 8);
         const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
         a[0] += x0.x; a[1] += x0.y; a[2] += x0.z; a[3] += x0.w;
         a[4] += x1.x; a[5] += x1.y; a[6] += x1.z; a[7] += x1.w;
       }
-      *reinterpret_cast<uint4*>(dq + (static_cast<int64_t>(row0) + q) * p.ld_qkv + h * kTcHD + c8 * 8) =
+      *reinterpret_cast<uint4*>(dq + (static_cast<int64_t>(row0) + v) * p.ld_qkv + h * hd + c8 * 8) =
           make_uint4(pack_bf16(a[0] * sc, a[1] * sc), pack_bf16(a[2] * sc, a[3] * sc),
                      pack_bf16(a[4] * sc, a[5] * sc), pack_bf16(a[6] * sc, a[7] * sc));
     }
@@ -697,82 +894,99 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn_tc() {
   return fn;
 }
 
-bool attention_tc_supported(const gx_attention_args& a) {
-  static const bool on = [] {
-    const char* e = std::getenv("GX_ATTN_TC");
-    return e == nullptr || e[0] != '0';
-  }();
-  return on && a.head_dim == kTcHD && a.seq >= 1 && a.seq <= kTcMaxKeys && a.win_shift == 0 && a.rpb == nullptr &&
-         (a.ld_qkv % 8) == 0 && (reinterpret_cast<uintptr_t>(a.qkv) % 16) == 0 &&
-         (a.ld_ctx % 8) == 0;
-}
-
-int attention_fwd_tc(const gx_attention_args& a, cudaStream_t st) {
-  auto fn = encode_fn_tc();
-  if (fn == nullptr) return set_error(kErrCuda, "attention_tc: no cuTensorMapEncodeTiled");
-  // qkv viewed as [rows][3*heads slots][64]: one 3-D map serves Q, K and V of every head
-  CUtensorMap map;
-  const uint64_t rows = static_cast<uint64_t>(a.batch) * a.seq;
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(kTcHD), static_cast<cuuint64_t>(3 * a.heads), rows};
-  cuuint64_t strides[2] = {kTcHD * 2, static_cast<cuuint64_t>(a.ld_qkv) * 2};
-  cuuint32_t box[3] = {kTcHD, 1, 64};
-  cuuint32_t estr[3] = {1, 1, 1};
-  const int nk = (a.seq + 63) / 64 * 64;
-  CUresult rc = fn(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a.qkv), dims,
-                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (rc != CUDA_SUCCESS) return set_error(kErrCuda, "attention_tc: tensor map encode failed");
-  const TcLayout L = tc_layout(a.seq);
-  const int smem = L.bytes + 1024;
-  dim3 grid((a.seq + kTcQ - 1) / kTcQ, a.batch * a.heads);
-#define GX_ATTN_TC(C)                                                                      \
-  {                                                                                        \
-    static bool set = false;                                                               \
-    if (!set) {                                                                            \
-      cudaFuncSetAttribute(attn_fwd_tc_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           227 * 1024);                                                    \
-      set = true;                                                                          \
-    }                                                                                      \
-    launch_k(attn_fwd_tc_kernel<C>, grid, dim3(kFwdThreads), smem, st, map, a);             \
-  }
-  if (nk <= 64) GX_ATTN_TC(64)
-  else if (nk <= 128) GX_ATTN_TC(128)
-  else if (nk <= 256) GX_ATTN_TC(256)
-  else GX_ATTN_TC(512)
-#undef GX_ATTN_TC
-  return check_launch("attn_fwd_tc_kernel");
-}
-
-
-static bool make_head_map(CUtensorMap* map, const void* base, int slots, uint64_t rows, int64_t ld) {
+// 2-D [rows][ld] bf16 map, 64 x 64 boxes, 128 B swizzle (columns past ld / rows past the end
+// read as zero)
+static bool make_map_2d(CUtensorMap* map, const void* base, uint64_t ld, uint64_t rows) {
   auto fn = encode_fn_tc();
   if (fn == nullptr) return false;
-  cuuint64_t dims[3] = {static_cast<cuuint64_t>(kTcHD), static_cast<cuuint64_t>(slots), rows};
-  cuuint64_t strides[2] = {kTcHD * 2, static_cast<cuuint64_t>(ld) * 2};
-  cuuint32_t box[3] = {kTcHD, 1, 64};
-  cuuint32_t estr[3] = {1, 1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+  cuuint32_t box[2] = {64, 64};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int attention_bwd_tc(const gx_attention_args& a, cudaStream_t st) {
+bool attention_tc_supported(const gx_attention_args& a) {
+  if (a.head_dim % 16 != 0 || a.head_dim < 32 || a.head_dim > kTcMaxHd || a.seq < 1 ||
+      a.batch < 1)
+    return false;
+  const Geom g = make_geom(a);
+  if (g.nk > kTcMaxKeys) return false;
+  if (fwd_layout(g.np, g.nk).bytes + 1024 > 227 * 1024) return false;
+  if (a.rpb != nullptr && (a.seq > 64 || a.rpb_side < 1 || a.rpb_side > kMaxSide ||
+                           a.rpb_side * a.rpb_side != a.seq))
+    return false;
+  if (a.win_shift > 0 && a.seq > 64) return false;
+  if (g.gmask && g.vseq > kTcQ && g.wpt > 1) return false;
+  return (a.ld_qkv % 8) == 0 && (a.ld_ctx % 8) == 0 &&
+         (reinterpret_cast<uintptr_t>(a.qkv) % 16) == 0 &&
+         (reinterpret_cast<uintptr_t>(a.ctx) % 16) == 0;
+}
+
+int attention_fwd_tc(const gx_attention_args& a, cudaStream_t st) {
+  const Geom g = make_geom(a);
+  CUtensorMap map;
   const uint64_t rows = static_cast<uint64_t>(a.batch) * a.seq;
-  CUtensorMap mq, md, mo;
-  if (!make_head_map(&mq, a.qkv, 3 * a.heads, rows, a.ld_qkv) ||
-      !make_head_map(&md, a.dctx, a.heads, rows, a.ld_ctx) ||
-      !make_head_map(&mo, a.ctx, a.heads, rows, a.ld_ctx))
+  if (!make_map_2d(&map, a.qkv, a.ld_qkv, rows))
     return set_error(kErrCuda, "attention_tc: tensor map encode failed");
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(attn_bwd_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         BwdLayout::kBytes + 1024);
-    set = true;
+  const int smem = fwd_layout(g.np, g.nk).bytes + 1024;
+  dim3 grid((g.vseq + kTcQ - 1) / kTcQ, g.tiles * a.heads);
+#define GX_ATTN_TC(C, G)                                                                     \
+  {                                                                                          \
+    static bool set = false;                                                                 \
+    if (!set) {                                                                              \
+      cudaFuncSetAttribute(attn_fwd_tc_kernel<C, G>,                                         \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);         \
+      set = true;                                                                            \
+    }                                                                                        \
+    launch_k(attn_fwd_tc_kernel<C, G>, grid, dim3(kFwdThreads), smem, st, map, a, g);        \
   }
-  dim3 grid((a.seq + 127) / 128, a.batch * a.heads);
-  // the key tiles of one head form a cluster (dQ reduction after a cluster barrier)
-  launch_k_cluster(attn_bwd_tc_kernel, grid, dim3(kBwdThreads), BwdLayout::kBytes + 1024, st,
-                   static_cast<unsigned>(grid.x), mq, md, mo, a);
+  if (g.gmask) {
+    if (g.nk <= 128) GX_ATTN_TC(128, true)
+    else if (g.nk <= 256) GX_ATTN_TC(256, true)
+    else GX_ATTN_TC(512, true)
+  } else {
+    if (g.nk <= 128) GX_ATTN_TC(128, false)
+    else if (g.nk <= 256) GX_ATTN_TC(256, false)
+    else GX_ATTN_TC(512, false)
+  }
+#undef GX_ATTN_TC
+  return check_launch("attn_fwd_tc_kernel");
+}
+
+int attention_bwd_tc(const gx_attention_args& a, cudaStream_t st) {
+  const Geom g = make_geom(a);
+  if (a.rpb_dpart != nullptr && g.vseq > kTcQ)
+    return set_error(kErrConfig, "attention_tc: bias gradient needs sequences of <= 128 rows");
+  const uint64_t rows = static_cast<uint64_t>(a.batch) * a.seq;
+  CUtensorMap mq, md;
+  if (!make_map_2d(&mq, a.qkv, a.ld_qkv, rows) || !make_map_2d(&md, a.dctx, a.ld_ctx, rows))
+    return set_error(kErrCuda, "attention_tc: tensor map encode failed");
+  const int smem = bwd_layout(g.np, a.rpb_dpart != nullptr).bytes + 1024;
+  dim3 grid((g.vseq + 127) / 128, g.tiles * a.heads);
+  // the key blocks of one tile x head form a cluster (dQ reduction after a cluster barrier)
+#define GX_ATTN_BWD(D, G)                                                                    \
+  {                                                                                          \
+    static bool set = false;                                                                 \
+    if (!set) {                                                                              \
+      cudaFuncSetAttribute(attn_bwd_tc_kernel<D, G>,                                         \
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);         \
+      set = true;                                                                            \
+    }                                                                                        \
+    launch_k_cluster(attn_bwd_tc_kernel<D, G>, grid, dim3(kBwdThreads), smem, st,            \
+                     static_cast<unsigned>(grid.x), mq, md, a, g);                           \
+  }
+  const bool gen = g.gmask || a.rpb_dpart != nullptr;
+  switch (a.head_dim) {
+    case 32: if (gen) GX_ATTN_BWD(32, true) else GX_ATTN_BWD(32, false) break;
+    case 48: if (gen) GX_ATTN_BWD(48, true) else GX_ATTN_BWD(48, false) break;
+    case 64: if (gen) GX_ATTN_BWD(64, true) else GX_ATTN_BWD(64, false) break;
+    case 80: if (gen) GX_ATTN_BWD(80, true) else GX_ATTN_BWD(80, false) break;
+    default: return set_error(kErrConfig, "attention_tc: backward head_dim must be 32, 48, 64 or 80");
+  }
+#undef GX_ATTN_BWD
   return check_launch("attn_bwd_tc_kernel");
 }
 

@@ -169,8 +169,9 @@ def attention_bwd(qkv, ctx, lse, dctx, batch, seq, heads, head_dim, p=0.0, seed=
     dqkv = torch.zeros_like(qkv)
     # fp32 dQ partials (one slice per 128-key tile on the tcgen05 path) and D / ticket words
     # (zero-initialised: the tcgen05 path keeps per-head tickets there)
-    dq_acc = torch.empty(((seq + 127) // 128) * batch * heads * seq * head_dim, device=qkv.device,
-                         dtype=torch.float32)
+    # (short sequences are packed 128 // seq per tile: one spare sequence of slack)
+    dq_acc = torch.empty(((seq + 127) // 128) * (batch + 1) * heads * seq * head_dim,
+                         device=qkv.device, dtype=torch.float32)
     dsum = torch.zeros(batch * heads * seq, device=qkv.device, dtype=torch.float32)
     a = _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, **kw)
     a.ctx, a.ld_ctx, a.lse = _ptr(ctx), ctx.stride(0), _ptr(lse)

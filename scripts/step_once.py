@@ -7,7 +7,8 @@ from paper_2211_13878_b200 import executor as gxe  # noqa: E402
 import bench  # noqa: E402
 
 W = int(os.environ.get("WARMUP", "2"))
-model, plan, _ = bench.choose_plan(1, 16.0, os.environ.get("MODEL", "bert-huge-32"))
+from paper_2211_13878_b200 import planner  # noqa: E402
+model, plan, _ = bench.search(planner.api(), os.environ.get("MODEL", "bert-huge-32"), 1, 16.0)
 sh = model["layers"][0]["shape"]
 x = torch.randn(plan["batch_size"] * sh["seq"], sh["hidden"]).to(torch.bfloat16)
 ex = gxe.PlanExecutor(plan, model, 1, dropout_attn=0.1, dropout_hidden=0.1)
