@@ -226,12 +226,22 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
                "r"(src), "r"(c0), "r"(c1)
                : "memory");
 }
-__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, uint32_t src, int32_t c0,
-                                                  int32_t c1) {
+// Output stores go through a 3-D map {cols, M, slices}: the slice coordinate is the split-K
+// index, so a 32-row block that straddles row M is clipped at its own slice's end instead of
+// spilling into the next slice's first rows.
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, uint32_t src, int32_t c0,
+                                             int32_t c1, int32_t c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* map, uint32_t src, int32_t c0,
+                                                  int32_t c1, int32_t c2) {
   asm volatile(
-      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+      "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
           reinterpret_cast<uint64_t>(map)),
-      "r"(src), "r"(c0), "r"(c1)
+      "r"(src), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_2d_u32(uint32_t dst, const CUtensorMap* map, uint32_t bar,
@@ -308,7 +318,7 @@ __device__ __forceinline__ void epi_stage_bias(const GemmEpilogue& ep, const Epi
 __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUtensorMap* map_out,
                                                const CUtensorMap* map_aux, EpiWarp& w,
                                                bool has_in, int cb, int64_t m_base,
-                                               int32_t store_row, int n0, int M, int N,
+                                               int32_t store_z, int n0, int M, int N,
                                                const uint32_t (&acc)[32]) {
   const uint32_t lane = lane_id();
   const int64_t row = m_base + lane;
@@ -360,9 +370,9 @@ __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUt
   if (dstamp) ep.trace[blockIdx.x * 16 + 14] = gtimer();
   if (lane == 0) {
     if (ep.out_kind == kOutF32Accumulate) {
-      tma_reduce_add_2d(map_out, obuf, n0, store_row);
+      tma_reduce_add_3d(map_out, obuf, n0, static_cast<int32_t>(m_base), store_z);
     } else {
-      tma_store_2d(map_out, obuf, n0, store_row);
+      tma_store_3d(map_out, obuf, n0, static_cast<int32_t>(m_base), store_z);
     }
     if (ep.gelu) tma_store_2d(map_aux, abuf, n0, static_cast<int32_t>(m_base));
     bulk_commit();
@@ -386,7 +396,7 @@ template <int BN>
 __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const CUtensorMap* map_out,
                                               const CUtensorMap* map_aux, EpiWarp& w, int ew,
                                               bool has_in, uint32_t taddr, int64_t m_base,
-                                              int32_t store_row, int n0, int M, int N) {
+                                              int32_t store_z, int n0, int M, int N) {
   int c_lo, c_hi;
   epilogue_chunks<BN>(ew, &c_lo, &c_hi);
 #pragma unroll 1
@@ -401,7 +411,7 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const CUte
     tmem_ld_wait();
     if (stamp) ep.trace[blockIdx.x * 16 + 9 + 2 * (c - c_lo)] = gtimer();
     if (m_base < M && n0 + c * 32 < N) {
-      epilogue_block(ep, map_out, map_aux, w, has_in, c - c_lo, m_base, store_row, n0 + c * 32, M,
+      epilogue_block(ep, map_out, map_aux, w, has_in, c - c_lo, m_base, store_z, n0 + c * 32, M,
                      N, r);
     } else if (has_in) {
       // keep the operand pipeline in step: consume (wait for) the block even if unused
@@ -577,12 +587,11 @@ __global__ void __maxnreg__(kGemmMaxRegs)
       epilogue_tile_prologue<BN>(ep, &map_aux, ew, warp - 4, has_in, m_base, n0, N);
       mbar_wait(&tfull_bar[buf], acc_phase);
       tc_fence_after();
-      // split-K slices: split s stores rows [s*M, (s+1)*M) of the [splits*M][N] output
-      const int32_t store_row = static_cast<int32_t>(
-          m_base + (ep.out_kind == kOutF32Split ? static_cast<int64_t>(unit / num_tiles) * M : 0));
+      // split-K slices: split s stores into slice s of the [splits][M][N] output
+      const int32_t store_z = ep.out_kind == kOutF32Split ? unit / num_tiles : 0;
       epilogue_tile<BN>(ep, &map_out, &map_aux, ew, warp - 4, has_in,
                         tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base,
-                        store_row, n0, M, N);
+                        store_z, n0, M, N);
       tc_fence_before();
       mbar_arrive(&tempty_bar[buf]);
     }
@@ -776,11 +785,11 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(kGemmMaxRegs)
       tc_fence_after();
       if (ep.trace != nullptr && local == 0 && warp == 4 && lane_id() == 0)
         ep.trace[blockIdx.x * 16 + 5] = gtimer();
-      const int32_t store_row = static_cast<int32_t>(
-          m_base + (ep.out_kind == kOutF32Split ? static_cast<int64_t>(unit / num_tiles) * M : 0));
+      // split-K slices: split s stores into slice s of the [splits][M][N] output
+      const int32_t store_z = ep.out_kind == kOutF32Split ? unit / num_tiles : 0;
       epilogue_tile<BN>(ep, &map_out, &map_aux, ew, warp - 4, has_in,
                         tmem_base + (static_cast<uint32_t>(q * 32) << 16) + buf * BN, m_base,
-                        store_row, n0, M, N);
+                        store_z, n0, M, N);
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) mbar_arrive_remote_relaxed(leader_tempty0 + buf * 8);
@@ -816,18 +825,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// Epilogue store map: 32 x 32 boxes over the [M][ld] output; bf16 uses 64 B swizzle,
-// fp32 128 B (matching the staging layout in epilogue_block).
+// Epilogue maps: 32 x 32 boxes over the [M][ld] output; bf16 uses 64 B swizzle, fp32 128 B
+// (matching the staging layout in epilogue_block).  The output map is 3-D {cols, M, slices}
+// (slices = the split-K count for kOutF32Split, else 1); the operand / aux map is 2-D.
 static bool make_out_map(CUtensorMap* map, const void* ptr, uint64_t cols, uint64_t rows,
-                         uint64_t ld, bool f32) {
+                         uint64_t ld, bool f32, uint64_t slices = 0) {
   auto fn = encode_fn();
   if (fn == nullptr || ptr == nullptr) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {ld * (f32 ? 4 : 2)};
-  cuuint32_t box[2] = {32, 32};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                  const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+  const uint64_t eb = f32 ? 4 : 2;
+  cuuint64_t dims[3] = {cols, rows, slices};
+  cuuint64_t strides[2] = {ld * eb, rows * ld * eb};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                  slices > 0 ? 3 : 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
                   f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -836,8 +848,8 @@ static bool make_out_map(CUtensorMap* map, const void* ptr, uint64_t cols, uint6
 static bool make_epi_maps(const GemmEpilogue& ep, int M, int N, int splits, CUtensorMap* mo,
                           CUtensorMap* mx) {
   const bool f32 = ep.out_kind != kOutBF16;
-  const uint64_t rows = static_cast<uint64_t>(M) * (ep.out_kind == kOutF32Split ? splits : 1);
-  if (!make_out_map(mo, ep.out, N, rows, ep.ldo, f32)) return false;
+  const uint64_t slices = ep.out_kind == kOutF32Split ? static_cast<uint64_t>(splits) : 1;
+  if (!make_out_map(mo, ep.out, N, M, ep.ldo, f32, slices)) return false;
   // map_aux: the GeLU pre-activation (written by gelu, read by gelu_bwd) or the residual read
   // by the epilogue's operand prefetch (never both in one GEMM)
   if (ep.gelu || ep.gelu_bwd) return make_out_map(mx, ep.aux, N, M, ep.ld_aux, false);

@@ -234,7 +234,7 @@ struct RankCtx {
   std::vector<RankLayer> layers;  // this stage's layers in order
   Arena arena;
   // scratch
-  bf16 *partial = nullptr, *dc = nullptr, *dx1 = nullptr, *dctx = nullptr, *da = nullptr;
+  bf16 *partial = nullptr, *dx1 = nullptr, *dctx = nullptr, *da = nullptr;
   // Gradients the weight-gradient GEMMs read, double-buffered by layer parity: layer l's
   // wgrads run on the wgrad stream while layer l-1's data-gradient chain writes the other
   // buffer.  wg_done[p] marks the last wgrad that read buffer set p.
@@ -283,7 +283,7 @@ struct RankCtx {
   int cur = 0;                      // index of gbuf holding the current dY
   bool idle_chunks = false;  // some (layer, micro-batch) chunk of this rank has no samples:
                              // gradients are zeroed whole each step and always accumulated
-  int dc_slices = 0, da_slices = 0;  // split-K slices pending in acc32 (0 = bf16 result)
+  int dc_slices = 0, da_slices = 0;  // fp32 slices pending in acc32 (da: 0 = bf16 in r.da)
 };
 
 // --------------------------------------------------------------------------------------
@@ -1088,7 +1088,6 @@ int ExecutorImpl::allocate(RankCtx& r) {
     if (cudaEventCreateWithFlags(&r.wg_done[p], cudaEventDisableTiming) != cudaSuccess)
       return set_error(kErrCuda, "executor: event creation failed");
   }
-  r.dc = A.a<bf16>(max_h);
   r.dx1 = A.a<bf16>(max_h);
   r.dctx = A.a<bf16>(max_c);
   r.da = A.a<bf16>(max_h);
@@ -1662,17 +1661,20 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     int sp_c = 1;
     if (t == 1)
       GX_TRY(gemm_splitk(r, dpre, ft, P + L.lay.w1.off, h, true, rows, h, ft, &sp_c));
-    r.dc_slices = sp_c > 1 ? sp_c : 0;
+    r.dc_slices = sp_c;
     if (sp_c == 1) {
+      // fp32 (one slice in acc32): LN2's backward reads the unrounded gradient, and TP partial
+      // sums are all-reduced in fp32 -- bf16 rounding of the partials before the LayerNorm's
+      // column sums cost up to 1.03e-2 relative error on dgamma (SURVEY 8(d) bar: 1e-2)
       gx_gemm_epilogue c = epi();
-      c.out_kind = kOutBF16;
-      c.out = r.dc;
+      c.out_kind = kOutF32;
+      c.out = r.acc32;
       c.ldo = h;
       GX_TRY(gemm(dpre, ft, false, P + L.lay.w1.off, h, true, rows, h, ft, c));  // dpre W1
     }
     if (t > 1)
-      return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
-                               stream_);
+      return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.acc32, static_cast<size_t>(rows) * h,
+                          DType::kF32, stream_);
     phase = 1;
   }
   // TP decoder layers: [MLP] [LN2 + cross attention] [LN3 + self-attention] [LN1] (+ [dmem
@@ -1682,7 +1684,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
   const int ln1_ph = xtp ? 3 : 2;
   if (phase == 1 || (xtp && phase == 2)) {
    if (phase == 1) {
-    const void* dc_in = r.dc_slices ? static_cast<const void*>(r.acc32) : static_cast<const void*>(r.dc);
+    const void* dc_in = r.acc32;
     // LN2 backward with the out-projection's dropout backward + bias gradient fused in:
     // dx1 = residual-stream gradient, dout = dropout_mask(dx1), dbo += colsum(dout)
     // (row pass on the critical path; the dgamma / dbeta / dbias column pass rides the wgrad
@@ -1694,7 +1696,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     bf16* const dz2 = xd ? r.dout2 : dout;
     float* fold2 = r.lnfold[par][0];
     GX_TRY(timed(kNorm, 0, 10.0 * rows * h, [&] { return layernorm_bwd_rows(dc_in, xr, A.mean2, A.rstd2, P + L.lay.ln2g.off, dY, r.dx1,
-                         rows, h, stream_, r.dc_slices > 0, &d, dz2, std::max(1, r.dc_slices),
+                         rows, h, stream_, true, &d, dz2, r.dc_slices,
                          static_cast<int64_t>(rows) * h, fold2); }));
     GX_TRY(on_wgrad([&] {
       return timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd_cols(fold2, true, xr, A.mean2, A.rstd2, dz2,
@@ -1703,10 +1705,10 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     if (xd) {
       // the wgrad-stream LN2 column pass above reads dout2 / fold2: let it finish first
       if (wg_active_) GX_TRY(fork(wg_, stream_));
-      GX_TRY(cross_bwd_attn(r, li, mb, wgrad_ep));  // -> dc3 (TP: partial) in r.dc
+      GX_TRY(cross_bwd_attn(r, li, mb, wgrad_ep));  // -> dc3 (TP: partial) in r.acc32 (fp32)
       if (t > 1)
-        return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.dc, static_cast<size_t>(rows) * h, DType::kBF16,
-                            stream_);
+        return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.acc32, static_cast<size_t>(rows) * h,
+                            DType::kF32, stream_);
     }
    }
     if (s.cross) GX_TRY(cross_bwd_ln3(r, li, mb, dout));  // dx1, dout (self-attention)
@@ -1772,11 +1774,11 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     int sp_a = 1;
     if (t == 1 && s.shift == 0)  // (SW-MSA rolls dA back before LN1: keep it bf16)
       GX_TRY(gemm_splitk(r, dqkv, 3 * ht, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, &sp_a));
-    r.da_slices = sp_a > 1 ? sp_a : 0;
+    r.da_slices = sp_a;
     if (sp_a == 1) {
       gx_gemm_epilogue a = epi();
-      a.out_kind = kOutBF16;
-      a.out = r.da;
+      a.out_kind = s.shift > 0 ? kOutBF16 : kOutF32;  // fp32 into LN1's backward, as for LN2
+      a.out = s.shift > 0 ? static_cast<void*>(r.da) : static_cast<void*>(r.acc32);
       a.ldo = h;
       GX_TRY(gemm(dqkv, 3 * ht, false, P + L.lay.wqkv.off, h, true, rows, h, 3 * ht, a));
       if (s.shift > 0) {  // LN1 (and the residual) live in the unrolled order
@@ -1789,9 +1791,13 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
                           "sw-msa da"));
       }
     }
+    if (s.shift > 0) r.da_slices = 0;  // bf16 in r.da
     if (t > 1)
-      return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.da, static_cast<size_t>(rows) * h, DType::kBF16,
-                               stream_);
+      return r.da_slices == 0
+                 ? c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.da, static_cast<size_t>(rows) * h,
+                                DType::kBF16, stream_)
+                 : c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.acc32,
+                                static_cast<size_t>(rows) * h, DType::kF32, stream_);
     phase = 2;
   }
   if (phase == ln1_ph) {
@@ -1968,7 +1974,8 @@ int ExecutorImpl::cross_bwd_attn(RankCtx& r, int li, int mb,
   m.out = r.dmem;
   m.ldo = h;
   GX_TRY(gemm(r.dqkv2 + ht, 3 * ht, false, P + L.lay.wkv2.off, h, true, rows, h, 2 * ht, m));
-  c.out = r.dc;
+  c.out_kind = kOutF32;  // fp32 into LN3's backward (and the TP all-reduce), as for LN2
+  c.out = r.acc32;
   c.ldo = h;
   return gemm(r.dqkv2, 3 * ht, false, P + L.lay.wq2.off, h, true, rows, h, ht, c);  // dq Wq2
 }
@@ -1992,9 +1999,9 @@ int ExecutorImpl::cross_bwd_ln3(RankCtx& r, int li, int mb, bf16* dout) {
   d.drop_ld = h;
   d.seed_offset = r.seed_off;
   return timed(kNorm, 0, 18.0 * rows * h, [&] {
-    return layernorm_bwd(r.dc, A.x1, A.mean3, A.rstd3, P + L.lay.ln3g.off, r.dx1, r.dx1,
+    return layernorm_bwd(r.acc32, A.x1, A.mean3, A.rstd3, P + L.lay.ln3g.off, r.dx1, r.dx1,
                          G + L.lay.ln3g.off, G + L.lay.ln3b.off, rows, h, r.ln_ws_x, stream_,
-                         false, &d, dout, G + L.lay.bo.off);
+                         true, &d, dout, G + L.lay.bo.off, 1, static_cast<int64_t>(rows) * h);
   });
 }
 
