@@ -76,6 +76,7 @@ Geom make_geom(const gx_attention_args& a) {
 // region and the head's bias table (log2 units).
 struct WinSmem {
   float tab[kTabMax];
+  int16_t kc[kTcQ];  // ty * (2 side - 1) + tx: bias index = row base - kc[key]
   int8_t ty[kTcQ], tx[kTcQ], reg[kTcQ];
 };
 
@@ -104,24 +105,10 @@ __device__ __forceinline__ void win_stage_tc(const gx_attention_args& p, const G
     const int tok = v % s, u = vb * g.wpt + v / s;
     w->ty[v] = static_cast<int8_t>(p.rpb_side > 0 ? tok / p.rpb_side : 0);
     w->tx[v] = static_cast<int8_t>(p.rpb_side > 0 ? tok % p.rpb_side : 0);
+    w->kc[v] = static_cast<int16_t>(w->ty[v] * (2 * p.rpb_side - 1) + w->tx[v]);
     w->reg[v] = static_cast<int8_t>(p.win_shift > 0 && v < g.vseq && u < p.batch
                                         ? swin_region_tc(p, u, tok) : 0);
   }
-}
-
-// Is the (virtual query, virtual key) pair attended?  (general path; both < vseq checked)
-__device__ __forceinline__ bool pair_ok(const gx_attention_args& p, const WinSmem* w, int s,
-                                        int vq, int vk) {
-  if (vq / s != vk / s) return false;  // different packed sequences
-  if (p.causal && vk % s > vq % s) return false;
-  if (p.win_shift > 0 && w->reg[vq] != w->reg[vk]) return false;
-  return true;
-}
-__device__ __forceinline__ float pair_bias(const gx_attention_args& p, const WinSmem* w, int vq,
-                                           int vk) {
-  if (p.rpb == nullptr) return 0.f;
-  const int side = p.rpb_side;
-  return w->tab[(w->ty[vq] - w->ty[vk] + side - 1) * (2 * side - 1) + (w->tx[vq] - w->tx[vk] + side - 1)];
 }
 
 // keep bit of real key kk (0..63) of a 64-key block: word (kk/2)%4, bit 2*(kk/8) + kk%2
@@ -297,27 +284,61 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   if (kGen) named_sync(1, kFwdThreads);  // window metadata staged
   GX_ATTN_STAMP(p, 2);
 
-  // fast path: keys [0, lim) exist for this row
-  const int lim = kGen ? 0 : s;
+  // fast path (!kGen): keys [0, s) exist for every row; a 64-key block is either full or
+  // the tail block, so only the tail compares per element.  The max is taken over the raw
+  // scores (c2 > 0) and scaled once.
+  // General path (kGen): per row, the attended keys are the virtual range [klo, khi) of the
+  // row's own packed sequence (causal: up to the query), intersected with its shifted-window
+  // region; the bias index is rowbase - kc[key].  Work goes in 32-column chunks: one per
+  // quarter for packed windows (nk <= 128), else both halves of the 64-key blocks kb = cq +
+  // 4 t (one Philox draw of four calls per block).
+  const int klo = (vq / s) * s;
+  const int khi = min(p.causal ? vq + 1 : klo + s, g.vseq);
+  const int rq = kGen && p.win_shift > 0 ? win->reg[r] : 0;
+  const int side = p.rpb_side;
+  const int rowbase = kGen && p.rpb != nullptr
+                          ? (win->ty[r] + side - 1) * (2 * side - 1) + win->tx[r] + side - 1 : 0;
+  auto gen_x = [&](int c, uint32_t raw) -> float {  // scaled score, or -inf if not attended
+    bool ok = c >= klo && c < khi;
+    if (p.win_shift > 0) ok = ok && win->reg[c] == rq;
+    if (!ok) return -INFINITY;
+    float x = __uint_as_float(raw) * c2;
+    if (p.rpb != nullptr) x += win->tab[rowbase - win->kc[c]];
+    return x;
+  };
+  const int nchunk = g.wpt > 1 ? 1 : 2;  // 32-column chunks per work item
+  const int nitem = g.wpt > 1 ? (cq * 32 < nk ? 1 : 0) : (nblk - cq + 3) / 4;
+  auto item_c0 = [&](int it, int hb) { return g.wpt > 1 ? cq * 32 : (cq + 4 * it) * 64 + hb * 32; };
   float mx = -INFINITY;
-  for (int kb = cq; kb < nblk; kb += 4) {
+  if (kGen) {
+    for (int it = 0; it < nitem; ++it)
+      for (int hb = 0; hb < nchunk; ++hb) {
+        const int c0 = item_c0(it, hb);
+        // tcgen05.ld is warp-collective: skip a chunk only when no lane of the warp needs it
+        if (!__any_sync(0xffffffffu, c0 < khi && c0 + 32 > klo)) continue;
+        uint32_t v[32];
+        tmem_ld32(trow + c0, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) mx = fmaxf(mx, gen_x(c0 + j, v[j]));
+      }
+  }
+  for (int kb = cq; kb < nblk && !kGen; kb += 4) {
     uint32_t v[64];
     tmem_ld32(trow + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
     tmem_ld32(trow + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
     tmem_ld_wait();
+    if (kb * 64 + 64 <= s) {
 #pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      const int c = kb * 64 + j;
-      float x;
-      if (kGen) {
-        x = c < g.vseq && pair_ok(p, win, s, vq, c)
-                ? __uint_as_float(v[j]) * c2 + pair_bias(p, win, vq, c) : -INFINITY;
-      } else {
-        x = c < lim ? __uint_as_float(v[j]) * c2 : -INFINITY;
-      }
-      mx = fmaxf(mx, x);
+      for (int j = 0; j < 64; j += 2)
+        mx = fmaxf(mx, fmaxf(__uint_as_float(v[j]), __uint_as_float(v[j + 1])));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 64; ++j)
+        if (kb * 64 + j < s) mx = fmaxf(mx, __uint_as_float(v[j]));
     }
   }
+  if (!kGen && mx != -INFINITY) mx *= c2;
   red[cq * kTcQ + r] = mx;
   named_sync(1, kFwdThreads);
   GX_ATTN_STAMP(p, 3);
@@ -336,20 +357,73 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint32_t wrow[4] = {0u, 0u, 0u, 0u};
   if (kGen && g.wpt > 1 && thr != 0u) {
     const uint64_t call0 = (stream + static_cast<uint64_t>(q)) * nkb * 4;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) wrow[t] = keep16(seed, p.site, call0 + t, thr);
+    keep16x4(seed, p.site, call0, thr, wrow);
     if (row_ok && cq == 0)
       *reinterpret_cast<uint64_t*>(mask + (bh_real * s + q) * nkb * 4) =
           static_cast<uint64_t>(wrow[0]) | (static_cast<uint64_t>(wrow[1]) << 16) |
           (static_cast<uint64_t>(wrow[2]) << 32) | (static_cast<uint64_t>(wrow[3]) << 48);
   }
+  // P = exp2(S c2 + bias - m) with dropped keys zeroed; the keep scale 1 / (1 - p) is applied
+  // once to O in the epilogue (row sums l are taken before dropout)
   float sum = 0.f;
-  for (int kb = cq; kb < nblk; kb += 4) {
-    uint32_t bits[4] = {wrow[0], wrow[1], wrow[2], wrow[3]};
-    if (thr != 0u && g.wpt == 1) {
-      const uint64_t call0 = ((stream + static_cast<uint64_t>(q)) * nkb + kb) * 4;
+  // one 32-column chunk of P -> the K-major SWIZZLE_128B tile of its 64-key group
+  auto store_p = [&](int c0, const uint32_t (&pk)[16]) {
+    const uint32_t g_addr = p_group_addr(L, sbase, c0 >> 6) + r * 128;
+    const int hb = (c0 >> 5) & 1;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) bits[t] = keep16(seed, p.site, call0 + t, thr);
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t sw = static_cast<uint32_t>((hb * 4 + i) ^ (r & 7));
+      st_shared_v4_tc(g_addr + (sw << 4), pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+    }
+  };
+  if (kGen) {
+    for (int it = 0; it < nitem; ++it) {
+      uint32_t bits[4] = {wrow[0], wrow[1], wrow[2], wrow[3]};
+      const int kb = g.wpt > 1 ? 0 : cq + 4 * it;
+      if (thr != 0u && g.wpt == 1) {
+        const uint64_t call0 = ((stream + static_cast<uint64_t>(q)) * nkb + kb) * 4;
+        keep16x4(seed, p.site, call0, thr, bits);
+        if (row_ok && kb < nkb)
+          *reinterpret_cast<uint64_t*>(mask + ((bh_real * s + q) * nkb + kb) * 4) =
+              static_cast<uint64_t>(bits[0]) | (static_cast<uint64_t>(bits[1]) << 16) |
+              (static_cast<uint64_t>(bits[2]) << 32) | (static_cast<uint64_t>(bits[3]) << 48);
+      }
+      for (int hb = 0; hb < nchunk; ++hb) {
+        const int c0 = item_c0(it, hb);
+        uint32_t pk[16];
+        if (!__any_sync(0xffffffffu, row_ok && c0 < khi && c0 + 32 > klo)) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = 0u;
+        } else {
+          uint32_t v[32];
+          tmem_ld32(trow + c0, v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j2 = 0; j2 < 16; ++j2) {
+            float e2[2];
+#pragma unroll
+            for (int uu = 0; uu < 2; ++uu) {
+              const int i = 2 * j2 + uu;
+              const int c = c0 + i;
+              const float x = row_ok ? gen_x(c, v[i]) : -INFINITY;
+              float e = x == -INFINITY ? 0.f : ex2_ftz(x - m);
+              sum += e;
+              const int kk = g.wpt > 1 ? c - klo : (c & 63);
+              if (thr != 0u) e = keep_bit(bits, kk) ? e : 0.f;
+              e2[uu] = e;
+            }
+            pk[j2] = pack_bf16(e2[0], e2[1]);
+          }
+        }
+        store_p(c0, pk);
+      }
+    }
+  }
+  for (int kb = cq; kb < nblk && !kGen; kb += 4) {
+    uint32_t bits[4] = {0u, 0u, 0u, 0u};
+    if (thr != 0u) {
+      const uint64_t call0 = ((stream + static_cast<uint64_t>(q)) * nkb + kb) * 4;
+      keep16x4(seed, p.site, call0, thr, bits);
       if (row_ok && kb < nkb) {
         const uint64_t packed = static_cast<uint64_t>(bits[0]) |
                                 (static_cast<uint64_t>(bits[1]) << 16) |
@@ -358,7 +432,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         *reinterpret_cast<uint64_t*>(mask + ((bh_real * s + q) * nkb + kb) * 4) = packed;
       }
     }
-    const uint32_t g_addr = p_group_addr(L, sbase, kb) + r * 128;
+    const bool full = kb * 64 + 64 <= s;
 #pragma unroll
     for (int hb = 0; hb < 2; ++hb) {
       const int c0 = kb * 64 + hb * 32;
@@ -372,29 +446,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int uu = 0; uu < 2; ++uu) {
           const int i = 2 * j2 + uu;
-          const int c = c0 + i;
-          float e;
-          int kk;  // the key's position in its real 64-key block (dropout bit)
-          if (kGen) {
-            const bool ok = row_ok && c < g.vseq && pair_ok(p, win, s, vq, c);
-            e = ok ? ex2_ftz(__uint_as_float(v[i]) * c2 + pair_bias(p, win, vq, c) - m) : 0.f;
-            kk = g.wpt > 1 ? c % s : (c & 63);
-          } else {
-            e = c < lim ? ex2_ftz(__uint_as_float(v[i]) * c2 - m) : 0.f;
-            kk = c & 63;
-          }
+          float e = ex2_ftz(fmaf(__uint_as_float(v[i]), c2, -m));
+          if (!full && c0 + i >= s) e = 0.f;
           sum += e;
-          if (thr != 0u) e = keep_bit(bits, kk) ? e * inv_keep : 0.f;
+          // compile-time key position: the keep bit's word and shift fold to constants
+          if (thr != 0u) e = keep_bit(bits, hb * 32 + i) ? e : 0.f;
           e2[uu] = e;
         }
         pk[j2] = pack_bf16(e2[0], e2[1]);
       }
-      // bf16 P row segment -> K-major SWIZZLE_128B tile of its 64-key group
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t sw = static_cast<uint32_t>((hb * 4 + i) ^ (r & 7));
-        st_shared_v4_tc(g_addr + (sw << 4), pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-      }
+      store_p(c0, pk);
     }
   }
   red[4 * kTcQ + cq * kTcQ + r] = sum;
@@ -427,7 +488,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   mbar_wait(bar_o, 0);
   tc_fence_after();
   GX_ATTN_STAMP(p, 5);
-  const float inv = l > 0.f ? 1.f / l : 0.f;
+  const float inv = l > 0.f ? (thr != 0u ? inv_keep : 1.f) / l : 0.f;
   auto* ctx = static_cast<__nv_bfloat16*>(p.ctx);
   for (int c16 = cq; c16 < hd / 16; c16 += 4) {  // O columns [16 c16, 16 c16 + 16) of this row
     uint32_t o[16];
@@ -585,6 +646,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int kk = g.wpt > 1 ? key % s : (kr & 63);
   const int mt = (kk >> 1) & 3, mbit = 2 * (kk >> 3) + (kk & 1);
   float* part = static_cast<float*>(p.dq_accum);
+  // general path: queries attending this key (virtual indices), and its bias-index base
+  const int qlo = p.causal ? key : (key / s) * s;
+  const int qhi = min((key / s) * s + s, g.vseq);
+  int kreg = 0, kbase = 0;  // (read from the staged window metadata after the first barrier)
 
   if (is_mma_warp) {
     // ------------------------------------------------ producer / MMA issue (one lane)
@@ -717,6 +782,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     };
     compute_d(0);
     named_sync(1, kBwdSoftmax);
+    if (kGen && key < kTcQ) {
+      if (p.win_shift > 0) kreg = win->reg[key];
+      if (p.rpb != nullptr)
+        kbase = (p.rpb_side - 1) * (2 * p.rpb_side - 1) + p.rpb_side - 1 - win->kc[key];
+    }
     GX_ATTN_STAMP(p, 2);
     for (int j = 0; j < nq; ++j) {
       mbar_wait(bar_s, j & 1);
@@ -746,8 +816,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             bool valid;
             float bias = 0.f;
             if (kGen) {
-              valid = key_ok && qg < g.vseq && pair_ok(p, win, s, qg, key);
-              if (valid) bias = pair_bias(p, win, qg, key);
+              // the key's own packed sequence [qlo, qhi) (causal: queries >= key), its
+              // shifted-window region, and the bias at kc[q] - kc[key] (see the forward)
+              valid = key_ok && qg >= qlo && qg < qhi;
+              if (p.win_shift > 0) valid = valid && win->reg[qg] == kreg;
+              if (valid && p.rpb != nullptr) bias = win->tab[win->kc[qg] + kbase];
             } else {
               valid = full || (qg < s && key < s);
             }

@@ -70,4 +70,51 @@ __host__ __device__ __forceinline__ uint32_t keep16(uint64_t seed, uint64_t site
 #endif
 }
 
+// keep16 of the four consecutive calls c, c+1, c+2, c+3 (the 64 keys of one attention key
+// block): the four Philox streams share their round keys, so the key schedule is paid once.
+// Bit-identical to four keep16 calls.
+__device__ __forceinline__ void keep16x4(uint64_t seed, uint64_t site, uint64_t c,
+                                         uint32_t thr8, uint32_t (&out)[4]) {
+  uint32_t x0[4], x1[4], x2[4], x3[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const uint64_t ct = c + static_cast<uint64_t>(t);
+    x0[t] = static_cast<uint32_t>(ct);
+    x1[t] = static_cast<uint32_t>(ct >> 32);
+    x2[t] = static_cast<uint32_t>(site);
+    x3[t] = static_cast<uint32_t>(site >> 32);
+  }
+  uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint64_t p0 = static_cast<uint64_t>(0xD2511F53u) * x0[t];
+      const uint64_t p1 = static_cast<uint64_t>(0xCD9E8D57u) * x2[t];
+      const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ x1[t] ^ k0;
+      const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ x3[t] ^ k1;
+      x1[t] = static_cast<uint32_t>(p1);
+      x3[t] = static_cast<uint32_t>(p0);
+      x0[t] = n0;
+      x2[t] = n2;
+    }
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  const uint32_t t4 = thr8 * 0x01010101u;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const uint32_t words[4] = {x0[t], x1[t], x2[t], x3[t]};
+    uint32_t bits = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t x = __vcmpgeu4(words[k], t4) & 0x01010101u;
+      x |= x >> 7;
+      x |= x >> 14;
+      bits |= (x & 0xFu) << (4 * k);
+    }
+    out[t] = bits;
+  }
+}
+
 }  // namespace gx

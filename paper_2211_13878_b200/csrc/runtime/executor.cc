@@ -2428,9 +2428,11 @@ int ExecutorImpl::step_once() {
       }
     }
   }
+  tmark("bwd_chain_end", stream_);
   if (wg_used_) {  // join the wgrad stream
     GX_TRY(fork(wg_, stream_));
   }
+  tmark("wgrad_joined", stream_);
   if (cs_used_) GX_TRY(fork(cs_, stream_));  // ... and the gradient-collective stream
   if (pp_used_) GX_TRY(fork(pp_, stream_));  // ... and the pipeline stream
   if (side_used_) {  // join the optimizer stream before the step completes

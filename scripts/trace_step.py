@@ -4,7 +4,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2211_13878_b200 import executor as gxe  # noqa: E402
 import bench  # noqa: E402
-model, plan, _ = bench.choose_plan(1, 16.0, "bert-huge-32")
+from paper_2211_13878_b200 import planner  # noqa: E402
+model, plan, _ = bench.search(planner.api(), "bert-huge-32", 1, 16.0)
 sh = model["layers"][0]["shape"]
 x = torch.randn(plan["batch_size"] * sh["seq"], sh["hidden"]).to(torch.bfloat16)
 kw = json.loads(sys.argv[1]) if len(sys.argv) > 1 else {}
