@@ -253,6 +253,15 @@ typedef struct gx_attention_args {
   const void* rpb;
   void* rpb_dpart;
   int rpb_side;
+  /* T5 relative attention bias (tcgen05 path): scores get relb[head][relb_map[k - q + seq - 1]]
+   * (bf16 [heads][relb_buckets] learned table, int8 relb_map[2 seq - 1] = the T5 bucket of
+   * each relative position, bidirectional or causal); bwd writes per-(sequence x head, key
+   * block) fp32 partial sums of dS over each relative position to relb_dpart
+   * ([batch*heads][ceil(seq/128)][2 seq - 1]) for gx_k_relb_grad.  relb NULL = no bias. */
+  const void* relb;
+  const void* relb_map;
+  int relb_buckets;
+  void* relb_dpart;
 } gx_attention_args;
 
 GX_API int gx_k_attention_fwd(const gx_attention_args* args, void* stream);
@@ -305,6 +314,10 @@ GX_API int gx_k_patch_merge(const void* src, void* dst, int samples, int grid_ou
  * (fixed order: deterministic). */
 GX_API int gx_k_rpb_grad(const void* dpart, int batch, int heads, int side, void* grad,
                          int accumulate, void* stream);
+/* T5 relative attention bias gradient: grad[h][b] (+)= fixed-order sum over the sequence tiles
+ * `tiles`, key blocks and relative positions d (map[d] == b) of the backward's relb_dpart. */
+GX_API int gx_k_relb_grad(const void* dpart, int tiles, int heads, int seq, const void* map,
+                          int buckets, void* grad, int accumulate, void* stream);
 GX_API int gx_k_window_roll(const void* src, void* dst, int samples, int grid, int window_side,
                             int shift, int channels, int inverse, void* stream);
 GX_API int gx_k_cast_bf16(const void* src, void* dst, int64_t n, void* stream);

@@ -96,6 +96,8 @@ class LayerShape:
     cross: bool = False   # T5 decoder: + cross-attention sublayer over the memory
     shift: int = 0        # Swin SW-MSA: tokens rolled by -shift around the window attention
     rpb: bool = False     # Swin relative-position bias table [heads][(2 side - 1)^2]
+    rms: bool = False     # T5: every LayerNorm of the layer is an RMSNorm (gain only, eps 1e-6)
+    relb: int = 0         # T5 relative attention bias: buckets (0 = none), max distance 128
 
     @property
     def att_seq(self):
@@ -162,6 +164,30 @@ def rel_index(window: int) -> np.ndarray:
     return (y[:, None] - y[None] + w - 1) * (2 * w - 1) + (x[:, None] - x[None] + w - 1)
 
 
+def t5_buckets(seq: int, bidirectional: bool, num_buckets: int = 32,
+               max_distance: int = 128) -> np.ndarray:
+    """T5's relative-position bucket (Raffel et al. 2020; the published
+    `_relative_position_bucket` of the T5 implementations) of each relative position
+    k - q = d for d in [-(seq-1), seq-1] (index d + seq - 1): |d| < max_exact exact, then
+    log-spaced up to max_distance, saturating; bidirectional splits the buckets by sign.
+    Computed in float64 (the executor's host code does the same)."""
+    d = np.arange(-(seq - 1), seq, dtype=np.int64)
+    n = -d  # query - key
+    nb = num_buckets
+    ret = np.zeros_like(n)
+    if bidirectional:
+        nb //= 2
+        ret = (n < 0).astype(np.int64) * nb
+        n = np.abs(n)
+    else:
+        n = np.maximum(n, 0)
+    max_exact = nb // 2
+    large = max_exact + (np.log(np.maximum(n, 1) / max_exact) / math.log(max_distance / max_exact)
+                         * (nb - max_exact)).astype(np.int64)
+    large = np.minimum(large, nb - 1)
+    return ret + np.where(n < max_exact, n, large)
+
+
 def init_layer_params(shape: LayerShape, rng: np.random.Generator, std=0.02) -> dict:
     h, f = shape.hidden, shape.ffn
     if shape.rpb:
@@ -169,6 +195,8 @@ def init_layer_params(shape: LayerShape, rng: np.random.Generator, std=0.02) -> 
         rp = {"rpb": 0.5 * rng.standard_normal((shape.heads, n2))}
     else:
         rp = {}
+    if shape.relb:
+        rp["relb"] = 0.5 * rng.standard_normal((shape.heads, shape.relb))
     merge = {} if not shape.merge else {
         "mln_g": 1.0 + 0.1 * rng.standard_normal(2 * h), "mln_b": 0.1 * rng.standard_normal(2 * h),
         "w_m": std * rng.standard_normal((h, 2 * h))}
@@ -188,6 +216,17 @@ def init_layer_params(shape: LayerShape, rng: np.random.Generator, std=0.02) -> 
     }
 
 
+def _rms_fwd(x, g, eps=1e-6):
+    """T5 RMSNorm: x * rsqrt(mean(x^2) + eps) * g (no centring, no bias)."""
+    rstd = 1.0 / np.sqrt((x * x).mean(-1, keepdims=True) + eps)
+    xh = x * rstd
+    return xh * g, (xh, rstd, True)
+
+
+def _norm_fwd(x, g, b, rms):
+    return _rms_fwd(x, g) if rms else _ln_fwd(x, g, b)
+
+
 def _ln_fwd(x, g, b, eps=1e-5):
     mu = x.mean(-1, keepdims=True)
     var = ((x - mu) ** 2).mean(-1, keepdims=True)
@@ -197,11 +236,13 @@ def _ln_fwd(x, g, b, eps=1e-5):
 
 
 def _ln_bwd(dy, cache, g):
-    xh, rstd = cache
-    h = xh.shape[-1]
+    """LayerNorm (or, for an RMSNorm cache, RMSNorm: no mean term, zero bias gradient)."""
+    xh, rstd = cache[0], cache[1]
+    rms = len(cache) > 2
     dxh = dy * g
-    dx = rstd * (dxh - dxh.mean(-1, keepdims=True) - xh * (dxh * xh).mean(-1, keepdims=True))
-    return dx, (dy * xh).sum(0), dy.sum(0)
+    mean_term = 0.0 if rms else dxh.mean(-1, keepdims=True)
+    dx = rstd * (dxh - mean_term - xh * (dxh * xh).mean(-1, keepdims=True))
+    return dx, (dy * xh).sum(0), (np.zeros(dy.shape[-1]) if rms else dy.sum(0))
 
 
 try:  # vectorised erf when scipy is present (CPU-baseline speed); identical math otherwise
@@ -301,7 +342,7 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
         x = mln @ P["w_m"].T
     n = x.shape[0] // s                      # attention sequences
     nw = shape.seq // s                      # per sample
-    a, ln1 = _ln_fwd(x, P["ln1_g"], P["ln1_b"])
+    a, ln1 = _norm_fwd(x, P["ln1_g"], P["ln1_b"], shape.rms)
     ar, perm = a, None
     if shape.shift:  # SW-MSA: roll the tokens (per sample), attend in windows, roll back
         ns = n // nw
@@ -314,6 +355,10 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
     sc = q @ k.transpose(0, 1, 3, 2) / math.sqrt(d)
     if shape.rpb:
         sc = sc + P["rpb"][:, rel_index(s)][None]
+    if shape.relb:  # T5: bias of bucket(k - q), bidirectional unless causal
+        bk = t5_buckets(s, not shape.causal, shape.relb)
+        rel = (np.arange(s)[None, :] - np.arange(s)[:, None]) + s - 1  # [q, k] -> k - q + s - 1
+        sc = sc + P["relb"][:, bk[rel]][None]
     if shape.causal:
         sc = np.where(np.triu(np.ones((s, s), dtype=bool), 1), -np.inf, sc)
     if shape.shift:
@@ -339,7 +384,7 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
     xr = x1
     if shape.cross:  # cross sublayer: q from LN3(x1), k / v from the memory
         sa, sh = cross_sites(layer_id, n_layers)
-        c3, ln3 = _ln_fwd(x1, P["ln3_g"], P["ln3_b"])
+        c3, ln3 = _norm_fwd(x1, P["ln3_g"], P["ln3_b"], shape.rms)
         q2 = c3 @ P["w_q2"].T + P["b_q2"]
         kv2 = memory @ P["w_kv2"].T + P["b_kv2"]
         am2 = _attn_mask(drop, sa, n, H, s, sample_offset)
@@ -347,7 +392,7 @@ def layer_forward(P: dict, x: np.ndarray, shape: LayerShape, layer_id: int = 0,
         m3 = _hidden_mask(drop, sh, n * s, h, sample_offset * shape.seq)
         xr = x1 + (ctx2 @ P["w_o2"].T + P["b_o2"]) * m3 * kh
         xcache = dict(c3=c3, ln3=ln3, ctx2=ctx2, ac=ac, m3=m3, memory=memory, x2=xr)
-    c, ln2 = _ln_fwd(xr, P["ln2_g"], P["ln2_b"])
+    c, ln2 = _norm_fwd(xr, P["ln2_g"], P["ln2_b"], shape.rms)
     pre = c @ P["w_1"].T + P["b_1"]
     g = _gelu(pre)
     z = g @ P["w_2"].T + P["b_2"]
@@ -403,6 +448,12 @@ def layer_backward(P: dict, dy: np.ndarray, cache: dict, shape: LayerShape):
         tot = dsc.sum(0).reshape(H, -1)  # [H, s*s]
         G["rpb"] = np.stack([np.bincount(idx, weights=tot[hh], minlength=P["rpb"].shape[1])
                              for hh in range(H)])
+    if shape.relb:
+        bk = t5_buckets(s, not shape.causal, shape.relb)
+        rel = (np.arange(s)[None, :] - np.arange(s)[:, None]) + s - 1
+        tot = dsc.sum(0).reshape(H, -1)  # [H, s*s]
+        G["relb"] = np.stack([np.bincount(bk[rel].ravel(), weights=tot[hh], minlength=shape.relb)
+                              for hh in range(H)])
     dsc = dsc / math.sqrt(d)
     dq = dsc @ cache["k"]
     dk = dsc.transpose(0, 1, 3, 2) @ cache["q"]

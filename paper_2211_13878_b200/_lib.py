@@ -69,7 +69,7 @@ def _declare(L: ctypes.CDLL) -> None:
     for name in ("gx_k_attention_fwd", "gx_k_attention_bwd", "gx_k_layernorm_fwd",
                  "gx_k_layernorm_bwd", "gx_k_bias_dropout_add", "gx_k_dropout_bwd_colsum",
                  "gx_k_colsum", "gx_k_mse_loss", "gx_k_adamw", "gx_k_cast_bf16",
-                 "gx_k_patch_merge", "gx_k_window_roll", "gx_k_rpb_grad"):
+                 "gx_k_patch_merge", "gx_k_window_roll", "gx_k_rpb_grad", "gx_k_relb_grad"):
         getattr(L, name).restype = c_int
     vp = c_void_p
     L.gx_k_attention_fwd.argtypes = [vp, vp]
@@ -86,6 +86,7 @@ def _declare(L: ctypes.CDLL) -> None:
     L.gx_k_patch_merge.argtypes = [vp, vp, c_int, c_int, c_int, c_int, c_int, vp]
     L.gx_k_window_roll.argtypes = [vp, vp, c_int, c_int, c_int, c_int, c_int, c_int, vp]
     L.gx_k_rpb_grad.argtypes = [vp, c_int, c_int, c_int, vp, c_int, vp]
+    L.gx_k_relb_grad.argtypes = [vp, c_int, c_int, c_int, vp, c_int, vp, c_int, vp]
     L.gx_exec_create.argtypes = [c_char_p, POINTER(c_void_p)]
     L.gx_exec_destroy.argtypes = [vp]
     L.gx_exec_set_layer_params.argtypes = [vp, c_int, vp, c_int64]

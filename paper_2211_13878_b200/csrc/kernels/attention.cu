@@ -665,9 +665,47 @@ int rpb_grad(const float* dpart, int batch, int heads, int side, float* grad, bo
   return check_launch("rpb_grad_kernel");
 }
 
+// T5 relative-bias gradient: grad[h][b] (+)= sum over sequence tiles t, key blocks and
+// relative positions d with map[d] == b of dpart[(t*heads + h)*nkt + kt][d]; one block per
+// (h, b), threads stride over the terms and a shared-memory tree adds them in fixed order.
+__global__ void relb_grad_kernel(const float* __restrict__ dpart, int tiles, int heads, int nkt,
+                                 int nd, const int8_t* __restrict__ map, int buckets,
+                                 float* __restrict__ grad, bool accumulate) {
+  pdl_enter();
+  const int hh = blockIdx.x / buckets, b = blockIdx.x % buckets;
+  float acc = 0.f;
+  const int64_t terms = static_cast<int64_t>(tiles) * nkt * nd;
+  for (int64_t i = threadIdx.x; i < terms; i += blockDim.x) {
+    const int d = static_cast<int>(i % nd);
+    if (map[d] != b) continue;
+    const int64_t tk = i / nd;  // t * nkt + kt
+    const int64_t t = tk / nkt, kt = tk % nkt;
+    acc += dpart[((t * heads + hh) * nkt + kt) * nd + d];
+  }
+  __shared__ float red[256];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (static_cast<int>(threadIdx.x) < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) grad[blockIdx.x] = (accumulate ? grad[blockIdx.x] : 0.f) + red[0];
+}
+
+int relb_grad(const float* dpart, int tiles, int heads, int seq, const void* map, int buckets,
+              float* grad, bool accumulate, cudaStream_t st) {
+  if (tiles <= 0) return kOk;
+  const int nkt = (seq + 127) / 128;
+  launch_k(relb_grad_kernel, dim3(heads * buckets), dim3(256), 0, st, dpart, tiles, heads, nkt,
+           2 * seq - 1, static_cast<const int8_t*>(map), buckets, grad, accumulate);
+  return check_launch("relb_grad_kernel");
+}
+
 int attention_fwd(const gx_attention_args& a, cudaStream_t st) {
   if (a.seq <= 0 || a.batch <= 0 || a.heads <= 0) return set_error(kErrConfig, "attention: empty");
   if (attention_tc_supported(a)) return attention_fwd_tc(a, st);
+  if (a.relb != nullptr)
+    return set_error(kErrConfig, "attention: the T5 relative bias needs the tcgen05 path");
   switch (a.head_dim) {
     case 32: return attention_fwd_impl<32>(a, st);
     case 64: return attention_fwd_impl<64>(a, st);
@@ -680,6 +718,8 @@ int attention_fwd(const gx_attention_args& a, cudaStream_t st) {
 int attention_bwd(const gx_attention_args& a, cudaStream_t st) {
   if (a.seq <= 0 || a.batch <= 0 || a.heads <= 0) return set_error(kErrConfig, "attention: empty");
   if (attention_tc_supported(a) && (a.ld_ctx % 8) == 0) return attention_bwd_tc(a, st);
+  if (a.relb != nullptr)
+    return set_error(kErrConfig, "attention: the T5 relative bias needs the tcgen05 path");
   switch (a.head_dim) {
     case 32: return attention_bwd_impl<32>(a, st);
     case 64: return attention_bwd_impl<64>(a, st);

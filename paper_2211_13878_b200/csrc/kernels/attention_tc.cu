@@ -68,13 +68,15 @@ Geom make_geom(const gx_attention_args& a) {
   g.vseq = g.wpt * a.seq;
   g.nk = (g.vseq + 63) / 64 * 64;
   g.tiles = (a.batch + g.wpt - 1) / g.wpt;
-  g.gmask = (g.wpt > 1 || a.causal || a.win_shift > 0 || a.rpb != nullptr) ? 1 : 0;
+  g.gmask = (g.wpt > 1 || a.causal || a.win_shift > 0 || a.rpb != nullptr || a.relb != nullptr)
+                ? 1 : 0;
   return g;
 }
 
 // Per-tile window metadata staged in smem: token (in-window) coordinates, shifted-window
 // region and the head's bias table (log2 units).
 struct WinSmem {
+  float rel[2 * kTcMaxKeys];  // T5 relative bias of relative position k - q + seq - 1 (log2 units)
   float tab[kTabMax];
   int16_t kc[kTcQ];  // ty * (2 side - 1) + tx: bias index = row base - kc[key]
   int8_t ty[kTcQ], tx[kTcQ], reg[kTcQ];
@@ -100,6 +102,12 @@ __device__ __forceinline__ void win_stage_tc(const gx_attention_args& p, const G
     const auto* t = static_cast<const __nv_bfloat16*>(p.rpb) + h * n * n;
     for (int e = threadIdx.x; e < n * n; e += nthreads)
       w->tab[e] = __bfloat162float(t[e]) * 1.4426950408889634f;
+  }
+  if (p.relb != nullptr) {  // T5: the head's bias of every relative position
+    const auto* t = static_cast<const __nv_bfloat16*>(p.relb) + h * p.relb_buckets;
+    const auto* map = static_cast<const int8_t*>(p.relb_map);
+    for (int d = threadIdx.x; d < 2 * s - 1; d += nthreads)
+      w->rel[d] = __bfloat162float(t[map[d]]) * 1.4426950408889634f;
   }
   for (int v = threadIdx.x; v < kTcQ; v += nthreads) {
     const int tok = v % s, u = vb * g.wpt + v / s;
@@ -304,6 +312,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (!ok) return -INFINITY;
     float x = __uint_as_float(raw) * c2;
     if (p.rpb != nullptr) x += win->tab[rowbase - win->kc[c]];
+    if (p.relb != nullptr) x += win->rel[c - vq + s - 1];
     return x;
   };
   const int nchunk = g.wpt > 1 ? 1 : 2;  // 32-column chunks per work item
@@ -530,11 +539,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 namespace {
 struct BwdLayout {
   int nb;  // Q / dO chunk buffers (3: prefetch two chunks ahead; 1 when smem is short)
-  int k, v, q, d_o, pd, ds, lse, dd, mask, win, ds32, bar, bytes;
+  int k, v, q, d_o, pd, ds, lse, dd, mask, win, ds32, diag, bar, bytes;
 };
-__host__ __device__ inline BwdLayout bwd_layout(int np, bool rpb) {
+// rpb / relb: the fp32 dS tile of a chunk is kept for the bias gradients (relb: plus the
+// per-relative-position sums of the CTA)
+__host__ __device__ inline BwdLayout bwd_layout(int np, bool rpb, bool relb = false) {
   BwdLayout L{};
-  L.nb = (np == 1 && !rpb) ? 3 : 1;
+  L.nb = (np == 1 && !rpb && !relb) ? 3 : 1;
   const int tile = np * kTcQ * 128;  // one 128-row head tile
   L.k = 0;
   L.v = L.k + tile;
@@ -547,7 +558,8 @@ __host__ __device__ inline BwdLayout bwd_layout(int np, bool rpb) {
   L.mask = L.dd + 1024;                  // [512 q][2 blocks][4] u16
   L.win = L.mask + 8192;
   L.ds32 = L.win + static_cast<int>((sizeof(WinSmem) + 15) / 16 * 16);
-  L.bar = L.ds32 + (rpb ? kTcQ * kTcQ * 4 : 0);  // fp32 dS [128 q][128 k] (bias gradient)
+  L.diag = L.ds32 + (rpb || relb ? kTcQ * kTcQ * 4 : 0);  // fp32 dS [128 q][128 k]
+  L.bar = L.diag + (relb ? 2 * kTcMaxKeys * 4 : 0);       // fp32 [2 seq - 1] dS sums
   L.bytes = L.bar + 128;
   return L;
 }
@@ -562,7 +574,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sb = smem_u32(smem);
   const bool has_rpb = kGen && p.rpb_dpart != nullptr;
-  const BwdLayout BL = bwd_layout((HD + 63) / 64, has_rpb);
+  const bool has_relb = kGen && p.relb_dpart != nullptr;
+  const BwdLayout BL = bwd_layout((HD + 63) / 64, has_rpb, has_relb);
+  float* sDiag = reinterpret_cast<float*>(smem + BL.diag);
   float* sLse = reinterpret_cast<float*>(smem + BL.lse);
   float* sD = reinterpret_cast<float*>(smem + BL.dd);
   uint16_t* sMask = reinterpret_cast<uint16_t*>(smem + BL.mask);  // [512 q][2 kb][4]
@@ -630,6 +644,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       *reinterpret_cast<uint64_t*>(sMask + i * 4) = w;
     }
     if (kGen) win_stage_tc(p, g, vb, h, win, kBwdSoftmax);
+    if (has_relb)
+      for (int d = threadIdx.x; d < 2 * s - 1; d += kBwdSoftmax) sDiag[d] = 0.f;
   }
 
   const int qd = warp & 3, cq = (warp >> 2) & 3;  // TMEM lane quarter, 32-column quarter
@@ -821,6 +837,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               valid = key_ok && qg >= qlo && qg < qhi;
               if (p.win_shift > 0) valid = valid && win->reg[qg] == kreg;
               if (valid && p.rpb != nullptr) bias = win->tab[win->kc[qg] + kbase];
+              if (valid && p.relb != nullptr) bias += win->rel[key - qg + s - 1];
             } else {
               valid = full || (qg < s && key < s);
             }
@@ -830,7 +847,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               f = valid && ((sMask[(qg * 2 + kslot) * 4 + mt] >> mbit) & 1u) != 0u ? inv_keep : 0.f;
             pd4[t] = pr * f;
             ds4[t] = pr * (__uint_as_float(dv[i]) * f - dd[t]);
-            if (has_rpb) sDs[qg * kTcQ + kr] = ds4[t];
+            if (has_rpb || has_relb) sDs[(c0 + i) * kTcQ + kr] = ds4[t];
           }
           ppd[2 * i4] = pack_bf16(pd4[0], pd4[1]);
           ppd[2 * i4 + 1] = pack_bf16(pd4[2], pd4[3]);
@@ -861,6 +878,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       tc_fence_before();
       mbar_arrive(bar_pds);  // the MMA warp may issue S(j+1) and the gradients of j
       GX_ATTN_STAMP(p, 7 + 5 * j);
+      if (has_relb) {
+        // T5 bias gradient: thread t sums the chunk tile's diagonal delta = key - query
+        // (local) = t - 127 in query order and adds it to the CTA's sum of relative position
+        // (kt - j) 128 + delta; chunks go in order (deterministic)
+        named_sync(1, kBwdSoftmax);  // the fp32 dS tile of chunk j is complete
+        if (threadIdx.x < 2 * kTcQ - 1) {
+          const int delta = static_cast<int>(threadIdx.x) - (kTcQ - 1);
+          float acc = 0.f;
+          for (int qi = max(0, -delta); qi < min(kTcQ, kTcQ - delta); ++qi)
+            acc += sDs[qi * (kTcQ + 1) + delta];
+          const int idx = (kt - j) * kTcQ + delta + s - 1;
+          if (idx >= 0 && idx < 2 * s - 1) sDiag[idx] += acc;
+        }
+      }
       // sD is double-buffered: sD[(j+1) & 1] was last read in chunk j-1, before every softmax
       // warp passed the barrier that ended chunk j-1
       if (j + 1 < nq) compute_d(j + 1);
@@ -884,6 +915,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         static_cast<float*>(p.rpb_dpart)[(static_cast<int64_t>(u) * H + h) * n * n + e] = acc;
       }
+    }
+    if (has_relb) {  // (the last chunk's sums are visible after the chunk-end barrier)
+      float* out = static_cast<float*>(p.relb_dpart) +
+                   (static_cast<int64_t>(blockIdx.y) * nkt + kt) * (2 * s - 1);
+      for (int d = threadIdx.x; d < 2 * s - 1; d += kBwdSoftmax) out[d] = sDiag[d];
     }
     mbar_wait(bar_mm, (nq - 1) & 1);
     tc_fence_after();
@@ -992,6 +1028,8 @@ bool attention_tc_supported(const gx_attention_args& a) {
                            a.rpb_side * a.rpb_side != a.seq))
     return false;
   if (a.win_shift > 0 && a.seq > 64) return false;
+  if (a.relb != nullptr && (a.relb_map == nullptr || a.relb_buckets < 1 || a.relb_buckets > 127))
+    return false;
   if (g.gmask && g.vseq > kTcQ && g.wpt > 1) return false;
   return (a.ld_qkv % 8) == 0 && (a.ld_ctx % 8) == 0 &&
          (reinterpret_cast<uintptr_t>(a.qkv) % 16) == 0 &&
@@ -1037,7 +1075,9 @@ int attention_bwd_tc(const gx_attention_args& a, cudaStream_t st) {
   CUtensorMap mq, md;
   if (!make_map_2d(&mq, a.qkv, a.ld_qkv, rows) || !make_map_2d(&md, a.dctx, a.ld_ctx, rows))
     return set_error(kErrCuda, "attention_tc: tensor map encode failed");
-  const int smem = bwd_layout(g.np, a.rpb_dpart != nullptr).bytes + 1024;
+  if (a.relb_dpart != nullptr && g.np > 1)
+    return set_error(kErrConfig, "attention_tc: the T5 bias gradient needs head_dim <= 64");
+  const int smem = bwd_layout(g.np, a.rpb_dpart != nullptr, a.relb_dpart != nullptr).bytes + 1024;
   dim3 grid((g.vseq + 127) / 128, g.tiles * a.heads);
   // the key blocks of one tile x head form a cluster (dQ reduction after a cluster barrier)
 #define GX_ATTN_BWD(D, G)                                                                    \
@@ -1051,7 +1091,7 @@ int attention_bwd_tc(const gx_attention_args& a, cudaStream_t st) {
     launch_k_cluster(attn_bwd_tc_kernel<D, G>, grid, dim3(kBwdThreads), smem, st,            \
                      static_cast<unsigned>(grid.x), mq, md, a, g);                           \
   }
-  const bool gen = g.gmask || a.rpb_dpart != nullptr;
+  const bool gen = g.gmask || a.rpb_dpart != nullptr || a.relb_dpart != nullptr;
   switch (a.head_dim) {
     case 32: if (gen) GX_ATTN_BWD(32, true) else GX_ATTN_BWD(32, false) break;
     case 48: if (gen) GX_ATTN_BWD(48, true) else GX_ATTN_BWD(48, false) break;

@@ -121,6 +121,11 @@ extern "C" int gx_k_window_roll(const void* src, void* dst, int samples, int gri
   return gx::window_roll(src, dst, samples, grid, window_side, shift, channels, inverse != 0,
                          S(stream));
 }
+extern "C" int gx_k_relb_grad(const void* dpart, int tiles, int heads, int seq, const void* map,
+                              int buckets, void* grad, int accumulate, void* stream) {
+  return gx::relb_grad(static_cast<const float*>(dpart), tiles, heads, seq, map, buckets,
+                       static_cast<float*>(grad), accumulate != 0, S(stream));
+}
 extern "C" int gx_k_rpb_grad(const void* dpart, int batch, int heads, int side, void* grad,
                              int accumulate, void* stream) {
   return gx::rpb_grad(static_cast<const float*>(dpart), batch, heads, side,

@@ -58,6 +58,8 @@ int attention_fwd_tc(const gx_attention_args& a, cudaStream_t st);
 // dQ partials) and dsum >= batch*heads words zero-initialised once (tickets, left reset)
 int attention_bwd_tc(const gx_attention_args& a, cudaStream_t st);
 int attention_bwd(const gx_attention_args& a, cudaStream_t st);
+// LayerNorm kernels: a NULL `mean` (fwd: not written; bwd: not read) selects RMSNorm (T5):
+// y = x * rsqrt(mean(x^2) + 1e-6) * gamma, no centring, no beta (dbeta is left untouched).
 int layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, void* mean,
                   void* rstd, int rows, int h, cudaStream_t st);
 // workspace: layernorm_bwd_ws_floats(h) fp32 words, zero-initialised once (column-pass
@@ -118,8 +120,9 @@ struct PtrPack {
 int sum_ptrs(const PtrPack& srcs, void* out, int64_t n, bool bf16, cudaStream_t st);
 // Flat per-rank parameter layout (slot order ln1g ln1b ln2g ln2b bqkv bo b1 b2 wqkv wo w1 w2,
 // then the patch-merging mlng mlnb wm, empty unless the layer merges).
+constexpr int kInitSlots = 25;
 struct InitLayout {
-  int64_t off[24], n[24];  // + cross-attention ln3g ln3b bq2 bkv2 bo2 wq2 wkv2 wo2, rpb
+  int64_t off[kInitSlots], n[kInitSlots];  // + cross ln3g ln3b bq2 bkv2 bo2 wq2 wkv2 wo2, rpb, relb
   int64_t h, f;
   int extra;               // 0 none, 1 patch merging, 2 cross-attention (after w_2)
   int t, tr;
@@ -141,6 +144,11 @@ int window_roll(const void* src, void* dst, int samples, int grid, int ws, int s
 // b < batch and the (q, k) pairs of offset e of dpart[b * heads + h][q][k]
 int rpb_grad(const float* dpart, int batch, int heads, int side, float* grad, bool accumulate,
              cudaStream_t st);
+// T5 relative attention bias gradient (attention.cu): grad[h][b] (+)= fixed-order sum over
+// sequence tiles, key blocks and relative positions d with map[d] == b of the backward's
+// relb_dpart partials ([tiles*heads][ceil(seq/128)][2 seq - 1])
+int relb_grad(const float* dpart, int tiles, int heads, int seq, const void* map, int buckets,
+              float* grad, bool accumulate, cudaStream_t st);
 int num_sms();
 
 }  // namespace gx

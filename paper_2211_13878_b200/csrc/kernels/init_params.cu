@@ -19,7 +19,7 @@ __device__ int64_t canon_of(const InitLayout& L, int64_t j) {
                 c_wo = c_wqkv + 3 * h * h, c_w1 = c_wo + h * h, c_w2 = c_w1 + f * h;
   const int64_t c_m = c_w2 + h * f;  // patch merging (mln_g, mln_b, w_m), unsharded
   int s = -1;
-  for (int i = 0; i < 24; ++i)
+  for (int i = 0; i < kInitSlots; ++i)
     if (j >= L.off[i] && j < L.off[i] + L.n[i]) s = i;
   if (s < 0) return -1;
   const int64_t k = j - L.off[s];
@@ -48,8 +48,10 @@ __device__ int64_t canon_of(const InitLayout& L, int64_t j) {
     case 20: return c_m + 6 * h + (tr * ht + k / h) * h + k % h;          // w_q2
     case 21: return c_m + 6 * h + h * h + ((k / h) / ht * h + tr * ht + (k / h) % ht) * h + k % h;
     case 22: return c_m + 6 * h + 3 * h * h + (k / ht) * h + tr * ht + k % ht;  // w_o2
-    // relative-position bias, after w_2 (+ the merge block): this rank's heads are contiguous
-    default: return c_m + (L.extra == 1 ? 4 * h + 2 * h * h : 0) + tr * L.n[23] + k;
+    // Swin relative-position bias, after w_2 (+ the merge block): this rank's heads contiguous
+    case 23: return c_m + (L.extra == 1 ? 4 * h + 2 * h * h : 0) + tr * L.n[23] + k;
+    // T5 relative attention bias, after w_2 (+ the cross block), this rank's heads contiguous
+    default: return c_m + (L.extra == 2 ? 6 * h + 4 * h * h : 0) + tr * L.n[24] + k;
   }
 }
 

@@ -18,6 +18,9 @@ namespace gx {
 namespace {
 
 constexpr float kLnEps = 1e-5f;
+// RMSNorm (T5): selected by a null `mean` pointer -- y = x * rsqrt(mean(x^2) + 1e-6) * gamma,
+// no centring and no beta (its gradient is left untouched)
+constexpr float kRmsEps = 1e-6f;
 
 #define GX_RC(expr)                 \
   do {                              \
@@ -131,7 +134,8 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const uint4* __restr
         for (int j = 0; j < 8; ++j) v[c][j] = 0.f;
       }
     }
-    const float mu = warp_sum(s) / static_cast<float>(h);
+    const bool rms = mean == nullptr;
+    const float mu = rms ? 0.f : warp_sum(s) / static_cast<float>(h);
     float ss = 0.f;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -143,22 +147,22 @@ __global__ void __launch_bounds__(256) layernorm_fwd_kernel(const uint4* __restr
         }
       }
     }
-    const float rs = rsqrtf(warp_sum(ss) / static_cast<float>(h) + kLnEps);
+    const float rs = rsqrtf(warp_sum(ss) / static_cast<float>(h) + (rms ? kRmsEps : kLnEps));
     uint4* yr = y + static_cast<int64_t>(r) * chunks;
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
       const int ci = c * 32 + lane;
       if (ci < chunks) {
-        float gm[8], bt[8], o[8];
+        float gm[8], bt[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, o[8];
         unpack8(__ldg(gamma + ci), gm);
-        unpack8(__ldg(beta + ci), bt);
+        if (!rms) unpack8(__ldg(beta + ci), bt);
 #pragma unroll
         for (int j = 0; j < 8; ++j) o[j] = (v[c][j] - mu) * rs * gm[j] + bt[j];
         yr[ci] = pack8(o);
       }
     }
     if (lane == 0) {
-      mean[r] = mu;
+      if (!rms) mean[r] = mu;
       rstd[r] = rs;
     }
   }
@@ -214,7 +218,8 @@ __global__ void __launch_bounds__(kMaxThreads) layernorm_bwd_rows_kernel(
   const int r = blockIdx.x;
   const bool active = ci < chunks;
   const int64_t i = static_cast<int64_t>(r) * chunks + ci;
-  const float mu = mean[r], rs = rstd[r];
+  const bool rms = mean == nullptr;
+  const float mu = rms ? 0.f : mean[r], rs = rstd[r];
   float xh[8], dv[8], gm[8], rv[8];
   float s1 = 0.f, s2 = 0.f;
   if (active) {
@@ -270,7 +275,7 @@ __global__ void __launch_bounds__(kMaxThreads) layernorm_bwd_rows_kernel(
     t2 += red[1][w];
   }
   if (!active) return;
-  const float m1 = t1 / static_cast<float>(h), m2 = t2 / static_cast<float>(h);
+  const float m1 = rms ? 0.f : t1 / static_cast<float>(h), m2 = t2 / static_cast<float>(h);
   float o[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) o[j] = rs * (dv[j] * gm[j] - m1 - xh[j] * m2) + rv[j];
@@ -316,7 +321,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cols_kernel(
       float xv[8], dv[8];
       unpack8(x[i], xv);
       load8s<kF32Dy>(dy, i, dv, dy_slices, dy_stride);
-      const float mu = mean[r], rs = rstd[r];
+      const float mu = mean != nullptr ? mean[r] : 0.f, rs = rstd[r];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         ag[j] += dv[j] * ((xv[j] - mu) * rs);
@@ -347,9 +352,10 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cols_kernel(
   if (owner) {
     for (int rl = 0; rl < 32; ++rl) s += red[rl][t];
   }
-  float* outs[3] = {dgamma, dbeta, dbias};
+  // RMSNorm (null mean): no beta, so its gradient is not touched
+  float* outs[3] = {dgamma, mean != nullptr ? dbeta : nullptr, dbias};
   if (slices == 1) {
-    if (owner) outs[t >> 6][col] += s;
+    if (owner && outs[t >> 6] != nullptr) outs[t >> 6][col] += s;
     return;
   }
   if (owner) ws[static_cast<int64_t>(blockIdx.y) * width + (t >> 6) * h + col] = s;
@@ -363,7 +369,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cols_kernel(
     float acc = 0.f;
     for (int y = 0; y < slices; ++y)
       acc += __ldcg(ws + static_cast<int64_t>(y) * width + (t >> 6) * h + col);
-    outs[t >> 6][col] += acc;
+    if (outs[t >> 6] != nullptr) outs[t >> 6][col] += acc;
   }
   if (threadIdx.x == 0) tickets[strip] = 0u;  // ready for the next call / graph replay
 }
@@ -542,7 +548,8 @@ __global__ void __launch_bounds__(512) residual_layernorm_kernel(
     unpack8(yb, v);  // the LayerNorm sees the stored bf16 values
   }
   if (gamma == nullptr) return;
-  // mean, then variance about it (two-pass, as layernorm_fwd)
+  // mean, then variance about it (two-pass, as layernorm_fwd); RMSNorm: no centring
+  const bool rms = mean == nullptr;
   float s1 = 0.f;
 #pragma unroll
   for (int j = 0; j < 8; ++j) s1 += v[j];
@@ -551,7 +558,7 @@ __global__ void __launch_bounds__(512) residual_layernorm_kernel(
   __syncthreads();
   float t = 0.f;
   for (int w = 0; w < nwarps; ++w) t += red[w];
-  const float mu = t / static_cast<float>(h);
+  const float mu = rms ? 0.f : t / static_cast<float>(h);
   float s2 = 0.f;
   if (active) {
 #pragma unroll
@@ -566,17 +573,17 @@ __global__ void __launch_bounds__(512) residual_layernorm_kernel(
   __syncthreads();
   float t2 = 0.f;
   for (int w = 0; w < nwarps; ++w) t2 += red[w];
-  const float rs = rsqrtf(t2 / static_cast<float>(h) + kLnEps);
+  const float rs = rsqrtf(t2 / static_cast<float>(h) + (rms ? kRmsEps : kLnEps));
   if (active) {
-    float gm[8], bt[8], o[8];
+    float gm[8], bt[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, o[8];
     unpack8(__ldg(gamma + ci), gm);
-    unpack8(__ldg(beta + ci), bt);
+    if (!rms) unpack8(__ldg(beta + ci), bt);
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[j] = (v[j] - mu) * rs * gm[j] + bt[j];
     ln[i] = pack8(o);
   }
   if (threadIdx.x == 0) {
-    mean[r] = mu;
+    if (!rms) mean[r] = mu;
     rstd[r] = rs;
   }
 }

@@ -70,6 +70,7 @@ Layout make_layout(const Shape& s, int tp, int sdp) {
   put(L.bkv2, 2 * xht);
   put(L.bo2, xh);
   put(L.rpb, s.rpb ? static_cast<int64_t>(s.heads / tp) * s.rpb_n() : 0);
+  put(L.relb, static_cast<int64_t>(s.heads / tp) * s.relb);
   L.acc_end = off;
   put(L.wqkv, 3 * h / tp * h);
   put(L.wo, h * (h / tp));
@@ -90,7 +91,9 @@ int64_t canonical_size(const Shape& s) {
   // ln3_g ln3_b b_q2 b_kv2(2h) b_o2, w_q2 [h][h], w_kv2 [2h][h], w_o2 [h][h]
   const int64_t cross = s.cross ? 6 * h + 4 * h * h : 0;
   const int64_t rpb = s.rpb ? static_cast<int64_t>(s.heads) * s.rpb_n() : 0;
-  return 4 * h + 3 * h + h + f + h + 3 * h * h + h * h + f * h + h * f + merge + cross + rpb;
+  const int64_t relb = static_cast<int64_t>(s.heads) * s.relb;  // T5 table [heads][buckets]
+  return 4 * h + 3 * h + h + f + h + 3 * h * h + h * h + f * h + h * f + merge + cross + rpb +
+         relb;
 }
 
 namespace {
@@ -139,6 +142,7 @@ int64_t canon_index(const Shape& s, const Layout& L, int t, int tr, int64_t j) {
   }
   if (in(L.wo2, k)) return c_m + 6 * h + 3 * h * h + (k / ht) * h + tr * ht + k % ht;
   if (in(L.rpb, k)) return c_m + (s.merge ? 4 * h + 2 * h * h : 0) + tr * L.rpb.n + k;
+  if (in(L.relb, k)) return c_m + (s.cross ? 6 * h + 4 * h * h : 0) + tr * L.relb.n + k;
   return -1;
 }
 
@@ -226,8 +230,36 @@ struct RankLayer {
   int64_t shard_n = 0;
   float *master = nullptr, *m = nullptr, *v = nullptr, *gfull = nullptr, *gshard = nullptr;
   bf16 *pshard = nullptr, *pfull = nullptr;
+  int8_t* relb_map = nullptr;  // T5: bucket of each relative position k - q + seq - 1
   std::vector<Acts> acts;  // per micro-batch
 };
+
+// T5's relative-position bucket of d = k - q (the published bucketing; pinned against
+// transformers' T5Attention in tests/test_layer_oracle.py), bidirectional unless causal,
+// max distance 128, computed in double as oracle/layer_oracle.py::t5_buckets does.
+static std::vector<int8_t> t5_bucket_map(int seq, bool bidirectional, int buckets) {
+  std::vector<int8_t> out(2 * seq - 1);
+  for (int i = 0; i < 2 * seq - 1; ++i) {
+    int n = -(i - (seq - 1));  // query - key
+    int nb = buckets, ret = 0;
+    if (bidirectional) {
+      nb /= 2;
+      ret = n < 0 ? nb : 0;
+      n = n < 0 ? -n : n;
+    } else {
+      n = n > 0 ? n : 0;
+    }
+    const int max_exact = nb / 2;
+    int v = n;
+    if (n >= max_exact) {
+      v = max_exact + static_cast<int>(std::log(static_cast<double>(n) / max_exact) /
+                                       std::log(128.0 / max_exact) * (nb - max_exact));
+      v = std::min(v, nb - 1);
+    }
+    out[i] = static_cast<int8_t>(ret + v);
+  }
+  return out;
+}
 
 struct RankCtx {
   int rank = 0, stage = 0, idx = 0;
@@ -255,6 +287,7 @@ struct RankCtx {
   bf16 *dout2 = nullptr, *dqkv2 = nullptr;
   bf16 *dctxr = nullptr, *rollbuf = nullptr;  // SW-MSA backward scratch (rolled dctx, da)
   float* rpb_part = nullptr;  // relative-position bias: per-(window, head) score gradients
+  float* relb_part = nullptr;  // T5 bias: per-(sequence x head, key block) relative-position sums
   float* dmem = nullptr;
   int dec_li = -1;  // local index of the model's first decoder layer on this rank, or -1
   // stages after the first decoder layer's: the memory received with each micro-batch's
@@ -753,6 +786,20 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
         s.shift = g > ws ? ws / 2 : 0;  // one window covers the grid: Swin skips the shift
       }
       s.rpb = kind == "window" && sh.value("rel_pos", false);
+      {
+        const std::string norm = sh.value("norm", std::string("layer"));
+        if (norm != "layer" && norm != "rms") {
+          *err = "executor: shape norm must be \"layer\" or \"rms\"";
+          return kErrConfig;
+        }
+        s.rms = norm == "rms";
+      }
+      s.relb = sh.value("rel_bias", 0);
+      if (s.relb < 0 || s.relb > 127 || (s.relb > 0 && (kind == "window" || s.hd > 64))) {
+        *err = "executor: rel_bias (T5 buckets, 1..127) needs a full-attention layer with "
+               "head_dim <= 64";
+        return kErrConfig;
+      }
       s.merge = sh.value("merge", false);
       if (s.merge) {
         const int g = static_cast<int>(std::lround(std::sqrt(static_cast<double>(s.seq))));
@@ -982,7 +1029,7 @@ int ExecutorImpl::allocate(RankCtx& r) {
   int64_t max_rows = 0, max_h = 0, max_f = 0, max_q = 0, max_c = 0, max_lse = 0, max_m = 0,
           max_x = 0;
   bool any_shift = false;
-  int64_t max_rpb = 0;
+  int64_t max_rpb = 0, max_relb = 0;
   for (size_t li = 0; li < r.layers.size(); ++li) {
     RankLayer& L = r.layers[li];
     const Shape& s = L.sh;
@@ -1049,13 +1096,16 @@ int ExecutorImpl::allocate(RankCtx& r) {
         if (thr_attn_ != 0u)
           a.amask2 = A.a<uint16_t>(static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq *
                                    ((s.seq + 63) / 64) * 4);
-        a.mean3 = A.a<float>(rows);
+        a.mean3 = s.rms ? nullptr : A.a<float>(rows);  // (null mean: RMSNorm)
         a.rstd3 = A.a<float>(rows);
         max_x = std::max(max_x, rows * h);
       }
       if (s.rpb)
         max_rpb = std::max<int64_t>(max_rpb, static_cast<int64_t>(a.samples) * s.windows() *
                                                  (s.heads / t) * s.rpb_n());
+      if (s.relb)
+        max_relb = std::max<int64_t>(max_relb, static_cast<int64_t>(a.samples) * (s.heads / t) *
+                                                   ((s.seq + 127) / 128) * (2 * s.seq - 1));
       if (s.shift > 0) {
         a.ln1r = A.a<bf16>(rows * h);
         a.ctxr = A.a<bf16>(rows * ht);
@@ -1065,9 +1115,9 @@ int ExecutorImpl::allocate(RankCtx& r) {
       if (thr_attn_ != 0u)
         a.amask = A.a<uint16_t>(static_cast<int64_t>(a.samples) * (s.heads / t) * s.seq *
                                 ((s.win + 63) / 64) * 4);
-      a.mean1 = A.a<float>(rows);
+      a.mean1 = s.rms ? nullptr : A.a<float>(rows);  // (null mean: RMSNorm)
       a.rstd1 = A.a<float>(rows);
-      a.mean2 = A.a<float>(rows);
+      a.mean2 = s.rms ? nullptr : A.a<float>(rows);
       a.rstd2 = A.a<float>(rows);
       max_rows = std::max(max_rows, rows);
       max_h = std::max(max_h, rows * h);
@@ -1099,6 +1149,15 @@ int ExecutorImpl::allocate(RankCtx& r) {
     r.rollbuf = A.a<bf16>(max_h);
   }
   if (max_rpb > 0) r.rpb_part = A.a<float>(max_rpb);
+  if (max_relb > 0) r.relb_part = A.a<float>(max_relb);
+  for (RankLayer& L : r.layers)
+    if (L.sh.relb > 0) {
+      const std::vector<int8_t> map = t5_bucket_map(L.sh.seq, !L.sh.causal, L.sh.relb);
+      L.relb_map = A.a<int8_t>(static_cast<int64_t>(map.size()));
+      if (L.relb_map != nullptr &&
+          cudaMemcpy(L.relb_map, map.data(), map.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+        return set_error(kErrCuda, "executor: relb map upload failed");
+    }
   if (max_x > 0) {
     int64_t hx = 0;
     for (const RankLayer& L : r.layers) hx = std::max<int64_t>(hx, L.sh.h);
@@ -1267,13 +1326,14 @@ int ExecutorImpl::init_params(uint64_t seed, float std_dev) {
   for (auto& r : ranks_) {
     for (RankLayer& L : r->layers) {
       InitLayout il{};
-      const Slot* slots[24] = {&L.lay.ln1g, &L.lay.ln1b, &L.lay.ln2g, &L.lay.ln2b, &L.lay.bqkv,
-                               &L.lay.bo,   &L.lay.b1,   &L.lay.b2,   &L.lay.wqkv, &L.lay.wo,
-                               &L.lay.w1,   &L.lay.w2,   &L.lay.mlng, &L.lay.mlnb, &L.lay.wm,
-                               &L.lay.ln3g, &L.lay.ln3b, &L.lay.bq2,  &L.lay.bkv2, &L.lay.bo2,
-                               &L.lay.wq2,  &L.lay.wkv2, &L.lay.wo2,  &L.lay.rpb};
+      const Slot* slots[kInitSlots] = {
+          &L.lay.ln1g, &L.lay.ln1b, &L.lay.ln2g, &L.lay.ln2b, &L.lay.bqkv, &L.lay.bo,
+          &L.lay.b1,   &L.lay.b2,   &L.lay.wqkv, &L.lay.wo,   &L.lay.w1,   &L.lay.w2,
+          &L.lay.mlng, &L.lay.mlnb, &L.lay.wm,   &L.lay.ln3g, &L.lay.ln3b, &L.lay.bq2,
+          &L.lay.bkv2, &L.lay.bo2,  &L.lay.wq2,  &L.lay.wkv2, &L.lay.wo2,  &L.lay.rpb,
+          &L.lay.relb};
       il.extra = L.sh.merge ? 1 : (L.sh.cross ? 2 : 0);
-      for (int i = 0; i < 24; ++i) {
+      for (int i = 0; i < kInitSlots; ++i) {
         il.off[i] = slots[i]->off;
         il.n[i] = slots[i]->n;
       }
@@ -1433,6 +1493,11 @@ int ExecutorImpl::fwd_phase(RankCtx& r, int li, int mb, int phase) {
     if (s.rpb) {
       at.rpb = P + L.lay.rpb.off;
       at.rpb_side = side_of(s);
+    }
+    if (s.relb) {  // T5 relative bias of this rank's heads
+      at.relb = P + L.lay.relb.off;
+      at.relb_map = L.relb_map;
+      at.relb_buckets = s.relb;
     }
     at.drop_threshold = thr_attn_;
     at.drop_scale = scale_of(p_attn_);
@@ -1745,6 +1810,12 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       at.rpb_side = side_of(s);
       at.rpb_dpart = r.rpb_part;
     }
+    if (s.relb) {
+      at.relb = P + L.lay.relb.off;
+      at.relb_map = L.relb_map;
+      at.relb_buckets = s.relb;
+      at.relb_dpart = r.relb_part;
+    }
     at.dctx = s.shift > 0 ? r.dctxr : r.dctx;
     at.dqkv = dqkv;
     at.dq_accum = r.dq_acc;
@@ -1760,6 +1831,13 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       const double af = 10.0 * A.samples * (s.heads / t) * double(s.seq) * s.win * s.hd;
       GX_TRY(timed(kAttnBwd, af, 2.0 * rows * 8 * ht, [&] { return attention_bwd(at, stream_); }));
     }
+    if (s.relb)  // T5 table gradient: fixed-order sum over sequences, key blocks, positions
+      GX_TRY(timed(kElementwise, 0, 4.0 * A.samples * (s.heads / t) * ((s.seq + 127) / 128) *
+                                        (2.0 * s.seq - 1), [&] {
+        const int wpt = s.seq <= 64 ? 128 / s.seq : 1;  // sequences per attention tile
+        return relb_grad(r.relb_part, (A.samples + wpt - 1) / wpt, s.heads / t, s.seq,
+                         L.relb_map, s.relb, G + L.lay.relb.off, true, stream_);
+      }));
     if (s.rpb)  // table gradient: fixed-order sum of the per-window score gradients
       GX_TRY(timed(kElementwise, 0, 4.0 * A.samples * s.windows() * (s.heads / t) * s.rpb_n(), [&] {
         return rpb_grad(r.rpb_part, A.samples * s.windows(), s.heads / t, side_of(s),

@@ -44,6 +44,10 @@ struct Shape {
   bool causal = false, cross = false;
   int shift = 0;  // Swin SW-MSA: tokens rolled by -shift in both grid axes around attention
   bool rpb = false;  // Swin relative-position bias table [heads][(2 side - 1)^2]
+  // T5: RMSNorm for every LayerNorm of the layer (gain only, eps 1e-6), and the bucketed
+  // relative attention bias of the self-attention (relb buckets, 0 = none; max distance 128)
+  bool rms = false;
+  int relb = 0;
   int rpb_n() const {  // table entries per head
     int w = 1;
     while (w * w < win) ++w;
@@ -63,6 +67,7 @@ struct Layout {
   // cross-attention (empty unless Shape::cross): LN3, q / kv / out projections
   Slot ln3g, ln3b, bq2, bkv2, bo2, wq2, wkv2, wo2;
   Slot rpb;  // Swin relative-position bias, this rank's heads (gradient accumulated)
+  Slot relb;  // T5 relative attention bias [heads / tp][buckets] (gradient accumulated)
   int64_t acc_end = 0;  // [0, acc_end): params whose grads accumulate with atomics
   int64_t total = 0;    // padded to a multiple of 64 * sdp
   int64_t shard() const { return total; }

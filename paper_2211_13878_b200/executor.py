@@ -22,13 +22,15 @@ CROSS_ORDER = ("ln3_g", "ln3_b", "b_q2", "b_kv2", "b_o2", "w_q2", "w_kv2", "w_o2
 def pack_canonical(P: dict) -> np.ndarray:
     """Layer parameter dict (oracle naming) -> canonical flat fp32 vector."""
     keys = CANONICAL_ORDER + (MERGE_ORDER if "w_m" in P else ()) + \
-        (CROSS_ORDER if "w_q2" in P else ()) + (("rpb",) if "rpb" in P else ())
+        (CROSS_ORDER if "w_q2" in P else ()) + (("rpb",) if "rpb" in P else ()) + \
+        (("relb",) if "relb" in P else ())
     return np.concatenate([np.asarray(P[k], dtype=np.float32).ravel() for k in keys])
 
 
 def unpack_canonical(flat: np.ndarray, hidden: int, ffn: int, merge: bool = False,
-                     cross: bool = False, rpb=None) -> dict:
-    """rpb: (heads, entries per head) of a relative-position-bias table, or None."""
+                     cross: bool = False, rpb=None, relb=None) -> dict:
+    """rpb: (heads, entries per head) of a Swin relative-position-bias table, or None;
+    relb: (heads, buckets) of a T5 relative attention bias table, or None."""
     h, f = hidden, ffn
     shapes = {"ln1_g": (h,), "ln1_b": (h,), "ln2_g": (h,), "ln2_b": (h,), "b_qkv": (3 * h,),
               "b_o": (h,), "b_1": (f,), "b_2": (h,), "w_qkv": (3 * h, h), "w_o": (h, h),
@@ -39,8 +41,10 @@ def unpack_canonical(flat: np.ndarray, hidden: int, ffn: int, merge: bool = Fals
     out, off = {}, 0
     if rpb is not None:
         shapes["rpb"] = tuple(rpb)
+    if relb is not None:
+        shapes["relb"] = tuple(relb)
     for k in CANONICAL_ORDER + (MERGE_ORDER if merge else ()) + (CROSS_ORDER if cross else ()) + \
-            (("rpb",) if rpb is not None else ()):
+            (("rpb",) if rpb is not None else ()) + (("relb",) if relb is not None else ()):
         n = int(np.prod(shapes[k]))
         out[k] = flat[off:off + n].reshape(shapes[k])
         off += n
@@ -118,9 +122,15 @@ class PlanExecutor:
         _lib.lib().gx_exec_canonical_size(s["hidden"], s["ffn"], ctypes.byref(n))
         h = s["hidden"]
         rp = self._rpb_shape(s)
+        rb = self._relb_shape(s)
         return n.value + (4 * h + 2 * h * h if s.get("merge") else 0) + \
             (6 * h + 4 * h * h if s.get("kind") == "decoder" else 0) + \
-            (rp[0] * rp[1] if rp else 0)
+            (rp[0] * rp[1] if rp else 0) + (rb[0] * rb[1] if rb else 0)
+
+    @staticmethod
+    def _relb_shape(s):
+        b = int(s.get("rel_bias", 0) or 0)
+        return (s["heads"], b) if b > 0 and s.get("kind") != "window" else None
 
     @staticmethod
     def _rpb_shape(s):
@@ -142,7 +152,8 @@ class PlanExecutor:
             out.ctypes.data_as(ctypes.c_void_p), n))
         s = self.shapes[layer]
         return unpack_canonical(out, s["hidden"], s["ffn"], bool(s.get("merge")),
-                                s.get("kind") == "decoder", self._rpb_shape(s))
+                                s.get("kind") == "decoder", self._rpb_shape(s),
+                                self._relb_shape(s))
 
     @property
     def stream(self) -> int:

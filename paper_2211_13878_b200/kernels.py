@@ -104,7 +104,9 @@ class _AttnArgs(ctypes.Structure):
                 ("seed_offset", ctypes.c_void_p), ("mask", ctypes.c_void_p),
                 ("trace", ctypes.c_void_p), ("causal", ctypes.c_int),
                 ("win_grid", ctypes.c_int), ("win_side", ctypes.c_int), ("win_shift", ctypes.c_int),
-                ("rpb", ctypes.c_void_p), ("rpb_dpart", ctypes.c_void_p), ("rpb_side", ctypes.c_int)]
+                ("rpb", ctypes.c_void_p), ("rpb_dpart", ctypes.c_void_p), ("rpb_side", ctypes.c_int),
+                ("relb", ctypes.c_void_p), ("relb_map", ctypes.c_void_p),
+                ("relb_buckets", ctypes.c_int), ("relb_dpart", ctypes.c_void_p)]
 
 
 class Dropout(ctypes.Structure):
@@ -123,9 +125,13 @@ def make_dropout(p, seed, site, row_offset=0, col_offset=0, drop_ld=0):
 
 
 def _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, heads_total=None, head_offset=0,
-               sample_offset=0, causal=False, win=None, rpb=None, rpb_dpart=None):
+               sample_offset=0, causal=False, win=None, rpb=None, rpb_dpart=None, relb=None,
+               relb_map=None, relb_dpart=None):
     a = _AttnArgs()
     a.causal = int(causal)
+    if relb is not None:  # T5 relative bias: bf16 [heads][buckets] + int8 bucket map [2 seq - 1]
+        a.relb, a.relb_map, a.relb_buckets = _ptr(relb), _ptr(relb_map), relb.shape[1]
+        a.relb_dpart = _ptr(relb_dpart) if relb_dpart is not None else None
     if rpb is not None:  # Swin relative-position bias table [heads][(2 side - 1)^2] (bf16)
         a.rpb, a.rpb_side = _ptr(rpb), int(round(seq ** 0.5))
         a.rpb_dpart = _ptr(rpb_dpart) if rpb_dpart is not None else None
@@ -180,6 +186,13 @@ def attention_bwd(qkv, ctx, lse, dctx, batch, seq, heads, head_dim, p=0.0, seed=
     a.trace = _ptr(trace)
     _lib.check(_lib.lib().gx_k_attention_bwd(ctypes.addressof(a), _lib.stream_ptr()))
     return dqkv
+
+
+def relb_grad(dpart, tiles, heads, seq, relb_map, buckets, out, accumulate=False):
+    """T5 relative-bias table gradient from attention_bwd's relb_dpart partials."""
+    _lib.check(_lib.lib().gx_k_relb_grad(_ptr(dpart), tiles, heads, seq, _ptr(relb_map), buckets,
+                                         _ptr(out), int(accumulate), _lib.stream_ptr()))
+    return out
 
 
 def layernorm_fwd(x, gamma, beta):

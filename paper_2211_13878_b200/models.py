@@ -55,9 +55,14 @@ def layer_param_count(shape) -> int:
 
 def _t5(n, param_bytes, act_bytes, fwd_ms, shape):
     """T5 flattened into one layer list: n/2 encoder layers, then n/2 decoder
-    layers (causal self-attention + cross-attention over the encoder output + MLP).  The
-    planner numbers stay uniform, as in the paper's Table 2 totals."""
+    layers (causal self-attention + cross-attention over the encoder output + MLP), with T5's
+    RMSNorm and the bucketed relative attention bias in every self-attention (bidirectional in
+    the encoder, causal in the decoder; each layer owns its table).  The planner numbers stay
+    uniform, as in the paper's Table 2 totals."""
     m = _uniform(n, param_bytes, act_bytes, fwd_ms, shape)
+    for layer in m["layers"]:
+        layer["shape"]["norm"] = "rms"      # T5LayerNorm (gain only)
+        layer["shape"]["rel_bias"] = 32     # bucketed relative attention bias, max distance 128
     for layer in m["layers"][n // 2:]:
         layer["shape"]["kind"] = "decoder"
     return m

@@ -55,7 +55,8 @@ def _oshape(shp):
                          shp.get("window", 0) if kind == "window" else 0,
                          bool(shp.get("merge", False)), kind in ("causal", "decoder"),
                          kind == "decoder", shift,
-                         bool(kind == "window" and shp.get("rel_pos", False)))
+                         bool(kind == "window" and shp.get("rel_pos", False)),
+                         shp.get("norm", "layer") == "rms", int(shp.get("rel_bias", 0)))
 
 
 def _run_case(plan, model, world, p_drop=0.0, seed=11, optimizer=False, std=0.02):
@@ -326,6 +327,31 @@ def test_t5_decoder_plans(cuda, case, p_drop):
     out = _run_case(gxe.make_plan(strategies, B, P, m, bounds), _t5_like(), world, p_drop)
     _check(out)
     assert {"w_q2", "w_kv2", "w_o2", "ln3_g"} <= set(out["grads"][2][1])
+
+
+T5_PROPER_CASES = [
+    (1, ["", "", "", ""], 2, 1, 1, None),
+    (2, ["tp:2", "tp:2", "tp:2", "tp:2"], 2, 1, 1, None),          # bias table split by heads
+    (4, ["dp:4", "sdp:4", "tp:2,sdp:2", "sdp:2,tp:2"], 4, 1, 1, None),
+    (2, ["", "", "", ""], 4, 2, 2, [0, 2, 4]),
+]
+
+
+@pytest.mark.parametrize("case", T5_PROPER_CASES, ids=lambda c: f"N{c[0]}-{'|'.join(s or 'serial' for s in c[1])}-P{c[3]}m{c[4]}")
+def test_t5_rmsnorm_relative_bias_plans(cuda, case):
+    """T5 proper: RMSNorm everywhere and the bucketed relative attention bias (32 buckets,
+    bidirectional in the encoder, causal in the decoder) at 160 tokens, so exact and
+    log-spaced buckets and two key blocks are exercised; the tables' gradients included."""
+    world, strategies, B, P, m, bounds = case
+    model = _t5_like(seq=160)
+    for layer in model["layers"]:
+        layer["shape"].update(norm="rms", rel_bias=32)
+    out = _run_case(gxe.make_plan(strategies, B, P, m, bounds), model, world, 0.1)
+    _check(out)
+    for l in range(4):
+        g = out["grads"][l][0]
+        assert np.all(g["ln1_b"] == 0) and np.all(g["ln2_b"] == 0)  # RMSNorm: no beta
+        assert "relb" in g and np.abs(g["relb"]).sum() > 0
 
 
 @pytest.mark.parametrize("strategies,world", [(["", "", ""], 1), (["tp:2", "sdp:2", "tp:2"], 2)])

@@ -75,9 +75,12 @@ def test_vit_huge_layers_tp2_sdp4(cuda):
 
 
 def test_t5_large_encoder_decoder_pipeline(cuda):
+    """T5-Large layers proper (RMSNorm, 32-bucket relative attention bias) across P = 2."""
     enc, dec = _enc(1024, 16, 512, 4096), _enc(1024, 16, 512, 4096, "decoder")
+    for sh in (enc, dec):
+        sh.update(norm="rms", rel_bias=32)
     plan = gxe.make_plan(["", "", "", ""], 2, pp_degree=2, micro_batches=2)
-    _check_print("t5-large 2 enc + 2 dec, P=2 m=2 B=2",
+    _check_print("t5-large (rms, rel-bias) 2 enc + 2 dec, P=2 m=2 B=2",
                  _run_case(plan, _model([enc, enc, dec, dec]), 2, 0.1, seed=5))
 
 

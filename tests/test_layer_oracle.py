@@ -95,7 +95,10 @@ def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0, memory=None, n_
     h, H, d, s = shape.hidden, shape.heads, shape.head_dim, shape.att_seq
     n = x.shape[0] // s
     nw, S = shape.seq // s, shape.seq
-    ln = lambda t, g, b: torch.nn.functional.layer_norm(t, (h,), g, b, 1e-5)  # noqa: E731
+    if shape.rms:  # T5LayerNorm: hidden * rsqrt(mean(hidden^2) + eps) * weight
+        ln = lambda t, g, b: t * torch.rsqrt(t.pow(2).mean(-1, keepdim=True) + 1e-6) * g  # noqa: E731
+    else:
+        ln = lambda t, g, b: torch.nn.functional.layer_norm(t, (h,), g, b, 1e-5)  # noqa: E731
     a = ln(x, P["ln1_g"], P["ln1_b"])
     qkv = a @ P["w_qkv"].T + P["b_qkv"]
     am = torch.from_numpy(lo._attn_mask(drop, 3 * layer_id, n, H, s, sample_offset * nw)).double()
@@ -108,6 +111,12 @@ def _torch_layer(P, x, shape, drop, layer_id=0, sample_offset=0, memory=None, n_
         rel = (coords[:, :, None] - coords[:, None, :]).permute(1, 2, 0) + (w - 1)
         rpi = rel[:, :, 0] * (2 * w - 1) + rel[:, :, 1]
         bias = P["rpb"][:, rpi]  # [H, s, s]
+    if shape.relb:  # T5's own bucketing (transformers' T5Attention), bidirectional unless causal
+        from transformers.models.t5.modeling_t5 import T5Attention
+        rp = torch.arange(s)[None, :] - torch.arange(s)[:, None]  # memory - query position
+        bk = T5Attention._relative_position_bucket(rp, bidirectional=not shape.causal,
+                                                   num_buckets=shape.relb, max_distance=128)
+        bias = P["relb"][:, bk]  # [H, s, s]
     if shape.shift:
         g, ws, sh = math.isqrt(S), math.isqrt(s), shape.shift
         a = _raster_to_wm(torch.roll(_wm_to_raster(a, g, ws), (-sh, -sh), (1, 2)), ws)
@@ -205,3 +214,49 @@ def test_t5_encoder_decoder_model_matches_autograd(p):
         assert set(grads[l]) == set(params[l])
         for k in params[l]:
             assert np.allclose(grads[l][k], tP[l][k].grad.numpy(), rtol=1e-8, atol=1e-12), (l, k)
+
+
+def test_t5_buckets_match_transformers():
+    """lo.t5_buckets equals the published T5 bucketing (transformers' T5Attention) over every
+    relative position of a 512-token sequence, both directions."""
+    from transformers.models.t5.modeling_t5 import T5Attention
+    for bi in (True, False):
+        d = torch.arange(-511, 512)
+        hf = T5Attention._relative_position_bucket(d, bidirectional=bi, num_buckets=32,
+                                                   max_distance=128).numpy()
+        assert np.array_equal(hf, lo.t5_buckets(512, bi, 32)), bi
+
+
+@pytest.mark.parametrize("p", [0.0, 0.1])
+def test_t5_rmsnorm_relative_bias_model_matches_autograd(p):
+    """T5 layers proper: RMSNorm everywhere and the bucketed relative attention bias (40
+    tokens: exact and log-spaced buckets), encoder (bidirectional) + causal decoder with
+    cross-attention; loss, dx and every parameter gradient vs torch.autograd."""
+    rng = np.random.default_rng(8)
+    enc = lo.LayerShape(hidden=32, heads=2, seq=40, ffn=64, rms=True, relb=32)
+    dec = lo.LayerShape(hidden=32, heads=2, seq=40, ffn=64, causal=True, cross=True, rms=True,
+                        relb=32)
+    shapes = [enc, dec]
+    params = [lo.init_layer_params(sh, rng, std=0.2) for sh in shapes]
+    x = rng.standard_normal((2 * 40, 32))
+    t = rng.standard_normal((2 * 40, 32))
+    drop = lo.Dropout(p, p, 23)
+    loss, y, dx, grads = lo.model_step(params, x, t, shapes, drop, sample_offset=1)
+
+    tP = [{k: torch.tensor(v, requires_grad=True) for k, v in P.items()} for P in params]
+    tx = torch.tensor(x, requires_grad=True)
+    hcur, mem = tx, None
+    for l, sh in enumerate(shapes):
+        if sh.cross and mem is None:
+            mem = hcur
+        hcur = _torch_layer(tP[l], hcur, sh, drop, l, 1, mem, len(shapes))
+    tl = ((hcur - torch.tensor(t)) ** 2).sum() / hcur.numel()
+    tl.backward()
+    assert abs(loss - tl.item()) <= 1e-10 * abs(loss)
+    assert np.allclose(y, hcur.detach().numpy(), rtol=1e-10, atol=1e-12)
+    assert np.allclose(dx, tx.grad.numpy(), rtol=1e-8, atol=1e-12)
+    for l in range(len(shapes)):
+        for k in params[l]:
+            ref = tP[l][k].grad
+            ref = np.zeros(params[l][k].shape) if ref is None else ref.numpy()  # RMSNorm: no beta
+            assert np.allclose(grads[l][k], ref, rtol=1e-8, atol=1e-12), (l, k)
