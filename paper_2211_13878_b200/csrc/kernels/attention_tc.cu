@@ -554,8 +554,8 @@ __host__ __device__ inline BwdLayout bwd_layout(int np, bool rpb, bool relb = fa
   L.pd = L.d_o + L.nb * tile;
   L.ds = L.pd + 32768;
   L.lse = L.ds + 32768;                  // [512] floats
-  L.dd = L.lse + 2048;                   // [2][128] floats
-  L.mask = L.dd + 1024;                  // [512 q][2 blocks][4] u16
+  L.dd = L.lse + 2048;                   // [512] floats: D of every query
+  L.mask = L.dd + 2048;                  // [512 q][2 blocks][4] u16
   L.win = L.mask + 8192;
   L.ds32 = L.win + static_cast<int>((sizeof(WinSmem) + 15) / 16 * 16);
   L.diag = L.ds32 + (rpb || relb ? kTcQ * kTcQ * 4 : 0);  // fp32 dS [128 q][128 k]
@@ -587,7 +587,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* bar_s = bar_kv + 4;
   uint64_t* bar_mm = bar_kv + 5;
   uint64_t* bar_pds = bar_kv + 6;  // Pd / dS of a chunk stored (all softmax threads)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_kv + 7);
+  uint64_t* bar_sfree = bar_kv + 7;  // S / dPd of a chunk read out of TMEM (all softmax threads)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_kv + 8);
 
   const int warp = static_cast<int>(warp_id());
   const int lane = static_cast<int>(lane_id());
@@ -600,7 +601,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int nkb = (s + 63) / 64;
   const int row0 = vb * g.wpt * s;
   const int tile = np * kTcQ * 128;
-  // TMEM columns (hd is a multiple of 16): S^T, dPd^T, then dV, dK, dQ -- 256 + 3 hd <= 512
+  // TMEM columns (hd is a multiple of 16): S^T, dPd^T, then dV, dK, dQ -- 256 + 3 hd <= 512;
+  // when 256 + 4 hd fits, dQ is double-buffered so chunk j's products run while dQ(j-1)
+  // drains to global memory
+  constexpr bool kDqDbl = 256 + 4 * HD <= 512;
   const uint32_t t_dv = 256, t_dk = 256 + hd, t_dq = 256 + 2 * hd;
 
   if (threadIdx.x == 0) {
@@ -613,6 +617,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(bar_s, 1);
     mbar_init(bar_mm, 1);
     mbar_init(bar_pds, kBwdSoftmax);
+    mbar_init(bar_sfree, kBwdSoftmax);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<512>(tmem_slot);
@@ -632,16 +637,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int u = vb * g.wpt + v / s;
       sLse[v] = u < p.batch ? lse_g[(static_cast<int64_t>(u) * H + h) * s + v % s] : 0.f;
     }
-    for (int i = threadIdx.x; i < 2 * g.vseq; i += kBwdSoftmax) {
+    // (2 vseq <= 1024 words: both of a thread's loads issued before either store)
+    uint64_t w[2];
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int i = threadIdx.x + it * kBwdSoftmax;
       const int v = i >> 1, u = vb * g.wpt + v / s;
       // packed sequences: every query's keys lie in real block 0 (slot 0); else the key
       // block's two 64-key halves
       const int kb = g.wpt > 1 ? 0 : kt * 2 + (i & 1);
-      uint64_t w = 0;
-      if (p.drop_threshold != 0u && kb < nkb && u < p.batch && (g.wpt == 1 || (i & 1) == 0))
-        w = *reinterpret_cast<const uint64_t*>(
+      w[it] = 0;
+      if (i < 2 * g.vseq && p.drop_threshold != 0u && kb < nkb && u < p.batch &&
+          (g.wpt == 1 || (i & 1) == 0))
+        w[it] = *reinterpret_cast<const uint64_t*>(
             mask_g + (((static_cast<int64_t>(u) * H + h) * s + v % s) * nkb + kb) * 4);
-      *reinterpret_cast<uint64_t*>(sMask + i * 4) = w;
+    }
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+      const int i = threadIdx.x + it * kBwdSoftmax;
+      if (i < 2 * g.vseq) *reinterpret_cast<uint64_t*>(sMask + i * 4) = w[it];
     }
     if (kGen) win_stage_tc(p, g, vb, h, win, kBwdSoftmax);
     if (has_relb)
@@ -715,7 +729,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     sdesc_sw128(do_b + k * 2048, 16384, 1024), idesc_kv, acc);
           umma_bf16(tmem + t_dk, sdesc_sw128(sb + BL.ds + a_kmaj, 16, 1024),
                     sdesc_sw128(q_b + k * 2048, 16384, 1024), idesc_kv, acc);
-          umma_bf16(tmem + t_dq, sdesc_sw128(sb + BL.ds + k * 2048, 16384, 1024),
+          umma_bf16(tmem + t_dq + (kDqDbl ? (j & 1) * hd : 0), sdesc_sw128(sb + BL.ds + k * 2048, 16384, 1024),
                     sdesc_sw128(sb + BL.k + k * 2048, 16384, 1024), idesc_q, k > 0 ? 1u : 0u);
         }
         umma_commit(bar_mm);
@@ -732,16 +746,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_wait(bar_kv, 0);
       issue_s(0);
       for (int j = 0; j < nq; ++j) {
-        mbar_wait(bar_pds, j & 1);  // Pd / dS(j) in smem; S / dPd(j) and dQ(j-1) out of TMEM
-        tc_fence_after();
         if (NB == 3) {
-          if (j + 1 < nq) issue_s(j + 1);  // next scores first ...
-          if (j >= 1) {  // chunk j-1's gradients (at most one bar_mm phase is ever pending here)
+          // S / dPd(j) are in registers once bar_sfree(j) completes: the next chunk's scores
+          // go into the same TMEM columns while the softmax warps still work on chunk j
+          mbar_wait(bar_sfree, j & 1);
+          tc_fence_after();
+          if (j + 1 < nq) issue_s(j + 1);  // (chunk j + 1 was loaded one iteration ahead)
+          if (j >= 1) {  // chunk j-1's products are done: its Q / dO buffer takes chunk j + 2
             mbar_wait(bar_mm, (j - 1) & 1);
-            if (j + 2 < nq) load_chunk(j + 2);  // ... its Q / dO buffer takes chunk j + 2
+            if (j + 2 < nq) load_chunk(j + 2);
           }
-          issue_grads(j);                     // ... then this chunk's gradient products
+          mbar_wait(bar_pds, j & 1);  // Pd / dS(j) in smem; dQ buffer j & 1 drained
+          tc_fence_after();
+          issue_grads(j);
         } else {  // one buffer: chunk j's products finish before chunk j + 1 loads into it
+          mbar_wait(bar_pds, j & 1);
+          tc_fence_after();
           issue_grads(j);
           if (j + 1 < nq) {
             mbar_wait(bar_mm, j & 1);
@@ -754,37 +774,57 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     __syncwarp();
   } else {
     // ------------------------------------------------------------ softmax warps (0..15)
-    // D = rowsum(dO * O) of chunk j's 128 queries -> sD[j & 1] (dO from smem, O from global)
-    auto compute_d = [&](int j) {
-      const int bf = j % NB;
-      mbar_wait(&bar_ld[bf], (j / NB) & 1);
-      const int qi = threadIdx.x >> 2, part4 = threadIdx.x & 3;  // 4 threads per query row
-      const int v = j * kTcQ + qi;
-      const uint8_t* dob = smem + BL.d_o + bf * tile + qi * 128;
-      float acc = 0.f;
-      if (v < g.vseq && vb * g.wpt + v / s < p.batch) {
-        const __nv_bfloat16* og = static_cast<const __nv_bfloat16*>(p.ctx) +
-                                  (static_cast<int64_t>(row0) + v) * p.ld_ctx + h * hd;
-        for (int cc = part4; cc < hd / 8; cc += 4) {  // 8-column chunks
-          const int sw = ((cc & 7) ^ (qi & 7)) << 4;
-          const uint4 a = *reinterpret_cast<const uint4*>(dob + (cc >> 3) * 16384 + sw);
-          const uint4 o = *reinterpret_cast<const uint4*>(og + cc * 8);
-          const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, ow[4] = {o.x, o.y, o.z, o.w};
+    // D = rowsum(dO * O) of every query of the tile -> sD (dO and O from global memory, four
+    // threads per query; once, in the prologue, so no chunk waits on it).  Two 128-query passes
+    // at a time with every load issued before the first use (the latency is paid once per
+    // pair of passes, not per load); every lane runs every pass (warp-wide shuffles).
+    {
+      constexpr int kCc = (HD / 8 + 3) / 4;  // 8-column chunks per thread
+      const int qi = threadIdx.x >> 2, part4 = threadIdx.x & 3;
+      for (int v0 = 0; v0 < g.vseq; v0 += kBwdSoftmax / 2) {
+        uint4 da[2][kCc], oa[2][kCc];
 #pragma unroll
-          for (int t = 0; t < 4; ++t)
-            acc += bf16_lo(aw[t]) * bf16_lo(ow[t]) + bf16_hi(aw[t]) * bf16_hi(ow[t]);
+        for (int ps = 0; ps < 2; ++ps) {
+          const int v = v0 + ps * (kBwdSoftmax / 4) + qi;
+          const bool ok = v < g.vseq && vb * g.wpt + v / s < p.batch;
+          const int64_t ro = (static_cast<int64_t>(row0) + v) * p.ld_ctx + h * hd;
+#pragma unroll
+          for (int c = 0; c < kCc; ++c) {
+            const int cc = part4 + 4 * c;
+            if (ok && cc < hd / 8) {
+              da[ps][c] = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.dctx) + ro + cc * 8);
+              oa[ps][c] = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ctx) + ro + cc * 8);
+            } else {
+              da[ps][c] = make_uint4(0u, 0u, 0u, 0u);
+              oa[ps][c] = make_uint4(0u, 0u, 0u, 0u);
+            }
+          }
+        }
+#pragma unroll
+        for (int ps = 0; ps < 2; ++ps) {
+          float acc = 0.f;
+#pragma unroll
+          for (int c = 0; c < kCc; ++c) {  // (zero words add exact zeros)
+            const uint32_t aw[4] = {da[ps][c].x, da[ps][c].y, da[ps][c].z, da[ps][c].w};
+            const uint32_t ow[4] = {oa[ps][c].x, oa[ps][c].y, oa[ps][c].z, oa[ps][c].w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              acc += bf16_lo(aw[t]) * bf16_lo(ow[t]) + bf16_hi(aw[t]) * bf16_hi(ow[t]);
+          }
+          acc += __shfl_xor_sync(0xffffffff, acc, 1);
+          acc += __shfl_xor_sync(0xffffffff, acc, 2);
+          const int v = v0 + ps * (kBwdSoftmax / 4) + qi;
+          if (part4 == 0 && v < g.vseq) sD[v] = acc;
         }
       }
-      acc += __shfl_xor_sync(0xffffffff, acc, 1);
-      acc += __shfl_xor_sync(0xffffffff, acc, 2);
-      if (part4 == 0) sD[(j & 1) * kTcQ + qi] = acc;
-    };
+    }
     // dQ_j partial (fp32) out of TMEM (lane = query row of the chunk, 16 columns per load)
     auto store_dq = [&](int j) {
       const int v = j * kTcQ + kr;
+      const uint32_t tq = t_dq + (kDqDbl ? (j & 1) * hd : 0);
       for (int c16 = cq; c16 < hd / 16; c16 += 4) {
         uint32_t o[16];
-        tmem_ld16(trow + t_dq + c16 * 16, o);
+        tmem_ld16(trow + tq + c16 * 16, o);
         tmem_ld_wait();
         if (v < g.vseq) {
           float4* dst = reinterpret_cast<float4*>(
@@ -796,8 +836,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       }
     };
-    compute_d(0);
-    named_sync(1, kBwdSoftmax);
+    named_sync(1, kBwdSoftmax);  // sD, sLse, sMask and the window metadata staged
     if (kGen && key < kTcQ) {
       if (p.win_shift > 0) kreg = win->reg[key];
       if (p.rpb != nullptr)
@@ -810,7 +849,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       GX_ATTN_STAMP(p, 4 + 5 * j);
       const int c0 = cq * 32;
       const int qg0 = j * kTcQ + c0;  // first virtual query of this warp's 32
-      const float* sDj = sD + (j & 1) * kTcQ;
       uint32_t ppd[16], pds[16];
       {
         // no masking needed for this 32-query x 128-key block
@@ -819,10 +857,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_ld32(trow + c0, sv);
         tmem_ld32(trow + 128 + c0, dv);
         tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(bar_sfree);  // the MMA warp may overwrite S / dPd with the next chunk's
 #pragma unroll
         for (int i4 = 0; i4 < 8; ++i4) {
           const float4 l4 = *reinterpret_cast<const float4*>(sLse + qg0 + 4 * i4);
-          const float4 d4 = *reinterpret_cast<const float4*>(sDj + c0 + 4 * i4);
+          const float4 d4 = *reinterpret_cast<const float4*>(sD + qg0 + 4 * i4);
           const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dd[4] = {d4.x, d4.y, d4.z, d4.w};
           float pd4[4], ds4[4];
 #pragma unroll
@@ -856,10 +896,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       }
       GX_ATTN_STAMP(p, 5 + 5 * j);
-      if (j > 0) {  // chunk j-1's gradient MMAs: done reading Pd / dS; its dQ leaves TMEM
+      if (j > 0) {  // chunk j-1's gradient MMAs are done reading Pd / dS
         mbar_wait(bar_mm, (j - 1) & 1);
         tc_fence_after();
-        store_dq(j - 1);
+        if (!kDqDbl) store_dq(j - 1);  // (single dQ buffer: drained before chunk j's products)
       }
       GX_ATTN_STAMP(p, 6 + 5 * j);
       {
@@ -875,8 +915,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
       }
       fence_proxy_async_smem_tc();
-      tc_fence_before();
-      mbar_arrive(bar_pds);  // the MMA warp may issue S(j+1) and the gradients of j
+      if (kDqDbl && j > 0) {
+        tc_fence_before();
+        mbar_arrive(bar_pds);  // the MMA warp may issue the gradients of chunk j ...
+        store_dq(j - 1);       // ... into the other dQ buffer while this one drains
+      } else {
+        tc_fence_before();
+        mbar_arrive(bar_pds);
+      }
       GX_ATTN_STAMP(p, 7 + 5 * j);
       if (has_relb) {
         // T5 bias gradient: thread t sums the chunk tile's diagonal delta = key - query
@@ -892,10 +938,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           if (idx >= 0 && idx < 2 * s - 1) sDiag[idx] += acc;
         }
       }
-      // sD is double-buffered: sD[(j+1) & 1] was last read in chunk j-1, before every softmax
-      // warp passed the barrier that ended chunk j-1
-      if (j + 1 < nq) compute_d(j + 1);
-      named_sync(1, kBwdSoftmax);  // sD(j+1) visible (and, last chunk, the fp32 dS tile)
+      // the fp32 dS tile (bias gradients) is rewritten by the next chunk: all readers first
+      if (has_rpb || has_relb) named_sync(1, kBwdSoftmax);
       GX_ATTN_STAMP(p, 8 + 5 * j);
     }
     if (has_rpb) {
@@ -958,25 +1002,47 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   cluster_sync();
   GX_ATTN_STAMP(p, 26);
   {
+    // loads of both items of a thread first, then the fixed-order sums (t = 0, 1, ...)
     auto* dq = static_cast<__nv_bfloat16*>(p.dqkv);
+    const float* __restrict__ src0 = part;
     const float sc = p.scale;
     const int q_lo = kt * kTcQ, q_hi = min(g.vseq, q_lo + kTcQ);
     const int c8n = hd / 8;
-#pragma unroll 4
-    for (int idx = threadIdx.x; idx < (q_hi - q_lo) * c8n; idx += kBwdThreads) {
-      const int v = q_lo + idx / c8n, c8 = idx % c8n;
-      if (vb * g.wpt + v / s >= p.batch) continue;
-      float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int t = 0; t < nkt; ++t) {
-        const float4* src = reinterpret_cast<const float4*>(
-            part + ((static_cast<int64_t>(t) * gridDim.y + blockIdx.y) * g.vseq + v) * hd + c8 * 8);
-        const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
-        a[0] += x0.x; a[1] += x0.y; a[2] += x0.z; a[3] += x0.w;
-        a[4] += x1.x; a[5] += x1.y; a[6] += x1.z; a[7] += x1.w;
+    constexpr int kMaxKt = kTcMaxKeys / kTcQ;
+    for (int base = threadIdx.x; base < (q_hi - q_lo) * c8n; base += 2 * kBwdThreads) {
+      float4 x[2][kMaxKt][2];
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const int idx = base + it * kBwdThreads;
+        const int v = q_lo + idx / c8n, c8 = idx % c8n;
+#pragma unroll
+        for (int t = 0; t < kMaxKt; ++t) {
+          if (idx < (q_hi - q_lo) * c8n && t < nkt) {
+            const float4* src = reinterpret_cast<const float4*>(
+                src0 + ((static_cast<int64_t>(t) * gridDim.y + blockIdx.y) * g.vseq + v) * hd + c8 * 8);
+            x[it][t][0] = __ldcg(src);
+            x[it][t][1] = __ldcg(src + 1);
+          } else {
+            x[it][t][0] = x[it][t][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
       }
-      *reinterpret_cast<uint4*>(dq + (static_cast<int64_t>(row0) + v) * p.ld_qkv + h * hd + c8 * 8) =
-          make_uint4(pack_bf16(a[0] * sc, a[1] * sc), pack_bf16(a[2] * sc, a[3] * sc),
-                     pack_bf16(a[4] * sc, a[5] * sc), pack_bf16(a[6] * sc, a[7] * sc));
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const int idx = base + it * kBwdThreads;
+        const int v = q_lo + idx / c8n, c8 = idx % c8n;
+        if (idx >= (q_hi - q_lo) * c8n || vb * g.wpt + v / s >= p.batch) continue;
+        float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int t = 0; t < kMaxKt; ++t) {
+          if (t >= nkt) break;
+          a[0] += x[it][t][0].x; a[1] += x[it][t][0].y; a[2] += x[it][t][0].z; a[3] += x[it][t][0].w;
+          a[4] += x[it][t][1].x; a[5] += x[it][t][1].y; a[6] += x[it][t][1].z; a[7] += x[it][t][1].w;
+        }
+        *reinterpret_cast<uint4*>(dq + (static_cast<int64_t>(row0) + v) * p.ld_qkv + h * hd + c8 * 8) =
+            make_uint4(pack_bf16(a[0] * sc, a[1] * sc), pack_bf16(a[2] * sc, a[3] * sc),
+                       pack_bf16(a[4] * sc, a[5] * sc), pack_bf16(a[6] * sc, a[7] * sc));
+      }
     }
   }
   GX_ATTN_STAMP(p, 27);
