@@ -197,10 +197,11 @@ typedef struct gx_gemm_epilogue {
   uint64_t site;
   int gelu_bwd;               /* out = acc * gelu'(aux) (aux = bf16 pre-activation, read); 2: out = acc * aux */
   const uint64_t* seed_offset;/* optional device counter added to seed (per-step masks) */
-  /* debug: when set, CTA b writes %globaltimer stamps [b][0..15] (entry, after PDL wait,
+  /* debug: when set, CTA b writes %globaltimer stamps [b][0..7] (entry, after PDL wait,
    * first TMA issued, first stage landed, last MMA issued, first accumulator ready, epilogue
-   * done, exit; then per epilogue chunk of warp 4: before / after its TMEM load) -- see
-   * scripts/gemm_trace.py */
+   * done, exit) and SM clock stamps [b][8..15] of epilogue warp 4 (before / after the TMEM
+   * loads of its first two chunks; first block: math start / end, staged, store issued) --
+   * see scripts/gemm_trace.py */
   unsigned long long* trace;
 } gx_gemm_epilogue;
 

@@ -813,8 +813,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           acc += __shfl_xor_sync(0xffffffff, acc, 1);
           acc += __shfl_xor_sync(0xffffffff, acc, 2);
+          // (queries past the tile's end get D = 0: the last chunk reads them, and a stale
+          // smem value could be NaN, which the zero P of a masked pair would not cancel)
           const int v = v0 + ps * (kBwdSoftmax / 4) + qi;
-          if (part4 == 0 && v < g.vseq) sD[v] = acc;
+          if (part4 == 0) sD[v] = acc;
         }
       }
     }

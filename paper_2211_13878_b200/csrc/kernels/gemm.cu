@@ -337,9 +337,9 @@ __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUt
   }
   float v[32], pre[32];
   const bool dstamp = ep.trace != nullptr && lane == 0 && (threadIdx.x >> 5) == 4 && w.sblk == 0;
-  if (dstamp) ep.trace[blockIdx.x * 16 + 12] = gtimer();
+  if (dstamp) ep.trace[blockIdx.x * 16 + 12] = clock64();
   epilogue_math(ep, row, n0, acc, bias_w, in_w, v, pre);
-  if (dstamp) ep.trace[blockIdx.x * 16 + 13] = gtimer();
+  if (dstamp) ep.trace[blockIdx.x * 16 + 13] = clock64();
   // Double-buffered staging, so block i+1's math overlaps block i's store: bf16 outputs use
   // the two halves of the 4 KB out buffer; fp32 outputs (weight gradients: no operand, no
   // aux) use the out buffer and the 4 KB operand/aux area; the GeLU pre-activation output
@@ -367,7 +367,7 @@ __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUt
   if (ep.gelu) stage_bf16_row(abuf, lane, pre);
   fence_proxy_async_smem();
   __syncwarp();
-  if (dstamp) ep.trace[blockIdx.x * 16 + 14] = gtimer();
+  if (dstamp) ep.trace[blockIdx.x * 16 + 14] = clock64();
   if (lane == 0) {
     if (ep.out_kind == kOutF32Accumulate) {
       tma_reduce_add_3d(map_out, obuf, n0, static_cast<int32_t>(m_base), store_z);
@@ -377,7 +377,7 @@ __device__ __forceinline__ void epilogue_block(const GemmEpilogue& ep, const CUt
     if (ep.gelu) tma_store_2d(map_aux, abuf, n0, static_cast<int32_t>(m_base));
     bulk_commit();
   }
-  if (dstamp) ep.trace[blockIdx.x * 16 + 15] = gtimer();
+  if (dstamp) ep.trace[blockIdx.x * 16 + 15] = clock64();
 }
 
 
@@ -406,10 +406,10 @@ __device__ __forceinline__ void epilogue_tile(const GemmEpilogue& ep, const CUte
       epi_prefetch(w, map_aux, w.blk + 1, n0 + (c + 1) * 32, static_cast<int32_t>(m_base));
     uint32_t r[32];
     const bool stamp = ep.trace != nullptr && ew == 0 && lane_id() == 0 && c - c_lo < 2;
-    if (stamp) ep.trace[blockIdx.x * 16 + 8 + 2 * (c - c_lo)] = gtimer();
+    if (stamp) ep.trace[blockIdx.x * 16 + 8 + 2 * (c - c_lo)] = clock64();
     tmem_ld32(taddr + c * 32, r);
     tmem_ld_wait();
-    if (stamp) ep.trace[blockIdx.x * 16 + 9 + 2 * (c - c_lo)] = gtimer();
+    if (stamp) ep.trace[blockIdx.x * 16 + 9 + 2 * (c - c_lo)] = clock64();
     if (m_base < M && n0 + c * 32 < N) {
       epilogue_block(ep, map_out, map_aux, w, has_in, c - c_lo, m_base, store_z, n0 + c * 32, M,
                      N, r);

@@ -32,6 +32,9 @@ for name, (M, N, Kd, bmn, epi) in shapes.items():
     t = t[used].double()
     t0 = t[:, 0].min()
     rel = (t - t0) / 1000.0  # us
-    med = [float(rel[t[:, i] > 0, i].median()) if (t[:, i] > 0).any() else None for i in range(16)]
+    med = [float(rel[t[:, i] > 0, i].median()) if (t[:, i] > 0).any() else None for i in range(8)]
+    # slots 8..15 are SM clock cycles (epilogue warp 4, lane 0), relative to slot 8
+    cyc = (t[:, 8:16] - t[:, 8:9]).median(dim=0).values.tolist()
+    med += [round(c) for c in cyc]
     print(json.dumps({"gemm": name, "ctas": int(used.sum()),
-                      "median_us": {n: round(v, 2) for n, v in zip(names, med) if v is not None}}), flush=True)
+                      "median_us(0-7) / cycles(8-15)": {n: round(v, 2) for n, v in zip(names, med) if v is not None}}), flush=True)
