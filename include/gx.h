@@ -215,8 +215,9 @@ GX_API int gx_k_gemm_bf16(const void* a, int64_t lda, int a_mn_major, const void
  * row stride ld_qkv).  fwd writes ctx ([M][heads*d], ld_ctx) and lse (fp32 [batch*heads][seq],
  * log2 domain); bwd reads qkv, ctx, lse, dctx and writes dqkv (qkv layout) using the fp32
  * workspaces dq_accum ([ceil(seq/128)][batch*heads*seq*d]: per-key-tile dQ partials) and
- * dsum ([batch*heads*seq], zero-initialised once by the caller; left reset).  head_dim 64 and
- * seq <= 512 run on tcgen05/TMEM (attention_tc.cu), head_dim 32/80/128 on mma.sync.  Windowed
+ * dsum ([batch*heads*seq], zero-initialised once by the caller; left reset).  head_dim 32-80
+ * (multiples of 16) and seq <= 512 run on tcgen05/TMEM (attention_tc.cu: every BASELINE shape,
+ * with the masks and biases below); head_dim 128 or longer sequences on mma.sync.  Windowed
  * (Swin) attention is this call with batch = samples * windows and seq = window.  Dropout
  * element (q,k) of global (sample_offset+b, head_offset+h) follows csrc/kernels/attention.cu. */
 typedef struct gx_attention_args {
@@ -244,9 +245,9 @@ typedef struct gx_attention_args {
   int causal;                  /* 1: query q attends keys k <= q only (decoder self-attention) */
   /* Swin shifted windows (SW-MSA): with win_shift > 0 the batch is samples x (grid/side)^2
    * windows of side win_side over a win_grid-wide grid rolled by win_shift; q and k attend
-   * only when they come from the same region of the unrolled grid (mma.sync path). */
+   * only when they come from the same region of the unrolled grid. */
   int win_grid, win_side, win_shift;
-  /* Swin relative-position bias (mma.sync path, seq = rpb_side^2 window tokens): scores get
+  /* Swin relative-position bias (seq = rpb_side^2 window tokens): scores get
    * rpb[head][(dy + side - 1) * (2 side - 1) + dx + side - 1] (bf16 [heads][(2 side - 1)^2],
    * this call's heads); bwd writes each (window, head)'s table gradient to rpb_dpart (fp32
    * [batch*heads][(2 side - 1)^2], seq <= 64) for gx_k_rpb_grad to sum over the batch in
