@@ -267,6 +267,9 @@ typedef struct gx_attention_args {
 } gx_attention_args;
 
 GX_API int gx_k_attention_fwd(const gx_attention_args* args, void* stream);
+/* Tests: fill every SM's shared memory with 0xFF (NaN) bytes, so a kernel launched next that
+ * reads shared memory it never wrote produces NaN. */
+GX_API int gx_k_poison_smem(void* stream);
 GX_API int gx_k_attention_bwd(const gx_attention_args* args, void* stream);
 
 /* LayerNorm over rows of h (bf16 in/out, fp32 statistics, eps 1e-5).

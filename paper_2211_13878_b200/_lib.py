@@ -69,11 +69,13 @@ def _declare(L: ctypes.CDLL) -> None:
     for name in ("gx_k_attention_fwd", "gx_k_attention_bwd", "gx_k_layernorm_fwd",
                  "gx_k_layernorm_bwd", "gx_k_bias_dropout_add", "gx_k_dropout_bwd_colsum",
                  "gx_k_colsum", "gx_k_mse_loss", "gx_k_adamw", "gx_k_cast_bf16",
-                 "gx_k_patch_merge", "gx_k_window_roll", "gx_k_rpb_grad", "gx_k_relb_grad"):
+                 "gx_k_patch_merge", "gx_k_window_roll", "gx_k_rpb_grad", "gx_k_relb_grad",
+                 "gx_k_poison_smem"):
         getattr(L, name).restype = c_int
     vp = c_void_p
     L.gx_k_attention_fwd.argtypes = [vp, vp]
     L.gx_k_attention_bwd.argtypes = [vp, vp]
+    L.gx_k_poison_smem.argtypes = [vp]
     L.gx_k_layernorm_fwd.argtypes = [vp, vp, vp, vp, vp, vp, c_int, c_int, vp]
     L.gx_k_layernorm_bwd.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, c_int, c_int, vp]
     L.gx_k_bias_dropout_add.argtypes = [vp, vp, vp, vp, c_int, c_int, vp, vp]

@@ -12,6 +12,15 @@ extern "C" int gx_k_gemm_bf16(const void* a, int64_t lda, int a_mn_major, const 
 
 namespace {
 cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Fills every SM's shared memory with 0xFF bytes (a NaN pattern in fp32 and bf16): one
+// maximum-size block per SM.  Tests launch it before a kernel so that a read of shared memory
+// the kernel never wrote shows up as NaN instead of as whatever the last kernel left there.
+__global__ void smem_poison_kernel(int bytes) {
+  extern __shared__ uint4 sm_poison[];
+  for (int i = threadIdx.x; i < bytes / 16; i += blockDim.x)
+    sm_poison[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+}
 // standalone entry points share one zero-initialised column-sum workspace (up to 8192 columns)
 float* colsum_ws() {
   static float* ws = nullptr;
@@ -42,6 +51,17 @@ extern "C" int gx_k_gemm_bf16_splitk(const void* a, int64_t lda, int a_mn_major,
   gx::GemmOperand A{a, lda, a_mn_major != 0};
   gx::GemmOperand B{b, ldb, b_mn_major != 0};
   return gx::gemm_bf16(A, B, M, N, K, ep, S(stream), tile, splits);
+}
+
+extern "C" int gx_k_poison_smem(void* stream) {
+  const int bytes = 227 * 1024;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(smem_poison_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    set = true;
+  }
+  smem_poison_kernel<<<gx::num_sms(), 1024, bytes, S(stream)>>>(bytes);
+  return gx::check_launch("smem_poison_kernel");
 }
 
 extern "C" int gx_k_attention_fwd(const gx_attention_args* a, void* stream) {

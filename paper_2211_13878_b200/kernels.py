@@ -148,6 +148,11 @@ def _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, heads_total=None
     return a
 
 
+def poison_smem():
+    """Fill every SM's shared memory with NaN bytes (tests: catches reads of unwritten smem)."""
+    _lib.check(_lib.lib().gx_k_poison_smem(_lib.stream_ptr()))
+
+
 def attention_mask_buffer(batch, seq, heads, device):
     import torch
     return torch.zeros(batch * heads * seq * ((seq + 63) // 64) * 4, device=device,
