@@ -214,7 +214,8 @@ GX_API int gx_k_gemm_bf16(const void* a, int64_t lda, int a_mn_major, const void
 /* Fused multi-head attention over a token-major qkv buffer ([M=batch*seq][3][heads][d],
  * row stride ld_qkv).  fwd writes ctx ([M][heads*d], ld_ctx) and lse (fp32 [batch*heads][seq],
  * log2 domain); bwd reads qkv, ctx, lse, dctx and writes dqkv (qkv layout) using the fp32
- * workspaces dq_accum ([ceil(seq/128)][batch*heads*seq*d]: per-key-tile dQ partials) and
+ * workspaces dq_accum ([ceil(seq/128)][batch*heads*round_up(seq,4)*d] fp32: per-key-tile dQ
+ * partials) and
  * dsum ([batch*heads*seq], zero-initialised once by the caller; left reset).  head_dim 32-80
  * (multiples of 16) and seq <= 512 run on tcgen05/TMEM (attention_tc.cu: every BASELINE shape,
  * with the masks and biases below); head_dim 128 or longer sequences on mma.sync.  Windowed

@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
     // (2 vseq <= 1024 words: both of a thread's loads issued before either store)
     uint64_t w[2];
-#pragma unroll
+  #pragma unroll
     for (int it = 0; it < 2; ++it) {
       const int i = threadIdx.x + it * kBwdSoftmax;
       const int v = i >> 1, u = vb * g.wpt + v / s;
@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         w[it] = *reinterpret_cast<const uint64_t*>(
             mask_g + (((static_cast<int64_t>(u) * H + h) * s + v % s) * nkb + kb) * 4);
     }
-#pragma unroll
+  #pragma unroll
     for (int it = 0; it < 2; ++it) {
       const int i = threadIdx.x + it * kBwdSoftmax;
       if (i < 2 * g.vseq) *reinterpret_cast<uint64_t*>(sMask + i * 4) = w[it];
@@ -821,6 +821,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
     // dQ_j partial (fp32) out of TMEM (lane = query row of the chunk, 16 columns per load)
+    // dQ_j partial (fp32) out of TMEM (lane = query row of the chunk, 16 columns per load),
+    // stored column-major per (key block, sequence x head): [hd][vld] (vld = vseq rounded up
+    // to 4), so a warp's 32 lanes (consecutive queries) write 128 contiguous bytes per column
+    const int vld = (g.vseq + 3) & ~3;
     auto store_dq = [&](int j) {
       const int v = j * kTcQ + kr;
       const uint32_t tq = t_dq + (kDqDbl ? (j & 1) * hd : 0);
@@ -829,12 +833,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tmem_ld16(trow + tq + c16 * 16, o);
         tmem_ld_wait();
         if (v < g.vseq) {
-          float4* dst = reinterpret_cast<float4*>(
-              part + ((static_cast<int64_t>(kt) * gridDim.y + blockIdx.y) * g.vseq + v) * hd + c16 * 16);
+          float* dst = part + ((static_cast<int64_t>(kt) * gridDim.y + blockIdx.y) * hd + c16 * 16) *
+                                  vld + v;
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = make_float4(__uint_as_float(o[4 * i]), __uint_as_float(o[4 * i + 1]),
-                                 __uint_as_float(o[4 * i + 2]), __uint_as_float(o[4 * i + 3]));
+          for (int i = 0; i < 16; ++i) dst[static_cast<int64_t>(i) * vld] = __uint_as_float(o[i]);
         }
       }
     };
@@ -852,9 +854,45 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int c0 = cq * 32;
       const int qg0 = j * kTcQ + c0;  // first virtual query of this warp's 32
       uint32_t ppd[16], pds[16];
-      {
-        // no masking needed for this 32-query x 128-key block
-        const bool full = !kGen && qg0 + 32 <= s && kt * 128 + 128 <= s;
+      if (!kGen) {
+        // Plain (unmasked) path: the validity of a partial chunk is one bit mask, the keep bit
+        // one shared load at a compile-time offset, and every element is FFMA, EX2, two
+        // selects and three multiply-adds.
+        uint32_t sv[32], dv[32];
+        tmem_ld32(trow + c0, sv);
+        tmem_ld32(trow + 128 + c0, dv);
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(bar_sfree);  // the MMA warp may overwrite S / dPd with the next chunk's
+        // this key's keep word for query qg0 + i sits i * 16 B further (compile-time offsets)
+        const uint16_t* mk = sMask + (qg0 * 2 + kslot) * 4 + mt;
+        const uint32_t mbitm = 1u << mbit;
+        // valid (query, key) pairs of this 32-query slice: query < s and key < s
+        const uint32_t vmask = key >= s || qg0 >= s ? 0u
+                               : (qg0 + 32 <= s ? ~0u : (1u << (s - qg0)) - 1u);
+        const float fk = thr != 0u ? inv_keep : 1.f;
+#pragma unroll
+        for (int i4 = 0; i4 < 8; ++i4) {
+          const float4 l4 = *reinterpret_cast<const float4*>(sLse + qg0 + 4 * i4);
+          const float4 d4 = *reinterpret_cast<const float4*>(sD + qg0 + 4 * i4);
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dd[4] = {d4.x, d4.y, d4.z, d4.w};
+          float pd4[4], ds4[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int i = 4 * i4 + t;
+            float pr = ex2_ftz(fmaf(__uint_as_float(sv[i]), c2, -lv[t]));
+            pr = (vmask >> i) & 1u ? pr : 0.f;  // (padding: lse / D may be stale there)
+            const float f = thr == 0u || (mk[i * 8] & mbitm) != 0u ? fk : 0.f;
+            pd4[t] = pr * f;
+            ds4[t] = pr * fmaf(__uint_as_float(dv[i]), f, -dd[t]);
+          }
+          ppd[2 * i4] = pack_bf16(pd4[0], pd4[1]);
+          ppd[2 * i4 + 1] = pack_bf16(pd4[2], pd4[3]);
+          pds[2 * i4] = pack_bf16(ds4[0], ds4[1]);
+          pds[2 * i4 + 1] = pack_bf16(ds4[2], ds4[3]);
+        }
+      } else {
+        const bool full = false;  // (masked path: every pair checked)
         uint32_t sv[32], dv[32];
         tmem_ld32(trow + c0, sv);
         tmem_ld32(trow + 128 + c0, dv);
@@ -1004,46 +1042,58 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   cluster_sync();
   GX_ATTN_STAMP(p, 26);
   {
-    // loads of both items of a thread first, then the fixed-order sums (t = 0, 1, ...)
+    // per (4 queries, 4 columns): the key blocks' partials (column-major [hd][vseq] each;
+    // consecutive threads = consecutive query quads: 16 B coalesced loads), summed in
+    // key-block order; two key blocks' loads in flight at a time
     auto* dq = static_cast<__nv_bfloat16*>(p.dqkv);
     const float* __restrict__ src0 = part;
     const float sc = p.scale;
     const int q_lo = kt * kTcQ, q_hi = min(g.vseq, q_lo + kTcQ);
-    const int c8n = hd / 8;
-    constexpr int kMaxKt = kTcMaxKeys / kTcQ;
-    for (int base = threadIdx.x; base < (q_hi - q_lo) * c8n; base += 2 * kBwdThreads) {
-      float4 x[2][kMaxKt][2];
+    const int nq4 = (q_hi - q_lo + 3) / 4, c4n = hd / 4;
+    const int vld = (g.vseq + 3) & ~3;  // column stride of the partials (16 B aligned quads)
+    for (int idx = threadIdx.x; idx < nq4 * c4n; idx += kBwdThreads) {
+      const int v0 = q_lo + 4 * (idx % nq4), c0 = 4 * (idx / nq4);
+      float a[4][4] = {};  // [query][column]
+      for (int t0 = 0; t0 < nkt; t0 += 2) {
+        float4 x[2][4];
 #pragma unroll
-      for (int it = 0; it < 2; ++it) {
-        const int idx = base + it * kBwdThreads;
-        const int v = q_lo + idx / c8n, c8 = idx % c8n;
+        for (int tt = 0; tt < 2; ++tt) {
+          const int t = t0 + tt;
 #pragma unroll
-        for (int t = 0; t < kMaxKt; ++t) {
-          if (idx < (q_hi - q_lo) * c8n && t < nkt) {
-            const float4* src = reinterpret_cast<const float4*>(
-                src0 + ((static_cast<int64_t>(t) * gridDim.y + blockIdx.y) * g.vseq + v) * hd + c8 * 8);
-            x[it][t][0] = __ldcg(src);
-            x[it][t][1] = __ldcg(src + 1);
-          } else {
-            x[it][t][0] = x[it][t][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int cc = 0; cc < 4; ++cc) {
+            const float* src = src0 + ((static_cast<int64_t>(t) * gridDim.y + blockIdx.y) * hd +
+                                       c0 + cc) * vld + v0;
+            if (t >= nkt) {
+              x[tt][cc] = make_float4(0.f, 0.f, 0.f, 0.f);
+            } else if (v0 + 4 <= q_hi) {
+              x[tt][cc] = __ldcg(reinterpret_cast<const float4*>(src));
+            } else {
+              x[tt][cc] = make_float4(v0 < q_hi ? __ldcg(src) : 0.f,
+                                      v0 + 1 < q_hi ? __ldcg(src + 1) : 0.f,
+                                      v0 + 2 < q_hi ? __ldcg(src + 2) : 0.f,
+                                      v0 + 3 < q_hi ? __ldcg(src + 3) : 0.f);
+            }
+          }
+        }
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+          if (t0 + tt >= nkt) break;
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            a[0][cc] += x[tt][cc].x;
+            a[1][cc] += x[tt][cc].y;
+            a[2][cc] += x[tt][cc].z;
+            a[3][cc] += x[tt][cc].w;
           }
         }
       }
 #pragma unroll
-      for (int it = 0; it < 2; ++it) {
-        const int idx = base + it * kBwdThreads;
-        const int v = q_lo + idx / c8n, c8 = idx % c8n;
-        if (idx >= (q_hi - q_lo) * c8n || vb * g.wpt + v / s >= p.batch) continue;
-        float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-        for (int t = 0; t < kMaxKt; ++t) {
-          if (t >= nkt) break;
-          a[0] += x[it][t][0].x; a[1] += x[it][t][0].y; a[2] += x[it][t][0].z; a[3] += x[it][t][0].w;
-          a[4] += x[it][t][1].x; a[5] += x[it][t][1].y; a[6] += x[it][t][1].z; a[7] += x[it][t][1].w;
-        }
-        *reinterpret_cast<uint4*>(dq + (static_cast<int64_t>(row0) + v) * p.ld_qkv + h * hd + c8 * 8) =
-            make_uint4(pack_bf16(a[0] * sc, a[1] * sc), pack_bf16(a[2] * sc, a[3] * sc),
-                       pack_bf16(a[4] * sc, a[5] * sc), pack_bf16(a[6] * sc, a[7] * sc));
+      for (int qq = 0; qq < 4; ++qq) {
+        const int v = v0 + qq;
+        if (v >= q_hi || vb * g.wpt + v / s >= p.batch) continue;
+        *reinterpret_cast<uint2*>(dq + (static_cast<int64_t>(row0) + v) * p.ld_qkv + h * hd + c0) =
+            make_uint2(pack_bf16(a[qq][0] * sc, a[qq][1] * sc),
+                       pack_bf16(a[qq][2] * sc, a[qq][3] * sc));
       }
     }
   }

@@ -125,7 +125,9 @@ int ExecutorImpl::allocate(RankCtx& r) {
   r.da = A.a<bf16>(max_h);
   r.gbuf[0] = A.a<bf16>(max_h);
   r.gbuf[1] = A.a<bf16>(max_h);
-  r.dq_acc = A.a<float>(4 * max_c);  // tcgen05 attention: one dQ partial per 128-key tile
+  // tcgen05 attention: one dQ partial per 128-key tile, columns padded to 4 rows (the slack
+  // covers ceil(seq / 128) x round_up(seq, 4) <= 5 seq)
+  r.dq_acc = A.a<float>(5 * max_c);
   if (any_shift) {
     r.dctxr = A.a<bf16>(max_c);
     r.rollbuf = A.a<bf16>(max_h);

@@ -181,7 +181,7 @@ def attention_bwd(qkv, ctx, lse, dctx, batch, seq, heads, head_dim, p=0.0, seed=
     # fp32 dQ partials (one slice per 128-key tile on the tcgen05 path) and D / ticket words
     # (zero-initialised: the tcgen05 path keeps per-head tickets there)
     # (short sequences are packed 128 // seq per tile: one spare sequence of slack)
-    dq_acc = torch.empty(((seq + 127) // 128) * (batch + 1) * heads * seq * head_dim,
+    dq_acc = torch.empty(((seq + 127) // 128) * (batch + 1) * heads * ((seq + 3) // 4 * 4) * head_dim,
                          device=qkv.device, dtype=torch.float32)
     dsum = torch.zeros(batch * heads * seq, device=qkv.device, dtype=torch.float32)
     a = _attn_args(qkv, batch, seq, heads, head_dim, p, seed, site, **kw)

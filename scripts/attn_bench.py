@@ -34,7 +34,7 @@ def run(name, n, s, H, d, kw):
     lse = torch.empty(n * H, s, device=dev)
     mask = K.attention_mask_buffer(n, s, H, dev)
     dqkv = torch.zeros_like(qkv)
-    dq_acc = torch.empty(((s + 127) // 128) * (n + 1) * H * s * d, device=dev)
+    dq_acc = torch.empty(((s + 127) // 128) * (n + 1) * H * ((s + 3) // 4 * 4) * d, device=dev)
     dsum = torch.zeros(n * H * s, device=dev)
     extra = {}
     tab = dpart = None
