@@ -33,6 +33,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "gx_internal.h"
 #include "launch.cuh"
@@ -441,13 +442,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         *reinterpret_cast<uint64_t*>(mask + ((bh_real * s + q) * nkb + kb) * 4) = packed;
       }
     }
-    const bool full = kb * 64 + 64 <= s;
-#pragma unroll
-    for (int hb = 0; hb < 2; ++hb) {
+    // (warp-uniform: full blocks, i.e. all but a sequence's tail block, skip the per-key
+    // bounds check; with dropout off the keep test is compiled out)
+    uint32_t vv[2][32];  // both 32-column halves of the block in flight at once
+    tmem_ld32(trow + kb * 64, vv[0]);
+    tmem_ld32(trow + kb * 64 + 32, vv[1]);
+    tmem_ld_wait();
+    auto half = [&](auto tail_tag, auto drop_tag, int hb) {
+      constexpr bool kTail = decltype(tail_tag)::value, kDrop = decltype(drop_tag)::value;
       const int c0 = kb * 64 + hb * 32;
-      uint32_t v[32];
-      tmem_ld32(trow + c0, v);
-      tmem_ld_wait();
+      const uint32_t (&v)[32] = vv[hb];
       uint32_t pk[16];
 #pragma unroll
       for (int j2 = 0; j2 < 16; ++j2) {
@@ -456,15 +460,26 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int uu = 0; uu < 2; ++uu) {
           const int i = 2 * j2 + uu;
           float e = ex2_ftz(fmaf(__uint_as_float(v[i]), c2, -m));
-          if (!full && c0 + i >= s) e = 0.f;
+          if (kTail && c0 + i >= s) e = 0.f;
           sum += e;
           // compile-time key position: the keep bit's word and shift fold to constants
-          if (thr != 0u) e = keep_bit(bits, hb * 32 + i) ? e : 0.f;
+          if (kDrop) e = keep_bit(bits, hb * 32 + i) ? e : 0.f;
           e2[uu] = e;
         }
         pk[j2] = pack_bf16(e2[0], e2[1]);
       }
       store_p(c0, pk);
+    };
+    using T_ = std::true_type;
+    using F_ = std::false_type;
+    const bool full = kb * 64 + 64 <= s;
+#pragma unroll
+    for (int hb = 0; hb < 2; ++hb) {
+      if (full) {
+        if (thr != 0u) half(F_{}, T_{}, hb); else half(F_{}, F_{}, hb);
+      } else {
+        if (thr != 0u) half(T_{}, T_{}, hb); else half(T_{}, F_{}, hb);
+      }
     }
   }
   red[4 * kTcQ + cq * kTcQ + r] = sum;
