@@ -252,13 +252,6 @@ __device__ __forceinline__ void tma_load_2d_u32(uint32_t dst, const CUtensorMap*
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
 }
-// TMA prefetch of one box of a 2-D map into L2 (no shared memory, no completion)
-__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(c0), "r"(c1)
-               : "memory");
-}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -436,16 +429,7 @@ __device__ __forceinline__ void epilogue_tile_prologue(const GemmEpilogue& ep,
                                                        int n0, int N) {
   int c_lo, c_hi;
   epilogue_chunks<BN>(ew, &c_lo, &c_hi);
-  if (has_in) {
-    // The operand (GeLU pre-activation / residual) usually comes from HBM (written in the
-    // forward, long evicted): pull every block this warp will need into L2 now, while the
-    // main loop runs, so the per-block TMA loads below hit L2 instead of paying a DRAM
-    // round trip each.
-    if (lane_id() == 0)
-      for (int c = c_lo + 1; c < c_hi; ++c)
-        tma_prefetch_l2_2d(map_aux, n0 + c * 32, static_cast<int32_t>(m_base));
-    epi_prefetch(w, map_aux, w.blk, n0 + c_lo * 32, static_cast<int32_t>(m_base));
-  }
+  if (has_in) epi_prefetch(w, map_aux, w.blk, n0 + c_lo * 32, static_cast<int32_t>(m_base));
   epi_stage_bias(ep, w, n0, N, c_lo, c_hi);
 }
 
