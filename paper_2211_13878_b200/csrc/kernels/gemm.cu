@@ -259,7 +259,6 @@ __device__ __forceinline__ void bulk_wait_read0() {
 __device__ __forceinline__ void bulk_wait_read1() {  // all but the most recent group read
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -595,7 +594,9 @@ __global__ void __maxnreg__(kGemmMaxRegs)
       tc_fence_before();
       mbar_arrive(&tempty_bar[buf]);
     }
-    if (lane_id() == 0) bulk_wait_all();
+    // only the shared-memory reads of the outstanding TMA stores must finish before the CTA
+    // releases its shared memory; their global writes complete with the grid
+    if (lane_id() == 0) bulk_wait_read0();
     __syncwarp();
   }
   tc_fence_before();
@@ -795,7 +796,9 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(kGemmMaxRegs)
       if (lane_id() == 0) mbar_arrive_remote_relaxed(leader_tempty0 + buf * 8);
     }
     if (ep.trace != nullptr && warp == 4 && lane_id() == 0) ep.trace[blockIdx.x * 16 + 6] = gtimer();
-    if (lane_id() == 0) bulk_wait_all();
+    // only the shared-memory reads of the outstanding TMA stores must finish before the CTA
+    // releases its shared memory; their global writes complete with the grid
+    if (lane_id() == 0) bulk_wait_read0();
     __syncwarp();
   }
   tc_fence_before();

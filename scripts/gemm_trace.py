@@ -7,9 +7,10 @@ from paper_2211_13878_b200 import kernels as K  # noqa: E402
 dev = torch.device("cuda:0")
 bf = torch.bfloat16
 names = ["entry", "pdl", "tma0", "stage0", "mma_last", "acc0", "epi_done", "exit", "c0", "c0ld", "c1", "c1ld", "blk0_math0", "blk0_math1", "blk0_staged", "blk0_stored"]
-shapes = {"up_fwd(gelu)": (512, 5120, 1280, False, "gelu"), "qkv_fwd": (512, 3840, 1280, False, None),
-          "dgrad_down(gelu_bwd)": (512, 5120, 1280, True, "gelu_bwd"), "out_fwd plain": (512, 1280, 1280, False, None),
-          "up_fwd plain": (512, 5120, 1280, False, None)}
+Mt = int(sys.argv[1]) if len(sys.argv) > 1 else 512
+shapes = {"up_fwd(gelu)": (Mt, 5120, 1280, False, "gelu"), "qkv_fwd": (Mt, 3840, 1280, False, None),
+          "dgrad_down(gelu_bwd)": (Mt, 5120, 1280, True, "gelu_bwd"), "out_fwd plain": (Mt, 1280, 1280, False, None),
+          "up_fwd plain": (Mt, 5120, 1280, False, None)}
 for name, (M, N, Kd, bmn, epi) in shapes.items():
     A = (torch.randn(M, Kd, device=dev) * 0.5).to(bf)
     B = (torch.randn(Kd, N, device=dev) if bmn else torch.randn(N, Kd, device=dev)).to(bf) * 0.05
