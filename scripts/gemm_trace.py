@@ -10,6 +10,7 @@ names = ["entry", "pdl", "tma0", "stage0", "mma_last", "acc0", "epi_done", "exit
 Mt = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 shapes = {"up_fwd(gelu)": (Mt, 5120, 1280, False, "gelu"), "qkv_fwd": (Mt, 3840, 1280, False, None),
           "dgrad_down(gelu_bwd)": (Mt, 5120, 1280, True, "gelu_bwd"), "out_fwd plain": (Mt, 1280, 1280, False, None),
+          "out_fwd residual+dropout": (Mt, 1280, 1280, False, "residual"),
           "up_fwd plain": (Mt, 5120, 1280, False, None)}
 for name, (M, N, Kd, bmn, epi) in shapes.items():
     A = (torch.randn(M, Kd, device=dev) * 0.5).to(bf)
@@ -22,6 +23,8 @@ for name, (M, N, Kd, bmn, epi) in shapes.items():
         kw = dict(bias=bias, gelu_aux=aux)
     elif epi == "gelu_bwd":
         kw = dict(gelu_bwd_aux=aux)
+    elif epi == "residual":
+        kw = dict(bias=bias, residual=aux, dropout_p=0.1, seed=1, site=1)
     for i in range(4):
         K.gemm(A, B, b_mn_major=bmn, trace=tr if i == 3 else None, **kw)
     torch.cuda.synchronize()
