@@ -65,4 +65,32 @@ inline cudaError_t launch_k_cluster(void (*kernel)(Exp...), dim3 grid, dim3 bloc
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
 }
 
+// Same, with a thread-block cluster of `cluster_y` CTAs along y (1: no cluster).
+template <typename... Exp, typename... Act>
+inline cudaError_t launch_k_cluster_y(void (*kernel)(Exp...), dim3 grid, dim3 block, size_t smem,
+                                      cudaStream_t st, unsigned cluster_y, Act&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (cluster_y > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = 1;
+    attr[n].val.clusterDim.y = cluster_y;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
+}
+
 }  // namespace gx

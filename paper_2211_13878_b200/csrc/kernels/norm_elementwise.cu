@@ -10,6 +10,7 @@
 
 #include "gx_internal.h"
 #include "launch.cuh"
+#include "sm100.cuh"
 #include "adam.cuh"
 #include "philox.cuh"
 
@@ -305,7 +306,6 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cols_kernel(
   pdl_enter();
   constexpr int kParts = kDrop ? 3 : 2;
   __shared__ float red[32][kParts * 64 + 1];
-  __shared__ bool last;
   const int chunks = h >> 3;
   const int strip = blockIdx.x;
   const int cl = threadIdx.x & 7;       // chunk within the 64-column strip
@@ -358,28 +358,30 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cols_kernel(
     if (owner && outs[t >> 6] != nullptr) outs[t >> 6][col] += s;
     return;
   }
-  if (owner) ws[static_cast<int64_t>(blockIdx.y) * width + (t >> 6) * h + col] = s;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&tickets[strip], 1u) == static_cast<unsigned>(slices - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  if (owner) {
+  // the row slices of a strip form one cluster along y: slice 0 adds the slices' partials
+  // in slice order over DSMEM (no global partials, fences or tickets)
+  __shared__ float part_s[kParts * 64];
+  if (t < kParts * 64) part_s[t] = s;
+  cluster_sync();
+  if (blockIdx.y == 0 && owner) {
     float acc = 0.f;
     for (int y = 0; y < slices; ++y)
-      acc += __ldcg(ws + static_cast<int64_t>(y) * width + (t >> 6) * h + col);
+      acc += ld_shared_cluster_f32(mapa_shared(smem_u32(&part_s[t]), y));
     if (outs[t >> 6] != nullptr) outs[t >> 6][col] += acc;
   }
-  if (threadIdx.x == 0) tickets[strip] = 0u;  // ready for the next call / graph replay
+  cluster_sync();  // the peers' shared memory stays alive until slice 0 has read it
+  (void)ws;
+  (void)tickets;
+  (void)width;
 }
 
+constexpr int kLnColsClusterMax = 8;  // row slices of a strip: one portable cluster along y
 static void ln_cols_grid(int rows, int h, int* strips, int* slices, int* rows_per_slice) {
   *strips = (h / 8 + 7) / 8;
   int ys = (2 * num_sms() + *strips - 1) / *strips;
   const int max_y = (rows + 31) / 32;
   if (ys > max_y) ys = max_y;
-  if (ys > kLnBwdMaxSlices) ys = kLnBwdMaxSlices;
+  if (ys > kLnColsClusterMax) ys = kLnColsClusterMax;
   if (ys < 1) ys = 1;
   *rows_per_slice = (rows + ys - 1) / ys;
   *slices = (rows + *rows_per_slice - 1) / *rows_per_slice;
@@ -429,11 +431,12 @@ int layernorm_bwd_cols(const void* dy, bool dy_f32, const void* x, const void* m
   unsigned int* tickets = reinterpret_cast<unsigned int*>(workspace);
   auto* kcols = dy_f32 ? (fuse ? layernorm_bwd_cols_kernel<true, true> : layernorm_bwd_cols_kernel<true, false>)
                        : (fuse ? layernorm_bwd_cols_kernel<false, true> : layernorm_bwd_cols_kernel<false, false>);
-  launch_k(kcols, dim3(strips, slices), dim3(256), 0, st, dy, static_cast<const uint4*>(x),
-           static_cast<const float*>(mean), static_cast<const float*>(rstd),
-           static_cast<const uint4*>(dz), static_cast<float*>(dgamma), static_cast<float*>(dbeta),
-           static_cast<float*>(dbias), workspace + kLnBwdTickets, tickets, rows, h, rps, 1,
-           int64_t{0});
+  launch_k_cluster_y(kcols, dim3(strips, slices), dim3(256), 0, st, static_cast<unsigned>(slices),
+                     dy, static_cast<const uint4*>(x),
+                     static_cast<const float*>(mean), static_cast<const float*>(rstd),
+                     static_cast<const uint4*>(dz), static_cast<float*>(dgamma), static_cast<float*>(dbeta),
+                     static_cast<float*>(dbias), workspace + kLnBwdTickets, tickets, rows, h, rps, 1,
+                     int64_t{0});
   return check_launch("layernorm_bwd_cols_kernel");
 }
 
@@ -606,15 +609,14 @@ int residual_layernorm(const float* x, int slices, int64_t slice_stride, const v
 
 // --------------------------------------------- dropout backward + bias-grad column sums
 // Block = (64-column strip, row slice): 8 chunks x 32 row lanes accumulate, the 32 lanes are
-// combined in shared memory in a fixed order, and the slices of a strip are added in slice
-// order by the strip's last block (ticket) -- deterministic, no floating-point atomics.
-// ws: kColsumTickets ticket words, then [slices][cols] partials (zero-initialised once).
+// combined in shared memory in a fixed order, and the slices of a strip (one cluster) are
+// added in slice order over DSMEM -- deterministic, no floating-point atomics.  (ws: unused,
+// kept in the signature of the C ABI entry points.)
 __global__ void __launch_bounds__(256) dropout_bwd_colsum_kernel(
     const uint4* __restrict__ dy, uint4* __restrict__ dz, float* __restrict__ dbias, int rows,
     int cols, int64_t ld_chunks, gx_dropout d, int rows_per_block, float* __restrict__ ws) {
   pdl_enter();
   __shared__ float red[32][65];
-  __shared__ bool last;
   const int cchunks = cols >> 3;
   const int cstrip = blockIdx.x * 8;           // first chunk of this strip
   const int cc = cstrip + (threadIdx.x & 7);   // this thread's chunk
@@ -623,7 +625,33 @@ __global__ void __launch_bounds__(256) dropout_bwd_colsum_kernel(
   const int r1 = min(rows, r0 + rows_per_block);
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (cc < cchunks) {
-    for (int r = r0 + rlane; r < r1; r += 32) {
+    // four rows' loads in flight before any is used (a lane strides 32 rows)
+    int r = r0 + rlane;
+    for (; r + 96 < r1; r += 128) {
+      uint4 x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = dy[static_cast<int64_t>(r + 32 * u) * ld_chunks + cc];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = static_cast<int64_t>(r + 32 * u) * ld_chunks + cc;
+        float v[8];
+        unpack8(x[u], v);
+        if (d.threshold != 0u) {
+          bool k[8];
+          keep8(d, static_cast<uint64_t>(d.row_offset + r + 32 * u) * d.drop_ld + d.col_offset + cc * 8, k);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = k[j] ? v[j] * d.scale : 0.f;
+          const uint4 o = pack8(v);
+          dz[i] = o;
+          unpack8(o, v);
+        } else if (dz != dy) {
+          dz[i] = x[u];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += v[j];
+      }
+    }
+    for (; r < r1; r += 32) {
       const int64_t i = static_cast<int64_t>(r) * ld_chunks + cc;
       float v[8];
       unpack8(dy[i], v);
@@ -655,29 +683,55 @@ __global__ void __launch_bounds__(256) dropout_bwd_colsum_kernel(
     if (threadIdx.x < 64 && col < cols) dbias[col] += sum;
     return;
   }
-  unsigned int* tickets = reinterpret_cast<unsigned int*>(ws);
-  float* part = ws + kColsumTickets;
-  if (threadIdx.x < 64 && col < cols) part[static_cast<int64_t>(blockIdx.y) * cols + col] = sum;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0)
-    last = atomicAdd(&tickets[blockIdx.x], 1u) == static_cast<unsigned>(gridDim.y - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  if (threadIdx.x < 64 && col < cols) {
+  // The row slices of a strip form one thread-block cluster along y: each slice leaves its 64
+  // column sums in shared memory, and slice 0 adds them in slice order over DSMEM after a
+  // cluster barrier -- no global partials, fences or tickets on the path.
+  __shared__ float part_s[64];
+  if (threadIdx.x < 64) part_s[threadIdx.x] = sum;
+  cluster_sync();
+  if (blockIdx.y == 0 && threadIdx.x < 64 && col < cols) {
     float t = 0.f;
     for (int y = 0; y < static_cast<int>(gridDim.y); ++y)
-      t += __ldcg(part + static_cast<int64_t>(y) * cols + col);
+      t += ld_shared_cluster_f32(mapa_shared(smem_u32(&part_s[threadIdx.x]), y));
     dbias[col] += t;
   }
-  if (threadIdx.x == 0) tickets[blockIdx.x] = 0u;
+  cluster_sync();  // the peers' shared memory stays alive until slice 0 has read it
+  (void)ws;
 }
 
-constexpr int kColsumSlicesUsed = 8;
+constexpr int kColsumSlicesUsed = 8;  // (<= 8: a portable cluster along y)
+
+// the column-sum kernel, its row slices clustered along y when there is more than one
+static void launch_colsum(dim3 grid, cudaStream_t st, const uint4* dy, uint4* dz, float* dbias,
+                          int rows, int cols, int64_t ld_chunks, const gx_dropout& d, int rpb,
+                          float* ws) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (grid.y > 1 && dbias != nullptr) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = 1;
+    attr[n].val.clusterDim.y = grid.y;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  cudaLaunchKernelEx(&cfg, dropout_bwd_colsum_kernel, dy, dz, dbias, rows, cols, ld_chunks, d,
+                     rpb, ws);
+}
 static void colsum_grid(int rows, int cols, dim3* grid, int* rpb) {
   const int strips = (cols / 8 + 7) / 8;
-  int ysplit = (num_sms() * 4 + strips - 1) / strips;
+  int ysplit = num_sms() / strips;  // about one wave of blocks
   const int max_y = (rows + 31) / 32;
   if (ysplit > max_y) ysplit = max_y;
   if (ysplit > kColsumSlicesUsed) ysplit = kColsumSlicesUsed;  // fewer, longer slices measured best
@@ -698,10 +752,8 @@ int dropout_bwd_colsum(const void* dy, void* dz, void* dbias, int rows, int cols
   dim3 grid;
   int rpb;
   colsum_grid(rows, cols, &grid, &rpb);
-  if (grid.y > 1 && ws == nullptr) return set_error(kErrConfig, "dropout_bwd: workspace required");
-  launch_k(dropout_bwd_colsum_kernel, grid, dim3(256), 0, st, static_cast<const uint4*>(dy),
-           static_cast<uint4*>(dz), static_cast<float*>(dbias), rows, cols,
-           static_cast<int64_t>(cols / 8), d, rpb, ws);
+  launch_colsum(grid, st, static_cast<const uint4*>(dy), static_cast<uint4*>(dz),
+                static_cast<float*>(dbias), rows, cols, static_cast<int64_t>(cols / 8), d, rpb, ws);
   return check_launch("dropout_bwd_colsum_kernel");
 }
 
@@ -713,10 +765,8 @@ int colsum(const void* x, int64_t ld, void* acc, int rows, int cols, cudaStream_
   dim3 grid;
   int rpb;
   colsum_grid(rows, cols, &grid, &rpb);
-  if (grid.y > 1 && ws == nullptr) return set_error(kErrConfig, "colsum: workspace required");
-  launch_k(dropout_bwd_colsum_kernel, grid, dim3(256), 0, st, static_cast<const uint4*>(x),
-           const_cast<uint4*>(static_cast<const uint4*>(x)), static_cast<float*>(acc), rows,
-           cols, static_cast<int64_t>(ld / 8), off, rpb, ws);
+  launch_colsum(grid, st, static_cast<const uint4*>(x), const_cast<uint4*>(static_cast<const uint4*>(x)),
+                static_cast<float*>(acc), rows, cols, static_cast<int64_t>(ld / 8), off, rpb, ws);
   return check_launch("colsum_kernel");
 }
 
