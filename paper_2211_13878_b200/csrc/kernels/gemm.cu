@@ -994,6 +994,11 @@ static int pick_bn(int M, int N) {
 // K splits as fit one wave of pairs while keeping >= 4 k-blocks per split.  Returns the
 // split count and sets *tile (the force_bn argument of gemm_bf16).
 int splitk_plan(int M, int N, int K, int* tile) {
+  // At most 4 slices: every slice is an M x N fp32 partial written here and read back by the
+  // consuming row pass, so beyond 4 the partials' traffic costs more inside the step than the
+  // extra CTAs gain (BERT-Huge-32, M = 512: 4 -> 8.94 ms / step, 7 -> 9.12, 3 -> 9.00; a
+  // kernel timed alone prefers more slices)
+  constexpr int kMaxSplits = 4;
   const int kb = (K + kBK - 1) / kBK;
   if (M >= 256) {
     const int bn = N > 128 ? 256 : 128;
