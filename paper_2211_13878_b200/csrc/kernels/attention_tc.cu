@@ -907,13 +907,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           pds[2 * i4 + 1] = pack_bf16(ds4[2], ds4[3]);
         }
       } else {
-        const bool full = false;  // (masked path: every pair checked)
         uint32_t sv[32], dv[32];
         tmem_ld32(trow + c0, sv);
         tmem_ld32(trow + 128 + c0, dv);
         tmem_ld_wait();
         tc_fence_before();
         mbar_arrive(bar_sfree);  // the MMA warp may overwrite S / dPd with the next chunk's
+        // the key's own packed sequence / causal range [qlo, qhi) as one 32-bit mask over the
+        // warp's queries; its shifted-window region and the biases per pair (see the forward)
+        uint32_t vmask = 0u;
+        if (key_ok) {
+          const int lo = max(qlo - qg0, 0), hi = min(qhi - qg0, 32);
+          if (hi > lo) vmask = (hi - lo == 32 ? ~0u : (1u << (hi - lo)) - 1u) << lo;
+        }
+        const uint16_t* mk = sMask + (qg0 * 2 + kslot) * 4 + mt;  // keep word of query qg0 + i: + 8 i
+        const uint32_t mbitm = 1u << mbit;
+        const float fk = thr != 0u ? inv_keep : 1.f;
 #pragma unroll
         for (int i4 = 0; i4 < 8; ++i4) {
           const float4 l4 = *reinterpret_cast<const float4*>(sLse + qg0 + 4 * i4);
@@ -924,24 +933,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int t = 0; t < 4; ++t) {
             const int i = 4 * i4 + t;
             const int qg = qg0 + i;
-            bool valid;
+            bool valid = ((vmask >> i) & 1u) != 0u;
+            if (p.win_shift > 0) valid = valid && win->reg[qg] == kreg;
             float bias = 0.f;
-            if (kGen) {
-              // the key's own packed sequence [qlo, qhi) (causal: queries >= key), its
-              // shifted-window region, and the bias at kc[q] - kc[key] (see the forward)
-              valid = key_ok && qg >= qlo && qg < qhi;
-              if (p.win_shift > 0) valid = valid && win->reg[qg] == kreg;
-              if (valid && p.rpb != nullptr) bias = win->tab[win->kc[qg] + kbase];
-              if (valid && p.relb != nullptr) bias += win->rel[key - qg + s - 1];
-            } else {
-              valid = full || (qg < s && key < s);
-            }
-            const float pr = valid ? ex2_ftz(__uint_as_float(sv[i]) * c2 + bias - lv[t]) : 0.f;
-            float f = 1.f;  // dropout factor: inv_keep or 0
-            if (thr != 0u)
-              f = valid && ((sMask[(qg * 2 + kslot) * 4 + mt] >> mbit) & 1u) != 0u ? inv_keep : 0.f;
+            if (valid && p.rpb != nullptr) bias = win->tab[win->kc[qg] + kbase];
+            if (valid && p.relb != nullptr) bias += win->rel[key - qg + s - 1];
+            float pr = ex2_ftz(fmaf(__uint_as_float(sv[i]), c2, bias - lv[t]));
+            pr = valid ? pr : 0.f;
+            const float f = thr == 0u || (mk[i * 8] & mbitm) != 0u ? fk : 0.f;
             pd4[t] = pr * f;
-            ds4[t] = pr * (__uint_as_float(dv[i]) * f - dd[t]);
+            ds4[t] = pr * fmaf(__uint_as_float(dv[i]), f, -dd[t]);
             if (has_rpb || has_relb) sDs[(c0 + i) * kTcQ + kr] = ds4[t];
           }
           ppd[2 * i4] = pack_bf16(pd4[0], pd4[1]);
