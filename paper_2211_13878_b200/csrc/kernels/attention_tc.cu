@@ -79,8 +79,9 @@ Geom make_geom(const gx_attention_args& a) {
 struct WinSmem {
   float rel[2 * kTcMaxKeys];  // T5 relative bias of relative position k - q + seq - 1 (log2 units)
   float tab[kTabMax];
-  int16_t kc[kTcQ];  // ty * (2 side - 1) + tx: bias index = row base - kc[key]
-  int8_t ty[kTcQ], tx[kTcQ], reg[kTcQ];
+  alignas(16) int16_t kc[kTcQ];  // ty * (2 side - 1) + tx: bias index = row base - kc[key]
+  int8_t ty[kTcQ], tx[kTcQ];
+  alignas(16) int8_t reg[kTcQ];  // (16 B aligned: read as vectors by the packed path)
 };
 
 // Swin shifted-window region (0..8) of token `tok` of attention sequence (window) `u`: the
@@ -320,7 +321,54 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int nitem = g.wpt > 1 ? (cq * 32 < nk ? 1 : 0) : (nblk - cq + 3) / 4;
   auto item_c0 = [&](int it, int hb) { return g.wpt > 1 ? cq * 32 : (cq + 4 * it) * 64 + hb * 32; };
   float mx = -INFINITY;
-  if (kGen) {
+  // Packed short sequences (Swin windows): a warp owns exactly one 32-column chunk, so its
+  // masked, biased scores are computed once here and kept in registers for the exp pass; the
+  // per-column metadata (region id, bias-table coordinate) comes in with vector loads.
+  float xs[32];
+  const bool packed = kGen && g.wpt > 1;
+  if (packed && nitem > 0) {
+    const int c0 = cq * 32;
+    uint32_t vmask = 0u;  // columns of this row's own window (range [klo, khi))
+    {
+      const int lo = max(klo - c0, 0), hi = min(khi - c0, 32);
+      if (row_ok && hi > lo) vmask = (hi - lo == 32 ? ~0u : (1u << (hi - lo)) - 1u) << lo;
+    }
+    uint32_t regw[8], kcw[16];
+    if (p.win_shift > 0) {
+      const uint4 a = *reinterpret_cast<const uint4*>(&win->reg[c0]);
+      const uint4 b = *reinterpret_cast<const uint4*>(&win->reg[c0 + 16]);
+      regw[0] = a.x; regw[1] = a.y; regw[2] = a.z; regw[3] = a.w;
+      regw[4] = b.x; regw[5] = b.y; regw[6] = b.z; regw[7] = b.w;
+    }
+    if (p.rpb != nullptr) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint4 a = *reinterpret_cast<const uint4*>(&win->kc[c0 + 8 * k]);
+        kcw[4 * k] = a.x; kcw[4 * k + 1] = a.y; kcw[4 * k + 2] = a.z; kcw[4 * k + 3] = a.w;
+      }
+    }
+    const bool any = __any_sync(0xffffffffu, vmask != 0u);
+    uint32_t v[32];
+    if (any) {
+      tmem_ld32(trow + c0, v);
+      tmem_ld_wait();
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      bool ok = any && ((vmask >> j) & 1u) != 0u;
+      if (p.win_shift > 0)
+        ok = ok && static_cast<int>(static_cast<int8_t>((regw[j >> 2] >> (8 * (j & 3))) & 0xffu)) == rq;
+      float x = -INFINITY;
+      if (ok) {
+        x = __uint_as_float(v[j]) * c2;
+        if (p.rpb != nullptr)
+          x += win->tab[rowbase - static_cast<int>(static_cast<int16_t>((kcw[j >> 1] >> (16 * (j & 1))) & 0xffffu))];
+      }
+      xs[j] = x;
+      mx = fmaxf(mx, x);
+    }
+  }
+  if (kGen && !packed) {
     for (int it = 0; it < nitem; ++it)
       for (int hb = 0; hb < nchunk; ++hb) {
         const int c0 = item_c0(it, hb);
@@ -386,7 +434,25 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       st_shared_v4_tc(g_addr + (sw << 4), pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
     }
   };
-  if (kGen) {
+  if (packed && nitem > 0) {
+    const int c0 = cq * 32;
+    uint32_t pk[16];
+#pragma unroll
+    for (int j2 = 0; j2 < 16; ++j2) {
+      float e2[2];
+#pragma unroll
+      for (int uu = 0; uu < 2; ++uu) {
+        const int j = 2 * j2 + uu;
+        float e = ex2_ftz(xs[j] - m);  // (-inf: not attended -> 0)
+        sum += e;
+        if (thr != 0u) e = keep_bit(wrow, (c0 + j - klo) & 63) ? e : 0.f;
+        e2[uu] = e;
+      }
+      pk[j2] = pack_bf16(e2[0], e2[1]);
+    }
+    store_p(c0, pk);
+  }
+  if (kGen && !packed) {
     for (int it = 0; it < nitem; ++it) {
       uint32_t bits[4] = {wrow[0], wrow[1], wrow[2], wrow[3]};
       const int kb = g.wpt > 1 ? 0 : cq + 4 * it;
