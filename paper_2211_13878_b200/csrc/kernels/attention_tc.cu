@@ -127,7 +127,7 @@ __device__ __forceinline__ uint32_t keep_bit(const uint32_t (&w)[4], int kk) {
 }
 
 struct FwdLayout {
-  int kq, kv, p_lo, p_hi, win, red, bar, bytes;
+  int kq, kv, p_lo, p_hi, win, red, kw, bar, bytes;
 };
 __host__ __device__ inline FwdLayout fwd_layout(int np, int nk) {
   FwdLayout L{};
@@ -139,7 +139,8 @@ __host__ __device__ inline FwdLayout fwd_layout(int np, int nk) {
   L.p_hi = L.kv + np * nk * 128;
   L.win = L.p_hi + (groups - L.p_lo) * 16 * 1024;
   L.red = L.win + static_cast<int>((sizeof(WinSmem) + 15) / 16 * 16);
-  L.bar = L.red + 8 * kTcQ * 4;  // [max | sum][4 column quarters][128 rows]
+  L.kw = L.red + 8 * kTcQ * 4;   // red: [max | sum][4 column quarters][128 rows]
+  L.bar = L.kw + 4 * kTcQ * 4;   // kw: packed windows' keep words [4 calls][128 rows]
   L.bytes = L.bar + 64;
   return L;
 }
@@ -397,6 +398,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
   }
   if (!kGen && mx != -INFINITY) mx *= c2;
+  // packed windows: the four column warps of a row split its four Philox calls (warp cq makes
+  // call cq) and share the keep words through shared memory, instead of each drawing all four
+  uint32_t* kwsm = reinterpret_cast<uint32_t*>(smem + L.kw);
+  if (kGen && g.wpt > 1 && p.drop_threshold != 0u) {
+    const uint64_t sd = p.seed + (p.seed_offset != nullptr ? *p.seed_offset : 0ull);
+    const uint64_t st =
+        (static_cast<uint64_t>(p.sample_offset + u) * p.heads_total + (p.head_offset + h)) * s;
+    kwsm[cq * kTcQ + r] = keep16(sd, p.site, (st + static_cast<uint64_t>(q)) * ((s + 63) / 64) * 4 + cq,
+                                 p.drop_threshold);
+  }
   red[cq * kTcQ + r] = mx;
   named_sync(1, kFwdThreads);
   GX_ATTN_STAMP(p, 3);
@@ -414,8 +425,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   // packed short sequences: one 64-key real block per query, drawn once per row
   uint32_t wrow[4] = {0u, 0u, 0u, 0u};
   if (kGen && g.wpt > 1 && thr != 0u) {
-    const uint64_t call0 = (stream + static_cast<uint64_t>(q)) * nkb * 4;
-    keep16x4(seed, p.site, call0, thr, wrow);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) wrow[i] = kwsm[i * kTcQ + r];  // (staged before the max barrier)
     if (row_ok && cq == 0)
       *reinterpret_cast<uint64_t*>(mask + (bh_real * s + q) * nkb * 4) =
           static_cast<uint64_t>(wrow[0]) | (static_cast<uint64_t>(wrow[1]) << 16) |
