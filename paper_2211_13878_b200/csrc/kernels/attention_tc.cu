@@ -1084,12 +1084,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int u = vb * g.wpt + wl;
         if (u >= p.batch) continue;
         const int dy = e / n - (side - 1), dx = e % n - (side - 1);
+        // the query tokens (yq, xq) whose key (yq - dy, xq - dx) lies in the window, in
+        // increasing token order (the same pairs and order as a scan over all queries)
         float acc = 0.f;
-        for (int qi = 0; qi < s; ++qi) {
-          const int yk = qi / side - dy, xk = qi % side - dx;
-          if (yk >= 0 && yk < side && xk >= 0 && xk < side)
-            acc += sDs[(wl * s + qi) * kTcQ + wl * s + yk * side + xk];
-        }
+        const int y0 = max(0, dy), y1 = min(side, side + dy);
+        const int x0 = max(0, dx), x1 = min(side, side + dx);
+        const float* base = sDs + wl * s * kTcQ + wl * s;
+        for (int yq = y0; yq < y1; ++yq)
+          for (int xq = x0; xq < x1; ++xq)
+            acc += base[(yq * side + xq) * kTcQ + (yq - dy) * side + (xq - dx)];
         static_cast<float*>(p.rpb_dpart)[(static_cast<int64_t>(u) * H + h) * n * n + e] = acc;
       }
     }

@@ -21,3 +21,19 @@ print(json.dumps({"ctas": int((t[:, 0] > 0).sum()), "span_us": round(float(rel[:
                   "per_cta_us": {n_: round(float(((t[:, i] - t[:, 0]) / 1000.0).median()), 2) for i, n_ in
                                  enumerate(["entry", "pdl", "s_ready", "max_done", "p_done", "o_ready"])},
                   "cta_total_median_us": round(float(dur.median()), 2)}))
+
+# backward: stamps 0 entry, 1 pdl, 2 prologue done, 4 chunk-0 scores ready, 5 softmax done,
+# 7 Pd / dS stored, 25 epilogue done, 26 cluster barrier passed, 27 exit
+ctx, lse, mask = K.attention_fwd(qkv, n, s, H, d, p=0.1, seed=1, rpb=tab)
+dctx = torch.randn(n * s, H * d, device=dev).to(torch.bfloat16)
+dpart = torch.empty(n * H * 169, device=dev)
+trb = torch.zeros(tiles * H * 32, dtype=torch.int64, device=dev)
+for i in range(3):
+    K.attention_bwd(qkv, ctx, lse, dctx, n, s, H, d, p=0.1, seed=1, mask=mask, rpb=tab,
+                    rpb_dpart=dpart, trace=trb if i == 2 else None)
+torch.cuda.synchronize()
+t = trb.view(-1, 32).cpu().double()
+names = {0: "entry", 1: "pdl", 2: "prologue_done", 4: "s_ready", 5: "softmax_done",
+         7: "pds_stored", 25: "epi_done", 26: "cluster_synced", 27: "exit"}
+print(json.dumps({"bwd_per_cta_us": {n_: round(float(((t[:, i] - t[:, 0]) / 1000.0).median()), 2)
+                                     for i, n_ in names.items()}}))
