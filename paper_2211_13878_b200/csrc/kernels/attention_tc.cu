@@ -924,7 +924,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint32_t o[16];
         tmem_ld16(trow + tq + c16 * 16, o);
         tmem_ld_wait();
-        if (v < g.vseq) {
+        if (nkt == 1) {  // the only key block: dQ is final -- bf16 straight into dqkv
+          if (v < g.vseq && vb * g.wpt + v / s < p.batch) {
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.dqkv) +
+                                                  (static_cast<int64_t>(row0) + v) * p.ld_qkv +
+                                                  h * hd + c16 * 16);
+            const float sc = p.scale;
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+              dst[i] = make_uint4(pack_bf16(__uint_as_float(o[8 * i]) * sc, __uint_as_float(o[8 * i + 1]) * sc),
+                                  pack_bf16(__uint_as_float(o[8 * i + 2]) * sc, __uint_as_float(o[8 * i + 3]) * sc),
+                                  pack_bf16(__uint_as_float(o[8 * i + 4]) * sc, __uint_as_float(o[8 * i + 5]) * sc),
+                                  pack_bf16(__uint_as_float(o[8 * i + 6]) * sc, __uint_as_float(o[8 * i + 7]) * sc));
+          }
+        } else if (v < g.vseq) {
           float* dst = part + ((static_cast<int64_t>(kt) * gridDim.y + blockIdx.y) * hd + c16 * 16) *
                                   vld + v;
 #pragma unroll
@@ -1134,6 +1147,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // every key block's dQ partials are in global memory after the cluster barrier; CTA kt then
   // owns query chunk kt and sums its partials in key-block order
   GX_ATTN_STAMP(p, 25);
+  if (nkt > 1) {  // (one key block: dQ was written final above)
   __threadfence();
   cluster_sync();
   GX_ATTN_STAMP(p, 26);
@@ -1193,6 +1207,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
   }
+  }  // nkt > 1
   GX_ATTN_STAMP(p, 27);
   __syncthreads();
   if (warp == 0) {
