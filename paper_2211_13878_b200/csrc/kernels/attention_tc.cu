@@ -59,6 +59,8 @@ struct Geom {
   int nk;     // keys staged per forward CTA: vseq rounded up to 64
   int tiles;  // ceil(batch / wpt)
   int gmask;  // the general masked path: windows packed, causal, shifted regions or bias
+  int fgen;   // forward: the general path (windows / regions / Swin bias); causal and the T5
+              // bias ride the plain path with per-block masking
 };
 
 Geom make_geom(const gx_attention_args& a) {
@@ -69,6 +71,7 @@ Geom make_geom(const gx_attention_args& a) {
   g.vseq = g.wpt * a.seq;
   g.nk = (g.vseq + 63) / 64 * 64;
   g.tiles = (a.batch + g.wpt - 1) / g.wpt;
+  g.fgen = (g.wpt > 1 || a.win_shift > 0 || a.rpb != nullptr) ? 1 : 0;
   g.gmask = (g.wpt > 1 || a.causal || a.win_shift > 0 || a.rpb != nullptr || a.relb != nullptr)
                 ? 1 : 0;
   return g;
@@ -200,7 +203,8 @@ constexpr int kFwdThreads = 512;  // 16 warps: four per TMEM lane quarter
 
 }  // namespace
 
-template <uint32_t kCols, bool kGen>
+// kCB (plain path only): causal masking and / or the T5 relative bias, per 64-key block
+template <uint32_t kCols, bool kGen, bool kCB = false>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const gx_attention_args p,
                        const Geom g) {
@@ -275,7 +279,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     __syncwarp();
   }
-  if (kGen) win_stage_tc(p, g, vb, h, win, kFwdThreads);  // visible after the barrier below
+  const bool relb = (kGen || kCB) && p.relb != nullptr;  // T5 relative bias
+  if (kGen || relb) win_stage_tc(p, g, vb, h, win, kFwdThreads);  // visible after the barrier below
 
   // ---------------------------------------------------------------- softmax over TMEM rows
   // 16 warps: four per TMEM lane quarter; 64-key blocks go round-robin to the four column
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const float c2 = p.scale * 1.4426950408889634f;
   mbar_wait(bar_s, 0);
   tc_fence_after();
-  if (kGen) named_sync(1, kFwdThreads);  // window metadata staged
+  if (kGen || relb) named_sync(1, kFwdThreads);  // window metadata staged
   GX_ATTN_STAMP(p, 2);
 
   // fast path (!kGen): keys [0, s) exist for every row; a 64-key block is either full or
@@ -382,22 +387,35 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int j = 0; j < 32; ++j) mx = fmaxf(mx, gen_x(c0 + j, v[j]));
       }
   }
+  // plain path: raw maxima where no key is masked or biased (scaled once below), scaled maxima
+  // of the masked / biased blocks (causal: keys past the row's query; T5: + bias)
+  const bool causal = kCB && p.causal != 0;
+  const int vq_lo_w = q0 + qd * 32;  // this warp's first row
+  float mxs = -INFINITY;
   for (int kb = cq; kb < nblk && !kGen; kb += 4) {
     uint32_t v[64];
     tmem_ld32(trow + kb * 64, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
     tmem_ld32(trow + kb * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
     tmem_ld_wait();
-    if (kb * 64 + 64 <= s) {
+    const bool clean = kb * 64 + 64 <= s && !(causal && kb * 64 + 63 > vq_lo_w) && !relb;
+    if (clean) {
 #pragma unroll
       for (int j = 0; j < 64; j += 2)
         mx = fmaxf(mx, fmaxf(__uint_as_float(v[j]), __uint_as_float(v[j + 1])));
     } else {
 #pragma unroll
-      for (int j = 0; j < 64; ++j)
-        if (kb * 64 + j < s) mx = fmaxf(mx, __uint_as_float(v[j]));
+      for (int j = 0; j < 64; ++j) {
+        const int c = kb * 64 + j;
+        if (c < s && !(causal && c > vq)) {
+          float x = __uint_as_float(v[j]) * c2;
+          if (relb && row_ok) x += win->rel[c - vq + s - 1];
+          mxs = fmaxf(mxs, x);
+        }
+      }
     }
   }
   if (!kGen && mx != -INFINITY) mx *= c2;
+  if (!kGen) mx = fmaxf(mx, mxs);
   // packed windows: the four column warps of a row split its four Philox calls (warp cq makes
   // call cq) and share the keep words through shared memory, instead of each drawing all four
   uint32_t* kwsm = reinterpret_cast<uint32_t*>(smem + L.kw);
@@ -536,8 +554,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int uu = 0; uu < 2; ++uu) {
           const int i = 2 * j2 + uu;
-          float e = ex2_ftz(fmaf(__uint_as_float(v[i]), c2, -m));
-          if (kTail && c0 + i >= s) e = 0.f;
+          float e;
+          if (kTail && kCB) {  // masked / biased block: causal, tail keys, T5 bias
+            const int c = c0 + i;
+            const bool ok = c < s && !(causal && c > vq);
+            const float b = relb && ok && row_ok ? win->rel[c - vq + s - 1] : 0.f;
+            e = ok ? ex2_ftz(fmaf(__uint_as_float(v[i]), c2, b - m)) : 0.f;
+          } else if (kTail) {  // tail keys only
+            e = c0 + i < s ? ex2_ftz(fmaf(__uint_as_float(v[i]), c2, -m)) : 0.f;
+          } else {
+            e = ex2_ftz(fmaf(__uint_as_float(v[i]), c2, -m));
+          }
           sum += e;
           // compile-time key position: the keep bit's word and shift fold to constants
           if (kDrop) e = keep_bit(bits, hb * 32 + i) ? e : 0.f;
@@ -549,7 +576,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     };
     using T_ = std::true_type;
     using F_ = std::false_type;
-    const bool full = kb * 64 + 64 <= s;
+    const bool full = kb * 64 + 64 <= s && !(causal && kb * 64 + 63 > vq_lo_w) && !relb;
 #pragma unroll
     for (int hb = 0; hb < 2; ++hb) {
       if (full) {
@@ -1273,24 +1300,28 @@ int attention_fwd_tc(const gx_attention_args& a, cudaStream_t st) {
     return set_error(kErrCuda, "attention_tc: tensor map encode failed");
   const int smem = fwd_layout(g.np, g.nk).bytes + 1024;
   dim3 grid((g.vseq + kTcQ - 1) / kTcQ, g.tiles * a.heads);
-#define GX_ATTN_TC(C, G)                                                                     \
+#define GX_ATTN_TC(C, G, CB)                                                                     \
   {                                                                                          \
     static bool set = false;                                                                 \
     if (!set) {                                                                              \
-      cudaFuncSetAttribute(attn_fwd_tc_kernel<C, G>,                                         \
+      cudaFuncSetAttribute(attn_fwd_tc_kernel<C, G, CB>,                                         \
                            cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);         \
       set = true;                                                                            \
     }                                                                                        \
-    launch_k(attn_fwd_tc_kernel<C, G>, grid, dim3(kFwdThreads), smem, st, map, a, g);        \
+    launch_k(attn_fwd_tc_kernel<C, G, CB>, grid, dim3(kFwdThreads), smem, st, map, a, g);        \
   }
-  if (g.gmask) {
-    if (g.nk <= 128) GX_ATTN_TC(128, true)
-    else if (g.nk <= 256) GX_ATTN_TC(256, true)
-    else GX_ATTN_TC(512, true)
+  if (g.fgen) {
+    if (g.nk <= 128) GX_ATTN_TC(128, true, false)
+    else if (g.nk <= 256) GX_ATTN_TC(256, true, false)
+    else GX_ATTN_TC(512, true, false)
+  } else if (a.causal || a.relb != nullptr) {
+    if (g.nk <= 128) GX_ATTN_TC(128, false, true)
+    else if (g.nk <= 256) GX_ATTN_TC(256, false, true)
+    else GX_ATTN_TC(512, false, true)
   } else {
-    if (g.nk <= 128) GX_ATTN_TC(128, false)
-    else if (g.nk <= 256) GX_ATTN_TC(256, false)
-    else GX_ATTN_TC(512, false)
+    if (g.nk <= 128) GX_ATTN_TC(128, false, false)
+    else if (g.nk <= 256) GX_ATTN_TC(256, false, false)
+    else GX_ATTN_TC(512, false, false)
   }
 #undef GX_ATTN_TC
   return check_launch("attn_fwd_tc_kernel");
