@@ -205,7 +205,7 @@ constexpr int kFwdThreads = 512;  // 16 warps: four per TMEM lane quarter
 
 // kCB (plain path only): causal masking and / or the T5 relative bias, per 64-key block
 template <uint32_t kCols, bool kGen, bool kCB = false>
-__global__ void __launch_bounds__(kFwdThreads, 1)
+__global__ void __launch_bounds__(kFwdThreads, (kGen && kCols == 128) ? 2 : 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const gx_attention_args p,
                        const Geom g) {
   extern __shared__ uint8_t smem_raw[];
