@@ -61,7 +61,6 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     e.aux = A.pre;
     e.ld_aux = ft;
     GX_TRY(gemm(dz, h, false, P + L.lay.w2.off, ft, true, rows, ft, h, e));  // dz W2 * gelu'
-    if (early_ok(r, L)) GX_TRY(early_adamw(r, L, L.lay.w2));
     GX_TRY(on_wgrad([&]() -> int {
       GX_TRY(timed(kElementwise, 0, 2.0 * rows * h, [&] { return colsum(dpre, ft, G + L.lay.b1.off, rows, ft, ls_, r.cs_ws[ls_ == stream_ ? 0 : 1]); }));
       const gx_gemm_epilogue w1 = wgrad_ep(L.lay.w1, h);
@@ -81,7 +80,6 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       c.ldo = h;
       GX_TRY(gemm(dpre, ft, false, P + L.lay.w1.off, h, true, rows, h, ft, c));  // dpre W1
     }
-    if (early_ok(r, L)) GX_TRY(early_adamw(r, L, L.lay.w1));
     if (t > 1)
       return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.acc32, static_cast<size_t>(rows) * h,
                           DType::kF32, stream_);
@@ -130,7 +128,6 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
     c.out = r.dctx;
     c.ldo = ht;
     GX_TRY(gemm(dout, h, false, P + L.lay.wo.off, ht, true, rows, ht, h, c));  // dout Wo
-    if (early_ok(r, L)) GX_TRY(early_adamw(r, L, L.lay.wo));
     gx_attention_args at{};
     at.batch = A.samples * s.windows();  // one attention sequence per window
     at.seq = s.win;
@@ -215,7 +212,6 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
                           "sw-msa da"));
       }
     }
-    if (early_ok(r, L)) GX_TRY(early_adamw(r, L, L.lay.wqkv));
     if (s.shift > 0) r.da_slices = 0;  // bf16 in r.da
     if (t > 1)
       return r.da_slices == 0

@@ -52,36 +52,11 @@ int ExecutorImpl::sync_phase(RankCtx& r, int li, int phase) {
     if (on_cs) GX_TRY(fork(cs_, side_));
     side_used_ = true;
     tmark("opt_begin L" + std::to_string(L.layer), side_);
-    if (early_ok(r, L)) {  // the four block matrices went early: the ranges between them
-      std::vector<Slot> done = {L.lay.wqkv, L.lay.wo, L.lay.w1, L.lay.w2};
-      std::sort(done.begin(), done.end(),
-                [](const Slot& a, const Slot& b) { return a.off < b.off; });
-      int64_t at = 0;
-      done.push_back(Slot{L.shard_n, 0});
-      for (const Slot& d : done) {
-        if (d.off > at)
-          GX_TRY(adamw_dev(L.master + at, L.gshard + at, L.m + at, L.v + at, L.pshard + at,
-                           d.off - at, lr_, b1_, b2_, eps_, wd_, r.step, side_, 2 * num_sms()));
-        at = std::max(at, d.off + d.n);
-      }
-    } else {
-      GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_,
-                       wd_, r.step, side_, 2 * num_sms()));
-    }
+    GX_TRY(adamw_dev(L.master, L.gshard, L.m, L.v, L.pshard, L.shard_n, lr_, b1_, b2_, eps_, wd_,
+                     r.step, side_, 2 * num_sms()));
     tmark("opt_end L" + std::to_string(L.layer), side_);
   }
   return kOk;
-}
-
-// AdamW of one weight matrix of layer L (see early_ok): after its weight gradient on wg_ and
-// its data-gradient GEMM on stream_
-int ExecutorImpl::early_adamw(RankCtx& r, RankLayer& L, const Slot& s) {
-  if (s.n == 0) return kOk;
-  GX_TRY(fork(stream_, side_));
-  GX_TRY(fork(wg_, side_));
-  side_used_ = true;
-  return adamw_dev(L.master + s.off, L.gshard + s.off, L.m + s.off, L.v + s.off, L.pshard + s.off,
-                   s.n, lr_, b1_, b2_, eps_, wd_, r.step, side_, 2 * num_sms());
 }
 
 int ExecutorImpl::gather_params(RankCtx& r, int li, cudaStream_t st) {

@@ -194,7 +194,6 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     comm_stream_ = cfg.value("comm_stream", true);
     trace_ = cfg.value("trace", false);
     fuse_dz_ = cfg.value("fuse_dz", false);
-    early_adamw_ = cfg.value("early_adamw", false);
     thr_attn_ = threshold_of(p_attn_);
     thr_hidden_ = threshold_of(p_hidden_);
 

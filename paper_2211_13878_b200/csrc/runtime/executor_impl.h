@@ -488,17 +488,6 @@ class ExecutorImpl final : public Executor {
   cudaStream_t ls_ = nullptr;
   bool wgrad_stream_ = true;  // cfg "wgrad_stream": false keeps the wgrads on stream_
   bool fuse_dz_ = false;      // previous layer's dropout bwd inside LN1 bwd (cfg "fuse_dz")
-  // cfg "early_adamw": the AdamW of each weight matrix of a layer runs on side_ as soon as its
-  // weight gradient (wg_) and its data-gradient GEMM (stream_, the last reader of the bf16
-  // weights in this step) are issued, so it reads the gradient while it is still in L2;
-  // phase 2 then updates only the rest of the layer (biases, LayerNorms, other matrices).
-  // Single micro-batch, no DP / SDP gradient collective, wgrad stream on.
-  bool early_adamw_ = false;
-  bool early_ok(const RankCtx& r, const RankLayer& L) const {
-    return early_adamw_ && optimizer_ && !profiling_ && wg_active_ && m_ == 1 && L.d.sdp == 1 &&
-           L.d.dp == 1 && !r.idle_chunks;
-  }
-  int early_adamw(RankCtx& r, RankLayer& L, const Slot& s);
   // AdamW of each layer runs on the side stream as a resident grid of 2 blocks per SM
   // (64-register blocks): enough HBM parallelism without crowding the backward's GEMMs off
   // their SMs (DESIGN.md §7.2 lists the placements measured and rejected).
