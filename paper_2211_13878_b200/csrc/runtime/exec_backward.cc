@@ -48,8 +48,7 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       r.wg_pending[par] = false;
     }
     d.site = 3ull * l + 2;
-    if (!A.dz_ready)
-      GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(dY, dz, G + L.lay.b2.off, rows, h, d, stream_, r.cs_ws[0]); }));
+    GX_TRY(timed(kElementwise, 0, 4.0 * rows * h, [&] { return dropout_bwd_colsum(dY, dz, G + L.lay.b2.off, rows, h, d, stream_, r.cs_ws[0]); }));
     const gx_gemm_epilogue w2 = wgrad_ep(L.lay.w2, ft);
     // dW2 = dz^T gel, as early as its inputs exist
     GX_TRY(on_wgrad([&] { return gemm(dz, h, true, A.gel, ft, true, h, ft, rows, w2); }));
@@ -223,39 +222,13 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
   }
   if (phase == ln1_ph) {
     const void* da_in = r.da_slices ? static_cast<const void*>(r.acc32) : static_cast<const void*>(r.da);
-    // When this layer's input is the previous layer's output (same rows), the previous
-    // layer's MLP dropout backward rides along: dz_{l-1} = dropout_mask(dX), db2_{l-1} +=
-    // colsum(dz_{l-1}) -- its phase 0 then starts straight at the GEMMs.
-    Acts* prev = nullptr;
-    RankLayer* Lp = nullptr;
-    if (fuse_dz_ && li > 0 && L.xin == Xin::kSame && r.layers[li - 1].sh.h == h) {
-      Lp = &r.layers[li - 1];
-      prev = &Lp->acts[mb];
-    }
-    gx_dropout dp{};
-    bf16* dz_prev = nullptr;
-    if (prev != nullptr) {
-      const int pp = (li - 1) & 1;
-      if (r.wg_pending[pp]) {  // that parity's buffers are free once their wgrads are done
-        GX_TRY(cuda_check(cudaStreamWaitEvent(stream_, r.wg_done[pp], 0), "wgrad wait"));
-        r.wg_pending[pp] = false;
-      }
-      dp.threshold = thr_hidden_;
-      dp.scale = scale_of(p_hidden_);
-      dp.seed = seed_;
-      dp.site = 3ull * Lp->layer + 2;
-      dp.row_offset = prev->sample0 * Lp->sh.seq;
-      dp.drop_ld = h;
-      dp.seed_offset = r.seed_off;
-      dz_prev = r.dzb[pp];
-    }
     float* fold1 = r.lnfold[par][1];
     GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd_rows(da_in, A.x, A.mean1, A.rstd1, P + L.lay.ln1g.off, r.dx1, dX,
-                         rows, h, stream_, r.da_slices > 0, prev ? &dp : nullptr, dz_prev,
+                         rows, h, stream_, r.da_slices > 0, nullptr, nullptr,
                          std::max(1, r.da_slices), static_cast<int64_t>(rows) * h, fold1); }));
     GX_TRY(on_wgrad([&]() -> int {
-      GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd_cols(fold1, true, A.x, A.mean1, A.rstd1, dz_prev,
-                           G + L.lay.ln1g.off, G + L.lay.ln1b.off, prev ? Lp->gfull + Lp->lay.b2.off : nullptr,
+      GX_TRY(timed(kNorm, 0, 8.0 * rows * h, [&] { return layernorm_bwd_cols(fold1, true, A.x, A.mean1, A.rstd1, nullptr,
+                           G + L.lay.ln1g.off, G + L.lay.ln1b.off, nullptr,
                            rows, h, r.ln_ws, ls_); }));
       if (wg_active_) {  // the last reader of this parity's buffers
         GX_TRY(cuda_check(cudaEventRecord(r.wg_done[par], wg_), "wgrad done"));
@@ -263,7 +236,6 @@ int ExecutorImpl::bwd_phase(RankCtx& r, int li, int mb, int phase) {
       }
       return kOk;
     }));
-    if (prev != nullptr) prev->dz_ready = true;
     if (s.merge) GX_TRY(merge_bwd(r, L, A, dX, wgrad_ep(L.lay.wm, 2 * h)));
     if (li == r.dec_li && t > 1)  // TP ranks hold per-head partial sums of dL/dmem
       return c_all_reduce(kTpAllReduce, L.g_tp, r.rank, r.dmem, static_cast<size_t>(rows) * h, DType::kF32,

@@ -25,7 +25,7 @@ int ExecutorImpl::step_once() {
   };
   for (auto& r : ranks_) {
     for (RankLayer& L : r->layers)
-      for (Acts& a : L.acts) a.ln1_ready = a.dz_ready = false;
+      for (Acts& a : L.acts) a.ln1_ready = false;
     GX_TRY(bump_step(r->step, nullptr, stream_));
     GX_TRY(cuda_check(cudaMemsetAsync(r->loss, 0, 4, stream_), "memset loss"));
     for (RankLayer& L : r->layers)

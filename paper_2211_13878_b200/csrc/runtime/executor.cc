@@ -193,7 +193,6 @@ int ExecutorImpl::init(const json& cfg, std::string* err) {
     wgrad_stream_ = cfg.value("wgrad_stream", true);
     comm_stream_ = cfg.value("comm_stream", true);
     trace_ = cfg.value("trace", false);
-    fuse_dz_ = cfg.value("fuse_dz", false);
     thr_attn_ = threshold_of(p_attn_);
     thr_hidden_ = threshold_of(p_hidden_);
 

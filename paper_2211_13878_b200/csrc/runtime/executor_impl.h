@@ -114,7 +114,6 @@ struct Acts {
   float *lse2 = nullptr, *mean3 = nullptr, *rstd3 = nullptr;
   uint16_t* amask2 = nullptr;
   bool ln1_ready = false;     // LN1 already produced by the previous layer's fused epilogue
-  bool dz_ready = false;      // backward: dz / db2 already produced by the next layer's LN1 bwd
 };
 
 enum class Xin { kSame, kSlice, kGather, kStageInput };
@@ -487,7 +486,6 @@ class ExecutorImpl final : public Executor {
   cudaStream_t wg_ = nullptr;
   cudaStream_t ls_ = nullptr;
   bool wgrad_stream_ = true;  // cfg "wgrad_stream": false keeps the wgrads on stream_
-  bool fuse_dz_ = false;      // previous layer's dropout bwd inside LN1 bwd (cfg "fuse_dz")
   // AdamW of each layer runs on the side stream as a resident grid of 2 blocks per SM
   // (64-register blocks): enough HBM parallelism without crowding the backward's GEMMs off
   // their SMs (DESIGN.md §7.2 lists the placements measured and rejected).

@@ -1,7 +1,7 @@
 """A/B of executor options on the bench workload (BERT-Huge-32, the searched N = 1 plan):
 graph-replayed ms per step for each option set, alternating, two rounds.
 
-  python scripts/knob_ab.py '{}' '{"fuse_dz": true}'
+  python scripts/knob_ab.py '{}' '{"splitk": false}'
 """
 import ctypes
 import json
