@@ -391,6 +391,8 @@ __global__ void __launch_bounds__(kFwdThreads, (kGen && kCols == 128) ? 2 : 1)
   // of the masked / biased blocks (causal: keys past the row's query; T5: + bias)
   const bool causal = kCB && p.causal != 0;
   const int vq_lo_w = q0 + qd * 32;  // this warp's first row
+  // T5 bias of key c for this row: relrow[c] (padding rows read row s - 1's; index <= 1022)
+  const float* relrow = win->rel + (s - 1 - min(vq, s - 1));
   float mxs = -INFINITY;
   for (int kb = cq; kb < nblk && !kGen; kb += 4) {
     uint32_t v[64];
@@ -403,15 +405,15 @@ __global__ void __launch_bounds__(kFwdThreads, (kGen && kCols == 128) ? 2 : 1)
       for (int j = 0; j < 64; j += 2)
         mx = fmaxf(mx, fmaxf(__uint_as_float(v[j]), __uint_as_float(v[j + 1])));
     } else {
+      float m2[2] = {-INFINITY, -INFINITY};  // (two chains: even / odd keys)
 #pragma unroll
       for (int j = 0; j < 64; ++j) {
         const int c = kb * 64 + j;
-        if (c < s && !(causal && c > vq)) {
-          float x = __uint_as_float(v[j]) * c2;
-          if (relb && row_ok) x += win->rel[c - vq + s - 1];
-          mxs = fmaxf(mxs, x);
-        }
+        float x = __uint_as_float(v[j]) * c2;
+        if (relb) x += relrow[c];
+        if (c < s && !(causal && c > vq)) m2[j & 1] = fmaxf(m2[j & 1], x);
       }
+      mxs = fmaxf(mxs, fmaxf(m2[0], m2[1]));
     }
   }
   if (!kGen && mx != -INFINITY) mx *= c2;
@@ -543,8 +545,9 @@ __global__ void __launch_bounds__(kFwdThreads, (kGen && kCols == 128) ? 2 : 1)
     tmem_ld32(trow + kb * 64, vv[0]);
     tmem_ld32(trow + kb * 64 + 32, vv[1]);
     tmem_ld_wait();
-    auto half = [&](auto tail_tag, auto drop_tag, int hb) {
+    auto half = [&](auto tail_tag, auto drop_tag, auto bias_tag, int hb) {
       constexpr bool kTail = decltype(tail_tag)::value, kDrop = decltype(drop_tag)::value;
+      constexpr bool kBias = decltype(bias_tag)::value;  // (full block, T5 bias only)
       const int c0 = kb * 64 + hb * 32;
       const uint32_t (&v)[32] = vv[hb];
       uint32_t pk[16];
@@ -558,8 +561,10 @@ __global__ void __launch_bounds__(kFwdThreads, (kGen && kCols == 128) ? 2 : 1)
           if (kTail && kCB) {  // masked / biased block: causal, tail keys, T5 bias
             const int c = c0 + i;
             const bool ok = c < s && !(causal && c > vq);
-            const float b = relb && ok && row_ok ? win->rel[c - vq + s - 1] : 0.f;
+            const float b = relb ? relrow[c] : 0.f;
             e = ok ? ex2_ftz(fmaf(__uint_as_float(v[i]), c2, b - m)) : 0.f;
+          } else if (kBias) {
+            e = ex2_ftz(fmaf(__uint_as_float(v[i]), c2, relrow[c0 + i] - m));
           } else if (kTail) {  // tail keys only
             e = c0 + i < s ? ex2_ftz(fmaf(__uint_as_float(v[i]), c2, -m)) : 0.f;
           } else {
@@ -576,13 +581,15 @@ __global__ void __launch_bounds__(kFwdThreads, (kGen && kCols == 128) ? 2 : 1)
     };
     using T_ = std::true_type;
     using F_ = std::false_type;
-    const bool full = kb * 64 + 64 <= s && !(causal && kb * 64 + 63 > vq_lo_w) && !relb;
+    const bool full = kb * 64 + 64 <= s && !(causal && kb * 64 + 63 > vq_lo_w);
 #pragma unroll
     for (int hb = 0; hb < 2; ++hb) {
-      if (full) {
-        if (thr != 0u) half(F_{}, T_{}, hb); else half(F_{}, F_{}, hb);
+      if (full && !relb) {
+        if (thr != 0u) half(F_{}, T_{}, F_{}, hb); else half(F_{}, F_{}, F_{}, hb);
+      } else if (kCB && full) {  // every key attended, T5 bias
+        if (thr != 0u) half(F_{}, T_{}, T_{}, hb); else half(F_{}, F_{}, T_{}, hb);
       } else {
-        if (thr != 0u) half(T_{}, T_{}, hb); else half(T_{}, F_{}, hb);
+        if (thr != 0u) half(T_{}, T_{}, F_{}, hb); else half(T_{}, F_{}, F_{}, hb);
       }
     }
   }
@@ -1101,14 +1108,32 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // T5 bias gradient: thread t sums the chunk tile's diagonal delta = key - query
         // (local) = t - 127 in query order and adds it to the CTA's sum of relative position
         // (kt - j) 128 + delta; chunks go in order (deterministic)
+        // All 512 threads: thread t sums one half (t / 256) of diagonal t % 256 - 127 with
+        // four interleaved accumulators; the halves are added in order after a barrier.
         named_sync(1, kBwdSoftmax);  // the fp32 dS tile of chunk j is complete
+        const int dl = static_cast<int>(threadIdx.x & 255);
+        const int delta = dl - (kTcQ - 1);
+        float acc = 0.f;
+        if (dl < 2 * kTcQ - 1) {
+          const int lo = max(0, -delta), hi = min(kTcQ, kTcQ - delta);
+          const int mid = (lo + hi) >> 1;
+          const int a0 = threadIdx.x < 256 ? lo : mid, a1 = threadIdx.x < 256 ? mid : hi;
+          float e[4] = {0.f, 0.f, 0.f, 0.f};
+          int qi = a0;
+          for (; qi + 3 < a1; qi += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) e[u] += sDs[(qi + u) * (kTcQ + 1) + delta];
+          }
+          for (; qi < a1; ++qi) e[0] += sDs[qi * (kTcQ + 1) + delta];
+          acc = (e[0] + e[1]) + (e[2] + e[3]);
+        }
+        float* dhalf = sDs + kTcQ * kTcQ - 256;  // (row 127's last 256 words: read above)
+        named_sync(1, kBwdSoftmax);
+        if (threadIdx.x >= 256) dhalf[dl] = acc;
+        named_sync(1, kBwdSoftmax);
         if (threadIdx.x < 2 * kTcQ - 1) {
-          const int delta = static_cast<int>(threadIdx.x) - (kTcQ - 1);
-          float acc = 0.f;
-          for (int qi = max(0, -delta); qi < min(kTcQ, kTcQ - delta); ++qi)
-            acc += sDs[qi * (kTcQ + 1) + delta];
           const int idx = (kt - j) * kTcQ + delta + s - 1;
-          if (idx >= 0 && idx < 2 * s - 1) sDiag[idx] += acc;
+          if (idx >= 0 && idx < 2 * s - 1) sDiag[idx] += acc + dhalf[dl];
         }
       }
       // the fp32 dS tile (bias gradients) is rewritten by the next chunk: all readers first

@@ -23,6 +23,8 @@ SHAPES = [  # (name, sequences, seq, heads, head_dim, kw)
     ("bert-huge B=2 (sdp:8 per GPU)", 2, 512, 20, 64, {}),
     ("vit-huge B=4", 4, 257, 16, 80, {}),
     ("t5 causal B=2", 2, 512, 16, 64, {"causal": True}),
+    ("t5 encoder relb B=2", 2, 512, 16, 64, {"relb": True}),
+    ("t5 decoder causal+relb B=2", 2, 512, 16, 64, {"causal": True, "relb": True}),
     ("swin stage0 8 samples (W-MSA+rpb)", 8 * 64, 49, 10, 32, {"rpb": True}),
 ]
 
@@ -45,6 +47,11 @@ def run(name, n, s, H, d, kw):
         extra = {"rpb": tab, "rpb_dpart": dpart}
     if kw.get("causal"):
         extra["causal"] = True
+    if kw.get("relb"):  # 32-bucket table; any in-range bucket map times the same
+        extra["relb"] = torch.randn(H, 32, device=dev).to(torch.bfloat16)
+        extra["relb_map"] = torch.tensor([min(abs(t) // 16, 31) for t in range(1 - s, s)],
+                                         dtype=torch.int8, device=dev)
+        extra["relb_dpart"] = torch.empty(n * H * ((s + 127) // 128) * (2 * s - 1), device=dev)
     a = K._attn_args(qkv, n, s, H, d, 0.1, 1234, 3, **extra)
     a.ctx, a.ld_ctx, a.lse, a.mask = K._ptr(ctx), ctx.stride(0), K._ptr(lse), K._ptr(mask)
     a.dctx, a.dqkv, a.dq_accum, a.dsum = K._ptr(dctx), K._ptr(dqkv), K._ptr(dq_acc), K._ptr(dsum)

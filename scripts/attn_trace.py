@@ -4,15 +4,24 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2211_13878_b200 import kernels as K  # noqa: E402
 dev = torch.device("cuda:0")
-B, s, H, d = 1, 512, 20, 64
+B, s, H, d = int(os.environ.get("B", 1)), 512, int(os.environ.get("H", 20)), 64
+kw = {}
+if os.environ.get("CAUSAL"):
+    kw["causal"] = True
+if os.environ.get("RELB"):  # T5 relative bias (any in-range bucket map times the same)
+    kw["relb"] = torch.randn(H, 32, device=dev).to(torch.bfloat16)
+    kw["relb_map"] = torch.tensor([min(abs(t) // 16, 31) for t in range(1 - s, s)],
+                                  dtype=torch.int8, device=dev)
 qkv = (torch.randn(B * s, 3 * H * d, device=dev) * 0.5).to(torch.bfloat16)
 dctx = torch.randn(B * s, H * d, device=dev).to(torch.bfloat16)
-ctx, lse, mask = K.attention_fwd(qkv, B, s, H, d, p=0.1, seed=1)
+ctx, lse, mask = K.attention_fwd(qkv, B, s, H, d, p=0.1, seed=1, **kw)
+if "relb" in kw:
+    kw["relb_dpart"] = torch.empty(B * H * 4 * (2 * s - 1), device=dev)
 ncta = 4 * B * H
 tr = torch.zeros(ncta * 32, dtype=torch.int64, device=dev)
 for i in range(4):
     K.attention_bwd(qkv, ctx, lse, dctx, B, s, H, d, p=0.1, seed=1, mask=mask,
-                    trace=tr if i == 3 else None)
+                    trace=tr if i == 3 else None, **kw)
 torch.cuda.synchronize()
 t = tr.view(ncta, 32).cpu().double()
 t0 = t[:, 0][t[:, 0] > 0].min()
@@ -32,7 +41,8 @@ print(json.dumps(out))
 nq = (s + 127) // 128
 trf = torch.zeros(nq * B * H * 32, dtype=torch.int64, device=dev)
 for i in range(4):
-    K.attention_fwd(qkv, B, s, H, d, p=0.1, seed=1, trace=trf if i == 3 else None)
+    K.attention_fwd(qkv, B, s, H, d, p=0.1, seed=1, trace=trf if i == 3 else None,
+                    **{k: v for k, v in kw.items() if k != "relb_dpart"})
 torch.cuda.synchronize()
 t = trf.view(-1, 32).cpu().double()
 t0 = t[:, 0][t[:, 0] > 0].min()
