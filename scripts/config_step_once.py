@@ -18,6 +18,8 @@ ex.load_batch(torch.zeros(B * sh["seq"], sh["hidden"], dtype=torch.int16),
 for _ in range(W):
     ex.run(False)
 torch.cuda.synchronize()
-print("launches_per_step", ex.info()["launches_per_step"], file=sys.stderr)
+info = ex.info()
+print("launches_per_step", info["launches_per_step"], file=sys.stderr)
+print("wgrad_split_gemms_per_step", info["wgrad_split_gemms_per_step"], file=sys.stderr)
 ex.run(False)
 torch.cuda.synchronize()
