@@ -20,6 +20,5 @@ for _ in range(W):
 torch.cuda.synchronize()
 info = ex.info()
 print("launches_per_step", info["launches_per_step"], file=sys.stderr)
-print("wgrad_split_gemms_per_step", info["wgrad_split_gemms_per_step"], file=sys.stderr)
 ex.run(False)
 torch.cuda.synchronize()
