@@ -263,6 +263,51 @@ __global__ void __launch_bounds__(kFwdThreads, (kGen && kCols == 128) ? 2 : 1)
       for (int pn = 0; pn < np; ++pn)
         for (int r = 0; r < nk; r += 64)
           tma_box(smem + L.kv + pn * nk * 128 + r * 128, &map_qkv, bar_v, cv + pn * 64, row0 + r);
+    }
+    __syncwarp();
+  }
+
+  // ---------------------------------------------------------------- rows of this thread
+  // 16 warps: four per TMEM lane quarter; 64-key blocks go round-robin to the four column
+  // quarters (a block's two 32-key halves stay with one thread, so its Philox draws are
+  // shared), and the quarters exchange row max / row sum through shared memory.
+  const int qd = warp & 3, cq = warp >> 2;
+  const int r = qd * 32 + lane;  // tile row == TMEM lane
+  const int vq = q0 + r;         // virtual query
+  const int u = vb * g.wpt + vq / s;  // its attention sequence (unit)
+  const int q = vq % s;               // real query index
+  const bool row_ok = vq < g.vseq && u < p.batch;
+  const int nblk = nk / 64;
+  const uint32_t thr = p.drop_threshold;
+  const uint64_t seed = p.seed + (p.seed_offset != nullptr ? *p.seed_offset : 0ull);
+  const int nkb = (s + 63) / 64;  // real 64-key blocks per query
+  const uint64_t stream =
+      (static_cast<uint64_t>(p.sample_offset + u) * p.heads_total + (p.head_offset + h)) * s;
+  uint16_t* mask = static_cast<uint16_t*>(p.mask);
+  const int64_t bh_real = static_cast<int64_t>(u) * H + h;
+  // Plain path: the dropout keep bits depend only on (seed, site, element), so each thread
+  // draws its blocks' Philox words while Q / K / V are still in flight (warp 0 before it
+  // issues S = Q K^T), and stores them for the backward; the exp pass only tests bits.
+  constexpr int kItems = (static_cast<int>(kCols) / 64 + 3) / 4;  // 64-key blocks per thread
+  uint32_t kbits[kItems][4];
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) kbits[it][0] = kbits[it][1] = kbits[it][2] = kbits[it][3] = 0u;
+  if (!kGen && thr != 0u) {
+#pragma unroll
+    for (int it = 0; it < kItems; ++it) {
+      const int kb = cq + 4 * it;
+      if (kb < nblk) {
+        keep16x4(seed, p.site, ((stream + static_cast<uint64_t>(q)) * nkb + kb) * 4, thr, kbits[it]);
+        if (row_ok && kb < nkb)
+          *reinterpret_cast<uint64_t*>(mask + ((bh_real * s + q) * nkb + kb) * 4) =
+              static_cast<uint64_t>(kbits[it][0]) | (static_cast<uint64_t>(kbits[it][1]) << 16) |
+              (static_cast<uint64_t>(kbits[it][2]) << 32) | (static_cast<uint64_t>(kbits[it][3]) << 48);
+      }
+    }
+  }
+
+  if (warp == 0) {
+    if (lane == 0) {
       mbar_wait(bar_qk, 0);
       tc_fence_after();
       for (int n0 = 0; n0 < nk; n0 += 256) {
@@ -283,16 +328,6 @@ __global__ void __launch_bounds__(kFwdThreads, (kGen && kCols == 128) ? 2 : 1)
   if (kGen || relb) win_stage_tc(p, g, vb, h, win, kFwdThreads);  // visible after the barrier below
 
   // ---------------------------------------------------------------- softmax over TMEM rows
-  // 16 warps: four per TMEM lane quarter; 64-key blocks go round-robin to the four column
-  // quarters (a block's two 32-key halves stay with one thread, so its Philox draws are
-  // shared), and the quarters exchange row max / row sum through shared memory.
-  const int qd = warp & 3, cq = warp >> 2;
-  const int r = qd * 32 + lane;  // tile row == TMEM lane
-  const int vq = q0 + r;         // virtual query
-  const int u = vb * g.wpt + vq / s;  // its attention sequence (unit)
-  const int q = vq % s;               // real query index
-  const bool row_ok = vq < g.vseq && u < p.batch;
-  const int nblk = nk / 64;
   const uint32_t trow = tmem + (static_cast<uint32_t>(qd * 32) << 16);
   const float c2 = p.scale * 1.4426950408889634f;
   mbar_wait(bar_s, 0);
@@ -434,14 +469,7 @@ __global__ void __launch_bounds__(kFwdThreads, (kGen && kCols == 128) ? 2 : 1)
   float m = fmaxf(fmaxf(red[r], red[kTcQ + r]), fmaxf(red[2 * kTcQ + r], red[3 * kTcQ + r]));
   if (m == -INFINITY) m = 0.f;  // an empty row (padding) keeps finite arithmetic
 
-  const uint32_t thr = p.drop_threshold;
   const float inv_keep = p.drop_scale;
-  const uint64_t seed = p.seed + (p.seed_offset != nullptr ? *p.seed_offset : 0ull);
-  const int nkb = (s + 63) / 64;  // real 64-key blocks per query
-  const uint64_t stream =
-      (static_cast<uint64_t>(p.sample_offset + u) * p.heads_total + (p.head_offset + h)) * s;
-  uint16_t* mask = static_cast<uint16_t*>(p.mask);
-  const int64_t bh_real = static_cast<int64_t>(u) * H + h;
   // packed short sequences: one 64-key real block per query, drawn once per row
   uint32_t wrow[4] = {0u, 0u, 0u, 0u};
   if (kGen && g.wpt > 1 && thr != 0u) {
@@ -526,19 +554,11 @@ __global__ void __launch_bounds__(kFwdThreads, (kGen && kCols == 128) ? 2 : 1)
       }
     }
   }
-  for (int kb = cq; kb < nblk && !kGen; kb += 4) {
-    uint32_t bits[4] = {0u, 0u, 0u, 0u};
-    if (thr != 0u) {
-      const uint64_t call0 = ((stream + static_cast<uint64_t>(q)) * nkb + kb) * 4;
-      keep16x4(seed, p.site, call0, thr, bits);
-      if (row_ok && kb < nkb) {
-        const uint64_t packed = static_cast<uint64_t>(bits[0]) |
-                                (static_cast<uint64_t>(bits[1]) << 16) |
-                                (static_cast<uint64_t>(bits[2]) << 32) |
-                                (static_cast<uint64_t>(bits[3]) << 48);
-        *reinterpret_cast<uint64_t*>(mask + ((bh_real * s + q) * nkb + kb) * 4) = packed;
-      }
-    }
+#pragma unroll
+  for (int it = 0; it < kItems; ++it) {
+    const int kb = cq + 4 * it;
+    if (kGen || kb >= nblk) break;
+    const uint32_t (&bits)[4] = kbits[it];  // drawn before S (above)
     // (warp-uniform: full blocks, i.e. all but a sequence's tail block, skip the per-key
     // bounds check; with dropout off the keep test is compiled out)
     uint32_t vv[2][32];  // both 32-column halves of the block in flight at once
