@@ -47,7 +47,7 @@ extern "C" int gx_k_gemm_bf16_splitk(const void* a, int64_t lda, int a_mn_major,
   ep.alpha = 1.f;
   ep.drop_scale = 1.f;
   int tile = tile_n;
-  if (splits <= 0) splits = gx::splitk_plan(M, N, K, &tile);
+  if (splits <= 0) splits = gx::splitk_plan(M, N, K, &tile, b_mn_major != 0);
   gx::GemmOperand A{a, lda, a_mn_major != 0};
   gx::GemmOperand B{b, ldb, b_mn_major != 0};
   return gx::gemm_bf16(A, B, M, N, K, ep, S(stream), tile, splits);

@@ -83,6 +83,70 @@ __device__ __forceinline__ float gelu_erf_grad(float x) {
   return g.phi_cdf + x * 0.3989422804014327f * g.e;
 }
 
+// Packed fp32 pairs (FFMA2 / FMUL2 / FADD2: one issue slot for two lanes' worth of math).
+// Each half rounds exactly like the scalar instruction, so results are bit-identical.
+using f2 = unsigned long long;
+__device__ __forceinline__ f2 f2_pack(float lo, float hi) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float f2_lo(f2 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return lo;
+}
+__device__ __forceinline__ float f2_hi(f2 v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return hi;
+}
+__device__ __forceinline__ f2 f2_splat(float a) { return f2_pack(a, a); }
+__device__ __forceinline__ f2 f2_fma(f2 a, f2 b, f2 c) {
+  f2 r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2 f2_mul(f2 a, f2 b) {
+  f2 r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// GeLU value and derivative of two bf16-rounded pre-activations (the gelu == 2 epilogue):
+// gelu_terms() on packed pairs.  The rational erf runs on the negated reciprocal
+// tn = -t = 1 / (-(1 + a z)), so -poly(t) comes out of one Horner chain with alternating
+// coefficient signs (negation is exact: every intermediate is the scalar chain's, negated).
+__device__ __forceinline__ void gelu2_pair(float x0, float x1, float& v0, float& v1, float& d0,
+                                           float& d1) {
+  const f2 x = f2_pack(x0, x1);
+  const f2 z = f2_mul(f2_pack(fabsf(x0), fabsf(x1)), f2_splat(0.70710678118654752f));
+  const f2 den = f2_fma(f2_splat(-0.3275911f), z, f2_splat(-1.f));
+  float tn0, tn1;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(tn0) : "f"(f2_lo(den)));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(tn1) : "f"(f2_hi(den)));
+  const f2 tn = f2_pack(tn0, tn1);
+  f2 hp = f2_fma(tn, f2_splat(1.061405429f), f2_splat(1.453152027f));
+  hp = f2_fma(tn, hp, f2_splat(1.421413741f));
+  hp = f2_fma(tn, hp, f2_splat(0.284496736f));
+  hp = f2_fma(tn, hp, f2_splat(0.254829592f));
+  const f2 npoly = f2_mul(tn, hp);  // -poly
+  const f2 arg = f2_mul(f2_mul(z, z), f2_splat(-1.4426950408889634f));  // (-z z) c, exactly
+  float e0, e1;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(f2_lo(arg)));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(f2_hi(arg)));
+  const f2 e = f2_pack(e0, e1);
+  const f2 erf_abs = f2_fma(npoly, e, f2_splat(1.f));  // 1 - poly e
+  const f2 s = f2_pack(copysignf(f2_lo(erf_abs), x0), copysignf(f2_hi(erf_abs), x1));
+  const f2 phi = f2_fma(s, f2_splat(0.5f), f2_splat(0.5f));  // 0.5 (1 + s): *0.5 is exact
+  const f2 v = f2_mul(x, phi);
+  const f2 d = f2_fma(f2_mul(x, f2_splat(0.3989422804014327f)), e, phi);
+  v0 = f2_lo(v);
+  v1 = f2_hi(v);
+  d0 = f2_lo(d);
+  d1 = f2_hi(d);
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -125,11 +189,10 @@ __device__ __forceinline__ void epilogue_math(const GemmEpilogue& ep, int64_t ro
     // forward that also hands the backward its derivative: aux <- gelu'(pre), computed from
     // the same erf / exp as the value, so the backward epilogue is a plain multiply
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float x = __bfloat162float(__float2bfloat16_rn(v[j]));
-      const GeluTerms g = gelu_terms(x);
-      v[j] = x * g.phi_cdf;
-      pre[j] = g.phi_cdf + x * 0.3989422804014327f * g.e;
+    for (int t = 0; t < 16; ++t) {
+      const float x0 = __bfloat162float(__float2bfloat16_rn(v[2 * t]));
+      const float x1 = __bfloat162float(__float2bfloat16_rn(v[2 * t + 1]));
+      gelu2_pair(x0, x1, v[2 * t], v[2 * t + 1], pre[2 * t], pre[2 * t + 1]);
     }
   } else if (ep.gelu) {
 #pragma unroll
@@ -993,7 +1056,7 @@ static int pick_bn(int M, int N) {
 // Split-K plan for a reduce-add GEMM: the CTA-pair 256-wide tile when M allows, and as many
 // K splits as fit one wave of pairs while keeping >= 4 k-blocks per split.  Returns the
 // split count and sets *tile (the force_bn argument of gemm_bf16).
-int splitk_plan(int M, int N, int K, int* tile) {
+int splitk_plan(int M, int N, int K, int* tile, bool b_mn) {
   // At most 4 slices: every slice is an M x N fp32 partial written here and read back by the
   // consuming row pass, so beyond 4 the partials' traffic costs more inside the step than the
   // extra CTAs gain (BERT-Huge-32, M = 512: 4 -> 8.94 ms / step, 7 -> 9.12, 3 -> 9.00; a
@@ -1001,12 +1064,31 @@ int splitk_plan(int M, int N, int K, int* tile) {
   constexpr int kMaxSplits = 4;
   const int kb = (K + kBK - 1) / kBK;
   if (M >= 256) {
-    const int bn = N > 128 ? 256 : 128;
-    *tile = -bn;
-    const int tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
-    int sp = (num_sms() / 2) / tiles;
-    sp = std::min(sp, kb / 4);
-    return std::max(1, std::min(sp, kMaxSplits));
+    // N tile: the one-wave plan whose CTAs each stream the fewest operand rows (128 of A +
+    // bn / 2 of B per k-block, over the split's k-blocks) -- at M = 512 the main loops are
+    // bound by each SM's ~120 GB/s of L2 ingest, not by its tensor rate.  160 (K-major B
+    // only) beats 256 for the MLP down-projection forward (N = 1280, K = 5120: 64 pairs of
+    // 208 rows x 20 k-blocks vs 40 pairs of 256 x 20; 13.4 -> 10.9 us, step -1.2 %); ties
+    // keep the wider tile.  (Charging the fp32 partial's bytes too picks 128 x 3 slices for
+    // the data-gradient GEMMs: each 12-14 % faster alone, but the step 2 % slower -- 120
+    // CTAs on the critical path leave fewer SMs to the weight-gradient / AdamW streams.)
+    int best_sp = 1, best_bn = N > 128 ? 256 : 128;
+    double best_cost = 1e30;
+    for (int bn : {256, 160, 128}) {
+      if ((bn == 256 && N <= 128) || (bn == 160 && (b_mn || N <= 128))) continue;
+      const int tiles = ((M + 255) / 256) * ((N + bn - 1) / bn);
+      int sp = std::min((num_sms() / 2) / tiles, kb / 4);
+      sp = std::max(1, std::min(sp, kMaxSplits));
+      const double cta_bytes = (128.0 + bn / 2) * kBK * 2 * ((kb + sp - 1) / sp);
+      const double cost = cta_bytes * ((tiles * sp + num_sms() / 2 - 1) / (num_sms() / 2));
+      if (cost < best_cost - 1e-9) {
+        best_cost = cost;
+        best_bn = bn;
+        best_sp = sp;
+      }
+    }
+    *tile = -best_bn;
+    return best_sp;
   }
   *tile = 128;
   const int tiles = ((M + kBM - 1) / kBM) * ((N + 127) / 128);

@@ -48,7 +48,7 @@ int gemm_bf16(const GemmOperand& a, const GemmOperand& b, int M, int N, int K,
 // [splits][M][N] fp32 buffer and the consumer (bias_dropout_add / layernorm_bwd) sums them in
 // slice order, so the result is deterministic (no atomics, no zero-fill).
 constexpr int kMaxSplits = 8;
-int splitk_plan(int M, int N, int K, int* tile);
+int splitk_plan(int M, int N, int K, int* tile, bool b_mn = true);
 
 int attention_fwd(const gx_attention_args& a, cudaStream_t st);
 // tcgen05/TMEM forward (attention_tc.cu): head_dim 64, seq <= 512; GX_ATTN_TC=0 disables

@@ -410,7 +410,7 @@ class ExecutorImpl final : public Executor {
     // out-projection K = 1280 split + row pass 19.8 us vs fused 10.4 + LayerNorm 5.5 us)
     if (!splitk_ || K < 2048) return kOk;
     int tile = 0;
-    const int sp = splitk_plan(M, N, K, &tile);
+    const int sp = splitk_plan(M, N, K, &tile, bmn);
     if (sp < 2) return kOk;
     gx_gemm_epilogue e{};
     e.alpha = 1.f;

@@ -56,7 +56,8 @@ def main():
     add("attn_fwd", 4.0 * B * H * s * s * hd, lambda: K.attention_fwd(qkv, B, s, H, hd, p=0.1, seed=1))
     add("out_fwd(bias+drop+res)", F(M, h, h),
         lambda: K.gemm(ctx, wo, out=outs["h"], bias=bh, residual=x, dropout_p=0.1, seed=1, site=1))
-    add("up_fwd(bias+gelu)", F(M, f, h), lambda: K.gemm(ln, w1, out=outs["f"], bias=bf_, gelu_aux=pre))
+    add("up_fwd(bias+gelu)", F(M, f, h), lambda: K.gemm(ln, w1, out=outs["f"], bias=bf_, gelu_aux=pre,
+                                                         gelu_mode=2))  # as the executor
     add("down_fwd(bias+drop+res)", F(M, h, f),
         lambda: K.gemm(gel, w2, out=outs["h"], bias=bh, residual=x, dropout_p=0.1, seed=1, site=2))
     add("down_fwd splitk", F(M, h, f), lambda: K.gemm_splitk(gel, w2, out=g32["mh"]))
@@ -65,7 +66,7 @@ def main():
     add("wgrad_down dW2", F(h, f, M), lambda: K.gemm(dz, gel, a_mn_major=True, b_mn_major=True,
                                                      out=g32["w2"], out_kind="f32"))
     add("dgrad_down(gelu_bwd)", F(M, f, h),
-        lambda: K.gemm(dz, w2, b_mn_major=True, out=outs["f"], gelu_bwd_aux=pre))
+        lambda: K.gemm(dz, w2, b_mn_major=True, out=outs["f"], gelu_bwd_aux=pre, gelu_mode=2))
     add("wgrad_up dW1", F(f, h, M), lambda: K.gemm(dpre, ln, a_mn_major=True, b_mn_major=True,
                                                    out=g32["w1"], out_kind="f32"))
     add("dgrad_up splitk", F(M, h, f), lambda: K.gemm_splitk(dpre, w1, b_mn_major=True, out=g32["mh"]))
