@@ -574,6 +574,15 @@ __global__ void __launch_bounds__(kFwdThreads, (kGen && kCols == 128) ? 2 : 1)
 #pragma unroll
       for (int j2 = 0; j2 < 16; ++j2) {
         float e2[2];
+        // full, unbiased block: both exp arguments from one packed FFMA2 (not in the causal /
+        // T5-bias instantiation: there it measured slower, 17.3 -> 20.0 us for T5 causal B = 2)
+        float a2[2] = {0.f, 0.f};
+        if constexpr (!kCB) {
+          const f2 arg = f2_fma(f2_pack(__uint_as_float(v[2 * j2]), __uint_as_float(v[2 * j2 + 1])),
+                                f2_splat(c2), f2_splat(-m));
+          a2[0] = f2_lo(arg);
+          a2[1] = f2_hi(arg);
+        }
 #pragma unroll
         for (int uu = 0; uu < 2; ++uu) {
           const int i = 2 * j2 + uu;
@@ -588,7 +597,7 @@ __global__ void __launch_bounds__(kFwdThreads, (kGen && kCols == 128) ? 2 : 1)
           } else if (kTail) {  // tail keys only
             e = c0 + i < s ? ex2_ftz(fmaf(__uint_as_float(v[i]), c2, -m)) : 0.f;
           } else {
-            e = ex2_ftz(fmaf(__uint_as_float(v[i]), c2, -m));
+            e = ex2_ftz(kCB ? fmaf(__uint_as_float(v[i]), c2, -m) : a2[uu]);
           }
           sum += e;
           // compile-time key position: the keep bit's word and shift fold to constants
@@ -781,7 +790,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const uint16_t* mask_g = static_cast<const uint16_t*>(p.mask);
     for (int v = threadIdx.x; v < g.vseq; v += kBwdSoftmax) {
       const int u = vb * g.wpt + v / s;
-      sLse[v] = u < p.batch ? lse_g[(static_cast<int64_t>(u) * H + h) * s + v % s] : 0.f;
+      // staged negated (as is D): the exp argument and dP - D are then plain (packed) FMAs
+      sLse[v] = u < p.batch ? -lse_g[(static_cast<int64_t>(u) * H + h) * s + v % s] : 0.f;
     }
     // (2 vseq <= 1024 words: both of a thread's loads issued before either store)
     uint64_t w[2];
@@ -962,7 +972,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           // (queries past the tile's end get D = 0: the last chunk reads them, and a stale
           // smem value could be NaN, which the zero P of a masked pair would not cancel)
           const int v = v0 + ps * (kBwdSoftmax / 4) + qi;
-          if (part4 == 0) sD[v] = acc;
+          if (part4 == 0) sD[v] = -acc;
         }
       }
     }
@@ -1036,14 +1046,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           const float4 d4 = *reinterpret_cast<const float4*>(sD + qg0 + 4 * i4);
           const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dd[4] = {d4.x, d4.y, d4.z, d4.w};
           float pd4[4], ds4[4];
+          // (lv, dd hold -lse, -D) pairs of queries on packed fp32 math: FFMA2 / FMUL2
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
+          for (int t = 0; t < 4; t += 2) {
             const int i = 4 * i4 + t;
-            float pr = ex2_ftz(fmaf(__uint_as_float(sv[i]), c2, -lv[t]));
-            pr = (vmask >> i) & 1u ? pr : 0.f;  // (padding: lse / D may be stale there)
-            const float f = thr == 0u || (mk[i * 8] & mbitm) != 0u ? fk : 0.f;
-            pd4[t] = pr * f;
-            ds4[t] = pr * fmaf(__uint_as_float(dv[i]), f, -dd[t]);
+            const f2 arg = f2_fma(f2_pack(__uint_as_float(sv[i]), __uint_as_float(sv[i + 1])),
+                                  f2_splat(c2), f2_pack(lv[t], lv[t + 1]));
+            float pr0 = ex2_ftz(f2_lo(arg)), pr1 = ex2_ftz(f2_hi(arg));
+            pr0 = (vmask >> i) & 1u ? pr0 : 0.f;  // (padding: lse / D may be stale there)
+            pr1 = (vmask >> (i + 1)) & 1u ? pr1 : 0.f;
+            const float f0 = thr == 0u || (mk[i * 8] & mbitm) != 0u ? fk : 0.f;
+            const float f1 = thr == 0u || (mk[(i + 1) * 8] & mbitm) != 0u ? fk : 0.f;
+            const f2 pr = f2_pack(pr0, pr1), f = f2_pack(f0, f1);
+            const f2 pd = f2_mul(pr, f);
+            const f2 ds = f2_mul(pr, f2_fma(f2_pack(__uint_as_float(dv[i]), __uint_as_float(dv[i + 1])),
+                                            f, f2_pack(dd[t], dd[t + 1])));
+            pd4[t] = f2_lo(pd);
+            pd4[t + 1] = f2_hi(pd);
+            ds4[t] = f2_lo(ds);
+            ds4[t + 1] = f2_hi(ds);
           }
           ppd[2 * i4] = pack_bf16(pd4[0], pd4[1]);
           ppd[2 * i4 + 1] = pack_bf16(pd4[2], pd4[3]);
@@ -1082,11 +1103,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             float bias = 0.f;
             if (valid && p.rpb != nullptr) bias = win->tab[win->kc[qg] + kbase];
             if (valid && p.relb != nullptr) bias += win->rel[key - qg + s - 1];
-            float pr = ex2_ftz(fmaf(__uint_as_float(sv[i]), c2, bias - lv[t]));
+            float pr = ex2_ftz(fmaf(__uint_as_float(sv[i]), c2, bias + lv[t]));  // (lv = -lse)
             pr = valid ? pr : 0.f;
             const float f = thr == 0u || (mk[i * 8] & mbitm) != 0u ? fk : 0.f;
             pd4[t] = pr * f;
-            ds4[t] = pr * fmaf(__uint_as_float(dv[i]), f, -dd[t]);
+            ds4[t] = pr * fmaf(__uint_as_float(dv[i]), f, dd[t]);  // (dd = -D)
             if (has_rpb || has_relb) sDs[(c0 + i) * kTcQ + kr] = ds4[t];
           }
           ppd[2 * i4] = pack_bf16(pd4[0], pd4[1]);

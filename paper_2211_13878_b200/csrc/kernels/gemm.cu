@@ -83,36 +83,6 @@ __device__ __forceinline__ float gelu_erf_grad(float x) {
   return g.phi_cdf + x * 0.3989422804014327f * g.e;
 }
 
-// Packed fp32 pairs (FFMA2 / FMUL2 / FADD2: one issue slot for two lanes' worth of math).
-// Each half rounds exactly like the scalar instruction, so results are bit-identical.
-using f2 = unsigned long long;
-__device__ __forceinline__ f2 f2_pack(float lo, float hi) {
-  f2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ float f2_lo(f2 v) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-  return lo;
-}
-__device__ __forceinline__ float f2_hi(f2 v) {
-  float lo, hi;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-  return hi;
-}
-__device__ __forceinline__ f2 f2_splat(float a) { return f2_pack(a, a); }
-__device__ __forceinline__ f2 f2_fma(f2 a, f2 b, f2 c) {
-  f2 r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-  return r;
-}
-__device__ __forceinline__ f2 f2_mul(f2 a, f2 b) {
-  f2 r;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
-
 // GeLU value and derivative of two bf16-rounded pre-activations (the gelu == 2 epilogue):
 // gelu_terms() on packed pairs.  The rational erf runs on the negated reciprocal
 // tn = -t = 1 / (-(1 + a z)), so -poly(t) comes out of one Horner chain with alternating

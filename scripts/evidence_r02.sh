@@ -30,3 +30,7 @@ timeout 300 python scripts/layer_kernels.py 512 > $O/kernels_m512.jsonl 2>&1
 timeout 300 python scripts/layer_kernels.py 2048 > $O/kernels_m2048.jsonl 2>&1
 timeout 200 python scripts/attn_bench.py > $O/attn_bench.jsonl 2>&1
 ls $O $O/ncu
+# gpurun copies back at most 64 MiB: keep the summaries, compress the launch lists
+rm -rf $O/ncu
+gzip -f $O/*.csv
+du -sh $O
